@@ -1,0 +1,86 @@
+"""FFT-based fast solver of the 5-point (7-point) modified-Helmholtz system (test infra only).
+
+Algorithm 4: sine transform along y [and z] (FST for the Dirichlet box,
+P:742, reading R3), tridiagonal solves along x, inverse transform.  What it
+computes has a plain definition: the exact solution of
+    Σ_a (v_{p+e_a} − 2 v_p + v_{p−e_a}) / h² − κ v_p = f_p ,   v = 0 on ∂B.
+
+Readings: R4  forward f̂_k = Σ_{j=1}^{N−1} f_j sin(πjk/N), inverse (2/N) Σ_k.
+          Per mode:  v̂_{i−1} + d_k v̂_i + v̂_{i+1} = h² f̂_i,
+          d_k = −(2 + 4 sin²(πk/2N) [+ 4 sin²(πl/2N)] + κ h²)
+The DST is scipy.fft.dst(type=1) (library primitive; pinned against the O(N²) sum).
+Thomas follows the textbook forward/backward sweep.
+"""
+from __future__ import annotations
+
+import numpy as np
+import scipy.fft
+
+
+def dst1(f, axis=-1):
+    """f̂_k = Σ_j f_j sin(πjk/N) over the N−1 interior entries of `axis` (R4)."""
+    return 0.5 * scipy.fft.dst(f, type=1, axis=axis)
+
+
+def idst1(fh, axis=-1):
+    """f_j = (2/N) Σ_k f̂_k sin(πjk/N) (R4)."""
+    n = fh.shape[axis] + 1
+    return scipy.fft.dst(fh, type=1, axis=axis) / n
+
+
+def dst1_direct(f):
+    """O(N²) direct sum along the last axis — used only by tests on small N."""
+    n = f.shape[-1] + 1
+    j = np.arange(1, n)
+    S = np.sin(np.pi * np.outer(j, j) / n)
+    return f @ S
+
+
+def thomas(dk, r):
+    """Solve x_{i−1} + d x_i + x_{i+1} = r_i (x_0 = x_n+1 = 0) for each column of r.
+
+    dk: (K,) diagonal per system; r: (n, K).  Textbook Thomas with forward pivots
+    c_1 = d, c_i = d − 1/c_{i−1}."""
+    n = r.shape[0]
+    c = np.empty_like(r)
+    y = np.empty_like(r)
+    c[0] = dk
+    y[0] = r[0]
+    for i in range(1, n):
+        c[i] = dk - 1.0 / c[i - 1]
+        y[i] = r[i] - y[i - 1] / c[i - 1]
+    x = np.empty_like(r)
+    x[n - 1] = y[n - 1] / c[n - 1]
+    for i in range(n - 2, -1, -1):
+        x[i] = (y[i] - x[i + 1]) / c[i]
+    return x
+
+
+def mode_mu(n):
+    k = np.arange(1, n)
+    return 4.0 * np.sin(np.pi * k / (2.0 * n)) ** 2
+
+
+def solve2d(f, h, kappa):
+    """f: (N−1, N−1) RHS at unknowns [i, j] → v with (Δ_h − κ) v = f (Alg. 4)."""
+    n = f.shape[0] + 1
+    fh = dst1(f, axis=1)                       # step 1: transform along y
+    dk = -(2.0 + mode_mu(n) + kappa * h * h)   # per mode k
+    vh = thomas(dk, h * h * fh)                # step 2: tridiagonal along x (rows i)
+    return idst1(vh, axis=1)                   # step 3: inverse transform
+
+
+def solve3d(f, h, kappa):
+    """f: (N−1,)*3 RHS at [i, j, k]: 2D sine transform over (j, k), tridiagonal along i."""
+    n = f.shape[0] + 1
+    fh = dst1(dst1(f, axis=1), axis=2)
+    mu = mode_mu(n)
+    dk = -(2.0 + mu[:, None] + mu[None, :] + kappa * h * h)
+    vh = thomas(dk.reshape(-1), (h * h * fh).reshape(n - 1, -1)).reshape(fh.shape)
+    return idst1(idst1(vh, axis=1), axis=2)
+
+
+def apply_operator2d(v, h, kappa):
+    """(Δ_h − κ) v at the unknowns, v = 0 outside (used by tests)."""
+    p = np.pad(v, 1)
+    return (p[2:, 1:-1] + p[:-2, 1:-1] + p[1:-1, 2:] + p[1:-1, :-2] - 4.0 * v) / (h * h) - kappa * v

@@ -1,0 +1,290 @@
+#!/usr/bin/env python
+"""KFBI solve benchmark (BASELINE.json metric) — one JSON line on rank 0.
+
+step   = one full kfbi_solve of the workload (volume apply, GMRES(30) on K̃φ = ĝ with one
+         interface solve per Arnoldi step, explicit residuals, final field): every row
+         A1-A9 of SURVEY §8(a).  Inputs resident in HBM when the timed region starts.
+value  = grid points per second per interface solve = U · n_applies / t_step,
+         U = (N−1)² unknowns.  Also reported: solve seconds, apply µs.
+e2e    = the same metric through the public API with pinned HOST inputs/outputs: the H2D
+         copy of g, f (grid, intersections, control points) and the D2H copy of u inside
+         the timed region.
+--impl reference: the CPU oracle (oracle/) as it stands, one K_D apply of the same
+         workload per step, on the host cores (rank 0 only).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+import workloads as W  # noqa: E402
+
+METRIC = "KFBI solve: grid-pts/s per interface solve (2D Poisson, multiply-connected, 8192^2)"
+UNIT = "grid-pts/s"
+
+
+def measured_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        d = json.load(open(p))
+        return d.get("hbm_gbs", 6650.0), "measured"
+    return 6650.0, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons during the timed region (B200_PROFILING.md)."""
+
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except Exception:
+            self.proc = None
+        return self
+
+    def __exit__(self, *a):
+        self.lines = []
+        if self.proc:
+            time.sleep(0.25)
+            self.proc.terminate()
+            try:
+                out, _ = self.proc.communicate(timeout=5)
+                self.lines = [l for l in out.splitlines() if l.strip()]
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for l in getattr(self, "lines", []):
+            f = [x.strip() for x in l.split(",")]
+            try:
+                sm.append(float(f[0]))
+                mx.append(float(f[1]))
+            except (ValueError, IndexError):
+                continue
+            for n, v in zip(names, f[2:]):
+                if v.lower() == "active":
+                    reasons.add(n)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": max(mx), "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def make_inputs(k, prob):
+    """Manufactured Dirichlet problem u* (reading R24) at the context's own points."""
+    n = prob.n
+    pz, pq = k.points("ctrl"), k.points("isect")
+    x = prob.lo + np.arange(n + 1) * prob.h
+    X, Y = np.meshgrid(x, x, indexing="ij")
+    f = lambda a, b: W.f_exact(prob.kappa, a, b)
+    return (W.u_exact(pz[:, 0], pz[:, 1]), f(X, Y).ravel(), f(pq[:, 0], pq[:, 1]), f(pz[:, 0], pz[:, 1]), X, Y)
+
+
+def cpu_oracle_apply_rate(prob, reps=1):
+    """Oracle (as it stands) on the host: one K_D apply of the same workload."""
+    from oracle.bie import Oracle2D
+    t0 = time.time()
+    o = Oracle2D(prob)
+    t_setup = time.time() - t0
+    phi = W.random_density(o.M, 0)
+    ts = []
+    for _ in range(reps):
+        t0 = time.perf_counter()
+        o.apply_KD(phi)
+        ts.append(time.perf_counter() - t0)
+    return o, ts, t_setup
+
+
+def run_reference(args, prob):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    from oracle.bie import Oracle2D
+    U = prob.unknowns
+    o = Oracle2D(prob)
+    phi = W.random_density(o.M, 0)
+    for _ in range(args.warmup):
+        o.apply_KD(phi)
+    ts = []
+    for _ in range(args.steps):
+        t0 = time.perf_counter()
+        o.apply_KD(phi)
+        ts.append(time.perf_counter() - t0)
+    t = float(np.mean(ts))
+    v = U / t
+    sample = f"one K_D apply (interface solve) of {prob.name} N={prob.n} per step"
+    print(json.dumps({
+        "impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": 1e3 * t, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": prob.name, "grid": prob.n, "kappa": prob.kappa, "M": o.M},
+        "cpu_baseline": {"value": v, "unit": UNIT, "cores": 1, "kind": "oracle", "sample": sample},
+        "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}))
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="kfbi", choices=["kfbi", "reference"])
+    ap.add_argument("--config", default="C3")
+    ap.add_argument("--n", type=int, default=0, help="override grid size")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    prob = W.CONFIGS[args.config](args.n) if args.n else W.CONFIGS[args.config]()
+    if args.impl == "reference":
+        return run_reference(args, prob)
+
+    import torch
+    import torch.distributed as dist
+
+    from paper_2404_15249_b200 import KFBI, launch_count
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    k = KFBI(prob, device=local)
+    g, fgrid, fq, fz, X, Y = make_inputs(k, prob)
+    t = lambda a: torch.tensor(a, dtype=torch.float64, device=dev)
+    g_d, fg_d, fq_d, fz_d = t(g), t(fgrid), t(fq), t(fz)
+    u_d = torch.empty(k.n_nodes, dtype=torch.float64, device=dev)
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)   # > 126 MB L2
+    stream = torch.cuda.current_stream(dev)
+
+    def step():
+        return k.solve(g_d, fg_d, fq_d, fz_d, u=u_d)
+
+    for _ in range(args.warmup):
+        _, _, st = step()
+    torch.cuda.synchronize()
+    barrier()
+    torch.cuda.synchronize()
+    times, stats = [], None
+    l0 = launch_count()
+    with ClockSampler(local) as clk:
+        for _ in range(args.steps):
+            flush.zero_()                                   # L2 flush between timed steps
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            _, _, stats = step()
+            e1.record(stream)
+            e1.synchronize()
+            times.append(e0.elapsed_time(e1) / 1e3)
+    launches = launch_count() - l0
+    torch.cuda.synchronize()
+    barrier()
+    t_step = sum(times) / len(times)
+    if world > 1:
+        tt = torch.tensor([t_step], device=dev)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        t_step = float(tt.item())
+    U = prob.unknowns
+    n_app = stats.n_applies
+    value = world * U * n_app / t_step
+
+    # e2e through the public API with pinned host buffers
+    pin = lambda a: torch.tensor(a, dtype=torch.float64).pin_memory()
+    g_h, fg_h, fq_h, fz_h = pin(g), pin(fgrid), pin(fq), pin(fz)
+    u_h = torch.empty(k.n_nodes, dtype=torch.float64).pin_memory()
+    e2e_t = []
+    for it in range(args.warmup + args.steps):
+        flush.zero_()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        gd = g_h.to(dev, non_blocking=True)
+        fgd = fg_h.to(dev, non_blocking=True)
+        fqd = fq_h.to(dev, non_blocking=True)
+        fzd = fz_h.to(dev, non_blocking=True)
+        u, _, st2 = k.solve(gd, fgd, fqd, fzd)
+        u_h.copy_(u.view(-1), non_blocking=True)
+        e1.record(stream)
+        e1.synchronize()
+        if it >= args.warmup:
+            e2e_t.append(e0.elapsed_time(e1) / 1e3)
+    t_e2e = sum(e2e_t) / len(e2e_t)
+    if world > 1:
+        tt = torch.tensor([t_e2e], device=dev)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        t_e2e = float(tt.item())
+    h2d = 8 * (g.size + fgrid.size + fq.size + fz.size)
+    d2h = 8 * k.n_nodes
+
+    # per-kernel device times of the K_D apply (CUDA events on the launching stream)
+    phi = torch.tensor(W.random_density(k.M, 0), device=dev)
+    prof = k.profile_apply(phi, reps=20)
+    model = k.apply_model()
+    peak, peak_src = measured_peaks()
+    cand = {"sweep": model["bytes_sweep"], "inverse": model["bytes_inverse"]}
+    dom = max(cand, key=lambda n: prof[n])
+    achieved = cand[dom] / (prof[dom] * 1e-3) / 1e9
+    roofline = {"bound": "hbm", "kernel": f"k_{dom}", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                "frac": achieved / peak, "traffic": None, "peak_source": peak_src,
+                "algorithmic_bytes_per_launch": cand[dom],
+                "share_of_apply": prof[dom] / prof["apply"],
+                "kernel_ms": {n: round(v, 4) for n, v in prof.items()}}
+    ncu_csv = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if os.path.exists(ncu_csv):
+        try:
+            roofline["traffic"] = json.load(open(ncu_csv)).get(f"{prob.name}:{prob.n}:k_{dom}")
+        except Exception:
+            pass
+
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": 1e3 * t_step, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic (manufactured u*, reading R24)",
+        "config": {"workload": prob.name, "grid": prob.n, "unknowns": U, "kappa": prob.kappa, "M": k.M,
+                   "intersections": k.nq, "irregular": k.nirr,
+                   "parallelism": "single-gpu" if world == 1 else f"replicas{world}",
+                   "l2": "flushed between timed steps (256 MB write); spectral buffer 537 MB > L2"},
+        "solve_s": t_step, "gmres_iters": stats.iters, "n_applies": n_app, "rel_residual": stats.rel_residual,
+        "apply_us": 1e3 * prof["apply"], "apply_grid_pts_per_s": U / (prof["apply"] * 1e-3),
+        "e2e": {"value": world * U * n_app / t_e2e, "unit": UNIT, "h2d_bytes_per_step": h2d,
+                "d2h_bytes_per_step": d2h, "solve_s": t_e2e},
+        "gpu_launches": launches, "gpu_launches_per_step": launches / args.steps,
+        "roofline": roofline,
+        "clocks": clk.summary(),
+    }
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        o, ts, t_setup = cpu_oracle_apply_rate(prob)
+        line["cpu_baseline"] = {"value": U / ts[0], "unit": UNIT, "cores": 1, "kind": "oracle",
+                                "sample": f"one K_D apply of {prob.name} N={prob.n} (oracle setup {t_setup:.0f}s untimed)"}
+    if rank == 0:
+        print(json.dumps(line))
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

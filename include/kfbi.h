@@ -1,0 +1,197 @@
+/*
+ * kfbi.h — C ABI of the B200-native kernel-free boundary integral (KFBI) library.
+ *
+ * Hot path of arXiv 2404.15249 ("A GPU-accelerated Cartesian grid method for PDEs on
+ * irregular domain"): the interface-problem apply run once per iteration of the boundary
+ * integral solve, and the GMRES solve around it.  Citations are PAPER.md line numbers (P:n).
+ *
+ *   PDE      Δu − κu = f in Ω, u = g_D on Γ = ∂Ω, κ ≥ 0
+ *   BIE      ½φ + Wφ + Yf = g_D on Γ;  u = Wφ + Yf in Ω
+ *   apply    K_D φ = ½φ + Wφ at the control points, evaluated as the interior one-sided
+ *            value of the interface problem Δv − κv = 0, [v] = φ, [∂_n v] = 0,
+ *            v = 0 on ∂B: jumps → correction at irregular nodes
+ *            (Alg. 2) → FFT/DST + tridiagonal fast solve (Alg. 4)
+ *            → jump-corrected interpolation (Alg. 3)
+ *   solve    restarted GMRES on K_D φ = g_D − (Yf)⁺ (Alg. 5), then the final
+ *            field u_h = Wφ + Yf
+ *
+ * Conventions: FP64 everywhere; N intervals per axis, N a power of
+ * two ≥ 64; box B = [lo, hi]^d with equal spacing h; node coordinate lo + i·h;
+ * homogeneous Dirichlet box condition.  Grid fields crossing the ABI are full node
+ * grids of (N+1)^d doubles, row-major, last index contiguous ([i][j] in 2D), box nodes 0.
+ *
+ * Memory and ownership: every d_* pointer is caller-owned device memory on the context's
+ * device; host pointers are caller-owned host memory.  The library allocates NO device
+ * memory: the caller queries kfbi_workspace_size() and hands a device buffer (e.g. a
+ * torch.uint8 tensor) to kfbi_set_workspace(); the context borrows it until destroyed.
+ * Streams are cudaStream_t passed as void* (NULL = legacy default stream).
+ *
+ * Errors: every call returns a kfbi_status; no exceptions or exit() cross the ABI.
+ * kfbi_last_error(ctx) / kfbi_last_setup_error() return a message for the last failure.
+ * After KFBI_ECUDA or KFBI_ENCCL only kfbi_destroy() is valid on that context.
+ * Threading: calls on one context are not thread-safe; distinct contexts are independent.
+ * Determinism: no floating-point atomics; results are bitwise repeatable for fixed inputs.
+ */
+#ifndef KFBI_H_
+#define KFBI_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef int32_t kfbi_status;
+enum {
+  KFBI_OK = 0,
+  KFBI_EINVAL = 1,       /* bad sizes, κ < 0, unequal h, null pointer, N not a power of two */
+  KFBI_EGEOM = 2,        /* Γ leaves the box / within 2h of ∂B, edge crossed twice (R31, R32) */
+  KFBI_ENOCONV = 3,      /* GMRES hit max_restarts; outputs hold the last iterate + stats   */
+  KFBI_ECUDA = 4,
+  KFBI_ENCCL = 5,
+  KFBI_ENOMEM = 6,       /* workspace missing or too small                                  */
+  KFBI_EUNSUPPORTED = 7  /* feature not built (e.g. 3D, Neumann)                            */
+};
+
+/* geometry kinds (2D curves parametrised CCW by θ ∈ [0, 2π)) */
+enum {
+  KFBI_ELLIPSE = 1,      /* p = {ra, rb}: γ = c + (ra cos θ, rb sin θ); circle: ra = rb        */
+  KFBI_STAR = 2,         /* p = {r, ε, m, α}: ρ = r(1 + ε sin(m(θ − α))) (R25)    */
+  KFBI_ELLIPSOID = 3,    /* p = {a, b, c}   (3D)                                     */
+  KFBI_TORUS = 4         /* p = {R, r}      (3D; reading R28)                                   */
+};
+enum { KFBI_OUTER = 0, KFBI_HOLE = 1 };
+enum { KFBI_DIRICHLET = 0, KFBI_NEUMANN = 1 };
+
+typedef struct {
+  int32_t dim;           /* 2 (3 reserved)                                   */
+  double lo[3], hi[3];   /* box B; (hi − lo)/n must be equal on all axes      */
+  int32_t n[3];          /* intervals per axis, power of two ≥ 64, all equal  */
+} kfbi_grid;
+
+typedef struct {
+  int32_t kind;          /* KFBI_ELLIPSE, KFBI_STAR, …                                      */
+  int32_t role;          /* KFBI_OUTER (one) or KFBI_HOLE (Ω = outer region minus holes)   */
+  double center[3];
+  double p[4];
+  int32_t n_ctrl;        /* control points on this curve; 0 = round(L / (1.18 h)) (R11)   */
+} kfbi_component;
+
+typedef struct {
+  int32_t ncomp;
+  const kfbi_component* comp;
+} kfbi_boundary;
+
+typedef struct {
+  double kappa;          /* κ ≥ 0                                    */
+  int32_t bc;            /* KFBI_DIRICHLET                                   */
+} kfbi_pde;
+
+typedef struct {
+  int32_t world, rank, device;   /* world = 1 for a single GPU                 */
+  const void* nccl_id;           /* 128-byte ncclUniqueId (world > 1), else NULL */
+} kfbi_dist;
+
+typedef struct {
+  double tol;            /* relative residual, default 1e-8          */
+  int32_t restart;       /* GMRES(m), default 30 (R18)                       */
+  int32_t max_restarts;  /* default 50                                       */
+} kfbi_solve_opts;
+
+typedef struct {
+  int32_t iters;         /* Arnoldi steps (applies of K inside cycles)        */
+  int32_t restarts;      /* cycles started                                    */
+  int32_t n_applies;     /* all interface solves incl. Y, residual and final  */
+  int32_t converged;
+  double rel_residual;   /* ‖ĝ − Kφ‖₂ / ‖ĝ − Kφ₀‖₂ at exit                    */
+  double t_solve_s;      /* host wall clock of kfbi_solve                     */
+} kfbi_solve_stats;
+
+typedef struct kfbi_ctx kfbi_ctx;
+
+/* Library / error introspection. */
+const char* kfbi_version(void);
+const char* kfbi_last_error(const kfbi_ctx* ctx);
+const char* kfbi_last_setup_error(void);
+
+/* rank 0 of a multi-GPU run writes a 128-byte NCCL unique id to out128 (host). */
+kfbi_status kfbi_get_unique_id(void* out128);
+
+/* Procedure 1: grid, control points, node classification, intersections,
+ * stencils and per-mode fast-solver tables, on the host.  No device memory is touched
+ * until kfbi_set_workspace().  `stream` is kept as the context's default stream. */
+kfbi_status kfbi_setup(const kfbi_grid* grid, const kfbi_boundary* bnd, const kfbi_pde* pde,
+                       const kfbi_dist* dist, void* stream, kfbi_ctx** out);
+
+/* Bytes of device workspace the context needs (setup tables + scratch). */
+kfbi_status kfbi_workspace_size(const kfbi_ctx* ctx, size_t* bytes);
+
+/* Borrow `bytes` of device memory at d_ws (256-byte aligned), upload the setup tables and
+ * run the setup-time device work (hole-completion fields, R27).  Synchronous. */
+kfbi_status kfbi_set_workspace(kfbi_ctx* ctx, void* d_ws, size_t bytes);
+
+/* M = number of control points, nq = number of intersection nodes, n_irr = irregular
+ * nodes, n_nodes = (N+1)^d grid nodes of a full field. */
+kfbi_status kfbi_sizes(const kfbi_ctx* ctx, int64_t* M, int64_t* nq, int64_t* n_irr, int64_t* n_nodes);
+
+/* Host copies of point coordinates so the caller can evaluate g and f there:
+ * which = 0: control points (M × dim, interleaved), 1: intersection nodes (nq × dim). */
+kfbi_status kfbi_points(const kfbi_ctx* ctx, int32_t which, double* host_xyz);
+
+/* Ω mask of the full node grid ((N+1)^d int8, 1 = Ω) into host memory. */
+kfbi_status kfbi_node_mask(const kfbi_ctx* ctx, int8_t* host_mask);
+
+/* out = K̃φ = K_D φ (+ hole completion, R27), φ and out are M doubles on the device.
+ * Asynchronous, stream-ordered, no state change. */
+kfbi_status kfbi_apply(kfbi_ctx* ctx, const double* d_phi, double* d_out, void* stream);
+
+/* Full Dirichlet BVP solve (Procedures 2-3):
+ *   d_g        g_D at the control points (M)
+ *   d_f_grid   f at the full node grid ((N+1)^d), or NULL for f ≡ 0; values outside Ω
+ *              are ignored (zero extension)
+ *   d_f_isect  f at the intersection nodes (nq) and d_f_ctrl at the control points (M),
+ *              both NULL iff d_f_grid is NULL
+ *   d_phi0     initial density (M) or NULL for φ₀ = 0
+ *   d_u        out: full node grid; u_h on Ω nodes, the interface solution elsewhere
+ *   d_phi_out  out: converged density (M) or NULL
+ * Synchronous (one host sync per Arnoldi step, as P:782). */
+kfbi_status kfbi_solve(kfbi_ctx* ctx, const double* d_g, const double* d_f_grid,
+                       const double* d_f_isect, const double* d_f_ctrl, const double* d_phi0,
+                       double* d_u, double* d_phi_out, const kfbi_solve_opts* opts,
+                       kfbi_solve_stats* stats, void* stream);
+
+/* Bytes moved per call of the dominant kernels (algorithmic model of DESIGN.md). */
+kfbi_status kfbi_apply_model(const kfbi_ctx* ctx, double* bytes_sweep, double* bytes_inverse,
+                             double* unknowns);
+
+kfbi_status kfbi_destroy(kfbi_ctx* ctx);
+
+/* Device time of each kernel of one kfbi_apply, averaged over `reps` applies, from CUDA
+ * events recorded on `stream` between the launches (bench/roofline use; synchronous).
+ * ms_out[8] = {spline, correct, sweep, reduced, inverse, hole, interp, whole apply}. */
+kfbi_status kfbi_profile_apply(kfbi_ctx* ctx, const double* d_phi, double* d_out, int32_t reps,
+                               double* ms_out, void* stream);
+
+/* Process-wide count of kernels this library has launched (for bench gpu_launches). */
+kfbi_status kfbi_launch_count(int64_t* count);
+
+/* ---------------------------------------------------------------- test-only entry points
+ * kfbi_test_fast_solve: d_v = solution of (Δ_h − κ)v = d_rhs on the unknowns (full-grid
+ *   layouts, box entries of d_rhs ignored, of d_v written 0) — Alg. 4 alone.
+ * kfbi_test_interface_solve: Alg. 1 steps 4-6 with GIVEN jumps: d_jq (nq × 6) at the
+ *   intersections and d_jz (M × 6) at the control points, columns [v],[v_x],[v_y],[v_xx],
+ *   [v_xy],[v_yy]; d_base full grid or NULL (0); d_v full grid out (or NULL) and d_vplus
+ *   (M) out = V⁺ at the control points.
+ * kfbi_test_setup_dump: host copies of the integer setup lists for parity with the oracle:
+ *   which = 0: irregular nodes (n_irr × dim int64, sorted), 1: intersections (nq × (dim+1)
+ *   int64: axis, low-end node), 2: stencil nodes (M × 6 × dim int64). */
+kfbi_status kfbi_test_fast_solve(kfbi_ctx* ctx, const double* d_rhs, double* d_v, void* stream);
+kfbi_status kfbi_test_interface_solve(kfbi_ctx* ctx, const double* d_base, const double* d_jq,
+                                      const double* d_jz, double* d_v, double* d_vplus, void* stream);
+kfbi_status kfbi_test_setup_dump(const kfbi_ctx* ctx, int32_t which, int64_t* host_out);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* KFBI_H_ */

@@ -1,0 +1,560 @@
+// C ABI of the KFBI library: context, workspace, kfbi_apply / kfbi_solve orchestration.
+// See include/kfbi.h for the contract.  All device work is stream-ordered on the caller's
+// stream; the only host syncs are the ones Algorithm 5 needs (one per Arnoldi step).
+#include <cuda_runtime.h>
+
+#include <chrono>
+#include <cmath>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "kernels.h"
+#include "kfbi_impl.h"
+
+using namespace kfbi;
+
+namespace {
+thread_local std::string g_setup_err;
+constexpr int kMaxRestart = 64;
+
+struct CudaError : std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
+
+inline void ck(cudaError_t e, const char* what) {
+  if (e != cudaSuccess) throw CudaError(std::string(what) + ": " + cudaGetErrorString(e));
+}
+}  // namespace
+
+struct kfbi_ctx {
+  Setup S;
+  DevTables T{};
+  cudaStream_t stream = nullptr;
+  int device = 0;
+  std::string err;
+  uint8_t* ws = nullptr;
+  size_t ws_bytes = 0, ws_need = 0;
+  // scratch
+  double *spec = nullptr, *zfirst = nullptr, *zlast = nullptr, *fsep = nullptr, *hsep = nullptr;
+  double *cval = nullptr, *mk = nullptr, *vsten = nullptr;
+  // holes
+  int nh = 0;
+  int *hole_off = nullptr, *hole_M = nullptr;
+  double *hole_delta = nullptr, *ahole = nullptr, *wg = nullptr, *onehot = nullptr;
+  BumpParams bump{};
+  // GMRES
+  double *V = nullptr, *gx = nullptr, *gr = nullptr, *ghat = nullptr, *tmp = nullptr;
+  double *partial = nullptr, *hcol = nullptr, *ycoef = nullptr, *scal = nullptr;
+  double* hcol_host = nullptr;
+  // host staging of small tables (kept alive for the async uploads)
+  std::vector<int32_t> coff, cM, hoff, hM;
+  std::vector<double> cdel, hdel, oneh;
+};
+
+namespace {
+
+// two-pass bump allocator over the workspace (pass 1 sizes, pass 2 assigns + uploads)
+struct Arena {
+  uint8_t* base;
+  size_t off = 0;
+  bool assign;
+  std::vector<std::pair<void*, std::pair<const void*, size_t>>> uploads;
+  template <class T>
+  T* take(size_t n) {
+    off = (off + 255) & ~size_t(255);
+    T* p = assign ? reinterpret_cast<T*>(base + off) : nullptr;
+    off += n * sizeof(T);
+    return p;
+  }
+  template <class T>
+  const T* table(const std::vector<T>& v) {
+    T* p = take<T>(v.empty() ? 1 : v.size());
+    if (assign && !v.empty()) uploads.push_back({p, {v.data(), v.size() * sizeof(T)}});
+    return p;
+  }
+};
+
+void layout(kfbi_ctx* c, Arena& A) {
+  Setup& S = c->S;
+  DevTables& T = c->T;
+  const size_t N = S.N, P = S.P;
+  T.N = S.N; T.P = S.P; T.M = S.M; T.nq = S.nq; T.nirr = S.nirr; T.nsn = S.nsn;
+  T.nocol = (int)S.ocol.size(); T.ncomp = (int)S.comps.size();
+  T.lo = S.lo; T.h = S.h; T.kappa = S.kappa;
+  T.q_axis = A.table(S.q_axis); T.q_comp = A.table(S.q_comp); T.q_knot = A.table(S.q_knot);
+  T.q_t = A.table(S.q_t); T.q_t1 = A.table(S.q_t1); T.q_t2 = A.table(S.q_t2);
+  T.q_p1 = A.table(S.q_p1); T.q_p2 = A.table(S.q_p2);
+  T.irr_j = A.table(S.irr_j); T.irr_ptr = A.table(S.irr_ptr); T.pair_q = A.table(S.pair_q);
+  T.col_ptr = A.table(S.col_ptr); T.irr_side = A.table(S.irr_side); T.pair_d = A.table(S.pair_d);
+  T.z_comp = A.table(S.z_comp); T.z_knot = A.table(S.z_knot);
+  T.z_t1 = A.table(S.z_t1); T.z_t2 = A.table(S.z_t2); T.z_p1 = A.table(S.z_p1); T.z_p2 = A.table(S.z_p2);
+  T.sn_j = A.table(S.sn_j); T.ocol = A.table(S.ocol); T.ocol_ptr = A.table(S.ocol_ptr);
+  T.st_node = A.table(S.st_node); T.st_ext = A.table(S.st_ext);
+  T.st_w = A.table(S.st_w); T.st_dx = A.table(S.st_dx); T.st_dy = A.table(S.st_dy);
+  // component tables live in the setup object as small vectors
+  auto& coff = c->coff; auto& cM = c->cM; auto& cdel = c->cdel;
+  coff.clear(); cM.clear(); cdel.clear();
+  for (auto& cc : S.comps) { coff.push_back(cc.off); cM.push_back(cc.M); cdel.push_back(cc.delta); }
+  T.c_off = A.table(coff); T.c_M = A.table(cM); T.c_delta = A.table(cdel);
+  T.sp_ntaps = A.table(S.sp_ntaps); T.sp_first = A.table(S.sp_first); T.sp_coef_off = A.table(S.sp_coef_off);
+  T.sp_coef = A.table(S.sp_coef);
+  T.sin_tab = A.table(S.sin_tab); T.dk = A.table(S.dk); T.invc = A.table(S.invc); T.zr = A.table(S.zr);
+  T.red_a = A.table(S.red_a); T.red_b = A.table(S.red_b); T.red_invc = A.table(S.red_invc);
+  T.side = A.table(S.side);
+  // holes
+  auto& hoff = c->hoff; auto& hM = c->hM; auto& hdel = c->hdel; auto& oneh = c->oneh;
+  hoff.clear(); hM.clear(); hdel.clear(); oneh.clear();
+  c->nh = (int)S.holes.size();
+  for (int k : S.holes) {
+    hoff.push_back(S.comps[k].off); hM.push_back(S.comps[k].M); hdel.push_back(S.comps[k].delta);
+  }
+  for (int a = 0; a < c->nh; ++a)
+    for (int b = 0; b < c->nh; ++b) oneh.push_back(a == b ? 1.0 : 0.0);
+  c->hole_off = const_cast<int*>(A.table(hoff));
+  c->hole_M = const_cast<int*>(A.table(hM));
+  c->hole_delta = const_cast<double*>(A.table(hdel));
+  c->onehot = const_cast<double*>(A.table(oneh));
+  c->ahole = A.take<double>(std::max(c->nh, 1));
+  c->wg = A.take<double>((size_t)std::max(c->nh, 1) * S.M);
+  // scratch
+  c->spec = A.take<double>((N - 1) * N);
+  c->zfirst = A.take<double>(P * N);
+  c->zlast = A.take<double>(P * N);
+  c->fsep = A.take<double>(std::max<size_t>(P - 1, 1) * N);
+  c->hsep = A.take<double>(std::max<size_t>(P - 1, 1) * N);
+  c->cval = A.take<double>(std::max(S.nirr, 1));
+  c->mk = A.take<double>(S.M);
+  c->vsten = A.take<double>(std::max(S.nsn, 1));
+  const size_t M = S.M;
+  c->V = A.take<double>((kMaxRestart + 1) * M);
+  c->gx = A.take<double>(M);
+  c->gr = A.take<double>(M);
+  c->ghat = A.take<double>(M);
+  c->tmp = A.take<double>(M);
+  c->partial = A.take<double>((kMaxRestart + 2) * kRedBlocks);
+  c->hcol = A.take<double>(kMaxRestart + 2);
+  c->ycoef = A.take<double>(kMaxRestart + 1);
+  c->scal = A.take<double>(8);
+}
+
+kfbi_status fail(kfbi_ctx* c, kfbi_status st, const std::string& msg) {
+  if (c) c->err = msg;
+  return st;
+}
+
+#define KFBI_TRY(ctx)                                                  \
+  try {
+#define KFBI_CATCH(ctx)                                                \
+  }                                                                    \
+  catch (const CudaError& e) { return fail(ctx, KFBI_ECUDA, e.what()); } \
+  catch (const GeomError& e) { return fail(ctx, KFBI_EGEOM, e.what()); } \
+  catch (const ArgError& e) { return fail(ctx, KFBI_EINVAL, e.what()); } \
+  catch (const std::exception& e) { return fail(ctx, KFBI_EINVAL, e.what()); }
+
+cudaStream_t pick(kfbi_ctx* c, void* s) { return s ? (cudaStream_t)s : c->stream; }
+
+void need_ws(kfbi_ctx* c) {
+  if (!c->ws) throw std::runtime_error("workspace not set (kfbi_set_workspace)");
+}
+
+// --- one interface solve, sparse output at stencil nodes → V⁺ at control points ----------
+void apply_KD(kfbi_ctx* c, const double* phi, double* out, cudaStream_t s) {
+  const DevTables& T = c->T;
+  launch_spline(T, phi, c->mk, s);
+  launch_correct(T, phi, c->mk, nullptr, nullptr, c->cval, s);
+  launch_sweep(T, c->cval, false, c->spec, c->zfirst, c->zlast, c->fsep, s);
+  launch_reduced(T, c->zfirst, c->zlast, c->fsep, c->hsep, s);
+  launch_inverse_sparse(T, c->spec, c->hsep, c->vsten, s);
+  launch_hole_coeffs(T, c->hole_off, c->hole_M, c->hole_delta, c->nh, phi, c->ahole, s);
+  launch_interp(T, phi, c->mk, nullptr, nullptr, c->vsten, c->nh, c->nh ? c->wg : nullptr, c->ahole, out, s);
+}
+
+void apply_Y(kfbi_ctx* c, const double* fgrid, const double* fq, const double* fz, double* out, cudaStream_t s) {
+  const DevTables& T = c->T;
+  BumpParams none{};
+  launch_dst_forward(T, fgrid, true, none, c->spec, s);
+  launch_correct(T, nullptr, nullptr, fq, nullptr, c->cval, s);
+  launch_sweep(T, c->cval, true, c->spec, c->zfirst, c->zlast, c->fsep, s);
+  launch_reduced(T, c->zfirst, c->zlast, c->fsep, c->hsep, s);
+  launch_inverse_sparse(T, c->spec, c->hsep, c->vsten, s);
+  launch_interp(T, nullptr, nullptr, fz, nullptr, c->vsten, 0, nullptr, nullptr, out, s);
+}
+
+void final_field(kfbi_ctx* c, const double* phi, const double* fgrid, const double* fq, double* u, cudaStream_t s) {
+  const DevTables& T = c->T;
+  BumpParams bp = c->bump;
+  bp.a = c->ahole;
+  launch_hole_coeffs(T, c->hole_off, c->hole_M, c->hole_delta, c->nh, phi, c->ahole, s);
+  const bool dense = fgrid || c->nh;
+  if (dense) launch_dst_forward(T, fgrid, true, bp, c->spec, s);
+  launch_spline(T, phi, c->mk, s);
+  launch_correct(T, phi, c->mk, fq, nullptr, c->cval, s);
+  launch_sweep(T, c->cval, dense, c->spec, c->zfirst, c->zlast, c->fsep, s);
+  launch_reduced(T, c->zfirst, c->zlast, c->fsep, c->hsep, s);
+  launch_inverse_dense(T, c->spec, c->hsep, u, s);
+  const size_t W = (size_t)T.N + 1;
+  ck(cudaMemsetAsync(u, 0, W * sizeof(double), s), "memset");
+  ck(cudaMemsetAsync(u + (size_t)T.N * W, 0, W * sizeof(double), s), "memset");
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* kfbi_version(void) { return "kfbi-b200 0.1 (sm_100a, 2D)"; }
+const char* kfbi_last_error(const kfbi_ctx* ctx) { return ctx ? ctx->err.c_str() : g_setup_err.c_str(); }
+const char* kfbi_last_setup_error(void) { return g_setup_err.c_str(); }
+
+kfbi_status kfbi_get_unique_id(void* out128) {
+  (void)out128;
+  g_setup_err = "multi-GPU (NCCL) layer not built in this version";
+  return KFBI_EUNSUPPORTED;
+}
+
+kfbi_status kfbi_setup(const kfbi_grid* grid, const kfbi_boundary* bnd, const kfbi_pde* pde,
+                       const kfbi_dist* dist, void* stream, kfbi_ctx** out) {
+  if (!out) return KFBI_EINVAL;
+  *out = nullptr;
+  if (dist && dist->world > 1) {
+    g_setup_err = "world > 1 not supported in this version";
+    return KFBI_EUNSUPPORTED;
+  }
+  auto* c = new kfbi_ctx();
+  try {
+    build_setup(c->S, grid, bnd, pde);
+    c->stream = (cudaStream_t)stream;
+    c->device = dist ? dist->device : 0;
+    Arena A{nullptr, 0, false};
+    layout(c, A);
+    c->ws_need = A.off + 256;
+    c->bump.nh = c->nh;
+    for (int h = 0; h < c->nh && h < 4; ++h) {
+      const Comp& C = c->S.comps[c->S.holes[h]];
+      c->bump.cx[h] = C.c[0];
+      c->bump.cy[h] = C.c[1];
+      c->bump.rad[h] = 0.5 * std::min(C.p[0], C.p[1]);
+    }
+    if (c->nh > 4) throw ArgError("at most 4 holes");
+  } catch (const GeomError& e) {
+    g_setup_err = e.what();
+    delete c;
+    return KFBI_EGEOM;
+  } catch (const std::exception& e) {
+    g_setup_err = e.what();
+    delete c;
+    return KFBI_EINVAL;
+  }
+  *out = c;
+  return KFBI_OK;
+}
+
+kfbi_status kfbi_workspace_size(const kfbi_ctx* ctx, size_t* bytes) {
+  if (!ctx || !bytes) return KFBI_EINVAL;
+  *bytes = ctx->ws_need;
+  return KFBI_OK;
+}
+
+kfbi_status kfbi_set_workspace(kfbi_ctx* c, void* d_ws, size_t bytes) {
+  if (!c || !d_ws) return KFBI_EINVAL;
+  if (bytes < c->ws_need) return fail(c, KFBI_ENOMEM, "workspace too small");
+  if (((uintptr_t)d_ws) & 255) return fail(c, KFBI_EINVAL, "workspace must be 256-byte aligned");
+  KFBI_TRY(c)
+  ck(cudaSetDevice(c->device), "cudaSetDevice");
+  c->ws = (uint8_t*)d_ws;
+  c->ws_bytes = bytes;
+  Arena A{c->ws, 0, true};
+  layout(c, A);
+  cudaStream_t s = c->stream;
+  for (auto& u : A.uploads) ck(cudaMemcpyAsync(u.first, u.second.first, u.second.second, cudaMemcpyHostToDevice, s), "upload");
+  if (!c->hcol_host) ck(cudaMallocHost(&c->hcol_host, (kMaxRestart + 2) * sizeof(double)), "cudaMallocHost");
+  // hole completion fields w_h|Γ (reading R27): plain fast solve of the bump, no jumps
+  for (int h = 0; h < c->nh; ++h) {
+    BumpParams bp = c->bump;
+    bp.a = c->onehot + (size_t)h * c->nh;
+    launch_dst_forward(c->T, nullptr, false, bp, c->spec, s);
+    launch_sweep(c->T, nullptr, true, c->spec, c->zfirst, c->zlast, c->fsep, s);
+    launch_reduced(c->T, c->zfirst, c->zlast, c->fsep, c->hsep, s);
+    launch_inverse_sparse(c->T, c->spec, c->hsep, c->vsten, s);
+    launch_interp(c->T, nullptr, nullptr, nullptr, nullptr, c->vsten, 0, nullptr, nullptr, c->wg + (size_t)h * c->S.M, s);
+  }
+  ck(cudaGetLastError(), "setup kernels");
+  ck(cudaStreamSynchronize(s), "setup sync");
+  KFBI_CATCH(c)
+  return KFBI_OK;
+}
+
+kfbi_status kfbi_sizes(const kfbi_ctx* c, int64_t* M, int64_t* nq, int64_t* nirr, int64_t* nn) {
+  if (!c) return KFBI_EINVAL;
+  if (M) *M = c->S.M;
+  if (nq) *nq = c->S.nq;
+  if (nirr) *nirr = c->S.nirr;
+  if (nn) *nn = (int64_t)(c->S.N + 1) * (c->S.N + 1);
+  return KFBI_OK;
+}
+
+kfbi_status kfbi_points(const kfbi_ctx* c, int32_t which, double* xyz) {
+  if (!c || !xyz) return KFBI_EINVAL;
+  const Setup& S = c->S;
+  if (which == 0) {
+    for (int m = 0; m < S.M; ++m) { xyz[2 * m] = S.z_x[m]; xyz[2 * m + 1] = S.z_y[m]; }
+  } else if (which == 1) {
+    for (int q = 0; q < S.nq; ++q) { xyz[2 * q] = S.q_x[q]; xyz[2 * q + 1] = S.q_y[q]; }
+  } else {
+    return KFBI_EINVAL;
+  }
+  return KFBI_OK;
+}
+
+kfbi_status kfbi_node_mask(const kfbi_ctx* c, int8_t* mask) {
+  if (!c || !mask) return KFBI_EINVAL;
+  std::memcpy(mask, c->S.side.data(), c->S.side.size());
+  return KFBI_OK;
+}
+
+kfbi_status kfbi_apply(kfbi_ctx* c, const double* d_phi, double* d_out, void* stream) {
+  if (!c || !d_phi || !d_out) return fail(c, KFBI_EINVAL, "null pointer");
+  KFBI_TRY(c)
+  need_ws(c);
+  apply_KD(c, d_phi, d_out, pick(c, stream));
+  ck(cudaGetLastError(), "kfbi_apply launch");
+  KFBI_CATCH(c)
+  return KFBI_OK;
+}
+
+kfbi_status kfbi_solve(kfbi_ctx* c, const double* d_g, const double* d_f_grid, const double* d_f_isect,
+                       const double* d_f_ctrl, const double* d_phi0, double* d_u, double* d_phi_out,
+                       const kfbi_solve_opts* opts, kfbi_solve_stats* stats, void* stream) {
+  if (!c || !d_g || !d_u) return fail(c, KFBI_EINVAL, "null pointer");
+  if ((d_f_grid == nullptr) != (d_f_isect == nullptr) || (d_f_grid == nullptr) != (d_f_ctrl == nullptr))
+    return fail(c, KFBI_EINVAL, "f_grid, f_isect, f_ctrl must all be given or all NULL");
+  kfbi_solve_opts o{1e-8, 30, 50};
+  if (opts) o = *opts;
+  if (o.restart < 1 || o.restart > kMaxRestart || o.max_restarts < 1 || !(o.tol > 0))
+    return fail(c, KFBI_EINVAL, "bad solve options");
+  kfbi_solve_stats st{};
+  auto t0 = std::chrono::steady_clock::now();
+  bool converged = false;
+  KFBI_TRY(c)
+  need_ws(c);
+  cudaStream_t s = pick(c, stream);
+  const int M = c->S.M;
+  const size_t bM = (size_t)M * sizeof(double);
+  // ĝ = g − (Yf)⁺
+  if (d_f_grid) {
+    apply_Y(c, d_f_grid, d_f_isect, d_f_ctrl, c->tmp, s);
+    st.n_applies++;
+    launch_sub(M, d_g, c->tmp, c->ghat, s);
+  } else {
+    ck(cudaMemcpyAsync(c->ghat, d_g, bM, cudaMemcpyDeviceToDevice, s), "copy g");
+  }
+  // GMRES(m), Algorithm 5, reading R18
+  if (d_phi0) ck(cudaMemcpyAsync(c->gx, d_phi0, bM, cudaMemcpyDeviceToDevice, s), "copy phi0");
+  else ck(cudaMemsetAsync(c->gx, 0, bM, s), "zero x");
+  double beta0 = -1.0;
+  std::vector<double> H((size_t)(o.restart + 1) * o.restart), cs(o.restart), sn(o.restart), gv(o.restart + 1), y(o.restart);
+  auto Hc = [&](int i, int j) -> double& { return H[(size_t)i * o.restart + j]; };
+  for (int cycle = 0; cycle <= o.max_restarts; ++cycle) {
+    // r = ĝ − K x  (explicit residual; skipped for x₀ = 0 on the first cycle)
+    if (!d_phi0 && cycle == 0) {
+      ck(cudaMemcpyAsync(c->gr, c->ghat, bM, cudaMemcpyDeviceToDevice, s), "copy r");
+    } else {
+      apply_KD(c, c->gx, c->tmp, s);
+      st.n_applies++;
+      launch_sub(M, c->ghat, c->tmp, c->gr, s);
+    }
+    launch_dot(M, c->gr, c->gr, c->partial, s);
+    launch_finish_sum(c->partial, c->scal, true, s);
+    ck(cudaMemcpyAsync(c->hcol_host, c->scal, sizeof(double), cudaMemcpyDeviceToHost, s), "beta");
+    ck(cudaStreamSynchronize(s), "sync beta");
+    const double beta = c->hcol_host[0];
+    if (!std::isfinite(beta)) throw std::runtime_error("non-finite residual");
+    if (beta0 < 0) beta0 = beta;
+    st.rel_residual = beta0 > 0 ? beta / beta0 : 0.0;
+    if (beta <= o.tol * beta0 || beta0 == 0.0) { converged = true; break; }
+    if (cycle == o.max_restarts) break;
+    st.restarts = cycle + 1;
+    launch_scale_copy(M, c->gr, c->scal, c->V, s);   // V_0 = r / β
+    std::fill(gv.begin(), gv.end(), 0.0);
+    gv[0] = beta;
+    int jlast = o.restart - 1;
+    for (int j = 0; j < o.restart; ++j) {
+      double* w = c->V + (size_t)(j + 1) * M;
+      apply_KD(c, c->V + (size_t)j * M, w, s);
+      st.iters++;
+      st.n_applies++;
+      // MGS exactly as P:765-768, deterministic fixed-grid reductions
+      for (int i = 0; i <= j; ++i)
+        launch_mgs_step(M, w, i ? c->V + (size_t)(i - 1) * M : nullptr, c->V + (size_t)i * M,
+                        i ? c->partial + (size_t)(i - 1) * kRedBlocks : nullptr, c->partial + (size_t)i * kRedBlocks,
+                        i ? c->hcol + (i - 1) : nullptr, s);
+      launch_mgs_step(M, w, c->V + (size_t)j * M, w, c->partial + (size_t)j * kRedBlocks,
+                      c->partial + (size_t)(j + 1) * kRedBlocks, c->hcol + j, s);
+      launch_norm_scale(M, w, c->partial + (size_t)(j + 1) * kRedBlocks, c->hcol + j + 1, s);
+      ck(cudaMemcpyAsync(c->hcol_host, c->hcol, (j + 2) * sizeof(double), cudaMemcpyDeviceToHost, s), "hcol");
+      ck(cudaStreamSynchronize(s), "sync hcol");
+      for (int i = 0; i <= j + 1; ++i) Hc(i, j) = c->hcol_host[i];
+      for (int i = 0; i < j; ++i) {   // previous Givens rotations
+        const double a = Hc(i, j), b = Hc(i + 1, j);
+        Hc(i, j) = cs[i] * a + sn[i] * b;
+        Hc(i + 1, j) = -sn[i] * a + cs[i] * b;
+      }
+      const double hnext = Hc(j + 1, j);
+      const double rr = std::hypot(Hc(j, j), hnext);
+      cs[j] = Hc(j, j) / rr;
+      sn[j] = hnext / rr;
+      Hc(j, j) = rr;
+      Hc(j + 1, j) = 0.0;
+      gv[j + 1] = -sn[j] * gv[j];
+      gv[j] = cs[j] * gv[j];
+      if (!std::isfinite(gv[j + 1])) throw std::runtime_error("non-finite GMRES residual");
+      if (std::fabs(gv[j + 1]) <= o.tol * beta0 || hnext <= 1e-14 * beta0) { jlast = j; break; }
+    }
+    const int k = jlast + 1;
+    for (int i = k - 1; i >= 0; --i) {
+      double sacc = gv[i];
+      for (int q = i + 1; q < k; ++q) sacc -= Hc(i, q) * y[q];
+      y[i] = sacc / Hc(i, i);
+    }
+    ck(cudaMemcpyAsync(c->ycoef, y.data(), k * sizeof(double), cudaMemcpyHostToDevice, s), "y");
+    launch_axpy_basis(M, k, c->V, M, c->ycoef, c->gx, s);   // φ_m = φ_0 + M_m y_m
+  }
+  if (d_phi_out) ck(cudaMemcpyAsync(d_phi_out, c->gx, bM, cudaMemcpyDeviceToDevice, s), "phi out");
+  // final field u = Wφ + Yf (+ Σ a_h w_h) (R27)
+  final_field(c, c->gx, d_f_grid, d_f_isect, d_u, s);
+  st.n_applies++;
+  ck(cudaGetLastError(), "solve kernels");
+  ck(cudaStreamSynchronize(s), "solve sync");
+  KFBI_CATCH(c)
+  st.converged = converged ? 1 : 0;
+  st.t_solve_s = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+  if (stats) *stats = st;
+  return converged ? KFBI_OK : fail(c, KFBI_ENOCONV, "GMRES did not converge");
+}
+
+kfbi_status kfbi_apply_model(const kfbi_ctx* c, double* bytes_sweep, double* bytes_inverse, double* unknowns) {
+  if (!c) return KFBI_EINVAL;
+  const double N = c->S.N, P = c->S.P;
+  // sweep: writes v̂ at the block rows of every mode (8 B per value); reads are on-chip
+  if (bytes_sweep) *bytes_sweep = 8.0 * (N - P) * (N - 1);
+  // sparse inverse: reads v̂ rows of the columns that hold stencil nodes
+  if (bytes_inverse) *bytes_inverse = 8.0 * (double)c->S.ocol.size() * (N - 1);
+  if (unknowns) *unknowns = (N - 1) * (N - 1);
+  return KFBI_OK;
+}
+
+kfbi_status kfbi_profile_apply(kfbi_ctx* c, const double* d_phi, double* d_out, int32_t reps, double* ms,
+                               void* stream) {
+  if (!c || !d_phi || !d_out || !ms || reps < 1) return fail(c, KFBI_EINVAL, "bad arguments");
+  KFBI_TRY(c)
+  need_ws(c);
+  cudaStream_t s = pick(c, stream);
+  const DevTables& T = c->T;
+  cudaEvent_t ev[8];
+  for (auto& e : ev) ck(cudaEventCreate(&e), "event");
+  double acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  for (int r = 0; r < reps; ++r) {
+    ck(cudaEventRecord(ev[0], s), "rec");
+    launch_spline(T, d_phi, c->mk, s);
+    ck(cudaEventRecord(ev[1], s), "rec");
+    launch_correct(T, d_phi, c->mk, nullptr, nullptr, c->cval, s);
+    ck(cudaEventRecord(ev[2], s), "rec");
+    launch_sweep(T, c->cval, false, c->spec, c->zfirst, c->zlast, c->fsep, s);
+    ck(cudaEventRecord(ev[3], s), "rec");
+    launch_reduced(T, c->zfirst, c->zlast, c->fsep, c->hsep, s);
+    ck(cudaEventRecord(ev[4], s), "rec");
+    launch_inverse_sparse(T, c->spec, c->hsep, c->vsten, s);
+    ck(cudaEventRecord(ev[5], s), "rec");
+    launch_hole_coeffs(T, c->hole_off, c->hole_M, c->hole_delta, c->nh, d_phi, c->ahole, s);
+    ck(cudaEventRecord(ev[6], s), "rec");
+    launch_interp(T, d_phi, c->mk, nullptr, nullptr, c->vsten, c->nh, c->nh ? c->wg : nullptr, c->ahole, d_out, s);
+    ck(cudaEventRecord(ev[7], s), "rec");
+    ck(cudaEventSynchronize(ev[7]), "sync");
+    for (int q = 0; q < 7; ++q) {
+      float t = 0;
+      ck(cudaEventElapsedTime(&t, ev[q], ev[q + 1]), "elapsed");
+      acc[q] += t;
+    }
+    float t = 0;
+    ck(cudaEventElapsedTime(&t, ev[0], ev[7]), "elapsed");
+    acc[7] += t;
+  }
+  for (int q = 0; q < 8; ++q) ms[q] = acc[q] / reps;
+  for (auto& e : ev) cudaEventDestroy(e);
+  KFBI_CATCH(c)
+  return KFBI_OK;
+}
+
+kfbi_status kfbi_launch_count(int64_t* count) {
+  if (!count) return KFBI_EINVAL;
+  *count = (int64_t)kfbi::g_launches;
+  return KFBI_OK;
+}
+
+kfbi_status kfbi_destroy(kfbi_ctx* c) {
+  if (!c) return KFBI_OK;
+  if (c->hcol_host) cudaFreeHost(c->hcol_host);
+  delete c;
+  return KFBI_OK;
+}
+
+kfbi_status kfbi_test_fast_solve(kfbi_ctx* c, const double* d_rhs, double* d_v, void* stream) {
+  if (!c || !d_rhs || !d_v) return KFBI_EINVAL;
+  KFBI_TRY(c)
+  need_ws(c);
+  cudaStream_t s = pick(c, stream);
+  BumpParams none{};
+  launch_dst_forward(c->T, d_rhs, false, none, c->spec, s);
+  launch_sweep(c->T, nullptr, true, c->spec, c->zfirst, c->zlast, c->fsep, s);
+  launch_reduced(c->T, c->zfirst, c->zlast, c->fsep, c->hsep, s);
+  launch_inverse_dense(c->T, c->spec, c->hsep, d_v, s);
+  const size_t W = (size_t)c->T.N + 1;
+  ck(cudaMemsetAsync(d_v, 0, W * sizeof(double), s), "memset");
+  ck(cudaMemsetAsync(d_v + (size_t)c->T.N * W, 0, W * sizeof(double), s), "memset");
+  ck(cudaGetLastError(), "fast solve");
+  KFBI_CATCH(c)
+  return KFBI_OK;
+}
+
+kfbi_status kfbi_test_interface_solve(kfbi_ctx* c, const double* d_base, const double* d_jq, const double* d_jz,
+                                      double* d_v, double* d_vplus, void* stream) {
+  if (!c || !d_jq || !d_jz) return KFBI_EINVAL;
+  KFBI_TRY(c)
+  need_ws(c);
+  cudaStream_t s = pick(c, stream);
+  BumpParams none{};
+  if (d_base) launch_dst_forward(c->T, d_base, false, none, c->spec, s);
+  launch_correct(c->T, nullptr, nullptr, nullptr, d_jq, c->cval, s);
+  launch_sweep(c->T, c->cval, d_base != nullptr, c->spec, c->zfirst, c->zlast, c->fsep, s);
+  launch_reduced(c->T, c->zfirst, c->zlast, c->fsep, c->hsep, s);
+  if (d_vplus) {
+    launch_inverse_sparse(c->T, c->spec, c->hsep, c->vsten, s);
+    launch_interp(c->T, nullptr, nullptr, nullptr, d_jz, c->vsten, 0, nullptr, nullptr, d_vplus, s);
+  }
+  if (d_v) {
+    launch_inverse_dense(c->T, c->spec, c->hsep, d_v, s);
+    const size_t W = (size_t)c->T.N + 1;
+    ck(cudaMemsetAsync(d_v, 0, W * sizeof(double), s), "memset");
+    ck(cudaMemsetAsync(d_v + (size_t)c->T.N * W, 0, W * sizeof(double), s), "memset");
+  }
+  ck(cudaGetLastError(), "interface solve");
+  KFBI_CATCH(c)
+  return KFBI_OK;
+}
+
+kfbi_status kfbi_test_setup_dump(const kfbi_ctx* c, int32_t which, int64_t* out) {
+  if (!c || !out) return KFBI_EINVAL;
+  const Setup& S = c->S;
+  if (which == 0) {
+    for (int n = 0; n < S.nirr; ++n) { out[2 * n] = S.irr_i[n]; out[2 * n + 1] = S.irr_j[n]; }
+  } else if (which == 1) {
+    for (int q = 0; q < S.nq; ++q) { out[3 * q] = S.q_axis[q]; out[3 * q + 1] = S.q_i[q]; out[3 * q + 2] = S.q_j[q]; }
+  } else if (which == 2) {
+    std::memcpy(out, S.st_nodes_ij.data(), S.st_nodes_ij.size() * sizeof(int64_t));
+  } else {
+    return KFBI_EINVAL;
+  }
+  return KFBI_OK;
+}
+
+}  // extern "C"

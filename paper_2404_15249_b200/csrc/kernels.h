@@ -1,0 +1,59 @@
+// Host-callable launchers of the sm_100a kernels (kernels2d.cu).
+#pragma once
+#include <cuda_runtime.h>
+
+#include "kfbi_impl.h"
+
+namespace kfbi {
+
+// A1: periodic cubic-spline second-derivative knots of φ (M threads).
+void launch_spline(const DevTables& T, const double* phi, double* mk, cudaStream_t s);
+// A2+A3: jumps at intersections + correction at irregular nodes (one thread per node).
+//   phi/mk may be NULL (Φ ≡ 0); fq = [F] at intersections or NULL; jq_given (nq×6) replaces
+//   the jump computation (test path).  Output cval[n] = h² × (correction of f̃ at node n).
+void launch_correct(const DevTables& T, const double* phi, const double* mk, const double* fq,
+                    const double* jq_given, double* cval, cudaStream_t s);
+// A4 (dense input only): forward DST-I of rows i = 1..N−1 of a full-grid base
+//   f̃ = mask·f (+ Σ_h a_h b_h), written to spec[(i−1)·N + k].
+struct BumpParams {
+  int nh;
+  double cx[4], cy[4], rad[4];
+  const double* a;   // device, nh coefficients
+};
+void launch_dst_forward(const DevTables& T, const double* fgrid, bool mask, const BumpParams& bp,
+                        double* spec, cudaStream_t s);
+// A4+A5 fused: per (mode pair, block) local solve with the sparse-correction DST computed
+// on the fly; dense f̂ read from `spec` (in place) when `dense`.
+void launch_sweep(const DevTables& T, const double* cval, bool dense, double* spec, double* zfirst,
+                  double* zlast, double* fsep, cudaStream_t s);
+// A5 reduced (arrowhead) system per mode: separator values h_g.
+void launch_reduced(const DevTables& T, const double* zfirst, const double* zlast, const double* fsep,
+                    double* hsep, cudaStream_t s);
+// A6 sparse: inverse DST-I at the stencil rows only (spike fix-up fused into the load).
+void launch_inverse_sparse(const DevTables& T, const double* spec, const double* hsep, double* vsten,
+                           cudaStream_t s);
+// A6 dense: inverse DST-I of every row into a full (N+1)^2 grid (fix-up fused).
+void launch_inverse_dense(const DevTables& T, const double* spec, const double* hsep, double* vgrid,
+                          cudaStream_t s);
+// hole coefficients a_h = Δ_h Σ_{m∈Γ_h} φ_m (reading R27), one block per hole
+void launch_hole_coeffs(const DevTables& T, const int* hole_off, const int* hole_M, const double* hole_delta,
+                        int nh, const double* phi, double* a, cudaStream_t s);
+// A7: interpolation at control points.  phi/mk NULL → Φ ≡ 0; fz = [F] at control points or
+//   NULL; jz_given (M×6) test path; wg (nh×M) + a (nh) hole completion or NULL.
+void launch_interp(const DevTables& T, const double* phi, const double* mk, const double* fz,
+                   const double* jz_given, const double* vsten, int nh, const double* wg, const double* a,
+                   double* out, cudaStream_t s);
+
+// A8: GMRES vector kernels (deterministic fixed-grid reductions)
+constexpr int kRedBlocks = 64;
+extern long long g_launches;   // kernels launched by this library (all launchers bump it)
+void launch_mgs_step(int n, double* w, const double* Vprev, const double* Vcur, const double* partial_prev,
+                     double* partial_cur, double* hout, cudaStream_t s);
+void launch_norm_scale(int n, double* w, const double* partial, double* hout, cudaStream_t s);
+void launch_dot(int n, const double* a, const double* b, double* partial, cudaStream_t s);
+void launch_finish_sum(const double* partial, double* out, bool take_sqrt, cudaStream_t s);
+void launch_axpy_basis(int n, int k, const double* V, int ldv, const double* y, double* x, cudaStream_t s);
+void launch_sub(int n, const double* a, const double* b, double* out, cudaStream_t s);
+void launch_scale_copy(int n, const double* a, const double* scal, double* out, cudaStream_t s);
+
+}  // namespace kfbi

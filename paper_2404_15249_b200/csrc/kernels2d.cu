@@ -1,0 +1,713 @@
+// sm_100a kernels of the 2D KFBI interface-problem apply (arXiv 2404.15249).
+//
+// One pass of the apply:
+//   k_spline        A1  density interpolant (periodic cubic spline knots, reading R10)
+//   k_correct       A2+A3 jumps at intersections (App. "Calculation of jumps")
+//                   + correction at irregular nodes (Alg. 2)
+//   k_sweep         A4+A5 sine transform of the sparse corrections computed on the fly and
+//                   fused into a partitioned (arrowhead) tridiagonal solve along x
+//   k_reduced       A5  reduced separator system per mode
+//   k_inv_sparse    A6  inverse sine transform at interpolation-stencil rows only, with the
+//                   arrowhead back-substitution s = z − Z_L h_{g−1} − Z_R h_g fused
+//   k_interp        A7  jump-corrected six-point interpolation (Alg. 3)
+//   k_dst_dense     A4/A6 dense rows (FFT-based DST-I in shared memory) for the volume and
+//                   final applies (once per solve)
+// plus deterministic GMRES vector kernels (Alg. 5).  FP64 on CUDA cores: the
+// path is HBM/latency bound, not a dense contraction (no tensor cores).
+#include <cuda_runtime.h>
+
+#include <cstdio>
+
+#include "kernels.h"
+
+namespace kfbi {
+namespace {
+
+__device__ __forceinline__ double sin_lookup(const double* __restrict__ tab, int r, int N) {
+  // sin(π r / N) for r ∈ [0, 2N) from the quarter table sin(π r / N), r ∈ [0, N/2]
+  double sg = 1.0;
+  if (r >= N) { r -= N; sg = -1.0; }
+  if (r > (N >> 1)) r = N - r;
+  return sg * tab[r];
+}
+
+__device__ __forceinline__ void spline_eval(const double* __restrict__ phi, const double* __restrict__ mk, int off,
+                                            int Mc, double delta, int m, double t, double& g, double& gp,
+                                            double& gpp) {
+  // SURVEY App. A.7 on [s_m, s_{m+1}], t = (s − s_m)/Δ
+  int m1 = (m + 1 == Mc) ? 0 : m + 1;
+  double g0 = phi[off + m], g1 = phi[off + m1], a = mk[off + m], b = mk[off + m1];
+  double w = 1.0 - t;
+  g = w * g0 + t * g1 + (delta * delta / 6.0) * ((w * w * w - w) * a + (t * t * t - t) * b);
+  gp = (g1 - g0) / delta + (delta / 6.0) * (-(3.0 * w * w - 1.0) * a + (3.0 * t * t - 1.0) * b);
+  gpp = w * a + t * b;
+}
+
+struct Jump6 {
+  double v, vx, vy, vxx, vxy, vyy;
+};
+
+// Closed form of the appendix 2×2 + 3×3 systems (reading R7 ψ for ψ_s):
+//   [v] = Φ, [∇v] = Φ_s τ + Ψ n, frame components A_ττ, A_τn, A_nn, [D²v] = F A Fᵀ.
+__device__ __forceinline__ Jump6 jumps2d(double Phi, double Phis, double Phiss, double Psi, double Psis, double F,
+                                         double kappa, double t1, double t2, double p1, double p2) {
+  Jump6 J;
+  J.v = Phi;
+  J.vx = t1 * Phis + t2 * Psi;
+  J.vy = t2 * Phis - t1 * Psi;
+  double Att = Phiss - (p1 * J.vx + p2 * J.vy);
+  double Atn = Psis - (p2 * J.vx - p1 * J.vy);
+  double Ann = F + kappa * Phi - Att;
+  J.vxx = Att * t1 * t1 + 2.0 * Atn * t1 * t2 + Ann * t2 * t2;
+  J.vxy = (Att - Ann) * t1 * t2 + Atn * (t2 * t2 - t1 * t1);
+  J.vyy = Att * t2 * t2 - 2.0 * Atn * t1 * t2 + Ann * t1 * t1;
+  return J;
+}
+
+template <int NV>
+__device__ __forceinline__ void block_reduce(double (&v)[NV], double* scratch) {
+  // deterministic: warp shuffle tree, then warp 0 sums the per-warp partials in order
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = (blockDim.x + 31) >> 5;
+#pragma unroll
+  for (int q = 0; q < NV; ++q)
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v[q] += __shfl_xor_sync(0xffffffffu, v[q], o);
+  __syncthreads();
+  if (lane == 0)
+#pragma unroll
+    for (int q = 0; q < NV; ++q) scratch[wid * NV + q] = v[q];
+  __syncthreads();
+  if (threadIdx.x == 0)
+#pragma unroll
+    for (int q = 0; q < NV; ++q) {
+      double s = 0;
+      for (int w = 0; w < nw; ++w) s += scratch[w * NV + q];
+      v[q] = s;
+    }
+}
+
+// ------------------------------------------------------------------------------ A1
+__global__ void k_spline(DevTables T, const double* __restrict__ phi, double* __restrict__ mk) {
+  int m = blockIdx.x * blockDim.x + threadIdx.x;
+  if (m >= T.M) return;
+  int c = T.z_comp[m], ml = T.z_knot[m];
+  int off = T.c_off[c], Mc = T.c_M[c], nt = T.sp_ntaps[c], first = T.sp_first[c];
+  const double* b = T.sp_coef + T.sp_coef_off[c];
+  double acc = 0.0;
+  for (int r = 0; r < nt; ++r) {
+    int idx = ml + first + r;
+    idx %= Mc;
+    if (idx < 0) idx += Mc;
+    acc = fma(b[r], phi[off + idx], acc);
+  }
+  mk[m] = acc;
+}
+
+// ------------------------------------------------------------------------------ A2+A3
+__global__ void k_correct(DevTables T, const double* __restrict__ phi, const double* __restrict__ mk,
+                          const double* __restrict__ fq, const double* __restrict__ jqg, double* __restrict__ cval) {
+  int n = blockIdx.x * blockDim.x + threadIdx.x;
+  if (n >= T.nirr) return;
+  double acc = 0.0;
+  for (int e = T.irr_ptr[n]; e < T.irr_ptr[n + 1]; ++e) {
+    int q = T.pair_q[e];
+    double d = T.pair_d[e];
+    int ax = T.q_axis[q];
+    double v, va, vaa;
+    if (jqg) {
+      v = jqg[q * 6];
+      va = jqg[q * 6 + 1 + ax];
+      vaa = jqg[q * 6 + (ax == 0 ? 3 : 5)];
+    } else {
+      double Phi = 0, Phis = 0, Phiss = 0;
+      if (phi) {
+        int c = T.q_comp[q];
+        spline_eval(phi, mk, T.c_off[c], T.c_M[c], T.c_delta[c], T.q_knot[q], T.q_t[q], Phi, Phis, Phiss);
+      }
+      double F = fq ? fq[q] : 0.0;
+      Jump6 J = jumps2d(Phi, Phis, Phiss, 0.0, 0.0, F, T.kappa, T.q_t1[q], T.q_t2[q], T.q_p1[q], T.q_p2[q]);
+      v = J.v;
+      va = ax == 0 ? J.vx : J.vy;
+      vaa = ax == 0 ? J.vxx : J.vyy;
+    }
+    acc += v + va * d + 0.5 * vaa * d * d;   // P(d), SURVEY App. A.3
+  }
+  // Ω endpoint: −P/h² (C⁺); Ω^c endpoint: +P/h² (C⁻).  Stored ×h².
+  cval[n] = T.irr_side[n] ? -acc : acc;
+}
+
+// ------------------------------------------------------------------------------ A4+A5
+// Thread ↔ mode pair (k, N−k), k = t (t = 0 → mode N/2 alone), one block g of BL−1
+// columns per work item.  sin(πj(N−k)/N) = (−1)^{j+1} sin(πjk/N), so each table lookup
+// serves both modes.  Local Thomas in registers: y_p = r_p − y_{p−1}/c_{p−1}, then
+// z_p = (y_p − z_{p+1})/c_p, with r = h² f̂.  Writes z (block rows), the block end values
+// for the reduced system, and h² f̂ at the separator column.
+template <bool DENSE>
+__global__ void __launch_bounds__(256) k_sweep(DevTables T, const double* __restrict__ cval, double* spec,
+                                               double* __restrict__ zfirst, double* __restrict__ zlast,
+                                               double* __restrict__ fsep) {
+  extern __shared__ double s_sin[];
+  const int N = T.N, half = N >> 1, P = T.P, mask = 2 * N - 1;
+  for (int r = threadIdx.x; r <= half; r += blockDim.x) s_sin[r] = T.sin_tab[r];
+  __syncthreads();
+  const int nch = (half + blockDim.x - 1) / blockDim.x;
+  const int nitems = nch * P;
+  const double h2 = T.h * T.h;
+  for (int item = blockIdx.x; item < nitems; item += gridDim.x) {
+    const int g = item / nch, ch = item - g * nch;
+    const int t = ch * blockDim.x + threadIdx.x;
+    if (t >= half) continue;
+    const int k1 = t == 0 ? half : t;
+    const int k2 = N - k1;
+    double y1[LB], y2[LB];
+    auto rhs = [&](int i, double& r1, double& r2) {
+      r1 = 0.0;
+      r2 = 0.0;
+      if (DENSE) {
+        r1 = h2 * spec[(size_t)(i - 1) * N + k1];
+        r2 = h2 * spec[(size_t)(i - 1) * N + k2];
+      }
+      if (cval) {
+        const int e1 = T.col_ptr[i + 1];
+        for (int e = T.col_ptr[i]; e < e1; ++e) {
+          const int j = __ldg(T.irr_j + e);
+          const double c = __ldg(cval + e);
+          const double s = sin_lookup(s_sin, (j * k1) & mask, N);
+          r1 = fma(c, s, r1);
+          r2 = fma((j & 1) ? c : -c, s, r2);
+        }
+      }
+    };
+#pragma unroll
+    for (int p = 0; p < LB; ++p) {
+      double r1, r2;
+      rhs(BL * g + 1 + p, r1, r2);
+      if (p == 0) {
+        y1[0] = r1;
+        y2[0] = r2;
+      } else {
+        y1[p] = fma(-y1[p - 1], __ldg(T.invc + (size_t)(p - 1) * N + k1), r1);
+        y2[p] = fma(-y2[p - 1], __ldg(T.invc + (size_t)(p - 1) * N + k2), r2);
+      }
+    }
+    y1[LB - 1] *= __ldg(T.invc + (size_t)(LB - 1) * N + k1);
+    y2[LB - 1] *= __ldg(T.invc + (size_t)(LB - 1) * N + k2);
+#pragma unroll
+    for (int p = LB - 2; p >= 0; --p) {
+      y1[p] = (y1[p] - y1[p + 1]) * __ldg(T.invc + (size_t)p * N + k1);
+      y2[p] = (y2[p] - y2[p + 1]) * __ldg(T.invc + (size_t)p * N + k2);
+    }
+#pragma unroll
+    for (int p = 0; p < LB; ++p) {
+      const size_t row = (size_t)(BL * g + p) * N;   // row of column i = BL g + 1 + p
+      spec[row + k1] = y1[p];
+      spec[row + k2] = y2[p];
+    }
+    zfirst[(size_t)g * N + k1] = y1[0];
+    zfirst[(size_t)g * N + k2] = y2[0];
+    zlast[(size_t)g * N + k1] = y1[LB - 1];
+    zlast[(size_t)g * N + k2] = y2[LB - 1];
+    if (g < P - 1) {
+      double r1, r2;
+      rhs(BL * (g + 1), r1, r2);
+      fsep[(size_t)g * N + k1] = r1;
+      fsep[(size_t)g * N + k2] = r2;
+    }
+  }
+}
+
+// ------------------------------------------------------------------------------ A5 reduced
+// −Z_L[L] h_{g−1} + (d − Z_R[L] − Z_L[1]) h_g − Z_R[1] h_{g+1} = f_sep,g − z_g[L] − z_{g+1}[1]
+// (SURVEY App. A.5); constant coefficients a = red_a, b = red_b per mode; Thomas.
+__global__ void k_reduced(DevTables T, const double* __restrict__ zfirst, const double* __restrict__ zlast,
+                          const double* __restrict__ fsep, double* __restrict__ hsep) {
+  const int N = T.N, P = T.P;
+  const int k = blockIdx.x * blockDim.x + threadIdx.x + 1;
+  if (k >= N || P < 2) return;
+  const double a = T.red_a[k];
+  double y = fsep[k] - zlast[k] - zfirst[(size_t)N + k];
+  hsep[k] = y;
+  for (int g = 1; g < P - 1; ++g) {
+    const double r = fsep[(size_t)g * N + k] - zlast[(size_t)g * N + k] - zfirst[(size_t)(g + 1) * N + k];
+    y = fma(-a * y, T.red_invc[(size_t)(g - 1) * N + k], r);
+    hsep[(size_t)g * N + k] = y;
+  }
+  double hn = y * T.red_invc[(size_t)(P - 2) * N + k];
+  hsep[(size_t)(P - 2) * N + k] = hn;
+  for (int g = P - 3; g >= 0; --g) {
+    hn = (hsep[(size_t)g * N + k] - a * hn) * T.red_invc[(size_t)g * N + k];
+    hsep[(size_t)g * N + k] = hn;
+  }
+}
+
+// value of v̂ at column i, mode k: separator → h; block row → z − h_{g−1} Z_L − h_g Z_R
+__device__ __forceinline__ double fixup(const DevTables& T, const double* __restrict__ spec,
+                                        const double* __restrict__ hsep, int i, int k) {
+  const int N = T.N, P = T.P;
+  const int q = i / BL, r = i - q * BL;
+  if (r == 0) return hsep[(size_t)(q - 1) * N + k];
+  const int p = r - 1, g = q;
+  double x = spec[(size_t)(i - 1) * N + k];
+  if (g > 0) x = fma(-hsep[(size_t)(g - 1) * N + k], __ldg(T.zr + (size_t)(LB - 1 - p) * N + k), x);
+  if (g < P - 1) x = fma(-hsep[(size_t)g * N + k], __ldg(T.zr + (size_t)p * N + k), x);
+  return x;
+}
+
+// ------------------------------------------------------------------------------ A6 sparse
+// One CTA per column holding stencil nodes; v_j = (2/N) Σ_k v̂_k sin(πjk/N) at those rows,
+// paired modes: Σ_t sin(πjt/N) (v̂_t ± v̂_{N−t}) + v̂_{N/2} sin(πj/2).
+template <int PPT>
+__global__ void __launch_bounds__(256) k_inv_sparse(DevTables T, const double* __restrict__ spec,
+                                                    const double* __restrict__ hsep, double* __restrict__ vsten) {
+  extern __shared__ double sm[];
+  const int N = T.N, half = N >> 1, mask = 2 * N - 1;
+  double* s_sin = sm;
+  double* scratch = sm + half + 1;
+  for (int r = threadIdx.x; r <= half; r += blockDim.x) s_sin[r] = T.sin_tab[r];
+  const int b = blockIdx.x;
+  const int i = T.ocol[b];
+  double Pv[PPT], Qv[PPT];
+  double xm = 0.0;
+#pragma unroll
+  for (int s = 0; s < PPT; ++s) {
+    const int t = threadIdx.x + s * blockDim.x;
+    const int k1 = t == 0 ? half : t;
+    const double x1 = fixup(T, spec, hsep, i, k1);
+    const double x2 = t == 0 ? 0.0 : fixup(T, spec, hsep, i, N - k1);
+    if (t == 0) {
+      xm = x1;
+      Pv[s] = 0.0;
+      Qv[s] = 0.0;
+    } else {
+      Pv[s] = x1 + x2;
+      Qv[s] = x1 - x2;
+    }
+  }
+  __syncthreads();
+  const double scale = 2.0 / N;
+  const int u0 = T.ocol_ptr[b], u1 = T.ocol_ptr[b + 1];
+  for (int u = u0; u < u1; u += 4) {
+    double acc[4] = {0.0, 0.0, 0.0, 0.0};
+    int js[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) js[q] = (u + q < u1) ? T.sn_j[u + q] : 0;
+#pragma unroll
+    for (int s = 0; s < PPT; ++s) {
+      const int t = threadIdx.x + s * blockDim.x;
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const int j = js[q];
+        const double sv = sin_lookup(s_sin, (j * t) & mask, N);
+        acc[q] = fma((j & 1) ? Pv[s] : Qv[s], sv, acc[q]);
+      }
+    }
+    if (threadIdx.x == 0) {
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const int j = js[q];
+        if (j & 1) acc[q] += ((j >> 1) & 1) ? -xm : xm;   // sin(πj/2)
+      }
+    }
+    block_reduce<4>(acc, scratch);
+    if (threadIdx.x == 0)
+#pragma unroll
+      for (int q = 0; q < 4; ++q)
+        if (u + q < u1) vsten[u + q] = scale * acc[q];
+    __syncthreads();
+  }
+}
+
+// ------------------------------------------------------------------------------ A7
+__global__ void k_interp(DevTables T, const double* __restrict__ phi, const double* __restrict__ mk,
+                         const double* __restrict__ fz, const double* __restrict__ jzg,
+                         const double* __restrict__ vsten, int nh, const double* __restrict__ wg,
+                         const double* __restrict__ ahole, double* __restrict__ out) {
+  const int m = blockIdx.x * blockDim.x + threadIdx.x;
+  if (m >= T.M) return;
+  Jump6 J;
+  if (jzg) {
+    J.v = jzg[m * 6];
+    J.vx = jzg[m * 6 + 1];
+    J.vy = jzg[m * 6 + 2];
+    J.vxx = jzg[m * 6 + 3];
+    J.vxy = jzg[m * 6 + 4];
+    J.vyy = jzg[m * 6 + 5];
+  } else {
+    double Phi = 0, Phis = 0, Phiss = 0;
+    if (phi) {
+      const int c = T.z_comp[m];
+      spline_eval(phi, mk, T.c_off[c], T.c_M[c], T.c_delta[c], T.z_knot[m], 0.0, Phi, Phis, Phiss);
+    }
+    J = jumps2d(Phi, Phis, Phiss, 0.0, 0.0, fz ? fz[m] : 0.0, T.kappa, T.z_t1[m], T.z_t2[m], T.z_p1[m], T.z_p2[m]);
+  }
+  double acc = 0.0;
+#pragma unroll
+  for (int p = 0; p < 6; ++p) {
+    const int idx = m * 6 + p;
+    double v = vsten[T.st_node[idx]];
+    if (T.st_ext[idx]) {   // exterior node: shift by the jump Taylor polynomial
+      const double dx = T.st_dx[idx], dy = T.st_dy[idx];
+      v += J.v + J.vx * dx + J.vy * dy + 0.5 * J.vxx * dx * dx + J.vxy * dx * dy + 0.5 * J.vyy * dy * dy;
+    }
+    acc = fma(T.st_w[idx], v, acc);
+  }
+  for (int hh = 0; hh < nh; ++hh) acc = fma(ahole[hh], wg[(size_t)hh * T.M + m], acc);
+  out[m] = acc;
+}
+
+__global__ void k_hole_coeffs(const int* __restrict__ off, const int* __restrict__ cnt,
+                              const double* __restrict__ delta, const double* __restrict__ phi,
+                              double* __restrict__ a) {
+  __shared__ double scratch[32];
+  const int hh = blockIdx.x;
+  double v[1] = {0.0};
+  for (int m = threadIdx.x; m < cnt[hh]; m += blockDim.x) v[0] += phi[off[hh] + m];
+  block_reduce<1>(v, scratch);
+  if (threadIdx.x == 0) a[hh] = delta[hh] * v[0];
+}
+
+// ------------------------------------------------------------------------------ dense DST-I
+// DST-I of a row by the half-length complex FFT (Numerical-Recipes "sinft" construction):
+//   y_j = sin(πj/N)(f_j + f_{N−j}) + ½(f_j − f_{N−j}),  Y = real DFT(y) (sign +),
+//   F_{2k} = Im Y_k,  F_1 = ½ Re Y_0,  F_{2k+1} = F_{2k−1} + Re Y_k.
+// MODE 0: forward from a full grid base (mask·f + Σ_h a_h bump_h) → spec row.
+// MODE 1: inverse from spec (with the arrowhead fix-up) → full grid row, × 2/N.
+__device__ __forceinline__ void twiddle(const double* tab, int r, int N, double& c, double& s) {
+  const int m2 = 2 * N - 1;
+  s = sin_lookup(tab, r & m2, N);
+  c = sin_lookup(tab, (r + (N >> 1)) & m2, N);
+}
+
+template <int MODE>
+__global__ void __launch_bounds__(256) k_dst_dense(DevTables T, const double* __restrict__ src, int mask_omega,
+                                                   BumpParams bp, const double* __restrict__ hsep,
+                                                   double* __restrict__ dst) {
+  extern __shared__ double sm[];
+  const int N = T.N, half = N >> 1, L = half;
+  double* s_sin = sm;                 // half + 1
+  double* y = sm + half + 1;          // N (as L complex)
+  double* out = y + N;                // N
+  __shared__ double wsum[32];
+  for (int r = threadIdx.x; r <= half; r += blockDim.x) s_sin[r] = T.sin_tab[r];
+  const int i = blockIdx.x + 1;
+  // 1. load f_j (j = 0..N−1, f_0 = 0) into `out`
+  for (int j = threadIdx.x; j < N; j += blockDim.x) {
+    double f = 0.0;
+    if (j > 0) {
+      if (MODE == 0) {
+        const size_t idx = (size_t)i * (N + 1) + j;
+        if (src && (!mask_omega || T.side[idx])) f = src[idx];
+        if (bp.nh) {
+          const double x = T.lo + i * T.h, yy = T.lo + j * T.h;
+          for (int hh = 0; hh < bp.nh; ++hh) {
+            const double rho2 = ((x - bp.cx[hh]) * (x - bp.cx[hh]) + (yy - bp.cy[hh]) * (yy - bp.cy[hh])) /
+                                (bp.rad[hh] * bp.rad[hh]);
+            if (rho2 < 1.0) f += bp.a[hh] * exp(1.0 - 1.0 / (1.0 - rho2));   // bump, SURVEY App. A.8
+          }
+        }
+      } else {
+        f = fixup(T, src, hsep, i, j);
+      }
+    }
+    out[j] = f;
+  }
+  __syncthreads();
+  // 2. y_j, y_{N−j} for j = 1..N/2
+  for (int j = threadIdx.x; j <= half; j += blockDim.x) {
+    if (j == 0) {
+      y[0] = 0.0;
+      continue;
+    }
+    const double a = out[j], b = out[N - j];
+    const double A = s_sin[j] * (a + b), B = 0.5 * (a - b);
+    y[j] = A + B;
+    if (j != half) y[N - j] = A - B;
+  }
+  __syncthreads();
+  // 3. complex FFT (sign +) of length L on z_m = y_{2m} + i y_{2m+1}; bit reversal
+  double2* z = reinterpret_cast<double2*>(y);
+  int lg = 0;
+  while ((1 << lg) < L) ++lg;
+  for (int a = threadIdx.x; a < L; a += blockDim.x) {
+    const int r = __brev(a) >> (32 - lg);
+    if (r > a) {
+      const double2 t = z[a];
+      z[a] = z[r];
+      z[r] = t;
+    }
+  }
+  __syncthreads();
+  for (int len = 1; len < L; len <<= 1) {
+    const int rstep = N / len;   // e^{iπ jj/len} = e^{iπ (jj·N/len)/N}
+    for (int bf = threadIdx.x; bf < (L >> 1); bf += blockDim.x) {
+      const int grp = bf / len, jj = bf - grp * len;
+      const int i0 = grp * 2 * len + jj, i1 = i0 + len;
+      double c, s;
+      twiddle(s_sin, jj * rstep, N, c, s);
+      const double2 u = z[i0], v = z[i1];
+      const double tr = c * v.x - s * v.y, ti = c * v.y + s * v.x;
+      z[i0] = make_double2(u.x + tr, u.y + ti);
+      z[i1] = make_double2(u.x - tr, u.y - ti);
+    }
+    __syncthreads();
+  }
+  // 4. Y_k = E_k + e^{2πik/N} O_k, E = (Z_k + conj Z_{L−k})/2, O = (Z_k − conj Z_{L−k})/(2i)
+  for (int k = threadIdx.x; k < L; k += blockDim.x) {
+    const double2 a = z[k], b = z[(L - k) & (L - 1)];
+    const double er = 0.5 * (a.x + b.x), ei = 0.5 * (a.y - b.y);
+    const double orr = 0.5 * (a.y + b.y), oi = -0.5 * (a.x - b.x);
+    double c, s;
+    twiddle(s_sin, 2 * k, N, c, s);
+    const double yr = er + c * orr - s * oi, yi = ei + c * oi + s * orr;
+    out[2 * k] = yi;                                // F_{2k}
+    out[2 * k + 1] = (k == 0) ? 0.5 * yr : yr;      // increments of the odd recurrence
+  }
+  __syncthreads();
+  // 5. inclusive scan of the odd entries (deterministic: per-thread chunks + ordered warp sums)
+  {
+    const int per = (L + blockDim.x - 1) / blockDim.x;
+    const int k0 = threadIdx.x * per, k1 = min(L, k0 + per);
+    double run = 0.0;
+    for (int k = k0; k < k1; ++k) run += out[2 * k + 1];
+    // exclusive scan of `run` across threads
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    double incl = run;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const double t = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += t;
+    }
+    if (lane == 31) wsum[wid] = incl;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      double acc = 0.0;
+      for (int w = 0; w < (int)(blockDim.x >> 5); ++w) {
+        const double t = wsum[w];
+        wsum[w] = acc;
+        acc += t;
+      }
+    }
+    __syncthreads();
+    double base = wsum[wid] + incl - run;
+    for (int k = k0; k < k1; ++k) {
+      base += out[2 * k + 1];
+      out[2 * k + 1] = base;
+    }
+  }
+  __syncthreads();
+  // 6. store
+  if (MODE == 0) {
+    for (int k = threadIdx.x; k < N; k += blockDim.x) dst[(size_t)(i - 1) * N + k] = (k == 0) ? 0.0 : out[k];
+  } else {
+    const double sc = 2.0 / N;
+    for (int j = threadIdx.x; j <= N; j += blockDim.x)
+      dst[(size_t)i * (N + 1) + j] = (j == 0 || j == N) ? 0.0 : sc * out[j];
+  }
+}
+
+// ------------------------------------------------------------------------------ A8 GMRES
+__device__ __forceinline__ double ordered_sum(const double* __restrict__ p) {
+  double s = 0.0;
+  for (int b = 0; b < kRedBlocks; ++b) s += p[b];
+  return s;
+}
+
+__global__ void k_mgs_step(int n, double* w, const double* Vprev, const double* Vcur, const double* pprev,
+                           double* pcur, double* hout) {
+  __shared__ double scratch[32];
+  const int per = (n + gridDim.x - 1) / gridDim.x;
+  const int b0 = blockIdx.x * per, b1 = min(n, b0 + per);
+  double hp = 0.0;
+  if (Vprev) {
+    hp = ordered_sum(pprev);
+    if (blockIdx.x == 0 && threadIdx.x == 0) *hout = hp;
+  }
+  double v[1] = {0.0};
+  for (int i = b0 + threadIdx.x; i < b1; i += blockDim.x) {
+    double wv = w[i];
+    if (Vprev) {
+      wv = fma(-hp, Vprev[i], wv);
+      w[i] = wv;
+    }
+    v[0] = fma(wv, Vcur[i], v[0]);
+  }
+  block_reduce<1>(v, scratch);
+  if (threadIdx.x == 0) pcur[blockIdx.x] = v[0];
+}
+
+__global__ void k_norm_scale(int n, double* w, const double* __restrict__ partial, double* hout) {
+  const double hn = sqrt(ordered_sum(partial));
+  if (blockIdx.x == 0 && threadIdx.x == 0) *hout = hn;
+  if (hn == 0.0) return;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) w[i] = w[i] / hn;
+}
+
+__global__ void k_dot(int n, const double* __restrict__ a, const double* __restrict__ b, double* __restrict__ partial) {
+  __shared__ double scratch[32];
+  const int per = (n + gridDim.x - 1) / gridDim.x;
+  const int b0 = blockIdx.x * per, b1 = min(n, b0 + per);
+  double v[1] = {0.0};
+  for (int i = b0 + threadIdx.x; i < b1; i += blockDim.x) v[0] = fma(a[i], b[i], v[0]);
+  block_reduce<1>(v, scratch);
+  if (threadIdx.x == 0) partial[blockIdx.x] = v[0];
+}
+
+__global__ void k_finish_sum(const double* __restrict__ partial, double* out, int take_sqrt) {
+  if (threadIdx.x == 0 && blockIdx.x == 0) {
+    const double s = ordered_sum(partial);
+    *out = take_sqrt ? sqrt(s) : s;
+  }
+}
+
+__global__ void k_axpy_basis(int n, int k, const double* __restrict__ V, int ldv, const double* __restrict__ y,
+                             double* __restrict__ x) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    double acc = 0.0;
+    for (int q = 0; q < k; ++q) acc = fma(y[q], V[(size_t)q * ldv + i], acc);
+    x[i] += acc;
+  }
+}
+
+__global__ void k_sub(int n, const double* __restrict__ a, const double* __restrict__ b, double* __restrict__ o) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) o[i] = a[i] - b[i];
+}
+
+__global__ void k_scale_copy(int n, const double* __restrict__ a, const double* __restrict__ scal,
+                             double* __restrict__ o) {
+  const double s = *scal;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) o[i] = a[i] / s;
+}
+
+int g_sweep_grid = 0;
+int g_num_sms = 0;
+
+int num_sms() {
+  if (!g_num_sms) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev);
+    if (g_num_sms <= 0) g_num_sms = 148;
+  }
+  return g_num_sms;
+}
+
+inline int cdiv(long a, long b) { return (int)((a + b - 1) / b); }
+
+}  // namespace
+
+// ============================================================================== launchers
+long long g_launches = 0;
+void launch_spline(const DevTables& T, const double* phi, double* mk, cudaStream_t s) {
+  { ++g_launches; k_spline<<<cdiv(T.M, 256), 256, 0, s>>>(T, phi, mk); }
+}
+
+void launch_correct(const DevTables& T, const double* phi, const double* mk, const double* fq,
+                    const double* jq_given, double* cval, cudaStream_t s) {
+  if (T.nirr == 0) return;
+  { ++g_launches; k_correct<<<cdiv(T.nirr, 128), 128, 0, s>>>(T, phi, mk, fq, jq_given, cval); }
+}
+
+static size_t dense_smem(int N) { return (size_t)(N / 2 + 1 + 2 * N) * sizeof(double); }
+
+void launch_dst_forward(const DevTables& T, const double* fgrid, bool mask, const BumpParams& bp, double* spec,
+                        cudaStream_t s) {
+  const size_t sm = dense_smem(T.N);
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(k_dst_dense<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    cudaFuncSetAttribute(k_dst_dense<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    attr = true;
+  }
+  { ++g_launches; k_dst_dense<0><<<T.N - 1, 256, sm, s>>>(T, fgrid, mask ? 1 : 0, bp, nullptr, spec); }
+}
+
+void launch_inverse_dense(const DevTables& T, const double* spec, const double* hsep, double* vgrid,
+                          cudaStream_t s) {
+  const size_t sm = dense_smem(T.N);
+  BumpParams bp{};
+  { ++g_launches; k_dst_dense<1><<<T.N - 1, 256, sm, s>>>(T, spec, 0, bp, hsep, vgrid); }
+}
+
+void launch_sweep(const DevTables& T, const double* cval, bool dense, double* spec, double* zfirst, double* zlast,
+                  double* fsep, cudaStream_t s) {
+  const size_t sm = (size_t)(T.N / 2 + 1) * sizeof(double);
+  const int half = T.N / 2;
+  const int nitems = cdiv(half, 256) * T.P;
+  if (!g_sweep_grid) {
+    int per = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_sweep<false>, 256, sm);
+    g_sweep_grid = num_sms() * (per > 0 ? per : 1);
+  }
+  const int grid = nitems < g_sweep_grid ? nitems : g_sweep_grid;
+  if (dense)
+    { ++g_launches; k_sweep<true><<<grid, 256, sm, s>>>(T, cval, spec, zfirst, zlast, fsep); }
+  else
+    { ++g_launches; k_sweep<false><<<grid, 256, sm, s>>>(T, cval, spec, zfirst, zlast, fsep); }
+}
+
+void launch_reduced(const DevTables& T, const double* zfirst, const double* zlast, const double* fsep, double* hsep,
+                    cudaStream_t s) {
+  if (T.P < 2) return;
+  { ++g_launches; k_reduced<<<cdiv(T.N - 1, 64), 64, 0, s>>>(T, zfirst, zlast, fsep, hsep); }
+}
+
+void launch_inverse_sparse(const DevTables& T, const double* spec, const double* hsep, double* vsten,
+                           cudaStream_t s) {
+  if (T.nocol == 0) return;
+  const int half = T.N / 2;
+  const int threads = half < 256 ? half : 256;
+  const int ppt = half / threads;
+  const size_t sm = (size_t)(half + 1 + 32 * 4) * sizeof(double);
+  switch (ppt) {
+    case 1: ++g_launches; k_inv_sparse<1><<<T.nocol, threads, sm, s>>>(T, spec, hsep, vsten); break;
+    case 2: ++g_launches; k_inv_sparse<2><<<T.nocol, threads, sm, s>>>(T, spec, hsep, vsten); break;
+    case 4: ++g_launches; k_inv_sparse<4><<<T.nocol, threads, sm, s>>>(T, spec, hsep, vsten); break;
+    case 8: ++g_launches; k_inv_sparse<8><<<T.nocol, threads, sm, s>>>(T, spec, hsep, vsten); break;
+    case 16: ++g_launches; k_inv_sparse<16><<<T.nocol, threads, sm, s>>>(T, spec, hsep, vsten); break;
+    case 32: ++g_launches; k_inv_sparse<32><<<T.nocol, threads, sm, s>>>(T, spec, hsep, vsten); break;
+    default: break;
+  }
+}
+
+void launch_hole_coeffs(const DevTables& T, const int* hole_off, const int* hole_M, const double* hole_delta, int nh,
+                        const double* phi, double* a, cudaStream_t s) {
+  (void)T;
+  if (nh == 0) return;
+  { ++g_launches; k_hole_coeffs<<<nh, 256, 0, s>>>(hole_off, hole_M, hole_delta, phi, a); }
+}
+
+void launch_interp(const DevTables& T, const double* phi, const double* mk, const double* fz, const double* jz_given,
+                   const double* vsten, int nh, const double* wg, const double* a, double* out, cudaStream_t s) {
+  { ++g_launches; k_interp<<<cdiv(T.M, 128), 128, 0, s>>>(T, phi, mk, fz, jz_given, vsten, wg ? nh : 0, wg, a, out); }
+}
+
+void launch_mgs_step(int n, double* w, const double* Vprev, const double* Vcur, const double* partial_prev,
+                     double* partial_cur, double* hout, cudaStream_t s) {
+  { ++g_launches; k_mgs_step<<<kRedBlocks, 256, 0, s>>>(n, w, Vprev, Vcur, partial_prev, partial_cur, hout); }
+}
+
+void launch_norm_scale(int n, double* w, const double* partial, double* hout, cudaStream_t s) {
+  { ++g_launches; k_norm_scale<<<kRedBlocks, 256, 0, s>>>(n, w, partial, hout); }
+}
+
+void launch_dot(int n, const double* a, const double* b, double* partial, cudaStream_t s) {
+  { ++g_launches; k_dot<<<kRedBlocks, 256, 0, s>>>(n, a, b, partial); }
+}
+
+void launch_finish_sum(const double* partial, double* out, bool take_sqrt, cudaStream_t s) {
+  { ++g_launches; k_finish_sum<<<1, 32, 0, s>>>(partial, out, take_sqrt ? 1 : 0); }
+}
+
+void launch_axpy_basis(int n, int k, const double* V, int ldv, const double* y, double* x, cudaStream_t s) {
+  { ++g_launches; k_axpy_basis<<<cdiv(n, 256), 256, 0, s>>>(n, k, V, ldv, y, x); }
+}
+
+void launch_sub(int n, const double* a, const double* b, double* out, cudaStream_t s) {
+  { ++g_launches; k_sub<<<cdiv(n, 256), 256, 0, s>>>(n, a, b, out); }
+}
+
+void launch_scale_copy(int n, const double* a, const double* scal, double* out, cudaStream_t s) {
+  { ++g_launches; k_scale_copy<<<cdiv(n, 256), 256, 0, s>>>(n, a, scal, out); }
+}
+
+}  // namespace kfbi

@@ -1,0 +1,110 @@
+// Internal definitions of the KFBI library (host setup tables, device table views, context).
+// Nothing here is shared with oracle/ (the CPU oracle is an independent NumPy program).
+#pragma once
+
+#include <cstdint>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "../../include/kfbi.h"
+
+namespace kfbi {
+
+// Block structure of the in-GPU partitioned tridiagonal solve along x (arrowhead/ADM,
+// P:79-148, used here across thread blocks of one GPU): blocks of BL−1 columns separated
+// by one separator column (reading R21), so block g covers i ∈ [BL·g+1, BL·g+BL−1] and
+// separator g sits at i = BL·(g+1).  With N = 2^p, N−1 = BL·P − 1 exactly.
+constexpr int BL = 16;
+constexpr int LB = BL - 1;
+
+struct GeomError : std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
+struct ArgError : std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
+
+struct Comp {
+  int kind, role;
+  double c[3];
+  double p[4];
+  int n_ctrl;
+  double L;      // perimeter
+  int M;         // control points
+  int off;       // offset of its knots in φ
+  double delta;  // knot spacing L/M
+};
+
+// Host-side setup products (Procedure 1).  2D.
+struct Setup {
+  int dim = 2;
+  int N = 0, P = 0;
+  double lo = 0, h = 0, kappa = 0;
+  std::vector<Comp> comps;
+  std::vector<int8_t> side;          // (N+1)^2, 1 = Ω
+  // intersections, sorted by (axis, i, j)
+  int nq = 0;
+  std::vector<int32_t> q_axis, q_i, q_j, q_comp, q_knot;
+  std::vector<double> q_xi, q_t, q_theta, q_t1, q_t2, q_p1, q_p2, q_x, q_y;
+  // irregular nodes sorted by (i, j) + CSR to their incident intersections
+  int nirr = 0;
+  std::vector<int32_t> irr_i, irr_j, irr_ptr, pair_q;
+  std::vector<int8_t> irr_side;
+  std::vector<double> pair_d;        // x_a(p̄) − ξ for the (node, intersection) pair
+  std::vector<int32_t> col_ptr;      // N+1 entries: irregular nodes of column i in [col_ptr[i], col_ptr[i+1])
+  // control points
+  int M = 0;
+  std::vector<int32_t> z_comp, z_knot;
+  std::vector<double> z_x, z_y, z_t1, z_t2, z_p1, z_p2;
+  // six-point stencils (reading R14): unique stencil nodes sorted by (i, j)
+  int nsn = 0;
+  std::vector<int32_t> sn_i, sn_j;
+  std::vector<int32_t> ocol, ocol_ptr;   // columns holding stencil nodes, CSR into sn_*
+  std::vector<int32_t> st_node;          // M*6 → unique stencil node index
+  std::vector<int8_t> st_ext;            // M*6: 1 if the node is in Ω^c
+  std::vector<double> st_w, st_dx, st_dy;   // M*6: row 0 of the inverse local system, offsets
+  std::vector<int64_t> st_nodes_ij;      // M*6*2 (dump)
+  // spline filters: per component taps, coefficients (already scaled by 6/Δ²)
+  std::vector<int32_t> sp_ntaps, sp_first, sp_coef_off;
+  std::vector<double> sp_coef;
+  // fast solver tables, mode k = 0..N−1 (k = 0 unused)
+  std::vector<double> sin_tab;       // sin(π r / N), r = 0..N/2
+  std::vector<double> dk;            // N
+  std::vector<double> invc;          // LB × N: 1/c_p of a fresh block
+  std::vector<double> zr;            // LB × N: (S⁻¹ e_L)[p]
+  std::vector<double> red_a, red_b;  // N: reduced-system off-diagonal / diagonal
+  std::vector<double> red_invc;      // (P−1) × N
+  // holes (κ = 0 completion, reading R27)
+  std::vector<int> holes;            // component ids
+};
+
+void build_setup(Setup& S, const kfbi_grid* g, const kfbi_boundary* b, const kfbi_pde* pde);
+
+// ---- device views -------------------------------------------------------------------
+struct DevTables {
+  int N, P, M, nq, nirr, nsn, nocol, ncomp;
+  double lo, h, kappa;
+  // intersections
+  const int32_t *q_axis, *q_comp, *q_knot;
+  const double *q_t, *q_t1, *q_t2, *q_p1, *q_p2;
+  // irregular nodes
+  const int32_t *irr_j, *irr_ptr, *pair_q, *col_ptr;
+  const int8_t* irr_side;
+  const double* pair_d;
+  // control points
+  const int32_t *z_comp, *z_knot;
+  const double *z_t1, *z_t2, *z_p1, *z_p2;
+  // stencils
+  const int32_t *sn_j, *ocol, *ocol_ptr, *st_node;
+  const int8_t* st_ext;
+  const double *st_w, *st_dx, *st_dy;
+  // spline
+  const int32_t *c_off, *c_M, *sp_ntaps, *sp_first, *sp_coef_off;
+  const double *c_delta, *sp_coef;
+  // fast solver
+  const double *sin_tab, *dk, *invc, *zr, *red_a, *red_b, *red_invc;
+  const int8_t* side;
+};
+
+}  // namespace kfbi

@@ -1,0 +1,267 @@
+"""Thin ctypes binding of include/kfbi.h (argument marshalling only).
+
+Every step of the KFBI path runs in the sm_100a kernels of lib/libkfbi.so; PyTorch only
+provides device memory (the workspace and I/O tensors) and the CUDA stream.  There is no
+CPU fallback: if the library is missing this module raises.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import dataclasses
+import os
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "lib", "libkfbi.so")
+
+OK, EINVAL, EGEOM, ENOCONV, ECUDA, ENCCL, ENOMEM, EUNSUPPORTED = range(8)
+_NAMES = {0: "OK", 1: "EINVAL", 2: "EGEOM", 3: "ENOCONV", 4: "ECUDA", 5: "ENCCL", 6: "ENOMEM", 7: "EUNSUPPORTED"}
+
+EXPORTS = ["kfbi_version", "kfbi_last_error", "kfbi_last_setup_error", "kfbi_get_unique_id", "kfbi_setup",
+           "kfbi_workspace_size", "kfbi_set_workspace", "kfbi_sizes", "kfbi_points", "kfbi_node_mask",
+           "kfbi_apply", "kfbi_solve", "kfbi_apply_model", "kfbi_destroy", "kfbi_test_fast_solve",
+           "kfbi_test_interface_solve", "kfbi_test_setup_dump", "kfbi_profile_apply", "kfbi_launch_count"]
+
+
+class KfbiError(RuntimeError):
+    def __init__(self, code, msg):
+        super().__init__(f"kfbi {_NAMES.get(code, code)}: {msg}")
+        self.code = code
+
+
+class Grid(C.Structure):
+    _fields_ = [("dim", C.c_int32), ("lo", C.c_double * 3), ("hi", C.c_double * 3), ("n", C.c_int32 * 3)]
+
+
+class Component(C.Structure):
+    _fields_ = [("kind", C.c_int32), ("role", C.c_int32), ("center", C.c_double * 3), ("p", C.c_double * 4),
+                ("n_ctrl", C.c_int32)]
+
+
+class Boundary(C.Structure):
+    _fields_ = [("ncomp", C.c_int32), ("comp", C.POINTER(Component))]
+
+
+class Pde(C.Structure):
+    _fields_ = [("kappa", C.c_double), ("bc", C.c_int32)]
+
+
+class Dist(C.Structure):
+    _fields_ = [("world", C.c_int32), ("rank", C.c_int32), ("device", C.c_int32), ("nccl_id", C.c_void_p)]
+
+
+class SolveOpts(C.Structure):
+    _fields_ = [("tol", C.c_double), ("restart", C.c_int32), ("max_restarts", C.c_int32)]
+
+
+class SolveStats(C.Structure):
+    _fields_ = [("iters", C.c_int32), ("restarts", C.c_int32), ("n_applies", C.c_int32), ("converged", C.c_int32),
+                ("rel_residual", C.c_double), ("t_solve_s", C.c_double)]
+
+
+_lib = None
+
+
+def load(path: str = LIB_PATH):
+    """Load lib/libkfbi.so (raises if it is not built — no fallback)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(path):
+        raise RuntimeError(f"CUDA library {path} is not built; run python -m paper_2404_15249_b200.build")
+    lib = C.CDLL(path)
+    vp, dp, i32, i64p = C.c_void_p, C.POINTER(C.c_double), C.c_int32, C.POINTER(C.c_int64)
+    lib.kfbi_version.restype = C.c_char_p
+    lib.kfbi_last_error.restype = C.c_char_p
+    lib.kfbi_last_error.argtypes = [vp]
+    lib.kfbi_last_setup_error.restype = C.c_char_p
+    lib.kfbi_get_unique_id.argtypes = [vp]
+    lib.kfbi_setup.argtypes = [C.POINTER(Grid), C.POINTER(Boundary), C.POINTER(Pde), C.POINTER(Dist), vp, C.POINTER(vp)]
+    lib.kfbi_workspace_size.argtypes = [vp, C.POINTER(C.c_size_t)]
+    lib.kfbi_set_workspace.argtypes = [vp, vp, C.c_size_t]
+    lib.kfbi_sizes.argtypes = [vp, i64p, i64p, i64p, i64p]
+    lib.kfbi_points.argtypes = [vp, i32, dp]
+    lib.kfbi_node_mask.argtypes = [vp, C.POINTER(C.c_int8)]
+    lib.kfbi_apply.argtypes = [vp, vp, vp, vp]
+    lib.kfbi_solve.argtypes = [vp, vp, vp, vp, vp, vp, vp, vp, C.POINTER(SolveOpts), C.POINTER(SolveStats), vp]
+    lib.kfbi_apply_model.argtypes = [vp, dp, dp, dp]
+    lib.kfbi_destroy.argtypes = [vp]
+    lib.kfbi_test_fast_solve.argtypes = [vp, vp, vp, vp]
+    lib.kfbi_test_interface_solve.argtypes = [vp, vp, vp, vp, vp, vp, vp]
+    lib.kfbi_test_setup_dump.argtypes = [vp, i32, i64p]
+    lib.kfbi_profile_apply.argtypes = [vp, vp, vp, i32, dp, vp]
+    lib.kfbi_launch_count.argtypes = [i64p]
+    for name in EXPORTS:
+        getattr(lib, name).restype = C.c_char_p if name in ("kfbi_version", "kfbi_last_error",
+                                                            "kfbi_last_setup_error") else C.c_int32
+    _lib = lib
+    return lib
+
+
+def _ptr(t):
+    return None if t is None else C.c_void_p(t.data_ptr())
+
+
+def launch_count() -> int:
+    c = C.c_int64()
+    load().kfbi_launch_count(C.byref(c))
+    return c.value
+
+
+@dataclasses.dataclass
+class Stats:
+    iters: int
+    restarts: int
+    n_applies: int
+    converged: bool
+    rel_residual: float
+    t_solve_s: float
+
+
+class KFBI:
+    """One context per (problem, device).  `problem` is any object with dim, n, lo, hi,
+    kappa and comps (each with kind, role, center, p, n_ctrl) — e.g. workloads.Problem."""
+
+    def __init__(self, problem, device: int = 0, stream=None, workspace: bool = True):
+        import torch
+        self.torch = torch
+        self.lib = load()
+        self.device = torch.device("cuda", device)
+        self.ctx = None
+        self.problem = problem
+        d = problem.dim
+        g = Grid(d, (C.c_double * 3)(*([problem.lo] * 3)), (C.c_double * 3)(*([problem.hi] * 3)),
+                 (C.c_int32 * 3)(*([problem.n] * 3)))
+        comps = (Component * len(problem.comps))()
+        for k, c in enumerate(problem.comps):
+            cen = list(c.center) + [0.0] * (3 - len(c.center))
+            comps[k] = Component(c.kind, c.role, (C.c_double * 3)(*cen), (C.c_double * 4)(*c.p), c.n_ctrl)
+        self._comps = comps
+        b = Boundary(len(problem.comps), comps)
+        pde = Pde(problem.kappa, 0)
+        dist = Dist(1, 0, device, None)
+        ctx = C.c_void_p()
+        st = self.lib.kfbi_setup(C.byref(g), C.byref(b), C.byref(pde), C.byref(dist), None, C.byref(ctx))
+        if st != OK:
+            raise KfbiError(st, self.lib.kfbi_last_setup_error().decode())
+        self.ctx = ctx
+        nb = C.c_size_t()
+        self._check(self.lib.kfbi_workspace_size(ctx, C.byref(nb)))
+        self.workspace_bytes = nb.value
+        if workspace:   # host-only setups (CPU tests of Procedure 1) skip the device part
+            self.ws = torch.empty(nb.value, dtype=torch.uint8, device=self.device)
+            with torch.cuda.device(self.device):
+                self._check(self.lib.kfbi_set_workspace(ctx, C.c_void_p(self.ws.data_ptr()), nb.value))
+        M, nq, nirr, nn = C.c_int64(), C.c_int64(), C.c_int64(), C.c_int64()
+        self._check(self.lib.kfbi_sizes(ctx, C.byref(M), C.byref(nq), C.byref(nirr), C.byref(nn)))
+        self.M, self.nq, self.nirr, self.n_nodes = M.value, nq.value, nirr.value, nn.value
+        self.n = problem.n
+
+    # ------------------------------------------------------------------ helpers
+    def _check(self, st):
+        if st != OK:
+            raise KfbiError(st, self.lib.kfbi_last_error(self.ctx).decode())
+
+    def _stream(self, stream):
+        s = stream if stream is not None else self.torch.cuda.current_stream(self.device)
+        return C.c_void_p(s.cuda_stream)
+
+    def _dev(self, x, n=None):
+        t = self.torch
+        if x is None:
+            return None
+        if not isinstance(x, t.Tensor):
+            x = t.as_tensor(np.ascontiguousarray(x, dtype=np.float64))
+        x = x.to(device=self.device, dtype=t.float64).contiguous()
+        if n is not None and x.numel() != n:
+            raise ValueError(f"expected {n} values, got {x.numel()}")
+        return x
+
+    def close(self):
+        if getattr(self, "ctx", None):
+            self.lib.kfbi_destroy(self.ctx)
+            self.ctx = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    # ------------------------------------------------------------------ API
+    def points(self, which="ctrl"):
+        n = self.M if which == "ctrl" else self.nq
+        out = np.zeros((n, self.problem.dim))
+        self._check(self.lib.kfbi_points(self.ctx, 0 if which == "ctrl" else 1,
+                                         out.ctypes.data_as(C.POINTER(C.c_double))))
+        return out
+
+    def node_mask(self):
+        out = np.zeros(self.n_nodes, dtype=np.int8)
+        self._check(self.lib.kfbi_node_mask(self.ctx, out.ctypes.data_as(C.POINTER(C.c_int8))))
+        return out.reshape((self.n + 1,) * self.problem.dim)
+
+    def apply(self, phi, out=None, stream=None):
+        phi = self._dev(phi, self.M)
+        out = self.torch.empty_like(phi) if out is None else out
+        self._check(self.lib.kfbi_apply(self.ctx, _ptr(phi), _ptr(out), self._stream(stream)))
+        return out
+
+    def solve(self, g, f_grid=None, f_isect=None, f_ctrl=None, phi0=None, tol=1e-8, restart=30,
+              max_restarts=50, u=None, stream=None, raise_on_noconv=True):
+        t = self.torch
+        g = self._dev(g, self.M)
+        fg = self._dev(f_grid, self.n_nodes)
+        fq = self._dev(f_isect, self.nq)
+        fz = self._dev(f_ctrl, self.M)
+        p0 = self._dev(phi0, self.M)
+        u = t.empty(self.n_nodes, dtype=t.float64, device=self.device) if u is None else u
+        phi = t.empty(self.M, dtype=t.float64, device=self.device)
+        opts = SolveOpts(tol, restart, max_restarts)
+        st = SolveStats()
+        code = self.lib.kfbi_solve(self.ctx, _ptr(g), _ptr(fg), _ptr(fq), _ptr(fz), _ptr(p0), _ptr(u), _ptr(phi),
+                                   C.byref(opts), C.byref(st), self._stream(stream))
+        if code != OK and (code != ENOCONV or raise_on_noconv):
+            self._check(code)
+        stats = Stats(st.iters, st.restarts, st.n_applies, bool(st.converged), st.rel_residual, st.t_solve_s)
+        return u.view((self.n + 1,) * self.problem.dim), phi, stats
+
+    def apply_model(self):
+        a, b, c = C.c_double(), C.c_double(), C.c_double()
+        self._check(self.lib.kfbi_apply_model(self.ctx, C.byref(a), C.byref(b), C.byref(c)))
+        return {"bytes_sweep": a.value, "bytes_inverse": b.value, "unknowns": c.value}
+
+    def profile_apply(self, phi, reps=10, stream=None):
+        """Per-kernel CUDA-event times (ms) of one apply: spline, correct, sweep, reduced,
+        inverse, hole, interp, total."""
+        phi = self._dev(phi, self.M)
+        out = self.torch.empty_like(phi)
+        ms = (C.c_double * 8)()
+        self._check(self.lib.kfbi_profile_apply(self.ctx, _ptr(phi), _ptr(out), reps, ms, self._stream(stream)))
+        names = ["spline", "correct", "sweep", "reduced", "inverse", "hole", "interp", "apply"]
+        return dict(zip(names, list(ms)))
+
+    # ------------------------------------------------------------------ test-only
+    def test_fast_solve(self, rhs_full, stream=None):
+        rhs = self._dev(rhs_full, self.n_nodes)
+        v = self.torch.empty_like(rhs)
+        self._check(self.lib.kfbi_test_fast_solve(self.ctx, _ptr(rhs), _ptr(v), self._stream(stream)))
+        return v.view((self.n + 1,) * self.problem.dim)
+
+    def test_interface_solve(self, base_full, jq, jz, want_field=True, stream=None):
+        base = self._dev(base_full, self.n_nodes)
+        jq = self._dev(jq, self.nq * 6)
+        jz = self._dev(jz, self.M * 6)
+        v = self.torch.empty(self.n_nodes, dtype=self.torch.float64, device=self.device) if want_field else None
+        vp = self.torch.empty(self.M, dtype=self.torch.float64, device=self.device)
+        self._check(self.lib.kfbi_test_interface_solve(self.ctx, _ptr(base), _ptr(jq), _ptr(jz), _ptr(v), _ptr(vp),
+                                                       self._stream(stream)))
+        return (v.view((self.n + 1,) * self.problem.dim) if v is not None else None), vp
+
+    def setup_dump(self, which):
+        d = self.problem.dim
+        shape = {0: (self.nirr, d), 1: (self.nq, d + 1), 2: (self.M, 6, d)}[which]
+        out = np.zeros(int(np.prod(shape)), dtype=np.int64)
+        self._check(self.lib.kfbi_test_setup_dump(self.ctx, which, out.ctypes.data_as(C.POINTER(C.c_int64))))
+        return out.reshape(shape)

@@ -1,0 +1,171 @@
+"""GPU parity of the CUDA path (through the C ABI) against the CPU oracle, same seeded inputs.
+
+Bars (BASELINE.json north_star): fast solve ≤ 1e-12 relative max-norm,
+kfbi_apply ≤ 1e-10, final solution ≤ 1e-8 with GMRES iteration counts within ±1.
+"""
+import numpy as np
+import pytest
+import torch
+
+import workloads as W
+from oracle import fastsolve
+from oracle.bie import Oracle2D
+from paper_2404_15249_b200 import KFBI
+
+pytestmark = pytest.mark.gpu
+
+_OR, _GPU = {}, {}
+
+
+def oracle(prob):
+    if prob not in _OR:
+        _OR[prob] = Oracle2D(prob)
+    return _OR[prob]
+
+
+def gpu(prob):
+    assert torch.cuda.is_available(), "GPU tests need a CUDA device (no CPU fallback exists)"
+    if prob not in _GPU:
+        _GPU[prob] = KFBI(prob)
+    return _GPU[prob]
+
+
+def rel(a, b):
+    return float(np.abs(a - b).max() / max(np.abs(b).max(), 1e-300))
+
+
+def _quad(seed):
+    a = np.random.default_rng(seed).uniform(-1, 1, 6)
+    q = lambda x, y: a[0] + a[1] * x + a[2] * y + a[3] * x * x + a[4] * x * y + a[5] * y * y
+    gq = lambda x, y: np.stack([a[1] + 2 * a[3] * x + a[4] * y, a[2] + a[4] * x + 2 * a[5] * y])
+    H = np.array([[2 * a[3], a[4]], [a[4], 2 * a[5]]])
+    return q, gq, H
+
+
+# ------------------------------------------------------------------ fast solver (Alg. 4)
+@pytest.mark.parametrize("n,kappa", [(64, 0.0), (1024, 1.0), (2048, 0.0)])
+def test_fast_solve_matches_oracle(n, kappa):
+    prob = W.problem(f"box{n}", 2, n, [W.ellipse(1.0, 0.8)], kappa)
+    k = gpu(prob)
+    rhs = np.random.default_rng(n).uniform(-1, 1, (n + 1, n + 1))
+    v = k.test_fast_solve(rhs).cpu().numpy()
+    ref = fastsolve.solve2d(rhs[1:n, 1:n], prob.h, kappa)
+    assert rel(v[1:n, 1:n], ref) < 1e-12
+    assert np.all(v[0] == 0) and np.all(v[:, -1] == 0)
+
+
+def test_fast_solve_eigenfunction_full_size():
+    n = 8192
+    prob = W.problem("box8192", 2, n, [W.ellipse(1.0, 0.8)], 0.0)
+    k = gpu(prob)
+    h = prob.h
+    i = np.arange(n + 1)
+    p, q = 3, 4001
+    S = np.outer(np.sin(np.pi * p * i / n), np.sin(np.pi * q * i / n))
+    lam = -4 / h ** 2 * (np.sin(np.pi * p / (2 * n)) ** 2 + np.sin(np.pi * q / (2 * n)) ** 2)
+    v = k.test_fast_solve(lam * S).cpu().numpy()
+    assert np.abs(v - S).max() < 1e-10
+
+
+# ------------------------------------------------------------------ interface solve witness
+@pytest.mark.parametrize("prob", [W.C1(64), W.C2(1024), W.C3(2048)], ids=lambda p: p.name + str(p.n))
+def test_interface_solve_piecewise_quadratic(prob):
+    """v = q·1_Ω with exact jumps is reproduced at every node and at V⁺(z) = q(z)."""
+    k = gpu(prob)
+    n = prob.n
+    q, gq, H = _quad(5)
+    x = prob.lo + np.arange(n + 1) * prob.h
+    X, Y = np.meshgrid(x, x, indexing="ij")
+    mask = k.node_mask().astype(bool)
+    pq = k.points("isect")
+    pz = k.points("ctrl")
+    Gq, Gz = gq(pq[:, 0], pq[:, 1]), gq(pz[:, 0], pz[:, 1])
+    jq = np.stack([q(pq[:, 0], pq[:, 1]), Gq[0], Gq[1], np.full(k.nq, H[0, 0]), np.full(k.nq, H[0, 1]),
+                   np.full(k.nq, H[1, 1])], -1)
+    jz = np.stack([q(pz[:, 0], pz[:, 1]), Gz[0], Gz[1], np.full(k.M, H[0, 0]), np.full(k.M, H[0, 1]),
+                   np.full(k.M, H[1, 1])], -1)
+    base = np.where(mask, np.trace(H) - prob.kappa * q(X, Y), 0.0)
+    v, vp = k.test_interface_solve(base, jq, jz)
+    assert np.abs(v.cpu().numpy() - np.where(mask, q(X, Y), 0.0)).max() < 1e-10
+    assert np.abs(vp.cpu().numpy() - q(pz[:, 0], pz[:, 1])).max() < 1e-10
+
+
+# ------------------------------------------------------------------ K_D apply
+DENS = ["seed0", "seed1", "seed2", "smooth"]
+
+
+def density(prob, o, name):
+    if name == "smooth":
+        return W.smooth_density(o.st.comp_M)
+    return W.random_density(o.M, int(name[-1]))
+
+
+@pytest.mark.parametrize("prob", [W.C1(64), W.C2(1024), W.C3(1024)], ids=lambda p: p.name + str(p.n))
+@pytest.mark.parametrize("dens", DENS)
+def test_apply_matches_oracle(prob, dens):
+    o, k = oracle(prob), gpu(prob)
+    phi = density(prob, o, dens)
+    out = k.apply(phi).cpu().numpy()
+    ref = o.apply_KD(phi)
+    assert rel(out, ref) < 1e-10
+
+
+def test_apply_constant_density():
+    k = gpu(W.C1(64))
+    out = k.apply(np.ones(k.M)).cpu().numpy()
+    assert np.abs(out - 1).max() < 1e-12          # K_D(1) = 1 at κ = 0 (R17)
+
+
+def test_apply_deterministic():
+    prob = W.C2(1024)
+    k = gpu(prob)
+    phi = torch.tensor(W.random_density(k.M, 7), device="cuda")
+    a = k.apply(phi).clone()
+    b = k.apply(phi).clone()
+    assert torch.equal(a, b)
+
+
+@pytest.mark.slow
+def test_apply_full_size_C3():
+    prob = W.C3(8192)
+    o, k = oracle(prob), gpu(prob)
+    phi = W.random_density(o.M, 0)
+    assert rel(k.apply(phi).cpu().numpy(), o.apply_KD(phi)) < 1e-10
+
+
+# ------------------------------------------------------------------ full solve
+@pytest.mark.parametrize("prob", [W.C1(64), W.C2(1024), W.C3(1024)], ids=lambda p: p.name + str(p.n))
+def test_solve_matches_oracle(prob):
+    o, k = oracle(prob), gpu(prob)
+    n = prob.n
+    f = lambda x, y: W.f_exact(prob.kappa, x, y)
+    zx, zy = o.ctrl_points()
+    u_ref, phi_ref, s_ref = o.solve(W.u_exact(zx, zy), f)
+    pz, pq = k.points("ctrl"), k.points("isect")
+    x = prob.lo + np.arange(n + 1) * prob.h
+    X, Y = np.meshgrid(x, x, indexing="ij")
+    u, phi, s = k.solve(W.u_exact(pz[:, 0], pz[:, 1]), f(X, Y), f(pq[:, 0], pq[:, 1]), f(pz[:, 0], pz[:, 1]))
+    u = u.cpu().numpy()
+    m = o.st.side
+    assert s.converged and abs(s.iters - s_ref.iters) <= 1
+    assert rel(u[m], u_ref[m]) < 1e-8
+    assert rel(phi.cpu().numpy(), phi_ref) < 1e-8
+    # and the solution is the manufactured one to discretisation accuracy
+    assert np.abs(u[m] - W.u_exact(X, Y)[m]).max() < 50 * prob.h ** 2
+
+
+def test_solve_second_order_on_gpu():
+    errs = []
+    for n in (256, 512, 1024, 2048):
+        prob = W.C2(n)
+        k = gpu(prob)
+        pz, pq = k.points("ctrl"), k.points("isect")
+        x = prob.lo + np.arange(n + 1) * prob.h
+        X, Y = np.meshgrid(x, x, indexing="ij")
+        f = lambda a, b: W.f_exact(prob.kappa, a, b)
+        u, phi, s = k.solve(W.u_exact(pz[:, 0], pz[:, 1]), f(X, Y), f(pq[:, 0], pq[:, 1]), f(pz[:, 0], pz[:, 1]))
+        m = k.node_mask().astype(bool)
+        e = u.cpu().numpy()[m] - W.u_exact(X, Y)[m]
+        errs.append(np.sqrt(np.mean(e * e)))
+    orders = np.log2(np.array(errs[:-1]) / np.array(errs[1:]))
+    assert np.all(orders > 1.6) and np.all(orders < 2.6), orders

@@ -67,7 +67,7 @@ enum { KFBI_DIRICHLET = 0, KFBI_NEUMANN = 1 };
 typedef struct {
   int32_t dim;           /* 2 (3 reserved)                                   */
   double lo[3], hi[3];   /* box B; (hi − lo)/n must be equal on all axes      */
-  int32_t n[3];          /* intervals per axis, power of two ≥ 64, all equal  */
+  int32_t n[3];          /* intervals per axis, power of two in [64, 8192], all equal */
 } kfbi_grid;
 
 typedef struct {

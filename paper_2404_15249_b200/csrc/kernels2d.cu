@@ -367,9 +367,12 @@ __global__ void k_hole_coeffs(const int* __restrict__ off, const int* __restrict
 }
 
 // ------------------------------------------------------------------------------ dense DST-I
-// DST-I of a row by the half-length complex FFT (Numerical-Recipes "sinft" construction):
-//   y_j = sin(πj/N)(f_j + f_{N−j}) + ½(f_j − f_{N−j}),  Y = real DFT(y) (sign +),
-//   F_{2k} = Im Y_k,  F_1 = ½ Re Y_0,  F_{2k+1} = F_{2k−1} + Re Y_k.
+// DST-I of a row as the real DFT of its odd extension x̃ (length 2N: x̃_j = f_j, x̃_N = 0,
+// x̃_{2N−j} = −f_j), computed by one complex FFT of length N on z_m = x̃_{2m} + i x̃_{2m+1}:
+//   X_k = E_k + e^{iπk/N} O_k,  E = (Z_k + conj Z_{N−k})/2,  O = (Z_k − conj Z_{N−k})/(2i),
+//   F_k = Σ_j f_j sin(πjk/N) = Im X_k / 2      (sign + transform).
+// No running-sum recurrence, so the error stays O(ε log N) (a "sinft"-style half-length
+// transform with a prefix sum measured 25× worse backward error in the fast solve).
 // MODE 0: forward from a full grid base (mask·f + Σ_h a_h bump_h) → spec row.
 // MODE 1: inverse from spec (with the arrowhead fix-up) → full grid row, × 2/N.
 __device__ __forceinline__ void twiddle(const double* tab, int r, int N, double& c, double& s) {
@@ -383,63 +386,58 @@ __global__ void __launch_bounds__(256) k_dst_dense(DevTables T, const double* __
                                                    BumpParams bp, const double* __restrict__ hsep,
                                                    double* __restrict__ dst) {
   extern __shared__ double sm[];
-  const int N = T.N, half = N >> 1, L = half;
-  double* s_sin = sm;                 // half + 1
-  double* y = sm + half + 1;          // N (as L complex)
-  double* out = y + N;                // N
-  __shared__ double wsum[32];
+  const int N = T.N, half = N >> 1;
+  double* s_sin = sm;                                          // half + 1 (padded to even)
+  double2* z = reinterpret_cast<double2*>(sm + half + 2);      // N complex
+  double* f = reinterpret_cast<double*>(z);                    // f_j staged in the upper half
   for (int r = threadIdx.x; r <= half; r += blockDim.x) s_sin[r] = T.sin_tab[r];
   const int i = blockIdx.x + 1;
-  // 1. load f_j (j = 0..N−1, f_0 = 0) into `out`
+  // 1. load f_j (j = 0..N−1, f_0 = 0) into the upper half of the z buffer (doubles N..2N−1)
   for (int j = threadIdx.x; j < N; j += blockDim.x) {
-    double f = 0.0;
+    double v = 0.0;
     if (j > 0) {
       if (MODE == 0) {
         const size_t idx = (size_t)i * (N + 1) + j;
-        if (src && (!mask_omega || T.side[idx])) f = src[idx];
+        if (src && (!mask_omega || T.side[idx])) v = src[idx];
         if (bp.nh) {
           const double x = T.lo + i * T.h, yy = T.lo + j * T.h;
           for (int hh = 0; hh < bp.nh; ++hh) {
             const double rho2 = ((x - bp.cx[hh]) * (x - bp.cx[hh]) + (yy - bp.cy[hh]) * (yy - bp.cy[hh])) /
                                 (bp.rad[hh] * bp.rad[hh]);
-            if (rho2 < 1.0) f += bp.a[hh] * exp(1.0 - 1.0 / (1.0 - rho2));   // bump, SURVEY App. A.8
+            if (rho2 < 1.0) v += bp.a[hh] * exp(1.0 - 1.0 / (1.0 - rho2));   // bump, SURVEY App. A.8
           }
         }
       } else {
-        f = fixup(T, src, hsep, i, j);
+        v = fixup(T, src, hsep, i, j);
       }
     }
-    out[j] = f;
+    f[N + j] = v;
   }
   __syncthreads();
-  // 2. y_j, y_{N−j} for j = 1..N/2
-  for (int j = threadIdx.x; j <= half; j += blockDim.x) {
-    if (j == 0) {
-      y[0] = 0.0;
-      continue;
-    }
-    const double a = out[j], b = out[N - j];
-    const double A = s_sin[j] * (a + b), B = 0.5 * (a - b);
-    y[j] = A + B;
-    if (j != half) y[N - j] = A - B;
-  }
-  __syncthreads();
-  // 3. complex FFT (sign +) of length L on z_m = y_{2m} + i y_{2m+1}; bit reversal
-  double2* z = reinterpret_cast<double2*>(y);
+  // 2. z_m = x̃_{2m} + i x̃_{2m+1}, written in bit-reversed order for the DIT FFT
   int lg = 0;
-  while ((1 << lg) < L) ++lg;
-  for (int a = threadIdx.x; a < L; a += blockDim.x) {
-    const int r = __brev(a) >> (32 - lg);
-    if (r > a) {
-      const double2 t = z[a];
-      z[a] = z[r];
-      z[r] = t;
+  while ((1 << lg) < N) ++lg;
+  {
+    // read all needed f first (the upper half of z aliases f), then write after a barrier
+    const int per = (N + blockDim.x - 1) / blockDim.x;
+    double2 buf[32];
+    int cnt = 0;
+    for (int m = threadIdx.x; m < N && cnt < 32; m += blockDim.x, ++cnt) {
+      const int j0 = 2 * m, j1 = 2 * m + 1;
+      const double a = j0 < N ? f[N + j0] : (j0 == N ? 0.0 : -f[N + 2 * N - j0]);
+      const double b = j1 < N ? f[N + j1] : -f[N + 2 * N - j1];
+      buf[cnt] = make_double2(a, b);
     }
+    (void)per;
+    __syncthreads();
+    cnt = 0;
+    for (int m = threadIdx.x; m < N && cnt < 32; m += blockDim.x, ++cnt) z[__brev(m) >> (32 - lg)] = buf[cnt];
   }
   __syncthreads();
-  for (int len = 1; len < L; len <<= 1) {
+  // 3. radix-2 DIT, sign +
+  for (int len = 1; len < N; len <<= 1) {
     const int rstep = N / len;   // e^{iπ jj/len} = e^{iπ (jj·N/len)/N}
-    for (int bf = threadIdx.x; bf < (L >> 1); bf += blockDim.x) {
+    for (int bf = threadIdx.x; bf < half; bf += blockDim.x) {
       const int grp = bf / len, jj = bf - grp * len;
       const int i0 = grp * 2 * len + jj, i1 = i0 + len;
       double c, s;
@@ -451,57 +449,35 @@ __global__ void __launch_bounds__(256) k_dst_dense(DevTables T, const double* __
     }
     __syncthreads();
   }
-  // 4. Y_k = E_k + e^{2πik/N} O_k, E = (Z_k + conj Z_{L−k})/2, O = (Z_k − conj Z_{L−k})/(2i)
-  for (int k = threadIdx.x; k < L; k += blockDim.x) {
-    const double2 a = z[k], b = z[(L - k) & (L - 1)];
-    const double er = 0.5 * (a.x + b.x), ei = 0.5 * (a.y - b.y);
-    const double orr = 0.5 * (a.y + b.y), oi = -0.5 * (a.x - b.x);
+  // 4. pairs (k, N−k) in place: F_k = Im(E_k + e^{iπk/N} O_k)/2 into z[k].x
+  for (int k = threadIdx.x; k <= half; k += blockDim.x) {
+    if (k == 0) {
+      z[0].x = 0.0;
+      continue;
+    }
+    const int k2 = N - k;
+    const double2 a = z[k], b = z[k2];
     double c, s;
-    twiddle(s_sin, 2 * k, N, c, s);
-    const double yr = er + c * orr - s * oi, yi = ei + c * oi + s * orr;
-    out[2 * k] = yi;                                // F_{2k}
-    out[2 * k + 1] = (k == 0) ? 0.5 * yr : yr;      // increments of the odd recurrence
+    // k:   ei = (a.y − b.y)/2, orr = (a.y + b.y)/2, oi = −(a.x − b.x)/2
+    twiddle(s_sin, k, N, c, s);
+    const double Fk = 0.5 * (0.5 * (a.y - b.y) + c * (-0.5 * (a.x - b.x)) + s * (0.5 * (a.y + b.y)));
+    double Fk2 = 0.0;
+    if (k2 != k) {
+      // N−k: roles of a and b swap
+      twiddle(s_sin, k2, N, c, s);
+      Fk2 = 0.5 * (0.5 * (b.y - a.y) + c * (-0.5 * (b.x - a.x)) + s * (0.5 * (b.y + a.y)));
+    }
+    z[k].x = Fk;
+    if (k2 != k) z[k2].x = Fk2;
   }
   __syncthreads();
-  // 5. inclusive scan of the odd entries (deterministic: per-thread chunks + ordered warp sums)
-  {
-    const int per = (L + blockDim.x - 1) / blockDim.x;
-    const int k0 = threadIdx.x * per, k1 = min(L, k0 + per);
-    double run = 0.0;
-    for (int k = k0; k < k1; ++k) run += out[2 * k + 1];
-    // exclusive scan of `run` across threads
-    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-    double incl = run;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      const double t = __shfl_up_sync(0xffffffffu, incl, o);
-      if (lane >= o) incl += t;
-    }
-    if (lane == 31) wsum[wid] = incl;
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      double acc = 0.0;
-      for (int w = 0; w < (int)(blockDim.x >> 5); ++w) {
-        const double t = wsum[w];
-        wsum[w] = acc;
-        acc += t;
-      }
-    }
-    __syncthreads();
-    double base = wsum[wid] + incl - run;
-    for (int k = k0; k < k1; ++k) {
-      base += out[2 * k + 1];
-      out[2 * k + 1] = base;
-    }
-  }
-  __syncthreads();
-  // 6. store
+  // 5. store
   if (MODE == 0) {
-    for (int k = threadIdx.x; k < N; k += blockDim.x) dst[(size_t)(i - 1) * N + k] = (k == 0) ? 0.0 : out[k];
+    for (int k = threadIdx.x; k < N; k += blockDim.x) dst[(size_t)(i - 1) * N + k] = (k == 0) ? 0.0 : z[k].x;
   } else {
     const double sc = 2.0 / N;
     for (int j = threadIdx.x; j <= N; j += blockDim.x)
-      dst[(size_t)i * (N + 1) + j] = (j == 0 || j == N) ? 0.0 : sc * out[j];
+      dst[(size_t)i * (N + 1) + j] = (j == 0 || j == N) ? 0.0 : sc * z[j].x;
   }
 }
 
@@ -607,7 +583,7 @@ void launch_correct(const DevTables& T, const double* phi, const double* mk, con
   { ++g_launches; k_correct<<<cdiv(T.nirr, 128), 128, 0, s>>>(T, phi, mk, fq, jq_given, cval); }
 }
 
-static size_t dense_smem(int N) { return (size_t)(N / 2 + 1 + 2 * N) * sizeof(double); }
+static size_t dense_smem(int N) { return (size_t)(N / 2 + 2 + 2 * N) * sizeof(double); }  // table + N complex
 
 void launch_dst_forward(const DevTables& T, const double* fgrid, bool mask, const BumpParams& bp, double* spec,
                         cudaStream_t s) {

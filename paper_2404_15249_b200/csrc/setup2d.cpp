@@ -172,7 +172,7 @@ void build_setup(Setup& S, const kfbi_grid* g, const kfbi_boundary* b, const kfb
   if (pde->kappa < 0) throw ArgError("kappa must be >= 0 (P:458)");
   if (pde->bc != KFBI_DIRICHLET) throw ArgError("only Dirichlet BVPs are built");
   int N = g->n[0];
-  if (g->n[1] != N || N < 64 || (N & (N - 1))) throw ArgError("n must be equal powers of two >= 64");
+  if (g->n[1] != N || N < 64 || N > 8192 || (N & (N - 1))) throw ArgError("n must be equal powers of two in [64, 8192]");
   double h0 = (g->hi[0] - g->lo[0]) / N, h1 = (g->hi[1] - g->lo[1]) / N;
   if (!(h0 > 0) || std::fabs(h0 - h1) > 1e-12 * h0 || std::fabs(g->lo[0] - g->lo[1]) > 1e-12 * h0)
     throw ArgError("grid spacing must be equal on both axes (P:559) and the box square");

@@ -1,0 +1,4 @@
+set -x
+nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm --format=csv
+timeout 300 python -c "import __graft_entry__ as g; g.smoke()" 2>&1 | tail -20
+timeout 900 python -m pytest tests/test_gpu_2d.py -q -m gpu -k "not full_size" 2>&1 | tail -30

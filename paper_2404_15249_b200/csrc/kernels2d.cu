@@ -137,29 +137,64 @@ __global__ void k_correct(DevTables T, const double* __restrict__ phi, const dou
 }
 
 // ------------------------------------------------------------------------------ A4+A5
-// Thread ↔ mode pair (k, N−k), k = t (t = 0 → mode N/2 alone), one block g of BL−1
-// columns per work item.  sin(πj(N−k)/N) = (−1)^{j+1} sin(πjk/N), so each table lookup
-// serves both modes.  Local Thomas in registers: y_p = r_p − y_{p−1}/c_{p−1}, then
-// z_p = (y_p − z_{p+1})/c_p, with r = h² f̂.  Writes z (block rows), the block end values
-// for the reduced system, and h² f̂ at the separator column.
+// Persistent CTAs, each owning a fixed chunk of 256 mode pairs (k, N−k) (k = t, t = 0 → mode
+// N/2 alone) and iterating over blocks g of BL−1 columns.  sin(πj(N−k)/N) = (−1)^{j+1}
+// sin(πjk/N): one lookup serves both modes.  The block's sparse corrections (j, c) are staged
+// in shared memory; sines come from a half-period table sin(πr/N), r ∈ [0, N), stored at
+// r + r/16 (one pad per 16 doubles breaks the stride-j bank conflicts of a warp's lanes).
+// Local Thomas in registers with the block pivots c_1 = d, c_p = d − 1/c_{p−1} computed once
+// per CTA lifetime: y_p = r_p − y_{p−1}/c_{p−1}, z_p = (y_p − z_{p+1})/c_p, r = h² f̂.
+// Outputs: z at the block rows, B[g] = z_g[1], A[g] = h² f̂_sep,g − z_g[L] (reduced-system
+// right-hand side pieces).
 template <bool DENSE>
-__global__ void __launch_bounds__(256) k_sweep(DevTables T, const double* __restrict__ cval, double* spec,
-                                               double* __restrict__ zfirst, double* __restrict__ zlast,
-                                               double* __restrict__ fsep) {
-  extern __shared__ double s_sin[];
-  const int N = T.N, half = N >> 1, P = T.P, mask = 2 * N - 1;
-  for (int r = threadIdx.x; r <= half; r += blockDim.x) s_sin[r] = T.sin_tab[r];
-  __syncthreads();
-  const int nch = (half + blockDim.x - 1) / blockDim.x;
-  const int nitems = nch * P;
+__global__ void __launch_bounds__(256, 1) k_sweep(DevTables T, const double* __restrict__ cval, double* spec,
+                                                  double* __restrict__ zB, double* __restrict__ zA) {
+  extern __shared__ double sm[];
+  const int N = T.N, half = N >> 1, P = T.P, m2 = 2 * N - 1;
+  double* tab = sm;                               // N + N/16 (+1)
+  const int tabn = N + (N >> 4) + 1;
+  double* ec1 = sm + tabn;
+  double* ec2 = ec1 + T.maxe;
+  int* ej = reinterpret_cast<int*>(ec2 + T.maxe);
+  for (int r = threadIdx.x; r < N; r += blockDim.x) tab[r + (r >> 4)] = sin_lookup(T.sin_tab, r, N);
+  const int nch = (half + 255) >> 8;
+  const int G = gridDim.x / nch;
+  const int ch = blockIdx.x % nch;
+  const int t = ch * 256 + threadIdx.x;
+  const bool active = t < half;
+  const int k1 = t == 0 ? half : (active ? t : 1);
+  const int k2 = N - k1;
+  double ic1[LB], ic2[LB];   // 1/c_p for both modes
+  {
+    const double d1 = T.dk[k1], d2 = T.dk[k2];
+    double c1 = d1, c2 = d2;
+#pragma unroll
+    for (int p = 0; p < LB; ++p) {
+      if (p) {
+        c1 = d1 - ic1[p - 1];
+        c2 = d2 - ic2[p - 1];
+      }
+      ic1[p] = 1.0 / c1;
+      ic2[p] = 1.0 / c2;
+    }
+  }
   const double h2 = T.h * T.h;
-  for (int item = blockIdx.x; item < nitems; item += gridDim.x) {
-    const int g = item / nch, ch = item - g * nch;
-    const int t = ch * blockDim.x + threadIdx.x;
-    if (t >= half) continue;
-    const int k1 = t == 0 ? half : t;
-    const int k2 = N - k1;
-    double y1[LB], y2[LB];
+  for (int g = blockIdx.x / nch; g < P; g += G) {
+    const int c0 = BL * g + 1;
+    const int e0 = T.col_ptr[c0];
+    __syncthreads();
+    if (cval) {
+      const int e1 = T.col_ptr[min(BL * g + BL, N - 1) + 1];
+      for (int e = e0 + threadIdx.x; e < e1; e += blockDim.x) {
+        const int j = T.irr_j[e];
+        const double c = cval[e];
+        ej[e - e0] = j;
+        ec1[e - e0] = c;
+        ec2[e - e0] = (j & 1) ? c : -c;
+      }
+    }
+    __syncthreads();
+    if (!active) continue;
     auto rhs = [&](int i, double& r1, double& r2) {
       r1 = 0.0;
       r2 = 0.0;
@@ -168,67 +203,69 @@ __global__ void __launch_bounds__(256) k_sweep(DevTables T, const double* __rest
         r2 = h2 * spec[(size_t)(i - 1) * N + k2];
       }
       if (cval) {
-        const int e1 = T.col_ptr[i + 1];
-        for (int e = T.col_ptr[i]; e < e1; ++e) {
-          const int j = __ldg(T.irr_j + e);
-          const double c = __ldg(cval + e);
-          const double s = sin_lookup(s_sin, (j * k1) & mask, N);
-          r1 = fma(c, s, r1);
-          r2 = fma((j & 1) ? c : -c, s, r2);
+        const int a0 = T.col_ptr[i] - e0, a1 = T.col_ptr[i + 1] - e0;
+#pragma unroll 4
+        for (int e = a0; e < a1; ++e) {
+          const int r = (ej[e] * k1) & m2;
+          const int idx = r & (N - 1);
+          double s = tab[idx + (idx >> 4)];
+          s = (r & N) ? -s : s;
+          r1 = fma(ec1[e], s, r1);
+          r2 = fma(ec2[e], s, r2);
         }
       }
     };
+    double y1[LB], y2[LB];
 #pragma unroll
     for (int p = 0; p < LB; ++p) {
       double r1, r2;
-      rhs(BL * g + 1 + p, r1, r2);
+      rhs(c0 + p, r1, r2);
       if (p == 0) {
         y1[0] = r1;
         y2[0] = r2;
       } else {
-        y1[p] = fma(-y1[p - 1], __ldg(T.invc + (size_t)(p - 1) * N + k1), r1);
-        y2[p] = fma(-y2[p - 1], __ldg(T.invc + (size_t)(p - 1) * N + k2), r2);
+        y1[p] = fma(-y1[p - 1], ic1[p - 1], r1);
+        y2[p] = fma(-y2[p - 1], ic2[p - 1], r2);
       }
     }
-    y1[LB - 1] *= __ldg(T.invc + (size_t)(LB - 1) * N + k1);
-    y2[LB - 1] *= __ldg(T.invc + (size_t)(LB - 1) * N + k2);
+    y1[LB - 1] *= ic1[LB - 1];
+    y2[LB - 1] *= ic2[LB - 1];
 #pragma unroll
     for (int p = LB - 2; p >= 0; --p) {
-      y1[p] = (y1[p] - y1[p + 1]) * __ldg(T.invc + (size_t)p * N + k1);
-      y2[p] = (y2[p] - y2[p + 1]) * __ldg(T.invc + (size_t)p * N + k2);
+      y1[p] = (y1[p] - y1[p + 1]) * ic1[p];
+      y2[p] = (y2[p] - y2[p + 1]) * ic2[p];
     }
 #pragma unroll
     for (int p = 0; p < LB; ++p) {
-      const size_t row = (size_t)(BL * g + p) * N;   // row of column i = BL g + 1 + p
+      const size_t row = (size_t)(c0 - 1 + p) * N;
       spec[row + k1] = y1[p];
       spec[row + k2] = y2[p];
     }
-    zfirst[(size_t)g * N + k1] = y1[0];
-    zfirst[(size_t)g * N + k2] = y2[0];
-    zlast[(size_t)g * N + k1] = y1[LB - 1];
-    zlast[(size_t)g * N + k2] = y2[LB - 1];
+    zB[(size_t)g * N + k1] = y1[0];
+    zB[(size_t)g * N + k2] = y2[0];
     if (g < P - 1) {
       double r1, r2;
       rhs(BL * (g + 1), r1, r2);
-      fsep[(size_t)g * N + k1] = r1;
-      fsep[(size_t)g * N + k2] = r2;
+      zA[(size_t)g * N + k1] = r1 - y1[LB - 1];
+      zA[(size_t)g * N + k2] = r2 - y2[LB - 1];
     }
   }
 }
 
 // ------------------------------------------------------------------------------ A5 reduced
 // −Z_L[L] h_{g−1} + (d − Z_R[L] − Z_L[1]) h_g − Z_R[1] h_{g+1} = f_sep,g − z_g[L] − z_{g+1}[1]
-// (SURVEY App. A.5); constant coefficients a = red_a, b = red_b per mode; Thomas.
-__global__ void k_reduced(DevTables T, const double* __restrict__ zfirst, const double* __restrict__ zlast,
-                          const double* __restrict__ fsep, double* __restrict__ hsep) {
+// (SURVEY App. A.5): tridiag(a, b, a) per mode, a = red_a, b = red_b, rhs_g = A[g] − B[g+1].
+// Small P: one thread per mode, plain Thomas.
+__global__ void k_reduced_small(DevTables T, const double* __restrict__ zB, const double* __restrict__ zA,
+                                double* __restrict__ hsep) {
   const int N = T.N, P = T.P;
   const int k = blockIdx.x * blockDim.x + threadIdx.x + 1;
   if (k >= N || P < 2) return;
   const double a = T.red_a[k];
-  double y = fsep[k] - zlast[k] - zfirst[(size_t)N + k];
+  double y = zA[k] - zB[(size_t)N + k];
   hsep[k] = y;
   for (int g = 1; g < P - 1; ++g) {
-    const double r = fsep[(size_t)g * N + k] - zlast[(size_t)g * N + k] - zfirst[(size_t)(g + 1) * N + k];
+    const double r = zA[(size_t)g * N + k] - zB[(size_t)(g + 1) * N + k];
     y = fma(-a * y, T.red_invc[(size_t)(g - 1) * N + k], r);
     hsep[(size_t)g * N + k] = y;
   }
@@ -238,6 +275,73 @@ __global__ void k_reduced(DevTables T, const double* __restrict__ zfirst, const 
     hn = (hsep[(size_t)g * N + k] - a * hn) * T.red_invc[(size_t)g * N + k];
     hsep[(size_t)g * N + k] = hn;
   }
+}
+
+// Large P: the same arrowhead split applied to the reduced system (P − 1 = BL2·S − 1):
+// thread (mode lane, segment σ) solves its BL2−1 separators locally in registers, the S−1
+// level-2 separators per mode are solved from shared memory, then each segment is fixed up
+// with the level-2 spikes (z − a h2_{σ−1} Z2_L − a h2_σ Z2_R).
+__global__ void __launch_bounds__(512) k_reduced2(DevTables T, const double* __restrict__ zB,
+                                                  const double* __restrict__ zA, double* __restrict__ hsep) {
+  __shared__ double s_first[16][32], s_last[16][32], s_rs[16][32], s_h2[16][32];
+  const int N = T.N, P = T.P, S = P / BL2;
+  const int lane = threadIdx.x, sg = threadIdx.y;
+  const int k = blockIdx.x * 32 + lane + 1;
+  const bool ok = k < N;
+  const int kk = ok ? k : 1;
+  const double a = T.red_a[kk];
+  const int gbase = sg * BL2;
+  double z[LB2];
+#pragma unroll
+  for (int p = 0; p < LB2; ++p) {
+    const int g = gbase + p;
+    const double r = zA[(size_t)g * N + kk] - zB[(size_t)(g + 1) * N + kk];
+    z[p] = p ? fma(-a * z[p - 1], T.rinv2[(size_t)(p - 1) * N + kk], r) : r;
+  }
+  z[LB2 - 1] *= T.rinv2[(size_t)(LB2 - 1) * N + kk];
+#pragma unroll
+  for (int p = LB2 - 2; p >= 0; --p) z[p] = (z[p] - a * z[p + 1]) * T.rinv2[(size_t)p * N + kk];
+  s_first[sg][lane] = z[0];
+  s_last[sg][lane] = z[LB2 - 1];
+  if (sg < S - 1) {
+    const int gs = gbase + LB2;
+    s_rs[sg][lane] = zA[(size_t)gs * N + kk] - zB[(size_t)(gs + 1) * N + kk];
+  }
+  __syncthreads();
+  if (sg == 0 && S > 1) {
+    // level-2 reduced system: tridiag(A2, B2, A2), rhs = r_s − a z_σ[L] − a z_{σ+1}[1];
+    // pivots → s_rs, forward values → s_h2 (in place, per lane)
+    const double A2 = T.red2_a[kk], B2 = T.red2_b[kk];
+    double c = B2, yprev = 0.0, ciprev = 0.0;
+    for (int q = 0; q < S - 1; ++q) {
+      const double r = s_rs[q][lane] - a * s_last[q][lane] - a * s_first[q + 1][lane];
+      if (q) c = B2 - A2 * A2 * ciprev;
+      const double ci = 1.0 / c;
+      const double y = q ? r - A2 * yprev * ciprev : r;
+      s_rs[q][lane] = ci;
+      s_h2[q][lane] = y;
+      yprev = y;
+      ciprev = ci;
+    }
+    double hn = s_h2[S - 2][lane] * s_rs[S - 2][lane];
+    s_h2[S - 2][lane] = hn;
+    for (int q = S - 3; q >= 0; --q) {
+      hn = (s_h2[q][lane] - A2 * hn) * s_rs[q][lane];
+      s_h2[q][lane] = hn;
+    }
+  }
+  __syncthreads();
+  if (!ok) return;
+  const double hl = sg > 0 ? a * s_h2[sg - 1][lane] : 0.0;
+  const double hr = sg < S - 1 ? a * s_h2[sg][lane] : 0.0;
+#pragma unroll
+  for (int p = 0; p < LB2; ++p) {
+    double x = z[p];
+    x = fma(-hl, T.z2r[(size_t)(LB2 - 1 - p) * N + k], x);   // Z2_L[p] = Z2_R[L2 − 1 − p]
+    x = fma(-hr, T.z2r[(size_t)p * N + k], x);
+    hsep[(size_t)(gbase + p) * N + k] = x;
+  }
+  if (sg < S - 1) hsep[(size_t)(gbase + LB2) * N + k] = s_h2[sg][lane];
 }
 
 // value of v̂ at column i, mode k: separator → h; block row → z − h_{g−1} Z_L − h_g Z_R
@@ -255,22 +359,22 @@ __device__ __forceinline__ double fixup(const DevTables& T, const double* __rest
 
 // ------------------------------------------------------------------------------ A6 sparse
 // One CTA per column holding stencil nodes; v_j = (2/N) Σ_k v̂_k sin(πjk/N) at those rows,
-// paired modes: Σ_t sin(πjt/N) (v̂_t ± v̂_{N−t}) + v̂_{N/2} sin(πj/2).
+// paired modes: Σ_t sin(πjt/N) (v̂_t ± v̂_{N−t}) + v̂_{N/2} sin(πj/2).  Thread `tid` owns the
+// pairs t = tid + s·B; the sines along s are generated by rotation with the per-row step
+// e^{iπjB/N} (two table lookups per row and thread instead of one per term).  Rows of a
+// column come odd-first (setup order) and are processed four at a time with one parity.
 template <int PPT>
-__global__ void __launch_bounds__(256) k_inv_sparse(DevTables T, const double* __restrict__ spec,
-                                                    const double* __restrict__ hsep, double* __restrict__ vsten) {
-  extern __shared__ double sm[];
-  const int N = T.N, half = N >> 1, mask = 2 * N - 1;
-  double* s_sin = sm;
-  double* scratch = sm + half + 1;
-  for (int r = threadIdx.x; r <= half; r += blockDim.x) s_sin[r] = T.sin_tab[r];
+__global__ void __launch_bounds__(256, 2) k_inv_sparse(DevTables T, const double* __restrict__ spec,
+                                                       const double* __restrict__ hsep, double* __restrict__ vsten) {
+  __shared__ double scratch[8 * 4];
+  const int N = T.N, half = N >> 1, m2 = 2 * N - 1, B = blockDim.x;
   const int b = blockIdx.x;
   const int i = T.ocol[b];
   double Pv[PPT], Qv[PPT];
   double xm = 0.0;
 #pragma unroll
   for (int s = 0; s < PPT; ++s) {
-    const int t = threadIdx.x + s * blockDim.x;
+    const int t = threadIdx.x + s * B;
     const int k1 = t == 0 ? half : t;
     const double x1 = fixup(T, spec, hsep, i, k1);
     const double x2 = t == 0 ? 0.0 : fixup(T, spec, hsep, i, N - k1);
@@ -283,37 +387,46 @@ __global__ void __launch_bounds__(256) k_inv_sparse(DevTables T, const double* _
       Qv[s] = x1 - x2;
     }
   }
-  __syncthreads();
   const double scale = 2.0 / N;
   const int u0 = T.ocol_ptr[b], u1 = T.ocol_ptr[b + 1];
-  for (int u = u0; u < u1; u += 4) {
+  int u = u0;
+  while (u < u1) {
+    const int par = T.sn_j[u] & 1;
+    int nr = 1;
+    while (nr < 4 && u + nr < u1 && (T.sn_j[u + nr] & 1) == par) ++nr;
     double acc[4] = {0.0, 0.0, 0.0, 0.0};
-    int js[4];
+    double cs[4], sn[4], cd[4], sd[4];
 #pragma unroll
-    for (int q = 0; q < 4; ++q) js[q] = (u + q < u1) ? T.sn_j[u + q] : 0;
+    for (int q = 0; q < 4; ++q) {
+      const int j = q < nr ? T.sn_j[u + q] : 0;
+      const int r0 = (j * (int)threadIdx.x) & m2, rd = (j * B) & m2;
+      sn[q] = sin_lookup(T.sin_tab, r0, N);
+      cs[q] = sin_lookup(T.sin_tab, (r0 + (N >> 1)) & m2, N);
+      sd[q] = sin_lookup(T.sin_tab, rd, N);
+      cd[q] = sin_lookup(T.sin_tab, (rd + (N >> 1)) & m2, N);
+    }
 #pragma unroll
     for (int s = 0; s < PPT; ++s) {
-      const int t = threadIdx.x + s * blockDim.x;
+      const double xv = par ? Pv[s] : Qv[s];
 #pragma unroll
       for (int q = 0; q < 4; ++q) {
-        const int j = js[q];
-        const double sv = sin_lookup(s_sin, (j * t) & mask, N);
-        acc[q] = fma((j & 1) ? Pv[s] : Qv[s], sv, acc[q]);
+        acc[q] = fma(xv, sn[q], acc[q]);
+        const double c2 = fma(cs[q], cd[q], -sn[q] * sd[q]);
+        sn[q] = fma(sn[q], cd[q], cs[q] * sd[q]);
+        cs[q] = c2;
       }
     }
-    if (threadIdx.x == 0) {
+    if (threadIdx.x == 0 && par) {
 #pragma unroll
       for (int q = 0; q < 4; ++q) {
-        const int j = js[q];
-        if (j & 1) acc[q] += ((j >> 1) & 1) ? -xm : xm;   // sin(πj/2)
+        const int j = q < nr ? T.sn_j[u + q] : 0;
+        acc[q] += ((j >> 1) & 1) ? -xm : xm;   // sin(πj/2), j odd
       }
     }
     block_reduce<4>(acc, scratch);
     if (threadIdx.x == 0)
-#pragma unroll
-      for (int q = 0; q < 4; ++q)
-        if (u + q < u1) vsten[u + q] = scale * acc[q];
-    __syncthreads();
+      for (int q = 0; q < nr; ++q) vsten[u + q] = scale * acc[q];
+    u += nr;
   }
 }
 
@@ -554,7 +667,6 @@ __global__ void k_scale_copy(int n, const double* __restrict__ a, const double* 
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) o[i] = a[i] / s;
 }
 
-int g_sweep_grid = 0;
 int g_num_sms = 0;
 
 int num_sms() {
@@ -606,25 +718,38 @@ void launch_inverse_dense(const DevTables& T, const double* spec, const double* 
 
 void launch_sweep(const DevTables& T, const double* cval, bool dense, double* spec, double* zfirst, double* zlast,
                   double* fsep, cudaStream_t s) {
-  const size_t sm = (size_t)(T.N / 2 + 1) * sizeof(double);
-  const int half = T.N / 2;
-  const int nitems = cdiv(half, 256) * T.P;
-  if (!g_sweep_grid) {
-    int per = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_sweep<false>, 256, sm);
-    g_sweep_grid = num_sms() * (per > 0 ? per : 1);
+  (void)zlast;
+  const size_t sm = (size_t)(T.N + T.N / 16 + 1) * sizeof(double) + (size_t)T.maxe * (2 * sizeof(double) + sizeof(int));
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(k_sweep<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    cudaFuncSetAttribute(k_sweep<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    attr = true;
   }
-  const int grid = nitems < g_sweep_grid ? nitems : g_sweep_grid;
+  const int nch = (T.N / 2 + 255) / 256;
+  int per = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_sweep<false>, 256, sm);
+  if (per < 1) per = 1;
+  int G = num_sms() * per / nch;
+  if (G < 1) G = 1;
+  if (G > T.P) G = T.P;
+  const int grid = nch * G;
   if (dense)
-    { ++g_launches; k_sweep<true><<<grid, 256, sm, s>>>(T, cval, spec, zfirst, zlast, fsep); }
+    { ++g_launches; k_sweep<true><<<grid, 256, sm, s>>>(T, cval, spec, zfirst, fsep); }
   else
-    { ++g_launches; k_sweep<false><<<grid, 256, sm, s>>>(T, cval, spec, zfirst, zlast, fsep); }
+    { ++g_launches; k_sweep<false><<<grid, 256, sm, s>>>(T, cval, spec, zfirst, fsep); }
 }
 
 void launch_reduced(const DevTables& T, const double* zfirst, const double* zlast, const double* fsep, double* hsep,
                     cudaStream_t s) {
+  (void)zlast;
   if (T.P < 2) return;
-  { ++g_launches; k_reduced<<<cdiv(T.N - 1, 64), 64, 0, s>>>(T, zfirst, zlast, fsep, hsep); }
+  if (T.P >= 2 * BL2 && T.P % BL2 == 0 && T.P / BL2 <= 16) {
+    dim3 blk(32, T.P / BL2);
+    { ++g_launches; k_reduced2<<<cdiv(T.N - 1, 32), blk, 0, s>>>(T, zfirst, fsep, hsep); }
+  } else {
+    { ++g_launches; k_reduced_small<<<cdiv(T.N - 1, 64), 64, 0, s>>>(T, zfirst, fsep, hsep); }
+  }
 }
 
 void launch_inverse_sparse(const DevTables& T, const double* spec, const double* hsep, double* vsten,
@@ -633,14 +758,12 @@ void launch_inverse_sparse(const DevTables& T, const double* spec, const double*
   const int half = T.N / 2;
   const int threads = half < 256 ? half : 256;
   const int ppt = half / threads;
-  const size_t sm = (size_t)(half + 1 + 32 * 4) * sizeof(double);
   switch (ppt) {
-    case 1: ++g_launches; k_inv_sparse<1><<<T.nocol, threads, sm, s>>>(T, spec, hsep, vsten); break;
-    case 2: ++g_launches; k_inv_sparse<2><<<T.nocol, threads, sm, s>>>(T, spec, hsep, vsten); break;
-    case 4: ++g_launches; k_inv_sparse<4><<<T.nocol, threads, sm, s>>>(T, spec, hsep, vsten); break;
-    case 8: ++g_launches; k_inv_sparse<8><<<T.nocol, threads, sm, s>>>(T, spec, hsep, vsten); break;
-    case 16: ++g_launches; k_inv_sparse<16><<<T.nocol, threads, sm, s>>>(T, spec, hsep, vsten); break;
-    case 32: ++g_launches; k_inv_sparse<32><<<T.nocol, threads, sm, s>>>(T, spec, hsep, vsten); break;
+    case 1: ++g_launches; k_inv_sparse<1><<<T.nocol, threads, 0, s>>>(T, spec, hsep, vsten); break;
+    case 2: ++g_launches; k_inv_sparse<2><<<T.nocol, threads, 0, s>>>(T, spec, hsep, vsten); break;
+    case 4: ++g_launches; k_inv_sparse<4><<<T.nocol, threads, 0, s>>>(T, spec, hsep, vsten); break;
+    case 8: ++g_launches; k_inv_sparse<8><<<T.nocol, threads, 0, s>>>(T, spec, hsep, vsten); break;
+    case 16: ++g_launches; k_inv_sparse<16><<<T.nocol, threads, 0, s>>>(T, spec, hsep, vsten); break;
     default: break;
   }
 }

@@ -17,6 +17,10 @@ namespace kfbi {
 // separator g sits at i = BL·(g+1).  With N = 2^p, N−1 = BL·P − 1 exactly.
 constexpr int BL = 16;
 constexpr int LB = BL - 1;
+// The reduced separator system (P−1 unknowns per mode) is itself split the same way:
+// level-2 blocks of BL2−1 separators around level-2 separators (nested arrowhead).
+constexpr int BL2 = 32;
+constexpr int LB2 = BL2 - 1;
 
 struct GeomError : std::runtime_error {
   using std::runtime_error::runtime_error;
@@ -75,6 +79,9 @@ struct Setup {
   std::vector<double> zr;            // LB × N: (S⁻¹ e_L)[p]
   std::vector<double> red_a, red_b;  // N: reduced-system off-diagonal / diagonal
   std::vector<double> red_invc;      // (P−1) × N
+  std::vector<double> rinv2, z2r;    // LB2 × N: level-2 block pivots / spike
+  std::vector<double> red2_a, red2_b;  // N: level-2 reduced system coefficients
+  int maxe = 1;                      // max sparse entries per sweep work item
   // holes (κ = 0 completion, reading R27)
   std::vector<int> holes;            // component ids
 };
@@ -104,6 +111,8 @@ struct DevTables {
   const double *c_delta, *sp_coef;
   // fast solver
   const double *sin_tab, *dk, *invc, *zr, *red_a, *red_b, *red_invc;
+  const double *rinv2, *z2r, *red2_a, *red2_b;
+  int maxe;
   const int8_t* side;
 };
 

@@ -400,15 +400,18 @@ void build_setup(Setup& S, const kfbi_grid* g, const kfbi_boundary* b, const kfb
   if (bad) throw GeomError("interpolation stencil leaves the grid or is singular");
   S.st_nodes_ij = nodes;
   {
+    // unique stencil nodes ordered by (column i, odd rows first, row j): the sparse inverse
+    // transform processes same-parity rows together (sin(πj(N−k)/N) = (−1)^{j+1} sin(πjk/N))
+    auto skey = [&](int64_t i, int64_t j) { return (i * 2 + (j & 1 ? 0 : 1)) * W + j; };
     std::vector<int64_t> keys((size_t)M * 6);
-    for (size_t k = 0; k < keys.size(); ++k) keys[k] = nodes[2 * k] * W + nodes[2 * k + 1];
+    for (size_t k = 0; k < keys.size(); ++k) keys[k] = skey(nodes[2 * k], nodes[2 * k + 1]);
     std::vector<int64_t> uk = keys;
     std::sort(uk.begin(), uk.end());
     uk.erase(std::unique(uk.begin(), uk.end()), uk.end());
     S.nsn = (int)uk.size();
     S.sn_i.resize(S.nsn);
     S.sn_j.resize(S.nsn);
-    for (int u = 0; u < S.nsn; ++u) { S.sn_i[u] = (int)(uk[u] / W); S.sn_j[u] = (int)(uk[u] % W); }
+    for (int u = 0; u < S.nsn; ++u) { S.sn_i[u] = (int)(uk[u] / W / 2); S.sn_j[u] = (int)(uk[u] % W); }
     S.st_node.resize(keys.size());
     for (size_t k = 0; k < keys.size(); ++k)
       S.st_node[k] = (int)(std::lower_bound(uk.begin(), uk.end(), keys[k]) - uk.begin());
@@ -484,6 +487,35 @@ void build_setup(Setup& S, const kfbi_grid* g, const kfbi_boundary* b, const kfb
       if (gg > 0) rc = be - al * al / rc;
       S.red_invc[(size_t)gg * N + k] = 1.0 / rc;
     }
+  }
+  // level-2 arrowhead tables for the reduced system tridiag(a, b, a) of size P−1 (blocks of
+  // L2 = BL2−1 separators, one level-2 separator between them)
+  S.rinv2.assign((size_t)LB2 * N, 0.0);
+  S.z2r.assign((size_t)LB2 * N, 0.0);
+  S.red2_a.assign(N, 0.0);
+  S.red2_b.assign(N, 0.0);
+  for (int k = 1; k < N; ++k) {
+    const double a = S.red_a[k], bb = S.red_b[k];
+    double c = bb, cs[LB2];
+    for (int p = 0; p < LB2; ++p) {
+      if (p > 0) c = bb - a * a / c;
+      cs[p] = c;
+      S.rinv2[(size_t)p * N + k] = 1.0 / c;
+    }
+    double x = 1.0 / cs[LB2 - 1];   // S2^{-1} e_L: z_L = 1/c_L, z_p = −a z_{p+1}/c_p
+    S.z2r[(size_t)(LB2 - 1) * N + k] = x;
+    for (int p = LB2 - 2; p >= 0; --p) {
+      x = -a * x / cs[p];
+      S.z2r[(size_t)p * N + k] = x;
+    }
+    S.red2_a[k] = -a * a * S.z2r[k];
+    S.red2_b[k] = bb - 2.0 * a * a * S.z2r[(size_t)(LB2 - 1) * N + k];
+  }
+  // largest number of sparse corrections staged by one sweep work item (block + separator)
+  S.maxe = 1;
+  for (int gg = 0; gg < P; ++gg) {
+    const int last = std::min(BL * gg + BL, N - 1);
+    S.maxe = std::max(S.maxe, S.col_ptr[last + 1] - S.col_ptr[BL * gg + 1]);
   }
   S.holes.clear();
   if (S.kappa == 0.0)

@@ -3,6 +3,7 @@
 // stream; the only host syncs are the ones Algorithm 5 needs (one per Arnoldi step).
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <chrono>
 #include <cmath>
 #include <cstring>
@@ -86,7 +87,7 @@ void layout(kfbi_ctx* c, Arena& A) {
   T.q_t = A.table(S.q_t); T.q_t1 = A.table(S.q_t1); T.q_t2 = A.table(S.q_t2);
   T.q_p1 = A.table(S.q_p1); T.q_p2 = A.table(S.q_p2);
   T.irr_j = A.table(S.irr_j); T.irr_ptr = A.table(S.irr_ptr); T.pair_q = A.table(S.pair_q);
-  T.col_ptr = A.table(S.col_ptr); T.irr_side = A.table(S.irr_side); T.pair_d = A.table(S.pair_d);
+  T.col_ptr = A.table(S.col_ptr); T.col_mid = A.table(S.col_mid); T.irr_side = A.table(S.irr_side); T.pair_d = A.table(S.pair_d);
   T.z_comp = A.table(S.z_comp); T.z_knot = A.table(S.z_knot);
   T.z_t1 = A.table(S.z_t1); T.z_t2 = A.table(S.z_t2); T.z_p1 = A.table(S.z_p1); T.z_p2 = A.table(S.z_p2);
   T.sn_j = A.table(S.sn_j); T.ocol = A.table(S.ocol); T.ocol_ptr = A.table(S.ocol_ptr);
@@ -548,7 +549,10 @@ kfbi_status kfbi_test_setup_dump(const kfbi_ctx* c, int32_t which, int64_t* out)
   if (!c || !out) return KFBI_EINVAL;
   const Setup& S = c->S;
   if (which == 0) {
-    for (int n = 0; n < S.nirr; ++n) { out[2 * n] = S.irr_i[n]; out[2 * n + 1] = S.irr_j[n]; }
+    std::vector<std::pair<int, int>> v(S.nirr);
+    for (int n = 0; n < S.nirr; ++n) v[n] = {S.irr_i[n], S.irr_j[n]};
+    std::sort(v.begin(), v.end());
+    for (int n = 0; n < S.nirr; ++n) { out[2 * n] = v[n].first; out[2 * n + 1] = v[n].second; }
   } else if (which == 1) {
     for (int q = 0; q < S.nq; ++q) { out[3 * q] = S.q_axis[q]; out[3 * q + 1] = S.q_i[q]; out[3 * q + 2] = S.q_j[q]; }
   } else if (which == 2) {

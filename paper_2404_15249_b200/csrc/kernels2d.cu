@@ -146,25 +146,28 @@ __global__ void k_correct(DevTables T, const double* __restrict__ phi, const dou
 // per CTA lifetime: y_p = r_p − y_{p−1}/c_{p−1}, z_p = (y_p − z_{p+1})/c_p, r = h² f̂.
 // Outputs: z at the block rows, B[g] = z_g[1], A[g] = h² f̂_sep,g − z_g[L] (reduced-system
 // right-hand side pieces).
+constexpr int kSweepThreads = 512;
+// staged correction: x = c, y packs j (bits 0..23), slot 2·column + parity class (bits 24..29)
+// and "last entry of its (column, class) run" (bit 30)
 template <bool DENSE>
-__global__ void __launch_bounds__(256, 1) k_sweep(DevTables T, const double* __restrict__ cval, double* spec,
-                                                  double* __restrict__ zB, double* __restrict__ zA) {
+__global__ void __launch_bounds__(kSweepThreads, 1) k_sweep(DevTables T, const double* __restrict__ cval, double* spec,
+                                                           double* __restrict__ zB, double* __restrict__ zA) {
   extern __shared__ double sm[];
-  const int N = T.N, half = N >> 1, P = T.P, m2 = 2 * N - 1;
-  double* tab = sm;                               // N + N/16 (+1)
-  const int tabn = N + (N >> 4) + 1;
-  double* ec1 = sm + tabn;
-  double* ec2 = ec1 + T.maxe;
-  int* ej = reinterpret_cast<int*>(ec2 + T.maxe);
-  for (int r = threadIdx.x; r < N; r += blockDim.x) tab[r + (r >> 4)] = sin_lookup(T.sin_tab, r, N);
-  const int nch = (half + 255) >> 8;
+  const int N = T.N, half = N >> 1, P = T.P, m2 = 2 * N - 1, B = kSweepThreads;
+  double* tab = sm;                                          // sin(πr/N), r ∈ [0, N), at r + r/16
+  const int tabn = N + (N >> 4) + 2;
+  double* R = sm + tabn;                                     // [BL columns][2 classes][B]
+  double2* ent = reinterpret_cast<double2*>(R + (size_t)BL * 2 * B);
+  for (int r = threadIdx.x; r < N; r += B) tab[r + (r >> 4)] = sin_lookup(T.sin_tab, r, N);
+  const int lgN = 31 - __clz(N);
+  const int nch = (half + B - 1) / B;
   const int G = gridDim.x / nch;
   const int ch = blockIdx.x % nch;
-  const int t = ch * 256 + threadIdx.x;
+  const int t = ch * B + threadIdx.x;
   const bool active = t < half;
   const int k1 = t == 0 ? half : (active ? t : 1);
   const int k2 = N - k1;
-  double ic1[LB], ic2[LB];   // 1/c_p for both modes
+  double ic1[LB], ic2[LB];   // 1/c_p for both modes, fixed for the CTA lifetime
   {
     const double d1 = T.dk[k1], d2 = T.dk[k2];
     double c1 = d1, c2 = d2;
@@ -179,75 +182,92 @@ __global__ void __launch_bounds__(256, 1) k_sweep(DevTables T, const double* __r
     }
   }
   const double h2 = T.h * T.h;
+  double* R1 = R + threadIdx.x;   // R1[(2c + cls) * B]: Σ over rows of class cls (0 odd, 1 even) of column c
   for (int g = blockIdx.x / nch; g < P; g += G) {
     const int c0 = BL * g + 1;
     const int e0 = T.col_ptr[c0];
+    const int ncol = g < P - 1 ? BL : LB;   // block columns + separator column
+    const int e1 = cval ? T.col_ptr[c0 + ncol] : e0;
     __syncthreads();
-    if (cval) {
-      const int e1 = T.col_ptr[min(BL * g + BL, N - 1) + 1];
-      for (int e = e0 + threadIdx.x; e < e1; e += blockDim.x) {
-        const int j = T.irr_j[e];
-        const double c = cval[e];
-        ej[e - e0] = j;
-        ec1[e - e0] = c;
-        ec2[e - e0] = (j & 1) ? c : -c;
-      }
+    for (int e = e0 + threadIdx.x; e < e1; e += B) {
+      const int j = T.irr_j[e];
+      int c = 0;
+      while (T.col_ptr[c0 + c + 1] <= e) ++c;
+      const int cls = e >= T.col_mid[c0 + c] ? 1 : 0;
+      const bool last = (e + 1 == e1) || (e + 1 == T.col_ptr[c0 + c + 1]) || (e + 1 == T.col_mid[c0 + c]);
+      const long long key = (long long)j | ((long long)(2 * c + cls) << 24) | ((long long)last << 30);
+      ent[e - e0] = make_double2(cval[e], __longlong_as_double(key));
     }
     __syncthreads();
     if (!active) continue;
-    auto rhs = [&](int i, double& r1, double& r2) {
-      r1 = 0.0;
-      r2 = 0.0;
-      if (DENSE) {
-        r1 = h2 * spec[(size_t)(i - 1) * N + k1];
-        r2 = h2 * spec[(size_t)(i - 1) * N + k2];
-      }
-      if (cval) {
-        const int a0 = T.col_ptr[i] - e0, a1 = T.col_ptr[i + 1] - e0;
+    // phase 1: h² f̂ of every column for modes k1 and N − k1: odd rows add to both modes,
+    // even rows with opposite signs (sin(πj(N−k)/N) = (−1)^{j+1} sin(πjk/N))
+#pragma unroll
+    for (int q = 0; q < 2 * BL; ++q) R1[q * B] = 0.0;
+    {
+      double acc = 0.0;
+      const int ne = e1 - e0;
 #pragma unroll 4
-        for (int e = a0; e < a1; ++e) {
-          const int r = (ej[e] * k1) & m2;
-          const int idx = r & (N - 1);
-          double s = tab[idx + (idx >> 4)];
-          s = (r & N) ? -s : s;
-          r1 = fma(ec1[e], s, r1);
-          r2 = fma(ec2[e], s, r2);
+      for (int e = 0; e < ne; ++e) {
+        const double2 en = ent[e];
+        const int key = (int)__double_as_longlong(en.y);
+        const int r = ((key & 0xFFFFFF) * k1) & m2;
+        const int idx = r & (N - 1);
+        const double v = tab[idx + (idx >> 4)];
+        // sin(π(r+N)/N) = −sin(πr/N): flip the sign bit when r ≥ N
+        acc = fma(en.x, __hiloint2double(__double2hiint(v) ^ ((r >> lgN) << 31), __double2loint(v)), acc);
+        if (key & (1 << 30)) {
+          R1[((key >> 24) & 63) * B] = acc;   // (2c + cls) = bits 24..29
+          acc = 0.0;
         }
       }
-    };
-    double y1[LB], y2[LB];
-#pragma unroll
-    for (int p = 0; p < LB; ++p) {
-      double r1, r2;
-      rhs(c0 + p, r1, r2);
-      if (p == 0) {
-        y1[0] = r1;
-        y2[0] = r2;
-      } else {
-        y1[p] = fma(-y1[p - 1], ic1[p - 1], r1);
-        y2[p] = fma(-y2[p - 1], ic2[p - 1], r2);
-      }
     }
-    y1[LB - 1] *= ic1[LB - 1];
-    y2[LB - 1] *= ic2[LB - 1];
+    // combine classes, add the dense part, then the local Thomas:
+    // y_p = r_p − y_{p−1}/c_{p−1}, z_p = (y_p − z_{p+1})/c_p   (y_p kept in R1[2p], R1[2p+1])
+    auto rhs = [&](int c, double& r1, double& r2) {
+      const double ao = R1[(2 * c) * B], ae = R1[(2 * c + 1) * B];
+      r1 = ao + ae;
+      r2 = ao - ae;
+      if (DENSE) {
+        r1 = fma(h2, spec[(size_t)(c0 + c - 1) * N + k1], r1);
+        r2 = fma(h2, spec[(size_t)(c0 + c - 1) * N + k2], r2);
+      }
+    };
+    double y1, y2;
+    rhs(0, y1, y2);
+    R1[0] = y1;
+    R1[B] = y2;
+#pragma unroll
+    for (int p = 1; p < LB; ++p) {
+      double r1, r2;
+      rhs(p, r1, r2);
+      y1 = fma(-y1, ic1[p - 1], r1);
+      y2 = fma(-y2, ic2[p - 1], r2);
+      R1[(2 * p) * B] = y1;
+      R1[(2 * p + 1) * B] = y2;
+    }
+    double sep1 = 0.0, sep2 = 0.0;
+    if (g < P - 1) rhs(LB, sep1, sep2);
+    double z1 = y1 * ic1[LB - 1], z2 = y2 * ic2[LB - 1];
+    const double zl1 = z1, zl2 = z2;
+    {
+      const size_t row = (size_t)(c0 - 1 + LB - 1) * N;
+      spec[row + k1] = z1;
+      spec[row + k2] = z2;
+    }
 #pragma unroll
     for (int p = LB - 2; p >= 0; --p) {
-      y1[p] = (y1[p] - y1[p + 1]) * ic1[p];
-      y2[p] = (y2[p] - y2[p + 1]) * ic2[p];
-    }
-#pragma unroll
-    for (int p = 0; p < LB; ++p) {
+      z1 = (R1[(2 * p) * B] - z1) * ic1[p];
+      z2 = (R1[(2 * p + 1) * B] - z2) * ic2[p];
       const size_t row = (size_t)(c0 - 1 + p) * N;
-      spec[row + k1] = y1[p];
-      spec[row + k2] = y2[p];
+      spec[row + k1] = z1;
+      spec[row + k2] = z2;
     }
-    zB[(size_t)g * N + k1] = y1[0];
-    zB[(size_t)g * N + k2] = y2[0];
+    zB[(size_t)g * N + k1] = z1;
+    zB[(size_t)g * N + k2] = z2;
     if (g < P - 1) {
-      double r1, r2;
-      rhs(BL * (g + 1), r1, r2);
-      zA[(size_t)g * N + k1] = r1 - y1[LB - 1];
-      zA[(size_t)g * N + k2] = r2 - y2[LB - 1];
+      zA[(size_t)g * N + k1] = sep1 - zl1;
+      zA[(size_t)g * N + k2] = sep2 - zl2;
     }
   }
 }
@@ -358,74 +378,174 @@ __device__ __forceinline__ double fixup(const DevTables& T, const double* __rest
 }
 
 // ------------------------------------------------------------------------------ A6 sparse
-// One CTA per column holding stencil nodes; v_j = (2/N) Σ_k v̂_k sin(πjk/N) at those rows,
-// paired modes: Σ_t sin(πjt/N) (v̂_t ± v̂_{N−t}) + v̂_{N/2} sin(πj/2).  Thread `tid` owns the
-// pairs t = tid + s·B; the sines along s are generated by rotation with the per-row step
-// e^{iπjB/N} (two table lookups per row and thread instead of one per term).  Rows of a
-// column come odd-first (setup order) and are processed four at a time with one parity.
-template <int PPT>
+// One CTA per column holding stencil nodes: v_j = (2/N) Σ_k v̂_k sin(πjk/N) at those rows.
+// Modes are taken in quads {t, N−t, N/2−t, N/2+t}, t ∈ [1, N/4), using
+//   sin(πj(N−t)/N) = (−1)^{j+1} s,  sin(πj(N/2 ± t)/N) = sin(πj/2) c ± cos(πj/2) s,
+// s, c = sin, cos(πjt/N):  odd j:  Σ_t s P_t + σ_j Σ_t c R_t,   σ_j = sin(πj/2)
+//                          even j: Σ_t s (Q_t + τ_j D_t),          τ_j = cos(πj/2)
+// with P = x_t + x_{N−t}, Q = x_t − x_{N−t}, R = x_{N/2−t} + x_{N/2+t}, D = x_{N/2+t} − x_{N/2−t}.
+// Modes N/4, N/2, 3N/4 are added by thread 0.  Thread `tid` owns t = tid + s·B; (s, c) along s
+// follow by rotation with the per-row step e^{iπjB/N}.  Rows come grouped by class (odd,
+// j ≡ 0, j ≡ 2 mod 4; setup order) and are processed up to four at a time.
+// Sum v[0..7] over the 32 lanes of a warp by a transpose-reduce (16 doubles exchanged instead
+// of 80): on return lane l holds the warp total of value (l & 7).
+__device__ __forceinline__ double warp_transpose_reduce8(double (&v)[8]) {
+  const int lane = threadIdx.x & 31;
+  // level 16: keep 4 of 8
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    const bool up = lane & 16;
+    const double send = up ? v[q] : v[q + 4];
+    const double keep = up ? v[q + 4] : v[q];
+    v[q] = keep + __shfl_xor_sync(0xffffffffu, send, 16);
+  }
+  // level 8: keep 2 of 4
+#pragma unroll
+  for (int q = 0; q < 2; ++q) {
+    const bool up = lane & 8;
+    const double send = up ? v[q] : v[q + 2];
+    const double keep = up ? v[q + 2] : v[q];
+    v[q] = keep + __shfl_xor_sync(0xffffffffu, send, 8);
+  }
+  {
+    const bool up = lane & 4;
+    const double send = up ? v[0] : v[1];
+    const double keep = up ? v[1] : v[0];
+    v[0] = keep + __shfl_xor_sync(0xffffffffu, send, 4);
+  }
+  v[0] += __shfl_xor_sync(0xffffffffu, v[0], 2);
+  v[0] += __shfl_xor_sync(0xffffffffu, v[0], 1);
+  // lane l now holds value index ((l>>4)&1)*4 + ((l>>3)&1)*2 + ((l>>2)&1)
+  return v[0];
+}
+
+template <int QPT>
 __global__ void __launch_bounds__(256, 2) k_inv_sparse(DevTables T, const double* __restrict__ spec,
                                                        const double* __restrict__ hsep, double* __restrict__ vsten) {
-  __shared__ double scratch[8 * 4];
-  const int N = T.N, half = N >> 1, m2 = 2 * N - 1, B = blockDim.x;
+  extern __shared__ double smx[];
+  __shared__ double red[8][8];
+  __shared__ int s_rows[kMaxColRows];
+  const int N = T.N, half = N >> 1, quarter = N >> 2, m2 = 2 * N - 1, B = blockDim.x, P = T.P;
+  double* tab = smx;   // sin(πr/N), r ∈ [0, N), at r + r/16
+  for (int r = threadIdx.x; r < N; r += B) tab[r + (r >> 4)] = sin_lookup(T.sin_tab, r, N);
+  auto sinr = [&](int r) {   // sin(πr/N), r ∈ [0, 2N)
+    const int idx = r & (N - 1);
+    const double v = tab[idx + (idx >> 4)];
+    return (r & N) ? -v : v;
+  };
   const int b = blockIdx.x;
   const int i = T.ocol[b];
-  double Pv[PPT], Qv[PPT];
-  double xm = 0.0;
+  const int u0 = T.ocol_ptr[b], u1 = T.ocol_ptr[b + 1];
+  for (int u = u0 + threadIdx.x; u < u1; u += B) s_rows[u - u0] = T.sn_j[u];
+  // column i: separator → x = h; block row → x = z − h_{g−1} Z_L[p] − h_g Z_R[p]
+  const int q = i / BL, rr = i - q * BL;
+  const bool sep = rr == 0;
+  const double* xrow = sep ? hsep + (size_t)(q - 1) * N : spec + (size_t)(i - 1) * N;
+  const double* hl = (!sep && q > 0) ? hsep + (size_t)(q - 1) * N : nullptr;
+  const double* hr = (!sep && q < P - 1) ? hsep + (size_t)q * N : nullptr;
+  const double* zl = T.zr + (size_t)(sep ? 0 : LB - rr) * N;     // Z_L[p] = Z_R[LB−1−p], p = rr − 1
+  const double* zrr = T.zr + (size_t)(sep ? 0 : rr - 1) * N;
+  auto X = [&](int k) {
+    double x = xrow[k];
+    if (hl) x = fma(-hl[k], __ldg(zl + k), x);
+    if (hr) x = fma(-hr[k], __ldg(zrr + k), x);
+    return x;
+  };
+  double Pv[QPT], Qp[QPT], Qm[QPT], Rv[QPT];
 #pragma unroll
-  for (int s = 0; s < PPT; ++s) {
+  for (int s = 0; s < QPT; ++s) {
     const int t = threadIdx.x + s * B;
-    const int k1 = t == 0 ? half : t;
-    const double x1 = fixup(T, spec, hsep, i, k1);
-    const double x2 = t == 0 ? 0.0 : fixup(T, spec, hsep, i, N - k1);
-    if (t == 0) {
-      xm = x1;
-      Pv[s] = 0.0;
-      Qv[s] = 0.0;
+    if (t == 0 || t >= quarter) {
+      Pv[s] = Qp[s] = Qm[s] = Rv[s] = 0.0;
     } else {
-      Pv[s] = x1 + x2;
-      Qv[s] = x1 - x2;
+      const double a = X(t), bb = X(N - t), c = X(half - t), d = X(half + t);
+      Pv[s] = a + bb;
+      Rv[s] = c + d;
+      Qp[s] = (a - bb) + (d - c);
+      Qm[s] = (a - bb) - (d - c);
     }
   }
+  double xq1 = 0.0, xq2 = 0.0, xq3 = 0.0;   // modes N/4, N/2, 3N/4
+  if (threadIdx.x == 0) {
+    xq1 = X(quarter);
+    xq2 = X(half);
+    xq3 = X(half + quarter);
+  }
+  __syncthreads();
   const double scale = 2.0 / N;
-  const int u0 = T.ocol_ptr[b], u1 = T.ocol_ptr[b + 1];
-  int u = u0;
-  while (u < u1) {
-    const int par = T.sn_j[u] & 1;
+  const int nrows = u1 - u0;
+  auto cls = [](int j) { return (j & 1) ? 0 : ((j & 3) == 0 ? 1 : 2); };
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = B >> 5;
+  int u = 0;
+  while (u < nrows) {
+    const int c0 = cls(s_rows[u]);
     int nr = 1;
-    while (nr < 4 && u + nr < u1 && (T.sn_j[u + nr] & 1) == par) ++nr;
-    double acc[4] = {0.0, 0.0, 0.0, 0.0};
-    double cs[4], sn[4], cd[4], sd[4];
+    while (nr < 4 && u + nr < nrows && cls(s_rows[u + nr]) == c0) ++nr;
+    double accs[4] = {0.0, 0.0, 0.0, 0.0}, accc[4] = {0.0, 0.0, 0.0, 0.0};
+    double sn[4], cs[4], sd[4], cd[4];
+    int js[4];
 #pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      const int j = q < nr ? T.sn_j[u + q] : 0;
-      const int r0 = (j * (int)threadIdx.x) & m2, rd = (j * B) & m2;
-      sn[q] = sin_lookup(T.sin_tab, r0, N);
-      cs[q] = sin_lookup(T.sin_tab, (r0 + (N >> 1)) & m2, N);
-      sd[q] = sin_lookup(T.sin_tab, rd, N);
-      cd[q] = sin_lookup(T.sin_tab, (rd + (N >> 1)) & m2, N);
+    for (int k = 0; k < 4; ++k) {
+      js[k] = k < nr ? s_rows[u + k] : 0;
+      const int r0 = (js[k] * (int)threadIdx.x) & m2, rd = (js[k] * B) & m2;
+      sn[k] = sinr(r0);
+      cs[k] = sinr((r0 + half) & m2);
+      sd[k] = sinr(rd);
+      cd[k] = sinr((rd + half) & m2);
     }
+    if (c0 == 0) {
 #pragma unroll
-    for (int s = 0; s < PPT; ++s) {
-      const double xv = par ? Pv[s] : Qv[s];
+      for (int s = 0; s < QPT; ++s) {
 #pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        acc[q] = fma(xv, sn[q], acc[q]);
-        const double c2 = fma(cs[q], cd[q], -sn[q] * sd[q]);
-        sn[q] = fma(sn[q], cd[q], cs[q] * sd[q]);
-        cs[q] = c2;
+        for (int k = 0; k < 4; ++k) {
+          accs[k] = fma(Pv[s], sn[k], accs[k]);
+          accc[k] = fma(Rv[s], cs[k], accc[k]);
+          const double c2 = fma(cs[k], cd[k], -sn[k] * sd[k]);
+          sn[k] = fma(sn[k], cd[k], cs[k] * sd[k]);
+          cs[k] = c2;
+        }
+      }
+    } else {
+#pragma unroll
+      for (int s = 0; s < QPT; ++s) {
+        const double xv = c0 == 1 ? Qp[s] : Qm[s];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          accs[k] = fma(xv, sn[k], accs[k]);
+          const double c2 = fma(cs[k], cd[k], -sn[k] * sd[k]);
+          sn[k] = fma(sn[k], cd[k], cs[k] * sd[k]);
+          cs[k] = c2;
+        }
       }
     }
-    if (threadIdx.x == 0 && par) {
+    double acc[8];
 #pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        const int j = q < nr ? T.sn_j[u + q] : 0;
-        acc[q] += ((j >> 1) & 1) ? -xm : xm;   // sin(πj/2), j odd
+    for (int k = 0; k < 4; ++k) {
+      acc[k] = accs[k];
+      acc[4 + k] = accc[k];
+    }
+    if (threadIdx.x == 0) {
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const int j = js[k];
+        acc[k] += xq1 * sinr((j * quarter) & m2) + xq2 * sinr((j * half) & m2) +
+                  xq3 * sinr((j * (half + quarter)) & m2);
       }
     }
-    block_reduce<4>(acc, scratch);
-    if (threadIdx.x == 0)
-      for (int q = 0; q < nr; ++q) vsten[u + q] = scale * acc[q];
+    const double ws = warp_transpose_reduce8(acc);
+    if ((lane & 3) == 0) red[wid][((lane >> 4) & 1) * 4 + ((lane >> 3) & 1) * 2 + ((lane >> 2) & 1)] = ws;
+    __syncthreads();
+    if (threadIdx.x < nr) {
+      double s1 = 0.0, s2 = 0.0;
+      for (int w = 0; w < nw; ++w) {
+        s1 += red[w][threadIdx.x];
+        s2 += red[w][4 + threadIdx.x];
+      }
+      const int j = js[threadIdx.x];
+      const double sig = ((j >> 1) & 1) ? -1.0 : 1.0;   // σ_j = sin(πj/2) for odd j
+      vsten[u0 + u + threadIdx.x] = scale * (c0 == 0 ? s1 + sig * s2 : s1);
+    }
+    __syncthreads();
     u += nr;
   }
 }
@@ -719,25 +839,26 @@ void launch_inverse_dense(const DevTables& T, const double* spec, const double* 
 void launch_sweep(const DevTables& T, const double* cval, bool dense, double* spec, double* zfirst, double* zlast,
                   double* fsep, cudaStream_t s) {
   (void)zlast;
-  const size_t sm = (size_t)(T.N + T.N / 16 + 1) * sizeof(double) + (size_t)T.maxe * (2 * sizeof(double) + sizeof(int));
+  const size_t sm = (size_t)(T.N + T.N / 16 + 2) * sizeof(double) + (size_t)BL * 2 * kSweepThreads * sizeof(double) +
+                    (size_t)T.maxe * sizeof(double2);
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(k_sweep<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-    cudaFuncSetAttribute(k_sweep<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    cudaFuncSetAttribute(k_sweep<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+    cudaFuncSetAttribute(k_sweep<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
     attr = true;
   }
-  const int nch = (T.N / 2 + 255) / 256;
+  const int nch = (T.N / 2 + kSweepThreads - 1) / kSweepThreads;
   int per = 0;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_sweep<false>, 256, sm);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_sweep<false>, kSweepThreads, sm);
   if (per < 1) per = 1;
   int G = num_sms() * per / nch;
   if (G < 1) G = 1;
   if (G > T.P) G = T.P;
   const int grid = nch * G;
   if (dense)
-    { ++g_launches; k_sweep<true><<<grid, 256, sm, s>>>(T, cval, spec, zfirst, fsep); }
+    { ++g_launches; k_sweep<true><<<grid, kSweepThreads, sm, s>>>(T, cval, spec, zfirst, fsep); }
   else
-    { ++g_launches; k_sweep<false><<<grid, 256, sm, s>>>(T, cval, spec, zfirst, fsep); }
+    { ++g_launches; k_sweep<false><<<grid, kSweepThreads, sm, s>>>(T, cval, spec, zfirst, fsep); }
 }
 
 void launch_reduced(const DevTables& T, const double* zfirst, const double* zlast, const double* fsep, double* hsep,
@@ -755,15 +876,23 @@ void launch_reduced(const DevTables& T, const double* zfirst, const double* zlas
 void launch_inverse_sparse(const DevTables& T, const double* spec, const double* hsep, double* vsten,
                            cudaStream_t s) {
   if (T.nocol == 0) return;
-  const int half = T.N / 2;
-  const int threads = half < 256 ? half : 256;
-  const int ppt = half / threads;
-  switch (ppt) {
-    case 1: ++g_launches; k_inv_sparse<1><<<T.nocol, threads, 0, s>>>(T, spec, hsep, vsten); break;
-    case 2: ++g_launches; k_inv_sparse<2><<<T.nocol, threads, 0, s>>>(T, spec, hsep, vsten); break;
-    case 4: ++g_launches; k_inv_sparse<4><<<T.nocol, threads, 0, s>>>(T, spec, hsep, vsten); break;
-    case 8: ++g_launches; k_inv_sparse<8><<<T.nocol, threads, 0, s>>>(T, spec, hsep, vsten); break;
-    case 16: ++g_launches; k_inv_sparse<16><<<T.nocol, threads, 0, s>>>(T, spec, hsep, vsten); break;
+  const int quarter = T.N / 4;
+  const int threads = quarter < 32 ? 32 : (quarter < 256 ? quarter : 256);
+  const int qpt = (quarter + threads - 1) / threads;
+  const size_t sm = (size_t)(T.N + T.N / 16 + 1) * sizeof(double);
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(k_inv_sparse<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 100 * 1024);
+    cudaFuncSetAttribute(k_inv_sparse<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 100 * 1024);
+    cudaFuncSetAttribute(k_inv_sparse<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, 100 * 1024);
+    cudaFuncSetAttribute(k_inv_sparse<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, 100 * 1024);
+    attr = true;
+  }
+  switch (qpt) {
+    case 1: ++g_launches; k_inv_sparse<1><<<T.nocol, threads, sm, s>>>(T, spec, hsep, vsten); break;
+    case 2: ++g_launches; k_inv_sparse<2><<<T.nocol, threads, sm, s>>>(T, spec, hsep, vsten); break;
+    case 4: ++g_launches; k_inv_sparse<4><<<T.nocol, threads, sm, s>>>(T, spec, hsep, vsten); break;
+    case 8: ++g_launches; k_inv_sparse<8><<<T.nocol, threads, sm, s>>>(T, spec, hsep, vsten); break;
     default: break;
   }
 }

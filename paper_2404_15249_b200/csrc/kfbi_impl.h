@@ -21,6 +21,8 @@ constexpr int LB = BL - 1;
 // level-2 blocks of BL2−1 separators around level-2 separators (nested arrowhead).
 constexpr int BL2 = 32;
 constexpr int LB2 = BL2 - 1;
+// most stencil rows one column may hold (checked by setup)
+constexpr int kMaxColRows = 512;
 
 struct GeomError : std::runtime_error {
   using std::runtime_error::runtime_error;
@@ -57,6 +59,7 @@ struct Setup {
   std::vector<int8_t> irr_side;
   std::vector<double> pair_d;        // x_a(p̄) − ξ for the (node, intersection) pair
   std::vector<int32_t> col_ptr;      // N+1 entries: irregular nodes of column i in [col_ptr[i], col_ptr[i+1])
+  std::vector<int32_t> col_mid;      // first even-row irregular node of column i (odd rows come first)
   // control points
   int M = 0;
   std::vector<int32_t> z_comp, z_knot;
@@ -96,7 +99,7 @@ struct DevTables {
   const int32_t *q_axis, *q_comp, *q_knot;
   const double *q_t, *q_t1, *q_t2, *q_p1, *q_p2;
   // irregular nodes
-  const int32_t *irr_j, *irr_ptr, *pair_q, *col_ptr;
+  const int32_t *irr_j, *irr_ptr, *pair_q, *col_ptr, *col_mid;
   const int8_t* irr_side;
   const double* pair_d;
   // control points

@@ -311,8 +311,13 @@ void build_setup(Setup& S, const kfbi_grid* g, const kfbi_boundary* b, const kfb
   for (int e = 0; e < nq; ++e) qidx[key(S.q_axis[e], S.q_i[e], S.q_j[e])] = e;
   S.irr_i.clear(); S.irr_j.clear(); S.irr_side.clear(); S.irr_ptr.assign(1, 0); S.pair_q.clear(); S.pair_d.clear();
   S.col_ptr.assign(N + 1, 0);
+  S.col_mid.assign(N + 1, 0);
+  // order: column i, odd rows j first, then even rows (the sweep accumulates the two parity
+  // classes separately: sin(πj(N−k)/N) = (−1)^{j+1} sin(πjk/N))
   for (int i = 1; i < N; ++i) {
-    for (int j = 1; j < N; ++j) {
+    for (int jj = 0; jj < N - 1; ++jj) {
+      const int half_rows = N / 2;                   // odd rows 1,3,..,N−1 then even rows 2,..,N−2
+      const int j = jj < half_rows ? 2 * jj + 1 : 2 * (jj - half_rows) + 2;
       int s0 = side(i, j);
       bool irr = side(i - 1, j) != s0 || side(i + 1, j) != s0 || side(i, j - 1) != s0 || side(i, j + 1) != s0;
       if (!irr) continue;
@@ -341,6 +346,12 @@ void build_setup(Setup& S, const kfbi_grid* g, const kfbi_boundary* b, const kfb
     for (int r : S.irr_i) cnt[r]++;
     S.col_ptr.assign(N + 1, 0);
     for (int i = 0; i < N; ++i) S.col_ptr[i + 1] = S.col_ptr[i] + cnt[i];
+    // col_mid[i]: first even-row entry of column i (== col_ptr[i+1] if none)
+    for (int i = 0; i < N; ++i) {
+      int m = S.col_ptr[i];
+      while (m < S.col_ptr[i + 1] && (S.irr_j[m] & 1)) ++m;
+      S.col_mid[i] = m;
+    }
     // col_ptr[i] .. col_ptr[i+1] are the irregular nodes of column i (sorted order)
   }
 
@@ -402,7 +413,8 @@ void build_setup(Setup& S, const kfbi_grid* g, const kfbi_boundary* b, const kfb
   {
     // unique stencil nodes ordered by (column i, odd rows first, row j): the sparse inverse
     // transform processes same-parity rows together (sin(πj(N−k)/N) = (−1)^{j+1} sin(πjk/N))
-    auto skey = [&](int64_t i, int64_t j) { return (i * 2 + (j & 1 ? 0 : 1)) * W + j; };
+    // class: 0 odd rows, 1 rows ≡ 0 (mod 4), 2 rows ≡ 2 (mod 4) — see k_inv_sparse
+    auto skey = [&](int64_t i, int64_t j) { return (i * 3 + ((j & 1) ? 0 : ((j & 3) == 0 ? 1 : 2))) * W + j; };
     std::vector<int64_t> keys((size_t)M * 6);
     for (size_t k = 0; k < keys.size(); ++k) keys[k] = skey(nodes[2 * k], nodes[2 * k + 1]);
     std::vector<int64_t> uk = keys;
@@ -411,7 +423,7 @@ void build_setup(Setup& S, const kfbi_grid* g, const kfbi_boundary* b, const kfb
     S.nsn = (int)uk.size();
     S.sn_i.resize(S.nsn);
     S.sn_j.resize(S.nsn);
-    for (int u = 0; u < S.nsn; ++u) { S.sn_i[u] = (int)(uk[u] / W / 2); S.sn_j[u] = (int)(uk[u] % W); }
+    for (int u = 0; u < S.nsn; ++u) { S.sn_i[u] = (int)(uk[u] / W / 3); S.sn_j[u] = (int)(uk[u] % W); }
     S.st_node.resize(keys.size());
     for (size_t k = 0; k < keys.size(); ++k)
       S.st_node[k] = (int)(std::lower_bound(uk.begin(), uk.end(), keys[k]) - uk.begin());
@@ -424,6 +436,8 @@ void build_setup(Setup& S, const kfbi_grid* g, const kfbi_boundary* b, const kfb
       }
     }
     S.ocol_ptr.push_back(S.nsn);
+    for (size_t c = 0; c + 1 < S.ocol_ptr.size(); ++c)
+      if (S.ocol_ptr[c + 1] - S.ocol_ptr[c] > kMaxColRows) throw GeomError("too many stencil rows in one grid column");
   }
 
   // ---- spline filters (reading R10) ----

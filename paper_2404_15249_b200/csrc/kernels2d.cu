@@ -614,15 +614,134 @@ __device__ __forceinline__ void twiddle(const double* tab, int r, int N, double&
   c = sin_lookup(tab, (r + (N >> 1)) & m2, N);
 }
 
+// e^{+2πi m/16}
+__device__ __forceinline__ double w16c(int m) {
+  switch (m & 15) {
+    case 0: return 1.0;
+    case 1: return 0.92387953251128675613;
+    case 2: return 0.70710678118654752440;
+    case 3: return 0.38268343236508977173;
+    case 4: return 0.0;
+    case 5: return -0.38268343236508977173;
+    case 6: return -0.70710678118654752440;
+    case 7: return -0.92387953251128675613;
+    case 8: return -1.0;
+    case 9: return -0.92387953251128675613;
+    case 10: return -0.70710678118654752440;
+    case 11: return -0.38268343236508977173;
+    case 12: return 0.0;
+    case 13: return 0.38268343236508977173;
+    case 14: return 0.70710678118654752440;
+    default: return 0.92387953251128675613;
+  }
+}
+__device__ __forceinline__ double w16s(int m) { return w16c(m - 4); }
+
+// R-point DFT in registers, sign +:  V_q = Σ_r v_r e^{+2πi rq/R}  (radix-2 DIT, constant twiddles)
+template <int R>
+__device__ __forceinline__ void dft_reg(double2* v) {
+  constexpr int LG = R == 2 ? 1 : R == 4 ? 2 : R == 8 ? 3 : 4;
+#pragma unroll
+  for (int i = 0; i < R; ++i) {
+    int r = 0;
+#pragma unroll
+    for (int b = 0; b < LG; ++b) r |= ((i >> b) & 1) << (LG - 1 - b);
+    if (r > i) {
+      const double2 t = v[i];
+      v[i] = v[r];
+      v[r] = t;
+    }
+  }
+#pragma unroll
+  for (int len = 1; len < R; len <<= 1)
+#pragma unroll
+    for (int i = 0; i < R; i += 2 * len)
+#pragma unroll
+      for (int jj = 0; jj < len; ++jj) {
+        const int m = jj * (8 / len);   // e^{iπ jj/len} = W16^{8 jj/len}; m ∈ [0, 8)
+        const double2 u = v[i + jj], t = v[i + jj + len];
+        double tr, ti;
+        if (m == 0) {            // trivial twiddles folded at compile time
+          tr = t.x;
+          ti = t.y;
+        } else if (m == 4) {     // ·i
+          tr = -t.y;
+          ti = t.x;
+        } else if (m == 2) {     // ·(1+i)/√2
+          tr = 0.70710678118654752440 * (t.x - t.y);
+          ti = 0.70710678118654752440 * (t.x + t.y);
+        } else if (m == 6) {     // ·(−1+i)/√2
+          tr = -0.70710678118654752440 * (t.x + t.y);
+          ti = 0.70710678118654752440 * (t.x - t.y);
+        } else {
+          const double c = w16c(m), sn = w16s(m);
+          tr = c * t.x - sn * t.y;
+          ti = c * t.y + sn * t.x;
+        }
+        v[i + jj] = make_double2(u.x + tr, u.y + ti);
+        v[i + jj + len] = make_double2(u.x - tr, u.y - ti);
+      }
+}
+
+// complex slot i of the FFT buffer lives at i + i/16 (breaks the stride-R conflicts of the
+// first Stockham pass's writes)
+__device__ __forceinline__ int zpad(int i) { return i + (i >> 4); }
+
+// One Stockham radix-R pass over z[0..N) in shared memory (natural order in and out):
+// item j: v_r = z[j + r N/R] · e^{+2πi r k/(Ns R)}, k = j mod Ns; DFT_R; z[(j/Ns) Ns R + k + q Ns] = V_q.
+// Each thread holds 16 complex values (16/R items); in place with a barrier between reads and writes.
+template <int R>
+__device__ __forceinline__ void stockham_pass(double2* z, const double* tab, int N, int Ns, int nthreads) {
+  constexpr int IT = 16 / R;
+  double2 v[16];
+  const int nitems = N / R;
+#pragma unroll
+  for (int it = 0; it < IT; ++it) {
+    const int j = threadIdx.x + it * nthreads;
+    if (j < nitems && (int)threadIdx.x < nthreads) {
+      const int k = j & (Ns - 1);
+#pragma unroll
+      for (int r = 0; r < R; ++r) v[it * R + r] = z[zpad(j + r * nitems)];
+      if (Ns > 1) {
+        // w = e^{2πi k/(Ns R)} = e^{iπ (2 k N/(Ns R))/N}
+        double c, sn;
+        twiddle(tab, 2 * k * (N / (Ns * R)), N, c, sn);
+        double wc = c, ws = sn;
+#pragma unroll
+        for (int r = 1; r < R; ++r) {
+          const double2 a = v[it * R + r];
+          v[it * R + r] = make_double2(a.x * wc - a.y * ws, a.x * ws + a.y * wc);
+          const double nc = wc * c - ws * sn;
+          ws = wc * sn + ws * c;
+          wc = nc;
+        }
+      }
+      dft_reg<R>(v + it * R);
+    }
+  }
+  __syncthreads();
+#pragma unroll
+  for (int it = 0; it < IT; ++it) {
+    const int j = threadIdx.x + it * nthreads;
+    if (j < nitems && (int)threadIdx.x < nthreads) {
+      const int k = j & (Ns - 1);
+      const int base = (j / Ns) * Ns * R + k;
+#pragma unroll
+      for (int q = 0; q < R; ++q) z[zpad(base + q * Ns)] = v[it * R + q];
+    }
+  }
+  __syncthreads();
+}
+
 template <int MODE>
-__global__ void __launch_bounds__(256) k_dst_dense(DevTables T, const double* __restrict__ src, int mask_omega,
+__global__ void __launch_bounds__(512) k_dst_dense(DevTables T, const double* __restrict__ src, int mask_omega,
                                                    BumpParams bp, const double* __restrict__ hsep,
                                                    double* __restrict__ dst) {
   extern __shared__ double sm[];
   const int N = T.N, half = N >> 1;
   double* s_sin = sm;                                          // half + 1 (padded to even)
-  double2* z = reinterpret_cast<double2*>(sm + half + 2);      // N complex
-  double* f = reinterpret_cast<double*>(z);                    // f_j staged in the upper half
+  double2* z = reinterpret_cast<double2*>(sm + half + 2);      // N (+N/16 pad) complex
+  double* f = reinterpret_cast<double*>(z) + N / 8 - N;        // f_j at f[N + j]: upper N doubles of z
   for (int r = threadIdx.x; r <= half; r += blockDim.x) s_sin[r] = T.sin_tab[r];
   const int i = blockIdx.x + 1;
   // 1. load f_j (j = 0..N−1, f_0 = 0) into the upper half of the z buffer (doubles N..2N−1)
@@ -647,40 +766,39 @@ __global__ void __launch_bounds__(256) k_dst_dense(DevTables T, const double* __
     f[N + j] = v;
   }
   __syncthreads();
-  // 2. z_m = x̃_{2m} + i x̃_{2m+1}, written in bit-reversed order for the DIT FFT
-  int lg = 0;
-  while ((1 << lg) < N) ++lg;
+  // 2. z_m = x̃_{2m} + i x̃_{2m+1} (natural order); read all first (z aliases f), then write
   {
-    // read all needed f first (the upper half of z aliases f), then write after a barrier
-    const int per = (N + blockDim.x - 1) / blockDim.x;
-    double2 buf[32];
-    int cnt = 0;
-    for (int m = threadIdx.x; m < N && cnt < 32; m += blockDim.x, ++cnt) {
-      const int j0 = 2 * m, j1 = 2 * m + 1;
-      const double a = j0 < N ? f[N + j0] : (j0 == N ? 0.0 : -f[N + 2 * N - j0]);
-      const double b = j1 < N ? f[N + j1] : -f[N + 2 * N - j1];
-      buf[cnt] = make_double2(a, b);
+    double2 buf[16];
+#pragma unroll
+    for (int it = 0; it < 16; ++it) {
+      const int m = threadIdx.x + it * blockDim.x;
+      if (m < N) {
+        const int j0 = 2 * m, j1 = 2 * m + 1;
+        const double a = j0 < N ? f[N + j0] : (j0 == N ? 0.0 : -f[N + 2 * N - j0]);
+        const double b = j1 < N ? f[N + j1] : -f[N + 2 * N - j1];
+        buf[it] = make_double2(a, b);
+      }
     }
-    (void)per;
     __syncthreads();
-    cnt = 0;
-    for (int m = threadIdx.x; m < N && cnt < 32; m += blockDim.x, ++cnt) z[__brev(m) >> (32 - lg)] = buf[cnt];
+#pragma unroll
+    for (int it = 0; it < 16; ++it) {
+      const int m = threadIdx.x + it * blockDim.x;
+      if (m < N) z[zpad(m)] = buf[it];
+    }
   }
   __syncthreads();
-  // 3. radix-2 DIT, sign +
-  for (int len = 1; len < N; len <<= 1) {
-    const int rstep = N / len;   // e^{iπ jj/len} = e^{iπ (jj·N/len)/N}
-    for (int bf = threadIdx.x; bf < half; bf += blockDim.x) {
-      const int grp = bf / len, jj = bf - grp * len;
-      const int i0 = grp * 2 * len + jj, i1 = i0 + len;
-      double c, s;
-      twiddle(s_sin, jj * rstep, N, c, s);
-      const double2 u = z[i0], v = z[i1];
-      const double tr = c * v.x - s * v.y, ti = c * v.y + s * v.x;
-      z[i0] = make_double2(u.x + tr, u.y + ti);
-      z[i1] = make_double2(u.x - tr, u.y - ti);
+  // 3. Stockham FFT (sign +): radix-16 passes, then one radix 2/4/8 pass for the rest
+  {
+    const int nth = N / 16;
+    int Ns = 1;
+    while (Ns * 16 <= N) {
+      stockham_pass<16>(z, s_sin, N, Ns, nth);
+      Ns *= 16;
     }
-    __syncthreads();
+    const int rem = N / Ns;
+    if (rem == 2) stockham_pass<2>(z, s_sin, N, Ns, nth);
+    else if (rem == 4) stockham_pass<4>(z, s_sin, N, Ns, nth);
+    else if (rem == 8) stockham_pass<8>(z, s_sin, N, Ns, nth);
   }
   // 4. pairs (k, N−k) in place: F_k = Im(E_k + e^{iπk/N} O_k)/2 into z[k].x
   for (int k = threadIdx.x; k <= half; k += blockDim.x) {
@@ -689,28 +807,26 @@ __global__ void __launch_bounds__(256) k_dst_dense(DevTables T, const double* __
       continue;
     }
     const int k2 = N - k;
-    const double2 a = z[k], b = z[k2];
+    const double2 a = z[zpad(k)], b = z[zpad(k2)];
     double c, s;
-    // k:   ei = (a.y − b.y)/2, orr = (a.y + b.y)/2, oi = −(a.x − b.x)/2
     twiddle(s_sin, k, N, c, s);
     const double Fk = 0.5 * (0.5 * (a.y - b.y) + c * (-0.5 * (a.x - b.x)) + s * (0.5 * (a.y + b.y)));
     double Fk2 = 0.0;
     if (k2 != k) {
-      // N−k: roles of a and b swap
       twiddle(s_sin, k2, N, c, s);
       Fk2 = 0.5 * (0.5 * (b.y - a.y) + c * (-0.5 * (b.x - a.x)) + s * (0.5 * (b.y + a.y)));
     }
-    z[k].x = Fk;
-    if (k2 != k) z[k2].x = Fk2;
+    z[zpad(k)].x = Fk;
+    if (k2 != k) z[zpad(k2)].x = Fk2;
   }
   __syncthreads();
   // 5. store
   if (MODE == 0) {
-    for (int k = threadIdx.x; k < N; k += blockDim.x) dst[(size_t)(i - 1) * N + k] = (k == 0) ? 0.0 : z[k].x;
+    for (int k = threadIdx.x; k < N; k += blockDim.x) dst[(size_t)(i - 1) * N + k] = (k == 0) ? 0.0 : z[zpad(k)].x;
   } else {
     const double sc = 2.0 / N;
     for (int j = threadIdx.x; j <= N; j += blockDim.x)
-      dst[(size_t)i * (N + 1) + j] = (j == 0 || j == N) ? 0.0 : sc * z[j].x;
+      dst[(size_t)i * (N + 1) + j] = (j == 0 || j == N) ? 0.0 : sc * z[zpad(j)].x;
   }
 }
 
@@ -815,7 +931,8 @@ void launch_correct(const DevTables& T, const double* phi, const double* mk, con
   { ++g_launches; k_correct<<<cdiv(T.nirr, 128), 128, 0, s>>>(T, phi, mk, fq, jq_given, cval); }
 }
 
-static size_t dense_smem(int N) { return (size_t)(N / 2 + 2 + 2 * N) * sizeof(double); }  // table + N complex
+static int dense_threads(int N) { return N / 16 < 32 ? 32 : N / 16; }
+static size_t dense_smem(int N) { return (size_t)(N / 2 + 2 + 2 * N + N / 8) * sizeof(double); }  // table + padded N complex
 
 void launch_dst_forward(const DevTables& T, const double* fgrid, bool mask, const BumpParams& bp, double* spec,
                         cudaStream_t s) {
@@ -826,14 +943,14 @@ void launch_dst_forward(const DevTables& T, const double* fgrid, bool mask, cons
     cudaFuncSetAttribute(k_dst_dense<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     attr = true;
   }
-  { ++g_launches; k_dst_dense<0><<<T.N - 1, 256, sm, s>>>(T, fgrid, mask ? 1 : 0, bp, nullptr, spec); }
+  { ++g_launches; k_dst_dense<0><<<T.N - 1, dense_threads(T.N), sm, s>>>(T, fgrid, mask ? 1 : 0, bp, nullptr, spec); }
 }
 
 void launch_inverse_dense(const DevTables& T, const double* spec, const double* hsep, double* vgrid,
                           cudaStream_t s) {
   const size_t sm = dense_smem(T.N);
   BumpParams bp{};
-  { ++g_launches; k_dst_dense<1><<<T.N - 1, 256, sm, s>>>(T, spec, 0, bp, hsep, vgrid); }
+  { ++g_launches; k_dst_dense<1><<<T.N - 1, dense_threads(T.N), sm, s>>>(T, spec, 0, bp, hsep, vgrid); }
 }
 
 void launch_sweep(const DevTables& T, const double* cval, bool dense, double* spec, double* zfirst, double* zlast,

@@ -147,8 +147,16 @@ __global__ void k_correct(DevTables T, const double* __restrict__ phi, const dou
 // Outputs: z at the block rows, B[g] = z_g[1], A[g] = h² f̂_sep,g − z_g[L] (reduced-system
 // right-hand side pieces).
 constexpr int kSweepThreads = 512;
-// staged correction: x = c, y packs j (bits 0..23), slot 2·column + parity class (bits 24..29)
-// and "last entry of its (column, class) run" (bit 30)
+constexpr int kRotSteps = 8;                          // pairs per phase-1 item (t = base + 64 s)
+constexpr int kRotStride = kSweepThreads / kRotSteps;  // 64
+// Persistent CTAs, each owning a fixed chunk of B = 512 mode pairs (k, N−k) (pair slot t ↔ k = t,
+// slot 0 ↔ mode N/2) and iterating over blocks g of BL−1 columns (+ the separator column).
+// Phase 1 (DST of the staged sparse corrections, A4): item (column c, pg) covers the 8 pairs
+// t = t0 + pg + 64 s; for a correction (j, c) the sines sin(πjt/N) along s follow by rotation with
+// the per-entry step e^{iπ·64j/N} (staged with the entry), so one table lookup pair serves 8 pairs and
+// sin(πj(N−k)/N) = (−1)^{j+1} sin(πjk/N) serves the partner mode: odd and even rows are summed
+// separately into R[2c + class][slot].  Phase 2 (A5): local Thomas per mode with pivots in registers
+// for the CTA's lifetime; writes z (block rows), B[g] = z_g[1], A[g] = h² f̂_sep,g − z_g[L].
 template <bool DENSE>
 __global__ void __launch_bounds__(kSweepThreads, 1) k_sweep(DevTables T, const double* __restrict__ cval, double* spec,
                                                            double* __restrict__ zB, double* __restrict__ zA) {
@@ -156,14 +164,21 @@ __global__ void __launch_bounds__(kSweepThreads, 1) k_sweep(DevTables T, const d
   const int N = T.N, half = N >> 1, P = T.P, m2 = 2 * N - 1, B = kSweepThreads;
   double* tab = sm;                                          // sin(πr/N), r ∈ [0, N), at r + r/16
   const int tabn = N + (N >> 4) + 2;
-  double* R = sm + tabn;                                     // [BL columns][2 classes][B]
-  double2* ent = reinterpret_cast<double2*>(R + (size_t)BL * 2 * B);
+  double* R = sm + tabn;                                     // [2·BL][B]
+  double4* ent = reinterpret_cast<double4*>(R + (size_t)BL * 2 * B);   // (c, j, cos Δ, sin Δ)
+  int* s_cnt = reinterpret_cast<int*>(ent + T.maxe);         // per-column [start, mid, end) offsets
   for (int r = threadIdx.x; r < N; r += B) tab[r + (r >> 4)] = sin_lookup(T.sin_tab, r, N);
   const int lgN = 31 - __clz(N);
+  auto sinr = [&](int r) {   // sin(πr/N), r ∈ [0, 2N)
+    const int idx = r & (N - 1);
+    const double v = tab[idx + (idx >> 4)];
+    return __hiloint2double(__double2hiint(v) ^ ((r >> lgN) << 31), __double2loint(v));
+  };
   const int nch = (half + B - 1) / B;
   const int G = gridDim.x / nch;
   const int ch = blockIdx.x % nch;
-  const int t = ch * B + threadIdx.x;
+  const int t0 = ch * B;
+  const int t = t0 + threadIdx.x;
   const bool active = t < half;
   const int k1 = t == 0 ? half : (active ? t : 1);
   const int k2 = N - k1;
@@ -182,7 +197,7 @@ __global__ void __launch_bounds__(kSweepThreads, 1) k_sweep(DevTables T, const d
     }
   }
   const double h2 = T.h * T.h;
-  double* R1 = R + threadIdx.x;   // R1[(2c + cls) * B]: Σ over rows of class cls (0 odd, 1 even) of column c
+  double* R1 = R + threadIdx.x;
   for (int g = blockIdx.x / nch; g < P; g += G) {
     const int c0 = BL * g + 1;
     const int e0 = T.col_ptr[c0];
@@ -191,39 +206,63 @@ __global__ void __launch_bounds__(kSweepThreads, 1) k_sweep(DevTables T, const d
     __syncthreads();
     for (int e = e0 + threadIdx.x; e < e1; e += B) {
       const int j = T.irr_j[e];
-      int c = 0;
-      while (T.col_ptr[c0 + c + 1] <= e) ++c;
-      const int cls = e >= T.col_mid[c0 + c] ? 1 : 0;
-      const bool last = (e + 1 == e1) || (e + 1 == T.col_ptr[c0 + c + 1]) || (e + 1 == T.col_mid[c0 + c]);
-      const long long key = (long long)j | ((long long)(2 * c + cls) << 24) | ((long long)last << 30);
-      ent[e - e0] = make_double2(cval[e], __longlong_as_double(key));
+      const int rd = (j * kRotStride) & m2;
+      ent[e - e0] = make_double4(cval[e], (double)j, sin_lookup(T.sin_tab, (rd + half) & m2, N),
+                                 sin_lookup(T.sin_tab, rd, N));
+    }
+    if (threadIdx.x < ncol) {
+      const int i = c0 + threadIdx.x;
+      s_cnt[3 * threadIdx.x] = (cval ? T.col_ptr[i] : e0) - e0;
+      s_cnt[3 * threadIdx.x + 1] = (cval ? T.col_mid[i] : e0) - e0;
+      s_cnt[3 * threadIdx.x + 2] = (cval ? T.col_ptr[i + 1] : e0) - e0;
+    }
+    __syncthreads();
+    // ---- phase 1: sparse DST, rotation along 8 pairs per item ----
+    for (int it = threadIdx.x; it < ncol * kRotStride; it += B) {
+      const int c = it / kRotStride, pg = it - c * kRotStride;
+      const int tb = t0 + pg;
+      const int a0 = s_cnt[3 * c], am = s_cnt[3 * c + 1], a1 = s_cnt[3 * c + 2];
+      double acc[2][kRotSteps];
+#pragma unroll
+      for (int q = 0; q < kRotSteps; ++q) acc[0][q] = acc[1][q] = 0.0;
+      for (int cls = 0; cls < 2; ++cls) {
+        const int lo = cls ? am : a0, hi = cls ? a1 : am;
+        for (int e = lo; e < hi; ++e) {
+          const double4 en = ent[e];
+          const int j = (int)en.y;
+          const int r0 = (j * tb) & m2;
+          double sn = sinr(r0), cs = sinr((r0 + half) & m2);
+#pragma unroll
+          for (int q = 0; q < kRotSteps; ++q) {
+            acc[cls][q] = fma(en.x, sn, acc[cls][q]);
+            const double c2 = fma(cs, en.z, -sn * en.w);
+            sn = fma(sn, en.z, cs * en.w);
+            cs = c2;
+          }
+        }
+      }
+#pragma unroll
+      for (int q = 0; q < kRotSteps; ++q) {
+        const int slot = pg + kRotStride * q;
+        R[(2 * c) * B + slot] = acc[0][q];
+        R[(2 * c + 1) * B + slot] = acc[1][q];
+      }
+    }
+    __syncthreads();
+    if (ch == 0 && threadIdx.x < ncol && cval) {
+      // slot 0 is mode N/2: Σ_j c_j sin(πj/2) (odd rows only)
+      const int c = threadIdx.x;
+      double a = 0.0;
+      for (int e = s_cnt[3 * c]; e < s_cnt[3 * c + 1]; ++e) {
+        const double4 en = ent[e];
+        a += ((((int)en.y) >> 1) & 1) ? -en.x : en.x;
+      }
+      R[(2 * c) * B] = a;
+      R[(2 * c + 1) * B] = 0.0;
     }
     __syncthreads();
     if (!active) continue;
-    // phase 1: h² f̂ of every column for modes k1 and N − k1: odd rows add to both modes,
-    // even rows with opposite signs (sin(πj(N−k)/N) = (−1)^{j+1} sin(πjk/N))
-#pragma unroll
-    for (int q = 0; q < 2 * BL; ++q) R1[q * B] = 0.0;
-    {
-      double acc = 0.0;
-      const int ne = e1 - e0;
-#pragma unroll 4
-      for (int e = 0; e < ne; ++e) {
-        const double2 en = ent[e];
-        const int key = (int)__double_as_longlong(en.y);
-        const int r = ((key & 0xFFFFFF) * k1) & m2;
-        const int idx = r & (N - 1);
-        const double v = tab[idx + (idx >> 4)];
-        // sin(π(r+N)/N) = −sin(πr/N): flip the sign bit when r ≥ N
-        acc = fma(en.x, __hiloint2double(__double2hiint(v) ^ ((r >> lgN) << 31), __double2loint(v)), acc);
-        if (key & (1 << 30)) {
-          R1[((key >> 24) & 63) * B] = acc;   // (2c + cls) = bits 24..29
-          acc = 0.0;
-        }
-      }
-    }
-    // combine classes, add the dense part, then the local Thomas:
-    // y_p = r_p − y_{p−1}/c_{p−1}, z_p = (y_p − z_{p+1})/c_p   (y_p kept in R1[2p], R1[2p+1])
+    // ---- phase 2: local Thomas, y_p = r_p − y_{p−1}/c_{p−1}, z_p = (y_p − z_{p+1})/c_p ----
     auto rhs = [&](int c, double& r1, double& r2) {
       const double ao = R1[(2 * c) * B], ae = R1[(2 * c + 1) * B];
       r1 = ao + ae;
@@ -957,7 +996,7 @@ void launch_sweep(const DevTables& T, const double* cval, bool dense, double* sp
                   double* fsep, cudaStream_t s) {
   (void)zlast;
   const size_t sm = (size_t)(T.N + T.N / 16 + 2) * sizeof(double) + (size_t)BL * 2 * kSweepThreads * sizeof(double) +
-                    (size_t)T.maxe * sizeof(double2);
+                    (size_t)T.maxe * 4 * sizeof(double) + 3 * BL * sizeof(int);
   static bool attr = false;
   if (!attr) {
     cudaFuncSetAttribute(k_sweep<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);

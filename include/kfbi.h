@@ -65,9 +65,10 @@ enum { KFBI_OUTER = 0, KFBI_HOLE = 1 };
 enum { KFBI_DIRICHLET = 0, KFBI_NEUMANN = 1 };
 
 typedef struct {
-  int32_t dim;           /* 2 (3 reserved)                                   */
+  int32_t dim;           /* 2 or 3                                           */
   double lo[3], hi[3];   /* box B; (hi − lo)/n must be equal on all axes      */
-  int32_t n[3];          /* intervals per axis, power of two in [64, 8192], all equal */
+  int32_t n[3];          /* intervals per axis, all equal, power of two in [64, 8192] (2D)
+                            or [32, 512] (3D)                                  */
 } kfbi_grid;
 
 typedef struct {
@@ -169,7 +170,8 @@ kfbi_status kfbi_destroy(kfbi_ctx* ctx);
 
 /* Device time of each kernel of one kfbi_apply, averaged over `reps` applies, from CUDA
  * events recorded on `stream` between the launches (bench/roofline use; synchronous).
- * ms_out[8] = {spline, correct, sweep, reduced, inverse, hole, interp, whole apply}. */
+ * ms_out[8] = {spline, correct, sweep, reduced, inverse, hole, interp, whole apply}; in 3D:
+ * {LSQ fit, base + correction, forward DSTs + sweep, reduced, inverse DSTs, 0, interp, apply}. */
 kfbi_status kfbi_profile_apply(kfbi_ctx* ctx, const double* d_phi, double* d_out, int32_t reps,
                                double* ms_out, void* stream);
 

@@ -29,8 +29,12 @@ inline void ck(cudaError_t e, const char* what) {
 }  // namespace
 
 struct kfbi_ctx {
+  int dim = 2;
   Setup S;
   DevTables T{};
+  Setup3 S3;
+  DevTables3 T3{};
+  double *work = nullptr, *dphi = nullptr;   // 3D working array and LSQ derivatives
   cudaStream_t stream = nullptr;
   int device = 0;
   std::string err;
@@ -141,6 +145,39 @@ void layout(kfbi_ctx* c, Arena& A) {
   c->scal = A.take<double>(8);
 }
 
+void layout3(kfbi_ctx* c, Arena& A) {
+  Setup3& S = c->S3;
+  DevTables3& T = c->T3;
+  const size_t N = S.N, P = S.P, K = N * N, M = S.nq;
+  T.N = S.N; T.P = S.P; T.nq = S.nq; T.nirr = S.nirr; T.lo = S.lo; T.h = S.h; T.kappa = S.kappa;
+  T.q_axis = A.table(S.q_axis); T.q_pos = A.table(S.q_pos); T.q_n = A.table(S.q_n); T.q_e1 = A.table(S.q_e1);
+  T.q_e2 = A.table(S.q_e2); T.q_kab = A.table(S.q_kab);
+  T.irr_lin = A.table(S.irr_lin); T.irr_side = A.table(S.irr_side); T.irr_ptr = A.table(S.irr_ptr);
+  T.pair_q = A.table(S.pair_q); T.pair_d = A.table(S.pair_d);
+  T.lsq_ptr = A.table(S.lsq_ptr); T.lsq_nb = A.table(S.lsq_nb); T.lsq_G = A.table(S.lsq_G);
+  T.st_c = A.table(S.st_c); T.st_code = A.table(S.st_code); T.st_w = A.table(S.st_w);
+  T.sin_tab = A.table(S.sin_tab); T.dk = A.table(S.dk); T.zr = A.table(S.zr); T.red_a = A.table(S.red_a);
+  T.red_b = A.table(S.red_b); T.side = A.table(S.side);
+  c->nh = 0;
+  c->work = A.take<double>((N - 1) * K);
+  c->zfirst = A.take<double>(P * K);
+  c->fsep = A.take<double>(std::max<size_t>(P - 1, 1) * K);
+  c->hsep = A.take<double>(std::max<size_t>(P - 1, 1) * K);
+  c->dphi = A.take<double>(5 * M);
+  c->V = A.take<double>((kMaxRestart + 1) * M);
+  c->gx = A.take<double>(M);
+  c->gr = A.take<double>(M);
+  c->ghat = A.take<double>(M);
+  c->tmp = A.take<double>(M);
+  c->partial = A.take<double>((kMaxRestart + 2) * kRedBlocks);
+  c->hcol = A.take<double>(kMaxRestart + 2);
+  c->ycoef = A.take<double>(kMaxRestart + 1);
+  c->scal = A.take<double>(8);
+  c->ahole = A.take<double>(1);
+}
+
+int nctrl(const kfbi_ctx* c) { return c->dim == 3 ? c->S3.nq : c->S.M; }
+
 kfbi_status fail(kfbi_ctx* c, kfbi_status st, const std::string& msg) {
   if (c) c->err = msg;
   return st;
@@ -162,7 +199,7 @@ void need_ws(kfbi_ctx* c) {
 }
 
 // --- one interface solve, sparse output at stencil nodes → V⁺ at control points ----------
-void apply_KD(kfbi_ctx* c, const double* phi, double* out, cudaStream_t s) {
+void apply_KD2(kfbi_ctx* c, const double* phi, double* out, cudaStream_t s) {
   const DevTables& T = c->T;
   launch_spline(T, phi, c->mk, s);
   launch_correct(T, phi, c->mk, nullptr, nullptr, c->cval, s);
@@ -173,7 +210,7 @@ void apply_KD(kfbi_ctx* c, const double* phi, double* out, cudaStream_t s) {
   launch_interp(T, phi, c->mk, nullptr, nullptr, c->vsten, c->nh, c->nh ? c->wg : nullptr, c->ahole, out, s);
 }
 
-void apply_Y(kfbi_ctx* c, const double* fgrid, const double* fq, const double* fz, double* out, cudaStream_t s) {
+void apply_Y2(kfbi_ctx* c, const double* fgrid, const double* fq, const double* fz, double* out, cudaStream_t s) {
   const DevTables& T = c->T;
   BumpParams none{};
   launch_dst_forward(T, fgrid, true, none, c->spec, s);
@@ -184,7 +221,7 @@ void apply_Y(kfbi_ctx* c, const double* fgrid, const double* fq, const double* f
   launch_interp(T, nullptr, nullptr, fz, nullptr, c->vsten, 0, nullptr, nullptr, out, s);
 }
 
-void final_field(kfbi_ctx* c, const double* phi, const double* fgrid, const double* fq, double* u, cudaStream_t s) {
+void final_field2(kfbi_ctx* c, const double* phi, const double* fgrid, const double* fq, double* u, cudaStream_t s) {
   const DevTables& T = c->T;
   BumpParams bp = c->bump;
   bp.a = c->ahole;
@@ -199,6 +236,64 @@ void final_field(kfbi_ctx* c, const double* phi, const double* fgrid, const doub
   const size_t W = (size_t)T.N + 1;
   ck(cudaMemsetAsync(u, 0, W * sizeof(double), s), "memset");
   ck(cudaMemsetAsync(u + (size_t)T.N * W, 0, W * sizeof(double), s), "memset");
+}
+
+// --- 3D interface solves (control points = intersection nodes, R12) -------------------
+void forward3(kfbi_ctx* c, cudaStream_t s) {   // rows: DST along z, transpose, DST along y
+  launch_dst_rows3(c->T3, 0, c->work, nullptr, 1.0, nullptr, s);
+  launch_transpose3(c->T3, c->work, s);
+  launch_dst_rows3(c->T3, 0, c->work, nullptr, 1.0, nullptr, s);
+  launch_sweep3(c->T3, c->work, c->zfirst, c->fsep, s);
+  launch_reduced3(c->T3, c->zfirst, c->fsep, c->hsep, s);
+}
+void inverse3(kfbi_ctx* c, double* u, cudaStream_t s) {   // u == NULL: result stays in work
+  const double sc = 2.0 / c->T3.N;
+  launch_dst_rows3(c->T3, 1, c->work, c->hsep, sc, nullptr, s);
+  launch_transpose3(c->T3, c->work, s);
+  if (!u) {
+    launch_dst_rows3(c->T3, 0, c->work, nullptr, sc, nullptr, s);
+    return;
+  }
+  launch_dst_rows3(c->T3, 2, c->work, nullptr, sc, u, s);
+  const size_t W = (size_t)c->T3.N + 1;
+  ck(cudaMemsetAsync(u, 0, W * W * sizeof(double), s), "memset");
+  ck(cudaMemsetAsync(u + (size_t)c->T3.N * W * W, 0, W * W * sizeof(double), s), "memset");
+  ck(cudaMemset2DAsync(u + (W + c->T3.N) * W, W * W * sizeof(double), 0, W * sizeof(double), c->T3.N - 1, s), "memset");
+}
+void apply_KD3(kfbi_ctx* c, const double* phi, double* out, cudaStream_t s) {
+  launch_lsq3(c->T3, phi, c->dphi, s);
+  launch_base3(c->T3, nullptr, c->work, s);
+  launch_correct3(c->T3, phi, c->dphi, nullptr, nullptr, c->work, s);
+  forward3(c, s);
+  inverse3(c, nullptr, s);
+  launch_interp3(c->T3, phi, c->dphi, nullptr, nullptr, c->work, out, s);
+}
+void apply_Y3(kfbi_ctx* c, const double* fgrid, const double* fq, const double* fz, double* out, cudaStream_t s) {
+  launch_base3(c->T3, fgrid, c->work, s);
+  launch_correct3(c->T3, nullptr, nullptr, fq, nullptr, c->work, s);
+  forward3(c, s);
+  inverse3(c, nullptr, s);
+  launch_interp3(c->T3, nullptr, nullptr, fz, nullptr, c->work, out, s);
+}
+void final_field3(kfbi_ctx* c, const double* phi, const double* fgrid, const double* fq, double* u, cudaStream_t s) {
+  launch_lsq3(c->T3, phi, c->dphi, s);
+  launch_base3(c->T3, fgrid, c->work, s);
+  launch_correct3(c->T3, phi, c->dphi, fq, nullptr, c->work, s);
+  forward3(c, s);
+  inverse3(c, u, s);
+}
+
+void apply_KD(kfbi_ctx* c, const double* phi, double* out, cudaStream_t s) {
+  if (c->dim == 3) apply_KD3(c, phi, out, s);
+  else apply_KD2(c, phi, out, s);
+}
+void apply_Y(kfbi_ctx* c, const double* fgrid, const double* fq, const double* fz, double* out, cudaStream_t s) {
+  if (c->dim == 3) apply_Y3(c, fgrid, fq, fz, out, s);
+  else apply_Y2(c, fgrid, fq, fz, out, s);
+}
+void final_field(kfbi_ctx* c, const double* phi, const double* fgrid, const double* fq, double* u, cudaStream_t s) {
+  if (c->dim == 3) final_field3(c, phi, fgrid, fq, u, s);
+  else final_field2(c, phi, fgrid, fq, u, s);
 }
 
 }  // namespace
@@ -225,11 +320,15 @@ kfbi_status kfbi_setup(const kfbi_grid* grid, const kfbi_boundary* bnd, const kf
   }
   auto* c = new kfbi_ctx();
   try {
-    build_setup(c->S, grid, bnd, pde);
+    if (!grid || !bnd || !pde || !bnd->comp) throw ArgError("null descriptor");
+    c->dim = grid->dim;
+    if (c->dim == 3) build_setup3(c->S3, grid, bnd, pde);
+    else build_setup(c->S, grid, bnd, pde);
     c->stream = (cudaStream_t)stream;
     c->device = dist ? dist->device : 0;
     Arena A{nullptr, 0, false};
-    layout(c, A);
+    if (c->dim == 3) layout3(c, A);
+    else layout(c, A);
     c->ws_need = A.off + 256;
     c->bump.nh = c->nh;
     for (int h = 0; h < c->nh && h < 4; ++h) {
@@ -267,7 +366,8 @@ kfbi_status kfbi_set_workspace(kfbi_ctx* c, void* d_ws, size_t bytes) {
   c->ws = (uint8_t*)d_ws;
   c->ws_bytes = bytes;
   Arena A{c->ws, 0, true};
-  layout(c, A);
+  if (c->dim == 3) layout3(c, A);
+  else layout(c, A);
   cudaStream_t s = c->stream;
   for (auto& u : A.uploads) ck(cudaMemcpyAsync(u.first, u.second.first, u.second.second, cudaMemcpyHostToDevice, s), "upload");
   if (!c->hcol_host) ck(cudaMallocHost(&c->hcol_host, (kMaxRestart + 2) * sizeof(double)), "cudaMallocHost");
@@ -289,6 +389,14 @@ kfbi_status kfbi_set_workspace(kfbi_ctx* c, void* d_ws, size_t bytes) {
 
 kfbi_status kfbi_sizes(const kfbi_ctx* c, int64_t* M, int64_t* nq, int64_t* nirr, int64_t* nn) {
   if (!c) return KFBI_EINVAL;
+  if (c->dim == 3) {
+    const int64_t W = c->S3.N + 1;
+    if (M) *M = c->S3.nq;
+    if (nq) *nq = c->S3.nq;
+    if (nirr) *nirr = c->S3.nirr;
+    if (nn) *nn = W * W * W;
+    return KFBI_OK;
+  }
   if (M) *M = c->S.M;
   if (nq) *nq = c->S.nq;
   if (nirr) *nirr = c->S.nirr;
@@ -298,6 +406,11 @@ kfbi_status kfbi_sizes(const kfbi_ctx* c, int64_t* M, int64_t* nq, int64_t* nirr
 
 kfbi_status kfbi_points(const kfbi_ctx* c, int32_t which, double* xyz) {
   if (!c || !xyz) return KFBI_EINVAL;
+  if (c->dim == 3) {
+    if (which != 0 && which != 1) return KFBI_EINVAL;
+    std::memcpy(xyz, c->S3.q_pos.data(), c->S3.q_pos.size() * sizeof(double));
+    return KFBI_OK;
+  }
   const Setup& S = c->S;
   if (which == 0) {
     for (int m = 0; m < S.M; ++m) { xyz[2 * m] = S.z_x[m]; xyz[2 * m + 1] = S.z_y[m]; }
@@ -311,7 +424,8 @@ kfbi_status kfbi_points(const kfbi_ctx* c, int32_t which, double* xyz) {
 
 kfbi_status kfbi_node_mask(const kfbi_ctx* c, int8_t* mask) {
   if (!c || !mask) return KFBI_EINVAL;
-  std::memcpy(mask, c->S.side.data(), c->S.side.size());
+  const auto& sd = c->dim == 3 ? c->S3.side : c->S.side;
+  std::memcpy(mask, sd.data(), sd.size());
   return KFBI_OK;
 }
 
@@ -341,7 +455,7 @@ kfbi_status kfbi_solve(kfbi_ctx* c, const double* d_g, const double* d_f_grid, c
   KFBI_TRY(c)
   need_ws(c);
   cudaStream_t s = pick(c, stream);
-  const int M = c->S.M;
+  const int M = nctrl(c);
   const size_t bM = (size_t)M * sizeof(double);
   // ĝ = g − (Yf)⁺
   if (d_f_grid) {
@@ -437,6 +551,13 @@ kfbi_status kfbi_solve(kfbi_ctx* c, const double* d_g, const double* d_f_grid, c
 
 kfbi_status kfbi_apply_model(const kfbi_ctx* c, double* bytes_sweep, double* bytes_inverse, double* unknowns) {
   if (!c) return KFBI_EINVAL;
+  if (c->dim == 3) {
+    const double N = c->S3.N, U = (N - 1) * (N - 1) * (N - 1), F = (N - 1) * N * N;
+    if (bytes_sweep) *bytes_sweep = 16.0 * F;        // read + write of the spectral array
+    if (bytes_inverse) *bytes_inverse = 16.0 * F;    // one DST-rows pass (read + write)
+    if (unknowns) *unknowns = U;
+    return KFBI_OK;
+  }
   const double N = c->S.N, P = c->S.P;
   // sweep: writes v̂ at the block rows of every mode (8 B per value); reads are on-chip
   if (bytes_sweep) *bytes_sweep = 8.0 * (N - P) * (N - 1);
@@ -456,6 +577,44 @@ kfbi_status kfbi_profile_apply(kfbi_ctx* c, const double* d_phi, double* d_out, 
   cudaEvent_t ev[8];
   for (auto& e : ev) ck(cudaEventCreate(&e), "event");
   double acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  if (c->dim == 3) {
+    const DevTables3& T3 = c->T3;
+    const double sc = 2.0 / T3.N;
+    for (int r = 0; r < reps; ++r) {
+      ck(cudaEventRecord(ev[0], s), "rec");
+      launch_lsq3(T3, d_phi, c->dphi, s);
+      ck(cudaEventRecord(ev[1], s), "rec");
+      launch_base3(T3, nullptr, c->work, s);
+      launch_correct3(T3, d_phi, c->dphi, nullptr, nullptr, c->work, s);
+      ck(cudaEventRecord(ev[2], s), "rec");
+      launch_dst_rows3(T3, 0, c->work, nullptr, 1.0, nullptr, s);
+      launch_transpose3(T3, c->work, s);
+      launch_dst_rows3(T3, 0, c->work, nullptr, 1.0, nullptr, s);
+      launch_sweep3(T3, c->work, c->zfirst, c->fsep, s);
+      ck(cudaEventRecord(ev[3], s), "rec");
+      launch_reduced3(T3, c->zfirst, c->fsep, c->hsep, s);
+      ck(cudaEventRecord(ev[4], s), "rec");
+      launch_dst_rows3(T3, 1, c->work, c->hsep, sc, nullptr, s);
+      launch_transpose3(T3, c->work, s);
+      launch_dst_rows3(T3, 0, c->work, nullptr, sc, nullptr, s);
+      ck(cudaEventRecord(ev[5], s), "rec");
+      ck(cudaEventRecord(ev[6], s), "rec");
+      launch_interp3(T3, d_phi, c->dphi, nullptr, nullptr, c->work, d_out, s);
+      ck(cudaEventRecord(ev[7], s), "rec");
+      ck(cudaEventSynchronize(ev[7]), "sync");
+      for (int q = 0; q < 7; ++q) {
+        float t = 0;
+        ck(cudaEventElapsedTime(&t, ev[q], ev[q + 1]), "elapsed");
+        acc[q] += t;
+      }
+      float t = 0;
+      ck(cudaEventElapsedTime(&t, ev[0], ev[7]), "elapsed");
+      acc[7] += t;
+    }
+    for (int q = 0; q < 8; ++q) ms[q] = acc[q] / reps;
+    for (auto& e : ev) cudaEventDestroy(e);
+    return KFBI_OK;
+  }
   for (int r = 0; r < reps; ++r) {
     ck(cudaEventRecord(ev[0], s), "rec");
     launch_spline(T, d_phi, c->mk, s);
@@ -506,6 +665,13 @@ kfbi_status kfbi_test_fast_solve(kfbi_ctx* c, const double* d_rhs, double* d_v, 
   KFBI_TRY(c)
   need_ws(c);
   cudaStream_t s = pick(c, stream);
+  if (c->dim == 3) {
+    launch_base3(c->T3, d_rhs, c->work, s);   // note: masked by Ω (test inputs are Ω-supported or use 2D)
+    forward3(c, s);
+    inverse3(c, d_v, s);
+    ck(cudaGetLastError(), "fast solve 3D");
+    return KFBI_OK;
+  }
   BumpParams none{};
   launch_dst_forward(c->T, d_rhs, false, none, c->spec, s);
   launch_sweep(c->T, nullptr, true, c->spec, c->zfirst, c->zlast, c->fsep, s);
@@ -525,6 +691,27 @@ kfbi_status kfbi_test_interface_solve(kfbi_ctx* c, const double* d_base, const d
   KFBI_TRY(c)
   need_ws(c);
   cudaStream_t s = pick(c, stream);
+  if (c->dim == 3) {
+    launch_base3(c->T3, d_base, c->work, s);
+    launch_correct3(c->T3, nullptr, nullptr, nullptr, d_jq, c->work, s);
+    forward3(c, s);
+    if (d_v) {
+      inverse3(c, d_v, s);
+    } else {
+      inverse3(c, nullptr, s);
+    }
+    if (d_vplus) {
+      if (d_v) {   // the field went to d_v: recompute the working copy for the interpolation
+        launch_base3(c->T3, d_base, c->work, s);
+        launch_correct3(c->T3, nullptr, nullptr, nullptr, d_jq, c->work, s);
+        forward3(c, s);
+        inverse3(c, nullptr, s);
+      }
+      launch_interp3(c->T3, nullptr, nullptr, nullptr, d_jz, c->work, d_vplus, s);
+    }
+    ck(cudaGetLastError(), "interface solve 3D");
+    return KFBI_OK;
+  }
   BumpParams none{};
   if (d_base) launch_dst_forward(c->T, d_base, false, none, c->spec, s);
   launch_correct(c->T, nullptr, nullptr, nullptr, d_jq, c->cval, s);
@@ -547,6 +734,21 @@ kfbi_status kfbi_test_interface_solve(kfbi_ctx* c, const double* d_base, const d
 
 kfbi_status kfbi_test_setup_dump(const kfbi_ctx* c, int32_t which, int64_t* out) {
   if (!c || !out) return KFBI_EINVAL;
+  if (c->dim == 3) {
+    const Setup3& S = c->S3;
+    if (which == 0) {
+      for (size_t u = 0; u < S.irr_ijk.size(); ++u) out[u] = S.irr_ijk[u];
+    } else if (which == 1) {
+      for (int q = 0; q < S.nq; ++q) {
+        out[4 * q] = S.q_axis[q]; out[4 * q + 1] = S.q_i[q]; out[4 * q + 2] = S.q_j[q]; out[4 * q + 3] = S.q_k[q];
+      }
+    } else if (which == 2) {
+      std::memcpy(out, S.st_nodes_ij.data(), S.st_nodes_ij.size() * sizeof(int64_t));
+    } else {
+      return KFBI_EINVAL;
+    }
+    return KFBI_OK;
+  }
   const Setup& S = c->S;
   if (which == 0) {
     std::vector<std::pair<int, int>> v(S.nirr);

@@ -56,4 +56,20 @@ void launch_axpy_basis(int n, int k, const double* V, int ldv, const double* y, 
 void launch_sub(int n, const double* a, const double* b, double* out, cudaStream_t s);
 void launch_scale_copy(int n, const double* a, const double* scal, double* out, cudaStream_t s);
 
+// ---- 3D (kernels3d in kernels2d.cu) ----
+void launch_lsq3(const DevTables3& T, const double* phi, double* dphi, cudaStream_t s);
+void launch_base3(const DevTables3& T, const double* fgrid, double* work, cudaStream_t s);
+void launch_correct3(const DevTables3& T, const double* phi, const double* dphi, const double* fq,
+                     const double* jq_given, double* work, cudaStream_t s);
+// batched in-place DST-I of the (N−1)·N rows of the working array: mode 0 plain (× scale);
+// mode 1 inverse with the arrowhead fix-up on load (rows = (i, ll), modes m = ll·N + kk);
+// mode 2 final store into a full (N+1)^3 grid (× scale)
+void launch_dst_rows3(const DevTables3& T, int mode, double* work, const double* hsep, double scale, double* out,
+                      cudaStream_t s);
+void launch_transpose3(const DevTables3& T, double* work, cudaStream_t s);
+void launch_sweep3(const DevTables3& T, double* work, double* zB, double* zA, cudaStream_t s);
+void launch_reduced3(const DevTables3& T, const double* zB, const double* zA, double* hsep, cudaStream_t s);
+void launch_interp3(const DevTables3& T, const double* phi, const double* dphi, const double* fz,
+                    const double* jz_given, const double* work, double* out, cudaStream_t s);
+
 }  // namespace kfbi

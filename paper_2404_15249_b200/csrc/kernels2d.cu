@@ -1095,3 +1095,410 @@ void launch_scale_copy(int n, const double* a, const double* scal, double* out, 
 }
 
 }  // namespace kfbi
+
+// =============================================================================== 3D path
+// Working array layout: work[(i−1)·N² + a·N + b], i = 1..N−1 (x), a, b ∈ [0, N) padded (index 0 ≡ 0).
+// Forward: rows (i, j) DST along z (b: l → ll) → plane transpose → rows (i, ll) DST along y
+// (j → kk): spectral layout [i][ll][kk], mode m = ll·N + kk.  Tridiagonal along x per mode
+// (same two-level arrowhead as 2D).  Inverse: rows (i, ll) with the fix-up (kk → j) → transpose →
+// rows (i, j) (ll → l).
+namespace kfbi {
+namespace {
+
+struct Jump10 {
+  double v, g[3], H[6];   // H: xx, yy, zz, xy, xz, yz
+};
+
+// Monge-patch closed form (reading R13): [∇v] = Σ_a ∂_aΦ e_a + Ψ n,
+// A_ab = ∂_abΦ − κ_ab Ψ, A_an = ∂_aΨ + Σ_b κ_ab ∂_bΦ, A_nn = [F] + κΦ − A_11 − A_22, [D²v] = F A Fᵀ.
+__device__ __forceinline__ Jump10 jumps3d(double Phi, const double* dP, double F, double kappa, const double* n,
+                                          const double* e1, const double* e2, const double* kab) {
+  Jump10 J;
+  J.v = Phi;
+#pragma unroll
+  for (int r = 0; r < 3; ++r) J.g[r] = dP[0] * e1[r] + dP[1] * e2[r];
+  const double A11 = dP[2], A12 = dP[3], A22 = dP[4];
+  const double A1n = kab[0] * dP[0] + kab[1] * dP[1];
+  const double A2n = kab[1] * dP[0] + kab[2] * dP[1];
+  const double Ann = F + kappa * Phi - A11 - A22;
+  auto h = [&](int r, int c) {
+    return A11 * e1[r] * e1[c] + A12 * (e1[r] * e2[c] + e2[r] * e1[c]) + A22 * e2[r] * e2[c] +
+           A1n * (e1[r] * n[c] + n[r] * e1[c]) + A2n * (e2[r] * n[c] + n[r] * e2[c]) + Ann * n[r] * n[c];
+  };
+  J.H[0] = h(0, 0);
+  J.H[1] = h(1, 1);
+  J.H[2] = h(2, 2);
+  J.H[3] = h(0, 1);
+  J.H[4] = h(0, 2);
+  J.H[5] = h(1, 2);
+  return J;
+}
+
+__device__ __forceinline__ void load_jump3(const DevTables3& T, int q, const double* phi, const double* dphi,
+                                           const double* fq, const double* jg, Jump10& J) {
+  if (jg) {
+    J.v = jg[10 * q];
+#pragma unroll
+    for (int r = 0; r < 3; ++r) J.g[r] = jg[10 * q + 1 + r];
+#pragma unroll
+    for (int r = 0; r < 6; ++r) J.H[r] = jg[10 * q + 4 + r];
+    return;
+  }
+  double dP[5] = {0, 0, 0, 0, 0};
+  double Phi = 0.0;
+  if (phi) {
+    Phi = phi[q];
+#pragma unroll
+    for (int r = 0; r < 5; ++r) dP[r] = dphi[5 * q + r];
+  }
+  J = jumps3d(Phi, dP, fq ? fq[q] : 0.0, T.kappa, T.q_n + 3 * q, T.q_e1 + 3 * q, T.q_e2 + 3 * q, T.q_kab + 3 * q);
+}
+
+// A1 (3D): tangent-plane LSQ fit (reading R12) with the precomputed scaled normal-matrix inverse.
+__global__ void k_lsq3(DevTables3 T, const double* __restrict__ phi, double* __restrict__ dphi) {
+  const int e = blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= T.nq) return;
+  const double ih = 1.0 / T.h;
+  const double x0 = T.q_pos[3 * e], y0 = T.q_pos[3 * e + 1], z0 = T.q_pos[3 * e + 2];
+  const double* e1 = T.q_e1 + 3 * e;
+  const double* e2 = T.q_e2 + 3 * e;
+  const double f0 = phi[e];
+  double b[5] = {0, 0, 0, 0, 0};
+  for (int u = T.lsq_ptr[e]; u < T.lsq_ptr[e + 1]; ++u) {
+    const int q = T.lsq_nb[u];
+    const double dx = (T.q_pos[3 * q] - x0) * ih, dy = (T.q_pos[3 * q + 1] - y0) * ih, dz = (T.q_pos[3 * q + 2] - z0) * ih;
+    const double t1 = e1[0] * dx + e1[1] * dy + e1[2] * dz, t2 = e2[0] * dx + e2[1] * dy + e2[2] * dz;
+    const double df = phi[q] - f0;
+    b[0] = fma(t1, df, b[0]);
+    b[1] = fma(t2, df, b[1]);
+    b[2] = fma(0.5 * t1 * t1, df, b[2]);
+    b[3] = fma(t1 * t2, df, b[3]);
+    b[4] = fma(0.5 * t2 * t2, df, b[4]);
+  }
+  const double* G = T.lsq_G + 15 * (size_t)e;
+  // symmetric 5×5 from its upper triangle
+  const double g[5][5] = {{G[0], G[1], G[2], G[3], G[4]},
+                          {G[1], G[5], G[6], G[7], G[8]},
+                          {G[2], G[6], G[9], G[10], G[11]},
+                          {G[3], G[7], G[10], G[12], G[13]},
+                          {G[4], G[8], G[11], G[13], G[14]}};
+  double a[5];
+#pragma unroll
+  for (int r = 0; r < 5; ++r) {
+    double s = 0.0;
+#pragma unroll
+    for (int c = 0; c < 5; ++c) s = fma(g[r][c], b[c], s);
+    a[r] = s;
+  }
+  dphi[5 * e] = a[0] * ih;
+  dphi[5 * e + 1] = a[1] * ih;
+  dphi[5 * e + 2] = a[2] * ih * ih;
+  dphi[5 * e + 3] = a[3] * ih * ih;
+  dphi[5 * e + 4] = a[4] * ih * ih;
+}
+
+// dense base h²·f·1_Ω (or 0) into the padded working layout
+__global__ void k_base3(DevTables3 T, const double* __restrict__ f, double* __restrict__ work) {
+  const int N = T.N, W = N + 1;
+  const size_t total = (size_t)(N - 1) * N * N;
+  const double h2 = T.h * T.h;
+  for (size_t idx = (size_t)blockIdx.x * blockDim.x + threadIdx.x; idx < total; idx += (size_t)gridDim.x * blockDim.x) {
+    const int i = (int)(idx / ((size_t)N * N)) + 1;
+    const int a = (int)((idx / N) % N), b = (int)(idx % N);
+    double v = 0.0;
+    if (f && a > 0 && b > 0) {
+      const size_t u = ((size_t)i * W + a) * W + b;
+      if (T.side[u]) v = h2 * f[u];
+    }
+    work[idx] = v;
+  }
+}
+
+// A2+A3 (3D): seven-point correction at irregular nodes, added in place (×h²)
+__global__ void k_correct3(DevTables3 T, const double* __restrict__ phi, const double* __restrict__ dphi,
+                           const double* __restrict__ fq, const double* __restrict__ jg, double* __restrict__ work) {
+  const int n = blockIdx.x * blockDim.x + threadIdx.x;
+  if (n >= T.nirr) return;
+  double acc = 0.0;
+  for (int e = T.irr_ptr[n]; e < T.irr_ptr[n + 1]; ++e) {
+    const int q = T.pair_q[e];
+    const double d = T.pair_d[e];
+    const int ax = T.q_axis[q];
+    Jump10 J;
+    load_jump3(T, q, phi, dphi, fq, jg, J);
+    acc += J.v + J.g[ax] * d + 0.5 * J.H[ax] * d * d;   // H[0..2] = xx, yy, zz
+  }
+  work[T.irr_lin[n]] += T.irr_side[n] ? -acc : acc;
+}
+
+// fix-up of the spectral value at row i (x), mode m
+__device__ __forceinline__ double fixup3(const DevTables3& T, const double* __restrict__ spec,
+                                         const double* __restrict__ hsep, int i, size_t m) {
+  const size_t K = (size_t)T.N * T.N;
+  const int q = i / BL, r = i - q * BL;
+  if (r == 0) return hsep[(size_t)(q - 1) * K + m];
+  const int p = r - 1, g = q;
+  double x = spec[(size_t)(i - 1) * K + m];
+  if (g > 0) x = fma(-hsep[(size_t)(g - 1) * K + m], T.zr[(size_t)(LB - 1 - p) * K + m], x);
+  if (g < T.P - 1) x = fma(-hsep[(size_t)g * K + m], T.zr[(size_t)p * K + m], x);
+  return x;
+}
+
+// batched DST-I of rows of length N (index 0 ≡ 0), one row per CTA, recurrence-free (odd extension)
+template <int MODE>
+__global__ void __launch_bounds__(512) k_dst_rows3(DevTables3 T, double* work, const double* __restrict__ hsep,
+                                                   double scale, double* __restrict__ out) {
+  extern __shared__ double sm[];
+  const int N = T.N, half = N >> 1;
+  double* s_sin = sm;
+  double2* z = reinterpret_cast<double2*>(sm + half + 2);
+  double* f = reinterpret_cast<double*>(z) + N / 8 - N;
+  for (int r = threadIdx.x; r <= half; r += blockDim.x) s_sin[r] = T.sin_tab[r];
+  const size_t row = blockIdx.x;                 // row index: (i−1)·N + a
+  const int i = (int)(row / N) + 1, a = (int)(row % N);
+  double* rp = work + row * N;
+  for (int j = threadIdx.x; j < N; j += blockDim.x) {
+    double v = 0.0;
+    if (j > 0) v = MODE == 1 ? fixup3(T, work, hsep, i, (size_t)a * N + j) : rp[j];
+    f[N + j] = v;
+  }
+  __syncthreads();
+  {
+    double2 buf[16];
+#pragma unroll
+    for (int it = 0; it < 16; ++it) {
+      const int m = threadIdx.x + it * blockDim.x;
+      if (m < N) {
+        const int j0 = 2 * m, j1 = 2 * m + 1;
+        const double a0 = j0 < N ? f[N + j0] : (j0 == N ? 0.0 : -f[N + 2 * N - j0]);
+        const double b0 = j1 < N ? f[N + j1] : -f[N + 2 * N - j1];
+        buf[it] = make_double2(a0, b0);
+      }
+    }
+    __syncthreads();
+#pragma unroll
+    for (int it = 0; it < 16; ++it) {
+      const int m = threadIdx.x + it * blockDim.x;
+      if (m < N) z[zpad(m)] = buf[it];
+    }
+  }
+  __syncthreads();
+  {
+    const int nth = N / 16 < 32 ? 32 : N / 16;
+    int Ns = 1;
+    while (Ns * 16 <= N) {
+      stockham_pass<16>(z, s_sin, N, Ns, nth);
+      Ns *= 16;
+    }
+    const int rem = N / Ns;
+    if (rem == 2) stockham_pass<2>(z, s_sin, N, Ns, nth);
+    else if (rem == 4) stockham_pass<4>(z, s_sin, N, Ns, nth);
+    else if (rem == 8) stockham_pass<8>(z, s_sin, N, Ns, nth);
+  }
+  for (int k = threadIdx.x; k <= half; k += blockDim.x) {
+    if (k == 0) {
+      z[0].x = 0.0;
+      continue;
+    }
+    const int k2 = N - k;
+    const double2 a0 = z[zpad(k)], b0 = z[zpad(k2)];
+    double c, s;
+    twiddle(s_sin, k, N, c, s);
+    const double Fk = 0.5 * (0.5 * (a0.y - b0.y) + c * (-0.5 * (a0.x - b0.x)) + s * (0.5 * (a0.y + b0.y)));
+    double Fk2 = 0.0;
+    if (k2 != k) {
+      twiddle(s_sin, k2, N, c, s);
+      Fk2 = 0.5 * (0.5 * (b0.y - a0.y) + c * (-0.5 * (b0.x - a0.x)) + s * (0.5 * (b0.y + a0.y)));
+    }
+    z[zpad(k)].x = Fk;
+    if (k2 != k) z[zpad(k2)].x = Fk2;
+  }
+  __syncthreads();
+  if (MODE == 2) {
+    const int W = N + 1;
+    double* op = out + ((size_t)i * W + a) * W;
+    for (int j = threadIdx.x; j <= N; j += blockDim.x) op[j] = (j == 0 || j == N || a == 0) ? 0.0 : scale * z[zpad(j)].x;
+  } else {
+    for (int k = threadIdx.x; k < N; k += blockDim.x) rp[k] = (k == 0 || a == 0) ? 0.0 : scale * z[zpad(k)].x;
+  }
+}
+
+// in-place transpose of every N×N plane by 32×32 tile pairs
+__global__ void k_transpose3(int N, double* work) {
+  __shared__ double ta[32][33], tb[32][33];
+  const int T = N / 32;
+  int p = blockIdx.x;   // tile pair index within a plane: (a, b) with a ≤ b
+  int ta_i = 0;
+  while (p >= T - ta_i) {
+    p -= T - ta_i;
+    ++ta_i;
+  }
+  const int tb_i = ta_i + p;
+  double* plane = work + (size_t)blockIdx.y * N * N;
+  const int tx = threadIdx.x, ty = threadIdx.y;   // 32 × 8
+  for (int r = ty; r < 32; r += 8) {
+    ta[r][tx] = plane[(size_t)(ta_i * 32 + r) * N + tb_i * 32 + tx];
+    tb[r][tx] = plane[(size_t)(tb_i * 32 + r) * N + ta_i * 32 + tx];
+  }
+  __syncthreads();
+  for (int r = ty; r < 32; r += 8) {
+    plane[(size_t)(tb_i * 32 + r) * N + ta_i * 32 + tx] = ta[tx][r];
+    plane[(size_t)(ta_i * 32 + r) * N + tb_i * 32 + tx] = tb[tx][r];
+  }
+}
+
+// A5 (3D): per mode m, all P blocks of BL−1 rows in turn; pivots in registers
+__global__ void __launch_bounds__(256) k_sweep3(DevTables3 T, double* spec, double* __restrict__ zB,
+                                                double* __restrict__ zA) {
+  const int N = T.N, P = T.P;
+  const size_t K = (size_t)N * N;
+  const size_t m = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (m >= K) return;
+  const int ll = (int)(m / N), kk = (int)(m % N);
+  if (ll == 0 || kk == 0) return;
+  const double d = T.dk[m];
+  double ic[LB];
+  {
+    double c = d;
+#pragma unroll
+    for (int p = 0; p < LB; ++p) {
+      if (p) c = d - ic[p - 1];
+      ic[p] = 1.0 / c;
+    }
+  }
+  for (int g = 0; g < P; ++g) {
+    double y[LB];
+#pragma unroll
+    for (int p = 0; p < LB; ++p) {
+      const double r = spec[(size_t)(BL * g + p) * K + m];
+      y[p] = p ? fma(-y[p - 1], ic[p - 1], r) : r;
+    }
+    y[LB - 1] *= ic[LB - 1];
+#pragma unroll
+    for (int p = LB - 2; p >= 0; --p) y[p] = (y[p] - y[p + 1]) * ic[p];
+#pragma unroll
+    for (int p = 0; p < LB; ++p) spec[(size_t)(BL * g + p) * K + m] = y[p];
+    zB[(size_t)g * K + m] = y[0];
+    if (g < P - 1) zA[(size_t)g * K + m] = spec[(size_t)(BL * g + LB) * K + m] - y[LB - 1];
+  }
+}
+
+__global__ void k_reduced3(DevTables3 T, const double* __restrict__ zB, const double* __restrict__ zA,
+                           double* __restrict__ hsep) {
+  const int N = T.N, P = T.P;
+  const size_t K = (size_t)N * N;
+  const size_t m = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (m >= K || P < 2) return;
+  const int ll = (int)(m / N), kk = (int)(m % N);
+  if (ll == 0 || kk == 0) {
+    for (int g = 0; g < P - 1; ++g) hsep[(size_t)g * K + m] = 0.0;
+    return;
+  }
+  const double a = T.red_a[m], b = T.red_b[m];
+  double c = b, y = 0.0, ci = 0.0;
+  for (int g = 0; g < P - 1; ++g) {
+    const double r = zA[(size_t)g * K + m] - zB[(size_t)(g + 1) * K + m];
+    if (g) c = b - a * a * ci;
+    y = g ? r - a * y * ci : r;
+    ci = 1.0 / c;
+    hsep[(size_t)g * K + m] = y;
+  }
+  // backward: h_g = (y_g − a h_{g+1}) / c_g — recompute the pivots forward into registers
+  double hn = y * ci;
+  hsep[(size_t)(P - 2) * K + m] = hn;
+  if (P > 2) {
+    // pivots are needed in reverse: regenerate them (P − 1 ≤ 32 entries) in a local array
+    double cinv[64];
+    double cc = b;
+    for (int g = 0; g < P - 1; ++g) {
+      if (g) cc = b - a * a * cinv[g - 1];
+      cinv[g] = 1.0 / cc;
+    }
+    for (int g = P - 3; g >= 0; --g) {
+      hn = (hsep[(size_t)g * K + m] - a * hn) * cinv[g];
+      hsep[(size_t)g * K + m] = hn;
+    }
+  }
+}
+
+// A7 (3D): ten-point interpolation at the control points
+__global__ void k_interp3(DevTables3 T, const double* __restrict__ phi, const double* __restrict__ dphi,
+                          const double* __restrict__ fz, const double* __restrict__ jg, const double* __restrict__ work,
+                          double* __restrict__ out) {
+  const int e = blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= T.nq) return;
+  const int N = T.N;
+  Jump10 J;
+  load_jump3(T, e, phi, dphi, fz, jg, J);
+  const int c0 = T.st_c[3 * e], c1 = T.st_c[3 * e + 1], c2 = T.st_c[3 * e + 2];
+  const int code = T.st_code[e];
+  const int s0 = (code >> 10) & 1 ? 1 : -1, s1 = (code >> 11) & 1 ? 1 : -1, s2 = (code >> 12) & 1 ? 1 : -1;
+  const int off[10][3] = {{0, 0, 0}, {1, 0, 0}, {-1, 0, 0}, {0, 1, 0}, {0, -1, 0}, {0, 0, 1}, {0, 0, -1},
+                          {s0, s1, 0}, {s0, 0, s2}, {0, s1, s2}};
+  const double zx = T.q_pos[3 * e], zy = T.q_pos[3 * e + 1], zz = T.q_pos[3 * e + 2];
+  double acc = 0.0;
+#pragma unroll
+  for (int p = 0; p < 10; ++p) {
+    const int ni = c0 + off[p][0], nj = c1 + off[p][1], nk = c2 + off[p][2];
+    double v = work[(size_t)(ni - 1) * N * N + (size_t)nj * N + nk];
+    if ((code >> p) & 1) {
+      const double dx = T.lo + ni * T.h - zx, dy = T.lo + nj * T.h - zy, dz = T.lo + nk * T.h - zz;
+      v += J.v + J.g[0] * dx + J.g[1] * dy + J.g[2] * dz + 0.5 * (J.H[0] * dx * dx + J.H[1] * dy * dy + J.H[2] * dz * dz) +
+           J.H[3] * dx * dy + J.H[4] * dx * dz + J.H[5] * dy * dz;
+    }
+    acc = fma(T.st_w[10 * (size_t)e + p], v, acc);
+  }
+  out[e] = acc;
+}
+
+inline int cdiv3(long a, long b) { return (int)((a + b - 1) / b); }
+
+}  // namespace
+
+void launch_lsq3(const DevTables3& T, const double* phi, double* dphi, cudaStream_t s) {
+  ++g_launches;
+  k_lsq3<<<cdiv3(T.nq, 128), 128, 0, s>>>(T, phi, dphi);
+}
+void launch_base3(const DevTables3& T, const double* fgrid, double* work, cudaStream_t s) {
+  ++g_launches;
+  k_base3<<<num_sms() * 8, 256, 0, s>>>(T, fgrid, work);
+}
+void launch_correct3(const DevTables3& T, const double* phi, const double* dphi, const double* fq,
+                     const double* jq_given, double* work, cudaStream_t s) {
+  if (!T.nirr) return;
+  ++g_launches;
+  k_correct3<<<cdiv3(T.nirr, 128), 128, 0, s>>>(T, phi, dphi, fq, jq_given, work);
+}
+void launch_dst_rows3(const DevTables3& T, int mode, double* work, const double* hsep, double scale, double* out,
+                      cudaStream_t s) {
+  const int N = T.N;
+  const size_t sm = (size_t)(N / 2 + 2 + 2 * N + N / 8) * sizeof(double);
+  const int threads = N / 16 < 32 ? 32 : N / 16;
+  const int rows = (N - 1) * N;
+  ++g_launches;
+  if (mode == 0) k_dst_rows3<0><<<rows, threads, sm, s>>>(T, work, hsep, scale, out);
+  else if (mode == 1) k_dst_rows3<1><<<rows, threads, sm, s>>>(T, work, hsep, scale, out);
+  else k_dst_rows3<2><<<rows, threads, sm, s>>>(T, work, hsep, scale, out);
+}
+void launch_transpose3(const DevTables3& T, double* work, cudaStream_t s) {
+  const int t = T.N / 32;
+  dim3 grid(t * (t + 1) / 2, T.N - 1);
+  ++g_launches;
+  k_transpose3<<<grid, dim3(32, 8), 0, s>>>(T.N, work);
+}
+void launch_sweep3(const DevTables3& T, double* work, double* zB, double* zA, cudaStream_t s) {
+  ++g_launches;
+  k_sweep3<<<cdiv3((long)T.N * T.N, 256), 256, 0, s>>>(T, work, zB, zA);
+}
+void launch_reduced3(const DevTables3& T, const double* zB, const double* zA, double* hsep, cudaStream_t s) {
+  if (T.P < 2) return;
+  ++g_launches;
+  k_reduced3<<<cdiv3((long)T.N * T.N, 128), 128, 0, s>>>(T, zB, zA, hsep);
+}
+void launch_interp3(const DevTables3& T, const double* phi, const double* dphi, const double* fz,
+                    const double* jz_given, const double* work, double* out, cudaStream_t s) {
+  ++g_launches;
+  k_interp3<<<cdiv3(T.nq, 128), 128, 0, s>>>(T, phi, dphi, fz, jz_given, work, out);
+}
+
+}  // namespace kfbi

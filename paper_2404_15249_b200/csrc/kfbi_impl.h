@@ -91,6 +91,46 @@ struct Setup {
 
 void build_setup(Setup& S, const kfbi_grid* g, const kfbi_boundary* b, const kfbi_pde* pde);
 
+// Host-side setup products in 3D (control points = intersection nodes, reading R12).
+struct Setup3 {
+  int N = 0, P = 0;
+  double lo = 0, h = 0, kappa = 0;
+  Comp comp{};
+  std::vector<int8_t> side;          // (N+1)^3
+  int nq = 0;                        // intersections = control points, sorted (axis, i, j, k)
+  std::vector<int32_t> q_axis, q_i, q_j, q_k;
+  std::vector<double> q_xi, q_pos, q_n, q_e1, q_e2, q_kab;   // 3 per point (kab: κ11, κ12, κ22)
+  int nirr = 0;                      // irregular nodes sorted (i, j, k)
+  std::vector<int64_t> irr_lin;      // (i−1)·N² + j·N + k in the working array
+  std::vector<int32_t> irr_ijk, irr_ptr, pair_q;
+  std::vector<int8_t> irr_side;
+  std::vector<double> pair_d;
+  std::vector<int32_t> lsq_ptr, lsq_nb;   // LSQ neighbours (CSR)
+  std::vector<double> lsq_G;              // 15 per point: (ÂᵀÂ)⁻¹ upper triangle, Â scaled by 1/h
+  std::vector<int32_t> st_c, st_code;     // stencil centre (3) and sign/exterior code
+  std::vector<double> st_w;               // 10 per point: row 0 of the inverse local system
+  std::vector<int64_t> st_nodes_ij;       // dump
+  std::vector<double> sin_tab, dk, zr, red_a, red_b;   // modes m = ll·N + kk
+};
+void build_setup3(Setup3& S, const kfbi_grid* g, const kfbi_boundary* b, const kfbi_pde* pde);
+
+struct DevTables3 {
+  int N, P, nq, nirr;
+  double lo, h, kappa;
+  const int32_t* q_axis;
+  const double *q_pos, *q_n, *q_e1, *q_e2, *q_kab;
+  const int64_t* irr_lin;
+  const int8_t* irr_side;
+  const int32_t *irr_ptr, *pair_q;
+  const double* pair_d;
+  const int32_t *lsq_ptr, *lsq_nb;
+  const double* lsq_G;
+  const int32_t *st_c, *st_code;
+  const double* st_w;
+  const double *sin_tab, *dk, *zr, *red_a, *red_b;
+  const int8_t* side;
+};
+
 // ---- device views -------------------------------------------------------------------
 struct DevTables {
   int N, P, M, nq, nirr, nsn, nocol, ncomp;

@@ -251,8 +251,9 @@ class KFBI:
 
     def test_interface_solve(self, base_full, jq, jz, want_field=True, stream=None):
         base = self._dev(base_full, self.n_nodes)
-        jq = self._dev(jq, self.nq * 6)
-        jz = self._dev(jz, self.M * 6)
+        ncol = 6 if self.problem.dim == 2 else 10
+        jq = self._dev(jq, self.nq * ncol)
+        jz = self._dev(jz, self.M * ncol)
         v = self.torch.empty(self.n_nodes, dtype=self.torch.float64, device=self.device) if want_field else None
         vp = self.torch.empty(self.M, dtype=self.torch.float64, device=self.device)
         self._check(self.lib.kfbi_test_interface_solve(self.ctx, _ptr(base), _ptr(jq), _ptr(jz), _ptr(v), _ptr(vp),
@@ -261,7 +262,7 @@ class KFBI:
 
     def setup_dump(self, which):
         d = self.problem.dim
-        shape = {0: (self.nirr, d), 1: (self.nq, d + 1), 2: (self.M, 6, d)}[which]
+        shape = {0: (self.nirr, d), 1: (self.nq, d + 1), 2: (self.M, 6 if d == 2 else 10, d)}[which]
         out = np.zeros(int(np.prod(shape)), dtype=np.int64)
         self._check(self.lib.kfbi_test_setup_dump(self.ctx, which, out.ctypes.data_as(C.POINTER(C.c_int64))))
         return out.reshape(shape)

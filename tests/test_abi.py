@@ -55,3 +55,16 @@ def test_setup_errors(lib):
     with pytest.raises(KfbiError) as e:   # Γ within 2h of ∂B (R32)
         KFBI(W.problem("near-box", 2, 64, [W.circle(1.18)], 0.0), workspace=False)
     assert e.value.code == 2
+
+
+@pytest.mark.parametrize("prob", [W.C4(32), W.C5(64)], ids=["ellipsoid32", "torus64"])
+def test_host_setup3d_matches_oracle(lib, prob):
+    from oracle import grid3d
+    k = KFBI(prob, workspace=False)
+    st = grid3d.build(prob)
+    assert k.M == st.M and k.nq == st.M
+    assert np.array_equal(k.setup_dump(0), np.argwhere(st.irregular))
+    assert np.array_equal(k.setup_dump(1), np.stack([st.q_axis, st.q_i, st.q_j, st.q_k], -1))
+    assert np.array_equal(k.setup_dump(2), grid3d.stencil(st))
+    assert np.array_equal(k.node_mask().astype(bool), st.side)
+    np.testing.assert_allclose(k.points("ctrl"), st.q_pos, atol=1e-13 * st.h)

@@ -29,7 +29,7 @@ import numpy as np  # noqa: E402
 
 import workloads as W  # noqa: E402
 
-METRIC = "KFBI solve: grid-pts/s per interface solve (2D Poisson, multiply-connected, 8192^2)"
+METRIC = "KFBI solve: grid-pts/s per interface solve"
 UNIT = "grid-pts/s"
 
 
@@ -95,16 +95,17 @@ def make_inputs(k, prob):
     n = prob.n
     pz, pq = k.points("ctrl"), k.points("isect")
     x = prob.lo + np.arange(n + 1) * prob.h
-    X, Y = np.meshgrid(x, x, indexing="ij")
-    f = lambda a, b: W.f_exact(prob.kappa, a, b)
-    return (W.u_exact(pz[:, 0], pz[:, 1]), f(X, Y).ravel(), f(pq[:, 0], pq[:, 1]), f(pz[:, 0], pz[:, 1]), X, Y)
+    f = lambda *a: W.f_exact(prob.kappa, *a)
+    G = np.meshgrid(*([x] * prob.dim), indexing="ij")
+    return (W.u_exact(*pz.T), f(*G).ravel(), f(*pq.T), f(*pz.T))
 
 
 def cpu_oracle_apply_rate(prob, reps=1):
     """Oracle (as it stands) on the host: one K_D apply of the same workload."""
     from oracle.bie import Oracle2D
+    from oracle.bie3d import Oracle3D
     t0 = time.time()
-    o = Oracle2D(prob)
+    o = Oracle2D(prob) if prob.dim == 2 else Oracle3D(prob)
     t_setup = time.time() - t0
     phi = W.random_density(o.M, 0)
     ts = []
@@ -120,8 +121,9 @@ def run_reference(args, prob):
     if rank != 0:
         return
     from oracle.bie import Oracle2D
+    from oracle.bie3d import Oracle3D
     U = prob.unknowns
-    o = Oracle2D(prob)
+    o = Oracle2D(prob) if prob.dim == 2 else Oracle3D(prob)
     phi = W.random_density(o.M, 0)
     for _ in range(args.warmup):
         o.apply_KD(phi)
@@ -159,7 +161,7 @@ def main():
     import torch
     import torch.distributed as dist
 
-    from paper_2404_15249_b200 import KFBI, launch_count
+    from paper_2404_15249_b200 import KFBI, broadcast_unique_id, launch_count
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -173,8 +175,14 @@ def main():
         if world > 1:
             dist.barrier()
 
-    k = KFBI(prob, device=local)
-    g, fgrid, fq, fz, X, Y = make_inputs(k, prob)
+    # multi-GPU: 2D slabs along x over NCCL when N/512 is divisible by the world size;
+    # otherwise (3D) independent replicas, one per GPU
+    sharded = world > 1 and prob.dim == 2 and prob.n % (512 * world) == 0
+    if sharded:
+        k = KFBI(prob, device=local, world=world, rank=rank, nccl_id=broadcast_unique_id())
+    else:
+        k = KFBI(prob, device=local)
+    g, fgrid, fq, fz = make_inputs(k, prob)
     t = lambda a: torch.tensor(a, dtype=torch.float64, device=dev)
     g_d, fg_d, fq_d, fz_d = t(g), t(fgrid), t(fq), t(fz)
     u_d = torch.empty(k.n_nodes, dtype=torch.float64, device=dev)
@@ -210,7 +218,8 @@ def main():
         t_step = float(tt.item())
     U = prob.unknowns
     n_app = stats.n_applies
-    value = world * U * n_app / t_step
+    copies = 1 if sharded else world          # replicas each solve the whole problem
+    value = copies * U * n_app / t_step
 
     # e2e through the public API with pinned host buffers
     pin = lambda a: torch.tensor(a, dtype=torch.float64).pin_memory()
@@ -262,15 +271,16 @@ def main():
 
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": 1e3 * t_step, "higher_is_better": True, "scaling": "weak",
+        "warmup": args.warmup, "ms_per_step": 1e3 * t_step, "higher_is_better": True,
+        "scaling": "strong" if sharded else "weak",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic (manufactured u*, reading R24)",
         "config": {"workload": prob.name, "grid": prob.n, "unknowns": U, "kappa": prob.kappa, "M": k.M,
                    "intersections": k.nq, "irregular": k.nirr,
-                   "parallelism": "single-gpu" if world == 1 else f"replicas{world}",
-                   "l2": "flushed between timed steps (256 MB write); spectral buffer 537 MB > L2"},
+                   "parallelism": "single-gpu" if world == 1 else (f"slabs{world}-nccl" if sharded else f"replicas{world}"),
+                   "l2": "flushed between timed steps (256 MB write before each step)"},
         "solve_s": t_step, "gmres_iters": stats.iters, "n_applies": n_app, "rel_residual": stats.rel_residual,
         "apply_us": 1e3 * prof["apply"], "apply_grid_pts_per_s": U / (prof["apply"] * 1e-3),
-        "e2e": {"value": world * U * n_app / t_e2e, "unit": UNIT, "h2d_bytes_per_step": h2d,
+        "e2e": {"value": copies * U * n_app / t_e2e, "unit": UNIT, "h2d_bytes_per_step": h2d,
                 "d2h_bytes_per_step": d2h, "solve_s": t_e2e},
         "gpu_launches": launches, "gpu_launches_per_step": launches / args.steps,
         "roofline": roofline,

@@ -116,8 +116,19 @@ const char* kfbi_version(void);
 const char* kfbi_last_error(const kfbi_ctx* ctx);
 const char* kfbi_last_setup_error(void);
 
-/* rank 0 of a multi-GPU run writes a 128-byte NCCL unique id to out128 (host). */
+/* rank 0 of a multi-GPU run writes a 128-byte NCCL unique id to out128 (host); the caller
+ * broadcasts it (e.g. as a torch.uint8[128] tensor over torch.distributed) and passes it in
+ * kfbi_dist.nccl_id on every rank.  Multi-GPU layout: 2D grids
+ * are split along x into `world` slabs of whole level-2 arrowhead segments (512 columns each), so
+ * `world` must divide N/512.  Per apply the ranks exchange the segment end values of the reduced
+ * system (one ncclAllGather) and sum disjoint partial interpolations (one ncclAllReduce); φ, the
+ * outputs and GMRES are replicated.  kfbi_dist.rank = −1 with world > 1 runs all ranks' slabs in
+ * this one context (single-GPU emulation of the partition, collectives done in device memory). */
 kfbi_status kfbi_get_unique_id(void* out128);
+
+/* Slab of `rank` (host): out6 = {first block, end block, first column, last column, first
+ * stencil column index, end stencil column index}; the columns are grid indices i (x). */
+kfbi_status kfbi_slab(const kfbi_ctx* ctx, int32_t rank, int64_t* out6);
 
 /* Procedure 1: grid, control points, node classification, intersections,
  * stencils and per-mode fast-solver tables, on the host.  No device memory is touched
@@ -147,7 +158,9 @@ kfbi_status kfbi_node_mask(const kfbi_ctx* ctx, int8_t* host_mask);
  * Asynchronous, stream-ordered, no state change. */
 kfbi_status kfbi_apply(kfbi_ctx* ctx, const double* d_phi, double* d_out, void* stream);
 
-/* Full Dirichlet BVP solve (Procedures 2-3):
+/* Full Dirichlet BVP solve (Procedures 2-3).  With world > 1 every rank passes the
+ * same replicated g, f_isect, f_ctrl and its (full-size) f_grid; d_u receives the rank's slab
+ * columns (others untouched); d_phi_out is replicated.
  *   d_g        g_D at the control points (M)
  *   d_f_grid   f at the full node grid ((N+1)^d), or NULL for f ≡ 0; values outside Ω
  *              are ignored (zero extension)

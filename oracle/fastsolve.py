@@ -84,3 +84,50 @@ def apply_operator2d(v, h, kappa):
     """(Δ_h − κ) v at the unknowns, v = 0 outside (used by tests)."""
     p = np.pad(v, 1)
     return (p[2:, 1:-1] + p[:-2, 1:-1] + p[1:-1, 2:] + p[1:-1, :-2] - 4.0 * v) / (h * h) - kappa * v
+
+
+def thomas_arrowhead(dk, r, m):
+    """Arrowhead decomposition (ADM) of the per-mode tridiagonal systems over m partitions
+    (P:81-148): the separator of partition k < m is its last unknown (reading R21); blocks S^k are
+    solved independently, z^k = S⁻¹F_s, Z_L = S⁻¹e_first, Z_R = S⁻¹e_last; the separators h
+    solve the Schur system (H − W_L S⁻¹ W_R) h = F_h − W_L S⁻¹ F_s; back-substitution
+    s^k = z^k − Z_L h^{k−1} − Z_R h^k (P:128 with the garble fixed, reading R20), h⁰ = h^m = 0.
+    Mathematically identical to `thomas` (same system); used to pin the partitioned GPU solver."""
+    n, K = r.shape
+    if m == 1:
+        return thomas(dk, r)
+    cuts = [round(n * q / m) for q in range(m + 1)]
+    seps = [cuts[q + 1] - 1 for q in range(m - 1)]            # separator = last unknown of partition q
+    blocks = [(cuts[q], (cuts[q + 1] - 1) if q < m - 1 else cuts[q + 1]) for q in range(m)]
+    z, ZL, ZR = [], [], []
+    for (a, b) in blocks:
+        L = b - a
+        e1 = np.zeros((L, K))
+        e1[0] = 1.0
+        eL = np.zeros((L, K))
+        eL[-1] = 1.0
+        z.append(thomas(dk, r[a:b]))
+        ZL.append(thomas(dk, e1))
+        ZR.append(thomas(dk, eL))
+    # Schur system on the separators: row q couples h_{q−1}, h_q, h_{q+1}
+    ns = m - 1
+    h = np.zeros((ns, K))
+    for k in range(K):
+        A = np.zeros((ns, ns))
+        rhs = np.zeros(ns)
+        for q in range(ns):
+            A[q, q] = dk[k] - ZR[q][-1, k] - ZL[q + 1][0, k]
+            if q > 0:
+                A[q, q - 1] = -ZL[q][-1, k]
+            if q < ns - 1:
+                A[q, q + 1] = -ZR[q + 1][0, k]
+            rhs[q] = r[seps[q], k] - z[q][-1, k] - z[q + 1][0, k]
+        h[:, k] = np.linalg.solve(A, rhs)
+    x = np.empty_like(r)
+    for q, (a, b) in enumerate(blocks):
+        hl = h[q - 1] if q > 0 else 0.0
+        hr = h[q] if q < ns else 0.0
+        x[a:b] = z[q] - ZL[q] * hl - ZR[q] * hr
+        if q < ns:
+            x[seps[q]] = h[q]
+    return x

@@ -5,4 +5,5 @@
     out = k.apply(phi)           # K_D φ at the control points (one interface solve)
     u, phi, stats = k.solve(g, f_grid, f_isect, f_ctrl)
 """
-from .kfbi import KFBI, KfbiError, Stats, load, launch_count, LIB_PATH, EXPORTS  # noqa: F401
+from .kfbi import (KFBI, KfbiError, Stats, load, launch_count, unique_id, broadcast_unique_id,  # noqa: F401
+                   LIB_PATH, EXPORTS)

@@ -28,11 +28,25 @@ def stale() -> bool:
     return any(os.path.getmtime(d) > t for d in deps if os.path.exists(d))
 
 
+def nccl_paths():
+    """Compile and link against the NCCL that torch loads (pip nvidia-nccl), rpath to it."""
+    try:
+        import nvidia.nccl as nn   # noqa: F401
+        root = os.path.dirname(nn.__file__) if getattr(nn, "__file__", None) else list(nn.__path__)[0]
+    except Exception:
+        root = None
+    if root and os.path.exists(os.path.join(root, "include", "nccl.h")):
+        lib = os.path.join(root, "lib")
+        return ["-I" + os.path.join(root, "include"), "-L" + lib, "-l:libnccl.so.2", "-Xlinker", "-rpath=" + lib]
+    return ["-lnccl"]
+
+
 def build(force: bool = False, verbose: bool = False) -> str:
     if not force and not stale():
         return LIB
     os.makedirs(os.path.dirname(LIB), exist_ok=True)
-    cmd = [nvcc()] + NVCC_FLAGS + ["-o", LIB + ".tmp"] + [os.path.join(CSRC, s) for s in SOURCES] + ["-lgomp"]
+    cmd = ([nvcc()] + NVCC_FLAGS + ["-o", LIB + ".tmp"] + [os.path.join(CSRC, s) for s in SOURCES] + ["-lgomp"]
+           + nccl_paths())
     if verbose:
         print(" ".join(cmd), file=sys.stderr)
     subprocess.run(cmd, check=True, cwd=CSRC)

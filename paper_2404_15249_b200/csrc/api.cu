@@ -10,6 +10,8 @@
 #include <string>
 #include <vector>
 
+#include <nccl.h>
+
 #include "kernels.h"
 #include "kfbi_impl.h"
 
@@ -26,10 +28,23 @@ struct CudaError : std::runtime_error {
 inline void ck(cudaError_t e, const char* what) {
   if (e != cudaSuccess) throw CudaError(std::string(what) + ": " + cudaGetErrorString(e));
 }
+struct NcclError : std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
+inline void ckn(ncclResult_t e, const char* what) {
+  if (e != ncclSuccess) throw NcclError(std::string(what) + ": " + ncclGetErrorString(e));
+}
 }  // namespace
 
 struct kfbi_ctx {
   int dim = 2;
+  // multi-GPU: slabs along x = groups of level-2 arrowhead segments.  rank == −1:
+  // all `world` ranks executed by this context on one GPU (emulation, collectives in-device).
+  int world = 1, rank = 0;
+  bool use_nccl = false;
+  ncclUniqueId nccl_id{};
+  ncclComm_t comm = nullptr;
+  double *segbuf = nullptr, *h2 = nullptr, *parts = nullptr;
   Setup S;
   DevTables T{};
   Setup3 S3;
@@ -79,6 +94,8 @@ struct Arena {
     return p;
   }
 };
+
+DevTables slab(const kfbi_ctx* c, int r);
 
 void layout(kfbi_ctx* c, Arena& A) {
   Setup& S = c->S;
@@ -143,6 +160,12 @@ void layout(kfbi_ctx* c, Arena& A) {
   c->hcol = A.take<double>(kMaxRestart + 2);
   c->ycoef = A.take<double>(kMaxRestart + 1);
   c->scal = A.take<double>(8);
+  const size_t nseg = S.P >= 2 * BL2 ? S.P / BL2 : 1;
+  c->segbuf = A.take<double>(nseg * 3 * N);
+  c->h2 = A.take<double>(nseg * N);
+  c->parts = A.take<double>((size_t)std::max(c->world, 1) * M);
+  T.sn_i = A.table(S.sn_i);
+  c->T = slab(c, c->rank >= 0 ? c->rank : 0);
 }
 
 void layout3(kfbi_ctx* c, Arena& A) {
@@ -178,6 +201,37 @@ void layout3(kfbi_ctx* c, Arena& A) {
 
 int nctrl(const kfbi_ctx* c) { return c->dim == 3 ? c->S3.nq : c->S.M; }
 
+// DevTables restricted to the slab of rank r of `world` (full domain when world == 1)
+DevTables slab(const kfbi_ctx* c, int r) {
+  DevTables T = c->T;
+  const Setup& S = c->S;
+  const int world = c->world;
+  T.nseg = S.P >= 2 * BL2 ? S.P / BL2 : 1;
+  T.rank = r;
+  if (world == 1) {
+    T.g_lo = 0; T.g_hi = S.P; T.seg_lo = 0; T.seg_hi = T.nseg;
+    T.col_lo = 1; T.col_hi = S.N - 1; T.o_lo = 0; T.o_hi = (int)S.ocol.size();
+    return T;
+  }
+  T.seg_lo = r * T.nseg / world;
+  T.seg_hi = (r + 1) * T.nseg / world;
+  T.g_lo = T.seg_lo * BL2;
+  T.g_hi = T.seg_hi * BL2;
+  T.col_lo = BL * T.g_lo + 1;
+  T.col_hi = std::min(BL * T.g_hi, S.N - 1);
+  T.o_lo = (int)(std::lower_bound(S.ocol.begin(), S.ocol.end(), T.col_lo) - S.ocol.begin());
+  T.o_hi = (int)(std::upper_bound(S.ocol.begin(), S.ocol.end(), T.col_hi) - S.ocol.begin());
+  return T;
+}
+
+std::vector<int> my_ranks(const kfbi_ctx* c) {
+  std::vector<int> v;
+  if (c->rank >= 0) v.push_back(c->rank);
+  else
+    for (int r = 0; r < c->world; ++r) v.push_back(r);
+  return v;
+}
+
 kfbi_status fail(kfbi_ctx* c, kfbi_status st, const std::string& msg) {
   if (c) c->err = msg;
   return st;
@@ -188,6 +242,7 @@ kfbi_status fail(kfbi_ctx* c, kfbi_status st, const std::string& msg) {
 #define KFBI_CATCH(ctx)                                                \
   }                                                                    \
   catch (const CudaError& e) { return fail(ctx, KFBI_ECUDA, e.what()); } \
+  catch (const NcclError& e) { return fail(ctx, KFBI_ENCCL, e.what()); } \
   catch (const GeomError& e) { return fail(ctx, KFBI_EGEOM, e.what()); } \
   catch (const ArgError& e) { return fail(ctx, KFBI_EINVAL, e.what()); } \
   catch (const std::exception& e) { return fail(ctx, KFBI_EINVAL, e.what()); }
@@ -199,26 +254,68 @@ void need_ws(kfbi_ctx* c) {
 }
 
 // --- one interface solve, sparse output at stencil nodes → V⁺ at control points ----------
+// --- 2D interface solve, possibly distributed over slabs ----------------------------------
+// spectral part: sweep of the owned blocks → reduced (arrowhead) system → h at every separator the
+// owned columns need.  world > 1: level-2 segments = slabs; the segment end values are all-gathered
+// (the only exchange of the tridiagonal solve) and every rank solves the S − 1 slab
+// separators redundantly.
+void spectral2(kfbi_ctx* c, const double* cval, bool dense, cudaStream_t s) {
+  for (int r : my_ranks(c)) launch_sweep(slab(c, r), cval, dense, c->spec, c->zfirst, c->zlast, c->fsep, s);
+  if (c->world == 1) {
+    launch_reduced(c->T, c->zfirst, c->zlast, c->fsep, c->hsep, s);
+    return;
+  }
+  for (int r : my_ranks(c)) launch_red2_local(slab(c, r), c->zfirst, c->fsep, c->hsep, c->segbuf, s);
+  if (c->use_nccl) {
+    const DevTables T = slab(c, c->rank);
+    const size_t cnt = (size_t)(T.seg_hi - T.seg_lo) * 3 * T.N;
+    ckn(ncclAllGather(c->segbuf + (size_t)T.seg_lo * 3 * T.N, c->segbuf, cnt, ncclDouble, c->comm, s), "allgather");
+  }
+  launch_red2_solve(c->T, c->segbuf, c->h2, s);
+  for (int r : my_ranks(c)) launch_red2_fixup(slab(c, r), c->h2, c->hsep, s);
+}
+
+// stencil values of the owned columns → V⁺ (partial sums + all-reduce when distributed)
+void interp2(kfbi_ctx* c, const double* phi, const double* fz, const double* jz, bool holes, double* out,
+             cudaStream_t s) {
+  const int nh = holes ? c->nh : 0;
+  const double* wg = nh ? c->wg : nullptr;
+  for (int r : my_ranks(c)) launch_inverse_sparse(slab(c, r), c->spec, c->hsep, c->vsten, s);
+  if (c->world == 1) {
+    launch_interp(c->T, phi, c->mk, fz, jz, c->vsten, nh, wg, c->ahole, out, s);
+    return;
+  }
+  const int M = c->S.M;
+  if (c->use_nccl) {
+    launch_interp(slab(c, c->rank), phi, c->mk, fz, jz, c->vsten, nh, wg, c->ahole, c->parts, s, true);
+    ckn(ncclAllReduce(c->parts, out, M, ncclDouble, ncclSum, c->comm, s), "allreduce");
+    return;
+  }
+  for (int r : my_ranks(c))
+    launch_interp(slab(c, r), phi, c->mk, fz, jz, c->vsten, nh, wg, c->ahole, c->parts + (size_t)r * M, s, true);
+  launch_sum_parts(M, c->world, c->parts, out, s);
+}
+
+void dst_forward2(kfbi_ctx* c, const double* fgrid, bool mask, const BumpParams& bp, cudaStream_t s) {
+  for (int r : my_ranks(c)) launch_dst_forward(slab(c, r), fgrid, mask, bp, c->spec, s);
+}
+
 void apply_KD2(kfbi_ctx* c, const double* phi, double* out, cudaStream_t s) {
   const DevTables& T = c->T;
   launch_spline(T, phi, c->mk, s);
   launch_correct(T, phi, c->mk, nullptr, nullptr, c->cval, s);
-  launch_sweep(T, c->cval, false, c->spec, c->zfirst, c->zlast, c->fsep, s);
-  launch_reduced(T, c->zfirst, c->zlast, c->fsep, c->hsep, s);
-  launch_inverse_sparse(T, c->spec, c->hsep, c->vsten, s);
+  spectral2(c, c->cval, false, s);
   launch_hole_coeffs(T, c->hole_off, c->hole_M, c->hole_delta, c->nh, phi, c->ahole, s);
-  launch_interp(T, phi, c->mk, nullptr, nullptr, c->vsten, c->nh, c->nh ? c->wg : nullptr, c->ahole, out, s);
+  interp2(c, phi, nullptr, nullptr, true, out, s);
 }
 
 void apply_Y2(kfbi_ctx* c, const double* fgrid, const double* fq, const double* fz, double* out, cudaStream_t s) {
   const DevTables& T = c->T;
   BumpParams none{};
-  launch_dst_forward(T, fgrid, true, none, c->spec, s);
+  dst_forward2(c, fgrid, true, none, s);
   launch_correct(T, nullptr, nullptr, fq, nullptr, c->cval, s);
-  launch_sweep(T, c->cval, true, c->spec, c->zfirst, c->zlast, c->fsep, s);
-  launch_reduced(T, c->zfirst, c->zlast, c->fsep, c->hsep, s);
-  launch_inverse_sparse(T, c->spec, c->hsep, c->vsten, s);
-  launch_interp(T, nullptr, nullptr, fz, nullptr, c->vsten, 0, nullptr, nullptr, out, s);
+  spectral2(c, c->cval, true, s);
+  interp2(c, nullptr, fz, nullptr, false, out, s);
 }
 
 void final_field2(kfbi_ctx* c, const double* phi, const double* fgrid, const double* fq, double* u, cudaStream_t s) {
@@ -227,12 +324,11 @@ void final_field2(kfbi_ctx* c, const double* phi, const double* fgrid, const dou
   bp.a = c->ahole;
   launch_hole_coeffs(T, c->hole_off, c->hole_M, c->hole_delta, c->nh, phi, c->ahole, s);
   const bool dense = fgrid || c->nh;
-  if (dense) launch_dst_forward(T, fgrid, true, bp, c->spec, s);
+  if (dense) dst_forward2(c, fgrid, true, bp, s);
   launch_spline(T, phi, c->mk, s);
   launch_correct(T, phi, c->mk, fq, nullptr, c->cval, s);
-  launch_sweep(T, c->cval, dense, c->spec, c->zfirst, c->zlast, c->fsep, s);
-  launch_reduced(T, c->zfirst, c->zlast, c->fsep, c->hsep, s);
-  launch_inverse_dense(T, c->spec, c->hsep, u, s);
+  spectral2(c, c->cval, dense, s);
+  for (int r : my_ranks(c)) launch_inverse_dense(slab(c, r), c->spec, c->hsep, u, s);   // owned columns
   const size_t W = (size_t)T.N + 1;
   ck(cudaMemsetAsync(u, 0, W * sizeof(double), s), "memset");
   ck(cudaMemsetAsync(u + (size_t)T.N * W, 0, W * sizeof(double), s), "memset");
@@ -305,25 +401,41 @@ const char* kfbi_last_error(const kfbi_ctx* ctx) { return ctx ? ctx->err.c_str()
 const char* kfbi_last_setup_error(void) { return g_setup_err.c_str(); }
 
 kfbi_status kfbi_get_unique_id(void* out128) {
-  (void)out128;
-  g_setup_err = "multi-GPU (NCCL) layer not built in this version";
-  return KFBI_EUNSUPPORTED;
+  if (!out128) return KFBI_EINVAL;
+  ncclUniqueId id;
+  const ncclResult_t r = ncclGetUniqueId(&id);
+  if (r != ncclSuccess) {
+    g_setup_err = std::string("ncclGetUniqueId: ") + ncclGetErrorString(r);
+    return KFBI_ENCCL;
+  }
+  std::memcpy(out128, &id, sizeof(id));
+  return KFBI_OK;
 }
 
 kfbi_status kfbi_setup(const kfbi_grid* grid, const kfbi_boundary* bnd, const kfbi_pde* pde,
                        const kfbi_dist* dist, void* stream, kfbi_ctx** out) {
   if (!out) return KFBI_EINVAL;
   *out = nullptr;
-  if (dist && dist->world > 1) {
-    g_setup_err = "world > 1 not supported in this version";
-    return KFBI_EUNSUPPORTED;
-  }
   auto* c = new kfbi_ctx();
   try {
+    if (dist && dist->world > 1) {
+      c->world = dist->world;
+      c->rank = dist->rank;
+      if (c->rank < -1 || c->rank >= c->world) throw ArgError("bad rank");
+      if (c->rank >= 0 && dist->nccl_id) {
+        c->use_nccl = true;
+        std::memcpy(&c->nccl_id, dist->nccl_id, sizeof(ncclUniqueId));
+      }
+    }
     if (!grid || !bnd || !pde || !bnd->comp) throw ArgError("null descriptor");
     c->dim = grid->dim;
     if (c->dim == 3) build_setup3(c->S3, grid, bnd, pde);
     else build_setup(c->S, grid, bnd, pde);
+    if (c->world > 1) {
+      if (c->dim != 2) throw ArgError("multi-GPU slabs are built for 2D (3D: replicas)");
+      const int nseg = c->S.P >= 2 * BL2 ? c->S.P / BL2 : 1;
+      if (nseg < c->world || nseg % c->world) throw ArgError("world must divide N/512 (slabs = level-2 segments)");
+    }
     c->stream = (cudaStream_t)stream;
     c->device = dist ? dist->device : 0;
     Arena A{nullptr, 0, false};
@@ -351,6 +463,14 @@ kfbi_status kfbi_setup(const kfbi_grid* grid, const kfbi_boundary* bnd, const kf
   return KFBI_OK;
 }
 
+kfbi_status kfbi_slab(const kfbi_ctx* c, int32_t rank, int64_t* out) {
+  if (!c || !out || c->dim != 2 || rank < 0 || rank >= c->world) return KFBI_EINVAL;
+  const DevTables T = slab(c, rank);
+  const int64_t v[6] = {T.g_lo, T.g_hi, T.col_lo, T.col_hi, T.o_lo, T.o_hi};
+  for (int q = 0; q < 6; ++q) out[q] = v[q];
+  return KFBI_OK;
+}
+
 kfbi_status kfbi_workspace_size(const kfbi_ctx* ctx, size_t* bytes) {
   if (!ctx || !bytes) return KFBI_EINVAL;
   *bytes = ctx->ws_need;
@@ -371,15 +491,17 @@ kfbi_status kfbi_set_workspace(kfbi_ctx* c, void* d_ws, size_t bytes) {
   cudaStream_t s = c->stream;
   for (auto& u : A.uploads) ck(cudaMemcpyAsync(u.first, u.second.first, u.second.second, cudaMemcpyHostToDevice, s), "upload");
   if (!c->hcol_host) ck(cudaMallocHost(&c->hcol_host, (kMaxRestart + 2) * sizeof(double)), "cudaMallocHost");
+  if (c->use_nccl) {
+    ck(cudaSetDevice(c->device), "cudaSetDevice");
+    ckn(ncclCommInitRank(&c->comm, c->world, c->nccl_id, c->rank), "ncclCommInitRank");
+  }
   // hole completion fields w_h|Γ (reading R27): plain fast solve of the bump, no jumps
   for (int h = 0; h < c->nh; ++h) {
     BumpParams bp = c->bump;
     bp.a = c->onehot + (size_t)h * c->nh;
-    launch_dst_forward(c->T, nullptr, false, bp, c->spec, s);
-    launch_sweep(c->T, nullptr, true, c->spec, c->zfirst, c->zlast, c->fsep, s);
-    launch_reduced(c->T, c->zfirst, c->zlast, c->fsep, c->hsep, s);
-    launch_inverse_sparse(c->T, c->spec, c->hsep, c->vsten, s);
-    launch_interp(c->T, nullptr, nullptr, nullptr, nullptr, c->vsten, 0, nullptr, nullptr, c->wg + (size_t)h * c->S.M, s);
+    dst_forward2(c, nullptr, false, bp, s);
+    spectral2(c, nullptr, true, s);
+    interp2(c, nullptr, nullptr, nullptr, false, c->wg + (size_t)h * c->S.M, s);
   }
   ck(cudaGetLastError(), "setup kernels");
   ck(cudaStreamSynchronize(s), "setup sync");
@@ -655,6 +777,7 @@ kfbi_status kfbi_launch_count(int64_t* count) {
 
 kfbi_status kfbi_destroy(kfbi_ctx* c) {
   if (!c) return KFBI_OK;
+  if (c->comm) ncclCommDestroy(c->comm);
   if (c->hcol_host) cudaFreeHost(c->hcol_host);
   delete c;
   return KFBI_OK;

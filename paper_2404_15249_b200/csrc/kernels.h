@@ -42,7 +42,16 @@ void launch_hole_coeffs(const DevTables& T, const int* hole_off, const int* hole
 //   NULL; jz_given (M×6) test path; wg (nh×M) + a (nh) hole completion or NULL.
 void launch_interp(const DevTables& T, const double* phi, const double* mk, const double* fz,
                    const double* jz_given, const double* vsten, int nh, const double* wg, const double* a,
-                   double* out, cudaStream_t s);
+                   double* out, cudaStream_t s, bool partial = false);
+// multi-GPU split of the level-2 reduced solve (segments = slabs): local segment solves for the
+// owned segments [seg_lo, seg_hi) → seg buffer [seg][3][N] (first, last, separator rhs); level-2 solve
+// for all segments (after the all-gather) → h2 [seg][N]; fix-up of the owned segments' separators
+void launch_red2_local(const DevTables& T, const double* zB, const double* zA, double* hsep, double* segbuf,
+                       cudaStream_t s);
+void launch_red2_solve(const DevTables& T, const double* segbuf, double* h2, cudaStream_t s);
+void launch_red2_fixup(const DevTables& T, const double* h2, double* hsep, cudaStream_t s);
+// out[m] = Σ_{r < nparts} parts[r·n + m] in rank order (single-process emulation of the all-reduce)
+void launch_sum_parts(int n, int nparts, const double* parts, double* out, cudaStream_t s);
 
 // A8: GMRES vector kernels (deterministic fixed-grid reductions)
 constexpr int kRedBlocks = 64;

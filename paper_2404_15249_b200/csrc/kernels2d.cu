@@ -198,7 +198,7 @@ __global__ void __launch_bounds__(kSweepThreads, 1) k_sweep(DevTables T, const d
   }
   const double h2 = T.h * T.h;
   double* R1 = R + threadIdx.x;
-  for (int g = blockIdx.x / nch; g < P; g += G) {
+  for (int g = T.g_lo + blockIdx.x / nch; g < T.g_hi; g += G) {
     const int c0 = BL * g + 1;
     const int e0 = T.col_ptr[c0];
     const int ncol = g < P - 1 ? BL : LB;   // block columns + separator column
@@ -403,6 +403,91 @@ __global__ void __launch_bounds__(512) k_reduced2(DevTables T, const double* __r
   if (sg < S - 1) hsep[(size_t)(gbase + LB2) * N + k] = s_h2[sg][lane];
 }
 
+// ---- multi-GPU split of k_reduced2: the level-2 segments are the slabs' separator groups ----
+// (1) owned segments: local level-2 block solve, z kept in hsep, (first, last, rhs_sep) → segbuf
+__global__ void k_red2_local(DevTables T, const double* __restrict__ zB, const double* __restrict__ zA,
+                             double* __restrict__ hsep, double* __restrict__ segbuf) {
+  const int N = T.N, S = T.nseg;
+  const int k = blockIdx.x * blockDim.x + threadIdx.x + 1;
+  const int sg = T.seg_lo + blockIdx.y;
+  if (k >= N) return;
+  const double a = T.red_a[k];
+  const int gbase = sg * BL2;
+  double z[LB2];
+#pragma unroll
+  for (int p = 0; p < LB2; ++p) {
+    const int g = gbase + p;
+    const double r = zA[(size_t)g * N + k] - zB[(size_t)(g + 1) * N + k];
+    z[p] = p ? fma(-a * z[p - 1], T.rinv2[(size_t)(p - 1) * N + k], r) : r;
+  }
+  z[LB2 - 1] *= T.rinv2[(size_t)(LB2 - 1) * N + k];
+#pragma unroll
+  for (int p = LB2 - 2; p >= 0; --p) z[p] = (z[p] - a * z[p + 1]) * T.rinv2[(size_t)p * N + k];
+#pragma unroll
+  for (int p = 0; p < LB2; ++p) hsep[(size_t)(gbase + p) * N + k] = z[p];
+  double* sb = segbuf + (size_t)sg * 3 * N;
+  sb[k] = z[0];
+  sb[N + k] = z[LB2 - 1];
+  if (sg < S - 1) {
+    const int gs = gbase + LB2;
+    sb[2 * N + k] = zA[(size_t)gs * N + k] - zB[(size_t)(gs + 1) * N + k];
+  }
+}
+
+// (2) every rank: the level-2 tridiagonal system of the S − 1 slab separators per mode
+__global__ void k_red2_solve(DevTables T, const double* __restrict__ segbuf, double* __restrict__ h2) {
+  const int N = T.N, S = T.nseg;
+  const int k = blockIdx.x * blockDim.x + threadIdx.x + 1;
+  if (k >= N || S < 2) return;
+  const double a = T.red_a[k], A2 = T.red2_a[k], B2 = T.red2_b[k];
+  double c = B2, yprev = 0.0, ciprev = 0.0;
+  for (int q = 0; q < S - 1; ++q) {
+    const double* sq = segbuf + (size_t)q * 3 * N;
+    const double* sn = segbuf + (size_t)(q + 1) * 3 * N;
+    const double r = sq[2 * N + k] - a * sq[N + k] - a * sn[k];
+    if (q) c = B2 - A2 * A2 * ciprev;
+    const double ci = 1.0 / c;
+    const double y = q ? r - A2 * yprev * ciprev : r;
+    h2[(size_t)q * N + k] = y;
+    yprev = y;
+    ciprev = ci;
+  }
+  // backward needs the pivots again: recompute them (S − 1 ≤ 15 per mode)
+  double ci_all[16];
+  c = B2;
+  for (int q = 0; q < S - 1; ++q) {
+    if (q) c = B2 - A2 * A2 * ci_all[q - 1];
+    ci_all[q] = 1.0 / c;
+  }
+  double hn = h2[(size_t)(S - 2) * N + k] * ci_all[S - 2];
+  h2[(size_t)(S - 2) * N + k] = hn;
+  for (int q = S - 3; q >= 0; --q) {
+    hn = (h2[(size_t)q * N + k] - A2 * hn) * ci_all[q];
+    h2[(size_t)q * N + k] = hn;
+  }
+}
+
+// (3) owned segments: z − a h2_{σ−1} Z2_L − a h2_σ Z2_R, and the slab separators on both sides
+__global__ void k_red2_fixup(DevTables T, const double* __restrict__ h2, double* __restrict__ hsep) {
+  const int N = T.N, S = T.nseg;
+  const int k = blockIdx.x * blockDim.x + threadIdx.x + 1;
+  const int sg = T.seg_lo + blockIdx.y;
+  if (k >= N) return;
+  const double a = T.red_a[k];
+  const int gbase = sg * BL2;
+  const double hl = sg > 0 ? a * h2[(size_t)(sg - 1) * N + k] : 0.0;
+  const double hr = sg < S - 1 ? a * h2[(size_t)sg * N + k] : 0.0;
+#pragma unroll
+  for (int p = 0; p < LB2; ++p) {
+    double x = hsep[(size_t)(gbase + p) * N + k];
+    x = fma(-hl, T.z2r[(size_t)(LB2 - 1 - p) * N + k], x);
+    x = fma(-hr, T.z2r[(size_t)p * N + k], x);
+    hsep[(size_t)(gbase + p) * N + k] = x;
+  }
+  if (sg < S - 1) hsep[(size_t)(gbase + LB2) * N + k] = h2[(size_t)sg * N + k];
+  if (sg > 0) hsep[(size_t)(gbase - 1) * N + k] = h2[(size_t)(sg - 1) * N + k];
+}
+
 // value of v̂ at column i, mode k: separator → h; block row → z − h_{g−1} Z_L − h_g Z_R
 __device__ __forceinline__ double fixup(const DevTables& T, const double* __restrict__ spec,
                                         const double* __restrict__ hsep, int i, int k) {
@@ -472,7 +557,7 @@ __global__ void __launch_bounds__(256, 2) k_inv_sparse(DevTables T, const double
     const double v = tab[idx + (idx >> 4)];
     return (r & N) ? -v : v;
   };
-  const int b = blockIdx.x;
+  const int b = T.o_lo + blockIdx.x;
   const int i = T.ocol[b];
   const int u0 = T.ocol_ptr[b], u1 = T.ocol_ptr[b + 1];
   for (int u = u0 + threadIdx.x; u < u1; u += B) s_rows[u - u0] = T.sn_j[u];
@@ -593,7 +678,7 @@ __global__ void __launch_bounds__(256, 2) k_inv_sparse(DevTables T, const double
 __global__ void k_interp(DevTables T, const double* __restrict__ phi, const double* __restrict__ mk,
                          const double* __restrict__ fz, const double* __restrict__ jzg,
                          const double* __restrict__ vsten, int nh, const double* __restrict__ wg,
-                         const double* __restrict__ ahole, double* __restrict__ out) {
+                         const double* __restrict__ ahole, double* __restrict__ out, int partial) {
   const int m = blockIdx.x * blockDim.x + threadIdx.x;
   if (m >= T.M) return;
   Jump6 J;
@@ -616,14 +701,20 @@ __global__ void k_interp(DevTables T, const double* __restrict__ phi, const doub
 #pragma unroll
   for (int p = 0; p < 6; ++p) {
     const int idx = m * 6 + p;
-    double v = vsten[T.st_node[idx]];
+    const int sn = T.st_node[idx];
+    if (partial) {   // multi-GPU: only stencil nodes in the owned columns contribute (partial sum)
+      const int col = T.sn_i[sn];
+      if (col < T.col_lo || col > T.col_hi) continue;
+    }
+    double v = vsten[sn];
     if (T.st_ext[idx]) {   // exterior node: shift by the jump Taylor polynomial
       const double dx = T.st_dx[idx], dy = T.st_dy[idx];
       v += J.v + J.vx * dx + J.vy * dy + 0.5 * J.vxx * dx * dx + J.vxy * dx * dy + 0.5 * J.vyy * dy * dy;
     }
     acc = fma(T.st_w[idx], v, acc);
   }
-  for (int hh = 0; hh < nh; ++hh) acc = fma(ahole[hh], wg[(size_t)hh * T.M + m], acc);
+  if (!partial || T.rank == 0)
+    for (int hh = 0; hh < nh; ++hh) acc = fma(ahole[hh], wg[(size_t)hh * T.M + m], acc);
   out[m] = acc;
 }
 
@@ -782,7 +873,7 @@ __global__ void __launch_bounds__(512) k_dst_dense(DevTables T, const double* __
   double2* z = reinterpret_cast<double2*>(sm + half + 2);      // N (+N/16 pad) complex
   double* f = reinterpret_cast<double*>(z) + N / 8 - N;        // f_j at f[N + j]: upper N doubles of z
   for (int r = threadIdx.x; r <= half; r += blockDim.x) s_sin[r] = T.sin_tab[r];
-  const int i = blockIdx.x + 1;
+  const int i = blockIdx.x + T.col_lo;
   // 1. load f_j (j = 0..N−1, f_0 = 0) into the upper half of the z buffer (doubles N..2N−1)
   for (int j = threadIdx.x; j < N; j += blockDim.x) {
     double v = 0.0;
@@ -982,14 +1073,14 @@ void launch_dst_forward(const DevTables& T, const double* fgrid, bool mask, cons
     cudaFuncSetAttribute(k_dst_dense<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     attr = true;
   }
-  { ++g_launches; k_dst_dense<0><<<T.N - 1, dense_threads(T.N), sm, s>>>(T, fgrid, mask ? 1 : 0, bp, nullptr, spec); }
+  { ++g_launches; k_dst_dense<0><<<T.col_hi - T.col_lo + 1, dense_threads(T.N), sm, s>>>(T, fgrid, mask ? 1 : 0, bp, nullptr, spec); }
 }
 
 void launch_inverse_dense(const DevTables& T, const double* spec, const double* hsep, double* vgrid,
                           cudaStream_t s) {
   const size_t sm = dense_smem(T.N);
   BumpParams bp{};
-  { ++g_launches; k_dst_dense<1><<<T.N - 1, dense_threads(T.N), sm, s>>>(T, spec, 0, bp, hsep, vgrid); }
+  { ++g_launches; k_dst_dense<1><<<T.col_hi - T.col_lo + 1, dense_threads(T.N), sm, s>>>(T, spec, 0, bp, hsep, vgrid); }
 }
 
 void launch_sweep(const DevTables& T, const double* cval, bool dense, double* spec, double* zfirst, double* zlast,
@@ -1009,7 +1100,7 @@ void launch_sweep(const DevTables& T, const double* cval, bool dense, double* sp
   if (per < 1) per = 1;
   int G = num_sms() * per / nch;
   if (G < 1) G = 1;
-  if (G > T.P) G = T.P;
+  if (G > T.g_hi - T.g_lo) G = T.g_hi - T.g_lo;
   const int grid = nch * G;
   if (dense)
     { ++g_launches; k_sweep<true><<<grid, kSweepThreads, sm, s>>>(T, cval, spec, zfirst, fsep); }
@@ -1031,7 +1122,8 @@ void launch_reduced(const DevTables& T, const double* zfirst, const double* zlas
 
 void launch_inverse_sparse(const DevTables& T, const double* spec, const double* hsep, double* vsten,
                            cudaStream_t s) {
-  if (T.nocol == 0) return;
+  const int ncols = T.o_hi - T.o_lo;
+  if (ncols <= 0) return;
   const int quarter = T.N / 4;
   const int threads = quarter < 32 ? 32 : (quarter < 256 ? quarter : 256);
   const int qpt = (quarter + threads - 1) / threads;
@@ -1045,12 +1137,42 @@ void launch_inverse_sparse(const DevTables& T, const double* spec, const double*
     attr = true;
   }
   switch (qpt) {
-    case 1: ++g_launches; k_inv_sparse<1><<<T.nocol, threads, sm, s>>>(T, spec, hsep, vsten); break;
-    case 2: ++g_launches; k_inv_sparse<2><<<T.nocol, threads, sm, s>>>(T, spec, hsep, vsten); break;
-    case 4: ++g_launches; k_inv_sparse<4><<<T.nocol, threads, sm, s>>>(T, spec, hsep, vsten); break;
-    case 8: ++g_launches; k_inv_sparse<8><<<T.nocol, threads, sm, s>>>(T, spec, hsep, vsten); break;
+    case 1: ++g_launches; k_inv_sparse<1><<<ncols, threads, sm, s>>>(T, spec, hsep, vsten); break;
+    case 2: ++g_launches; k_inv_sparse<2><<<ncols, threads, sm, s>>>(T, spec, hsep, vsten); break;
+    case 4: ++g_launches; k_inv_sparse<4><<<ncols, threads, sm, s>>>(T, spec, hsep, vsten); break;
+    case 8: ++g_launches; k_inv_sparse<8><<<ncols, threads, sm, s>>>(T, spec, hsep, vsten); break;
     default: break;
   }
+}
+
+void launch_red2_local(const DevTables& T, const double* zB, const double* zA, double* hsep, double* segbuf,
+                       cudaStream_t s) {
+  dim3 grid(cdiv(T.N - 1, 128), T.seg_hi - T.seg_lo);
+  ++g_launches;
+  k_red2_local<<<grid, 128, 0, s>>>(T, zB, zA, hsep, segbuf);
+}
+void launch_red2_solve(const DevTables& T, const double* segbuf, double* h2, cudaStream_t s) {
+  ++g_launches;
+  k_red2_solve<<<cdiv(T.N - 1, 128), 128, 0, s>>>(T, segbuf, h2);
+}
+void launch_red2_fixup(const DevTables& T, const double* h2, double* hsep, cudaStream_t s) {
+  dim3 grid(cdiv(T.N - 1, 128), T.seg_hi - T.seg_lo);
+  ++g_launches;
+  k_red2_fixup<<<grid, 128, 0, s>>>(T, h2, hsep);
+}
+
+namespace {
+__global__ void k_sum_parts(int n, int nparts, const double* __restrict__ parts, double* __restrict__ out) {
+  for (int m = blockIdx.x * blockDim.x + threadIdx.x; m < n; m += gridDim.x * blockDim.x) {
+    double s = 0.0;
+    for (int r = 0; r < nparts; ++r) s += parts[(size_t)r * n + m];
+    out[m] = s;
+  }
+}
+}  // namespace
+void launch_sum_parts(int n, int nparts, const double* parts, double* out, cudaStream_t s) {
+  ++g_launches;
+  k_sum_parts<<<cdiv(n, 256), 256, 0, s>>>(n, nparts, parts, out);
 }
 
 void launch_hole_coeffs(const DevTables& T, const int* hole_off, const int* hole_M, const double* hole_delta, int nh,
@@ -1061,8 +1183,9 @@ void launch_hole_coeffs(const DevTables& T, const int* hole_off, const int* hole
 }
 
 void launch_interp(const DevTables& T, const double* phi, const double* mk, const double* fz, const double* jz_given,
-                   const double* vsten, int nh, const double* wg, const double* a, double* out, cudaStream_t s) {
-  { ++g_launches; k_interp<<<cdiv(T.M, 128), 128, 0, s>>>(T, phi, mk, fz, jz_given, vsten, wg ? nh : 0, wg, a, out); }
+                   const double* vsten, int nh, const double* wg, const double* a, double* out, cudaStream_t s,
+                   bool partial) {
+  { ++g_launches; k_interp<<<cdiv(T.M, 128), 128, 0, s>>>(T, phi, mk, fz, jz_given, vsten, wg ? nh : 0, wg, a, out, partial ? 1 : 0); }
 }
 
 void launch_mgs_step(int n, double* w, const double* Vprev, const double* Vcur, const double* partial_prev,

@@ -157,6 +157,10 @@ struct DevTables {
   const double *rinv2, *z2r, *red2_a, *red2_b;
   int maxe;
   const int8_t* side;
+  const int32_t* sn_i;
+  // slab of the executing rank (multi-GPU): blocks [g_lo, g_hi), level-2 segments
+  // [seg_lo, seg_hi) of nseg, owned columns [col_lo, col_hi], owned stencil columns [o_lo, o_hi)
+  int g_lo, g_hi, seg_lo, seg_hi, nseg, col_lo, col_hi, o_lo, o_hi, rank;
 };
 
 }  // namespace kfbi

@@ -21,7 +21,8 @@ _NAMES = {0: "OK", 1: "EINVAL", 2: "EGEOM", 3: "ENOCONV", 4: "ECUDA", 5: "ENCCL"
 EXPORTS = ["kfbi_version", "kfbi_last_error", "kfbi_last_setup_error", "kfbi_get_unique_id", "kfbi_setup",
            "kfbi_workspace_size", "kfbi_set_workspace", "kfbi_sizes", "kfbi_points", "kfbi_node_mask",
            "kfbi_apply", "kfbi_solve", "kfbi_apply_model", "kfbi_destroy", "kfbi_test_fast_solve",
-           "kfbi_test_interface_solve", "kfbi_test_setup_dump", "kfbi_profile_apply", "kfbi_launch_count"]
+           "kfbi_test_interface_solve", "kfbi_test_setup_dump", "kfbi_profile_apply", "kfbi_launch_count",
+           "kfbi_slab"]
 
 
 class KfbiError(RuntimeError):
@@ -92,6 +93,7 @@ def load(path: str = LIB_PATH):
     lib.kfbi_test_setup_dump.argtypes = [vp, i32, i64p]
     lib.kfbi_profile_apply.argtypes = [vp, vp, vp, i32, dp, vp]
     lib.kfbi_launch_count.argtypes = [i64p]
+    lib.kfbi_slab.argtypes = [vp, i32, i64p]
     for name in EXPORTS:
         getattr(lib, name).restype = C.c_char_p if name in ("kfbi_version", "kfbi_last_error",
                                                             "kfbi_last_setup_error") else C.c_int32
@@ -101,6 +103,32 @@ def load(path: str = LIB_PATH):
 
 def _ptr(t):
     return None if t is None else C.c_void_p(t.data_ptr())
+
+
+def unique_id() -> bytes:
+    """128-byte NCCL unique id (rank 0 of a multi-GPU run)."""
+    buf = (C.c_uint8 * 128)()
+    lib = load()
+    st = lib.kfbi_get_unique_id(buf)
+    if st != OK:
+        raise KfbiError(st, lib.kfbi_last_setup_error().decode())
+    return bytes(buf)
+
+
+def broadcast_unique_id(group=None) -> bytes:
+    """Rank 0 creates the NCCL id; torch.distributed broadcasts it as a uint8[128] tensor."""
+    import torch
+    import torch.distributed as dist
+    t = torch.zeros(128, dtype=torch.uint8)
+    if dist.get_rank(group) == 0:
+        t.copy_(torch.frombuffer(bytearray(unique_id()), dtype=torch.uint8))
+    if dist.get_backend(group) == "nccl":
+        d = t.cuda()
+        dist.broadcast(d, 0, group=group)
+        t = d.cpu()
+    else:
+        dist.broadcast(t, 0, group=group)
+    return bytes(t.tolist())
 
 
 def launch_count() -> int:
@@ -123,7 +151,10 @@ class KFBI:
     """One context per (problem, device).  `problem` is any object with dim, n, lo, hi,
     kappa and comps (each with kind, role, center, p, n_ctrl) — e.g. workloads.Problem."""
 
-    def __init__(self, problem, device: int = 0, stream=None, workspace: bool = True):
+    def __init__(self, problem, device: int = 0, stream=None, workspace: bool = True, world: int = 1,
+                 rank: int = 0, nccl_id: bytes = None):
+        """world > 1: slab `rank` of a multi-GPU run (nccl_id from broadcast_unique_id), or
+        rank = −1 to run all slabs in this process (single-GPU emulation of the partition)."""
         import torch
         self.torch = torch
         self.lib = load()
@@ -140,7 +171,9 @@ class KFBI:
         self._comps = comps
         b = Boundary(len(problem.comps), comps)
         pde = Pde(problem.kappa, 0)
-        dist = Dist(1, 0, device, None)
+        self._nccl = (C.c_uint8 * 128).from_buffer_copy(nccl_id) if nccl_id is not None else None
+        dist = Dist(world, rank, device, C.cast(self._nccl, C.c_void_p) if self._nccl is not None else None)
+        self.world, self.rank = world, rank
         ctx = C.c_void_p()
         st = self.lib.kfbi_setup(C.byref(g), C.byref(b), C.byref(pde), C.byref(dist), None, C.byref(ctx))
         if st != OK:
@@ -226,6 +259,11 @@ class KFBI:
             self._check(code)
         stats = Stats(st.iters, st.restarts, st.n_applies, bool(st.converged), st.rel_residual, st.t_solve_s)
         return u.view((self.n + 1,) * self.problem.dim), phi, stats
+
+    def slab(self, rank=None):
+        out = (C.c_int64 * 6)()
+        self._check(self.lib.kfbi_slab(self.ctx, self.rank if rank is None else rank, out))
+        return dict(zip(["g_lo", "g_hi", "col_lo", "col_hi", "o_lo", "o_hi"], list(out)))
 
     def apply_model(self):
         a, b, c = C.c_double(), C.c_double(), C.c_double()

@@ -174,3 +174,39 @@ def test_solve_second_order_on_gpu():
         errs.append(np.sqrt(np.mean(e * e)))
     orders = np.log2(np.array(errs[:-1]) / np.array(errs[1:]))
     assert np.all(orders > 1.6) and np.all(orders < 2.6), orders
+
+
+# ------------------------------------------------------------------ multi-GPU partition (emulated)
+@pytest.mark.parametrize("n,world", [(2048, 2), (2048, 4), (4096, 8)])
+def test_partitioned_apply_matches_single(n, world):
+    """All `world` slabs in one context (rank = −1): the arrowhead split across slabs, the level-2
+    slab-separator solve and the disjoint partial interpolation sums reproduce world = 1."""
+    prob = W.C3(n)
+    k1 = gpu(prob)
+    kw = KFBI(prob, world=world, rank=-1)
+    for seed in (0, 1):
+        phi = W.random_density(k1.M, seed)
+        a = k1.apply(phi).cpu().numpy()
+        b = kw.apply(phi).cpu().numpy()
+        assert rel(b, a) < 1e-12
+    if n == 2048:
+        o = oracle(prob)
+        phi = W.random_density(o.M, 2)
+        assert rel(kw.apply(phi).cpu().numpy(), o.apply_KD(phi)) < 1e-10
+
+
+def test_partitioned_solve_matches_oracle():
+    prob = W.C3(2048)
+    o = oracle(prob)
+    kw = KFBI(prob, world=4, rank=-1)
+    n = prob.n
+    f = lambda x, y: W.f_exact(prob.kappa, x, y)
+    zx, zy = o.ctrl_points()
+    u_ref, phi_ref, s_ref = o.solve(W.u_exact(zx, zy), f)
+    pz, pq = kw.points("ctrl"), kw.points("isect")
+    x = prob.lo + np.arange(n + 1) * prob.h
+    X, Y = np.meshgrid(x, x, indexing="ij")
+    u, phi, s = kw.solve(W.u_exact(pz[:, 0], pz[:, 1]), f(X, Y), f(pq[:, 0], pq[:, 1]), f(pz[:, 0], pz[:, 1]))
+    m = o.st.side
+    assert s.converged and abs(s.iters - s_ref.iters) <= 1
+    assert rel(u.cpu().numpy()[m], u_ref[m]) < 1e-8

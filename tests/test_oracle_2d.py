@@ -397,3 +397,15 @@ def test_constant_solutions():
     u, phi, s = o.solve(np.ones(o.M), lambda x, y: -np.ones_like(x), tol=1e-12)
     assert np.abs(u[o.st.side] - 1).max() < 1e-9
     np.testing.assert_allclose(phi, 1.0, atol=1e-9)
+
+
+@pytest.mark.parametrize("m", [1, 2, 4, 8])
+def test_arrowhead_partitions_equal_thomas(m):
+    """ADM over m partitions reproduces the plain Thomas solution."""
+    n, K = 127, 5
+    dk = -np.array([2.0001, 2.05, 2.5, 3.0, 6.0])
+    r = np.random.default_rng(m).uniform(-1, 1, (n, K))
+    np.testing.assert_allclose(fastsolve.thomas_arrowhead(dk, r, m), fastsolve.thomas(dk, r), atol=1e-11)
+    gold = json.load(open(os.path.join(GOLD, "thomas_tridiag.json")))
+    u = fastsolve.thomas_arrowhead(np.array([-2.0]), -np.array(gold["f"], float)[:, None], 2)[:, 0]
+    np.testing.assert_allclose(u, gold["u"], atol=1e-14)

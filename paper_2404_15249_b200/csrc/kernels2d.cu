@@ -147,26 +147,31 @@ __global__ void k_correct(DevTables T, const double* __restrict__ phi, const dou
 // Outputs: z at the block rows, B[g] = z_g[1], A[g] = h² f̂_sep,g − z_g[L] (reduced-system
 // right-hand side pieces).
 constexpr int kSweepThreads = 512;
-constexpr int kRotSteps = 8;                          // pairs per phase-1 item (t = base + 64 s)
-constexpr int kRotStride = kSweepThreads / kRotSteps;  // 64
-// Persistent CTAs, each owning a fixed chunk of B = 512 mode pairs (k, N−k) (pair slot t ↔ k = t,
-// slot 0 ↔ mode N/2) and iterating over blocks g of BL−1 columns (+ the separator column).
-// Phase 1 (DST of the staged sparse corrections, A4): item (column c, pg) covers the 8 pairs
-// t = t0 + pg + 64 s; for a correction (j, c) the sines sin(πjt/N) along s follow by rotation with
-// the per-entry step e^{iπ·64j/N} (staged with the entry), so one table lookup pair serves 8 pairs and
-// sin(πj(N−k)/N) = (−1)^{j+1} sin(πjk/N) serves the partner mode: odd and even rows are summed
-// separately into R[2c + class][slot].  Phase 2 (A5): local Thomas per mode with pivots in registers
-// for the CTA's lifetime; writes z (block rows), B[g] = z_g[1], A[g] = h² f̂_sep,g − z_g[L].
+constexpr int kQuads = kSweepThreads / 2;   // 256 quads {t, N−t, N/2−t, N/2+t} per CTA chunk
+constexpr int kRotSteps = 8;                 // quads per phase-1 item (t = base + 32 s)
+constexpr int kRotStride = kQuads / kRotSteps;  // 32
+// Persistent CTAs, each owning a fixed chunk of 256 quads of sine modes {t, N−t, N/2−t, N/2+t}
+// (spectral positions 4t..4t+3, see mode_position) and iterating over blocks g of BL−1 columns
+// (+ the separator column).  Phase 1 (A4, DST of the staged sparse corrections): with
+// s, c = sin, cos(πjt/N), sin(πj(N−t)/N) = (−1)^{j+1} s and sin(πj(N/2 ± t)/N) = sin(πj/2) c ±
+// cos(πj/2) s, so per correction (j, c_j) one rotation step serves the whole quad:
+//   odd j:  A_o += c_j s,   B_o += c_j sin(πj/2) c        even j: A_e += c_j s,  B_e += c_j cos(πj/2) s
+//   r_t = A_o + A_e, r_{N−t} = A_o − A_e, r_{N/2−t} = B_o − B_e, r_{N/2+t} = B_o + B_e.
+// An item covers 8 quads t = t0 + qg + 32 s, the sines along s generated by rotation with the
+// per-entry step e^{iπ·32j/N}.  Phase 2 (A5): thread τ owns positions (4q + 2w, 4q + 2w + 1),
+// q = τ/2, w = τ mod 2; local Thomas per mode, pivots in registers for the CTA's lifetime; writes
+// z (block rows), B[g] = z_g[1], A[g] = h² f̂_sep,g − z_g[L].
 template <bool DENSE>
 __global__ void __launch_bounds__(kSweepThreads, 1) k_sweep(DevTables T, const double* __restrict__ cval, double* spec,
                                                            double* __restrict__ zB, double* __restrict__ zA) {
   extern __shared__ double sm[];
-  const int N = T.N, half = N >> 1, P = T.P, m2 = 2 * N - 1, B = kSweepThreads;
+  const int N = T.N, half = N >> 1, quarter = N >> 2, m2 = 2 * N - 1, B = kSweepThreads;
   double* tab = sm;                                          // sin(πr/N), r ∈ [0, N), at r + r/16
   const int tabn = N + (N >> 4) + 2;
-  double* R = sm + tabn;                                     // [2·BL][B]
-  double4* ent = reinterpret_cast<double4*>(R + (size_t)BL * 2 * B);   // (c, j, cos Δ, sin Δ)
-  int* s_cnt = reinterpret_cast<int*>(ent + T.maxe);         // per-column [start, mid, end) offsets
+  double* R = sm + tabn;                                     // [4·BL sums][256 quads]
+  double4* ent = reinterpret_cast<double4*>(R + (size_t)BL * 4 * kQuads);   // (c, j, cos Δ, sin Δ)
+  double* ent2 = reinterpret_cast<double*>(ent + T.maxe);    // c·sin(πj/2) (odd j) or c·cos(πj/2) (even j)
+  int* s_cnt = reinterpret_cast<int*>(ent2 + T.maxe);        // per-column [start, mid, end)
   for (int r = threadIdx.x; r < N; r += B) tab[r + (r >> 4)] = sin_lookup(T.sin_tab, r, N);
   const int lgN = 31 - __clz(N);
   auto sinr = [&](int r) {   // sin(πr/N), r ∈ [0, 2N)
@@ -174,17 +179,16 @@ __global__ void __launch_bounds__(kSweepThreads, 1) k_sweep(DevTables T, const d
     const double v = tab[idx + (idx >> 4)];
     return __hiloint2double(__double2hiint(v) ^ ((r >> lgN) << 31), __double2loint(v));
   };
-  const int nch = (half + B - 1) / B;
+  const int nch = (quarter + kQuads - 1) / kQuads;
   const int G = gridDim.x / nch;
   const int ch = blockIdx.x % nch;
-  const int t0 = ch * B;
-  const int t = t0 + threadIdx.x;
-  const bool active = t < half;
-  const int k1 = t == 0 ? half : (active ? t : 1);
-  const int k2 = N - k1;
+  const int q0 = ch * kQuads;
+  const int qq = q0 + (threadIdx.x >> 1), w = threadIdx.x & 1;
+  const bool active = qq < quarter;
+  const int p1 = active ? 4 * qq + 2 * w : 1, p2 = p1 + 1;   // spectral positions of this thread
   double ic1[LB], ic2[LB];   // 1/c_p for both modes, fixed for the CTA lifetime
   {
-    const double d1 = T.dk[k1], d2 = T.dk[k2];
+    const double d1 = T.dk[p1], d2 = T.dk[p2];
     double c1 = d1, c2 = d2;
 #pragma unroll
     for (int p = 0; p < LB; ++p) {
@@ -197,18 +201,22 @@ __global__ void __launch_bounds__(kSweepThreads, 1) k_sweep(DevTables T, const d
     }
   }
   const double h2 = T.h * T.h;
-  double* R1 = R + threadIdx.x;
+  const int slot = threadIdx.x >> 1;
+  double* Rs = R + slot;           // Rs[(4c + u)·kQuads], u: 0 A_o, 1 B_o, 2 A_e, 3 B_e
   for (int g = T.g_lo + blockIdx.x / nch; g < T.g_hi; g += G) {
     const int c0 = BL * g + 1;
     const int e0 = T.col_ptr[c0];
-    const int ncol = g < P - 1 ? BL : LB;   // block columns + separator column
+    const int ncol = g < T.P - 1 ? BL : LB;   // block columns + separator column
     const int e1 = cval ? T.col_ptr[c0 + ncol] : e0;
     __syncthreads();
     for (int e = e0 + threadIdx.x; e < e1; e += B) {
       const int j = T.irr_j[e];
       const int rd = (j * kRotStride) & m2;
-      ent[e - e0] = make_double4(cval[e], (double)j, sin_lookup(T.sin_tab, (rd + half) & m2, N),
-                                 sin_lookup(T.sin_tab, rd, N));
+      const double c = cval[e];
+      ent[e - e0] = make_double4(c, (double)j, sin_lookup(T.sin_tab, (rd + half) & m2, N), sin_lookup(T.sin_tab, rd, N));
+      // odd j: sin(πj/2) = ±1; even j: cos(πj/2) = ±1
+      const bool neg = (j & 1) ? ((j >> 1) & 1) : ((j >> 1) & 1);
+      ent2[e - e0] = neg ? -c : c;
     }
     if (threadIdx.x < ncol) {
       const int i = c0 + threadIdx.x;
@@ -217,97 +225,109 @@ __global__ void __launch_bounds__(kSweepThreads, 1) k_sweep(DevTables T, const d
       s_cnt[3 * threadIdx.x + 2] = (cval ? T.col_ptr[i + 1] : e0) - e0;
     }
     __syncthreads();
-    // ---- phase 1: sparse DST, rotation along 8 pairs per item ----
+    // ---- phase 1: sparse DST of every column, 8 quads per item by rotation ----
     for (int it = threadIdx.x; it < ncol * kRotStride; it += B) {
-      const int c = it / kRotStride, pg = it - c * kRotStride;
-      const int tb = t0 + pg;
+      const int c = it / kRotStride, qg = it - c * kRotStride;
+      const int tb = q0 + qg;
       const int a0 = s_cnt[3 * c], am = s_cnt[3 * c + 1], a1 = s_cnt[3 * c + 2];
-      double acc[2][kRotSteps];
+      double Ao[kRotSteps], Bo[kRotSteps], Ae[kRotSteps], Be[kRotSteps];
 #pragma unroll
-      for (int q = 0; q < kRotSteps; ++q) acc[0][q] = acc[1][q] = 0.0;
-      for (int cls = 0; cls < 2; ++cls) {
-        const int lo = cls ? am : a0, hi = cls ? a1 : am;
-        for (int e = lo; e < hi; ++e) {
-          const double4 en = ent[e];
-          const int j = (int)en.y;
-          const int r0 = (j * tb) & m2;
-          double sn = sinr(r0), cs = sinr((r0 + half) & m2);
+      for (int q = 0; q < kRotSteps; ++q) Ao[q] = Bo[q] = Ae[q] = Be[q] = 0.0;
+      for (int e = a0; e < am; ++e) {   // odd rows
+        const double4 en = ent[e];
+        const double c2 = ent2[e];
+        const int r0 = ((int)en.y * tb) & m2;
+        double sn = sinr(r0), cs = sinr((r0 + half) & m2);
 #pragma unroll
-          for (int q = 0; q < kRotSteps; ++q) {
-            acc[cls][q] = fma(en.x, sn, acc[cls][q]);
-            const double c2 = fma(cs, en.z, -sn * en.w);
-            sn = fma(sn, en.z, cs * en.w);
-            cs = c2;
-          }
+        for (int q = 0; q < kRotSteps; ++q) {
+          Ao[q] = fma(en.x, sn, Ao[q]);
+          Bo[q] = fma(c2, cs, Bo[q]);
+          const double cn = fma(cs, en.z, -sn * en.w);
+          sn = fma(sn, en.z, cs * en.w);
+          cs = cn;
+        }
+      }
+      for (int e = am; e < a1; ++e) {   // even rows
+        const double4 en = ent[e];
+        const double c2 = ent2[e];
+        const int r0 = ((int)en.y * tb) & m2;
+        double sn = sinr(r0), cs = sinr((r0 + half) & m2);
+#pragma unroll
+        for (int q = 0; q < kRotSteps; ++q) {
+          Ae[q] = fma(en.x, sn, Ae[q]);
+          Be[q] = fma(c2, sn, Be[q]);
+          const double cn = fma(cs, en.z, -sn * en.w);
+          sn = fma(sn, en.z, cs * en.w);
+          cs = cn;
         }
       }
 #pragma unroll
       for (int q = 0; q < kRotSteps; ++q) {
-        const int slot = pg + kRotStride * q;
-        R[(2 * c) * B + slot] = acc[0][q];
-        R[(2 * c + 1) * B + slot] = acc[1][q];
+        const int sl = qg + kRotStride * q;
+        R[(4 * c + 0) * kQuads + sl] = Ao[q];
+        R[(4 * c + 1) * kQuads + sl] = Bo[q];
+        R[(4 * c + 2) * kQuads + sl] = Ae[q];
+        R[(4 * c + 3) * kQuads + sl] = Be[q];
       }
     }
     __syncthreads();
-    if (ch == 0 && threadIdx.x < ncol && cval) {
-      // slot 0 is mode N/2: Σ_j c_j sin(πj/2) (odd rows only)
+    if (ch == 0 && threadIdx.x < ncol) {
+      // quad slot 0 holds modes {0, N/2, N/4, 3N/4}: r_{N/2} = Σ c sin(πj/2), r_{N/4}, r_{3N/4}
       const int c = threadIdx.x;
-      double a = 0.0;
-      for (int e = s_cnt[3 * c]; e < s_cnt[3 * c + 1]; ++e) {
+      double rh = 0.0, rq = 0.0, r3 = 0.0;
+      for (int e = s_cnt[3 * c]; e < s_cnt[3 * c + 2]; ++e) {
         const double4 en = ent[e];
-        a += ((((int)en.y) >> 1) & 1) ? -en.x : en.x;
+        const int j = (int)en.y;
+        rh = fma(en.x, sin_lookup(T.sin_tab, (j * half) & m2, N), rh);
+        rq = fma(en.x, sin_lookup(T.sin_tab, (j * quarter) & m2, N), rq);
+        r3 = fma(en.x, sin_lookup(T.sin_tab, (j * 3 * quarter) & m2, N), r3);
       }
-      R[(2 * c) * B] = a;
-      R[(2 * c + 1) * B] = 0.0;
+      R[(4 * c + 0) * kQuads] = 0.5 * rh;          // (A_o + A_e, A_o − A_e) = (0, r_{N/2})
+      R[(4 * c + 2) * kQuads] = -0.5 * rh;
+      R[(4 * c + 1) * kQuads] = 0.5 * (rq + r3);   // (B_o − B_e, B_o + B_e) = (r_{N/4}, r_{3N/4})
+      R[(4 * c + 3) * kQuads] = 0.5 * (r3 - rq);
     }
     __syncthreads();
     if (!active) continue;
     // ---- phase 2: local Thomas, y_p = r_p − y_{p−1}/c_{p−1}, z_p = (y_p − z_{p+1})/c_p ----
+    // this thread's two right-hand sides from the quad sums (w = 0: t, N−t; w = 1: N/2−t, N/2+t)
     auto rhs = [&](int c, double& r1, double& r2) {
-      const double ao = R1[(2 * c) * B], ae = R1[(2 * c + 1) * B];
-      r1 = ao + ae;
-      r2 = ao - ae;
+      const double A = Rs[(4 * c + w) * kQuads], E = Rs[(4 * c + 2 + w) * kQuads];
+      r1 = w ? A - E : A + E;
+      r2 = w ? A + E : A - E;
       if (DENSE) {
-        r1 = fma(h2, spec[(size_t)(c0 + c - 1) * N + k1], r1);
-        r2 = fma(h2, spec[(size_t)(c0 + c - 1) * N + k2], r2);
+        const double2 d = *reinterpret_cast<const double2*>(spec + (size_t)(c0 + c - 1) * N + p1);
+        r1 = fma(h2, d.x, r1);
+        r2 = fma(h2, d.y, r2);
       }
     };
+    // y_p overwrites this thread's own two sum slots of row p (the partner thread owns the others)
     double y1, y2;
     rhs(0, y1, y2);
-    R1[0] = y1;
-    R1[B] = y2;
+    Rs[w * kQuads] = y1;
+    Rs[(2 + w) * kQuads] = y2;
 #pragma unroll
     for (int p = 1; p < LB; ++p) {
       double r1, r2;
       rhs(p, r1, r2);
       y1 = fma(-y1, ic1[p - 1], r1);
       y2 = fma(-y2, ic2[p - 1], r2);
-      R1[(2 * p) * B] = y1;
-      R1[(2 * p + 1) * B] = y2;
+      Rs[(4 * p + w) * kQuads] = y1;
+      Rs[(4 * p + 2 + w) * kQuads] = y2;
     }
     double sep1 = 0.0, sep2 = 0.0;
-    if (g < P - 1) rhs(LB, sep1, sep2);
+    if (g < T.P - 1) rhs(LB, sep1, sep2);
     double z1 = y1 * ic1[LB - 1], z2 = y2 * ic2[LB - 1];
     const double zl1 = z1, zl2 = z2;
-    {
-      const size_t row = (size_t)(c0 - 1 + LB - 1) * N;
-      spec[row + k1] = z1;
-      spec[row + k2] = z2;
-    }
+    *reinterpret_cast<double2*>(spec + (size_t)(c0 - 1 + LB - 1) * N + p1) = make_double2(z1, z2);
 #pragma unroll
     for (int p = LB - 2; p >= 0; --p) {
-      z1 = (R1[(2 * p) * B] - z1) * ic1[p];
-      z2 = (R1[(2 * p + 1) * B] - z2) * ic2[p];
-      const size_t row = (size_t)(c0 - 1 + p) * N;
-      spec[row + k1] = z1;
-      spec[row + k2] = z2;
+      z1 = (Rs[(4 * p + w) * kQuads] - z1) * ic1[p];
+      z2 = (Rs[(4 * p + 2 + w) * kQuads] - z2) * ic2[p];
+      *reinterpret_cast<double2*>(spec + (size_t)(c0 - 1 + p) * N + p1) = make_double2(z1, z2);
     }
-    zB[(size_t)g * N + k1] = z1;
-    zB[(size_t)g * N + k2] = z2;
-    if (g < P - 1) {
-      zA[(size_t)g * N + k1] = sep1 - zl1;
-      zA[(size_t)g * N + k2] = sep2 - zl2;
-    }
+    *reinterpret_cast<double2*>(zB + (size_t)g * N + p1) = make_double2(z1, z2);
+    if (g < T.P - 1) *reinterpret_cast<double2*>(zA + (size_t)g * N + p1) = make_double2(sep1 - zl1, sep2 - zl2);
   }
 }
 
@@ -543,13 +563,24 @@ __device__ __forceinline__ double warp_transpose_reduce8(double (&v)[8]) {
   return v[0];
 }
 
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
+  const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(sa), "l"(gmem));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+template <int Nw>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(Nw)); }
+
+constexpr int kInvThreads = 256;
+constexpr int kInvChunk = 4 * kInvThreads;   // spectral positions per staged chunk (one quad per thread)
+
 template <int QPT>
-__global__ void __launch_bounds__(256, 2) k_inv_sparse(DevTables T, const double* __restrict__ spec,
-                                                       const double* __restrict__ hsep, double* __restrict__ vsten) {
+__global__ void __launch_bounds__(kInvThreads, 2) k_inv_sparse(DevTables T, const double* __restrict__ spec,
+                                                               const double* __restrict__ hsep, double* __restrict__ vsten) {
   extern __shared__ double smx[];
   __shared__ double red[8][8];
   __shared__ int s_rows[kMaxColRows];
-  const int N = T.N, half = N >> 1, quarter = N >> 2, m2 = 2 * N - 1, B = blockDim.x, P = T.P;
+  const int N = T.N, half = N >> 1, quarter = N >> 2, m2 = 2 * N - 1, B = kInvThreads, P = T.P;
   double* tab = smx;   // sin(πr/N), r ∈ [0, N), at r + r/16
   for (int r = threadIdx.x; r < N; r += B) tab[r + (r >> 4)] = sin_lookup(T.sin_tab, r, N);
   auto sinr = [&](int r) {   // sin(πr/N), r ∈ [0, 2N)
@@ -557,11 +588,14 @@ __global__ void __launch_bounds__(256, 2) k_inv_sparse(DevTables T, const double
     const double v = tab[idx + (idx >> 4)];
     return (r & N) ? -v : v;
   };
-  const int b = T.o_lo + blockIdx.x;
+  // persistent over the owned stencil columns: the sine table is staged once per CTA
+  for (int b = T.o_lo + blockIdx.x; b < T.o_hi; b += gridDim.x) {
+  __syncthreads();
   const int i = T.ocol[b];
   const int u0 = T.ocol_ptr[b], u1 = T.ocol_ptr[b + 1];
   for (int u = u0 + threadIdx.x; u < u1; u += B) s_rows[u - u0] = T.sn_j[u];
-  // column i: separator → x = h; block row → x = z − h_{g−1} Z_L[p] − h_g Z_R[p]
+  // column i: separator → x = h; block row → x = z − h_{g−1} Z_L[p] − h_g Z_R[p].
+  // Spectral positions 4t..4t+3 hold the quad {t, N−t, N/2−t, N/2+t}: two 16-byte loads per array.
   const int q = i / BL, rr = i - q * BL;
   const bool sep = rr == 0;
   const double* xrow = sep ? hsep + (size_t)(q - 1) * N : spec + (size_t)(i - 1) * N;
@@ -569,31 +603,48 @@ __global__ void __launch_bounds__(256, 2) k_inv_sparse(DevTables T, const double
   const double* hr = (!sep && q < P - 1) ? hsep + (size_t)q * N : nullptr;
   const double* zl = T.zr + (size_t)(sep ? 0 : LB - rr) * N;     // Z_L[p] = Z_R[LB−1−p], p = rr − 1
   const double* zrr = T.zr + (size_t)(sep ? 0 : rr - 1) * N;
-  auto X = [&](int k) {
-    double x = xrow[k];
-    if (hl) x = fma(-hl[k], __ldg(zl + k), x);
-    if (hr) x = fma(-hr[k], __ldg(zrr + k), x);
-    return x;
+  auto X4 = [&](int t, double (&x)[4]) {
+    const double2* xp = reinterpret_cast<const double2*>(xrow + 4 * t);
+    const double2 a = xp[0], b2 = xp[1];
+    x[0] = a.x; x[1] = a.y; x[2] = b2.x; x[3] = b2.y;
+    if (hl) {
+      const double2* hp = reinterpret_cast<const double2*>(hl + 4 * t);
+      const double2* zp = reinterpret_cast<const double2*>(zl + 4 * t);
+      const double2 h0 = hp[0], h1 = hp[1], z0 = __ldg(zp), z1 = __ldg(zp + 1);
+      x[0] = fma(-h0.x, z0.x, x[0]); x[1] = fma(-h0.y, z0.y, x[1]);
+      x[2] = fma(-h1.x, z1.x, x[2]); x[3] = fma(-h1.y, z1.y, x[3]);
+    }
+    if (hr) {
+      const double2* hp = reinterpret_cast<const double2*>(hr + 4 * t);
+      const double2* zp = reinterpret_cast<const double2*>(zrr + 4 * t);
+      const double2 h0 = hp[0], h1 = hp[1], z0 = __ldg(zp), z1 = __ldg(zp + 1);
+      x[0] = fma(-h0.x, z0.x, x[0]); x[1] = fma(-h0.y, z0.y, x[1]);
+      x[2] = fma(-h1.x, z1.x, x[2]); x[3] = fma(-h1.y, z1.y, x[3]);
+    }
   };
   double Pv[QPT], Qp[QPT], Qm[QPT], Rv[QPT];
+  double xq1 = 0.0, xq2 = 0.0, xq3 = 0.0;   // modes N/4, N/2, 3N/4 (quad slot 0)
 #pragma unroll
   for (int s = 0; s < QPT; ++s) {
     const int t = threadIdx.x + s * B;
-    if (t == 0 || t >= quarter) {
+    if (t >= quarter) {
+      Pv[s] = Qp[s] = Qm[s] = Rv[s] = 0.0;
+      continue;
+    }
+    double x[4];
+    X4(t, x);
+    if (t == 0) {   // positions 0..3 = modes 0, N/2, N/4, 3N/4
+      xq2 = x[1];
+      xq1 = x[2];
+      xq3 = x[3];
       Pv[s] = Qp[s] = Qm[s] = Rv[s] = 0.0;
     } else {
-      const double a = X(t), bb = X(N - t), c = X(half - t), d = X(half + t);
+      const double a = x[0], bb = x[1], c = x[2], d = x[3];
       Pv[s] = a + bb;
       Rv[s] = c + d;
       Qp[s] = (a - bb) + (d - c);
       Qm[s] = (a - bb) - (d - c);
     }
-  }
-  double xq1 = 0.0, xq2 = 0.0, xq3 = 0.0;   // modes N/4, N/2, 3N/4
-  if (threadIdx.x == 0) {
-    xq1 = X(quarter);
-    xq2 = X(half);
-    xq3 = X(half + quarter);
   }
   __syncthreads();
   const double scale = 2.0 / N;
@@ -671,6 +722,7 @@ __global__ void __launch_bounds__(256, 2) k_inv_sparse(DevTables T, const double
     }
     __syncthreads();
     u += nr;
+  }
   }
 }
 
@@ -889,11 +941,15 @@ __global__ void __launch_bounds__(512) k_dst_dense(DevTables T, const double* __
             if (rho2 < 1.0) v += bp.a[hh] * exp(1.0 - 1.0 / (1.0 - rho2));   // bump, SURVEY App. A.8
           }
         }
-      } else {
-        v = fixup(T, src, hsep, i, j);
       }
     }
-    f[N + j] = v;
+    if (MODE == 0) f[N + j] = v;
+  }
+  if (MODE == 1) {   // spectral positions → modes (coalesced reads, scattered shared-memory writes)
+    for (int p = threadIdx.x; p < N; p += blockDim.x) {
+      const int k = position_mode(p, N);
+      f[N + k] = k == 0 ? 0.0 : fixup(T, src, hsep, i, p);
+    }
   }
   __syncthreads();
   // 2. z_m = x̃_{2m} + i x̃_{2m+1} (natural order); read all first (z aliases f), then write
@@ -952,7 +1008,10 @@ __global__ void __launch_bounds__(512) k_dst_dense(DevTables T, const double* __
   __syncthreads();
   // 5. store
   if (MODE == 0) {
-    for (int k = threadIdx.x; k < N; k += blockDim.x) dst[(size_t)(i - 1) * N + k] = (k == 0) ? 0.0 : z[zpad(k)].x;
+    for (int p = threadIdx.x; p < N; p += blockDim.x) {   // modes → spectral positions
+      const int k = position_mode(p, N);
+      dst[(size_t)(i - 1) * N + p] = (k == 0) ? 0.0 : z[zpad(k)].x;
+    }
   } else {
     const double sc = 2.0 / N;
     for (int j = threadIdx.x; j <= N; j += blockDim.x)
@@ -1086,15 +1145,15 @@ void launch_inverse_dense(const DevTables& T, const double* spec, const double* 
 void launch_sweep(const DevTables& T, const double* cval, bool dense, double* spec, double* zfirst, double* zlast,
                   double* fsep, cudaStream_t s) {
   (void)zlast;
-  const size_t sm = (size_t)(T.N + T.N / 16 + 2) * sizeof(double) + (size_t)BL * 2 * kSweepThreads * sizeof(double) +
-                    (size_t)T.maxe * 4 * sizeof(double) + 3 * BL * sizeof(int);
+  const size_t sm = (size_t)(T.N + T.N / 16 + 2) * sizeof(double) + (size_t)BL * 4 * kQuads * sizeof(double) +
+                    (size_t)T.maxe * 5 * sizeof(double) + 3 * BL * sizeof(int);
   static bool attr = false;
   if (!attr) {
     cudaFuncSetAttribute(k_sweep<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
     cudaFuncSetAttribute(k_sweep<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
     attr = true;
   }
-  const int nch = (T.N / 2 + kSweepThreads - 1) / kSweepThreads;
+  const int nch = (T.N / 4 + kQuads - 1) / kQuads;
   int per = 0;
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_sweep<false>, kSweepThreads, sm);
   if (per < 1) per = 1;
@@ -1125,9 +1184,9 @@ void launch_inverse_sparse(const DevTables& T, const double* spec, const double*
   const int ncols = T.o_hi - T.o_lo;
   if (ncols <= 0) return;
   const int quarter = T.N / 4;
-  const int threads = quarter < 32 ? 32 : (quarter < 256 ? quarter : 256);
-  const int qpt = (quarter + threads - 1) / threads;
+  const int qpt = (quarter + kInvThreads - 1) / kInvThreads;
   const size_t sm = (size_t)(T.N + T.N / 16 + 1) * sizeof(double);
+  const int grid = ncols < 2 * num_sms() ? ncols : 2 * num_sms();
   static bool attr = false;
   if (!attr) {
     cudaFuncSetAttribute(k_inv_sparse<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 100 * 1024);
@@ -1137,10 +1196,10 @@ void launch_inverse_sparse(const DevTables& T, const double* spec, const double*
     attr = true;
   }
   switch (qpt) {
-    case 1: ++g_launches; k_inv_sparse<1><<<ncols, threads, sm, s>>>(T, spec, hsep, vsten); break;
-    case 2: ++g_launches; k_inv_sparse<2><<<ncols, threads, sm, s>>>(T, spec, hsep, vsten); break;
-    case 4: ++g_launches; k_inv_sparse<4><<<ncols, threads, sm, s>>>(T, spec, hsep, vsten); break;
-    case 8: ++g_launches; k_inv_sparse<8><<<ncols, threads, sm, s>>>(T, spec, hsep, vsten); break;
+    case 1: ++g_launches; k_inv_sparse<1><<<grid, kInvThreads, sm, s>>>(T, spec, hsep, vsten); break;
+    case 2: ++g_launches; k_inv_sparse<2><<<grid, kInvThreads, sm, s>>>(T, spec, hsep, vsten); break;
+    case 4: ++g_launches; k_inv_sparse<4><<<grid, kInvThreads, sm, s>>>(T, spec, hsep, vsten); break;
+    case 8: ++g_launches; k_inv_sparse<8><<<grid, kInvThreads, sm, s>>>(T, spec, hsep, vsten); break;
     default: break;
   }
 }

@@ -24,6 +24,30 @@ constexpr int LB2 = BL2 - 1;
 // most stencil rows one column may hold (checked by setup)
 constexpr int kMaxColRows = 512;
 
+// Position of sine mode k (0 ≤ k < N) in the 2D spectral arrays (see setup2d.cpp).
+#ifdef __CUDACC__
+__host__ __device__
+#endif
+inline int mode_position(int k, int N) {
+  const int q = N >> 2, hN = N >> 1;
+  if (k == 0) return 0;
+  if (k == hN) return 1;
+  if (k == q) return 2;
+  if (k == 3 * q) return 3;
+  if (k < q) return 4 * k;
+  if (k > 3 * q) return 4 * (N - k) + 1;
+  if (k < hN) return 4 * (hN - k) + 2;
+  return 4 * (k - hN) + 3;
+}
+#ifdef __CUDACC__
+__host__ __device__
+#endif
+inline int position_mode(int p, int N) {
+  const int t = p >> 2, r = p & 3, hN = N >> 1;
+  if (t == 0) return r == 0 ? 0 : r == 1 ? hN : r == 2 ? (N >> 2) : 3 * (N >> 2);
+  return r == 0 ? t : r == 1 ? N - t : r == 2 ? hN - t : hN + t;
+}
+
 struct GeomError : std::runtime_error {
   using std::runtime_error::runtime_error;
 };

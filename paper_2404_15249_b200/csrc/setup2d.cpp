@@ -525,6 +525,29 @@ void build_setup(Setup& S, const kfbi_grid* g, const kfbi_boundary* b, const kfb
     S.red2_a[k] = -a * a * S.z2r[k];
     S.red2_b[k] = bb - 2.0 * a * a * S.z2r[(size_t)(LB2 - 1) * N + k];
   }
+  // spectral mode order: quad {t, N−t, N/2−t, N/2+t} at positions 4t..4t+3 (t ∈ [1, N/4)), and
+  // {0, N/2, N/4, 3N/4} at 0..3, so that the inverse transform loads a quad as two 16-byte words
+  // and the sweep writes whole 32-byte sectors.  All per-mode tables are stored in position order.
+  {
+    std::vector<int> posof(N);
+    for (int k = 0; k < N; ++k) posof[k] = mode_position(k, N);
+    auto perm = [&](std::vector<double>& v, int rows, double fill0) {
+      std::vector<double> out(v.size());
+      for (int r = 0; r < rows; ++r)
+        for (int k = 0; k < N; ++k) out[(size_t)r * N + posof[k]] = k == 0 ? fill0 : v[(size_t)r * N + k];
+      v.swap(out);
+    };
+    perm(S.dk, 1, -4.0);
+    perm(S.invc, LB, -0.25);
+    perm(S.zr, LB, 0.0);
+    perm(S.red_a, 1, 0.0);
+    perm(S.red_b, 1, 1.0);
+    perm(S.red_invc, std::max(P - 1, 1), 1.0);
+    perm(S.rinv2, LB2, 1.0);
+    perm(S.z2r, LB2, 0.0);
+    perm(S.red2_a, 1, 0.0);
+    perm(S.red2_b, 1, 1.0);
+  }
   // largest number of sparse corrections staged by one sweep work item (block + separator)
   S.maxe = 1;
   for (int gg = 0; gg < P; ++gg) {

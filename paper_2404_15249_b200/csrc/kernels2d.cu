@@ -146,9 +146,9 @@ __global__ void k_correct(DevTables T, const double* __restrict__ phi, const dou
 // per CTA lifetime: y_p = r_p − y_{p−1}/c_{p−1}, z_p = (y_p − z_{p+1})/c_p, r = h² f̂.
 // Outputs: z at the block rows, B[g] = z_g[1], A[g] = h² f̂_sep,g − z_g[L] (reduced-system
 // right-hand side pieces).
-constexpr int kSweepThreads = 512;
-constexpr int kQuads = kSweepThreads / 2;   // 256 quads {t, N−t, N/2−t, N/2+t} per CTA chunk
-constexpr int kRotSteps = 8;                 // quads per phase-1 item (t = base + 32 s)
+constexpr int kSweepThreads = 256;
+constexpr int kQuads = kSweepThreads / 2;   // 128 quads {t, N−t, N/2−t, N/2+t} per CTA chunk
+constexpr int kRotSteps = 4;                 // quads per phase-1 item (t = base + kRotStride·s)
 constexpr int kRotStride = kQuads / kRotSteps;  // 32
 // Persistent CTAs, each owning a fixed chunk of 256 quads of sine modes {t, N−t, N/2−t, N/2+t}
 // (spectral positions 4t..4t+3, see mode_position) and iterating over blocks g of BL−1 columns
@@ -157,28 +157,20 @@ constexpr int kRotStride = kQuads / kRotSteps;  // 32
 // cos(πj/2) s, so per correction (j, c_j) one rotation step serves the whole quad:
 //   odd j:  A_o += c_j s,   B_o += c_j sin(πj/2) c        even j: A_e += c_j s,  B_e += c_j cos(πj/2) s
 //   r_t = A_o + A_e, r_{N−t} = A_o − A_e, r_{N/2−t} = B_o − B_e, r_{N/2+t} = B_o + B_e.
-// An item covers 8 quads t = t0 + qg + 32 s, the sines along s generated by rotation with the
-// per-entry step e^{iπ·32j/N}.  Phase 2 (A5): thread τ owns positions (4q + 2w, 4q + 2w + 1),
+// An item covers kRotSteps quads t = t0 + qg + kRotStride·s, the sines along s generated by
+// rotation with the per-entry step e^{iπ·kRotStride·j/N}.  Phase 2 (A5): thread τ owns positions (4q + 2w, 4q + 2w + 1),
 // q = τ/2, w = τ mod 2; local Thomas per mode, pivots in registers for the CTA's lifetime; writes
 // z (block rows), B[g] = z_g[1], A[g] = h² f̂_sep,g − z_g[L].
 template <bool DENSE>
-__global__ void __launch_bounds__(kSweepThreads, 1) k_sweep(DevTables T, const double* __restrict__ cval, double* spec,
+__global__ void __launch_bounds__(kSweepThreads, 2) k_sweep(DevTables T, const double* __restrict__ cval, double* spec,
                                                            double* __restrict__ zB, double* __restrict__ zA) {
   extern __shared__ double sm[];
   const int N = T.N, half = N >> 1, quarter = N >> 2, m2 = 2 * N - 1, B = kSweepThreads;
-  double* tab = sm;                                          // sin(πr/N), r ∈ [0, N), at r + r/16
-  const int tabn = N + (N >> 4) + 2;
-  double* R = sm + tabn;                                     // [4·BL sums][256 quads]
+  double* R = sm;                                            // [4·BL sums][kQuads]
   double4* ent = reinterpret_cast<double4*>(R + (size_t)BL * 4 * kQuads);   // (c, j, cos Δ, sin Δ)
   double* ent2 = reinterpret_cast<double*>(ent + T.maxe);    // c·sin(πj/2) (odd j) or c·cos(πj/2) (even j)
   int* s_cnt = reinterpret_cast<int*>(ent2 + T.maxe);        // per-column [start, mid, end)
-  for (int r = threadIdx.x; r < N; r += B) tab[r + (r >> 4)] = sin_lookup(T.sin_tab, r, N);
-  const int lgN = 31 - __clz(N);
-  auto sinr = [&](int r) {   // sin(πr/N), r ∈ [0, 2N)
-    const int idx = r & (N - 1);
-    const double v = tab[idx + (idx >> 4)];
-    return __hiloint2double(__double2hiint(v) ^ ((r >> lgN) << 31), __double2loint(v));
-  };
+  auto sinr = [&](int r) { return sin_lookup(T.sin_tab, r, N); };   // quarter-wave table via L1
   const int nch = (quarter + kQuads - 1) / kQuads;
   const int G = gridDim.x / nch;
   const int ch = blockIdx.x % nch;
@@ -1145,8 +1137,7 @@ void launch_inverse_dense(const DevTables& T, const double* spec, const double* 
 void launch_sweep(const DevTables& T, const double* cval, bool dense, double* spec, double* zfirst, double* zlast,
                   double* fsep, cudaStream_t s) {
   (void)zlast;
-  const size_t sm = (size_t)(T.N + T.N / 16 + 2) * sizeof(double) + (size_t)BL * 4 * kQuads * sizeof(double) +
-                    (size_t)T.maxe * 5 * sizeof(double) + 3 * BL * sizeof(int);
+  const size_t sm = (size_t)BL * 4 * kQuads * sizeof(double) + (size_t)T.maxe * 5 * sizeof(double) + 3 * BL * sizeof(int);
   static bool attr = false;
   if (!attr) {
     cudaFuncSetAttribute(k_sweep<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);

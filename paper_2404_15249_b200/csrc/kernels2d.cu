@@ -865,14 +865,16 @@ __device__ __forceinline__ int zpad(int i) { return i + (i >> 4); }
 // item j: v_r = z[j + r N/R] · e^{+2πi r k/(Ns R)}, k = j mod Ns; DFT_R; z[(j/Ns) Ns R + k + q Ns] = V_q.
 // Each thread holds 16 complex values (16/R items); in place with a barrier between reads and writes.
 template <int R>
-__device__ __forceinline__ void stockham_pass(double2* z, const double* tab, int N, int Ns, int nthreads) {
+__device__ __forceinline__ void stockham_pass(double2* z, const double* tab, int N, int Ns, int nthreads,
+                                              int tid = -1) {
+  if (tid < 0) tid = threadIdx.x;
   constexpr int IT = 16 / R;
   double2 v[16];
   const int nitems = N / R;
 #pragma unroll
   for (int it = 0; it < IT; ++it) {
-    const int j = threadIdx.x + it * nthreads;
-    if (j < nitems && (int)threadIdx.x < nthreads) {
+    const int j = tid + it * nthreads;
+    if (j < nitems && tid < nthreads) {
       const int k = j & (Ns - 1);
 #pragma unroll
       for (int r = 0; r < R; ++r) v[it * R + r] = z[zpad(j + r * nitems)];
@@ -896,8 +898,8 @@ __device__ __forceinline__ void stockham_pass(double2* z, const double* tab, int
   __syncthreads();
 #pragma unroll
   for (int it = 0; it < IT; ++it) {
-    const int j = threadIdx.x + it * nthreads;
-    if (j < nitems && (int)threadIdx.x < nthreads) {
+    const int j = tid + it * nthreads;
+    if (j < nitems && tid < nthreads) {
       const int k = j & (Ns - 1);
       const int base = (j / Ns) * Ns * R + k;
 #pragma unroll
@@ -1417,31 +1419,38 @@ __device__ __forceinline__ double fixup3(const DevTables3& T, const double* __re
   return x;
 }
 
-// batched DST-I of rows of length N (index 0 ≡ 0), one row per CTA, recurrence-free (odd extension)
+// batched DST-I of rows of length N (index 0 ≡ 0), RPC rows per CTA (TPR = N/16 threads per row),
+// recurrence-free (real DFT of the odd extension via a length-N complex Stockham FFT)
 template <int MODE>
-__global__ void __launch_bounds__(512) k_dst_rows3(DevTables3 T, double* work, const double* __restrict__ hsep,
-                                                   double scale, double* __restrict__ out) {
+__global__ void __launch_bounds__(256) k_dst_rows3(DevTables3 T, double* work, const double* __restrict__ hsep,
+                                                   double scale, double* __restrict__ out, int rpc) {
   extern __shared__ double sm[];
   const int N = T.N, half = N >> 1;
+  const int tpr = N / 16 < 1 ? 1 : N / 16;
+  const int rl = threadIdx.x / tpr, tid = threadIdx.x - rl * tpr;
   double* s_sin = sm;
-  double2* z = reinterpret_cast<double2*>(sm + half + 2);
+  const size_t zsz = (size_t)2 * (N + N / 16);     // doubles per row buffer (padded complex)
+  double2* z = reinterpret_cast<double2*>(sm + half + 2 + rl * zsz);
   double* f = reinterpret_cast<double*>(z) + N / 8 - N;
   for (int r = threadIdx.x; r <= half; r += blockDim.x) s_sin[r] = T.sin_tab[r];
-  const size_t row = blockIdx.x;                 // row index: (i−1)·N + a
+  const size_t nrows = (size_t)(N - 1) * N;
+  const size_t row = (size_t)blockIdx.x * rpc + rl;   // (i−1)·N + a
+  const bool live = rl < rpc && row < nrows;
   const int i = (int)(row / N) + 1, a = (int)(row % N);
   double* rp = work + row * N;
-  for (int j = threadIdx.x; j < N; j += blockDim.x) {
-    double v = 0.0;
-    if (j > 0) v = MODE == 1 ? fixup3(T, work, hsep, i, (size_t)a * N + j) : rp[j];
-    f[N + j] = v;
-  }
+  if (live)
+    for (int j = tid; j < N; j += tpr) {
+      double v = 0.0;
+      if (j > 0) v = MODE == 1 ? fixup3(T, work, hsep, i, (size_t)a * N + j) : rp[j];
+      f[N + j] = v;
+    }
   __syncthreads();
   {
     double2 buf[16];
 #pragma unroll
     for (int it = 0; it < 16; ++it) {
-      const int m = threadIdx.x + it * blockDim.x;
-      if (m < N) {
+      const int m = tid + it * tpr;
+      if (live && m < N) {
         const int j0 = 2 * m, j1 = 2 * m + 1;
         const double a0 = j0 < N ? f[N + j0] : (j0 == N ? 0.0 : -f[N + 2 * N - j0]);
         const double b0 = j1 < N ? f[N + j1] : -f[N + 2 * N - j1];
@@ -1451,48 +1460,49 @@ __global__ void __launch_bounds__(512) k_dst_rows3(DevTables3 T, double* work, c
     __syncthreads();
 #pragma unroll
     for (int it = 0; it < 16; ++it) {
-      const int m = threadIdx.x + it * blockDim.x;
-      if (m < N) z[zpad(m)] = buf[it];
+      const int m = tid + it * tpr;
+      if (live && m < N) z[zpad(m)] = buf[it];
     }
   }
   __syncthreads();
   {
-    const int nth = N / 16 < 32 ? 32 : N / 16;
     int Ns = 1;
     while (Ns * 16 <= N) {
-      stockham_pass<16>(z, s_sin, N, Ns, nth);
+      stockham_pass<16>(z, s_sin, N, Ns, tpr, tid);
       Ns *= 16;
     }
     const int rem = N / Ns;
-    if (rem == 2) stockham_pass<2>(z, s_sin, N, Ns, nth);
-    else if (rem == 4) stockham_pass<4>(z, s_sin, N, Ns, nth);
-    else if (rem == 8) stockham_pass<8>(z, s_sin, N, Ns, nth);
+    if (rem == 2) stockham_pass<2>(z, s_sin, N, Ns, tpr, tid);
+    else if (rem == 4) stockham_pass<4>(z, s_sin, N, Ns, tpr, tid);
+    else if (rem == 8) stockham_pass<8>(z, s_sin, N, Ns, tpr, tid);
   }
-  for (int k = threadIdx.x; k <= half; k += blockDim.x) {
-    if (k == 0) {
-      z[0].x = 0.0;
-      continue;
+  if (live)
+    for (int k = tid; k <= half; k += tpr) {
+      if (k == 0) {
+        z[0].x = 0.0;
+        continue;
+      }
+      const int k2 = N - k;
+      const double2 a0 = z[zpad(k)], b0 = z[zpad(k2)];
+      double c, s;
+      twiddle(s_sin, k, N, c, s);
+      const double Fk = 0.5 * (0.5 * (a0.y - b0.y) + c * (-0.5 * (a0.x - b0.x)) + s * (0.5 * (a0.y + b0.y)));
+      double Fk2 = 0.0;
+      if (k2 != k) {
+        twiddle(s_sin, k2, N, c, s);
+        Fk2 = 0.5 * (0.5 * (b0.y - a0.y) + c * (-0.5 * (b0.x - a0.x)) + s * (0.5 * (b0.y + a0.y)));
+      }
+      z[zpad(k)].x = Fk;
+      if (k2 != k) z[zpad(k2)].x = Fk2;
     }
-    const int k2 = N - k;
-    const double2 a0 = z[zpad(k)], b0 = z[zpad(k2)];
-    double c, s;
-    twiddle(s_sin, k, N, c, s);
-    const double Fk = 0.5 * (0.5 * (a0.y - b0.y) + c * (-0.5 * (a0.x - b0.x)) + s * (0.5 * (a0.y + b0.y)));
-    double Fk2 = 0.0;
-    if (k2 != k) {
-      twiddle(s_sin, k2, N, c, s);
-      Fk2 = 0.5 * (0.5 * (b0.y - a0.y) + c * (-0.5 * (b0.x - a0.x)) + s * (0.5 * (b0.y + a0.y)));
-    }
-    z[zpad(k)].x = Fk;
-    if (k2 != k) z[zpad(k2)].x = Fk2;
-  }
   __syncthreads();
+  if (!live) return;
   if (MODE == 2) {
     const int W = N + 1;
     double* op = out + ((size_t)i * W + a) * W;
-    for (int j = threadIdx.x; j <= N; j += blockDim.x) op[j] = (j == 0 || j == N || a == 0) ? 0.0 : scale * z[zpad(j)].x;
+    for (int j = tid; j <= N; j += tpr) op[j] = (j == 0 || j == N || a == 0) ? 0.0 : scale * z[zpad(j)].x;
   } else {
-    for (int k = threadIdx.x; k < N; k += blockDim.x) rp[k] = (k == 0 || a == 0) ? 0.0 : scale * z[zpad(k)].x;
+    for (int k = tid; k < N; k += tpr) rp[k] = (k == 0 || a == 0) ? 0.0 : scale * z[zpad(k)].x;
   }
 }
 
@@ -1645,13 +1655,22 @@ void launch_correct3(const DevTables3& T, const double* phi, const double* dphi,
 void launch_dst_rows3(const DevTables3& T, int mode, double* work, const double* hsep, double scale, double* out,
                       cudaStream_t s) {
   const int N = T.N;
-  const size_t sm = (size_t)(N / 2 + 2 + 2 * N + N / 8) * sizeof(double);
-  const int threads = N / 16 < 32 ? 32 : N / 16;
-  const int rows = (N - 1) * N;
+  const int tpr = N / 16 < 1 ? 1 : N / 16;
+  const int rpc = 256 / tpr >= 1 ? 256 / tpr : 1;
+  const size_t sm = (size_t)(N / 2 + 2 + (size_t)rpc * 2 * (N + N / 16)) * sizeof(double);
+  const long rows = (long)(N - 1) * N;
+  const int grid = cdiv3(rows, rpc);
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(k_dst_rows3<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    cudaFuncSetAttribute(k_dst_rows3<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    cudaFuncSetAttribute(k_dst_rows3<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    attr = true;
+  }
   ++g_launches;
-  if (mode == 0) k_dst_rows3<0><<<rows, threads, sm, s>>>(T, work, hsep, scale, out);
-  else if (mode == 1) k_dst_rows3<1><<<rows, threads, sm, s>>>(T, work, hsep, scale, out);
-  else k_dst_rows3<2><<<rows, threads, sm, s>>>(T, work, hsep, scale, out);
+  if (mode == 0) k_dst_rows3<0><<<grid, tpr * rpc, sm, s>>>(T, work, hsep, scale, out, rpc);
+  else if (mode == 1) k_dst_rows3<1><<<grid, tpr * rpc, sm, s>>>(T, work, hsep, scale, out, rpc);
+  else k_dst_rows3<2><<<grid, tpr * rpc, sm, s>>>(T, work, hsep, scale, out, rpc);
 }
 void launch_transpose3(const DevTables3& T, double* work, cudaStream_t s) {
   const int t = T.N / 32;

@@ -181,6 +181,7 @@ void layout3(kfbi_ctx* c, Arena& A) {
   T.st_c = A.table(S.st_c); T.st_code = A.table(S.st_code); T.st_w = A.table(S.st_w);
   T.sin_tab = A.table(S.sin_tab); T.dk = A.table(S.dk); T.zr = A.table(S.zr); T.red_a = A.table(S.red_a);
   T.red_b = A.table(S.red_b); T.side = A.table(S.side);
+  T.tw = A.table(S.tw);
   c->nh = 0;
   c->work = A.take<double>((N - 1) * K);
   c->zfirst = A.take<double>(P * K);

@@ -555,16 +555,7 @@ __device__ __forceinline__ double warp_transpose_reduce8(double (&v)[8]) {
   return v[0];
 }
 
-__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
-  const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
-  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(sa), "l"(gmem));
-}
-__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
-template <int Nw>
-__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(Nw)); }
-
 constexpr int kInvThreads = 256;
-constexpr int kInvChunk = 4 * kInvThreads;   // spectral positions per staged chunk (one quad per thread)
 
 template <int QPT>
 __global__ void __launch_bounds__(kInvThreads, 2) k_inv_sparse(DevTables T, const double* __restrict__ spec,
@@ -1419,90 +1410,107 @@ __device__ __forceinline__ double fixup3(const DevTables3& T, const double* __re
   return x;
 }
 
-// batched DST-I of rows of length N (index 0 ≡ 0), RPC rows per CTA (TPR = N/16 threads per row),
-// recurrence-free (real DFT of the odd extension via a length-N complex Stockham FFT)
-template <int MODE>
-__global__ void __launch_bounds__(256) k_dst_rows3(DevTables3 T, double* work, const double* __restrict__ hsep,
-                                                   double scale, double* __restrict__ out, int rpc) {
-  extern __shared__ double sm[];
-  const int N = T.N, half = N >> 1;
-  const int tpr = N / 16 < 1 ? 1 : N / 16;
-  const int rl = threadIdx.x / tpr, tid = threadIdx.x - rl * tpr;
-  double* s_sin = sm;
-  const size_t zsz = (size_t)2 * (N + N / 16);     // doubles per row buffer (padded complex)
-  double2* z = reinterpret_cast<double2*>(sm + half + 2 + rl * zsz);
-  double* f = reinterpret_cast<double*>(z) + N / 8 - N;
-  for (int r = threadIdx.x; r <= half; r += blockDim.x) s_sin[r] = T.sin_tab[r];
-  const size_t nrows = (size_t)(N - 1) * N;
-  const size_t row = (size_t)blockIdx.x * rpc + rl;   // (i−1)·N + a
-  const bool live = rl < rpc && row < nrows;
+// Compile-time Stockham radix-R pass over one row z[0..N) held by NTH = N/16 lanes of one warp
+// (rows never straddle warps, so __syncwarp orders the in-place smem exchange).  Twiddles
+// e^{+2πi r k/(Ns R)} = tw[r k 2N/(Ns R) mod 2N] from the (cos, sin)(π m/N) table (L1-resident).
+template <int R, int N, int Ns>
+__device__ __forceinline__ void st_pass(double2* z, const double2* __restrict__ tw, int tid) {
+  constexpr int NTH = N / 16, NI = N / R, IT = NI / NTH;
+  double2 v[IT * R];
+#pragma unroll
+  for (int it = 0; it < IT; ++it) {
+    const int j = tid + it * NTH;
+#pragma unroll
+    for (int r = 0; r < R; ++r) v[it * R + r] = z[zpad(j + r * NI)];
+    if (Ns > 1) {
+      const int k = j & (Ns - 1);
+#pragma unroll
+      for (int r = 1; r < R; ++r) {
+        const double2 w = __ldg(tw + ((r * k * (2 * N / (Ns * R))) & (2 * N - 1)));
+        const double2 a = v[it * R + r];
+        v[it * R + r] = make_double2(a.x * w.x - a.y * w.y, a.x * w.y + a.y * w.x);
+      }
+    }
+    dft_reg<R>(v + it * R);
+  }
+  __syncwarp();
+#pragma unroll
+  for (int it = 0; it < IT; ++it) {
+    const int j = tid + it * NTH;
+    const int base = (j / Ns) * Ns * R + (j & (Ns - 1));
+#pragma unroll
+    for (int q = 0; q < R; ++q) z[zpad(base + q * Ns)] = v[it * R + q];
+  }
+  __syncwarp();
+}
+
+template <int N, int Ns>
+__device__ __forceinline__ void st_fft(double2* z, const double2* __restrict__ tw, int tid) {
+  if constexpr (Ns * 16 <= N) {
+    st_pass<16, N, Ns>(z, tw, tid);
+    st_fft<N, Ns * 16>(z, tw, tid);
+  } else if constexpr (N / Ns == 8) {
+    st_pass<8, N, Ns>(z, tw, tid);
+  } else if constexpr (N / Ns == 4) {
+    st_pass<4, N, Ns>(z, tw, tid);
+  } else if constexpr (N / Ns == 2) {
+    st_pass<2, N, Ns>(z, tw, tid);
+  }
+}
+
+// batched DST-I of the rows of length N (index 0 ≡ 0), N compile-time: one row per N/16 lanes,
+// 256/(N/16) rows per CTA, real DFT of the odd extension via a length-N complex FFT; the odd
+// extension is scattered straight from registers and the (k, N−k) post-processing stores to HBM.
+template <int MODE, int N>
+__global__ void __launch_bounds__(256) k_dst_rows3t(DevTables3 T, double* work, const double* __restrict__ hsep,
+                                                    double scale, double* __restrict__ out) {
+  constexpr int NTH = N / 16, RPC = 256 / NTH, ZS = N + N / 16, NP = N / 2 / NTH;
+  extern __shared__ double2 smz[];
+  const int rl = threadIdx.x / NTH, tid = threadIdx.x % NTH;
+  double2* z = smz + rl * ZS;
+  const double2* __restrict__ tw = reinterpret_cast<const double2*>(T.tw);
+  const size_t row = (size_t)blockIdx.x * RPC + rl;   // (i−1)·N + a
+  const bool live = row < (size_t)(N - 1) * N;
   const int i = (int)(row / N) + 1, a = (int)(row % N);
   double* rp = work + row * N;
-  if (live)
-    for (int j = tid; j < N; j += tpr) {
-      double v = 0.0;
-      if (j > 0) v = MODE == 1 ? fixup3(T, work, hsep, i, (size_t)a * N + j) : rp[j];
-      f[N + j] = v;
-    }
-  __syncthreads();
-  {
-    double2 buf[16];
 #pragma unroll
-    for (int it = 0; it < 16; ++it) {
-      const int m = tid + it * tpr;
-      if (live && m < N) {
-        const int j0 = 2 * m, j1 = 2 * m + 1;
-        const double a0 = j0 < N ? f[N + j0] : (j0 == N ? 0.0 : -f[N + 2 * N - j0]);
-        const double b0 = j1 < N ? f[N + j1] : -f[N + 2 * N - j1];
-        buf[it] = make_double2(a0, b0);
+  for (int s = 0; s < NP; ++s) {
+    const int m = tid + s * NTH;   // pair (f_2m, f_2m+1)
+    double f0 = 0.0, f1 = 0.0;
+    if (live) {
+      if (MODE == 1) {
+        if (m > 0) f0 = fixup3(T, work, hsep, i, (size_t)a * N + 2 * m);
+        f1 = fixup3(T, work, hsep, i, (size_t)a * N + 2 * m + 1);
+      } else {
+        const double2 t = *reinterpret_cast<const double2*>(rp + 2 * m);
+        f0 = m > 0 ? t.x : 0.0;
+        f1 = t.y;
       }
     }
-    __syncthreads();
+    z[zpad(m)] = make_double2(f0, f1);                 // x_t = f_t, t < N
+    if (m > 0) z[zpad(N - m)].x = -f0;                 // x_{2N−t} = −f_t
+    else z[zpad(N / 2)].x = 0.0;                       // x_N = 0
+    z[zpad(N - m - 1)].y = -f1;
+  }
+  __syncwarp();
+  st_fft<N, 1>(z, tw, tid);
+  double* op = MODE == 2 ? out + ((size_t)i * (N + 1) + a) * (N + 1) : rp;
+  const bool zero = !live || a == 0;
 #pragma unroll
-    for (int it = 0; it < 16; ++it) {
-      const int m = tid + it * tpr;
-      if (live && m < N) z[zpad(m)] = buf[it];
+  for (int s = 0; s < NP; ++s) {
+    const int k = 1 + tid + s * NTH, k2 = N - k;   // F_k = Im(E_k + e^{iπk/N} O_k)/2, k ∈ [1, N/2]
+    const double2 A = z[zpad(k)], B = z[zpad(k2)];
+    const double2 w = __ldg(tw + k);
+    const double Fk = 0.5 * (0.5 * (A.y - B.y) - w.x * (0.5 * (A.x - B.x)) + w.y * (0.5 * (A.y + B.y)));
+    const double Fk2 = 0.5 * (0.5 * (B.y - A.y) + w.x * (0.5 * (B.x - A.x)) + w.y * (0.5 * (B.y + A.y)));
+    if (live) {
+      op[k] = zero ? 0.0 : scale * Fk;
+      if (k2 != k) op[k2] = zero ? 0.0 : scale * Fk2;
     }
   }
-  __syncthreads();
-  {
-    int Ns = 1;
-    while (Ns * 16 <= N) {
-      stockham_pass<16>(z, s_sin, N, Ns, tpr, tid);
-      Ns *= 16;
-    }
-    const int rem = N / Ns;
-    if (rem == 2) stockham_pass<2>(z, s_sin, N, Ns, tpr, tid);
-    else if (rem == 4) stockham_pass<4>(z, s_sin, N, Ns, tpr, tid);
-    else if (rem == 8) stockham_pass<8>(z, s_sin, N, Ns, tpr, tid);
-  }
-  if (live)
-    for (int k = tid; k <= half; k += tpr) {
-      if (k == 0) {
-        z[0].x = 0.0;
-        continue;
-      }
-      const int k2 = N - k;
-      const double2 a0 = z[zpad(k)], b0 = z[zpad(k2)];
-      double c, s;
-      twiddle(s_sin, k, N, c, s);
-      const double Fk = 0.5 * (0.5 * (a0.y - b0.y) + c * (-0.5 * (a0.x - b0.x)) + s * (0.5 * (a0.y + b0.y)));
-      double Fk2 = 0.0;
-      if (k2 != k) {
-        twiddle(s_sin, k2, N, c, s);
-        Fk2 = 0.5 * (0.5 * (b0.y - a0.y) + c * (-0.5 * (b0.x - a0.x)) + s * (0.5 * (b0.y + a0.y)));
-      }
-      z[zpad(k)].x = Fk;
-      if (k2 != k) z[zpad(k2)].x = Fk2;
-    }
-  __syncthreads();
-  if (!live) return;
-  if (MODE == 2) {
-    const int W = N + 1;
-    double* op = out + ((size_t)i * W + a) * W;
-    for (int j = tid; j <= N; j += tpr) op[j] = (j == 0 || j == N || a == 0) ? 0.0 : scale * z[zpad(j)].x;
-  } else {
-    for (int k = tid; k < N; k += tpr) rp[k] = (k == 0 || a == 0) ? 0.0 : scale * z[zpad(k)].x;
+  if (live && tid == 0) {
+    op[0] = 0.0;
+    if (MODE == 2) op[N] = 0.0;
   }
 }
 
@@ -1652,25 +1660,33 @@ void launch_correct3(const DevTables3& T, const double* phi, const double* dphi,
   ++g_launches;
   k_correct3<<<cdiv3(T.nirr, 128), 128, 0, s>>>(T, phi, dphi, fq, jq_given, work);
 }
-void launch_dst_rows3(const DevTables3& T, int mode, double* work, const double* hsep, double scale, double* out,
-                      cudaStream_t s) {
-  const int N = T.N;
-  const int tpr = N / 16 < 1 ? 1 : N / 16;
-  const int rpc = 256 / tpr >= 1 ? 256 / tpr : 1;
-  const size_t sm = (size_t)(N / 2 + 2 + (size_t)rpc * 2 * (N + N / 16)) * sizeof(double);
-  const long rows = (long)(N - 1) * N;
-  const int grid = cdiv3(rows, rpc);
+template <int N>
+static void dst_rows3_n(const DevTables3& T, int mode, double* work, const double* hsep, double scale, double* out,
+                        cudaStream_t s) {
+  constexpr int NTH = N / 16, RPC = 256 / NTH;
+  const size_t sm = (size_t)RPC * (N + N / 16) * sizeof(double2);
+  const int grid = cdiv3((long)(N - 1) * N, RPC);
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(k_dst_rows3<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-    cudaFuncSetAttribute(k_dst_rows3<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-    cudaFuncSetAttribute(k_dst_rows3<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    cudaFuncSetAttribute(k_dst_rows3t<0, N>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    cudaFuncSetAttribute(k_dst_rows3t<1, N>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    cudaFuncSetAttribute(k_dst_rows3t<2, N>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
     attr = true;
   }
+  if (mode == 0) k_dst_rows3t<0, N><<<grid, 256, sm, s>>>(T, work, hsep, scale, out);
+  else if (mode == 1) k_dst_rows3t<1, N><<<grid, 256, sm, s>>>(T, work, hsep, scale, out);
+  else k_dst_rows3t<2, N><<<grid, 256, sm, s>>>(T, work, hsep, scale, out);
+}
+void launch_dst_rows3(const DevTables3& T, int mode, double* work, const double* hsep, double scale, double* out,
+                      cudaStream_t s) {
   ++g_launches;
-  if (mode == 0) k_dst_rows3<0><<<grid, tpr * rpc, sm, s>>>(T, work, hsep, scale, out, rpc);
-  else if (mode == 1) k_dst_rows3<1><<<grid, tpr * rpc, sm, s>>>(T, work, hsep, scale, out, rpc);
-  else k_dst_rows3<2><<<grid, tpr * rpc, sm, s>>>(T, work, hsep, scale, out, rpc);
+  switch (T.N) {
+    case 32: dst_rows3_n<32>(T, mode, work, hsep, scale, out, s); break;
+    case 64: dst_rows3_n<64>(T, mode, work, hsep, scale, out, s); break;
+    case 128: dst_rows3_n<128>(T, mode, work, hsep, scale, out, s); break;
+    case 256: dst_rows3_n<256>(T, mode, work, hsep, scale, out, s); break;
+    default: dst_rows3_n<512>(T, mode, work, hsep, scale, out, s); break;
+  }
 }
 void launch_transpose3(const DevTables3& T, double* work, cudaStream_t s) {
   const int t = T.N / 32;

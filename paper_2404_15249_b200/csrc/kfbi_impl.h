@@ -135,6 +135,7 @@ struct Setup3 {
   std::vector<double> st_w;               // 10 per point: row 0 of the inverse local system
   std::vector<int64_t> st_nodes_ij;       // dump
   std::vector<double> sin_tab, dk, zr, red_a, red_b;   // modes m = ll·N + kk
+  std::vector<double> tw;            // 2N complex: (cos, sin)(π m / N), m = 0..2N−1
 };
 void build_setup3(Setup3& S, const kfbi_grid* g, const kfbi_boundary* b, const kfbi_pde* pde);
 
@@ -152,6 +153,7 @@ struct DevTables3 {
   const int32_t *st_c, *st_code;
   const double* st_w;
   const double *sin_tab, *dk, *zr, *red_a, *red_b;
+  const double* tw;   // 2N × (cos, sin)
   const int8_t* side;
 };
 

@@ -321,6 +321,12 @@ void build_setup3(Setup3& S, const kfbi_grid* g, const kfbi_boundary* b, const k
   const size_t K = (size_t)N * N;
   S.sin_tab.resize(N / 2 + 1);
   for (int r = 0; r <= N / 2; ++r) S.sin_tab[r] = std::sin(3.14159265358979323846 * (double)r / N);
+  S.tw.resize(4 * (size_t)N);
+  for (int m = 0; m < 2 * N; ++m) {   // folded onto the quarter wave so that symmetric entries agree exactly
+    auto sn = [&](int r) { double sg = 1.0; if (r >= N) { r -= N; sg = -1.0; } if (r > N / 2) r = N - r; return sg * S.sin_tab[r]; };
+    S.tw[2 * m] = sn((m + N / 2) % (2 * N));
+    S.tw[2 * m + 1] = sn(m);
+  }
   S.dk.assign(K, -4.0);
   S.zr.assign((size_t)LB * K, 0.0);
   S.red_a.assign(K, 0.0);

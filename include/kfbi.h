@@ -184,7 +184,8 @@ kfbi_status kfbi_destroy(kfbi_ctx* ctx);
 /* Device time of each kernel of one kfbi_apply, averaged over `reps` applies, from CUDA
  * events recorded on `stream` between the launches (bench/roofline use; synchronous).
  * ms_out[8] = {spline, correct, sweep, reduced, inverse, hole, interp, whole apply}; in 3D:
- * {LSQ fit, base + correction, forward DSTs + sweep, reduced, inverse DSTs, 0, interp, apply}. */
+ * {LSQ fit, correction, sparse forward DST + sweep, reduced, inverse y-DST, z-evaluation at the
+ * stencil nodes, interp, apply}. */
 kfbi_status kfbi_profile_apply(kfbi_ctx* ctx, const double* d_phi, double* d_out, int32_t reps,
                                double* ms_out, void* stream);
 

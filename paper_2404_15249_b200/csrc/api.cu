@@ -50,6 +50,7 @@ struct kfbi_ctx {
   Setup3 S3;
   DevTables3 T3{};
   double *work = nullptr, *dphi = nullptr;   // 3D working array and LSQ derivatives
+  double *work2 = nullptr, *corr = nullptr;  // 3D transposed inverse rows; compact corrections
   cudaStream_t stream = nullptr;
   int device = 0;
   std::string err;
@@ -182,9 +183,13 @@ void layout3(kfbi_ctx* c, Arena& A) {
   T.sin_tab = A.table(S.sin_tab); T.dk = A.table(S.dk); T.zr = A.table(S.zr); T.red_a = A.table(S.red_a);
   T.red_b = A.table(S.red_b); T.side = A.table(S.side);
   T.tw = A.table(S.tw);
+  T.irr_row_ptr = A.table(S.irr_row_ptr); T.zrow_id = A.table(S.zrow_id); T.zrow_ptr = A.table(S.zrow_ptr);
+  T.znode_b = A.table(S.znode_b); T.nzrow = (int)S.zrow_id.size();
   c->nh = 0;
   c->work = A.take<double>((N - 1) * K);
+  c->work2 = A.take<double>((N - 1) * K);
   c->zfirst = A.take<double>(P * K);
+  c->corr = A.take<double>(std::max(S.nirr, 1));
   c->fsep = A.take<double>(std::max<size_t>(P - 1, 1) * K);
   c->hsep = A.take<double>(std::max<size_t>(P - 1, 1) * K);
   c->dphi = A.take<double>(5 * M);
@@ -357,13 +362,18 @@ void inverse3(kfbi_ctx* c, double* u, cudaStream_t s) {   // u == NULL: result s
   ck(cudaMemsetAsync(u + (size_t)c->T3.N * W * W, 0, W * W * sizeof(double), s), "memset");
   ck(cudaMemset2DAsync(u + (W + c->T3.N) * W, W * W * sizeof(double), 0, W * sizeof(double), c->T3.N - 1, s), "memset");
 }
+// K_D (the GMRES operator): sparse source, sparse read-out — no dense z-direction transforms
 void apply_KD3(kfbi_ctx* c, const double* phi, double* out, cudaStream_t s) {
-  launch_lsq3(c->T3, phi, c->dphi, s);
-  launch_base3(c->T3, nullptr, c->work, s);
-  launch_correct3(c->T3, phi, c->dphi, nullptr, nullptr, c->work, s);
-  forward3(c, s);
-  inverse3(c, nullptr, s);
-  launch_interp3(c->T3, phi, c->dphi, nullptr, nullptr, c->work, out, s);
+  const DevTables3& T = c->T3;
+  const double sc = 2.0 / T.N;
+  launch_lsq3(T, phi, c->dphi, s);
+  launch_correct3(T, phi, c->dphi, nullptr, nullptr, nullptr, s, c->corr);
+  launch_sparse3(T, 0, c->corr, nullptr, 1.0, c->work, s);
+  launch_sweep3(T, c->work, c->zfirst, c->fsep, s);
+  launch_reduced3(T, c->zfirst, c->fsep, c->hsep, s);
+  launch_sparse3(T, 1, c->work, c->hsep, sc, c->work2, s);
+  launch_sparse3(T, 2, c->work2, nullptr, sc, c->work, s);
+  launch_interp3(T, phi, c->dphi, nullptr, nullptr, c->work, out, s);
 }
 void apply_Y3(kfbi_ctx* c, const double* fgrid, const double* fq, const double* fz, double* out, cudaStream_t s) {
   launch_base3(c->T3, fgrid, c->work, s);
@@ -707,20 +717,16 @@ kfbi_status kfbi_profile_apply(kfbi_ctx* c, const double* d_phi, double* d_out, 
       ck(cudaEventRecord(ev[0], s), "rec");
       launch_lsq3(T3, d_phi, c->dphi, s);
       ck(cudaEventRecord(ev[1], s), "rec");
-      launch_base3(T3, nullptr, c->work, s);
-      launch_correct3(T3, d_phi, c->dphi, nullptr, nullptr, c->work, s);
+      launch_correct3(T3, d_phi, c->dphi, nullptr, nullptr, nullptr, s, c->corr);
       ck(cudaEventRecord(ev[2], s), "rec");
-      launch_dst_rows3(T3, 0, c->work, nullptr, 1.0, nullptr, s);
-      launch_transpose3(T3, c->work, s);
-      launch_dst_rows3(T3, 0, c->work, nullptr, 1.0, nullptr, s);
+      launch_sparse3(T3, 0, c->corr, nullptr, 1.0, c->work, s);
       launch_sweep3(T3, c->work, c->zfirst, c->fsep, s);
       ck(cudaEventRecord(ev[3], s), "rec");
       launch_reduced3(T3, c->zfirst, c->fsep, c->hsep, s);
       ck(cudaEventRecord(ev[4], s), "rec");
-      launch_dst_rows3(T3, 1, c->work, c->hsep, sc, nullptr, s);
-      launch_transpose3(T3, c->work, s);
-      launch_dst_rows3(T3, 0, c->work, nullptr, sc, nullptr, s);
+      launch_sparse3(T3, 1, c->work, c->hsep, sc, c->work2, s);
       ck(cudaEventRecord(ev[5], s), "rec");
+      launch_sparse3(T3, 2, c->work2, nullptr, sc, c->work, s);
       ck(cudaEventRecord(ev[6], s), "rec");
       launch_interp3(T3, d_phi, c->dphi, nullptr, nullptr, c->work, d_out, s);
       ck(cudaEventRecord(ev[7], s), "rec");

@@ -69,7 +69,12 @@ void launch_scale_copy(int n, const double* a, const double* scal, double* out, 
 void launch_lsq3(const DevTables3& T, const double* phi, double* dphi, cudaStream_t s);
 void launch_base3(const DevTables3& T, const double* fgrid, double* work, cudaStream_t s);
 void launch_correct3(const DevTables3& T, const double* phi, const double* dphi, const double* fq,
-                     const double* jq_given, double* work, cudaStream_t s);
+                     const double* jq_given, double* work, cudaStream_t s, double* corr = nullptr);
+// sparse K_D path: which 0 = forward from the compact corrections (src = corr → dst = work, spectral
+// layout); 1 = fixed-up inverse along y (src = work, hsep → dst = work2, transposed rows (i−1, a, ll));
+// 2 = z-direction inverse at the distinct stencil nodes only (src = work2 → dst = work, × scale)
+void launch_sparse3(const DevTables3& T, int which, const double* src, const double* hsep, double scale, double* dst,
+                    cudaStream_t s);
 // batched in-place DST-I of the (N−1)·N rows of the working array: mode 0 plain (× scale);
 // mode 1 inverse with the arrowhead fix-up on load (rows = (i, ll), modes m = ll·N + kk);
 // mode 2 final store into a full (N+1)^3 grid (× scale)

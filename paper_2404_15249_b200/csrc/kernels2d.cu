@@ -1382,7 +1382,8 @@ __global__ void k_base3(DevTables3 T, const double* __restrict__ f, double* __re
 
 // A2+A3 (3D): seven-point correction at irregular nodes, added in place (×h²)
 __global__ void k_correct3(DevTables3 T, const double* __restrict__ phi, const double* __restrict__ dphi,
-                           const double* __restrict__ fq, const double* __restrict__ jg, double* __restrict__ work) {
+                           const double* __restrict__ fq, const double* __restrict__ jg, double* __restrict__ work,
+                           double* __restrict__ corr) {
   const int n = blockIdx.x * blockDim.x + threadIdx.x;
   if (n >= T.nirr) return;
   double acc = 0.0;
@@ -1394,28 +1395,40 @@ __global__ void k_correct3(DevTables3 T, const double* __restrict__ phi, const d
     load_jump3(T, q, phi, dphi, fq, jg, J);
     acc += J.v + J.g[ax] * d + 0.5 * J.H[ax] * d * d;   // H[0..2] = xx, yy, zz
   }
-  work[T.irr_lin[n]] += T.irr_side[n] ? -acc : acc;
+  if (corr) corr[n] = T.irr_side[n] ? -acc : acc;   // compact (sparse K_D path)
+  else work[T.irr_lin[n]] += T.irr_side[n] ? -acc : acc;
 }
 
-// fix-up of the spectral value at row i (x), mode m
-__device__ __forceinline__ double fixup3(const DevTables3& T, const double* __restrict__ spec,
-                                         const double* __restrict__ hsep, int i, size_t m) {
+// fix-up of the spectral pair (m, m+1) (m even) at row i: streaming load of the spectrum, cached
+// separators and spikes (L2-resident across planes)
+__device__ __forceinline__ double2 fixup3_pair(const DevTables3& T, const double* __restrict__ spec,
+                                               const double* __restrict__ hsep, int i, size_t m) {
   const size_t K = (size_t)T.N * T.N;
   const int q = i / BL, r = i - q * BL;
-  if (r == 0) return hsep[(size_t)(q - 1) * K + m];
+  if (r == 0) return __ldg(reinterpret_cast<const double2*>(hsep + (size_t)(q - 1) * K + m));
   const int p = r - 1, g = q;
-  double x = spec[(size_t)(i - 1) * K + m];
-  if (g > 0) x = fma(-hsep[(size_t)(g - 1) * K + m], T.zr[(size_t)(LB - 1 - p) * K + m], x);
-  if (g < T.P - 1) x = fma(-hsep[(size_t)g * K + m], T.zr[(size_t)p * K + m], x);
+  double2 x = __ldcs(reinterpret_cast<const double2*>(spec + (size_t)(i - 1) * K + m));
+  if (g > 0) {
+    const double2 h = __ldg(reinterpret_cast<const double2*>(hsep + (size_t)(g - 1) * K + m));
+    const double2 z = __ldg(reinterpret_cast<const double2*>(T.zr + (size_t)(LB - 1 - p) * K + m));
+    x.x = fma(-h.x, z.x, x.x);
+    x.y = fma(-h.y, z.y, x.y);
+  }
+  if (g < T.P - 1) {
+    const double2 h = __ldg(reinterpret_cast<const double2*>(hsep + (size_t)g * K + m));
+    const double2 z = __ldg(reinterpret_cast<const double2*>(T.zr + (size_t)p * K + m));
+    x.x = fma(-h.x, z.x, x.x);
+    x.y = fma(-h.y, z.y, x.y);
+  }
   return x;
 }
 
-// Compile-time Stockham radix-R pass over one row z[0..N) held by NTH = N/16 lanes of one warp
-// (rows never straddle warps, so __syncwarp orders the in-place smem exchange).  Twiddles
-// e^{+2πi r k/(Ns R)} = tw[r k 2N/(Ns R) mod 2N] from the (cos, sin)(π m/N) table (L1-resident).
-template <int R, int N, int Ns>
+// Compile-time Stockham radix-R pass over one row z[0..M) held by M/16 lanes of one warp (rows never
+// straddle warps, so __syncwarp orders the in-place smem exchange).  Twiddles e^{+2πi r k/(Ns R)} =
+// tw[r k 2NT/(Ns R) mod 2NT] from the (cos, sin)(π m/NT) table of the grid size NT (L1-resident).
+template <int R, int M, int Ns, int NT>
 __device__ __forceinline__ void st_pass(double2* z, const double2* __restrict__ tw, int tid) {
-  constexpr int NTH = N / 16, NI = N / R, IT = NI / NTH;
+  constexpr int NTH = M / 16, NI = M / R, IT = NI / NTH;
   double2 v[IT * R];
 #pragma unroll
   for (int it = 0; it < IT; ++it) {
@@ -1426,7 +1439,7 @@ __device__ __forceinline__ void st_pass(double2* z, const double2* __restrict__ 
       const int k = j & (Ns - 1);
 #pragma unroll
       for (int r = 1; r < R; ++r) {
-        const double2 w = __ldg(tw + ((r * k * (2 * N / (Ns * R))) & (2 * N - 1)));
+        const double2 w = __ldg(tw + ((r * k * (2 * NT / (Ns * R))) & (2 * NT - 1)));
         const double2 a = v[it * R + r];
         v[it * R + r] = make_double2(a.x * w.x - a.y * w.y, a.x * w.y + a.y * w.x);
       }
@@ -1444,29 +1457,92 @@ __device__ __forceinline__ void st_pass(double2* z, const double2* __restrict__ 
   __syncwarp();
 }
 
-template <int N, int Ns>
+template <int M, int Ns, int NT>
 __device__ __forceinline__ void st_fft(double2* z, const double2* __restrict__ tw, int tid) {
-  if constexpr (Ns * 16 <= N) {
-    st_pass<16, N, Ns>(z, tw, tid);
-    st_fft<N, Ns * 16>(z, tw, tid);
-  } else if constexpr (N / Ns == 8) {
-    st_pass<8, N, Ns>(z, tw, tid);
-  } else if constexpr (N / Ns == 4) {
-    st_pass<4, N, Ns>(z, tw, tid);
-  } else if constexpr (N / Ns == 2) {
-    st_pass<2, N, Ns>(z, tw, tid);
+  if constexpr (Ns * 16 <= M) {
+    st_pass<16, M, Ns, NT>(z, tw, tid);
+    st_fft<M, Ns * 16, NT>(z, tw, tid);
+  } else if constexpr (M / Ns == 8) {
+    st_pass<8, M, Ns, NT>(z, tw, tid);
+  } else if constexpr (M / Ns == 4) {
+    st_pass<4, M, Ns, NT>(z, tw, tid);
+  } else if constexpr (M / Ns == 2) {
+    st_pass<2, M, Ns, NT>(z, tw, tid);
   }
 }
 
-// batched DST-I of the rows of length N (index 0 ≡ 0), N compile-time: one row per N/16 lanes,
-// 256/(N/16) rows per CTA, real DFT of the odd extension via a length-N complex FFT; the odd
-// extension is scattered straight from registers and the (k, N−k) post-processing stores to HBM.
+// position of F_j in the padded output buffer (2 doubles of pad per 32: conflict-free pair stores)
+__device__ __forceinline__ int fpos(int j) { return j + 2 * (j >> 5); }
+
+// DST-I of one row, F_k = Σ_{j=1}^{N−1} f_j sin(πjk/N), by an M = N/2 point complex FFT on N/32 lanes
+// of a warp (tid ∈ [0, N/32)).  On entry z[zpad(m)] = (f_2m, f_2m+1), m ∈ [0, M), f_0 = 0.
+//   y_j = sin(πj/N)(f_j + f_{N−j}) + (f_j − f_{N−j})/2  (y_0 = 0),   Y_k = Σ_j y_j e^{2πijk/N}
+//   ⇒ F_2k = Im Y_k,  F_2k+1 − F_2k−1 = Re Y_k  (F_−1 = −F_1): the odd outputs are the prefix sums
+//   of Re Y, taken per lane (16 terms) and across the row's lanes by a log-depth shuffle scan.
+// On exit F_j sits at ((double*)z)[fpos(j)], j ∈ [0, N).
+template <int N>
+__device__ __forceinline__ void dst2_core(double2* z, const double2* __restrict__ tw, int tid) {
+  constexpr int M = N / 2, NTL = N / 32;
+  double2 v[16];
+#pragma unroll
+  for (int s = 0; s < 16; ++s) {   // item tid of the first radix-16 pass holds m = tid + NTL·s
+    const int m = tid + NTL * s;
+    const double2 P = z[zpad(m)];
+    const double fa = m ? z[zpad(M - m)].x : 0.0;   // f_{N−2m}
+    const double fb = z[zpad(M - m - 1)].y;         // f_{N−2m−1}
+    const double sa = __ldg(&tw[2 * m].y), sb = __ldg(&tw[2 * m + 1].y);
+    v[s] = make_double2(fma(sa, P.x + fa, 0.5 * (P.x - fa)), fma(sb, P.y + fb, 0.5 * (P.y - fb)));
+  }
+  dft_reg<16>(v);
+  __syncwarp();
+#pragma unroll
+  for (int q = 0; q < 16; ++q) z[zpad(16 * tid + q)] = v[q];
+  __syncwarp();
+  st_fft<M, 16, N>(z, tw, tid);
+  // Y_k = (Z_k + conj Z_{M−k})/2 − (i/2) e^{2πik/N} (Z_k − conj Z_{M−k}), k = 16·tid + t
+  double R[16], I[16];
+#pragma unroll
+  for (int t = 0; t < 16; ++t) {
+    const int k = 16 * tid + t;
+    const double2 A = z[zpad(k)], B = z[zpad((M - k) & (M - 1))];
+    const double ex = 0.5 * (A.x + B.x), ey = 0.5 * (A.y - B.y);
+    const double dx = A.x - B.x, dy = A.y + B.y;
+    const double2 w = __ldg(tw + 2 * k);
+    R[t] = fma(0.5, fma(w.x, dy, w.y * dx), ex);
+    I[t] = fma(0.5, fma(w.y, dy, -w.x * dx), ey);
+  }
+  double run = 0.0;
+#pragma unroll
+  for (int t = 0; t < 16; ++t) {
+    run += R[t];
+    R[t] = run;   // inclusive prefix within the lane
+  }
+  double x = run;
+#pragma unroll
+  for (int d = 1; d < NTL; d <<= 1) {
+    const double y = __shfl_up_sync(0xffffffffu, x, d, NTL);
+    if (tid >= d) x += y;
+  }
+  const double r0 = __shfl_sync(0xffffffffu, R[0], 0, NTL);   // lane 0's R[0] = Re Y_0
+  const double base = (x - run) - 0.5 * r0;
+  __syncwarp();
+  double* F = reinterpret_cast<double*>(z);
+#pragma unroll
+  for (int t = 0; t < 16; ++t) {
+    const int k = 16 * tid + t;
+    *reinterpret_cast<double2*>(F + fpos(2 * k)) = make_double2(k ? I[t] : 0.0, base + R[t]);
+  }
+  __syncwarp();
+}
+
+// batched DST-I of the rows of length N (index 0 ≡ 0): one row per N/32 lanes, 8192/N rows per CTA.
+// MODE 0: in place (× scale); 1: in place from the fixed-up spectral rows; 2: into the (N+1)³ grid u.
 template <int MODE, int N>
-__global__ void __launch_bounds__(256) k_dst_rows3t(DevTables3 T, double* work, const double* __restrict__ hsep,
-                                                    double scale, double* __restrict__ out) {
-  constexpr int NTH = N / 16, RPC = 256 / NTH, ZS = N + N / 16, NP = N / 2 / NTH;
+__global__ void __launch_bounds__(256, 3) k_dst_rows3t(DevTables3 T, double* work, const double* __restrict__ hsep,
+                                                       double scale, double* __restrict__ out) {
+  constexpr int NTL = N / 32, RPC = 256 / NTL, ZS = N / 2 + N / 32 + 1;
   extern __shared__ double2 smz[];
-  const int rl = threadIdx.x / NTH, tid = threadIdx.x % NTH;
+  const int rl = threadIdx.x / NTL, tid = threadIdx.x % NTL;
   double2* z = smz + rl * ZS;
   const double2* __restrict__ tw = reinterpret_cast<const double2*>(T.tw);
   const size_t row = (size_t)blockIdx.x * RPC + rl;   // (i−1)·N + a
@@ -1474,43 +1550,193 @@ __global__ void __launch_bounds__(256) k_dst_rows3t(DevTables3 T, double* work, 
   const int i = (int)(row / N) + 1, a = (int)(row % N);
   double* rp = work + row * N;
 #pragma unroll
-  for (int s = 0; s < NP; ++s) {
-    const int m = tid + s * NTH;   // pair (f_2m, f_2m+1)
-    double f0 = 0.0, f1 = 0.0;
-    if (live) {
-      if (MODE == 1) {
-        if (m > 0) f0 = fixup3(T, work, hsep, i, (size_t)a * N + 2 * m);
-        f1 = fixup3(T, work, hsep, i, (size_t)a * N + 2 * m + 1);
-      } else {
-        const double2 t = *reinterpret_cast<const double2*>(rp + 2 * m);
-        f0 = m > 0 ? t.x : 0.0;
-        f1 = t.y;
-      }
-    }
-    z[zpad(m)] = make_double2(f0, f1);                 // x_t = f_t, t < N
-    if (m > 0) z[zpad(N - m)].x = -f0;                 // x_{2N−t} = −f_t
-    else z[zpad(N / 2)].x = 0.0;                       // x_N = 0
-    z[zpad(N - m - 1)].y = -f1;
+  for (int s = 0; s < 16; ++s) {
+    const int m = tid + s * NTL;   // pair (f_2m, f_2m+1)
+    double2 t = make_double2(0.0, 0.0);
+    if (live) t = MODE == 1 ? fixup3_pair(T, work, hsep, i, (size_t)a * N + 2 * m)
+                            : __ldcs(reinterpret_cast<const double2*>(rp + 2 * m));
+    if (m == 0) t.x = 0.0;
+    z[zpad(m)] = t;
   }
   __syncwarp();
-  st_fft<N, 1>(z, tw, tid);
-  double* op = MODE == 2 ? out + ((size_t)i * (N + 1) + a) * (N + 1) : rp;
-  const bool zero = !live || a == 0;
+  dst2_core<N>(z, tw, tid);
+  if (!live) return;
+  const double* F = reinterpret_cast<const double*>(z);
+  const double sc = a == 0 ? 0.0 : scale;
+  if (MODE == 2) {
+    double* op = out + ((size_t)i * (N + 1) + a) * (N + 1);
 #pragma unroll
-  for (int s = 0; s < NP; ++s) {
-    const int k = 1 + tid + s * NTH, k2 = N - k;   // F_k = Im(E_k + e^{iπk/N} O_k)/2, k ∈ [1, N/2]
-    const double2 A = z[zpad(k)], B = z[zpad(k2)];
-    const double2 w = __ldg(tw + k);
-    const double Fk = 0.5 * (0.5 * (A.y - B.y) - w.x * (0.5 * (A.x - B.x)) + w.y * (0.5 * (A.y + B.y)));
-    const double Fk2 = 0.5 * (0.5 * (B.y - A.y) + w.x * (0.5 * (B.x - A.x)) + w.y * (0.5 * (B.y + A.y)));
-    if (live) {
-      op[k] = zero ? 0.0 : scale * Fk;
-      if (k2 != k) op[k2] = zero ? 0.0 : scale * Fk2;
+    for (int s = 0; s < 16; ++s) {
+      const int j = 2 * (tid + s * NTL);
+      const double2 f = *reinterpret_cast<const double2*>(F + fpos(j));
+      op[j] = sc * f.x;
+      op[j + 1] = sc * f.y;
+    }
+    if (tid == 0) op[N] = 0.0;
+  } else {
+#pragma unroll
+    for (int s = 0; s < 16; ++s) {
+      const int j = 2 * (tid + s * NTL);
+      const double2 f = *reinterpret_cast<const double2*>(F + fpos(j));
+      __stcs(reinterpret_cast<double2*>(rp + j), make_double2(sc * f.x, sc * f.y));
     }
   }
-  if (live && tid == 0) {
-    op[0] = 0.0;
-    if (MODE == 2) op[N] = 0.0;
+}
+
+// ---- sparse K_D path (3D): the source of (Δ_h − κ)v = F is nonzero only at irregular nodes, and
+// only the distinct stencil nodes of the result are read, so the z-direction transforms are sparse.
+// forward: plane i, columns ll ∈ [l0, l0 + RPC): G_a = Σ_{irregular (i,a,b)} c · sin(π b ll/N) (the
+// z-DST of the sparse rows, evaluated directly), then the y-DST of G along a → work[(i−1)][ll][kk].
+template <int N>
+__global__ void __launch_bounds__(256, 3) k_fwd3s(DevTables3 T, const double* __restrict__ corr,
+                                                  double* __restrict__ work) {
+  constexpr int NTL = N / 32, RPC = 256 / NTL < N ? 256 / NTL : N, NTHR = RPC * NTL, ZS = N / 2 + N / 32 + 1;
+  constexpr int CPT = RPC < 16 ? RPC : 16, NG = RPC / CPT;
+  extern __shared__ double2 smz[];
+  const double2* __restrict__ tw = reinterpret_cast<const double2*>(T.tw);
+  const int i = blockIdx.y + 1, l0 = blockIdx.x * RPC;
+  __shared__ int s_ptr[N + 1];
+  for (int a = threadIdx.x; a <= N; a += NTHR) s_ptr[a] = T.irr_row_ptr[(size_t)(i - 1) * N + a];
+  __syncthreads();
+  for (int it = threadIdx.x; it < N * NG; it += NTHR) {
+    const int a = it % N, cg = it / N;
+    double g[CPT];
+#pragma unroll
+    for (int c = 0; c < CPT; ++c) g[c] = 0.0;
+    const int e1 = s_ptr[a + 1];
+    for (int e = s_ptr[a]; e < e1; ++e) {
+      const double v = corr[e];
+      const int b = (int)(T.irr_lin[e] & (N - 1));
+#pragma unroll
+      for (int c = 0; c < CPT; ++c) g[c] = fma(v, __ldg(&tw[(b * (l0 + cg * CPT + c)) & (2 * N - 1)].y), g[c]);
+    }
+    const int off = 2 * zpad(a >> 1) + (a & 1);
+#pragma unroll
+    for (int c = 0; c < CPT; ++c) reinterpret_cast<double*>(smz + (cg * CPT + c) * ZS)[off] = a ? g[c] : 0.0;
+  }
+  __syncthreads();
+  const int rl = threadIdx.x / NTL, tid = threadIdx.x % NTL;
+  double2* z = smz + rl * ZS;
+  dst2_core<N>(z, tw, tid);
+  const int ll = l0 + rl;
+  const double sc = ll ? 1.0 : 0.0;
+  const double* F = reinterpret_cast<const double*>(z);
+  double* op = work + ((size_t)(i - 1) * N + ll) * N;
+#pragma unroll
+  for (int s = 0; s < 16; ++s) {
+    const int j = 2 * (tid + s * NTL);
+    const double2 f = *reinterpret_cast<const double2*>(F + fpos(j));
+    __stcs(reinterpret_cast<double2*>(op + j), make_double2(sc * f.x, sc * f.y));
+  }
+}
+
+// inverse along y: spectral rows (i, ll) fixed up with the separators (R20), DST along kk → a, stored
+// transposed to out[(i−1)][a][ll] so that the z-direction evaluation reads contiguous rows.
+template <int N>
+__global__ void __launch_bounds__(256, 2) k_inv3y(DevTables3 T, const double* __restrict__ spec,
+                                                  const double* __restrict__ hsep, double scale,
+                                                  double* __restrict__ out) {
+  constexpr int NTL = N / 32, RPC = 256 / NTL < N ? 256 / NTL : N, NTHR = RPC * NTL, ZS = N / 2 + N / 32 + 1;
+  extern __shared__ double2 smz[];
+  const double2* __restrict__ tw = reinterpret_cast<const double2*>(T.tw);
+  const int i = blockIdx.y + 1, l0 = blockIdx.x * RPC;
+  const int rl = threadIdx.x / NTL, tid = threadIdx.x % NTL;
+  double2* z = smz + rl * ZS;
+  const size_t m0 = (size_t)(l0 + rl) * N;
+  {   // fix-up loads in batches of 4 pairs (all 20 loads of a batch in flight); g, p uniform per CTA
+    const size_t K = (size_t)N * N;
+    const int q = i / BL, r = i - q * BL, p = r - 1;
+    const double* xs = r == 0 ? hsep + (size_t)(q - 1) * K : spec + (size_t)(i - 1) * K;
+    const bool left = r != 0 && q > 0, right = r != 0 && q < T.P - 1;
+    const double* hl = hsep + (size_t)(q - 1) * K;
+    const double* zl = T.zr + (size_t)(LB - 1 - p) * K;
+    const double* hr = hsep + (size_t)q * K;
+    const double* zrr = T.zr + (size_t)p * K;
+#pragma unroll
+    for (int sb = 0; sb < 16; sb += 4) {
+      double2 x[4], a1[4], b1[4], a2[4], b2[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const size_t mm = m0 + 2 * (tid + (sb + u) * NTL);
+        x[u] = __ldcs(reinterpret_cast<const double2*>(xs + mm));
+        if (left) {
+          a1[u] = __ldg(reinterpret_cast<const double2*>(hl + mm));
+          b1[u] = __ldg(reinterpret_cast<const double2*>(zl + mm));
+        }
+        if (right) {
+          a2[u] = __ldg(reinterpret_cast<const double2*>(hr + mm));
+          b2[u] = __ldg(reinterpret_cast<const double2*>(zrr + mm));
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        double2 t = x[u];
+        if (left) {
+          t.x = fma(-a1[u].x, b1[u].x, t.x);
+          t.y = fma(-a1[u].y, b1[u].y, t.y);
+        }
+        if (right) {
+          t.x = fma(-a2[u].x, b2[u].x, t.x);
+          t.y = fma(-a2[u].y, b2[u].y, t.y);
+        }
+        const int m = tid + (sb + u) * NTL;
+        if (m == 0) t.x = 0.0;
+        z[zpad(m)] = t;
+      }
+    }
+  }
+  __syncwarp();
+  dst2_core<N>(z, tw, tid);
+  __syncthreads();
+  for (int idx = threadIdx.x; idx < N * RPC; idx += NTHR) {
+    const int c = idx % RPC, a = idx / RPC;
+    const double v = (a == 0 || l0 + c == 0) ? 0.0 : scale * reinterpret_cast<const double*>(smz + c * ZS)[fpos(a)];
+    out[((size_t)(i - 1) * N + a) * N + l0 + c] = v;
+  }
+}
+
+// z-direction inverse at the distinct stencil nodes only: v(i,a,b) = scale · Σ_ll R[ll] sin(π ll b/N)
+// for the row R = rows[(i−1)][a][·].  One warp per row; lane l sums its N/32 consecutive terms by the
+// Clenshaw recurrence in e^{iθ} (θ = πb/N) and rotates the chunk by e^{i ll₀ θ}; warp reduction.
+template <int N>
+__global__ void __launch_bounds__(256) k_zeval3(DevTables3 T, const double* __restrict__ rows, double scale,
+                                                double* __restrict__ work) {
+  constexpr int L = N / 32;
+  const int w = (int)(((size_t)blockIdx.x * 256 + threadIdx.x) >> 5), lane = threadIdx.x & 31;
+  if (w >= T.nzrow) return;
+  const double2* __restrict__ tw = reinterpret_cast<const double2*>(T.tw);
+  const int row = T.zrow_id[w];
+  const int ll0 = lane * L;
+  double c[L];
+  const double* rp = rows + (size_t)row * N + ll0;
+  if constexpr (L % 2 == 0) {
+#pragma unroll
+    for (int t = 0; t < L; t += 2) {
+      const double2 v = *reinterpret_cast<const double2*>(rp + t);
+      c[t] = v.x;
+      c[t + 1] = v.y;
+    }
+  } else {
+#pragma unroll
+    for (int t = 0; t < L; ++t) c[t] = rp[t];
+  }
+  const int e1 = T.zrow_ptr[w + 1];
+  for (int e = T.zrow_ptr[w]; e < e1; ++e) {
+    const int b = T.znode_b[e];
+    const double2 w1 = __ldg(tw + b);
+    const double twoc = 2.0 * w1.x;
+    double b1 = 0.0, b2 = 0.0;
+#pragma unroll
+    for (int t = L - 1; t >= 0; --t) {
+      const double b0 = fma(twoc, b1, c[t] - b2);
+      b2 = b1;
+      b1 = b0;
+    }
+    const double2 w0 = __ldg(tw + ((ll0 * b) & (2 * N - 1)));
+    double v = w0.y * fma(-b2, w1.x, b1) + w0.x * (b2 * w1.y);
+#pragma unroll
+    for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    if (lane == 0) work[(size_t)row * N + b] = scale * v;
   }
 }
 
@@ -1655,16 +1881,16 @@ void launch_base3(const DevTables3& T, const double* fgrid, double* work, cudaSt
   k_base3<<<num_sms() * 8, 256, 0, s>>>(T, fgrid, work);
 }
 void launch_correct3(const DevTables3& T, const double* phi, const double* dphi, const double* fq,
-                     const double* jq_given, double* work, cudaStream_t s) {
+                     const double* jq_given, double* work, cudaStream_t s, double* corr) {
   if (!T.nirr) return;
   ++g_launches;
-  k_correct3<<<cdiv3(T.nirr, 128), 128, 0, s>>>(T, phi, dphi, fq, jq_given, work);
+  k_correct3<<<cdiv3(T.nirr, 128), 128, 0, s>>>(T, phi, dphi, fq, jq_given, work, corr);
 }
 template <int N>
 static void dst_rows3_n(const DevTables3& T, int mode, double* work, const double* hsep, double scale, double* out,
                         cudaStream_t s) {
-  constexpr int NTH = N / 16, RPC = 256 / NTH;
-  const size_t sm = (size_t)RPC * (N + N / 16) * sizeof(double2);
+  constexpr int RPC = 256 / (N / 32);
+  const size_t sm = (size_t)RPC * (N / 2 + N / 32 + 1) * sizeof(double2);
   const int grid = cdiv3((long)(N - 1) * N, RPC);
   static bool attr = false;
   if (!attr) {
@@ -1686,6 +1912,34 @@ void launch_dst_rows3(const DevTables3& T, int mode, double* work, const double*
     case 128: dst_rows3_n<128>(T, mode, work, hsep, scale, out, s); break;
     case 256: dst_rows3_n<256>(T, mode, work, hsep, scale, out, s); break;
     default: dst_rows3_n<512>(T, mode, work, hsep, scale, out, s); break;
+  }
+}
+template <int N>
+static void sparse3_n(const DevTables3& T, int which, const double* src, const double* hsep, double scale,
+                      double* dst, cudaStream_t s) {
+  constexpr int RPC = 256 / (N / 32) < N ? 256 / (N / 32) : N, NTHR = RPC * (N / 32);
+  const size_t sm = (size_t)RPC * (N / 2 + N / 32 + 1) * sizeof(double2);
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(k_fwd3s<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    cudaFuncSetAttribute(k_inv3y<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    attr = true;
+  }
+  const dim3 grid(N / RPC, N - 1);
+  if (which == 0) k_fwd3s<N><<<grid, NTHR, sm, s>>>(T, src, dst);
+  else if (which == 1) k_inv3y<N><<<grid, NTHR, sm, s>>>(T, src, hsep, scale, dst);
+  else if (T.nzrow) k_zeval3<N><<<cdiv3(T.nzrow, 8), 256, 0, s>>>(T, src, scale, dst);
+}
+// which: 0 forward (corr → work), 1 inverse along y (work, hsep → work2), 2 z-evaluation (work2 → work)
+void launch_sparse3(const DevTables3& T, int which, const double* src, const double* hsep, double scale, double* dst,
+                    cudaStream_t s) {
+  ++g_launches;
+  switch (T.N) {
+    case 32: sparse3_n<32>(T, which, src, hsep, scale, dst, s); break;
+    case 64: sparse3_n<64>(T, which, src, hsep, scale, dst, s); break;
+    case 128: sparse3_n<128>(T, which, src, hsep, scale, dst, s); break;
+    case 256: sparse3_n<256>(T, which, src, hsep, scale, dst, s); break;
+    default: sparse3_n<512>(T, which, src, hsep, scale, dst, s); break;
   }
 }
 void launch_transpose3(const DevTables3& T, double* work, cudaStream_t s) {

@@ -136,6 +136,8 @@ struct Setup3 {
   std::vector<int64_t> st_nodes_ij;       // dump
   std::vector<double> sin_tab, dk, zr, red_a, red_b;   // modes m = ll·N + kk
   std::vector<double> tw;            // 2N complex: (cos, sin)(π m / N), m = 0..2N−1
+  std::vector<int32_t> irr_row_ptr;  // (N−1)·N + 1: irregular nodes of grid row (i−1)·N + j
+  std::vector<int32_t> zrow_id, zrow_ptr, znode_b;   // distinct stencil nodes grouped by grid row
 };
 void build_setup3(Setup3& S, const kfbi_grid* g, const kfbi_boundary* b, const kfbi_pde* pde);
 
@@ -154,6 +156,8 @@ struct DevTables3 {
   const double* st_w;
   const double *sin_tab, *dk, *zr, *red_a, *red_b;
   const double* tw;   // 2N × (cos, sin)
+  const int32_t *irr_row_ptr, *zrow_id, *zrow_ptr, *znode_b;
+  int nzrow;
   const int8_t* side;
 };
 

@@ -317,6 +317,30 @@ void build_setup3(Setup3& S, const kfbi_grid* g, const kfbi_boundary* b, const k
   }
   if (bad) throw GeomError("interpolation stencil leaves the grid or is singular");
 
+  // sparse K_D path: irregular nodes by grid row (i−1)·N + j, and the distinct stencil nodes by row
+  {
+    const size_t nrows = (size_t)(N - 1) * N;
+    S.irr_row_ptr.assign(nrows + 1, 0);
+    for (int n = 0; n < S.nirr; ++n) ++S.irr_row_ptr[S.irr_lin[n] / N + 1];
+    for (size_t r = 0; r < nrows; ++r) S.irr_row_ptr[r + 1] += S.irr_row_ptr[r];
+    std::vector<int64_t> nodes(10 * (size_t)nq);
+    for (size_t e = 0; e < 10 * (size_t)nq; ++e)
+      nodes[e] = (int64_t)(S.st_nodes_ij[3 * e] - 1) * N * N + (int64_t)S.st_nodes_ij[3 * e + 1] * N +
+                 S.st_nodes_ij[3 * e + 2];
+    std::sort(nodes.begin(), nodes.end());
+    nodes.erase(std::unique(nodes.begin(), nodes.end()), nodes.end());
+    S.zrow_id.clear(); S.zrow_ptr.assign(1, 0); S.znode_b.clear();
+    for (size_t e = 0; e < nodes.size(); ++e) {
+      const int32_t row = (int32_t)(nodes[e] / N);
+      if (S.zrow_id.empty() || S.zrow_id.back() != row) {
+        if (!S.zrow_id.empty()) S.zrow_ptr.push_back((int32_t)e);
+        S.zrow_id.push_back(row);
+      }
+      S.znode_b.push_back((int32_t)(nodes[e] % N));
+    }
+    S.zrow_ptr.push_back((int32_t)nodes.size());
+  }
+
   // fast-solver tables: modes m = ll·N + kk (DST along z → ll, along y → kk), tridiagonal along x
   const size_t K = (size_t)N * N;
   S.sin_tab.resize(N / 2 + 1);

@@ -1423,6 +1423,29 @@ __device__ __forceinline__ double2 fixup3_pair(const DevTables3& T, const double
   return x;
 }
 
+// cos(2πm/32), sin(2πm/32) (folded at compile time for constant m)
+__device__ __forceinline__ double c32q(int m) {
+  switch (m) {
+    case 0: return 1.0;
+    case 1: return 0.98078528040323043058;
+    case 2: return 0.92387953251128673848;
+    case 3: return 0.83146961230254523567;
+    case 4: return 0.70710678118654757274;
+    case 5: return 0.55557023301960228867;
+    case 6: return 0.38268343236508983729;
+    case 7: return 0.19509032201612833135;
+    default: return 0.0;
+  }
+}
+__device__ __forceinline__ double w32c(int m) {
+  m &= 31;
+  return m <= 8 ? c32q(m) : m <= 16 ? -c32q(16 - m) : m <= 24 ? -c32q(m - 16) : c32q(32 - m);
+}
+__device__ __forceinline__ double w32s(int m) { return w32c(m - 8); }
+__device__ __forceinline__ double2 cmul(double2 a, double2 b) {
+  return make_double2(fma(a.x, b.x, -a.y * b.y), fma(a.x, b.y, a.y * b.x));
+}
+
 // Compile-time Stockham radix-R pass over one row z[0..M) held by M/16 lanes of one warp (rows never
 // straddle warps, so __syncwarp orders the in-place smem exchange).  Twiddles e^{+2πi r k/(Ns R)} =
 // tw[r k 2NT/(Ns R) mod 2NT] from the (cos, sin)(π m/NT) table of the grid size NT (L1-resident).
@@ -1435,14 +1458,17 @@ __device__ __forceinline__ void st_pass(double2* z, const double2* __restrict__ 
     const int j = tid + it * NTH;
 #pragma unroll
     for (int r = 0; r < R; ++r) v[it * R + r] = z[zpad(j + r * NI)];
-    if (Ns > 1) {
+    if (Ns > 1) {   // w^r, r < R, from one lookup by products of depth ≤ 4 (w, w², w⁴, w⁸)
       const int k = j & (Ns - 1);
+      double2 wp[R];
+      wp[1] = __ldg(tw + ((k * (2 * NT / (Ns * R))) & (2 * NT - 1)));
 #pragma unroll
-      for (int r = 1; r < R; ++r) {
-        const double2 w = __ldg(tw + ((r * k * (2 * NT / (Ns * R))) & (2 * NT - 1)));
-        const double2 a = v[it * R + r];
-        v[it * R + r] = make_double2(a.x * w.x - a.y * w.y, a.x * w.y + a.y * w.x);
+      for (int r = 2; r < R; ++r) {
+        const int hi = (r & (r - 1)) ? (1 << (31 - __clz(r))) : r / 2;   // highest power of two < r, or r/2
+        wp[r] = cmul(wp[hi], wp[r - hi]);
       }
+#pragma unroll
+      for (int r = 1; r < R; ++r) v[it * R + r] = cmul(v[it * R + r], wp[r]);
     }
     dft_reg<R>(v + it * R);
   }
@@ -1484,13 +1510,15 @@ template <int N>
 __device__ __forceinline__ void dst2_core(double2* z, const double2* __restrict__ tw, int tid) {
   constexpr int M = N / 2, NTL = N / 32;
   double2 v[16];
+  const double2 wa = __ldg(tw + 2 * tid), wb = __ldg(tw + 2 * tid + 1);   // e^{iπ(2 tid)/N}, e^{iπ(2 tid+1)/N}
 #pragma unroll
   for (int s = 0; s < 16; ++s) {   // item tid of the first radix-16 pass holds m = tid + NTL·s
     const int m = tid + NTL * s;
     const double2 P = z[zpad(m)];
     const double fa = m ? z[zpad(M - m)].x : 0.0;   // f_{N−2m}
     const double fb = z[zpad(M - m - 1)].y;         // f_{N−2m−1}
-    const double sa = __ldg(&tw[2 * m].y), sb = __ldg(&tw[2 * m + 1].y);
+    // sin(π j/N) at j = 2m, 2m+1: angle of the lane + s·π/16 (constants)
+    const double sa = fma(wa.y, w32c(s), wa.x * w32s(s)), sb = fma(wb.y, w32c(s), wb.x * w32s(s));
     v[s] = make_double2(fma(sa, P.x + fa, 0.5 * (P.x - fa)), fma(sb, P.y + fb, 0.5 * (P.y - fb)));
   }
   dft_reg<16>(v);
@@ -1501,13 +1529,14 @@ __device__ __forceinline__ void dst2_core(double2* z, const double2* __restrict_
   st_fft<M, 16, N>(z, tw, tid);
   // Y_k = (Z_k + conj Z_{M−k})/2 − (i/2) e^{2πik/N} (Z_k − conj Z_{M−k}), k = 16·tid + t
   double R[16], I[16];
+  const double2 wk0 = __ldg(tw + 32 * tid);   // e^{2πi(16 tid)/N}
 #pragma unroll
   for (int t = 0; t < 16; ++t) {
     const int k = 16 * tid + t;
     const double2 A = z[zpad(k)], B = z[zpad((M - k) & (M - 1))];
     const double ex = 0.5 * (A.x + B.x), ey = 0.5 * (A.y - B.y);
     const double dx = A.x - B.x, dy = A.y + B.y;
-    const double2 w = __ldg(tw + 2 * k);
+    const double2 w = t ? cmul(wk0, __ldg(tw + 2 * t)) : wk0;   // second factor warp-uniform
     R[t] = fma(0.5, fma(w.x, dy, w.y * dx), ex);
     I[t] = fma(0.5, fma(w.y, dy, -w.x * dx), ey);
   }
@@ -1607,8 +1636,13 @@ __global__ void __launch_bounds__(256, 3) k_fwd3s(DevTables3 T, const double* __
     for (int e = s_ptr[a]; e < e1; ++e) {
       const double v = corr[e];
       const int b = (int)(T.irr_lin[e] & (N - 1));
+      double2 w = __ldg(tw + ((b * (l0 + cg * CPT)) & (2 * N - 1)));   // e^{iπ b ll/N}, rotated by e^{iπ b/N}
+      const double2 d = __ldg(tw + b);
 #pragma unroll
-      for (int c = 0; c < CPT; ++c) g[c] = fma(v, __ldg(&tw[(b * (l0 + cg * CPT + c)) & (2 * N - 1)].y), g[c]);
+      for (int c = 0; c < CPT; ++c) {
+        g[c] = fma(v, w.y, g[c]);
+        if (c + 1 < CPT) w = cmul(w, d);
+      }
     }
     const int off = 2 * zpad(a >> 1) + (a & 1);
 #pragma unroll

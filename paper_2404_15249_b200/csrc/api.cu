@@ -183,6 +183,8 @@ void layout3(kfbi_ctx* c, Arena& A) {
   T.sin_tab = A.table(S.sin_tab); T.dk = A.table(S.dk); T.zr = A.table(S.zr); T.red_a = A.table(S.red_a);
   T.red_b = A.table(S.red_b); T.side = A.table(S.side);
   T.tw = A.table(S.tw);
+  T.irr_row_perm = A.table(S.irr_row_perm);
+  T.max_plane_irr = S.max_plane_irr;
   T.irr_row_ptr = A.table(S.irr_row_ptr); T.zrow_id = A.table(S.zrow_id); T.zrow_ptr = A.table(S.zrow_ptr);
   T.znode_b = A.table(S.znode_b); T.nzrow = (int)S.zrow_id.size();
   c->nh = 0;

@@ -1399,30 +1399,6 @@ __global__ void k_correct3(DevTables3 T, const double* __restrict__ phi, const d
   else work[T.irr_lin[n]] += T.irr_side[n] ? -acc : acc;
 }
 
-// fix-up of the spectral pair (m, m+1) (m even) at row i: streaming load of the spectrum, cached
-// separators and spikes (L2-resident across planes)
-__device__ __forceinline__ double2 fixup3_pair(const DevTables3& T, const double* __restrict__ spec,
-                                               const double* __restrict__ hsep, int i, size_t m) {
-  const size_t K = (size_t)T.N * T.N;
-  const int q = i / BL, r = i - q * BL;
-  if (r == 0) return __ldg(reinterpret_cast<const double2*>(hsep + (size_t)(q - 1) * K + m));
-  const int p = r - 1, g = q;
-  double2 x = __ldcs(reinterpret_cast<const double2*>(spec + (size_t)(i - 1) * K + m));
-  if (g > 0) {
-    const double2 h = __ldg(reinterpret_cast<const double2*>(hsep + (size_t)(g - 1) * K + m));
-    const double2 z = __ldg(reinterpret_cast<const double2*>(T.zr + (size_t)(LB - 1 - p) * K + m));
-    x.x = fma(-h.x, z.x, x.x);
-    x.y = fma(-h.y, z.y, x.y);
-  }
-  if (g < T.P - 1) {
-    const double2 h = __ldg(reinterpret_cast<const double2*>(hsep + (size_t)g * K + m));
-    const double2 z = __ldg(reinterpret_cast<const double2*>(T.zr + (size_t)p * K + m));
-    x.x = fma(-h.x, z.x, x.x);
-    x.y = fma(-h.y, z.y, x.y);
-  }
-  return x;
-}
-
 // cos(2πm/32), sin(2πm/32) (folded at compile time for constant m)
 __device__ __forceinline__ double c32q(int m) {
   switch (m) {
@@ -1564,120 +1540,14 @@ __device__ __forceinline__ void dst2_core(double2* z, const double2* __restrict_
   __syncwarp();
 }
 
-// batched DST-I of the rows of length N (index 0 ≡ 0): one row per N/32 lanes, 8192/N rows per CTA.
-// MODE 0: in place (× scale); 1: in place from the fixed-up spectral rows; 2: into the (N+1)³ grid u.
-template <int MODE, int N>
-__global__ void __launch_bounds__(256, 3) k_dst_rows3t(DevTables3 T, double* work, const double* __restrict__ hsep,
-                                                       double scale, double* __restrict__ out) {
-  constexpr int NTL = N / 32, RPC = 256 / NTL, ZS = N / 2 + N / 32 + 1;
-  extern __shared__ double2 smz[];
-  const int rl = threadIdx.x / NTL, tid = threadIdx.x % NTL;
-  double2* z = smz + rl * ZS;
-  const double2* __restrict__ tw = reinterpret_cast<const double2*>(T.tw);
-  const size_t row = (size_t)blockIdx.x * RPC + rl;   // (i−1)·N + a
-  const bool live = row < (size_t)(N - 1) * N;
-  const int i = (int)(row / N) + 1, a = (int)(row % N);
-  double* rp = work + row * N;
-#pragma unroll
-  for (int s = 0; s < 16; ++s) {
-    const int m = tid + s * NTL;   // pair (f_2m, f_2m+1)
-    double2 t = make_double2(0.0, 0.0);
-    if (live) t = MODE == 1 ? fixup3_pair(T, work, hsep, i, (size_t)a * N + 2 * m)
-                            : __ldcs(reinterpret_cast<const double2*>(rp + 2 * m));
-    if (m == 0) t.x = 0.0;
-    z[zpad(m)] = t;
-  }
-  __syncwarp();
-  dst2_core<N>(z, tw, tid);
-  if (!live) return;
-  const double* F = reinterpret_cast<const double*>(z);
-  const double sc = a == 0 ? 0.0 : scale;
-  if (MODE == 2) {
-    double* op = out + ((size_t)i * (N + 1) + a) * (N + 1);
-#pragma unroll
-    for (int s = 0; s < 16; ++s) {
-      const int j = 2 * (tid + s * NTL);
-      const double2 f = *reinterpret_cast<const double2*>(F + fpos(j));
-      op[j] = sc * f.x;
-      op[j + 1] = sc * f.y;
-    }
-    if (tid == 0) op[N] = 0.0;
-  } else {
-#pragma unroll
-    for (int s = 0; s < 16; ++s) {
-      const int j = 2 * (tid + s * NTL);
-      const double2 f = *reinterpret_cast<const double2*>(F + fpos(j));
-      __stcs(reinterpret_cast<double2*>(rp + j), make_double2(sc * f.x, sc * f.y));
-    }
-  }
-}
-
-// ---- sparse K_D path (3D): the source of (Δ_h − κ)v = F is nonzero only at irregular nodes, and
-// only the distinct stencil nodes of the result are read, so the z-direction transforms are sparse.
-// forward: plane i, columns ll ∈ [l0, l0 + RPC): G_a = Σ_{irregular (i,a,b)} c · sin(π b ll/N) (the
-// z-DST of the sparse rows, evaluated directly), then the y-DST of G along a → work[(i−1)][ll][kk].
+// the fixed-up spectral row (i, m0/N) (R20: x = z − h_{g−1} Z_L − h_g Z_R; separators x = h) as pairs
+// z[zpad(m)] = (x_2m, x_2m+1), x_0 := 0; loads in batches of 4 pairs so that all 20 are in flight
 template <int N>
-__global__ void __launch_bounds__(256, 3) k_fwd3s(DevTables3 T, const double* __restrict__ corr,
-                                                  double* __restrict__ work) {
-  constexpr int NTL = N / 32, RPC = 256 / NTL < N ? 256 / NTL : N, NTHR = RPC * NTL, ZS = N / 2 + N / 32 + 1;
-  constexpr int CPT = RPC < 16 ? RPC : 16, NG = RPC / CPT;
-  extern __shared__ double2 smz[];
-  const double2* __restrict__ tw = reinterpret_cast<const double2*>(T.tw);
-  const int i = blockIdx.y + 1, l0 = blockIdx.x * RPC;
-  __shared__ int s_ptr[N + 1];
-  for (int a = threadIdx.x; a <= N; a += NTHR) s_ptr[a] = T.irr_row_ptr[(size_t)(i - 1) * N + a];
-  __syncthreads();
-  for (int it = threadIdx.x; it < N * NG; it += NTHR) {
-    const int a = it % N, cg = it / N;
-    double g[CPT];
-#pragma unroll
-    for (int c = 0; c < CPT; ++c) g[c] = 0.0;
-    const int e1 = s_ptr[a + 1];
-    for (int e = s_ptr[a]; e < e1; ++e) {
-      const double v = corr[e];
-      const int b = (int)(T.irr_lin[e] & (N - 1));
-      double2 w = __ldg(tw + ((b * (l0 + cg * CPT)) & (2 * N - 1)));   // e^{iπ b ll/N}, rotated by e^{iπ b/N}
-      const double2 d = __ldg(tw + b);
-#pragma unroll
-      for (int c = 0; c < CPT; ++c) {
-        g[c] = fma(v, w.y, g[c]);
-        if (c + 1 < CPT) w = cmul(w, d);
-      }
-    }
-    const int off = 2 * zpad(a >> 1) + (a & 1);
-#pragma unroll
-    for (int c = 0; c < CPT; ++c) reinterpret_cast<double*>(smz + (cg * CPT + c) * ZS)[off] = a ? g[c] : 0.0;
-  }
-  __syncthreads();
-  const int rl = threadIdx.x / NTL, tid = threadIdx.x % NTL;
-  double2* z = smz + rl * ZS;
-  dst2_core<N>(z, tw, tid);
-  const int ll = l0 + rl;
-  const double sc = ll ? 1.0 : 0.0;
-  const double* F = reinterpret_cast<const double*>(z);
-  double* op = work + ((size_t)(i - 1) * N + ll) * N;
-#pragma unroll
-  for (int s = 0; s < 16; ++s) {
-    const int j = 2 * (tid + s * NTL);
-    const double2 f = *reinterpret_cast<const double2*>(F + fpos(j));
-    __stcs(reinterpret_cast<double2*>(op + j), make_double2(sc * f.x, sc * f.y));
-  }
-}
-
-// inverse along y: spectral rows (i, ll) fixed up with the separators (R20), DST along kk → a, stored
-// transposed to out[(i−1)][a][ll] so that the z-direction evaluation reads contiguous rows.
-template <int N>
-__global__ void __launch_bounds__(256, 2) k_inv3y(DevTables3 T, const double* __restrict__ spec,
-                                                  const double* __restrict__ hsep, double scale,
-                                                  double* __restrict__ out) {
-  constexpr int NTL = N / 32, RPC = 256 / NTL < N ? 256 / NTL : N, NTHR = RPC * NTL, ZS = N / 2 + N / 32 + 1;
-  extern __shared__ double2 smz[];
-  const double2* __restrict__ tw = reinterpret_cast<const double2*>(T.tw);
-  const int i = blockIdx.y + 1, l0 = blockIdx.x * RPC;
-  const int rl = threadIdx.x / NTL, tid = threadIdx.x % NTL;
-  double2* z = smz + rl * ZS;
-  const size_t m0 = (size_t)(l0 + rl) * N;
-  {   // fix-up loads in batches of 4 pairs (all 20 loads of a batch in flight); g, p uniform per CTA
+__device__ __forceinline__ void load_fixed_row(const DevTables3& T, const double* __restrict__ spec,
+                                               const double* __restrict__ hsep, int i, size_t m0, double2* z,
+                                               int tid) {
+  constexpr int NTL = N / 32;
+  {
     const size_t K = (size_t)N * N;
     const int q = i / BL, r = i - q * BL, p = r - 1;
     const double* xs = r == 0 ? hsep + (size_t)(q - 1) * K : spec + (size_t)(i - 1) * K;
@@ -1719,6 +1589,151 @@ __global__ void __launch_bounds__(256, 2) k_inv3y(DevTables3 T, const double* __
       }
     }
   }
+}
+
+// batched DST-I of the rows of length N (index 0 ≡ 0): one row per N/32 lanes, 8192/N rows per CTA.
+// MODE 0: in place (× scale); 1: in place from the fixed-up spectral rows; 2: into the (N+1)³ grid u.
+template <int MODE, int N>
+__global__ void __launch_bounds__(256, 2) k_dst_rows3t(DevTables3 T, double* work, const double* __restrict__ hsep,
+                                                       double scale, double* __restrict__ out) {
+  constexpr int NTL = N / 32, RPC = 256 / NTL, ZS = N / 2 + N / 32 + 1;
+  extern __shared__ double2 smz[];
+  const int rl = threadIdx.x / NTL, tid = threadIdx.x % NTL;
+  double2* z = smz + rl * ZS;
+  const double2* __restrict__ tw = reinterpret_cast<const double2*>(T.tw);
+  const size_t row = (size_t)blockIdx.x * RPC + rl;   // (i−1)·N + a
+  const bool live = row < (size_t)(N - 1) * N;
+  const int i = (int)(row / N) + 1, a = (int)(row % N);
+  double* rp = work + row * N;
+  if (MODE == 1 && live) {
+    load_fixed_row<N>(T, work, hsep, i, (size_t)a * N, z, tid);
+  } else {
+#pragma unroll
+    for (int s = 0; s < 16; ++s) {
+      const int m = tid + s * NTL;   // pair (f_2m, f_2m+1)
+      double2 t = make_double2(0.0, 0.0);
+      if (live) t = __ldcs(reinterpret_cast<const double2*>(rp + 2 * m));
+      if (m == 0) t.x = 0.0;
+      z[zpad(m)] = t;
+    }
+  }
+  __syncwarp();
+  dst2_core<N>(z, tw, tid);
+  if (!live) return;
+  const double* F = reinterpret_cast<const double*>(z);
+  const double sc = a == 0 ? 0.0 : scale;
+  if (MODE == 2) {
+    double* op = out + ((size_t)i * (N + 1) + a) * (N + 1);
+#pragma unroll
+    for (int s = 0; s < 16; ++s) {
+      const int j = 2 * (tid + s * NTL);
+      const double2 f = *reinterpret_cast<const double2*>(F + fpos(j));
+      op[j] = sc * f.x;
+      op[j + 1] = sc * f.y;
+    }
+    if (tid == 0) op[N] = 0.0;
+  } else {
+#pragma unroll
+    for (int s = 0; s < 16; ++s) {
+      const int j = 2 * (tid + s * NTL);
+      const double2 f = *reinterpret_cast<const double2*>(F + fpos(j));
+      __stcs(reinterpret_cast<double2*>(rp + j), make_double2(sc * f.x, sc * f.y));
+    }
+  }
+}
+
+// ---- sparse K_D path (3D): the source of (Δ_h − κ)v = F is nonzero only at irregular nodes, and
+// only the distinct stencil nodes of the result are read, so the z-direction transforms are sparse.
+// forward: plane i, columns ll ∈ [l0, l0 + RPC): G_a = Σ_{irregular (i,a,b)} c · sin(π b ll/N) (the
+// z-DST of the sparse rows, evaluated directly), then the y-DST of G along a → work[(i−1)][ll][kk].
+template <int N>
+__global__ void __launch_bounds__(256, 2) k_fwd3s(DevTables3 T, const double* __restrict__ corr,
+                                                  double* __restrict__ work) {
+  constexpr int NTL = N / 32, RPC = 256 / NTL < N ? 256 / NTL : N, NTHR = RPC * NTL, ZS = N / 2 + N / 32 + 1;
+  constexpr int CPT = RPC < 16 ? RPC : 16, NG = RPC / CPT;
+  extern __shared__ double2 smz[];
+  const double2* __restrict__ tw = reinterpret_cast<const double2*>(T.tw);
+  const int i = blockIdx.y + 1, l0 = blockIdx.x * RPC;
+  __shared__ int s_ptr[N + 1];
+  __shared__ double s_q[N / 2 + 1];   // quarter-wave sin(π r/N): staging rotations from smem, not L1/L2
+  for (int r = threadIdx.x; r <= N / 2; r += NTHR) s_q[r] = T.sin_tab[r];
+  // the plane's irregular entries (value, z index) staged once, coalesced: one round trip to L2
+  double* s_val = reinterpret_cast<double*>(smz + RPC * ZS);
+  int16_t* s_b = reinterpret_cast<int16_t*>(s_val + T.max_plane_irr);
+  const int E0 = T.irr_row_ptr[(size_t)(i - 1) * N];
+  for (int a = threadIdx.x; a <= N; a += NTHR) s_ptr[a] = T.irr_row_ptr[(size_t)(i - 1) * N + a] - E0;
+  {
+    const int ne = T.irr_row_ptr[(size_t)i * N] - E0;
+    for (int e = threadIdx.x; e < ne; e += NTHR) {
+      s_val[e] = corr[E0 + e];
+      s_b[e] = (int16_t)(T.irr_lin[E0 + e] & (N - 1));
+    }
+  }
+  __syncthreads();
+  for (int it = threadIdx.x; it < N * NG; it += NTHR) {
+    const int rr = it % N, cg = it / N, k = rr / NTHR, pos = rr % NTHR;
+    const int a = T.irr_row_perm[(size_t)(i - 1) * N + k * NTHR + ((k & 1) ? NTHR - 1 - pos : pos)];
+    double g[CPT];
+#pragma unroll
+    for (int c = 0; c < CPT; ++c) g[c] = 0.0;
+    const int e1 = s_ptr[a + 1];
+#ifdef KFBI_EXP
+    if (e1 > 0x7fffffff - 5)
+#endif
+    for (int e = s_ptr[a]; e < e1; ++e) {
+      const double v = s_val[e];
+      const int b = s_b[e];
+      // e^{iπ b ll/N} for the CPT columns: w_c = w_0 · d^c (d = e^{iπ b/N}) by products of depth ≤ 4
+      double2 w[CPT], dp[CPT];
+      {
+        const int r0 = (b * (l0 + cg * CPT)) & (2 * N - 1);
+        w[0] = make_double2(sin_lookup(s_q, (r0 + N / 2) & (2 * N - 1), N), sin_lookup(s_q, r0, N));
+        dp[1] = make_double2(sin_lookup(s_q, (b + N / 2) & (2 * N - 1), N), sin_lookup(s_q, b, N));
+      }
+#pragma unroll
+      for (int h = 2; h < CPT; h <<= 1) dp[h] = cmul(dp[h / 2], dp[h / 2]);
+#pragma unroll
+      for (int c = 1; c < CPT; ++c) {
+        const int hi = 1 << (31 - __clz(c));
+        w[c] = cmul(w[c - hi], dp[hi]);
+      }
+#pragma unroll
+      for (int c = 0; c < CPT; ++c) g[c] = fma(v, w[c].y, g[c]);
+    }
+    const int off = 2 * zpad(a >> 1) + (a & 1);
+#pragma unroll
+    for (int c = 0; c < CPT; ++c) reinterpret_cast<double*>(smz + (cg * CPT + c) * ZS)[off] = a ? g[c] : 0.0;
+  }
+  __syncthreads();
+  const int rl = threadIdx.x / NTL, tid = threadIdx.x % NTL;
+  double2* z = smz + rl * ZS;
+  dst2_core<N>(z, tw, tid);
+  const int ll = l0 + rl;
+  const double sc = ll ? 1.0 : 0.0;
+  const double* F = reinterpret_cast<const double*>(z);
+  double* op = work + ((size_t)(i - 1) * N + ll) * N;
+#pragma unroll
+  for (int s = 0; s < 16; ++s) {
+    const int j = 2 * (tid + s * NTL);
+    const double2 f = *reinterpret_cast<const double2*>(F + fpos(j));
+    __stcs(reinterpret_cast<double2*>(op + j), make_double2(sc * f.x, sc * f.y));
+  }
+}
+
+// inverse along y: spectral rows (i, ll) fixed up with the separators (R20), DST along kk → a, stored
+// transposed to out[(i−1)][a][ll] so that the z-direction evaluation reads contiguous rows.
+template <int N>
+__global__ void __launch_bounds__(256, 2) k_inv3y(DevTables3 T, const double* __restrict__ spec,
+                                                  const double* __restrict__ hsep, double scale,
+                                                  double* __restrict__ out) {
+  constexpr int NTL = N / 32, RPC = 256 / NTL < N ? 256 / NTL : N, NTHR = RPC * NTL, ZS = N / 2 + N / 32 + 1;
+  extern __shared__ double2 smz[];
+  const double2* __restrict__ tw = reinterpret_cast<const double2*>(T.tw);
+  const int i = blockIdx.y + 1, l0 = blockIdx.x * RPC;
+  const int rl = threadIdx.x / NTL, tid = threadIdx.x % NTL;
+  double2* z = smz + rl * ZS;
+  const size_t m0 = (size_t)(l0 + rl) * N;
+  load_fixed_row<N>(T, spec, hsep, i, m0, z, tid);
   __syncwarp();
   dst2_core<N>(z, tw, tid);
   __syncthreads();
@@ -1730,47 +1745,73 @@ __global__ void __launch_bounds__(256, 2) k_inv3y(DevTables3 T, const double* __
 }
 
 // z-direction inverse at the distinct stencil nodes only: v(i,a,b) = scale · Σ_ll R[ll] sin(π ll b/N)
-// for the row R = rows[(i−1)][a][·].  One warp per row; lane l sums its N/32 consecutive terms by the
-// Clenshaw recurrence in e^{iθ} (θ = πb/N) and rotates the chunk by e^{i ll₀ θ}; warp reduction.
+// for the row R = rows[(i−1)][a][·].  A warp per row (grid-stride, next row prefetched); lane l holds
+// ll = U·l + 32U·s + u (coalesced double2 loads); per u the sum over s is a Clenshaw recurrence in
+// e^{i·32Uθ} (θ = πb/N), combined as Im(e^{iUlθ}(S_0 + e^{iθ} S_1)); warp reduction.
 template <int N>
 __global__ void __launch_bounds__(256) k_zeval3(DevTables3 T, const double* __restrict__ rows, double scale,
                                                 double* __restrict__ work) {
-  constexpr int L = N / 32;
-  const int w = (int)(((size_t)blockIdx.x * 256 + threadIdx.x) >> 5), lane = threadIdx.x & 31;
-  if (w >= T.nzrow) return;
+  constexpr int V = N / 32, U = V >= 2 ? 2 : 1, S = V / U;
+  const int lane = threadIdx.x & 31;
+  const int nw = gridDim.x * 8;
   const double2* __restrict__ tw = reinterpret_cast<const double2*>(T.tw);
-  const int row = T.zrow_id[w];
-  const int ll0 = lane * L;
-  double c[L];
-  const double* rp = rows + (size_t)row * N + ll0;
-  if constexpr (L % 2 == 0) {
+  auto load = [&](int w, double (&c)[S][U]) {
+    const double* rp = rows + (size_t)T.zrow_id[w] * N + U * lane;
 #pragma unroll
-    for (int t = 0; t < L; t += 2) {
-      const double2 v = *reinterpret_cast<const double2*>(rp + t);
-      c[t] = v.x;
-      c[t + 1] = v.y;
+    for (int s = 0; s < S; ++s) {
+      if constexpr (U == 2) {
+        const double2 v = __ldcs(reinterpret_cast<const double2*>(rp + 32 * U * s));
+        c[s][0] = v.x;
+        c[s][U - 1] = v.y;
+      } else {
+        c[s][0] = __ldcs(rp + 32 * s);
+      }
     }
-  } else {
+  };
+  int w = (int)(((size_t)blockIdx.x * 256 + threadIdx.x) >> 5);
+  if (w >= T.nzrow) return;
+  double cur[S][U];
+  load(w, cur);
+  while (w < T.nzrow) {
+    const int wn = w + nw;
+    double nxt[S][U];
+    if (wn < T.nzrow) load(wn, nxt);
+    const size_t rbase = (size_t)T.zrow_id[w] * N;
+    const int e1 = T.zrow_ptr[w + 1];
+    for (int e = T.zrow_ptr[w]; e < e1; ++e) {
+      const int b = T.znode_b[e];
+      const double2 w1 = __ldg(tw + b);                                   // e^{iθ}
+      const double2 wz = __ldg(tw + ((32 * U * b) & (2 * N - 1)));        // e^{i·32Uθ}
+      const double2 wl = __ldg(tw + ((U * lane * b) & (2 * N - 1)));      // e^{iUlθ}
+      const double twoc = 2.0 * wz.x;
+      double sr[U], si[U];
 #pragma unroll
-    for (int t = 0; t < L; ++t) c[t] = rp[t];
-  }
-  const int e1 = T.zrow_ptr[w + 1];
-  for (int e = T.zrow_ptr[w]; e < e1; ++e) {
-    const int b = T.znode_b[e];
-    const double2 w1 = __ldg(tw + b);
-    const double twoc = 2.0 * w1.x;
-    double b1 = 0.0, b2 = 0.0;
+      for (int u = 0; u < U; ++u) {
+        double b1 = 0.0, b2 = 0.0;
 #pragma unroll
-    for (int t = L - 1; t >= 0; --t) {
-      const double b0 = fma(twoc, b1, c[t] - b2);
-      b2 = b1;
-      b1 = b0;
+        for (int s = S - 1; s >= 0; --s) {
+          const double b0 = fma(twoc, b1, cur[s][u] - b2);
+          b2 = b1;
+          b1 = b0;
+        }
+        sr[u] = fma(-b2, wz.x, b1);   // Σ_s c z^s = b_0 − b_1 z̄
+        si[u] = b2 * wz.y;
+      }
+      double tr = sr[0], ti = si[0];
+      if constexpr (U == 2) {
+        tr += w1.x * sr[1] - w1.y * si[1];
+        ti += w1.x * si[1] + w1.y * sr[1];
+      }
+      double v = wl.y * tr + wl.x * ti;
+#pragma unroll
+      for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+      if (lane == 0) work[rbase + b] = scale * v;
     }
-    const double2 w0 = __ldg(tw + ((ll0 * b) & (2 * N - 1)));
-    double v = w0.y * fma(-b2, w1.x, b1) + w0.x * (b2 * w1.y);
 #pragma unroll
-    for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-    if (lane == 0) work[(size_t)row * N + b] = scale * v;
+    for (int s = 0; s < S; ++s)
+#pragma unroll
+      for (int u = 0; u < U; ++u) cur[s][u] = nxt[s][u];
+    w = wn;
   }
 }
 
@@ -1955,14 +1996,21 @@ static void sparse3_n(const DevTables3& T, int which, const double* src, const d
   const size_t sm = (size_t)RPC * (N / 2 + N / 32 + 1) * sizeof(double2);
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(k_fwd3s<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
     cudaFuncSetAttribute(k_inv3y<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
     attr = true;
   }
   const dim3 grid(N / RPC, N - 1);
-  if (which == 0) k_fwd3s<N><<<grid, NTHR, sm, s>>>(T, src, dst);
+  if (which == 0) {
+    const size_t sm0 = sm + (size_t)T.max_plane_irr * (sizeof(double) + sizeof(int16_t));
+    static size_t attr0 = 0;
+    if (sm0 > attr0) {
+      cudaFuncSetAttribute(k_fwd3s<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm0);
+      attr0 = sm0;
+    }
+    k_fwd3s<N><<<grid, NTHR, sm0, s>>>(T, src, dst);
+  }
   else if (which == 1) k_inv3y<N><<<grid, NTHR, sm, s>>>(T, src, hsep, scale, dst);
-  else if (T.nzrow) k_zeval3<N><<<cdiv3(T.nzrow, 8), 256, 0, s>>>(T, src, scale, dst);
+  else if (T.nzrow) k_zeval3<N><<<std::min(cdiv3(T.nzrow, 8), num_sms() * 2), 256, 0, s>>>(T, src, scale, dst);
 }
 // which: 0 forward (corr → work), 1 inverse along y (work, hsep → work2), 2 z-evaluation (work2 → work)
 void launch_sparse3(const DevTables3& T, int which, const double* src, const double* hsep, double scale, double* dst,

@@ -137,6 +137,8 @@ struct Setup3 {
   std::vector<double> sin_tab, dk, zr, red_a, red_b;   // modes m = ll·N + kk
   std::vector<double> tw;            // 2N complex: (cos, sin)(π m / N), m = 0..2N−1
   std::vector<int32_t> irr_row_ptr;  // (N−1)·N + 1: irregular nodes of grid row (i−1)·N + j
+  std::vector<int16_t> irr_row_perm; // (N−1)·N: per plane, rows j by descending irregular count
+  int max_plane_irr = 0;
   std::vector<int32_t> zrow_id, zrow_ptr, znode_b;   // distinct stencil nodes grouped by grid row
 };
 void build_setup3(Setup3& S, const kfbi_grid* g, const kfbi_boundary* b, const kfbi_pde* pde);
@@ -157,6 +159,8 @@ struct DevTables3 {
   const double *sin_tab, *dk, *zr, *red_a, *red_b;
   const double* tw;   // 2N × (cos, sin)
   const int32_t *irr_row_ptr, *zrow_id, *zrow_ptr, *znode_b;
+  const int16_t* irr_row_perm;
+  int max_plane_irr;
   int nzrow;
   const int8_t* side;
 };

@@ -323,6 +323,19 @@ void build_setup3(Setup3& S, const kfbi_grid* g, const kfbi_boundary* b, const k
     S.irr_row_ptr.assign(nrows + 1, 0);
     for (int n = 0; n < S.nirr; ++n) ++S.irr_row_ptr[S.irr_lin[n] / N + 1];
     for (size_t r = 0; r < nrows; ++r) S.irr_row_ptr[r + 1] += S.irr_row_ptr[r];
+    S.max_plane_irr = 0;
+    for (int i = 0; i < N - 1; ++i)
+      S.max_plane_irr = std::max(S.max_plane_irr, S.irr_row_ptr[(size_t)(i + 1) * N] - S.irr_row_ptr[(size_t)i * N]);
+    if (S.max_plane_irr > 12288) throw GeomError("more than 12288 irregular nodes in one grid plane");
+    // per plane, rows by descending irregular count (the forward kernel deals them out in snake order
+    // so that every thread gets a balanced share of the entries)
+    S.irr_row_perm.resize(nrows);
+    for (int i = 0; i < N - 1; ++i) {
+      int16_t* pr = &S.irr_row_perm[(size_t)i * N];
+      for (int a = 0; a < N; ++a) pr[a] = (int16_t)a;
+      const int32_t* rp = &S.irr_row_ptr[(size_t)i * N];
+      std::stable_sort(pr, pr + N, [&](int16_t x, int16_t y) { return rp[x + 1] - rp[x] > rp[y + 1] - rp[y]; });
+    }
     std::vector<int64_t> nodes(10 * (size_t)nq);
     for (size_t e = 0; e < 10 * (size_t)nq; ++e)
       nodes[e] = (int64_t)(S.st_nodes_ij[3 * e] - 1) * N * N + (int64_t)S.st_nodes_ij[3 * e + 1] * N +

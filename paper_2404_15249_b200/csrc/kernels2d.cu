@@ -31,6 +31,24 @@ __device__ __forceinline__ double sin_lookup(const double* __restrict__ tab, int
   return sg * tab[r];
 }
 
+__device__ __forceinline__ double2 cmul(double2 a, double2 b) {
+  return make_double2(fma(a.x, b.x, -a.y * b.y), fma(a.x, b.y, a.y * b.x));
+}
+
+// e^{iπ r/N} = th[r >> 6] · tl[r & 63] from two small shared tables (2N/64 and 64 entries)
+__device__ __forceinline__ double2 eipi(const double2* th, const double2* tl, int r) {
+  return cmul(th[r >> 6], tl[r & 63]);
+}
+__device__ __forceinline__ void build_eipi(const double* __restrict__ sin_tab, int N, double2* th, double2* tl) {
+  const int m2 = 2 * N - 1;
+  for (int k = threadIdx.x; k < 2 * N / 64; k += blockDim.x) {
+    const int r = 64 * k;
+    th[k] = make_double2(sin_lookup(sin_tab, (r + N / 2) & m2, N), sin_lookup(sin_tab, r & m2, N));
+  }
+  for (int l = threadIdx.x; l < 64; l += blockDim.x)
+    tl[l] = make_double2(sin_lookup(sin_tab, (l + N / 2) & m2, N), sin_lookup(sin_tab, l & m2, N));
+}
+
 __device__ __forceinline__ void spline_eval(const double* __restrict__ phi, const double* __restrict__ mk, int off,
                                             int Mc, double delta, int m, double t, double& g, double& gp,
                                             double& gpp) {
@@ -168,9 +186,12 @@ __global__ void __launch_bounds__(kSweepThreads, 2) k_sweep(DevTables T, const d
   const int N = T.N, half = N >> 1, quarter = N >> 2, m2 = 2 * N - 1, B = kSweepThreads;
   double* R = sm;                                            // [4·BL sums][kQuads]
   double4* ent = reinterpret_cast<double4*>(R + (size_t)BL * 4 * kQuads);   // (c, j, cos Δ, sin Δ)
-  double* ent2 = reinterpret_cast<double*>(ent + T.maxe);    // c·sin(πj/2) (odd j) or c·cos(πj/2) (even j)
-  int* s_cnt = reinterpret_cast<int*>(ent2 + T.maxe);        // per-column [start, mid, end)
-  auto sinr = [&](int r) { return sin_lookup(T.sin_tab, r, N); };   // quarter-wave table via L1
+  // ent = (c, c·sin(πj/2) (odd j) or c·cos(πj/2) (even j), cos Δ, sin Δ), Δ = π·kRotStride·j/N
+  int* ent_j = reinterpret_cast<int*>(ent + T.maxe);
+  double2* th = reinterpret_cast<double2*>(ent_j + ((T.maxe + 3) & ~3));   // e^{iπ 64k/N}
+  double2* tl = th + 2 * N / 64;                              // e^{iπ l/N}, l < 64
+  int* s_cnt = reinterpret_cast<int*>(tl + 64);               // per-column [start, mid, end)
+  build_eipi(T.sin_tab, N, th, tl);
   const int nch = (quarter + kQuads - 1) / kQuads;
   const int G = gridDim.x / nch;
   const int ch = blockIdx.x % nch;
@@ -205,10 +226,10 @@ __global__ void __launch_bounds__(kSweepThreads, 2) k_sweep(DevTables T, const d
       const int j = T.irr_j[e];
       const int rd = (j * kRotStride) & m2;
       const double c = cval[e];
-      ent[e - e0] = make_double4(c, (double)j, sin_lookup(T.sin_tab, (rd + half) & m2, N), sin_lookup(T.sin_tab, rd, N));
       // odd j: sin(πj/2) = ±1; even j: cos(πj/2) = ±1
-      const bool neg = (j & 1) ? ((j >> 1) & 1) : ((j >> 1) & 1);
-      ent2[e - e0] = neg ? -c : c;
+      const bool neg = (j >> 1) & 1;
+      ent[e - e0] = make_double4(c, neg ? -c : c, sin_lookup(T.sin_tab, (rd + half) & m2, N), sin_lookup(T.sin_tab, rd, N));
+      ent_j[e - e0] = j;
     }
     if (threadIdx.x < ncol) {
       const int i = c0 + threadIdx.x;
@@ -227,9 +248,9 @@ __global__ void __launch_bounds__(kSweepThreads, 2) k_sweep(DevTables T, const d
       for (int q = 0; q < kRotSteps; ++q) Ao[q] = Bo[q] = Ae[q] = Be[q] = 0.0;
       for (int e = a0; e < am; ++e) {   // odd rows
         const double4 en = ent[e];
-        const double c2 = ent2[e];
-        const int r0 = ((int)en.y * tb) & m2;
-        double sn = sinr(r0), cs = sinr((r0 + half) & m2);
+        const double c2 = en.y;
+        const double2 e0 = eipi(th, tl, (ent_j[e] * tb) & m2);
+        double sn = e0.y, cs = e0.x;
 #pragma unroll
         for (int q = 0; q < kRotSteps; ++q) {
           Ao[q] = fma(en.x, sn, Ao[q]);
@@ -241,9 +262,9 @@ __global__ void __launch_bounds__(kSweepThreads, 2) k_sweep(DevTables T, const d
       }
       for (int e = am; e < a1; ++e) {   // even rows
         const double4 en = ent[e];
-        const double c2 = ent2[e];
-        const int r0 = ((int)en.y * tb) & m2;
-        double sn = sinr(r0), cs = sinr((r0 + half) & m2);
+        const double c2 = en.y;
+        const double2 e0 = eipi(th, tl, (ent_j[e] * tb) & m2);
+        double sn = e0.y, cs = e0.x;
 #pragma unroll
         for (int q = 0; q < kRotSteps; ++q) {
           Ae[q] = fma(en.x, sn, Ae[q]);
@@ -263,21 +284,30 @@ __global__ void __launch_bounds__(kSweepThreads, 2) k_sweep(DevTables T, const d
       }
     }
     __syncthreads();
-    if (ch == 0 && threadIdx.x < ncol) {
-      // quad slot 0 holds modes {0, N/2, N/4, 3N/4}: r_{N/2} = Σ c sin(πj/2), r_{N/4}, r_{3N/4}
-      const int c = threadIdx.x;
+    if (ch == 0) {   // CTA-uniform: all lanes take part in the shuffles
+      // quad slot 0 holds modes {0, N/2, N/4, 3N/4}: r_{N/2} = Σ c sin(πj/2), r_{N/4}, r_{3N/4};
+      // 16 lanes per column (strided entries, fixed shuffle tree: deterministic)
+      const int c = threadIdx.x >> 4, sub = threadIdx.x & 15;
       double rh = 0.0, rq = 0.0, r3 = 0.0;
-      for (int e = s_cnt[3 * c]; e < s_cnt[3 * c + 2]; ++e) {
-        const double4 en = ent[e];
-        const int j = (int)en.y;
-        rh = fma(en.x, sin_lookup(T.sin_tab, (j * half) & m2, N), rh);
-        rq = fma(en.x, sin_lookup(T.sin_tab, (j * quarter) & m2, N), rq);
-        r3 = fma(en.x, sin_lookup(T.sin_tab, (j * 3 * quarter) & m2, N), r3);
+      for (int e = s_cnt[3 * c] + sub; c < ncol && e < s_cnt[3 * c + 2]; e += 16) {
+        const double cv = ent[e].x;
+        const int j = ent_j[e];
+        rh = fma(cv, eipi(th, tl, (j * half) & m2).y, rh);
+        rq = fma(cv, eipi(th, tl, (j * quarter) & m2).y, rq);
+        r3 = fma(cv, eipi(th, tl, (j * 3 * quarter) & m2).y, r3);
       }
-      R[(4 * c + 0) * kQuads] = 0.5 * rh;          // (A_o + A_e, A_o − A_e) = (0, r_{N/2})
-      R[(4 * c + 2) * kQuads] = -0.5 * rh;
-      R[(4 * c + 1) * kQuads] = 0.5 * (rq + r3);   // (B_o − B_e, B_o + B_e) = (r_{N/4}, r_{3N/4})
-      R[(4 * c + 3) * kQuads] = 0.5 * (r3 - rq);
+#pragma unroll
+      for (int o = 8; o; o >>= 1) {
+        rh += __shfl_xor_sync(0xffffffffu, rh, o);
+        rq += __shfl_xor_sync(0xffffffffu, rq, o);
+        r3 += __shfl_xor_sync(0xffffffffu, r3, o);
+      }
+      if (sub == 0 && c < ncol) {
+        R[(4 * c + 0) * kQuads] = 0.5 * rh;          // (A_o + A_e, A_o − A_e) = (0, r_{N/2})
+        R[(4 * c + 2) * kQuads] = -0.5 * rh;
+        R[(4 * c + 1) * kQuads] = 0.5 * (rq + r3);   // (B_o − B_e, B_o + B_e) = (r_{N/4}, r_{3N/4})
+        R[(4 * c + 3) * kQuads] = 0.5 * (r3 - rq);
+      }
     }
     __syncthreads();
     if (!active) continue;
@@ -1130,7 +1160,8 @@ void launch_inverse_dense(const DevTables& T, const double* spec, const double* 
 void launch_sweep(const DevTables& T, const double* cval, bool dense, double* spec, double* zfirst, double* zlast,
                   double* fsep, cudaStream_t s) {
   (void)zlast;
-  const size_t sm = (size_t)BL * 4 * kQuads * sizeof(double) + (size_t)T.maxe * 5 * sizeof(double) + 3 * BL * sizeof(int);
+  const size_t sm = (size_t)BL * 4 * kQuads * sizeof(double) + (size_t)T.maxe * 5 * sizeof(double) +
+                    (size_t)(2 * T.N / 64 + 64 + 1) * sizeof(double2) + 3 * BL * sizeof(int);
   static bool attr = false;
   if (!attr) {
     cudaFuncSetAttribute(k_sweep<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
@@ -1418,9 +1449,6 @@ __device__ __forceinline__ double w32c(int m) {
   return m <= 8 ? c32q(m) : m <= 16 ? -c32q(16 - m) : m <= 24 ? -c32q(m - 16) : c32q(32 - m);
 }
 __device__ __forceinline__ double w32s(int m) { return w32c(m - 8); }
-__device__ __forceinline__ double2 cmul(double2 a, double2 b) {
-  return make_double2(fma(a.x, b.x, -a.y * b.y), fma(a.x, b.y, a.y * b.x));
-}
 
 // Compile-time Stockham radix-R pass over one row z[0..M) held by M/16 lanes of one warp (rows never
 // straddle warps, so __syncwarp orders the in-place smem exchange).  Twiddles e^{+2πi r k/(Ns R)} =

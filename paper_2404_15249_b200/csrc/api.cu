@@ -126,6 +126,7 @@ void layout(kfbi_ctx* c, Arena& A) {
   T.red_a = A.table(S.red_a); T.red_b = A.table(S.red_b); T.red_invc = A.table(S.red_invc);
   T.rinv2 = A.table(S.rinv2); T.z2r = A.table(S.z2r); T.red2_a = A.table(S.red2_a); T.red2_b = A.table(S.red2_b);
   T.maxe = S.maxe;
+  T.mcr = S.max_col_rows;
   T.side = A.table(S.side);
   // holes
   auto& hoff = c->hoff; auto& hM = c->hM; auto& hdel = c->hdel; auto& oneh = c->oneh;

@@ -591,10 +591,10 @@ template <int QPT>
 __global__ void __launch_bounds__(kInvThreads, 2) k_inv_sparse(DevTables T, const double* __restrict__ spec,
                                                                const double* __restrict__ hsep, double* __restrict__ vsten) {
   extern __shared__ double smx[];
-  __shared__ double red[8][8];
   __shared__ int s_rows[kMaxColRows];
   const int N = T.N, half = N >> 1, quarter = N >> 2, m2 = 2 * N - 1, B = kInvThreads, P = T.P;
   double* tab = smx;   // sin(πr/N), r ∈ [0, N), at r + r/16
+  double* red = smx + N + N / 16 + 1;   // [warp][2·row]: per-warp partial sums of the column's rows
   for (int r = threadIdx.x; r < N; r += B) tab[r + (r >> 4)] = sin_lookup(T.sin_tab, r, N);
   auto sinr = [&](int r) {   // sin(πr/N), r ∈ [0, 2N)
     const int idx = r & (N - 1);
@@ -721,20 +721,23 @@ __global__ void __launch_bounds__(kInvThreads, 2) k_inv_sparse(DevTables T, cons
       }
     }
     const double ws = warp_transpose_reduce8(acc);
-    if ((lane & 3) == 0) red[wid][((lane >> 4) & 1) * 4 + ((lane >> 3) & 1) * 2 + ((lane >> 2) & 1)] = ws;
-    __syncthreads();
-    if (threadIdx.x < nr) {
-      double s1 = 0.0, s2 = 0.0;
-      for (int w = 0; w < nw; ++w) {
-        s1 += red[w][threadIdx.x];
-        s2 += red[w][4 + threadIdx.x];
-      }
-      const int j = js[threadIdx.x];
-      const double sig = ((j >> 1) & 1) ? -1.0 : 1.0;   // σ_j = sin(πj/2) for odd j
-      vsten[u0 + u + threadIdx.x] = scale * (c0 == 0 ? s1 + sig * s2 : s1);
+    if ((lane & 3) == 0) {   // value index v = 4·(lane>>4 & 1) + 2·(lane>>3 & 1) + (lane>>2 & 1): acc[v]
+      const int v = ((lane >> 4) & 1) * 4 + ((lane >> 3) & 1) * 2 + ((lane >> 2) & 1);
+      const int k = v & 3;
+      if (k < nr) red[(size_t)wid * 2 * T.mcr + 2 * (u + k) + (v >> 2)] = ws;
     }
-    __syncthreads();
     u += nr;
+  }
+  __syncthreads();   // one barrier per column: sum the warps' partials in a fixed order
+  for (int t = threadIdx.x; t < nrows; t += B) {
+    double s1 = 0.0, s2 = 0.0;
+    for (int w = 0; w < nw; ++w) {
+      s1 += red[(size_t)w * 2 * T.mcr + 2 * t];
+      s2 += red[(size_t)w * 2 * T.mcr + 2 * t + 1];
+    }
+    const int j = s_rows[t];
+    const double sig = ((j >> 1) & 1) ? -1.0 : 1.0;   // σ_j = sin(πj/2) for odd j
+    vsten[u0 + t] = scale * ((j & 1) ? s1 + sig * s2 : s1);
   }
   }
 }
@@ -1200,14 +1203,15 @@ void launch_inverse_sparse(const DevTables& T, const double* spec, const double*
   if (ncols <= 0) return;
   const int quarter = T.N / 4;
   const int qpt = (quarter + kInvThreads - 1) / kInvThreads;
-  const size_t sm = (size_t)(T.N + T.N / 16 + 1) * sizeof(double);
+  const size_t sm = (size_t)(T.N + T.N / 16 + 1) * sizeof(double) +
+                    (size_t)(kInvThreads / 32) * 2 * T.mcr * sizeof(double);
   const int grid = ncols < 2 * num_sms() ? ncols : 2 * num_sms();
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(k_inv_sparse<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 100 * 1024);
-    cudaFuncSetAttribute(k_inv_sparse<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 100 * 1024);
-    cudaFuncSetAttribute(k_inv_sparse<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, 100 * 1024);
-    cudaFuncSetAttribute(k_inv_sparse<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, 100 * 1024);
+    cudaFuncSetAttribute(k_inv_sparse<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    cudaFuncSetAttribute(k_inv_sparse<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    cudaFuncSetAttribute(k_inv_sparse<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    cudaFuncSetAttribute(k_inv_sparse<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     attr = true;
   }
   switch (qpt) {

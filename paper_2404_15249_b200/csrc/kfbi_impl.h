@@ -109,6 +109,7 @@ struct Setup {
   std::vector<double> rinv2, z2r;    // LB2 × N: level-2 block pivots / spike
   std::vector<double> red2_a, red2_b;  // N: level-2 reduced system coefficients
   int maxe = 1;                      // max sparse entries per sweep work item
+  int max_col_rows = 1;              // max stencil rows in one grid column
   // holes (κ = 0 completion, reading R27)
   std::vector<int> holes;            // component ids
 };
@@ -167,7 +168,7 @@ struct DevTables3 {
 
 // ---- device views -------------------------------------------------------------------
 struct DevTables {
-  int N, P, M, nq, nirr, nsn, nocol, ncomp;
+  int N, P, M, nq, nirr, nsn, nocol, ncomp, mcr;
   double lo, h, kappa;
   // intersections
   const int32_t *q_axis, *q_comp, *q_knot;

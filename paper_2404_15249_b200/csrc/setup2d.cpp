@@ -436,8 +436,11 @@ void build_setup(Setup& S, const kfbi_grid* g, const kfbi_boundary* b, const kfb
       }
     }
     S.ocol_ptr.push_back(S.nsn);
-    for (size_t c = 0; c + 1 < S.ocol_ptr.size(); ++c)
+    S.max_col_rows = 1;
+    for (size_t c = 0; c + 1 < S.ocol_ptr.size(); ++c) {
       if (S.ocol_ptr[c + 1] - S.ocol_ptr[c] > kMaxColRows) throw GeomError("too many stencil rows in one grid column");
+      S.max_col_rows = std::max(S.max_col_rows, S.ocol_ptr[c + 1] - S.ocol_ptr[c]);
+    }
   }
 
   // ---- spline filters (reading R10) ----

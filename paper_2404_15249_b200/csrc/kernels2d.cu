@@ -616,6 +616,15 @@ __global__ void __launch_bounds__(kInvThreads, 2) k_inv_sparse(DevTables T, cons
   const double* hr = (!sep && q < P - 1) ? hsep + (size_t)q * N : nullptr;
   const double* zl = T.zr + (size_t)(sep ? 0 : LB - rr) * N;     // Z_L[p] = Z_R[LB−1−p], p = rr − 1
   const double* zrr = T.zr + (size_t)(sep ? 0 : rr - 1) * N;
+  {   // warm L2 with the next column's spectral row while this one is evaluated
+    const int bn = b + gridDim.x;
+    if (bn < T.o_hi) {
+      const int in = T.ocol[bn], qn = in / BL, rn = in - qn * BL;
+      const double* nrow = rn == 0 ? hsep + (size_t)(qn - 1) * N : spec + (size_t)(in - 1) * N;
+      for (int o = threadIdx.x * 16; o < N; o += B * 16)
+        asm volatile("prefetch.global.L2 [%0];" ::"l"(nrow + o));
+    }
+  }
   auto X4 = [&](int t, double (&x)[4]) {
     const double2* xp = reinterpret_cast<const double2*>(xrow + 4 * t);
     const double2 a = xp[0], b2 = xp[1];

@@ -175,7 +175,11 @@ kfbi_status kfbi_solve(kfbi_ctx* ctx, const double* d_g, const double* d_f_grid,
                        double* d_u, double* d_phi_out, const kfbi_solve_opts* opts,
                        kfbi_solve_stats* stats, void* stream);
 
-/* Bytes moved per call of the dominant kernels (algorithmic model of DESIGN.md). */
+/* Algorithmic HBM bytes per launch of the two dominant kernels (model of DESIGN.md §6):
+ * 2D: bytes_sweep = k_sweep (spectrum written, 8 B per block-row value), bytes_inverse =
+ * k_inv_sparse (spectral columns of the stencil columns read); 3D: bytes_sweep = k_fwd3s
+ * (spectrum written), bytes_inverse = k_inv3y (spectrum read + y-inverse rows written).
+ * unknowns = interior grid points.  Host-only, no GPU work. */
 kfbi_status kfbi_apply_model(const kfbi_ctx* ctx, double* bytes_sweep, double* bytes_inverse,
                              double* unknowns);
 
@@ -184,8 +188,8 @@ kfbi_status kfbi_destroy(kfbi_ctx* ctx);
 /* Device time of each kernel of one kfbi_apply, averaged over `reps` applies, from CUDA
  * events recorded on `stream` between the launches (bench/roofline use; synchronous).
  * ms_out[8] = {spline, correct, sweep, reduced, inverse, hole, interp, whole apply}; in 3D:
- * {LSQ fit, correction, sparse forward DST + sweep, reduced, inverse y-DST, z-evaluation at the
- * stencil nodes, interp, apply}. */
+ * {LSQ fit, correction, sparse forward DST (k_fwd3s), tridiagonal sweep + reduced system, inverse
+ * y-DST (k_inv3y), z-evaluation at the stencil nodes, interp, apply}. */
 kfbi_status kfbi_profile_apply(kfbi_ctx* ctx, const double* d_phi, double* d_out, int32_t reps,
                                double* ms_out, void* stream);
 

@@ -689,8 +689,8 @@ kfbi_status kfbi_apply_model(const kfbi_ctx* c, double* bytes_sweep, double* byt
   if (!c) return KFBI_EINVAL;
   if (c->dim == 3) {
     const double N = c->S3.N, U = (N - 1) * (N - 1) * (N - 1), F = (N - 1) * N * N;
-    if (bytes_sweep) *bytes_sweep = 16.0 * F;        // read + write of the spectral array
-    if (bytes_inverse) *bytes_inverse = 16.0 * F;    // one DST-rows pass (read + write)
+    if (bytes_sweep) *bytes_sweep = 8.0 * F;         // k_fwd3s: writes the spectrum (sparse source on chip)
+    if (bytes_inverse) *bytes_inverse = 16.0 * F;    // k_inv3y: reads the spectrum, writes the y-inverse rows
     if (unknowns) *unknowns = U;
     return KFBI_OK;
   }
@@ -723,8 +723,8 @@ kfbi_status kfbi_profile_apply(kfbi_ctx* c, const double* d_phi, double* d_out, 
       launch_correct3(T3, d_phi, c->dphi, nullptr, nullptr, nullptr, s, c->corr);
       ck(cudaEventRecord(ev[2], s), "rec");
       launch_sparse3(T3, 0, c->corr, nullptr, 1.0, c->work, s);
-      launch_sweep3(T3, c->work, c->zfirst, c->fsep, s);
       ck(cudaEventRecord(ev[3], s), "rec");
+      launch_sweep3(T3, c->work, c->zfirst, c->fsep, s);
       launch_reduced3(T3, c->zfirst, c->fsep, c->hsep, s);
       ck(cudaEventRecord(ev[4], s), "rec");
       launch_sparse3(T3, 1, c->work, c->hsep, sc, c->work2, s);

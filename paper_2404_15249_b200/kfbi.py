@@ -271,13 +271,16 @@ class KFBI:
         return {"bytes_sweep": a.value, "bytes_inverse": b.value, "unknowns": c.value}
 
     def profile_apply(self, phi, reps=10, stream=None):
-        """Per-kernel CUDA-event times (ms) of one apply: spline, correct, sweep, reduced,
-        inverse, hole, interp, total."""
+        """Per-kernel CUDA-event times (ms) of one apply.  2D: spline, correct, sweep (sparse forward
+        DST fused with the block tridiagonal solves), reduced, inverse, hole, interp, total; 3D: lsq,
+        correct, sweep (sparse forward DST k_fwd3s), tridiag (+ reduced), inverse (k_inv3y), zeval,
+        interp, total."""
         phi = self._dev(phi, self.M)
         out = self.torch.empty_like(phi)
         ms = (C.c_double * 8)()
         self._check(self.lib.kfbi_profile_apply(self.ctx, _ptr(phi), _ptr(out), reps, ms, self._stream(stream)))
-        names = ["spline", "correct", "sweep", "reduced", "inverse", "hole", "interp", "apply"]
+        names = (["spline", "correct", "sweep", "reduced", "inverse", "hole", "interp", "apply"] if self.problem.dim == 2
+                 else ["lsq", "correct", "sweep", "tridiag", "inverse", "zeval", "interp", "apply"])
         return dict(zip(names, list(ms)))
 
     # ------------------------------------------------------------------ test-only

@@ -59,17 +59,27 @@ def test_fast_solve_matches_oracle(n, kappa):
     assert np.all(v[0] == 0) and np.all(v[:, -1] == 0)
 
 
-def test_fast_solve_eigenfunction_full_size():
+@pytest.mark.parametrize("p,q", [(1234, 3001), (3, 4001)])
+def test_fast_solve_eigenfunction_full_size(p, q):
+    """A discrete eigenfunction sin(πpi/N) sin(πqj/N) of Δ_h is reproduced at N = 8192.  For a
+    stiff pair (one index near N/2, the other tiny) the forward transform's rounding leaks
+    ε·|f̂| into the low modes, which (Δ_h)⁻¹ amplifies by ~N²: there the bound is the FP64
+    error of the same algorithm on the CPU oracle (scipy DST-I + Thomas), not a fixed 1e-10."""
     n = 8192
     prob = W.problem("box8192", 2, n, [W.ellipse(1.0, 0.8)], 0.0)
     k = gpu(prob)
     h = prob.h
     i = np.arange(n + 1)
-    p, q = 3, 4001
     S = np.outer(np.sin(np.pi * p * i / n), np.sin(np.pi * q * i / n))
     lam = -4 / h ** 2 * (np.sin(np.pi * p / (2 * n)) ** 2 + np.sin(np.pi * q / (2 * n)) ** 2)
     v = k.test_fast_solve(lam * S).cpu().numpy()
-    assert np.abs(v - S).max() < 1e-10
+    err = np.abs(v - S).max()
+    if min(p, q) > 100:
+        assert err < 1e-10
+    else:
+        ref = fastsolve.solve2d((lam * S)[1:n, 1:n], h, 0.0)
+        err_oracle = np.abs(ref - S[1:n, 1:n]).max()
+        assert err < 8 * err_oracle + 1e-13, (err, err_oracle)
 
 
 # ------------------------------------------------------------------ interface solve witness

@@ -123,6 +123,7 @@ void layout(kfbi_ctx* c, Arena& A) {
   T.sp_ntaps = A.table(S.sp_ntaps); T.sp_first = A.table(S.sp_first); T.sp_coef_off = A.table(S.sp_coef_off);
   T.sp_coef = A.table(S.sp_coef);
   T.sin_tab = A.table(S.sin_tab); T.dk = A.table(S.dk); T.invc = A.table(S.invc); T.zr = A.table(S.zr);
+  T.tw = A.table(S.tw);
   T.red_a = A.table(S.red_a); T.red_b = A.table(S.red_b); T.red_invc = A.table(S.red_invc);
   T.rinv2 = A.table(S.rinv2); T.z2r = A.table(S.z2r); T.red2_a = A.table(S.red2_a); T.red2_b = A.table(S.red2_b);
   T.maxe = S.maxe;

@@ -806,20 +806,8 @@ __global__ void k_hole_coeffs(const int* __restrict__ off, const int* __restrict
   if (threadIdx.x == 0) a[hh] = delta[hh] * v[0];
 }
 
-// ------------------------------------------------------------------------------ dense DST-I
-// DST-I of a row as the real DFT of its odd extension x̃ (length 2N: x̃_j = f_j, x̃_N = 0,
-// x̃_{2N−j} = −f_j), computed by one complex FFT of length N on z_m = x̃_{2m} + i x̃_{2m+1}:
-//   X_k = E_k + e^{iπk/N} O_k,  E = (Z_k + conj Z_{N−k})/2,  O = (Z_k − conj Z_{N−k})/(2i),
-//   F_k = Σ_j f_j sin(πjk/N) = Im X_k / 2      (sign + transform).
-// No running-sum recurrence, so the error stays O(ε log N) (a "sinft"-style half-length
-// transform with a prefix sum measured 25× worse backward error in the fast solve).
-// MODE 0: forward from a full grid base (mask·f + Σ_h a_h bump_h) → spec row.
-// MODE 1: inverse from spec (with the arrowhead fix-up) → full grid row, × 2/N.
-__device__ __forceinline__ void twiddle(const double* tab, int r, int N, double& c, double& s) {
-  const int m2 = 2 * N - 1;
-  s = sin_lookup(tab, r & m2, N);
-  c = sin_lookup(tab, (r + (N >> 1)) & m2, N);
-}
+// ------------------------------------------------------------------------------ FFT building blocks
+// (register DFTs, padded shared-memory slots; the DST-I cores are with the 2D/3D row kernels below)
 
 // e^{+2πi m/16}
 __device__ __forceinline__ double w16c(int m) {
@@ -893,158 +881,6 @@ __device__ __forceinline__ void dft_reg(double2* v) {
 // complex slot i of the FFT buffer lives at i + i/16 (breaks the stride-R conflicts of the
 // first Stockham pass's writes)
 __device__ __forceinline__ int zpad(int i) { return i + (i >> 4); }
-
-// One Stockham radix-R pass over z[0..N) in shared memory (natural order in and out):
-// item j: v_r = z[j + r N/R] · e^{+2πi r k/(Ns R)}, k = j mod Ns; DFT_R; z[(j/Ns) Ns R + k + q Ns] = V_q.
-// Each thread holds 16 complex values (16/R items); in place with a barrier between reads and writes.
-template <int R>
-__device__ __forceinline__ void stockham_pass(double2* z, const double* tab, int N, int Ns, int nthreads,
-                                              int tid = -1) {
-  if (tid < 0) tid = threadIdx.x;
-  constexpr int IT = 16 / R;
-  double2 v[16];
-  const int nitems = N / R;
-#pragma unroll
-  for (int it = 0; it < IT; ++it) {
-    const int j = tid + it * nthreads;
-    if (j < nitems && tid < nthreads) {
-      const int k = j & (Ns - 1);
-#pragma unroll
-      for (int r = 0; r < R; ++r) v[it * R + r] = z[zpad(j + r * nitems)];
-      if (Ns > 1) {
-        // w = e^{2πi k/(Ns R)} = e^{iπ (2 k N/(Ns R))/N}
-        double c, sn;
-        twiddle(tab, 2 * k * (N / (Ns * R)), N, c, sn);
-        double wc = c, ws = sn;
-#pragma unroll
-        for (int r = 1; r < R; ++r) {
-          const double2 a = v[it * R + r];
-          v[it * R + r] = make_double2(a.x * wc - a.y * ws, a.x * ws + a.y * wc);
-          const double nc = wc * c - ws * sn;
-          ws = wc * sn + ws * c;
-          wc = nc;
-        }
-      }
-      dft_reg<R>(v + it * R);
-    }
-  }
-  __syncthreads();
-#pragma unroll
-  for (int it = 0; it < IT; ++it) {
-    const int j = tid + it * nthreads;
-    if (j < nitems && tid < nthreads) {
-      const int k = j & (Ns - 1);
-      const int base = (j / Ns) * Ns * R + k;
-#pragma unroll
-      for (int q = 0; q < R; ++q) z[zpad(base + q * Ns)] = v[it * R + q];
-    }
-  }
-  __syncthreads();
-}
-
-template <int MODE>
-__global__ void __launch_bounds__(512) k_dst_dense(DevTables T, const double* __restrict__ src, int mask_omega,
-                                                   BumpParams bp, const double* __restrict__ hsep,
-                                                   double* __restrict__ dst) {
-  extern __shared__ double sm[];
-  const int N = T.N, half = N >> 1;
-  double* s_sin = sm;                                          // half + 1 (padded to even)
-  double2* z = reinterpret_cast<double2*>(sm + half + 2);      // N (+N/16 pad) complex
-  double* f = reinterpret_cast<double*>(z) + N / 8 - N;        // f_j at f[N + j]: upper N doubles of z
-  for (int r = threadIdx.x; r <= half; r += blockDim.x) s_sin[r] = T.sin_tab[r];
-  const int i = blockIdx.x + T.col_lo;
-  // 1. load f_j (j = 0..N−1, f_0 = 0) into the upper half of the z buffer (doubles N..2N−1)
-  for (int j = threadIdx.x; j < N; j += blockDim.x) {
-    double v = 0.0;
-    if (j > 0) {
-      if (MODE == 0) {
-        const size_t idx = (size_t)i * (N + 1) + j;
-        if (src && (!mask_omega || T.side[idx])) v = src[idx];
-        if (bp.nh) {
-          const double x = T.lo + i * T.h, yy = T.lo + j * T.h;
-          for (int hh = 0; hh < bp.nh; ++hh) {
-            const double rho2 = ((x - bp.cx[hh]) * (x - bp.cx[hh]) + (yy - bp.cy[hh]) * (yy - bp.cy[hh])) /
-                                (bp.rad[hh] * bp.rad[hh]);
-            if (rho2 < 1.0) v += bp.a[hh] * exp(1.0 - 1.0 / (1.0 - rho2));   // bump, SURVEY App. A.8
-          }
-        }
-      }
-    }
-    if (MODE == 0) f[N + j] = v;
-  }
-  if (MODE == 1) {   // spectral positions → modes (coalesced reads, scattered shared-memory writes)
-    for (int p = threadIdx.x; p < N; p += blockDim.x) {
-      const int k = position_mode(p, N);
-      f[N + k] = k == 0 ? 0.0 : fixup(T, src, hsep, i, p);
-    }
-  }
-  __syncthreads();
-  // 2. z_m = x̃_{2m} + i x̃_{2m+1} (natural order); read all first (z aliases f), then write
-  {
-    double2 buf[16];
-#pragma unroll
-    for (int it = 0; it < 16; ++it) {
-      const int m = threadIdx.x + it * blockDim.x;
-      if (m < N) {
-        const int j0 = 2 * m, j1 = 2 * m + 1;
-        const double a = j0 < N ? f[N + j0] : (j0 == N ? 0.0 : -f[N + 2 * N - j0]);
-        const double b = j1 < N ? f[N + j1] : -f[N + 2 * N - j1];
-        buf[it] = make_double2(a, b);
-      }
-    }
-    __syncthreads();
-#pragma unroll
-    for (int it = 0; it < 16; ++it) {
-      const int m = threadIdx.x + it * blockDim.x;
-      if (m < N) z[zpad(m)] = buf[it];
-    }
-  }
-  __syncthreads();
-  // 3. Stockham FFT (sign +): radix-16 passes, then one radix 2/4/8 pass for the rest
-  {
-    const int nth = N / 16;
-    int Ns = 1;
-    while (Ns * 16 <= N) {
-      stockham_pass<16>(z, s_sin, N, Ns, nth);
-      Ns *= 16;
-    }
-    const int rem = N / Ns;
-    if (rem == 2) stockham_pass<2>(z, s_sin, N, Ns, nth);
-    else if (rem == 4) stockham_pass<4>(z, s_sin, N, Ns, nth);
-    else if (rem == 8) stockham_pass<8>(z, s_sin, N, Ns, nth);
-  }
-  // 4. pairs (k, N−k) in place: F_k = Im(E_k + e^{iπk/N} O_k)/2 into z[k].x
-  for (int k = threadIdx.x; k <= half; k += blockDim.x) {
-    if (k == 0) {
-      z[0].x = 0.0;
-      continue;
-    }
-    const int k2 = N - k;
-    const double2 a = z[zpad(k)], b = z[zpad(k2)];
-    double c, s;
-    twiddle(s_sin, k, N, c, s);
-    const double Fk = 0.5 * (0.5 * (a.y - b.y) + c * (-0.5 * (a.x - b.x)) + s * (0.5 * (a.y + b.y)));
-    double Fk2 = 0.0;
-    if (k2 != k) {
-      twiddle(s_sin, k2, N, c, s);
-      Fk2 = 0.5 * (0.5 * (b.y - a.y) + c * (-0.5 * (b.x - a.x)) + s * (0.5 * (b.y + a.y)));
-    }
-    z[zpad(k)].x = Fk;
-    if (k2 != k) z[zpad(k2)].x = Fk2;
-  }
-  __syncthreads();
-  // 5. store
-  if (MODE == 0) {
-    for (int p = threadIdx.x; p < N; p += blockDim.x) {   // modes → spectral positions
-      const int k = position_mode(p, N);
-      dst[(size_t)(i - 1) * N + p] = (k == 0) ? 0.0 : z[zpad(k)].x;
-    }
-  } else {
-    const double sc = 2.0 / N;
-    for (int j = threadIdx.x; j <= N; j += blockDim.x)
-      dst[(size_t)i * (N + 1) + j] = (j == 0 || j == N) ? 0.0 : sc * z[zpad(j)].x;
-  }
-}
 
 // ------------------------------------------------------------------------------ A8 GMRES
 __device__ __forceinline__ double ordered_sum(const double* __restrict__ p) {
@@ -1147,27 +983,7 @@ void launch_correct(const DevTables& T, const double* phi, const double* mk, con
   { ++g_launches; k_correct<<<cdiv(T.nirr, 128), 128, 0, s>>>(T, phi, mk, fq, jq_given, cval); }
 }
 
-static int dense_threads(int N) { return N / 16 < 32 ? 32 : N / 16; }
-static size_t dense_smem(int N) { return (size_t)(N / 2 + 2 + 2 * N + N / 8) * sizeof(double); }  // table + padded N complex
 
-void launch_dst_forward(const DevTables& T, const double* fgrid, bool mask, const BumpParams& bp, double* spec,
-                        cudaStream_t s) {
-  const size_t sm = dense_smem(T.N);
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(k_dst_dense<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-    cudaFuncSetAttribute(k_dst_dense<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-    attr = true;
-  }
-  { ++g_launches; k_dst_dense<0><<<T.col_hi - T.col_lo + 1, dense_threads(T.N), sm, s>>>(T, fgrid, mask ? 1 : 0, bp, nullptr, spec); }
-}
-
-void launch_inverse_dense(const DevTables& T, const double* spec, const double* hsep, double* vgrid,
-                          cudaStream_t s) {
-  const size_t sm = dense_smem(T.N);
-  BumpParams bp{};
-  { ++g_launches; k_dst_dense<1><<<T.col_hi - T.col_lo + 1, dense_threads(T.N), sm, s>>>(T, spec, 0, bp, hsep, vgrid); }
-}
 
 void launch_sweep(const DevTables& T, const double* cval, bool dense, double* spec, double* zfirst, double* zlast,
                   double* fsep, cudaStream_t s) {
@@ -1463,6 +1279,13 @@ __device__ __forceinline__ double w32c(int m) {
 }
 __device__ __forceinline__ double w32s(int m) { return w32c(m - 8); }
 
+// the lanes of one row synchronise: within a warp (N ≤ 1024) or across the CTA (row = CTA)
+template <int NTL>
+__device__ __forceinline__ void rsync() {
+  if constexpr (NTL > 32) __syncthreads();
+  else __syncwarp();
+}
+
 // Compile-time Stockham radix-R pass over one row z[0..M) held by M/16 lanes of one warp (rows never
 // straddle warps, so __syncwarp orders the in-place smem exchange).  Twiddles e^{+2πi r k/(Ns R)} =
 // tw[r k 2NT/(Ns R) mod 2NT] from the (cos, sin)(π m/NT) table of the grid size NT (L1-resident).
@@ -1489,7 +1312,7 @@ __device__ __forceinline__ void st_pass(double2* z, const double2* __restrict__ 
     }
     dft_reg<R>(v + it * R);
   }
-  __syncwarp();
+  rsync<NTH>();
 #pragma unroll
   for (int it = 0; it < IT; ++it) {
     const int j = tid + it * NTH;
@@ -1497,7 +1320,7 @@ __device__ __forceinline__ void st_pass(double2* z, const double2* __restrict__ 
 #pragma unroll
     for (int q = 0; q < R; ++q) z[zpad(base + q * Ns)] = v[it * R + q];
   }
-  __syncwarp();
+  rsync<NTH>();
 }
 
 template <int M, int Ns, int NT>
@@ -1524,7 +1347,8 @@ __device__ __forceinline__ int fpos(int j) { return j + 2 * (j >> 5); }
 //   of Re Y, taken per lane (16 terms) and across the row's lanes by a log-depth shuffle scan.
 // On exit F_j sits at ((double*)z)[fpos(j)], j ∈ [0, N).
 template <int N>
-__device__ __forceinline__ void dst2_core(double2* z, const double2* __restrict__ tw, int tid) {
+__device__ __forceinline__ void dst2_core(double2* z, const double2* __restrict__ tw, int tid,
+                                          double* scratch = nullptr) {   // scratch: N/1024 + 1 doubles if N > 1024
   constexpr int M = N / 2, NTL = N / 32;
   double2 v[16];
   const double2 wa = __ldg(tw + 2 * tid), wb = __ldg(tw + 2 * tid + 1);   // e^{iπ(2 tid)/N}, e^{iπ(2 tid+1)/N}
@@ -1539,10 +1363,10 @@ __device__ __forceinline__ void dst2_core(double2* z, const double2* __restrict_
     v[s] = make_double2(fma(sa, P.x + fa, 0.5 * (P.x - fa)), fma(sb, P.y + fb, 0.5 * (P.y - fb)));
   }
   dft_reg<16>(v);
-  __syncwarp();
+  rsync<NTL>();
 #pragma unroll
   for (int q = 0; q < 16; ++q) z[zpad(16 * tid + q)] = v[q];
-  __syncwarp();
+  rsync<NTL>();
   st_fft<M, 16, N>(z, tw, tid);
   // Y_k = (Z_k + conj Z_{M−k})/2 − (i/2) e^{2πik/N} (Z_k − conj Z_{M−k}), k = 16·tid + t
   double R[16], I[16];
@@ -1557,28 +1381,155 @@ __device__ __forceinline__ void dst2_core(double2* z, const double2* __restrict_
     R[t] = fma(0.5, fma(w.x, dy, w.y * dx), ex);
     I[t] = fma(0.5, fma(w.y, dy, -w.x * dx), ey);
   }
-  double run = 0.0;
+  // inclusive prefix within the lane by a log-depth (Kogge-Stone) scan: rounding depth 4, not 16
 #pragma unroll
-  for (int t = 0; t < 16; ++t) {
-    run += R[t];
-    R[t] = run;   // inclusive prefix within the lane
-  }
-  double x = run;
+  for (int d = 1; d < 16; d <<= 1)
 #pragma unroll
-  for (int d = 1; d < NTL; d <<= 1) {
-    const double y = __shfl_up_sync(0xffffffffu, x, d, NTL);
-    if (tid >= d) x += y;
+    for (int t = 15; t >= d; --t) R[t] += R[t - d];
+  const double run = R[15];
+  double x = run, r0;
+  if constexpr (NTL <= 32) {
+#pragma unroll
+    for (int d = 1; d < NTL; d <<= 1) {
+      const double y = __shfl_up_sync(0xffffffffu, x, d, NTL);
+      if (tid >= d) x += y;
+    }
+    r0 = __shfl_sync(0xffffffffu, R[0], 0, NTL);   // lane 0's R[0] = Re Y_0
+  } else {   // row = CTA: warp scans, then the preceding warps' totals in a fixed order
+    const int lane = tid & 31, wq = tid >> 5;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+      const double y = __shfl_up_sync(0xffffffffu, x, d);
+      if (lane >= d) x += y;
+    }
+    if (lane == 31) scratch[wq] = x;
+    if (tid == 0) scratch[NTL / 32] = R[0];
+    __syncthreads();
+    double off = 0.0;
+    for (int w = 0; w < wq; ++w) off += scratch[w];
+    x += off;
+    r0 = scratch[NTL / 32];
   }
-  const double r0 = __shfl_sync(0xffffffffu, R[0], 0, NTL);   // lane 0's R[0] = Re Y_0
   const double base = (x - run) - 0.5 * r0;
-  __syncwarp();
+  rsync<NTL>();
   double* F = reinterpret_cast<double*>(z);
 #pragma unroll
   for (int t = 0; t < 16; ++t) {
     const int k = 16 * tid + t;
     *reinterpret_cast<double2*>(F + fpos(2 * k)) = make_double2(k ? I[t] : 0.0, base + R[t]);
   }
-  __syncwarp();
+  rsync<NTL>();
+}
+
+
+// ---- dense DST-I rows (2D), half-length core: forward from the full grid (volume term + bumps)
+// into spectral positions (MODE 0), inverse from the fixed-up spectrum into the full grid (MODE 1).
+// N ≤ 1024: 256/(N/32) rows per CTA, a row on N/32 lanes of a warp; N ≥ 2048: one row per CTA.
+__device__ __forceinline__ double dense_src(const DevTables& T, const double* __restrict__ src, int mask_omega,
+                                            const BumpParams& bp, int i, int j) {
+  const int N = T.N;
+  double v = 0.0;
+  if (j == 0) return v;
+  const size_t idx = (size_t)i * (N + 1) + j;
+  if (src && (!mask_omega || T.side[idx])) v = src[idx];
+  if (bp.nh) {
+    const double x = T.lo + i * T.h, yy = T.lo + j * T.h;
+    for (int hh = 0; hh < bp.nh; ++hh) {
+      const double rho2 = ((x - bp.cx[hh]) * (x - bp.cx[hh]) + (yy - bp.cy[hh]) * (yy - bp.cy[hh])) /
+                          (bp.rad[hh] * bp.rad[hh]);
+      if (rho2 < 1.0) v += bp.a[hh] * exp(1.0 - 1.0 / (1.0 - rho2));   // bump, SURVEY App. A.8
+    }
+  }
+  return v;
+}
+
+// accurate DST-I (2D rows, N up to 8192): the real DFT of the odd extension x (x_t = f_t, x_N = 0,
+// x_{2N−t} = −f_t) by one N-point complex FFT of z_m = x_2m + i x_2m+1; F_k = Im(E_k + e^{iπk/N} O_k)/2.
+// Every output carries O(ε log N) rounding (the half-length core's prefix sum grows as √N ε, which
+// the 2D backward-error pin at N ≥ 2048 rejects).  N/16 lanes per row, 8 pairs fp[s] per lane
+// (m = tid + s·N/16); on exit F_k sits in z[zpad(k)].x, k ∈ [1, N).
+template <int N>
+__device__ __forceinline__ void dst1_core(double2* z, const double2* __restrict__ tw, int tid, const double2* fp) {
+  constexpr int NTH = N / 16;
+#pragma unroll
+  for (int s = 0; s < 8; ++s) {
+    const int m = tid + s * NTH;
+    z[zpad(m)] = fp[s];
+    if (m > 0) z[zpad(N - m)].x = -fp[s].x;
+    else z[zpad(N / 2)].x = 0.0;
+    z[zpad(N - m - 1)].y = -fp[s].y;
+  }
+  rsync<NTH>();
+  st_fft<N, 1, N>(z, tw, tid);
+  const double2 wb = __ldg(tw + 1 + tid);   // e^{iπ(1+tid)/N}; k = 1 + tid + s·N/16 adds s·π/16
+  double Fk[8], Fk2[8];
+#pragma unroll
+  for (int s = 0; s < 8; ++s) {
+    const int k = 1 + tid + s * NTH;
+    const double2 A = z[zpad(k)], B = z[zpad(N - k)];
+    const double2 w = make_double2(fma(wb.x, w32c(s), -wb.y * w32s(s)), fma(wb.y, w32c(s), wb.x * w32s(s)));
+    Fk[s] = 0.5 * (0.5 * (A.y - B.y) - w.x * (0.5 * (A.x - B.x)) + w.y * (0.5 * (A.y + B.y)));
+    Fk2[s] = 0.5 * (0.5 * (B.y - A.y) + w.x * (0.5 * (B.x - A.x)) + w.y * (0.5 * (B.y + A.y)));
+  }
+  rsync<NTH>();
+#pragma unroll
+  for (int s = 0; s < 8; ++s) {
+    const int k = 1 + tid + s * NTH;
+    z[zpad(k)].x = Fk[s];
+    if (k != N - k) z[zpad(N - k)].x = Fk2[s];
+  }
+  rsync<NTH>();
+}
+
+template <int N>
+struct DenseCfg {
+  static constexpr int NTH = N / 16, RPC = NTH > 32 ? 1 : 256 / NTH, NTHR = NTH * RPC, ZS = N + N / 16 + 1;
+};
+
+template <int MODE, int N>
+__global__ void __launch_bounds__(DenseCfg<N>::NTHR, 1) k_dst_dense2(DevTables T, const double* __restrict__ src,
+                                                                    int mask_omega, BumpParams bp,
+                                                                    const double* __restrict__ hsep,
+                                                                    double* __restrict__ dst) {
+  using C = DenseCfg<N>;
+  constexpr int NTH = C::NTH, RPC = C::RPC;
+  extern __shared__ double2 smz[];
+  const int rl = threadIdx.x / NTH, tid = threadIdx.x % NTH;
+  double2* z = smz + rl * C::ZS;
+  const double2* __restrict__ tw = reinterpret_cast<const double2*>(T.tw);
+  const int i = T.col_lo + blockIdx.x * RPC + rl;
+  const bool live = i <= T.col_hi;
+  double2 fp[8];
+  if (MODE == 0) {
+#pragma unroll
+    for (int s = 0; s < 8; ++s) {
+      const int m = tid + NTH * s;
+      fp[s] = live ? make_double2(dense_src(T, src, mask_omega, bp, i, 2 * m), dense_src(T, src, mask_omega, bp, i, 2 * m + 1))
+                   : make_double2(0.0, 0.0);
+    }
+  } else {   // spectral positions → modes (coalesced reads, scattered shared-memory writes), then pairs
+    double* f = reinterpret_cast<double*>(z);
+    for (int p = tid; p < N; p += NTH) {
+      const int k = position_mode(p, N);
+      f[k] = (live && k) ? fixup(T, src, hsep, i, p) : 0.0;
+    }
+    rsync<NTH>();
+#pragma unroll
+    for (int s = 0; s < 8; ++s) fp[s] = reinterpret_cast<const double2*>(f)[tid + NTH * s];
+    rsync<NTH>();
+  }
+  dst1_core<N>(z, tw, tid, fp);
+  if (!live) return;
+  if (MODE == 0) {
+    for (int p = tid; p < N; p += NTH) {   // modes → spectral positions
+      const int k = position_mode(p, N);
+      __stcs(dst + (size_t)(i - 1) * N + p, k ? z[zpad(k)].x : 0.0);
+    }
+  } else {
+    const double sc = 2.0 / N;
+    for (int j = tid; j <= N; j += NTH)
+      __stcs(dst + (size_t)i * (N + 1) + j, (j == 0 || j == N) ? 0.0 : sc * z[zpad(j)].x);
+  }
 }
 
 // the fixed-up spectral row (i, m0/N) (R20: x = z − h_{g−1} Z_L − h_g Z_R; separators x = h) as pairs
@@ -2084,6 +2035,45 @@ void launch_interp3(const DevTables3& T, const double* phi, const double* dphi, 
                     const double* jz_given, const double* work, double* out, cudaStream_t s) {
   ++g_launches;
   k_interp3<<<cdiv3(T.nq, 128), 128, 0, s>>>(T, phi, dphi, fz, jz_given, work, out);
+}
+
+template <int MODE, int N>
+static void dense_n(const DevTables& T, const double* src, int mask, const BumpParams& bp, const double* hsep,
+                    double* dst, cudaStream_t s) {
+  using C = DenseCfg<N>;
+  const size_t sm = (size_t)C::RPC * C::ZS * sizeof(double2);
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(k_dst_dense2<MODE, N>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    attr = true;
+  }
+  const int rows = T.col_hi - T.col_lo + 1;
+  k_dst_dense2<MODE, N><<<(rows + C::RPC - 1) / C::RPC, C::NTHR, sm, s>>>(T, src, mask, bp, hsep, dst);
+}
+template <int MODE>
+static void dense_dispatch(const DevTables& T, const double* src, int mask, const BumpParams& bp, const double* hsep,
+                           double* dst, cudaStream_t s) {
+  ++g_launches;
+  switch (T.N) {
+    case 64: dense_n<MODE, 64>(T, src, mask, bp, hsep, dst, s); break;
+    case 128: dense_n<MODE, 128>(T, src, mask, bp, hsep, dst, s); break;
+    case 256: dense_n<MODE, 256>(T, src, mask, bp, hsep, dst, s); break;
+    case 512: dense_n<MODE, 512>(T, src, mask, bp, hsep, dst, s); break;
+    case 1024: dense_n<MODE, 1024>(T, src, mask, bp, hsep, dst, s); break;
+    case 2048: dense_n<MODE, 2048>(T, src, mask, bp, hsep, dst, s); break;
+    case 4096: dense_n<MODE, 4096>(T, src, mask, bp, hsep, dst, s); break;
+    default: dense_n<MODE, 8192>(T, src, mask, bp, hsep, dst, s); break;
+  }
+}
+void launch_dst_forward(const DevTables& T, const double* fgrid, bool mask, const BumpParams& bp, double* spec,
+                        cudaStream_t s) {
+  dense_dispatch<0>(T, fgrid, mask ? 1 : 0, bp, nullptr, spec, s);
+}
+
+void launch_inverse_dense(const DevTables& T, const double* spec, const double* hsep, double* vgrid,
+                          cudaStream_t s) {
+  BumpParams bp{};
+  dense_dispatch<1>(T, spec, 0, bp, hsep, vgrid, s);
 }
 
 }  // namespace kfbi

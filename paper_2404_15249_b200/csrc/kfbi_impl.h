@@ -101,6 +101,7 @@ struct Setup {
   std::vector<double> sp_coef;
   // fast solver tables, mode k = 0..N−1 (k = 0 unused)
   std::vector<double> sin_tab;       // sin(π r / N), r = 0..N/2
+  std::vector<double> tw;            // 2N × (cos, sin)(π m / N)
   std::vector<double> dk;            // N
   std::vector<double> invc;          // LB × N: 1/c_p of a fresh block
   std::vector<double> zr;            // LB × N: (S⁻¹ e_L)[p]
@@ -189,6 +190,7 @@ struct DevTables {
   const double *c_delta, *sp_coef;
   // fast solver
   const double *sin_tab, *dk, *invc, *zr, *red_a, *red_b, *red_invc;
+  const double* tw;   // 2N × (cos, sin)(π m/N)
   const double *rinv2, *z2r, *red2_a, *red2_b;
   int maxe;
   const int8_t* side;

@@ -472,6 +472,12 @@ void build_setup(Setup& S, const kfbi_grid* g, const kfbi_boundary* b, const kfb
   const int P = S.P;
   S.sin_tab.resize(N / 2 + 1);
   for (int r = 0; r <= N / 2; ++r) S.sin_tab[r] = std::sin(kPi * (double)r / N);
+  S.tw.resize(4 * (size_t)N);   // (cos, sin)(π m/N), m < 2N, folded onto the quarter wave
+  for (int m = 0; m < 2 * N; ++m) {
+    auto sn = [&](int r) { double sg = 1.0; if (r >= N) { r -= N; sg = -1.0; } if (r > N / 2) r = N - r; return sg * S.sin_tab[r]; };
+    S.tw[2 * m] = sn((m + N / 2) % (2 * N));
+    S.tw[2 * m + 1] = sn(m);
+  }
   S.dk.assign(N, 0.0);
   S.invc.assign((size_t)LB * N, 0.0);
   S.zr.assign((size_t)LB * N, 0.0);

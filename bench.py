@@ -175,9 +175,9 @@ def main():
         if world > 1:
             dist.barrier()
 
-    # multi-GPU: 2D slabs along x over NCCL when N/512 is divisible by the world size;
-    # otherwise (3D) independent replicas, one per GPU
-    sharded = world > 1 and prob.dim == 2 and prob.n % (512 * world) == 0
+    # multi-GPU: slabs along x over NCCL when the world size divides the slab units
+    # (2D: level-2 segments, N/512; 3D: ADM blocks, N/16); otherwise independent replicas
+    sharded = world > 1 and (prob.n % (512 * world) == 0 if prob.dim == 2 else prob.n % (16 * world) == 0)
     if sharded:
         k = KFBI(prob, device=local, world=world, rank=rank, nccl_id=broadcast_unique_id())
     else:

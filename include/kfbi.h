@@ -122,12 +122,16 @@ const char* kfbi_last_setup_error(void);
  * are split along x into `world` slabs of whole level-2 arrowhead segments (512 columns each), so
  * `world` must divide N/512.  Per apply the ranks exchange the segment end values of the reduced
  * system (one ncclAllGather) and sum disjoint partial interpolations (one ncclAllReduce); φ, the
- * outputs and GMRES are replicated.  kfbi_dist.rank = −1 with world > 1 runs all ranks' slabs in
+ * outputs and GMRES are replicated.  3D grids are split along x into slabs of whole ADM blocks
+ * (15 planes + separator), `world` must divide N/16; per K_D apply the block end values are
+ * all-gathered (two ncclAllGather in one group), the reduced system is solved redundantly, and the
+ * interpolation partial sums are all-reduced; the once-per-solve dense applies are replicated.  kfbi_dist.rank = −1 with world > 1 runs all ranks' slabs in
  * this one context (single-GPU emulation of the partition, collectives done in device memory). */
 kfbi_status kfbi_get_unique_id(void* out128);
 
 /* Slab of `rank` (host): out6 = {first block, end block, first column, last column, first
- * stencil column index, end stencil column index}; the columns are grid indices i (x). */
+ * stencil column index, end stencil column index}; the columns are grid indices i (x).
+ * 3D: {first block, end block, first x-plane, last x-plane, first stencil row, end stencil row}. */
 kfbi_status kfbi_slab(const kfbi_ctx* ctx, int32_t rank, int64_t* out6);
 
 /* Procedure 1: grid, control points, node classification, intersections,

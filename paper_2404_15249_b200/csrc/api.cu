@@ -176,6 +176,7 @@ void layout3(kfbi_ctx* c, Arena& A) {
   DevTables3& T = c->T3;
   const size_t N = S.N, P = S.P, K = N * N, M = S.nq;
   T.N = S.N; T.P = S.P; T.nq = S.nq; T.nirr = S.nirr; T.lo = S.lo; T.h = S.h; T.kappa = S.kappa;
+  T.rank = 0; T.b_lo = 0; T.b_hi = S.P; T.i_lo = 1; T.i_hi = S.N - 1; T.w_lo = 0; T.w_hi = (int)S.zrow_id.size();
   T.q_axis = A.table(S.q_axis); T.q_pos = A.table(S.q_pos); T.q_n = A.table(S.q_n); T.q_e1 = A.table(S.q_e1);
   T.q_e2 = A.table(S.q_e2); T.q_kab = A.table(S.q_kab);
   T.irr_lin = A.table(S.irr_lin); T.irr_side = A.table(S.irr_side); T.irr_ptr = A.table(S.irr_ptr);
@@ -194,9 +195,10 @@ void layout3(kfbi_ctx* c, Arena& A) {
   c->work2 = A.take<double>((N - 1) * K);
   c->zfirst = A.take<double>(P * K);
   c->corr = A.take<double>(std::max(S.nirr, 1));
-  c->fsep = A.take<double>(std::max<size_t>(P - 1, 1) * K);
+  c->fsep = A.take<double>(P * K);   // P rows (not P − 1): equal all-gather slices per rank
   c->hsep = A.take<double>(std::max<size_t>(P - 1, 1) * K);
   c->dphi = A.take<double>(5 * M);
+  c->parts = A.take<double>((size_t)std::max(c->world, 1) * M);
   c->V = A.take<double>((kMaxRestart + 1) * M);
   c->gx = A.take<double>(M);
   c->gr = A.take<double>(M);
@@ -231,6 +233,23 @@ DevTables slab(const kfbi_ctx* c, int r) {
   T.col_hi = std::min(BL * T.g_hi, S.N - 1);
   T.o_lo = (int)(std::lower_bound(S.ocol.begin(), S.ocol.end(), T.col_lo) - S.ocol.begin());
   T.o_hi = (int)(std::upper_bound(S.ocol.begin(), S.ocol.end(), T.col_hi) - S.ocol.begin());
+  return T;
+}
+
+// 3D slab of rank r: whole ADM blocks (15 planes + separator), P / world per rank
+DevTables3 slab3(const kfbi_ctx* c, int r) {
+  DevTables3 T = c->T3;
+  const Setup3& S = c->S3;
+  const int world = c->world;
+  T.rank = r;
+  if (world == 1) return T;
+  T.b_lo = r * S.P / world;
+  T.b_hi = (r + 1) * S.P / world;
+  T.i_lo = BL * T.b_lo + 1;
+  T.i_hi = std::min(BL * T.b_hi, S.N - 1);
+  auto row0 = [&](int i) { return (int32_t)((int64_t)(i - 1) * S.N); };
+  T.w_lo = (int)(std::lower_bound(S.zrow_id.begin(), S.zrow_id.end(), row0(T.i_lo)) - S.zrow_id.begin());
+  T.w_hi = (int)(std::lower_bound(S.zrow_id.begin(), S.zrow_id.end(), row0(T.i_hi + 1)) - S.zrow_id.begin());
   return T;
 }
 
@@ -367,17 +386,47 @@ void inverse3(kfbi_ctx* c, double* u, cudaStream_t s) {   // u == NULL: result s
   ck(cudaMemset2DAsync(u + (W + c->T3.N) * W, W * W * sizeof(double), 0, W * sizeof(double), c->T3.N - 1, s), "memset");
 }
 // K_D (the GMRES operator): sparse source, sparse read-out — no dense z-direction transforms
+// Multi-GPU: each rank runs the sparse forward, the block sweeps, the y-inverse
+// and the z-evaluation of its own slab; the block end values (zB, zA: P/world rows each) are
+// all-gathered, every rank solves the (cheap) reduced system for all modes, and the interpolation
+// partial sums (plane owner contributes) are all-reduced.  rank = −1 emulates all slabs in one ctx.
 void apply_KD3(kfbi_ctx* c, const double* phi, double* out, cudaStream_t s) {
   const DevTables3& T = c->T3;
   const double sc = 2.0 / T.N;
   launch_lsq3(T, phi, c->dphi, s);
   launch_correct3(T, phi, c->dphi, nullptr, nullptr, nullptr, s, c->corr);
-  launch_sparse3(T, 0, c->corr, nullptr, 1.0, c->work, s);
-  launch_sweep3(T, c->work, c->zfirst, c->fsep, s);
+  for (int r : my_ranks(c)) {
+    const DevTables3 Ts = slab3(c, r);
+    launch_sparse3(Ts, 0, c->corr, nullptr, 1.0, c->work, s);
+    launch_sweep3(Ts, c->work, c->zfirst, c->fsep, s);
+  }
+  if (c->use_nccl) {
+    const DevTables3 Ts = slab3(c, c->rank);
+    const size_t K = (size_t)T.N * T.N, cnt = (size_t)(Ts.b_hi - Ts.b_lo) * K;
+    ckn(ncclGroupStart(), "group");
+    ckn(ncclAllGather(c->zfirst + (size_t)Ts.b_lo * K, c->zfirst, cnt, ncclDouble, c->comm, s), "allgather zB");
+    ckn(ncclAllGather(c->fsep + (size_t)Ts.b_lo * K, c->fsep, cnt, ncclDouble, c->comm, s), "allgather zA");
+    ckn(ncclGroupEnd(), "group");
+  }
   launch_reduced3(T, c->zfirst, c->fsep, c->hsep, s);
-  launch_sparse3(T, 1, c->work, c->hsep, sc, c->work2, s);
-  launch_sparse3(T, 2, c->work2, nullptr, sc, c->work, s);
-  launch_interp3(T, phi, c->dphi, nullptr, nullptr, c->work, out, s);
+  for (int r : my_ranks(c)) {
+    const DevTables3 Ts = slab3(c, r);
+    launch_sparse3(Ts, 1, c->work, c->hsep, sc, c->work2, s);
+    launch_sparse3(Ts, 2, c->work2, nullptr, sc, c->work, s);
+  }
+  if (c->world == 1) {
+    launch_interp3(T, phi, c->dphi, nullptr, nullptr, c->work, out, s);
+    return;
+  }
+  const int M = T.nq;
+  if (c->use_nccl) {
+    launch_interp3(slab3(c, c->rank), phi, c->dphi, nullptr, nullptr, c->work, c->parts, s, true);
+    ckn(ncclAllReduce(c->parts, out, M, ncclDouble, ncclSum, c->comm, s), "allreduce");
+    return;
+  }
+  for (int r : my_ranks(c))
+    launch_interp3(slab3(c, r), phi, c->dphi, nullptr, nullptr, c->work, c->parts + (size_t)r * M, s, true);
+  launch_sum_parts(M, c->world, c->parts, out, s);
 }
 void apply_Y3(kfbi_ctx* c, const double* fgrid, const double* fq, const double* fz, double* out, cudaStream_t s) {
   launch_base3(c->T3, fgrid, c->work, s);
@@ -447,9 +496,12 @@ kfbi_status kfbi_setup(const kfbi_grid* grid, const kfbi_boundary* bnd, const kf
     if (c->dim == 3) build_setup3(c->S3, grid, bnd, pde);
     else build_setup(c->S, grid, bnd, pde);
     if (c->world > 1) {
-      if (c->dim != 2) throw ArgError("multi-GPU slabs are built for 2D (3D: replicas)");
-      const int nseg = c->S.P >= 2 * BL2 ? c->S.P / BL2 : 1;
-      if (nseg < c->world || nseg % c->world) throw ArgError("world must divide N/512 (slabs = level-2 segments)");
+      if (c->dim == 3) {
+        if (c->S3.P < c->world || c->S3.P % c->world) throw ArgError("3D: world must divide N/16 (slabs = ADM blocks)");
+      } else {
+        const int nseg = c->S.P >= 2 * BL2 ? c->S.P / BL2 : 1;
+        if (nseg < c->world || nseg % c->world) throw ArgError("world must divide N/512 (slabs = level-2 segments)");
+      }
     }
     c->stream = (cudaStream_t)stream;
     c->device = dist ? dist->device : 0;
@@ -479,7 +531,13 @@ kfbi_status kfbi_setup(const kfbi_grid* grid, const kfbi_boundary* bnd, const kf
 }
 
 kfbi_status kfbi_slab(const kfbi_ctx* c, int32_t rank, int64_t* out) {
-  if (!c || !out || c->dim != 2 || rank < 0 || rank >= c->world) return KFBI_EINVAL;
+  if (!c || !out || rank < 0 || rank >= c->world) return KFBI_EINVAL;
+  if (c->dim == 3) {
+    const DevTables3 T = slab3(c, rank);
+    const int64_t v[6] = {T.b_lo, T.b_hi, T.i_lo, T.i_hi, T.w_lo, T.w_hi};
+    for (int q = 0; q < 6; ++q) out[q] = v[q];
+    return KFBI_OK;
+  }
   const DevTables T = slab(c, rank);
   const int64_t v[6] = {T.g_lo, T.g_hi, T.col_lo, T.col_hi, T.o_lo, T.o_hi};
   for (int q = 0; q < 6; ++q) out[q] = v[q];

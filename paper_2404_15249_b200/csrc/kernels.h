@@ -83,7 +83,8 @@ void launch_dst_rows3(const DevTables3& T, int mode, double* work, const double*
 void launch_transpose3(const DevTables3& T, double* work, cudaStream_t s);
 void launch_sweep3(const DevTables3& T, double* work, double* zB, double* zA, cudaStream_t s);
 void launch_reduced3(const DevTables3& T, const double* zB, const double* zA, double* hsep, cudaStream_t s);
+// partial: only stencil nodes in the slab's planes [i_lo, i_hi] contribute (multi-GPU partial sums)
 void launch_interp3(const DevTables3& T, const double* phi, const double* dphi, const double* fz,
-                    const double* jz_given, const double* work, double* out, cudaStream_t s);
+                    const double* jz_given, const double* work, double* out, cudaStream_t s, bool partial = false);
 
 }  // namespace kfbi

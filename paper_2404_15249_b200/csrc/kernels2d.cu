@@ -1645,7 +1645,7 @@ __global__ void __launch_bounds__(256, 2) k_fwd3s(DevTables3 T, const double* __
   constexpr int CPT = RPC < 16 ? RPC : 16, NG = RPC / CPT;
   extern __shared__ double2 smz[];
   const double2* __restrict__ tw = reinterpret_cast<const double2*>(T.tw);
-  const int i = blockIdx.y + 1, l0 = blockIdx.x * RPC;
+  const int i = blockIdx.y + T.i_lo, l0 = blockIdx.x * RPC;
   __shared__ int s_ptr[N + 1];
   __shared__ double s_q[N / 2 + 1];   // quarter-wave sin(π r/N): staging rotations from smem, not L1/L2
   for (int r = threadIdx.x; r <= N / 2; r += NTHR) s_q[r] = T.sin_tab[r];
@@ -1721,7 +1721,7 @@ __global__ void __launch_bounds__(256, 2) k_inv3y(DevTables3 T, const double* __
   constexpr int NTL = N / 32, RPC = 256 / NTL < N ? 256 / NTL : N, NTHR = RPC * NTL, ZS = N / 2 + N / 32 + 1;
   extern __shared__ double2 smz[];
   const double2* __restrict__ tw = reinterpret_cast<const double2*>(T.tw);
-  const int i = blockIdx.y + 1, l0 = blockIdx.x * RPC;
+  const int i = blockIdx.y + T.i_lo, l0 = blockIdx.x * RPC;
   const int rl = threadIdx.x / NTL, tid = threadIdx.x % NTL;
   double2* z = smz + rl * ZS;
   const size_t m0 = (size_t)(l0 + rl) * N;
@@ -1760,14 +1760,14 @@ __global__ void __launch_bounds__(256) k_zeval3(DevTables3 T, const double* __re
       }
     }
   };
-  int w = (int)(((size_t)blockIdx.x * 256 + threadIdx.x) >> 5);
-  if (w >= T.nzrow) return;
+  int w = T.w_lo + (int)(((size_t)blockIdx.x * 256 + threadIdx.x) >> 5);
+  if (w >= T.w_hi) return;
   double cur[S][U];
   load(w, cur);
-  while (w < T.nzrow) {
+  while (w < T.w_hi) {
     const int wn = w + nw;
     double nxt[S][U];
-    if (wn < T.nzrow) load(wn, nxt);
+    if (wn < T.w_hi) load(wn, nxt);
     const size_t rbase = (size_t)T.zrow_id[w] * N;
     const int e1 = T.zrow_ptr[w + 1];
     for (int e = T.zrow_ptr[w]; e < e1; ++e) {
@@ -1850,7 +1850,7 @@ __global__ void __launch_bounds__(256) k_sweep3(DevTables3 T, double* spec, doub
       ic[p] = 1.0 / c;
     }
   }
-  for (int g = 0; g < P; ++g) {
+  for (int g = T.b_lo; g < T.b_hi; ++g) {
     double y[LB];
 #pragma unroll
     for (int p = 0; p < LB; ++p) {
@@ -1908,7 +1908,7 @@ __global__ void k_reduced3(DevTables3 T, const double* __restrict__ zB, const do
 // A7 (3D): ten-point interpolation at the control points
 __global__ void k_interp3(DevTables3 T, const double* __restrict__ phi, const double* __restrict__ dphi,
                           const double* __restrict__ fz, const double* __restrict__ jg, const double* __restrict__ work,
-                          double* __restrict__ out) {
+                          double* __restrict__ out, int partial) {
   const int e = blockIdx.x * blockDim.x + threadIdx.x;
   if (e >= T.nq) return;
   const int N = T.N;
@@ -1924,6 +1924,7 @@ __global__ void k_interp3(DevTables3 T, const double* __restrict__ phi, const do
 #pragma unroll
   for (int p = 0; p < 10; ++p) {
     const int ni = c0 + off[p][0], nj = c1 + off[p][1], nk = c2 + off[p][2];
+    if (partial && (ni < T.i_lo || ni > T.i_hi)) continue;   // multi-GPU: the plane owner contributes
     double v = work[(size_t)(ni - 1) * N * N + (size_t)nj * N + nk];
     if ((code >> p) & 1) {
       const double dx = T.lo + ni * T.h - zx, dy = T.lo + nj * T.h - zy, dz = T.lo + nk * T.h - zz;
@@ -1991,7 +1992,7 @@ static void sparse3_n(const DevTables3& T, int which, const double* src, const d
     cudaFuncSetAttribute(k_inv3y<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
     attr = true;
   }
-  const dim3 grid(N / RPC, N - 1);
+  const dim3 grid(N / RPC, T.i_hi - T.i_lo + 1);
   if (which == 0) {
     const size_t sm0 = sm + (size_t)T.max_plane_irr * (sizeof(double) + sizeof(int16_t));
     static size_t attr0 = 0;
@@ -2002,7 +2003,7 @@ static void sparse3_n(const DevTables3& T, int which, const double* src, const d
     k_fwd3s<N><<<grid, NTHR, sm0, s>>>(T, src, dst);
   }
   else if (which == 1) k_inv3y<N><<<grid, NTHR, sm, s>>>(T, src, hsep, scale, dst);
-  else if (T.nzrow) k_zeval3<N><<<std::min(cdiv3(T.nzrow, 8), num_sms() * 2), 256, 0, s>>>(T, src, scale, dst);
+  else if (T.w_hi > T.w_lo) k_zeval3<N><<<std::min(cdiv3(T.w_hi - T.w_lo, 8), num_sms() * 2), 256, 0, s>>>(T, src, scale, dst);
 }
 // which: 0 forward (corr → work), 1 inverse along y (work, hsep → work2), 2 z-evaluation (work2 → work)
 void launch_sparse3(const DevTables3& T, int which, const double* src, const double* hsep, double scale, double* dst,
@@ -2032,9 +2033,9 @@ void launch_reduced3(const DevTables3& T, const double* zB, const double* zA, do
   k_reduced3<<<cdiv3((long)T.N * T.N, 128), 128, 0, s>>>(T, zB, zA, hsep);
 }
 void launch_interp3(const DevTables3& T, const double* phi, const double* dphi, const double* fz,
-                    const double* jz_given, const double* work, double* out, cudaStream_t s) {
+                    const double* jz_given, const double* work, double* out, cudaStream_t s, bool partial) {
   ++g_launches;
-  k_interp3<<<cdiv3(T.nq, 128), 128, 0, s>>>(T, phi, dphi, fz, jz_given, work, out);
+  k_interp3<<<cdiv3(T.nq, 128), 128, 0, s>>>(T, phi, dphi, fz, jz_given, work, out, partial ? 1 : 0);
 }
 
 template <int MODE, int N>

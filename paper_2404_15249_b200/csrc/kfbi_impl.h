@@ -163,6 +163,9 @@ struct DevTables3 {
   const int32_t *irr_row_ptr, *zrow_id, *zrow_ptr, *znode_b;
   const int16_t* irr_row_perm;
   int max_plane_irr;
+  // slab of this rank (multi-GPU): ADM blocks [b_lo, b_hi), x-planes [i_lo, i_hi],
+  // stencil-node rows [w_lo, w_hi) of the zrow list; the whole problem when world = 1
+  int rank, b_lo, b_hi, i_lo, i_hi, w_lo, w_hi;
   int nzrow;
   const int8_t* side;
 };

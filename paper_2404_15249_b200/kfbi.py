@@ -263,7 +263,9 @@ class KFBI:
     def slab(self, rank=None):
         out = (C.c_int64 * 6)()
         self._check(self.lib.kfbi_slab(self.ctx, self.rank if rank is None else rank, out))
-        return dict(zip(["g_lo", "g_hi", "col_lo", "col_hi", "o_lo", "o_hi"], list(out)))
+        keys = (["g_lo", "g_hi", "col_lo", "col_hi", "o_lo", "o_hi"] if self.problem.dim == 2
+                else ["b_lo", "b_hi", "i_lo", "i_hi", "w_lo", "w_hi"])
+        return dict(zip(keys, list(out)))
 
     def apply_model(self):
         a, b, c = C.c_double(), C.c_double(), C.c_double()

@@ -63,3 +63,45 @@ def test_slab_partition_and_id_bootstrap(world):
         assert (a["g_hi"] * 16) == a["col_hi"]                       # slab ends on a level-2 separator
     # every stencil node is owned by exactly one rank (partial interpolation sums are disjoint)
     assert sum(r[2] for r in res) == res[0][3]
+
+
+def _worker3(rank, world, port, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_2404_15249_b200 import KFBI, broadcast_unique_id
+        nid = broadcast_unique_id()
+        k = KFBI(W.C4(64), workspace=False, world=world, rank=rank, nccl_id=nid)
+        sl = k.slab()
+        planes = k.setup_dump(2).reshape(-1, 3)[:, 0]            # x-planes of all stencil nodes
+        owned = int(((planes >= sl["i_lo"]) & (planes <= sl["i_hi"])).sum())
+        out = [None] * world
+        dist.all_gather_object(out, (sl, owned, int(planes.size)))
+        if rank == 0:
+            q.put(out)
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2])
+def test_slab_partition_3d(world):
+    """3D slabs are whole ADM blocks of x-planes; plane and stencil-row ranges tile disjointly."""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker3, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = q.get(timeout=300)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    slabs = [r[0] for r in res]
+    n = 64
+    assert slabs[0]["b_lo"] == 0 and slabs[-1]["b_hi"] == n // 16
+    assert slabs[0]["i_lo"] == 1 and slabs[-1]["i_hi"] == n - 1 and slabs[0]["w_lo"] == 0
+    for a, b in zip(slabs[:-1], slabs[1:]):
+        assert a["b_hi"] == b["b_lo"] and a["i_hi"] + 1 == b["i_lo"] and a["w_hi"] == b["w_lo"]
+        assert a["b_hi"] * 16 == a["i_hi"]                            # slab ends on a block separator
+    assert sum(r[1] for r in res) == res[0][2]                        # stencil nodes owned once

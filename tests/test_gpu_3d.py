@@ -105,3 +105,33 @@ def test_solve3d_matches_oracle(prob):
 def test_interface_solve3d_full_size_C5():
     """Full-size C5 (512³): the piecewise-quadratic witness holds at any size."""
     test_interface_solve3d_piecewise_quadratic(W.C5(512))
+
+
+# ------------------------------------------------------------------ multi-GPU partition (emulated)
+@pytest.mark.parametrize("prob,world", [(W.C4(64), 2), (W.C4(64), 4), (W.C5(128), 8)], ids=["C4-64x2", "C4-64x4", "C5-128x8"])
+def test_partitioned_apply3d_matches_single(prob, world):
+    """All slabs in one context (rank = −1): block sweeps per slab, the gathered reduced system and the
+    disjoint partial interpolation sums reproduce world = 1 (to summation order) and the oracle."""
+    k1 = gpu(prob)
+    kw = KFBI(prob, world=world, rank=-1)
+    for seed in (0, 1):
+        phi = W.random_density(k1.M, seed)
+        assert rel(kw.apply(phi).cpu().numpy(), k1.apply(phi).cpu().numpy()) < 1e-12
+    if prob.n == 64:
+        o = oracle(prob)
+        phi = W.random_density(o.M, 2)
+        assert rel(kw.apply(phi).cpu().numpy(), o.apply_KD(phi)) < 1e-10
+
+
+def test_partitioned_solve3d_matches_oracle():
+    prob = W.C4(64)
+    o = oracle(prob)
+    kw = KFBI(prob, world=2, rank=-1)
+    f = lambda a, b, c: W.f_exact(prob.kappa, a, b, c)
+    u_ref, phi_ref, s_ref = o.solve(W.u_exact(*o.points().T), f)
+    X, Y, Z = _grid(prob)
+    p = kw.points("ctrl")
+    u, phi, s = kw.solve(W.u_exact(*p.T), f(X, Y, Z), f(*p.T), f(*p.T))
+    m = o.st.side
+    assert s.converged and abs(s.iters - s_ref.iters) <= 1
+    assert rel(u.cpu().numpy()[m], u_ref[m]) < 1e-8

@@ -249,6 +249,58 @@ def main():
     h2d = 8 * (g.size + fgrid.size + fq.size + fz.size)
     d2h = 8 * k.n_nodes
 
+    # e2e, pipelined serving loop through the same public API: step k+1's inputs are uploaded on an
+    # H2D copy stream while step k solves, and step k's field is downloaded on a D2H copy stream while
+    # step k+1 solves (double-buffered device inputs/outputs; PCIe is full duplex).  Every step still
+    # moves its own inputs and result; the timed region spans the first upload to the last download.
+    def e2e_pipelined(nsteps):
+        h2d_s, d2h_s = torch.cuda.Stream(dev), torch.cuda.Stream(dev)
+        din = [[torch.empty_like(x, device=dev) for x in (g_h, fg_h, fq_h, fz_h)] for _ in range(2)]
+        dout = [torch.empty(k.n_nodes, dtype=torch.float64, device=dev) for _ in range(2)]
+        hout = [torch.empty(k.n_nodes, dtype=torch.float64).pin_memory() for _ in range(2)]
+        ev_in = [torch.cuda.Event() for _ in range(2)]
+        ev_done = [torch.cuda.Event() for _ in range(2)]
+        ev_out = [torch.cuda.Event() for _ in range(2)]
+
+        def upload(j):
+            b = j % 2
+            with torch.cuda.stream(h2d_s):
+                if j >= 2:
+                    h2d_s.wait_event(ev_done[b])            # solve j−2 no longer reads these inputs
+                for dst, src in zip(din[b], (g_h, fg_h, fq_h, fz_h)):
+                    dst.copy_(src, non_blocking=True)
+                ev_in[b].record(h2d_s)
+
+        t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        flush.zero_()
+        torch.cuda.synchronize()
+        t0.record(h2d_s)
+        upload(0)
+        for j in range(nsteps):
+            b = j % 2
+            if j + 1 < nsteps:
+                upload(j + 1)
+            stream.wait_event(ev_in[b])
+            if j >= 2:
+                stream.wait_event(ev_out[b])                # download j−2 has left dout[b]
+            k.solve(*din[b], u=dout[b])
+            ev_done[b].record(stream)
+            with torch.cuda.stream(d2h_s):
+                d2h_s.wait_event(ev_done[b])
+                hout[b].copy_(dout[b], non_blocking=True)
+                ev_out[b].record(d2h_s)
+        d2h_s.wait_stream(h2d_s)
+        t1.record(d2h_s)
+        t1.synchronize()
+        return t0.elapsed_time(t1) / 1e3 / nsteps
+
+    e2e_pipelined(max(args.warmup, 2))
+    t_e2e_pipe = e2e_pipelined(max(args.steps, 2))
+    if world > 1:
+        tt = torch.tensor([t_e2e_pipe], device=dev)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        t_e2e_pipe = float(tt.item())
+
     # per-kernel device times of the K_D apply (CUDA events on the launching stream)
     phi = torch.tensor(W.random_density(k.M, 0), device=dev)
     prof = k.profile_apply(phi, reps=20)
@@ -280,8 +332,12 @@ def main():
                    "l2": "flushed between timed steps (256 MB write before each step)"},
         "solve_s": t_step, "gmres_iters": stats.iters, "n_applies": n_app, "rel_residual": stats.rel_residual,
         "apply_us": 1e3 * prof["apply"], "apply_grid_pts_per_s": U / (prof["apply"] * 1e-3),
-        "e2e": {"value": copies * U * n_app / t_e2e, "unit": UNIT, "h2d_bytes_per_step": h2d,
-                "d2h_bytes_per_step": d2h, "solve_s": t_e2e},
+        "e2e": {"value": copies * U * n_app / t_e2e_pipe, "unit": UNIT, "h2d_bytes_per_step": h2d,
+                "d2h_bytes_per_step": d2h, "s_per_step": t_e2e_pipe,
+                "mode": "pipelined serving loop: H2D of step k+1 and D2H of step k overlap the solves "
+                        "(two copy streams, double-buffered); timed from the first upload to the last download",
+                "serial": {"value": copies * U * n_app / t_e2e, "s_per_step": t_e2e,
+                           "mode": "H2D, solve, D2H back to back every step"}},
         "gpu_launches": launches, "gpu_launches_per_step": launches / args.steps,
         "roofline": roofline,
         "clocks": clk.summary(),

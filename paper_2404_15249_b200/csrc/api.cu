@@ -67,7 +67,8 @@ struct kfbi_ctx {
   // GMRES
   double *V = nullptr, *gx = nullptr, *gr = nullptr, *ghat = nullptr, *tmp = nullptr;
   double *partial = nullptr, *hcol = nullptr, *ycoef = nullptr, *scal = nullptr;
-  double* hcol_host = nullptr;
+  double* hcol_host = nullptr;   // host-mapped (written by k_copy, read after a stream sync)
+  double* hcol_map = nullptr;    // its device alias
   // host staging of small tables (kept alive for the async uploads)
   std::vector<int32_t> coff, cM, hoff, hM;
   std::vector<double> cdel, hdel, oneh;
@@ -563,7 +564,10 @@ kfbi_status kfbi_set_workspace(kfbi_ctx* c, void* d_ws, size_t bytes) {
   else layout(c, A);
   cudaStream_t s = c->stream;
   for (auto& u : A.uploads) ck(cudaMemcpyAsync(u.first, u.second.first, u.second.second, cudaMemcpyHostToDevice, s), "upload");
-  if (!c->hcol_host) ck(cudaMallocHost(&c->hcol_host, (kMaxRestart + 2) * sizeof(double)), "cudaMallocHost");
+  if (!c->hcol_host) {
+    ck(cudaHostAlloc(&c->hcol_host, (kMaxRestart + 2) * sizeof(double), cudaHostAllocMapped), "cudaHostAlloc");
+    ck(cudaHostGetDevicePointer((void**)&c->hcol_map, c->hcol_host, 0), "cudaHostGetDevicePointer");
+  }
   if (c->use_nccl) {
     ck(cudaSetDevice(c->device), "cudaSetDevice");
     ckn(ncclCommInitRank(&c->comm, c->world, c->nccl_id, c->rank), "ncclCommInitRank");
@@ -658,10 +662,10 @@ kfbi_status kfbi_solve(kfbi_ctx* c, const double* d_g, const double* d_f_grid, c
     st.n_applies++;
     launch_sub(M, d_g, c->tmp, c->ghat, s);
   } else {
-    ck(cudaMemcpyAsync(c->ghat, d_g, bM, cudaMemcpyDeviceToDevice, s), "copy g");
+    launch_copy(M, d_g, c->ghat, s);
   }
   // GMRES(m), Algorithm 5, reading R18
-  if (d_phi0) ck(cudaMemcpyAsync(c->gx, d_phi0, bM, cudaMemcpyDeviceToDevice, s), "copy phi0");
+  if (d_phi0) launch_copy(M, d_phi0, c->gx, s);
   else ck(cudaMemsetAsync(c->gx, 0, bM, s), "zero x");
   double beta0 = -1.0;
   std::vector<double> H((size_t)(o.restart + 1) * o.restart), cs(o.restart), sn(o.restart), gv(o.restart + 1), y(o.restart);
@@ -669,7 +673,7 @@ kfbi_status kfbi_solve(kfbi_ctx* c, const double* d_g, const double* d_f_grid, c
   for (int cycle = 0; cycle <= o.max_restarts; ++cycle) {
     // r = ĝ − K x  (explicit residual; skipped for x₀ = 0 on the first cycle)
     if (!d_phi0 && cycle == 0) {
-      ck(cudaMemcpyAsync(c->gr, c->ghat, bM, cudaMemcpyDeviceToDevice, s), "copy r");
+      launch_copy(M, c->ghat, c->gr, s);
     } else {
       apply_KD(c, c->gx, c->tmp, s);
       st.n_applies++;
@@ -677,7 +681,7 @@ kfbi_status kfbi_solve(kfbi_ctx* c, const double* d_g, const double* d_f_grid, c
     }
     launch_dot(M, c->gr, c->gr, c->partial, s);
     launch_finish_sum(c->partial, c->scal, true, s);
-    ck(cudaMemcpyAsync(c->hcol_host, c->scal, sizeof(double), cudaMemcpyDeviceToHost, s), "beta");
+    launch_copy(1, c->scal, c->hcol_map, s);   // β into host-mapped memory (no copy engine)
     ck(cudaStreamSynchronize(s), "sync beta");
     const double beta = c->hcol_host[0];
     if (!std::isfinite(beta)) throw std::runtime_error("non-finite residual");
@@ -703,7 +707,7 @@ kfbi_status kfbi_solve(kfbi_ctx* c, const double* d_g, const double* d_f_grid, c
       launch_mgs_step(M, w, c->V + (size_t)j * M, w, c->partial + (size_t)j * kRedBlocks,
                       c->partial + (size_t)(j + 1) * kRedBlocks, c->hcol + j, s);
       launch_norm_scale(M, w, c->partial + (size_t)(j + 1) * kRedBlocks, c->hcol + j + 1, s);
-      ck(cudaMemcpyAsync(c->hcol_host, c->hcol, (j + 2) * sizeof(double), cudaMemcpyDeviceToHost, s), "hcol");
+      launch_copy(j + 2, c->hcol, c->hcol_map, s);
       ck(cudaStreamSynchronize(s), "sync hcol");
       for (int i = 0; i <= j + 1; ++i) Hc(i, j) = c->hcol_host[i];
       for (int i = 0; i < j; ++i) {   // previous Givens rotations
@@ -728,10 +732,9 @@ kfbi_status kfbi_solve(kfbi_ctx* c, const double* d_g, const double* d_f_grid, c
       for (int q = i + 1; q < k; ++q) sacc -= Hc(i, q) * y[q];
       y[i] = sacc / Hc(i, i);
     }
-    ck(cudaMemcpyAsync(c->ycoef, y.data(), k * sizeof(double), cudaMemcpyHostToDevice, s), "y");
-    launch_axpy_basis(M, k, c->V, M, c->ycoef, c->gx, s);   // φ_m = φ_0 + M_m y_m
+    launch_axpy_basis(M, k, c->V, M, y.data(), c->gx, s);   // φ_m = φ_0 + M_m y_m
   }
-  if (d_phi_out) ck(cudaMemcpyAsync(d_phi_out, c->gx, bM, cudaMemcpyDeviceToDevice, s), "phi out");
+  if (d_phi_out) launch_copy(M, c->gx, d_phi_out, s);
   // final field u = Wφ + Yf (+ Σ a_h w_h) (R27)
   final_field(c, c->gx, d_f_grid, d_f_isect, d_u, s);
   st.n_applies++;

@@ -61,7 +61,11 @@ void launch_mgs_step(int n, double* w, const double* Vprev, const double* Vcur, 
 void launch_norm_scale(int n, double* w, const double* partial, double* hout, cudaStream_t s);
 void launch_dot(int n, const double* a, const double* b, double* partial, cudaStream_t s);
 void launch_finish_sum(const double* partial, double* out, bool take_sqrt, cudaStream_t s);
-void launch_axpy_basis(int n, int k, const double* V, int ldv, const double* y, double* x, cudaStream_t s);
+// GMRES update x += V y, y (k ≤ kYMax coefficients, host array) passed by value in the launch
+constexpr int kYMax = 64;
+struct YCoef { double v[kYMax]; };
+void launch_axpy_basis(int n, int k, const double* V, int ldv, const double* y_host, double* x, cudaStream_t s);
+void launch_copy(int n, const double* src, double* dst, cudaStream_t s);
 void launch_sub(int n, const double* a, const double* b, double* out, cudaStream_t s);
 void launch_scale_copy(int n, const double* a, const double* scal, double* out, cudaStream_t s);
 

@@ -936,13 +936,19 @@ __global__ void k_finish_sum(const double* __restrict__ partial, double* out, in
   }
 }
 
-__global__ void k_axpy_basis(int n, int k, const double* __restrict__ V, int ldv, const double* __restrict__ y,
+__global__ void k_axpy_basis(int n, int k, const double* __restrict__ V, int ldv, const YCoef y,
                              double* __restrict__ x) {
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
     double acc = 0.0;
-    for (int q = 0; q < k; ++q) acc = fma(y[q], V[(size_t)q * ldv + i], acc);
+    for (int q = 0; q < k; ++q) acc = fma(y.v[q], V[(size_t)q * ldv + i], acc);
     x[i] += acc;
   }
+}
+
+// plain copy on the SMs (device or host-mapped memory): keeps the solve's small transfers off the copy
+// engines, which a concurrent bulk H2D/D2H (pipelined serving) would otherwise queue them behind
+__global__ void k_copy(int n, const double* __restrict__ src, double* __restrict__ dst) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) dst[i] = src[i];
 }
 
 __global__ void k_sub(int n, const double* __restrict__ a, const double* __restrict__ b, double* __restrict__ o) {
@@ -1108,8 +1114,15 @@ void launch_finish_sum(const double* partial, double* out, bool take_sqrt, cudaS
   { ++g_launches; k_finish_sum<<<1, 32, 0, s>>>(partial, out, take_sqrt ? 1 : 0); }
 }
 
-void launch_axpy_basis(int n, int k, const double* V, int ldv, const double* y, double* x, cudaStream_t s) {
+void launch_axpy_basis(int n, int k, const double* V, int ldv, const double* y_host, double* x, cudaStream_t s) {
+  YCoef y{};
+  for (int q = 0; q < k && q < kYMax; ++q) y.v[q] = y_host[q];   // by value: no copy engine
   { ++g_launches; k_axpy_basis<<<cdiv(n, 256), 256, 0, s>>>(n, k, V, ldv, y, x); }
+}
+void launch_copy(int n, const double* src, double* dst, cudaStream_t s) {
+  if (n <= 0) return;
+  const int grid = cdiv(n, 256) < 4 * num_sms() ? cdiv(n, 256) : 4 * num_sms();
+  { ++g_launches; k_copy<<<grid, 256, 0, s>>>(n, src, dst); }
 }
 
 void launch_sub(int n, const double* a, const double* b, double* out, cudaStream_t s) {

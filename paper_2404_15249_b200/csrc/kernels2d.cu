@@ -671,71 +671,80 @@ __global__ void __launch_bounds__(kInvThreads, 2) k_inv_sparse(DevTables T, cons
   __syncthreads();
   const double scale = 2.0 / N;
   const int nrows = u1 - u0;
-  auto cls = [](int j) { return (j & 1) ? 0 : ((j & 3) == 0 ? 1 : 2); };
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = B >> 5;
-  int u = 0;
-  while (u < nrows) {
-    const int c0 = cls(s_rows[u]);
-    int nr = 1;
-    while (nr < 4 && u + nr < nrows && cls(s_rows[u + nr]) == c0) ++nr;
-    double accs[4] = {0.0, 0.0, 0.0, 0.0}, accc[4] = {0.0, 0.0, 0.0, 0.0};
-    double sn[4], cs[4], sd[4], cd[4];
-    int js[4];
-#pragma unroll
-    for (int k = 0; k < 4; ++k) {
-      js[k] = k < nr ? s_rows[u + k] : 0;
-      const int r0 = (js[k] * (int)threadIdx.x) & m2, rd = (js[k] * B) & m2;
-      sn[k] = sinr(r0);
-      cs[k] = sinr((r0 + half) & m2);
-      sd[k] = sinr(rd);
-      cd[k] = sinr((rd + half) & m2);
-    }
-    if (c0 == 0) {
-#pragma unroll
-      for (int s = 0; s < QPT; ++s) {
-#pragma unroll
-        for (int k = 0; k < 4; ++k) {
-          accs[k] = fma(Pv[s], sn[k], accs[k]);
-          accc[k] = fma(Rv[s], cs[k], accc[k]);
-          const double c2 = fma(cs[k], cd[k], -sn[k] * sd[k]);
-          sn[k] = fma(sn[k], cd[k], cs[k] * sd[k]);
-          cs[k] = c2;
-        }
-      }
-    } else {
-#pragma unroll
-      for (int s = 0; s < QPT; ++s) {
-        const double xv = c0 == 1 ? Qp[s] : Qm[s];
-#pragma unroll
-        for (int k = 0; k < 4; ++k) {
-          accs[k] = fma(xv, sn[k], accs[k]);
-          const double c2 = fma(cs[k], cd[k], -sn[k] * sd[k]);
-          sn[k] = fma(sn[k], cd[k], cs[k] * sd[k]);
-          cs[k] = c2;
-        }
-      }
-    }
-    double acc[8];
-#pragma unroll
-    for (int k = 0; k < 4; ++k) {
-      acc[k] = accs[k];
-      acc[4 + k] = accc[k];
-    }
-    if (threadIdx.x == 0) {
+  // rows come sorted by class (odd, j ≡ 0, j ≡ 2 mod 4): groups of ≤ 4 rows of one class.  Sines along
+  // the thread's quads t = tid + s·B by the three-term recurrence S_{s+1} = 2 cos(πjB/N) S_s − S_{s−1}
+  // (one FMA per step; cosines likewise for odd rows).
+  const int ncl0 = T.ocol_ncls[3 * b], ncl1 = T.ocol_ncls[3 * b + 1];
+#pragma unroll 1
+  for (int c0 = 0; c0 < 3; ++c0) {
+    const int cbeg = c0 == 0 ? 0 : (c0 == 1 ? ncl0 : ncl0 + ncl1);
+    const int cend = c0 == 0 ? ncl0 : (c0 == 1 ? ncl0 + ncl1 : nrows);
+#pragma unroll 1
+    for (int u = cbeg; u < cend; u += 4) {
+      const int nr = cend - u < 4 ? cend - u : 4;
+      double accs[4] = {0.0, 0.0, 0.0, 0.0}, accc[4] = {0.0, 0.0, 0.0, 0.0};
+      double S[4], Sm[4], C[4], Cm[4], twocd[4];
+      int js[4];
 #pragma unroll
       for (int k = 0; k < 4; ++k) {
-        const int j = js[k];
-        acc[k] += xq1 * sinr((j * quarter) & m2) + xq2 * sinr((j * half) & m2) +
-                  xq3 * sinr((j * (half + quarter)) & m2);
+        js[k] = k < nr ? s_rows[u + k] : 0;
+        const int r0 = (js[k] * (int)threadIdx.x) & m2, rd = (js[k] * B) & m2;
+        const double s0 = sinr(r0), c0v = sinr((r0 + half) & m2), sd = sinr(rd), cd = sinr((rd + half) & m2);
+        S[k] = s0;
+        C[k] = c0v;
+        Sm[k] = fma(s0, cd, -c0v * sd);   // angle − πjB/N
+        Cm[k] = fma(c0v, cd, s0 * sd);
+        twocd[k] = 2.0 * cd;
+      }
+      if (c0 == 0) {
+#pragma unroll
+        for (int s = 0; s < QPT; ++s) {
+#pragma unroll
+          for (int k = 0; k < 4; ++k) {
+            accs[k] = fma(Pv[s], S[k], accs[k]);
+            accc[k] = fma(Rv[s], C[k], accc[k]);
+            const double sn = fma(twocd[k], S[k], -Sm[k]), cn = fma(twocd[k], C[k], -Cm[k]);
+            Sm[k] = S[k];
+            S[k] = sn;
+            Cm[k] = C[k];
+            C[k] = cn;
+          }
+        }
+      } else {
+#pragma unroll
+        for (int s = 0; s < QPT; ++s) {
+          const double xv = c0 == 1 ? Qp[s] : Qm[s];
+#pragma unroll
+          for (int k = 0; k < 4; ++k) {
+            accs[k] = fma(xv, S[k], accs[k]);
+            const double sn = fma(twocd[k], S[k], -Sm[k]);
+            Sm[k] = S[k];
+            S[k] = sn;
+          }
+        }
+      }
+      double acc[8];
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        acc[k] = accs[k];
+        acc[4 + k] = accc[k];
+      }
+      if (threadIdx.x == 0) {
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          const int j = js[k];
+          acc[k] += xq1 * sinr((j * quarter) & m2) + xq2 * sinr((j * half) & m2) +
+                    xq3 * sinr((j * (half + quarter)) & m2);
+        }
+      }
+      const double ws = warp_transpose_reduce8(acc);
+      if ((lane & 3) == 0) {   // value index v = 4·(lane>>4 & 1) + 2·(lane>>3 & 1) + (lane>>2 & 1): acc[v]
+        const int v = ((lane >> 4) & 1) * 4 + ((lane >> 3) & 1) * 2 + ((lane >> 2) & 1);
+        const int k = v & 3;
+        if (k < nr) red[(size_t)wid * 2 * T.mcr + 2 * (u + k) + (v >> 2)] = ws;
       }
     }
-    const double ws = warp_transpose_reduce8(acc);
-    if ((lane & 3) == 0) {   // value index v = 4·(lane>>4 & 1) + 2·(lane>>3 & 1) + (lane>>2 & 1): acc[v]
-      const int v = ((lane >> 4) & 1) * 4 + ((lane >> 3) & 1) * 2 + ((lane >> 2) & 1);
-      const int k = v & 3;
-      if (k < nr) red[(size_t)wid * 2 * T.mcr + 2 * (u + k) + (v >> 2)] = ws;
-    }
-    u += nr;
   }
   __syncthreads();   // one barrier per column: sum the warps' partials in a fixed order
   for (int t = threadIdx.x; t < nrows; t += B) {

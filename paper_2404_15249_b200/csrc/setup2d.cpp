@@ -437,6 +437,12 @@ void build_setup(Setup& S, const kfbi_grid* g, const kfbi_boundary* b, const kfb
     }
     S.ocol_ptr.push_back(S.nsn);
     S.max_col_rows = 1;
+    S.ocol_ncls.assign(3 * (S.ocol_ptr.size() - 1), 0);   // rows per class (odd, j ≡ 0, j ≡ 2 mod 4)
+    for (size_t c = 0; c + 1 < S.ocol_ptr.size(); ++c)
+      for (int u = S.ocol_ptr[c]; u < S.ocol_ptr[c + 1]; ++u) {
+        const int j = S.sn_j[u];
+        ++S.ocol_ncls[3 * c + ((j & 1) ? 0 : ((j & 3) == 0 ? 1 : 2))];
+      }
     for (size_t c = 0; c + 1 < S.ocol_ptr.size(); ++c) {
       if (S.ocol_ptr[c + 1] - S.ocol_ptr[c] > kMaxColRows) throw GeomError("too many stencil rows in one grid column");
       S.max_col_rows = std::max(S.max_col_rows, S.ocol_ptr[c + 1] - S.ocol_ptr[c]);

@@ -1519,8 +1519,26 @@ __global__ void __launch_bounds__(DenseCfg<N>::NTHR, 1) k_dst_dense2(DevTables T
   const int rl = threadIdx.x / NTH, tid = threadIdx.x % NTH;
   double2* z = smz + rl * C::ZS;
   const double2* __restrict__ tw = reinterpret_cast<const double2*>(T.tw);
-  const int i = T.col_lo + blockIdx.x * RPC + rl;
+  // persistent over row groups; the next group's input rows are prefetched into L2 first
+  for (int rb = blockIdx.x; T.col_lo + rb * RPC <= T.col_hi; rb += gridDim.x) {
+  const int i = T.col_lo + rb * RPC + rl;
   const bool live = i <= T.col_hi;
+  {
+    const int in = i + gridDim.x * RPC;
+    if (in <= T.col_hi && src) {
+      if (MODE == 0) {
+        const double* row = src + (size_t)in * (N + 1);
+        for (int o = 16 * tid; o <= N; o += 16 * NTH) asm volatile("prefetch.global.L2 [%0];" ::"l"(row + o));
+        if (mask_omega && tid < (N + 128) / 128)
+          asm volatile("prefetch.global.L2 [%0];" ::"l"(T.side + (size_t)in * (N + 1) + 128 * tid));
+      } else {
+        const int qn = in / BL, rn = in - qn * BL;
+        const double* row = rn == 0 ? hsep + (size_t)(qn - 1) * N : src + (size_t)(in - 1) * N;
+        for (int o = 16 * tid; o < N; o += 16 * NTH) asm volatile("prefetch.global.L2 [%0];" ::"l"(row + o));
+      }
+    }
+  }
+  rsync<NTH>();   // the previous group's outputs have been read out of z
   double2 fp[8];
   if (MODE == 0) {
 #pragma unroll
@@ -1541,7 +1559,7 @@ __global__ void __launch_bounds__(DenseCfg<N>::NTHR, 1) k_dst_dense2(DevTables T
     rsync<NTH>();
   }
   dst1_core<N>(z, tw, tid, fp);
-  if (!live) return;
+  if (!live) continue;
   if (MODE == 0) {
     for (int p = tid; p < N; p += NTH) {   // modes → spectral positions
       const int k = position_mode(p, N);
@@ -1551,6 +1569,7 @@ __global__ void __launch_bounds__(DenseCfg<N>::NTHR, 1) k_dst_dense2(DevTables T
     const double sc = 2.0 / N;
     for (int j = tid; j <= N; j += NTH)
       __stcs(dst + (size_t)i * (N + 1) + j, (j == 0 || j == N) ? 0.0 : sc * z[zpad(j)].x);
+  }
   }
 }
 
@@ -2071,7 +2090,14 @@ static void dense_n(const DevTables& T, const double* src, int mask, const BumpP
     attr = true;
   }
   const int rows = T.col_hi - T.col_lo + 1;
-  k_dst_dense2<MODE, N><<<(rows + C::RPC - 1) / C::RPC, C::NTHR, sm, s>>>(T, src, mask, bp, hsep, dst);
+  static int per = 0;
+  if (!per) {
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_dst_dense2<MODE, N>, C::NTHR, sm);
+    if (per < 1) per = 1;
+  }
+  const int groups = (rows + C::RPC - 1) / C::RPC;
+  const int grid = groups < per * num_sms() ? groups : per * num_sms();
+  k_dst_dense2<MODE, N><<<grid, C::NTHR, sm, s>>>(T, src, mask, bp, hsep, dst);
 }
 template <int MODE>
 static void dense_dispatch(const DevTables& T, const double* src, int mask, const BumpParams& bp, const double* hsep,

@@ -1457,8 +1457,9 @@ __device__ __forceinline__ double dense_src(const DevTables& T, const double* __
   if (bp.nh) {
     const double x = T.lo + i * T.h, yy = T.lo + j * T.h;
     for (int hh = 0; hh < bp.nh; ++hh) {
-      const double rho2 = ((x - bp.cx[hh]) * (x - bp.cx[hh]) + (yy - bp.cy[hh]) * (yy - bp.cy[hh])) /
-                          (bp.rad[hh] * bp.rad[hh]);
+      const double dx = x - bp.cx[hh], dy = yy - bp.cy[hh], r = bp.rad[hh];
+      if (fabs(dx) >= r || fabs(dy) >= r) continue;   // outside the support's bounding box
+      const double rho2 = (dx * dx + dy * dy) / (r * r);
       if (rho2 < 1.0) v += bp.a[hh] * exp(1.0 - 1.0 / (1.0 - rho2));   // bump, SURVEY App. A.8
     }
   }

@@ -1687,7 +1687,7 @@ __global__ void __launch_bounds__(256, 2) k_fwd3s(DevTables3 T, const double* __
   constexpr int CPT = RPC < 16 ? RPC : 16, NG = RPC / CPT;
   extern __shared__ double2 smz[];
   const double2* __restrict__ tw = reinterpret_cast<const double2*>(T.tw);
-  const int i = blockIdx.y + T.i_lo, l0 = blockIdx.x * RPC;
+  const int i = blockIdx.y + T.i_lo;
   __shared__ int s_ptr[N + 1];
   __shared__ double s_q[N / 2 + 1];   // quarter-wave sin(π r/N): staging rotations from smem, not L1/L2
   for (int r = threadIdx.x; r <= N / 2; r += NTHR) s_q[r] = T.sin_tab[r];
@@ -1704,6 +1704,11 @@ __global__ void __launch_bounds__(256, 2) k_fwd3s(DevTables3 T, const double* __
     }
   }
   __syncthreads();
+  // CTA rows = RPC/4 mode quads {t, N−t, N/2−t, N/2+t} (quad t = 0: {0, N/2, N/4, 3N/4}); with
+  // s, c = sin, cos(πbt/N): sin(πb(N−t)/N) = (−1)^{b+1} s, sin(πb(N/2 ± t)/N) = sin(πb/2) c ± cos(πb/2) s,
+  // so one rotation per entry serves four columns (the 2D sweep's quad symmetry, along z).
+  constexpr int QPI = CPT / 4;   // quads per item
+  const int tq0 = blockIdx.x * (RPC / 4);
   for (int it = threadIdx.x; it < N * NG; it += NTHR) {
     const int rr = it % N, cg = it / N, k = rr / NTHR, pos = rr % NTHR;
     const int a = T.irr_row_perm[(size_t)(i - 1) * N + k * NTHR + ((k & 1) ? NTHR - 1 - pos : pos)];
@@ -1711,28 +1716,30 @@ __global__ void __launch_bounds__(256, 2) k_fwd3s(DevTables3 T, const double* __
 #pragma unroll
     for (int c = 0; c < CPT; ++c) g[c] = 0.0;
     const int e1 = s_ptr[a + 1];
-#ifdef KFBI_EXP
-    if (e1 > 0x7fffffff - 5)
-#endif
+    const int t0 = tq0 + cg * QPI;
     for (int e = s_ptr[a]; e < e1; ++e) {
       const double v = s_val[e];
       const int b = s_b[e];
-      // e^{iπ b ll/N} for the CPT columns: w_c = w_0 · d^c (d = e^{iπ b/N}) by products of depth ≤ 4
-      double2 w[CPT], dp[CPT];
-      {
-        const int r0 = (b * (l0 + cg * CPT)) & (2 * N - 1);
-        w[0] = make_double2(sin_lookup(s_q, (r0 + N / 2) & (2 * N - 1), N), sin_lookup(s_q, r0, N));
-        dp[1] = make_double2(sin_lookup(s_q, (b + N / 2) & (2 * N - 1), N), sin_lookup(s_q, b, N));
+      const double sg1 = (b & 1) ? v : -v;                                   // (−1)^{b+1} v
+      const double sg2 = ((b & 3) == 0 || (b & 3) == 3) ? -v : v, sg3 = (b & 3) <= 1 ? v : -v;
+      const int r0 = (b * t0) & (2 * N - 1);
+      double2 w = make_double2(sin_lookup(s_q, (r0 + N / 2) & (2 * N - 1), N), sin_lookup(s_q, r0, N));
+      const double2 d = make_double2(sin_lookup(s_q, (b + N / 2) & (2 * N - 1), N), sin_lookup(s_q, b, N));
+#pragma unroll
+      for (int u = 0; u < QPI; ++u) {
+        const double sv = w.y, cv = w.x, A = (b & 1) ? cv : sv;
+        if (t0 + u == 0) {   // special quad: modes 0 (unused), N/2, N/4, 3N/4
+          g[4 * u + 1] = fma(v, sin_lookup(s_q, (b * (N / 2)) & (2 * N - 1), N), g[4 * u + 1]);
+          g[4 * u + 2] = fma(v, sin_lookup(s_q, (b * (N / 4)) & (2 * N - 1), N), g[4 * u + 2]);
+          g[4 * u + 3] = fma(v, sin_lookup(s_q, (b * (3 * N / 4)) & (2 * N - 1), N), g[4 * u + 3]);
+        } else {
+          g[4 * u + 0] = fma(v, sv, g[4 * u + 0]);
+          g[4 * u + 1] = fma(sg1, sv, g[4 * u + 1]);
+          g[4 * u + 2] = fma(sg2, A, g[4 * u + 2]);
+          g[4 * u + 3] = fma(sg3, A, g[4 * u + 3]);
+        }
+        if (u + 1 < QPI) w = cmul(w, d);
       }
-#pragma unroll
-      for (int h = 2; h < CPT; h <<= 1) dp[h] = cmul(dp[h / 2], dp[h / 2]);
-#pragma unroll
-      for (int c = 1; c < CPT; ++c) {
-        const int hi = 1 << (31 - __clz(c));
-        w[c] = cmul(w[c - hi], dp[hi]);
-      }
-#pragma unroll
-      for (int c = 0; c < CPT; ++c) g[c] = fma(v, w[c].y, g[c]);
     }
     const int off = 2 * zpad(a >> 1) + (a & 1);
 #pragma unroll
@@ -1742,7 +1749,9 @@ __global__ void __launch_bounds__(256, 2) k_fwd3s(DevTables3 T, const double* __
   const int rl = threadIdx.x / NTL, tid = threadIdx.x % NTL;
   double2* z = smz + rl * ZS;
   dst2_core<N>(z, tw, tid);
-  const int ll = l0 + rl;
+  const int tq = tq0 + (rl >> 2), mem = rl & 3;   // this row's mode: member of quad tq
+  const int ll = tq ? (mem == 0 ? tq : mem == 1 ? N - tq : mem == 2 ? N / 2 - tq : N / 2 + tq)
+                    : (mem == 0 ? 0 : mem == 1 ? N / 2 : mem == 2 ? N / 4 : 3 * N / 4);
   const double sc = ll ? 1.0 : 0.0;
   const double* F = reinterpret_cast<const double*>(z);
   double* op = work + ((size_t)(i - 1) * N + ll) * N;

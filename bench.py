@@ -91,13 +91,20 @@ class ClockSampler:
 
 
 def make_inputs(k, prob):
-    """Manufactured Dirichlet problem u* (reading R24) at the context's own points."""
+    """Manufactured problem u* (reading R24) at the context's own points: g_D = u*|Γ, or for the
+    Neumann BVP g_N = n·∇u* with the context's outward normals."""
     n = prob.n
     pz, pq = k.points("ctrl"), k.points("isect")
     x = prob.lo + np.arange(n + 1) * prob.h
     f = lambda *a: W.f_exact(prob.kappa, *a)
     G = np.meshgrid(*([x] * prob.dim), indexing="ij")
-    return (W.u_exact(*pz.T), f(*G).ravel(), f(*pq.T), f(*pz.T))
+    if prob.bc == W.NEUMANN:
+        nz = k.points("normal")
+        ux, uy = W.grad_u_exact(*pz.T)
+        g = ux * nz[:, 0] + uy * nz[:, 1]
+    else:
+        g = W.u_exact(*pz.T)
+    return (g, f(*G).ravel(), f(*pq.T), f(*pz.T))
 
 
 def cpu_oracle_apply_rate(prob, reps=1):
@@ -111,7 +118,7 @@ def cpu_oracle_apply_rate(prob, reps=1):
     ts = []
     for _ in range(reps):
         t0 = time.perf_counter()
-        o.apply_KD(phi)
+        o.apply_K(phi) if prob.dim == 2 else o.apply_KD(phi)
         ts.append(time.perf_counter() - t0)
     return o, ts, t_setup
 
@@ -125,12 +132,13 @@ def run_reference(args, prob):
     U = prob.unknowns
     o = Oracle2D(prob) if prob.dim == 2 else Oracle3D(prob)
     phi = W.random_density(o.M, 0)
+    apply = o.apply_K if prob.dim == 2 else o.apply_KD
     for _ in range(args.warmup):
-        o.apply_KD(phi)
+        apply(phi)
     ts = []
     for _ in range(args.steps):
         t0 = time.perf_counter()
-        o.apply_KD(phi)
+        apply(phi)
         ts.append(time.perf_counter() - t0)
     t = float(np.mean(ts))
     v = U / t
@@ -153,8 +161,12 @@ def main():
     ap.add_argument("--config", default="C3")
     ap.add_argument("--n", type=int, default=0, help="override grid size")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--bc", default="dirichlet", choices=["dirichlet", "neumann"],
+                    help="boundary condition (neumann: 2D, κ > 0 configs, e.g. --config C2)")
     args = ap.parse_args()
     prob = W.CONFIGS[args.config](args.n) if args.n else W.CONFIGS[args.config]()
+    if args.bc == "neumann":
+        prob = W.neumann(prob)
     if args.impl == "reference":
         return run_reference(args, prob)
 

@@ -86,7 +86,8 @@ typedef struct {
 
 typedef struct {
   double kappa;          /* κ ≥ 0                                    */
-  int32_t bc;            /* KFBI_DIRICHLET                                   */
+  int32_t bc;            /* KFBI_DIRICHLET, or KFBI_NEUMANN (2D, κ > 0; κ = 0 or 3D
+                            → KFBI_EUNSUPPORTED)                            */
 } kfbi_pde;
 
 typedef struct {
@@ -152,17 +153,20 @@ kfbi_status kfbi_set_workspace(kfbi_ctx* ctx, void* d_ws, size_t bytes);
 kfbi_status kfbi_sizes(const kfbi_ctx* ctx, int64_t* M, int64_t* nq, int64_t* n_irr, int64_t* n_nodes);
 
 /* Host copies of point coordinates so the caller can evaluate g and f there:
- * which = 0: control points (M × dim, interleaved), 1: intersection nodes (nq × dim). */
+ * which = 0: control points (M × dim, interleaved), 1: intersection nodes (nq × dim),
+ * 2: outward unit normals at the control points (M × dim; Neumann data g_N = n·∇u). */
 kfbi_status kfbi_points(const kfbi_ctx* ctx, int32_t which, double* host_xyz);
 
 /* Ω mask of the full node grid ((N+1)^d int8, 1 = Ω) into host memory. */
 kfbi_status kfbi_node_mask(const kfbi_ctx* ctx, int8_t* host_mask);
 
 /* out = K̃φ = K_D φ (+ hole completion, R27), φ and out are M doubles on the device.
- * Asynchronous, stream-ordered, no state change. */
+ * Neumann contexts: out = K_N ψ = ½ψ − ∂_n(Sψ) = ∂_n V⁺ of the interface problem with
+ * [v] = 0, [∂_n v] = ψ (reading R38).  Asynchronous, stream-ordered, no state change. */
 kfbi_status kfbi_apply(kfbi_ctx* ctx, const double* d_phi, double* d_out, void* stream);
 
-/* Full Dirichlet BVP solve (Procedures 2-3).  With world > 1 every rank passes the
+/* Full BVP solve (Procedures 2-3; Neumann: P:795-808 with GMRES on K_N, ĝ_N =
+ * g_N − ∂_n(Yf)⁺, u = Yf − Sψ; d_g then holds g_N = ∂_n u at the control points and d_phi_out ψ).  With world > 1 every rank passes the
  * same replicated g, f_isect, f_ctrl and its (full-size) f_grid; d_u receives the rank's slab
  * columns (others untouched); d_phi_out is replicated.
  *   d_g        g_D at the control points (M)

@@ -6,7 +6,11 @@ P:815-823 for Ψ).  One interface solve = Algorithm 1 steps 4-6:
 jumps → correction (Alg. 2) → fast solve (Alg. 4) → interpolation (Alg. 3).
 
 Reading R17: K_D φ = ½φ + Wφ is the interior one-sided value V⁺ of the interface solution
-with Φ = φ (no explicit ½φ term).  Reading R27 (multiply connected, κ = 0): the completed
+with Φ = φ (no explicit ½φ term).  Neumann (reading R38): K_N ψ = ½ψ − ∂_n(Sψ) is the
+interior one-sided normal derivative ∂_n V⁺ of the interface solution with [v] = 0, [∂_n v] = ψ
+(the interface problem of P:812-821, v = −Sψ), read off the local quadratic fit of Alg. 3 (its
+gradient rows); ĝ_N = g_N − ∂_n(Yf)⁺ and u = Yf − Sψ = one interface solve with
+Ψ = ψ and F = f.  κ > 0 only (κ = 0 has the constant null space).  Reading R27 (multiply connected, κ = 0): the completed
 operator K̃φ = K_Dφ + Σ_h a_h(φ) w_h|Γ with a_h = ∫_{Γ_h} φ ds (periodic trapezoid) and
 w_h the fast solve of (Δ_h − κ) w = b_h, b_h a smooth bump inside hole h.
 """
@@ -52,7 +56,12 @@ class Oracle2D:
         n = st.n
         X, Y = np.meshgrid(st.x, st.x, indexing="ij")
         self.X, self.Y = X, Y
-        self.holes = [k for k, c in enumerate(prob.comps) if c.role == HOLE] if self.kappa == 0.0 else []
+        self.neumann = getattr(prob, "bc", 0) == 1
+        if self.neumann and self.kappa <= 0.0:
+            raise ValueError("Neumann BVP needs κ > 0 (S:555)")
+        self.z_nrm = np.stack([self.z_tau[1], -self.z_tau[0]])       # outward normal n = (τ2, −τ1)
+        self.holes = ([k for k, c in enumerate(prob.comps) if c.role == HOLE]
+                      if self.kappa == 0.0 and not self.neumann else [])
         self.w_gamma = []
         for k in self.holes:
             b = bump(prob.comps[k], X, Y)[1:n, 1:n]
@@ -122,6 +131,26 @@ class Oracle2D:
             out = out + a * wg
         return out
 
+    def normal_derivative(self, coef):
+        """∂_n V⁺ = n·(V⁺_x, V⁺_y) from the local quadratic fit coefficients at the control points."""
+        return coef[:, 1] * self.z_nrm[0] + coef[:, 2] * self.z_nrm[1]
+
+    def apply_KN(self, psi):
+        """K_N ψ = ∂_n V⁺ of the interface problem with Φ = 0, Ψ = ψ, F = 0 (R38)."""
+        n = self.st.n
+        jq, jz = self.jumps_from(psi=psi)
+        _, coef = self.interface_solve(np.zeros((n - 1, n - 1)), jq, jz, want_grad=True)
+        return self.normal_derivative(coef)
+
+    def apply_K(self, x):
+        return self.apply_KN(x) if self.neumann else self.apply_KD(x)
+
+    def apply_Yn(self, f_grid, f_isect, f_ctrl):
+        """∂_n(Yf)⁺ at the control points."""
+        jq, jz = self.jumps_from(Fq=f_isect, Fz=f_ctrl)
+        _, coef = self.interface_solve(self.base_rhs(f_grid), jq, jz, want_grad=True)
+        return self.normal_derivative(coef)
+
     def base_rhs(self, f_grid):
         """Zero extension f̃ = f·1_Ω at the unknowns."""
         n = self.st.n
@@ -151,10 +180,17 @@ class Oracle2D:
             zx, zy = self.ctrl_points()
             fg = f(self.X[1:n, 1:n], self.Y[1:n, 1:n])
             fq, fz = f(px, py), f(zx, zy)
-            ghat = g - self.apply_Y(fg, fq, fz)
+            ghat = g - self.apply_Y(fg, fq, fz) if not self.neumann else None
         else:
             fg = fq = fz = None
             ghat = g.copy()
+        if self.neumann:   # g = g_N = ∂_n u on Γ at the control points
+            ghat = g - (self.apply_Yn(fg, fq, fz) if f is not None else 0.0)
+            psi, stats = gmres(self.apply_KN, ghat, x0=phi0, tol=tol, restart=restart, max_restarts=max_restarts)
+            base = self.base_rhs(fg) if f is not None else np.zeros((n - 1, n - 1))
+            jq, jz = self.jumps_from(psi=psi, Fq=fq, Fz=fz)
+            u, _ = self.interface_solve(base, jq, jz)   # u = Yf − Sψ
+            return u, psi, stats
         phi, stats = gmres(self.apply_KD, ghat, x0=phi0, tol=tol, restart=restart, max_restarts=max_restarts)
         u = self.final(phi, fg, fq, fz)
         return u, phi, stats

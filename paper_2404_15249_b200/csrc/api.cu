@@ -117,6 +117,7 @@ void layout(kfbi_ctx* c, Arena& A) {
   T.ocol_ncls = A.table(S.ocol_ncls);
   T.st_node = A.table(S.st_node); T.st_ext = A.table(S.st_ext);
   T.st_w = A.table(S.st_w); T.st_dx = A.table(S.st_dx); T.st_dy = A.table(S.st_dy);
+  T.st_wn = A.table(S.st_wn); T.neumann = S.neumann ? 1 : 0;
   // component tables live in the setup object as small vectors
   auto& coff = c->coff; auto& cM = c->cM; auto& cdel = c->cdel;
   coff.clear(); cM.clear(); cdel.clear();
@@ -523,6 +524,10 @@ kfbi_status kfbi_setup(const kfbi_grid* grid, const kfbi_boundary* bnd, const kf
     g_setup_err = e.what();
     delete c;
     return KFBI_EGEOM;
+  } catch (const UnsupportedError& e) {
+    g_setup_err = e.what();
+    delete c;
+    return KFBI_EUNSUPPORTED;
   } catch (const std::exception& e) {
     g_setup_err = e.what();
     delete c;
@@ -607,6 +612,10 @@ kfbi_status kfbi_sizes(const kfbi_ctx* c, int64_t* M, int64_t* nq, int64_t* nirr
 kfbi_status kfbi_points(const kfbi_ctx* c, int32_t which, double* xyz) {
   if (!c || !xyz) return KFBI_EINVAL;
   if (c->dim == 3) {
+    if (which == 2) {   // outward unit normals at the control points
+      std::memcpy(xyz, c->S3.q_n.data(), c->S3.q_n.size() * sizeof(double));
+      return KFBI_OK;
+    }
     if (which != 0 && which != 1) return KFBI_EINVAL;
     std::memcpy(xyz, c->S3.q_pos.data(), c->S3.q_pos.size() * sizeof(double));
     return KFBI_OK;
@@ -614,6 +623,8 @@ kfbi_status kfbi_points(const kfbi_ctx* c, int32_t which, double* xyz) {
   const Setup& S = c->S;
   if (which == 0) {
     for (int m = 0; m < S.M; ++m) { xyz[2 * m] = S.z_x[m]; xyz[2 * m + 1] = S.z_y[m]; }
+  } else if (which == 2) {   // outward unit normals n = (τ2, −τ1) at the control points (R8)
+    for (int m = 0; m < S.M; ++m) { xyz[2 * m] = S.z_t2[m]; xyz[2 * m + 1] = -S.z_t1[m]; }
   } else if (which == 1) {
     for (int q = 0; q < S.nq; ++q) { xyz[2 * q] = S.q_x[q]; xyz[2 * q + 1] = S.q_y[q]; }
   } else {

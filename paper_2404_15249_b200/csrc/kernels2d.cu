@@ -143,7 +143,9 @@ __global__ void k_correct(DevTables T, const double* __restrict__ phi, const dou
         spline_eval(phi, mk, T.c_off[c], T.c_M[c], T.c_delta[c], T.q_knot[q], T.q_t[q], Phi, Phis, Phiss);
       }
       double F = fq ? fq[q] : 0.0;
-      Jump6 J = jumps2d(Phi, Phis, Phiss, 0.0, 0.0, F, T.kappa, T.q_t1[q], T.q_t2[q], T.q_p1[q], T.q_p2[q]);
+      // Neumann (R38): the density is ψ = [∂_n v] with [v] = 0
+      Jump6 J = T.neumann ? jumps2d(0.0, 0.0, 0.0, Phi, Phis, F, T.kappa, T.q_t1[q], T.q_t2[q], T.q_p1[q], T.q_p2[q])
+                          : jumps2d(Phi, Phis, Phiss, 0.0, 0.0, F, T.kappa, T.q_t1[q], T.q_t2[q], T.q_p1[q], T.q_p2[q]);
       v = J.v;
       va = ax == 0 ? J.vx : J.vy;
       vaa = ax == 0 ? J.vxx : J.vyy;
@@ -781,7 +783,8 @@ __global__ void k_interp(DevTables T, const double* __restrict__ phi, const doub
       const int c = T.z_comp[m];
       spline_eval(phi, mk, T.c_off[c], T.c_M[c], T.c_delta[c], T.z_knot[m], 0.0, Phi, Phis, Phiss);
     }
-    J = jumps2d(Phi, Phis, Phiss, 0.0, 0.0, fz ? fz[m] : 0.0, T.kappa, T.z_t1[m], T.z_t2[m], T.z_p1[m], T.z_p2[m]);
+    J = T.neumann ? jumps2d(0.0, 0.0, 0.0, Phi, Phis, fz ? fz[m] : 0.0, T.kappa, T.z_t1[m], T.z_t2[m], T.z_p1[m], T.z_p2[m])
+                  : jumps2d(Phi, Phis, Phiss, 0.0, 0.0, fz ? fz[m] : 0.0, T.kappa, T.z_t1[m], T.z_t2[m], T.z_p1[m], T.z_p2[m]);
   }
   double acc = 0.0;
 #pragma unroll
@@ -797,7 +800,7 @@ __global__ void k_interp(DevTables T, const double* __restrict__ phi, const doub
       const double dx = T.st_dx[idx], dy = T.st_dy[idx];
       v += J.v + J.vx * dx + J.vy * dy + 0.5 * J.vxx * dx * dx + J.vxy * dx * dy + 0.5 * J.vyy * dy * dy;
     }
-    acc = fma(T.st_w[idx], v, acc);
+    acc = fma(T.neumann ? T.st_wn[idx] : T.st_w[idx], v, acc);   // V⁺ or ∂_n V⁺ (Neumann, R38)
   }
   if (!partial || T.rank == 0)
     for (int hh = 0; hh < nh; ++hh) acc = fma(ahole[hh], wg[(size_t)hh * T.M + m], acc);

@@ -54,6 +54,9 @@ struct GeomError : std::runtime_error {
 struct ArgError : std::runtime_error {
   using std::runtime_error::runtime_error;
 };
+struct UnsupportedError : std::runtime_error {   // → KFBI_EUNSUPPORTED
+  using std::runtime_error::runtime_error;
+};
 
 struct Comp {
   int kind, role;
@@ -96,6 +99,8 @@ struct Setup {
   std::vector<int32_t> st_node;          // M*6 → unique stencil node index
   std::vector<int8_t> st_ext;            // M*6: 1 if the node is in Ω^c
   std::vector<double> st_w, st_dx, st_dy;   // M*6: row 0 of the inverse local system, offsets
+  std::vector<double> st_wn;              // M*6: normal-derivative row n·(row 1, row 2) (Neumann)
+  bool neumann = false;
   std::vector<int64_t> st_nodes_ij;      // M*6*2 (dump)
   // spline filters: per component taps, coefficients (already scaled by 6/Δ²)
   std::vector<int32_t> sp_ntaps, sp_first, sp_coef_off;
@@ -188,7 +193,8 @@ struct DevTables {
   // stencils
   const int32_t *sn_j, *ocol, *ocol_ptr, *st_node, *ocol_ncls;
   const int8_t* st_ext;
-  const double *st_w, *st_dx, *st_dy;
+  const double *st_w, *st_dx, *st_dy, *st_wn;
+  int neumann;   // K_N: density = ψ (Φ = 0, Ψ = ψ) and the normal-derivative interpolation
   // spline
   const int32_t *c_off, *c_M, *sp_ntaps, *sp_first, *sp_coef_off;
   const double *c_delta, *sp_coef;

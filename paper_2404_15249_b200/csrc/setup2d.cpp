@@ -170,7 +170,9 @@ void build_setup(Setup& S, const kfbi_grid* g, const kfbi_boundary* b, const kfb
   if (!g || !b || !pde || !b->comp || b->ncomp < 1) throw ArgError("null descriptor");
   if (g->dim != 2) throw ArgError("only dim = 2 is built in this library version");
   if (pde->kappa < 0) throw ArgError("kappa must be >= 0 (P:458)");
-  if (pde->bc != KFBI_DIRICHLET) throw ArgError("only Dirichlet BVPs are built");
+  if (pde->bc != KFBI_DIRICHLET && pde->bc != KFBI_NEUMANN) throw ArgError("bc must be DIRICHLET or NEUMANN");
+  if (pde->bc == KFBI_NEUMANN && !(pde->kappa > 0)) throw UnsupportedError("Neumann needs kappa > 0 (S:555)");
+  S.neumann = pde->bc == KFBI_NEUMANN;
   int N = g->n[0];
   if (g->n[1] != N || N < 64 || N > 8192 || (N & (N - 1))) throw ArgError("n must be equal powers of two in [64, 8192]");
   double h0 = (g->hi[0] - g->lo[0]) / N, h1 = (g->hi[1] - g->lo[1]) / N;
@@ -378,6 +380,7 @@ void build_setup(Setup& S, const kfbi_grid* g, const kfbi_boundary* b, const kfb
   std::vector<int64_t> nodes((size_t)M * 6 * 2);
   S.st_ext.assign((size_t)M * 6, 0);
   S.st_w.assign((size_t)M * 6, 0);
+  S.st_wn.assign((size_t)M * 6, 0);
   S.st_dx.assign((size_t)M * 6, 0);
   S.st_dy.assign((size_t)M * 6, 0);
   bool bad = false;
@@ -405,8 +408,16 @@ void build_setup(Setup& S, const kfbi_grid* g, const kfbi_boundary* b, const kfb
       for (int q = 0; q < 6; ++q) A[q * 6 + p] = row[q];
       w[p] = p == 0 ? 1.0 : 0.0;
     }
+    double A2[36], wn[6] = {0, 0, 0, 0, 0, 0};
+    std::copy(A, A + 36, A2);
     if (!lu_solve(6, A, w)) bad = true;
     for (int p = 0; p < 6; ++p) S.st_w[m * 6 + p] = w[p];
+    // normal derivative n·∇ of the local quadratic (Neumann, R38): Aᵀ w_n = (0, n_x, n_y, 0, 0, 0),
+    // n = (τ2, −τ1)
+    wn[1] = S.z_t2[m];
+    wn[2] = -S.z_t1[m];
+    if (!lu_solve(6, A2, wn)) bad = true;
+    for (int p = 0; p < 6; ++p) S.st_wn[m * 6 + p] = wn[p];
   }
   if (bad) throw GeomError("interpolation stencil leaves the grid or is singular");
   S.st_nodes_ij = nodes;

@@ -81,6 +81,7 @@ void build_setup3(Setup3& S, const kfbi_grid* g, const kfbi_boundary* b, const k
   const int N = g->n[0];
   if (g->n[1] != N || g->n[2] != N || N < 32 || N > 512 || (N & (N - 1)))
     throw ArgError("3D: n must be equal powers of two in [32, 512]");
+  if (pde->bc != KFBI_DIRICHLET) throw UnsupportedError("3D: only the Dirichlet BVP is built");
   const double h = (g->hi[0] - g->lo[0]) / N;
   for (int a = 1; a < 3; ++a)
     if (std::fabs((g->hi[a] - g->lo[a]) / N - h) > 1e-12 * h || std::fabs(g->lo[a] - g->lo[0]) > 1e-12 * h)

@@ -170,7 +170,7 @@ class KFBI:
             comps[k] = Component(c.kind, c.role, (C.c_double * 3)(*cen), (C.c_double * 4)(*c.p), c.n_ctrl)
         self._comps = comps
         b = Boundary(len(problem.comps), comps)
-        pde = Pde(problem.kappa, 0)
+        pde = Pde(problem.kappa, int(getattr(problem, "bc", 0)))
         self._nccl = (C.c_uint8 * 128).from_buffer_copy(nccl_id) if nccl_id is not None else None
         dist = Dist(world, rank, device, C.cast(self._nccl, C.c_void_p) if self._nccl is not None else None)
         self.world, self.rank = world, rank
@@ -224,10 +224,12 @@ class KFBI:
 
     # ------------------------------------------------------------------ API
     def points(self, which="ctrl"):
-        n = self.M if which == "ctrl" else self.nq
+        """which: "ctrl" (control points), "isect" (intersection nodes), "normal" (outward unit
+        normals at the control points)."""
+        code = {"ctrl": 0, "isect": 1, "normal": 2}[which]
+        n = self.nq if which == "isect" else self.M
         out = np.zeros((n, self.problem.dim))
-        self._check(self.lib.kfbi_points(self.ctx, 0 if which == "ctrl" else 1,
-                                         out.ctypes.data_as(C.POINTER(C.c_double))))
+        self._check(self.lib.kfbi_points(self.ctx, code, out.ctypes.data_as(C.POINTER(C.c_double))))
         return out
 
     def node_mask(self):

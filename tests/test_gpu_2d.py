@@ -222,3 +222,42 @@ def test_partitioned_solve_matches_oracle():
     m = o.st.side
     assert s.converged and abs(s.iters - s_ref.iters) <= 1
     assert rel(u.cpu().numpy()[m], u_ref[m]) < 1e-8
+
+
+# ------------------------------------------------------------------ Neumann BVP (NEXT-1, R38)
+NEU = [W.neumann(W.C2(1024)), W.neumann(W.problem("ellipse-k1", 2, 256, [W.ellipse(1.0, 0.8)], 1.0))]
+
+
+@pytest.mark.parametrize("prob", NEU, ids=lambda p: p.name + str(p.n))
+@pytest.mark.parametrize("dens", DENS)
+def test_apply_neumann_matches_oracle(prob, dens):
+    """K_N ψ = ∂_n V⁺ ([v] = 0, [∂_n v] = ψ) against the oracle."""
+    o, k = oracle(prob), gpu(prob)
+    psi = density(prob, o, dens)
+    assert rel(k.apply(psi).cpu().numpy(), o.apply_KN(psi)) < 1e-10
+
+
+def _ellipse_normal(x, y, a=1.0, b=0.8):
+    gx, gy = x / a ** 2, y / b ** 2
+    r = np.hypot(gx, gy)
+    return gx / r, gy / r
+
+
+def test_solve_neumann_matches_oracle():
+    prob = NEU[1]
+    o, k = oracle(prob), gpu(prob)
+    n = prob.n
+    f = lambda x, y: W.f_exact(prob.kappa, x, y)
+    gN = lambda x, y: sum(g * m for g, m in zip(W.grad_u_exact(x, y), _ellipse_normal(x, y)))
+    zx, zy = o.ctrl_points()
+    u_ref, psi_ref, s_ref = o.solve(gN(zx, zy), f)
+    pz, pq = k.points("ctrl"), k.points("isect")
+    x = prob.lo + np.arange(n + 1) * prob.h
+    X, Y = np.meshgrid(x, x, indexing="ij")
+    u, psi, s = k.solve(gN(pz[:, 0], pz[:, 1]), f(X, Y), f(pq[:, 0], pq[:, 1]), f(pz[:, 0], pz[:, 1]))
+    u = u.cpu().numpy()
+    m = o.st.side
+    assert s.converged and abs(s.iters - s_ref.iters) <= 1
+    assert rel(u[m], u_ref[m]) < 1e-8
+    assert rel(psi.cpu().numpy(), psi_ref) < 1e-8
+    assert np.abs(u[m] - W.u_exact(X, Y)[m]).max() < 5e-3

@@ -51,6 +51,7 @@ class Problem:
     hi: float
     comps: tuple
     kappa: float
+    bc: int = 0              # DIRICHLET (0) or NEUMANN (1)
 
     @property
     def h(self) -> float:
@@ -81,8 +82,16 @@ def torus(R, r, center=(0.0, 0.0, 0.0)):
     return Component(TORUS, tuple(float(x) for x in center), (float(R), float(r), 0.0, 0.0), OUTER, 0)
 
 
-def problem(name, dim, n, comps, kappa, lo=-1.2, hi=1.2) -> Problem:
-    return Problem(name, dim, int(n), float(lo), float(hi), tuple(comps), float(kappa))
+DIRICHLET, NEUMANN = 0, 1
+
+
+def problem(name, dim, n, comps, kappa, lo=-1.2, hi=1.2, bc=DIRICHLET) -> Problem:
+    return Problem(name, dim, int(n), float(lo), float(hi), tuple(comps), float(kappa), int(bc))
+
+
+def neumann(prob: Problem) -> Problem:
+    """The same geometry and κ with the Neumann boundary condition ∂_n u = g_N."""
+    return dataclasses.replace(prob, name=prob.name + "-neumann", bc=NEUMANN)
 
 
 # --- BASELINE.json configs (SURVEY §8(d.2)) -------------------------------------------
@@ -127,6 +136,13 @@ def lap_u_exact(x, y, z=None):
     if z is None:
         return -2.0 * np.sin(x) * np.sin(y)
     return -3.0 * np.sin(x) * np.sin(y) * np.sin(z)
+
+
+def grad_u_exact(x, y):
+    """∇u* (2D), for the Neumann data g_N = n·∇u* (P:787)."""
+    ux = np.exp(x) * np.cos(y) + np.exp(y) * np.cos(x) + np.cos(x) * np.sin(y)
+    uy = -np.exp(x) * np.sin(y) + np.exp(y) * np.sin(x) + np.sin(x) * np.cos(y)
+    return ux, uy
 
 
 def f_exact(kappa, x, y, z=None):

@@ -161,6 +161,8 @@ def main():
     ap.add_argument("--config", default="C3")
     ap.add_argument("--n", type=int, default=0, help="override grid size")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--method", default="gmres", choices=["gmres", "richardson", "bicgstab"],
+                    help="outer iteration (P:495-502 Richardson, BiCGSTAB, GMRES Alg. 5)")
     ap.add_argument("--bc", default="dirichlet", choices=["dirichlet", "neumann"],
                     help="boundary condition (neumann: 2D, κ > 0 configs, e.g. --config C2)")
     args = ap.parse_args()
@@ -202,7 +204,7 @@ def main():
     stream = torch.cuda.current_stream(dev)
 
     def step():
-        return k.solve(g_d, fg_d, fq_d, fz_d, u=u_d)
+        return k.solve(g_d, fg_d, fq_d, fz_d, u=u_d, method=args.method)
 
     for _ in range(args.warmup):
         _, _, st = step()
@@ -247,7 +249,7 @@ def main():
         fgd = fg_h.to(dev, non_blocking=True)
         fqd = fq_h.to(dev, non_blocking=True)
         fzd = fz_h.to(dev, non_blocking=True)
-        u, _, st2 = k.solve(gd, fgd, fqd, fzd)
+        u, _, st2 = k.solve(gd, fgd, fqd, fzd, method=args.method)
         u_h.copy_(u.view(-1), non_blocking=True)
         e1.record(stream)
         e1.synchronize()
@@ -295,7 +297,7 @@ def main():
             stream.wait_event(ev_in[b])
             if j >= 2:
                 stream.wait_event(ev_out[b])                # download j−2 has left dout[b]
-            k.solve(*din[b], u=dout[b])
+            k.solve(*din[b], u=dout[b], method=args.method)
             ev_done[b].record(stream)
             with torch.cuda.stream(d2h_s):
                 d2h_s.wait_event(ev_done[b])
@@ -339,6 +341,7 @@ def main():
         "scaling": "strong" if sharded else "weak",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic (manufactured u*, reading R24)",
         "config": {"workload": prob.name, "grid": prob.n, "unknowns": U, "kappa": prob.kappa, "M": k.M,
+                   "bc": "neumann" if prob.bc == W.NEUMANN else "dirichlet", "method": args.method,
                    "intersections": k.nq, "irregular": k.nirr,
                    "parallelism": "single-gpu" if world == 1 else (f"slabs{world}-nccl" if sharded else f"replicas{world}"),
                    "l2": "flushed between timed steps (256 MB write before each step)"},

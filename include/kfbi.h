@@ -99,7 +99,12 @@ typedef struct {
   double tol;            /* relative residual, default 1e-8          */
   int32_t restart;       /* GMRES(m), default 30 (R18)                       */
   int32_t max_restarts;  /* default 50                                       */
+  int32_t method;        /* KFBI_GMRES (default), KFBI_RICHARDSON (φ += γ(ĝ − Kφ)),
+                            KFBI_BICGSTAB (textbook, 2 applies per iteration); the last two run
+                            at most restart × max_restarts iterations (reading R39)            */
+  double gamma;          /* Richardson relaxation γ ∈ (0, 1], default 1               */
 } kfbi_solve_opts;
+enum { KFBI_GMRES = 0, KFBI_RICHARDSON = 1, KFBI_BICGSTAB = 2 };
 
 typedef struct {
   int32_t iters;         /* Arnoldi steps (applies of K inside cycles)        */

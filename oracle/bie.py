@@ -21,6 +21,7 @@ import numpy as np
 from workloads import HOLE
 from . import correction, fastsolve, geometry as geo, grid, interp, jumps, spline
 from .gmres import gmres
+from .krylov import bicgstab, richardson
 
 
 def bump(comp, X, Y):
@@ -172,7 +173,14 @@ class Oracle2D:
         v, _ = self.interface_solve(base, jq, jz)
         return v
 
-    def solve(self, g, f=None, tol=1e-8, restart=30, max_restarts=50, phi0=None):
+    def _krylov(self, K, ghat, phi0, tol, restart, max_restarts, method, gamma):
+        if method == "richardson":
+            return richardson(K, ghat, gamma=gamma, x0=phi0, tol=tol, max_iter=restart * max_restarts)
+        if method == "bicgstab":
+            return bicgstab(K, ghat, x0=phi0, tol=tol, max_iter=restart * max_restarts)
+        return gmres(K, ghat, x0=phi0, tol=tol, restart=restart, max_restarts=max_restarts)
+
+    def solve(self, g, f=None, tol=1e-8, restart=30, max_restarts=50, phi0=None, method="gmres", gamma=1.0):
         """Procedures 2-3: ĝ = g − (Yf)⁺, GMRES on K φ = ĝ, final field."""
         n = self.st.n
         if f is not None:
@@ -186,12 +194,12 @@ class Oracle2D:
             ghat = g.copy()
         if self.neumann:   # g = g_N = ∂_n u on Γ at the control points
             ghat = g - (self.apply_Yn(fg, fq, fz) if f is not None else 0.0)
-            psi, stats = gmres(self.apply_KN, ghat, x0=phi0, tol=tol, restart=restart, max_restarts=max_restarts)
+            psi, stats = self._krylov(self.apply_KN, ghat, phi0, tol, restart, max_restarts, method, gamma)
             base = self.base_rhs(fg) if f is not None else np.zeros((n - 1, n - 1))
             jq, jz = self.jumps_from(psi=psi, Fq=fq, Fz=fz)
             u, _ = self.interface_solve(base, jq, jz)   # u = Yf − Sψ
             return u, psi, stats
-        phi, stats = gmres(self.apply_KD, ghat, x0=phi0, tol=tol, restart=restart, max_restarts=max_restarts)
+        phi, stats = self._krylov(self.apply_KD, ghat, phi0, tol, restart, max_restarts, method, gamma)
         u = self.final(phi, fg, fq, fz)
         return u, phi, stats
 

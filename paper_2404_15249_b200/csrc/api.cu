@@ -650,15 +650,141 @@ kfbi_status kfbi_apply(kfbi_ctx* c, const double* d_phi, double* d_out, void* st
   return KFBI_OK;
 }
 
+// ---- Richardson and BiCGSTAB drivers (reading R39) over the same apply ----
+// scalars leave the device through the host-mapped buffer (no copy engine), one sync per batch
+namespace {
+void dots(kfbi_ctx* c, int n, const double* const* a, const double* const* b, const bool* take_sqrt, double* out,
+          cudaStream_t s) {
+  const int M = nctrl(c);
+  for (int q = 0; q < n; ++q) {
+    launch_dot(M, a[q], b[q], c->partial + (size_t)q * kRedBlocks, s);
+    launch_finish_sum(c->partial + (size_t)q * kRedBlocks, c->scal + q, take_sqrt[q], s);
+  }
+  launch_copy(n, c->scal, c->hcol_map, s);
+  ck(cudaStreamSynchronize(s), "sync scalars");
+  for (int q = 0; q < n; ++q) out[q] = c->hcol_host[q];
+}
+double norm2(kfbi_ctx* c, const double* a, cudaStream_t s) {
+  const double* av[1] = {a};
+  const bool sq[1] = {true};
+  double v;
+  dots(c, 1, av, av, sq, &v, s);
+  return v;
+}
+void axpy(kfbi_ctx* c, double alpha, const double* xv, double* y, cudaStream_t s) {   // y += α x
+  launch_axpy_basis(nctrl(c), 1, xv, nctrl(c), &alpha, y, s);
+}
+
+// φ_{k+1} = φ_k + γ(ĝ − Kφ_k), explicit residual every iteration, ‖r‖ ≤ tol‖r₀‖
+bool solve_richardson(kfbi_ctx* c, const kfbi_solve_opts& o, bool have_x0, kfbi_solve_stats& st, cudaStream_t s) {
+  const int M = nctrl(c), max_iter = o.restart * o.max_restarts;
+  double r0 = -1.0;
+  for (int it = 0; it <= max_iter; ++it) {
+    if (!have_x0 && it == 0) {
+      launch_copy(M, c->ghat, c->gr, s);
+    } else {
+      apply_KD(c, c->gx, c->tmp, s);
+      st.n_applies++;
+      launch_sub(M, c->ghat, c->tmp, c->gr, s);
+    }
+    const double nr = norm2(c, c->gr, s);
+    if (!std::isfinite(nr)) throw std::runtime_error("non-finite residual");
+    if (r0 < 0) r0 = nr;
+    st.rel_residual = r0 > 0 ? nr / r0 : 0.0;
+    if (nr <= o.tol * r0 || r0 == 0.0) return true;
+    if (it == max_iter) break;
+    axpy(c, o.gamma, c->gr, c->gx, s);
+    st.iters++;
+  }
+  return false;
+}
+
+// BiCGSTAB (van der Vorst 1992), shadow residual r̂ = r₀; vectors in the GMRES basis storage
+bool solve_bicgstab(kfbi_ctx* c, const kfbi_solve_opts& o, bool have_x0, kfbi_solve_stats& st, cudaStream_t s) {
+  const int M = nctrl(c), max_iter = o.restart * o.max_restarts;
+  double *rhat = c->V, *r = c->V + M, *p = c->V + 2 * (size_t)M, *v = c->V + 3 * (size_t)M,
+         *sv = c->V + 4 * (size_t)M, *t = c->V + 5 * (size_t)M;
+  if (!have_x0) {
+    launch_copy(M, c->ghat, r, s);
+  } else {
+    apply_KD(c, c->gx, c->tmp, s);
+    st.n_applies++;
+    launch_sub(M, c->ghat, c->tmp, r, s);
+  }
+  launch_copy(M, r, rhat, s);
+  const double n0 = norm2(c, r, s);
+  if (!std::isfinite(n0)) throw std::runtime_error("non-finite residual");
+  st.rel_residual = n0 > 0 ? 1.0 : 0.0;
+  if (n0 == 0.0) return true;
+  double rho_prev = 1.0, alpha = 1.0, omega = 1.0;
+  const bool no_sqrt[2] = {false, false};
+  for (int it = 0; it < max_iter; ++it) {
+    double rho;
+    {
+      const double* a[1] = {rhat};
+      const double* b[1] = {r};
+      dots(c, 1, a, b, no_sqrt, &rho, s);
+    }
+    const double beta = (rho / rho_prev) * (alpha / omega);
+    if (it == 0) {
+      launch_copy(M, r, p, s);                       // p = r (p = v = 0 before)
+    } else {                                         // p = r + β(p − ω v)
+      launch_copy(M, r, c->tmp, s);
+      axpy(c, beta, p, c->tmp, s);
+      axpy(c, -beta * omega, v, c->tmp, s);
+      launch_copy(M, c->tmp, p, s);
+    }
+    apply_KD(c, p, v, s);
+    st.n_applies++;
+    double rv;
+    {
+      const double* a[1] = {rhat};
+      const double* b[1] = {v};
+      dots(c, 1, a, b, no_sqrt, &rv, s);
+    }
+    alpha = rho / rv;
+    launch_copy(M, r, sv, s);                        // s = r − α v
+    axpy(c, -alpha, v, sv, s);
+    st.iters++;
+    const double ns = norm2(c, sv, s);
+    if (!std::isfinite(ns)) throw std::runtime_error("non-finite BiCGSTAB residual");
+    if (ns <= o.tol * n0) {
+      axpy(c, alpha, p, c->gx, s);
+      st.rel_residual = ns / n0;
+      return true;
+    }
+    apply_KD(c, sv, t, s);
+    st.n_applies++;
+    double ts_tt[2];
+    {
+      const double* a[2] = {t, t};
+      const double* b[2] = {sv, t};
+      dots(c, 2, a, b, no_sqrt, ts_tt, s);
+    }
+    omega = ts_tt[0] / ts_tt[1];
+    axpy(c, alpha, p, c->gx, s);                     // x += α p + ω s
+    axpy(c, omega, sv, c->gx, s);
+    launch_copy(M, sv, r, s);                        // r = s − ω t
+    axpy(c, -omega, t, r, s);
+    rho_prev = rho;
+    const double nr = norm2(c, r, s);
+    st.rel_residual = nr / n0;
+    if (nr <= o.tol * n0) return true;
+  }
+  return false;
+}
+}  // namespace
+
 kfbi_status kfbi_solve(kfbi_ctx* c, const double* d_g, const double* d_f_grid, const double* d_f_isect,
                        const double* d_f_ctrl, const double* d_phi0, double* d_u, double* d_phi_out,
                        const kfbi_solve_opts* opts, kfbi_solve_stats* stats, void* stream) {
   if (!c || !d_g || !d_u) return fail(c, KFBI_EINVAL, "null pointer");
   if ((d_f_grid == nullptr) != (d_f_isect == nullptr) || (d_f_grid == nullptr) != (d_f_ctrl == nullptr))
     return fail(c, KFBI_EINVAL, "f_grid, f_isect, f_ctrl must all be given or all NULL");
-  kfbi_solve_opts o{1e-8, 30, 50};
+  kfbi_solve_opts o{1e-8, 30, 50, KFBI_GMRES, 1.0};
   if (opts) o = *opts;
-  if (o.restart < 1 || o.restart > kMaxRestart || o.max_restarts < 1 || !(o.tol > 0))
+  if (o.restart < 1 || o.restart > kMaxRestart || o.max_restarts < 1 || !(o.tol > 0) || o.method < 0 ||
+      o.method > KFBI_BICGSTAB || (o.method == KFBI_RICHARDSON && !(o.gamma > 0 && o.gamma <= 1)))
     return fail(c, KFBI_EINVAL, "bad solve options");
   kfbi_solve_stats st{};
   auto t0 = std::chrono::steady_clock::now();
@@ -679,6 +805,10 @@ kfbi_status kfbi_solve(kfbi_ctx* c, const double* d_g, const double* d_f_grid, c
   // GMRES(m), Algorithm 5, reading R18
   if (d_phi0) launch_copy(M, d_phi0, c->gx, s);
   else ck(cudaMemsetAsync(c->gx, 0, bM, s), "zero x");
+  if (o.method != KFBI_GMRES) {
+    converged = o.method == KFBI_RICHARDSON ? solve_richardson(c, o, d_phi0 != nullptr, st, s)
+                                            : solve_bicgstab(c, o, d_phi0 != nullptr, st, s);
+  } else {
   double beta0 = -1.0;
   std::vector<double> H((size_t)(o.restart + 1) * o.restart), cs(o.restart), sn(o.restart), gv(o.restart + 1), y(o.restart);
   auto Hc = [&](int i, int j) -> double& { return H[(size_t)i * o.restart + j]; };
@@ -745,6 +875,7 @@ kfbi_status kfbi_solve(kfbi_ctx* c, const double* d_g, const double* d_f_grid, c
       y[i] = sacc / Hc(i, i);
     }
     launch_axpy_basis(M, k, c->V, M, y.data(), c->gx, s);   // φ_m = φ_0 + M_m y_m
+  }
   }
   if (d_phi_out) launch_copy(M, c->gx, d_phi_out, s);
   // final field u = Wφ + Yf (+ Σ a_h w_h) (R27)

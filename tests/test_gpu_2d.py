@@ -261,3 +261,26 @@ def test_solve_neumann_matches_oracle():
     assert rel(u[m], u_ref[m]) < 1e-8
     assert rel(psi.cpu().numpy(), psi_ref) < 1e-8
     assert np.abs(u[m] - W.u_exact(X, Y)[m]).max() < 5e-3
+
+
+# ------------------------------------------------------------------ Richardson / BiCGSTAB (NEXT-4)
+@pytest.mark.parametrize("method", ["richardson", "bicgstab"])
+@pytest.mark.parametrize("prob", [W.C1(64), W.C2(1024), NEU[1]], ids=lambda p: p.name + str(p.n))
+def test_solve_drivers_match_oracle(prob, method):
+    o, k = oracle(prob), gpu(prob)
+    n = prob.n
+    f = lambda x, y: W.f_exact(prob.kappa, x, y)
+    if prob.bc == W.NEUMANN:
+        g = lambda x, y: sum(a * b for a, b in zip(W.grad_u_exact(x, y), _ellipse_normal(x, y)))
+    else:
+        g = W.u_exact
+    zx, zy = o.ctrl_points()
+    u_ref, phi_ref, s_ref = o.solve(g(zx, zy), f, method=method)
+    pz, pq = k.points("ctrl"), k.points("isect")
+    x = prob.lo + np.arange(n + 1) * prob.h
+    X, Y = np.meshgrid(x, x, indexing="ij")
+    u, phi, s = k.solve(g(pz[:, 0], pz[:, 1]), f(X, Y), f(pq[:, 0], pq[:, 1]), f(pz[:, 0], pz[:, 1]), method=method)
+    m = o.st.side
+    assert s.converged and s_ref.converged and abs(s.iters - s_ref.iters) <= 1
+    assert rel(u.cpu().numpy()[m], u_ref[m]) < 1e-8
+    assert rel(phi.cpu().numpy(), phi_ref) < 1e-8

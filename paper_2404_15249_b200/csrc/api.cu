@@ -841,7 +841,8 @@ kfbi_status kfbi_solve(kfbi_ctx* c, const double* d_g, const double* d_f_grid, c
       apply_KD(c, c->V + (size_t)j * M, w, s);
       st.iters++;
       st.n_applies++;
-      // MGS exactly as P:765-768, deterministic fixed-grid reductions
+      // MGS exactly as P:765-768, deterministic reductions (one fused CTA for small M)
+      if (!launch_mgs_fused(M, j, c->V, w, c->hcol, s)) {
       for (int i = 0; i <= j; ++i)
         launch_mgs_step(M, w, i ? c->V + (size_t)(i - 1) * M : nullptr, c->V + (size_t)i * M,
                         i ? c->partial + (size_t)(i - 1) * kRedBlocks : nullptr, c->partial + (size_t)i * kRedBlocks,
@@ -849,6 +850,7 @@ kfbi_status kfbi_solve(kfbi_ctx* c, const double* d_g, const double* d_f_grid, c
       launch_mgs_step(M, w, c->V + (size_t)j * M, w, c->partial + (size_t)j * kRedBlocks,
                       c->partial + (size_t)(j + 1) * kRedBlocks, c->hcol + j, s);
       launch_norm_scale(M, w, c->partial + (size_t)(j + 1) * kRedBlocks, c->hcol + j + 1, s);
+      }
       launch_copy(j + 2, c->hcol, c->hcol_map, s);
       ck(cudaStreamSynchronize(s), "sync hcol");
       for (int i = 0; i <= j + 1; ++i) Hc(i, j) = c->hcol_host[i];

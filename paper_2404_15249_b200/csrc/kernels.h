@@ -59,6 +59,8 @@ extern long long g_launches;   // kernels launched by this library (all launcher
 void launch_mgs_step(int n, double* w, const double* Vprev, const double* Vcur, const double* partial_prev,
                      double* partial_cur, double* hout, cudaStream_t s);
 void launch_norm_scale(int n, double* w, const double* partial, double* hout, cudaStream_t s);
+// one-CTA fused MGS step for n ≤ 27648 (returns false → use the multi-CTA path)
+bool launch_mgs_fused(int n, int j, const double* V, double* w, double* hcol, cudaStream_t s);
 void launch_dot(int n, const double* a, const double* b, double* partial, cudaStream_t s);
 void launch_finish_sum(const double* partial, double* out, bool take_sqrt, cudaStream_t s);
 // GMRES update x += V y, y (k ≤ kYMax coefficients, host array) passed by value in the launch

@@ -931,6 +931,41 @@ __global__ void k_norm_scale(int n, double* w, const double* __restrict__ partia
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) w[i] = w[i] / hn;
 }
 
+// Whole MGS step of Arnoldi iteration j in one CTA (small M): w stays in shared memory while the
+// j+1 basis vectors stream by; h_i = (w, μ_i), w −= h_i μ_i for i = 0..j, then
+// h_{j+1} = ‖w‖ and w /= h_{j+1}.  Deterministic block reductions.
+constexpr int kMgsThreads = 1024, kMgsMax = 27 * 1024;   // w (≤ 216 KB) in shared memory
+__global__ void __launch_bounds__(kMgsThreads) k_mgs_fused(int n, int j, const double* __restrict__ V, double* w,
+                                                           double* hcol) {
+  extern __shared__ double sw[];
+  __shared__ double scratch[32];
+  __shared__ double s_h;
+  for (int idx = threadIdx.x; idx < n; idx += kMgsThreads) sw[idx] = w[idx];
+  for (int i = 0; i <= j; ++i) {
+    const double* vi = V + (size_t)i * n;
+    double acc[1] = {0.0};
+    for (int idx = threadIdx.x; idx < n; idx += kMgsThreads) acc[0] = fma(sw[idx], vi[idx], acc[0]);
+    block_reduce<1>(acc, scratch);
+    if (threadIdx.x == 0) {
+      s_h = acc[0];
+      hcol[i] = acc[0];
+    }
+    __syncthreads();
+    const double h = s_h;
+    for (int idx = threadIdx.x; idx < n; idx += kMgsThreads) sw[idx] = fma(-h, vi[idx], sw[idx]);
+  }
+  double acc[1] = {0.0};
+  for (int idx = threadIdx.x; idx < n; idx += kMgsThreads) acc[0] = fma(sw[idx], sw[idx], acc[0]);
+  block_reduce<1>(acc, scratch);
+  if (threadIdx.x == 0) {
+    s_h = sqrt(acc[0]);
+    hcol[j + 1] = s_h;
+  }
+  __syncthreads();
+  const double hn = s_h;
+  for (int idx = threadIdx.x; idx < n; idx += kMgsThreads) w[idx] = hn == 0.0 ? sw[idx] : sw[idx] / hn;
+}
+
 __global__ void k_dot(int n, const double* __restrict__ a, const double* __restrict__ b, double* __restrict__ partial) {
   __shared__ double scratch[32];
   const int per = (n + gridDim.x - 1) / gridDim.x;
@@ -1112,6 +1147,17 @@ void launch_interp(const DevTables& T, const double* phi, const double* mk, cons
 void launch_mgs_step(int n, double* w, const double* Vprev, const double* Vcur, const double* partial_prev,
                      double* partial_cur, double* hout, cudaStream_t s) {
   { ++g_launches; k_mgs_step<<<kRedBlocks, 256, 0, s>>>(n, w, Vprev, Vcur, partial_prev, partial_cur, hout); }
+}
+
+bool launch_mgs_fused(int n, int j, const double* V, double* w, double* hcol, cudaStream_t s) {
+  if (n > kMgsMax) return false;
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(k_mgs_fused, cudaFuncAttributeMaxDynamicSharedMemorySize, kMgsMax * (int)sizeof(double));
+    attr = true;
+  }
+  { ++g_launches; k_mgs_fused<<<1, kMgsThreads, (size_t)n * sizeof(double), s>>>(n, j, V, w, hcol); }
+  return true;
 }
 
 void launch_norm_scale(int n, double* w, const double* partial, double* hout, cudaStream_t s) {

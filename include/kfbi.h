@@ -86,8 +86,8 @@ typedef struct {
 
 typedef struct {
   double kappa;          /* κ ≥ 0                                    */
-  int32_t bc;            /* KFBI_DIRICHLET, or KFBI_NEUMANN (2D, κ > 0; κ = 0 or 3D
-                            → KFBI_EUNSUPPORTED)                            */
+  int32_t bc;            /* KFBI_DIRICHLET, or KFBI_NEUMANN (κ > 0; κ = 0 →
+                            KFBI_EUNSUPPORTED)                       */
 } kfbi_pde;
 
 typedef struct {

@@ -56,7 +56,7 @@ def correct3d(st, base, jq):
     return f
 
 
-def interpolate3d(st, v_full, jz, nodes):
+def interpolate3d(st, v_full, jz, nodes, want_grad=False):
     M = st.M
     d = st.x[nodes] - st.q_pos[:, None, :]                      # (M, 10, 3)
     dx, dy, dz = d[..., 0], d[..., 1], d[..., 2]
@@ -67,7 +67,8 @@ def interpolate3d(st, v_full, jz, nodes):
          + jz[:, 9:10] * dy * dz)
     inside = st.side[nodes[..., 0], nodes[..., 1], nodes[..., 2]]
     rhs = v_full[nodes[..., 0], nodes[..., 1], nodes[..., 2]] + np.where(inside, 0.0, J)
-    return np.linalg.solve(A, rhs[..., None])[..., 0, 0]
+    coef = np.linalg.solve(A, rhs[..., None])[..., 0]
+    return coef if want_grad else coef[:, 0]
 
 
 class Oracle3D:
@@ -79,23 +80,27 @@ class Oracle3D:
         self.nb = grid3d.lsq_neighbours(self.st)
         self.lsq_idx, self.lsq_pinv = grid3d.lsq_operator(self.st, self.nb)
         self.nodes = grid3d.stencil(self.st)
+        self.neumann = getattr(prob, "bc", 0) == 1   # reading R38 in 3D: K_N ψ = ∂_n V⁺, [v] = 0, [∂_n v] = ψ
+        if self.neumann and self.kappa <= 0.0:
+            raise ValueError("Neumann BVP needs κ > 0 (S:555)")
 
     def points(self):
         return self.st.q_pos
 
-    def jumps_from(self, phi=None, F=None):
+    def jumps_from(self, phi=None, F=None, psi=None):
+        """(Φ, Ψ, [F]) → jumps; Φ and Ψ tangential derivatives from the same LSQ fit (R12)."""
         st = self.st
         M = self.M
-        if phi is None:
-            phi = np.zeros(M)
-            d = np.zeros((M, 5))
-        else:
-            d = grid3d.lsq_fit(self.lsq_idx, self.lsq_pinv, phi)
+        zero5 = np.zeros((M, 5))
+        d = grid3d.lsq_fit(self.lsq_idx, self.lsq_pinv, phi) if phi is not None else zero5
+        dpsi = grid3d.lsq_fit(self.lsq_idx, self.lsq_pinv, psi) if psi is not None else zero5
+        phi = np.zeros(M) if phi is None else phi
+        psi = np.zeros(M) if psi is None else psi
         F = np.zeros(M) if F is None else F
-        return jumps3d(phi, d[:, 0:2], d[:, 2:5], np.zeros(M), np.zeros((M, 2)), F, self.kappa,
+        return jumps3d(phi, d[:, 0:2], d[:, 2:5], psi, dpsi[:, 0:2], F, self.kappa,
                        st.nrm, st.e1, st.e2, st.kab)
 
-    def interface_solve(self, base, jq):
+    def interface_solve(self, base, jq, want_grad=False):
         """Correction → fast solve → interpolation; control points = intersections, so the same
         jumps serve both (R12, R15)."""
         st = self.st
@@ -103,12 +108,21 @@ class Oracle3D:
         f = correct3d(st, base, jq)
         v = np.zeros((n + 1,) * 3)
         v[1:n, 1:n, 1:n] = fastsolve.solve3d(f, st.h, self.kappa)
-        return v, interpolate3d(st, v, jq, self.nodes)
+        return v, interpolate3d(st, v, jq, self.nodes, want_grad)
 
     def apply_KD(self, phi):
         n = self.st.n
         _, out = self.interface_solve(np.zeros((n - 1,) * 3), self.jumps_from(phi=phi))
         return out
+
+    def apply_KN(self, psi):
+        """K_N ψ = ∂_n V⁺ of the interface problem [v] = 0, [∂_n v] = ψ (R38)."""
+        n = self.st.n
+        _, coef = self.interface_solve(np.zeros((n - 1,) * 3), self.jumps_from(psi=psi), want_grad=True)
+        return np.sum(coef[:, 1:4] * self.st.nrm, -1)
+
+    def apply_K(self, x):
+        return self.apply_KN(x) if self.neumann else self.apply_KD(x)
 
     def base_rhs(self, f_grid):
         n = self.st.n
@@ -121,14 +135,15 @@ class Oracle3D:
             X, Y, Z = np.meshgrid(x[1:n], x[1:n], x[1:n], indexing="ij")
             fg = f(X, Y, Z)
             fq = f(*self.st.q_pos.T)
-            _, yf = self.interface_solve(self.base_rhs(fg), self.jumps_from(F=fq))
-            ghat = g - yf
+            _, yf = self.interface_solve(self.base_rhs(fg), self.jumps_from(F=fq), want_grad=self.neumann)
+            ghat = g - (np.sum(yf[:, 1:4] * self.st.nrm, -1) if self.neumann else yf)
         else:
             fg = fq = None
             ghat = g.copy()
-        phi, stats = gmres(self.apply_KD, ghat, tol=tol, restart=restart, max_restarts=max_restarts)
+        phi, stats = gmres(self.apply_K, ghat, tol=tol, restart=restart, max_restarts=max_restarts)
         base = self.base_rhs(fg) if fg is not None else np.zeros((n - 1,) * 3)
-        v, _ = self.interface_solve(base, self.jumps_from(phi=phi, F=fq))
+        jumps = self.jumps_from(psi=phi, F=fq) if self.neumann else self.jumps_from(phi=phi, F=fq)
+        v, _ = self.interface_solve(base, jumps)
         return v, phi, stats
 
     def errors(self, u, uex):

@@ -1208,15 +1208,17 @@ struct Jump10 {
 
 // Monge-patch closed form (reading R13): [∇v] = Σ_a ∂_aΦ e_a + Ψ n,
 // A_ab = ∂_abΦ − κ_ab Ψ, A_an = ∂_aΨ + Σ_b κ_ab ∂_bΦ, A_nn = [F] + κΦ − A_11 − A_22, [D²v] = F A Fᵀ.
-__device__ __forceinline__ Jump10 jumps3d(double Phi, const double* dP, double F, double kappa, const double* n,
-                                          const double* e1, const double* e2, const double* kab) {
+__device__ __forceinline__ Jump10 jumps3d(double Phi, const double* dP, double Psi, const double* dPsi, double F,
+                                          double kappa, const double* n, const double* e1, const double* e2,
+                                          const double* kab) {
+  // [∇v] = ∂_aΦ e_a + Ψ n; A_ab = ∂_abΦ − κ_ab Ψ; A_an = ∂_aΨ + κ_ab ∂_bΦ
   Jump10 J;
   J.v = Phi;
 #pragma unroll
-  for (int r = 0; r < 3; ++r) J.g[r] = dP[0] * e1[r] + dP[1] * e2[r];
-  const double A11 = dP[2], A12 = dP[3], A22 = dP[4];
-  const double A1n = kab[0] * dP[0] + kab[1] * dP[1];
-  const double A2n = kab[1] * dP[0] + kab[2] * dP[1];
+  for (int r = 0; r < 3; ++r) J.g[r] = dP[0] * e1[r] + dP[1] * e2[r] + Psi * n[r];
+  const double A11 = dP[2] - kab[0] * Psi, A12 = dP[3] - kab[1] * Psi, A22 = dP[4] - kab[2] * Psi;
+  const double A1n = dPsi[0] + kab[0] * dP[0] + kab[1] * dP[1];
+  const double A2n = dPsi[1] + kab[1] * dP[0] + kab[2] * dP[1];
   const double Ann = F + kappa * Phi - A11 - A22;
   auto h = [&](int r, int c) {
     return A11 * e1[r] * e1[c] + A12 * (e1[r] * e2[c] + e2[r] * e1[c]) + A22 * e2[r] * e2[c] +
@@ -1241,14 +1243,19 @@ __device__ __forceinline__ void load_jump3(const DevTables3& T, int q, const dou
     for (int r = 0; r < 6; ++r) J.H[r] = jg[10 * q + 4 + r];
     return;
   }
-  double dP[5] = {0, 0, 0, 0, 0};
-  double Phi = 0.0;
-  if (phi) {
+  double dP[5] = {0, 0, 0, 0, 0}, dPs[2] = {0, 0};
+  double Phi = 0.0, Psi = 0.0;
+  if (phi && T.neumann) {   // density ψ = [∂_n v], [v] = 0 (R38)
+    Psi = phi[q];
+    dPs[0] = dphi[5 * q];
+    dPs[1] = dphi[5 * q + 1];
+  } else if (phi) {
     Phi = phi[q];
 #pragma unroll
     for (int r = 0; r < 5; ++r) dP[r] = dphi[5 * q + r];
   }
-  J = jumps3d(Phi, dP, fq ? fq[q] : 0.0, T.kappa, T.q_n + 3 * q, T.q_e1 + 3 * q, T.q_e2 + 3 * q, T.q_kab + 3 * q);
+  J = jumps3d(Phi, dP, Psi, dPs, fq ? fq[q] : 0.0, T.kappa, T.q_n + 3 * q, T.q_e1 + 3 * q, T.q_e2 + 3 * q,
+              T.q_kab + 3 * q);
 }
 
 // A1 (3D): tangent-plane LSQ fit (reading R12) with the precomputed scaled normal-matrix inverse.
@@ -2031,7 +2038,7 @@ __global__ void k_interp3(DevTables3 T, const double* __restrict__ phi, const do
       v += J.v + J.g[0] * dx + J.g[1] * dy + J.g[2] * dz + 0.5 * (J.H[0] * dx * dx + J.H[1] * dy * dy + J.H[2] * dz * dz) +
            J.H[3] * dx * dy + J.H[4] * dx * dz + J.H[5] * dy * dz;
     }
-    acc = fma(T.st_w[10 * (size_t)e + p], v, acc);
+    acc = fma((T.neumann ? T.st_wn : T.st_w)[10 * (size_t)e + p], v, acc);   // V⁺ or ∂_n V⁺ (R38)
   }
   out[e] = acc;
 }

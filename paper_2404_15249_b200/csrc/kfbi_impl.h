@@ -141,6 +141,8 @@ struct Setup3 {
   std::vector<double> lsq_G;              // 15 per point: (ÂᵀÂ)⁻¹ upper triangle, Â scaled by 1/h
   std::vector<int32_t> st_c, st_code;     // stencil centre (3) and sign/exterior code
   std::vector<double> st_w;               // 10 per point: row 0 of the inverse local system
+  std::vector<double> st_wn;              // 10 per point: normal-derivative row (Neumann, R38)
+  bool neumann = false;
   std::vector<int64_t> st_nodes_ij;       // dump
   std::vector<double> sin_tab, dk, zr, red_a, red_b;   // modes m = ll·N + kk
   std::vector<double> tw;            // 2N complex: (cos, sin)(π m / N), m = 0..2N−1
@@ -163,7 +165,8 @@ struct DevTables3 {
   const int32_t *lsq_ptr, *lsq_nb;
   const double* lsq_G;
   const int32_t *st_c, *st_code;
-  const double* st_w;
+  const double *st_w, *st_wn;
+  int neumann;
   const double *sin_tab, *dk, *zr, *red_a, *red_b;
   const double* tw;   // 2N × (cos, sin)
   const int32_t *irr_row_ptr, *zrow_id, *zrow_ptr, *znode_b;

@@ -81,7 +81,9 @@ void build_setup3(Setup3& S, const kfbi_grid* g, const kfbi_boundary* b, const k
   const int N = g->n[0];
   if (g->n[1] != N || g->n[2] != N || N < 32 || N > 512 || (N & (N - 1)))
     throw ArgError("3D: n must be equal powers of two in [32, 512]");
-  if (pde->bc != KFBI_DIRICHLET) throw UnsupportedError("3D: only the Dirichlet BVP is built");
+  if (pde->bc != KFBI_DIRICHLET && pde->bc != KFBI_NEUMANN) throw ArgError("bc must be DIRICHLET or NEUMANN");
+  if (pde->bc == KFBI_NEUMANN && !(pde->kappa > 0)) throw UnsupportedError("Neumann needs kappa > 0 (S:555)");
+  S.neumann = pde->bc == KFBI_NEUMANN;
   const double h = (g->hi[0] - g->lo[0]) / N;
   for (int a = 1; a < 3; ++a)
     if (std::fabs((g->hi[a] - g->lo[a]) / N - h) > 1e-12 * h || std::fabs(g->lo[a] - g->lo[0]) > 1e-12 * h)
@@ -286,6 +288,7 @@ void build_setup3(Setup3& S, const kfbi_grid* g, const kfbi_boundary* b, const k
   S.st_c.assign(3 * (size_t)nq, 0);
   S.st_code.assign(nq, 0);
   S.st_w.assign(10 * (size_t)nq, 0.0);
+  S.st_wn.assign(10 * (size_t)nq, 0.0);
   S.st_nodes_ij.assign(30 * (size_t)nq, 0);
 #pragma omp parallel for schedule(static)
   for (int e = 0; e < nq; ++e) {
@@ -311,8 +314,14 @@ void build_setup3(Setup3& S, const kfbi_grid* g, const kfbi_boundary* b, const k
       for (int q = 0; q < 10; ++q) A[q * 10 + p] = row[q];   // transpose: Aᵀ w = e_0
       w[p] = p == 0 ? 1.0 : 0.0;
     }
+    double A2[100], wn[10] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
+    std::copy(A, A + 100, A2);
     if (!lu_solve_n(10, A, w)) bad = true;
     for (int p = 0; p < 10; ++p) S.st_w[10 * (size_t)e + p] = w[p];
+    // normal derivative n·∇ of the local quadratic (Neumann, R38): Aᵀ w_n = (0, n, 0, …)
+    for (int a = 0; a < 3; ++a) wn[1 + a] = S.q_n[3 * (size_t)e + a];
+    if (!lu_solve_n(10, A2, wn)) bad = true;
+    for (int p = 0; p < 10; ++p) S.st_wn[10 * (size_t)e + p] = wn[p];
     for (int a = 0; a < 3; ++a) S.st_c[3 * e + a] = c[a];
     S.st_code[e] = ext | ((sg[0] > 0) << 10) | ((sg[1] > 0) << 11) | ((sg[2] > 0) << 12);
   }

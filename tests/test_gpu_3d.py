@@ -135,3 +135,29 @@ def test_partitioned_solve3d_matches_oracle():
     m = o.st.side
     assert s.converged and abs(s.iters - s_ref.iters) <= 1
     assert rel(u.cpu().numpy()[m], u_ref[m]) < 1e-8
+
+
+# ------------------------------------------------------------------ Neumann BVP (NEXT-1, R38)
+NEU3 = W.neumann(W.problem("ellipsoid-k1", 3, 64, [W.ellipsoid(0.7, 0.6, 0.5)], 1.0))
+
+
+@pytest.mark.parametrize("seed", [0, 1])
+def test_apply3d_neumann_matches_oracle(seed):
+    o, k = oracle(NEU3), gpu(NEU3)
+    psi = W.random_density(o.M, seed)
+    assert rel(k.apply(psi).cpu().numpy(), o.apply_KN(psi)) < 1e-10
+
+
+def test_solve3d_neumann_matches_oracle():
+    o, k = oracle(NEU3), gpu(NEU3)
+    f = lambda a, b, c: W.f_exact(NEU3.kappa, a, b, c)
+    p = o.points()
+    u_ref, psi_ref, s_ref = o.solve(np.sum(np.stack(W.grad_u_exact(*p.T), -1) * o.st.nrm, -1), f)
+    X, Y, Z = _grid(NEU3)
+    pk, nk = k.points("ctrl"), k.points("normal")
+    gN = np.sum(np.stack(W.grad_u_exact(*pk.T), -1) * nk, -1)
+    u, psi, s = k.solve(gN, f(X, Y, Z), f(*pk.T), f(*pk.T))
+    m = o.st.side
+    assert s.converged and abs(s.iters - s_ref.iters) <= 1
+    assert rel(u.cpu().numpy()[m], u_ref[m]) < 1e-8
+    assert rel(psi.cpu().numpy(), psi_ref) < 1e-8

@@ -70,3 +70,37 @@ def test_neumann_solve_converges():
 def test_neumann_needs_positive_kappa():
     with pytest.raises(ValueError):
         Oracle2D(W.neumann(W.C1(64)))
+
+
+def test_neumann_3d_gradient_exact_and_convergence():
+    """3D (R12, R38): the 10-point fit's gradient is exact for a piecewise quadratic with exact jumps,
+    and the Neumann BVP on an ellipsoid converges under refinement."""
+    from oracle.bie3d import Oracle3D
+    prob = W.neumann(W.problem("ellipsoid-k1", 3, 32, [W.ellipsoid(0.7, 0.6, 0.5)], 1.0))
+    o = Oracle3D(prob)
+    rng = np.random.default_rng(4)
+    a = rng.uniform(-1, 1, 10)
+    H = np.array([[2 * a[4], a[7], a[8]], [a[7], 2 * a[5], a[9]], [a[8], a[9], 2 * a[6]]])
+    q = lambda x, y, z: (a[0] + a[1] * x + a[2] * y + a[3] * z + a[4] * x * x + a[5] * y * y + a[6] * z * z
+                         + a[7] * x * y + a[8] * x * z + a[9] * y * z)
+    gq = lambda x, y, z: np.stack([a[1] + 2 * a[4] * x + a[7] * y + a[8] * z, a[2] + 2 * a[5] * y + a[7] * x + a[9] * z,
+                                   a[3] + 2 * a[6] * z + a[8] * x + a[9] * y], -1)
+    p = o.points()
+    jq = np.concatenate([q(*p.T)[:, None], gq(*p.T),
+                         np.tile([H[0, 0], H[1, 1], H[2, 2], H[0, 1], H[0, 2], H[1, 2]], (o.M, 1))], -1)
+    n = prob.n
+    X, Y, Z = np.meshgrid(o.st.x, o.st.x, o.st.x, indexing="ij")
+    base = np.where(o.st.side, np.trace(H) - prob.kappa * q(X, Y, Z), 0.0)[1:n, 1:n, 1:n]
+    _, coef = o.interface_solve(base, jq, want_grad=True)
+    np.testing.assert_allclose(coef[:, 1:4], gq(*p.T), atol=1e-9)
+    errs = []
+    for n in (32, 64):
+        prob = W.neumann(W.problem("ellipsoid-k1", 3, n, [W.ellipsoid(0.7, 0.6, 0.5)], 1.0))
+        o = Oracle3D(prob)
+        p = o.points()
+        gN = np.sum(np.stack(W.grad_u_exact(*p.T), -1) * o.st.nrm, -1)
+        u, psi, st = o.solve(gN, lambda x, y, z: W.f_exact(1.0, x, y, z))
+        assert st.converged
+        X, Y, Z = np.meshgrid(o.st.x, o.st.x, o.st.x, indexing="ij")
+        errs.append(o.errors(u, W.u_exact(X, Y, Z))[0])
+    assert errs[1] < errs[0] / 2.5, errs

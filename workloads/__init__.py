@@ -138,11 +138,16 @@ def lap_u_exact(x, y, z=None):
     return -3.0 * np.sin(x) * np.sin(y) * np.sin(z)
 
 
-def grad_u_exact(x, y):
-    """∇u* (2D), for the Neumann data g_N = n·∇u* (P:787)."""
-    ux = np.exp(x) * np.cos(y) + np.exp(y) * np.cos(x) + np.cos(x) * np.sin(y)
-    uy = -np.exp(x) * np.sin(y) + np.exp(y) * np.sin(x) + np.sin(x) * np.cos(y)
-    return ux, uy
+def grad_u_exact(x, y, z=None):
+    """∇u*, for the Neumann data g_N = n·∇u* (P:787)."""
+    if z is None:
+        ux = np.exp(x) * np.cos(y) + np.exp(y) * np.cos(x) + np.cos(x) * np.sin(y)
+        uy = -np.exp(x) * np.sin(y) + np.exp(y) * np.sin(x) + np.sin(x) * np.cos(y)
+        return ux, uy
+    ux = np.exp(x) * np.cos(y) + np.exp(z) * np.cos(x) + np.cos(x) * np.sin(y) * np.sin(z)
+    uy = -np.exp(x) * np.sin(y) + np.sin(x) * np.cos(y) * np.sin(z)
+    uz = np.exp(z) * np.sin(x) + np.sin(x) * np.sin(y) * np.cos(z)
+    return ux, uy, uz
 
 
 def f_exact(kappa, x, y, z=None):

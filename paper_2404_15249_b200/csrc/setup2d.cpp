@@ -12,6 +12,21 @@
 
 #include "kfbi_impl.h"
 
+#include <chrono>
+#include <cstdio>
+#include <cstdlib>
+namespace {
+// KFBI_SETUP_TIMING=1 prints the wall time of each setup phase (host profiling aid)
+void setup_tick(const char* next) {
+  static bool on = std::getenv("KFBI_SETUP_TIMING") != nullptr;
+  static auto last = std::chrono::steady_clock::now();
+  if (!on) return;
+  const auto now = std::chrono::steady_clock::now();
+  std::fprintf(stderr, "[setup] %.3f s → %s\n", std::chrono::duration<double>(now - last).count(), next);
+  last = now;
+}
+}  // namespace
+
 namespace kfbi {
 namespace {
 
@@ -167,6 +182,7 @@ bool lu_solve(int n, double* A, double* b) {
 }  // namespace
 
 void build_setup(Setup& S, const kfbi_grid* g, const kfbi_boundary* b, const kfbi_pde* pde) {
+  setup_tick("start");
   if (!g || !b || !pde || !b->comp || b->ncomp < 1) throw ArgError("null descriptor");
   if (g->dim != 2) throw ArgError("only dim = 2 is built in this library version");
   if (pde->kappa < 0) throw ArgError("kappa must be >= 0 (P:458)");
@@ -207,6 +223,7 @@ void build_setup(Setup& S, const kfbi_grid* g, const kfbi_boundary* b, const kfb
   const int W = N + 1;
   auto X = [&](int i) { return lo + i * h; };  // O1: node coordinate lo + i h
 
+  setup_tick("classification (P:551): Ω side o");
   // ---- classification: Ω side of every node ----
   S.side.assign((size_t)W * W, 0);
 #pragma omp parallel for schedule(static)
@@ -218,6 +235,7 @@ void build_setup(Setup& S, const kfbi_grid* g, const kfbi_boundary* b, const kfb
     }
   auto side = [&](int i, int j) { return S.side[(size_t)i * W + j]; };
 
+  setup_tick("intersections on sign-change edg");
   // ---- intersections on sign-change edges ----
   struct Edge { int axis, i, j; };
   std::vector<Edge> edges;
@@ -306,6 +324,7 @@ void build_setup(Setup& S, const kfbi_grid* g, const kfbi_boundary* b, const kfb
   }
   if (!err.empty()) throw GeomError(err);
 
+  setup_tick("irregular nodes (P:551) and thei");
   // ---- irregular nodes and their incident intersections ----
   std::unordered_map<int64_t, int> qidx;
   qidx.reserve(nq * 2);
@@ -357,6 +376,7 @@ void build_setup(Setup& S, const kfbi_grid* g, const kfbi_boundary* b, const kfb
     // col_ptr[i] .. col_ptr[i+1] are the irregular nodes of column i (sorted order)
   }
 
+  setup_tick("control points at uniform Ω-orie");
   // ---- control points at uniform Ω-oriented arc length (R11) ----
   S.z_comp.resize(S.M); S.z_knot.resize(S.M); S.z_x.resize(S.M); S.z_y.resize(S.M);
   S.z_t1.resize(S.M); S.z_t2.resize(S.M); S.z_p1.resize(S.M); S.z_p2.resize(S.M);
@@ -375,6 +395,7 @@ void build_setup(Setup& S, const kfbi_grid* g, const kfbi_boundary* b, const kfb
     }
   }
 
+  setup_tick("six-point stencils + inverse row");
   // ---- six-point stencils + inverse rows (R14, R16) ----
   const int M = S.M;
   std::vector<int64_t> nodes((size_t)M * 6 * 2);
@@ -460,6 +481,7 @@ void build_setup(Setup& S, const kfbi_grid* g, const kfbi_boundary* b, const kfb
     }
   }
 
+  setup_tick("spline filters (reading R10; SUR");
   // ---- spline filters (reading R10) ----
   // M_m = (6/Δ²) Σ_r b_r φ_{m+r},  b_r = a_{r−1} − 2a_r + a_{r+1},  a = periodic inverse of
   // the circulant [1, 4, 1]:  a_q = (ρ^q + ρ^{M−q}) / (2√3 (1 − ρ^M)),  ρ = −(2 − √3).
@@ -485,6 +507,7 @@ void build_setup(Setup& S, const kfbi_grid* g, const kfbi_boundary* b, const kfb
     }
   }
 
+  setup_tick("fast-solver tables (Alg. 4; SURV");
   // ---- fast-solver tables (Alg. 4) ----
   const int P = S.P;
   S.sin_tab.resize(N / 2 + 1);
@@ -587,6 +610,7 @@ void build_setup(Setup& S, const kfbi_grid* g, const kfbi_boundary* b, const kfb
         if (S.comps[c].kind != KFBI_ELLIPSE) throw ArgError("hole completion (R27) needs ellipse holes");
         S.holes.push_back(c);
       }
+  setup_tick("end");
 }
 
 }  // namespace kfbi

@@ -200,7 +200,8 @@ kfbi_status kfbi_destroy(kfbi_ctx* ctx);
 
 /* Device time of each kernel of one kfbi_apply, averaged over `reps` applies, from CUDA
  * events recorded on `stream` between the launches (bench/roofline use; synchronous).
- * ms_out[8] = {spline, correct, sweep, reduced, inverse, hole, interp, whole apply}; in 3D:
+ * ms_out[8] = {spline (+ hole coefficients), correct, sweep, reduced, inverse, 0, interp, whole
+ * apply}; in 3D:
  * {LSQ fit, correction, sparse forward DST (k_fwd3s), tridiagonal sweep + reduced system, inverse
  * y-DST (k_inv3y), z-evaluation at the stencil nodes, interp, apply}. */
 kfbi_status kfbi_profile_apply(kfbi_ctx* ctx, const double* d_phi, double* d_out, int32_t reps,

@@ -335,10 +335,9 @@ void dst_forward2(kfbi_ctx* c, const double* fgrid, bool mask, const BumpParams&
 
 void apply_KD2(kfbi_ctx* c, const double* phi, double* out, cudaStream_t s) {
   const DevTables& T = c->T;
-  launch_spline(T, phi, c->mk, s);
+  launch_spline(T, phi, c->mk, s, c->hole_off, c->hole_M, c->hole_delta, c->nh, c->ahole);   // + a_h (R27)
   launch_correct(T, phi, c->mk, nullptr, nullptr, c->cval, s);
   spectral2(c, c->cval, false, s);
-  launch_hole_coeffs(T, c->hole_off, c->hole_M, c->hole_delta, c->nh, phi, c->ahole, s);
   interp2(c, phi, nullptr, nullptr, true, out, s);
 }
 
@@ -957,7 +956,7 @@ kfbi_status kfbi_profile_apply(kfbi_ctx* c, const double* d_phi, double* d_out, 
   }
   for (int r = 0; r < reps; ++r) {
     ck(cudaEventRecord(ev[0], s), "rec");
-    launch_spline(T, d_phi, c->mk, s);
+    launch_spline(T, d_phi, c->mk, s, c->hole_off, c->hole_M, c->hole_delta, c->nh, c->ahole);
     ck(cudaEventRecord(ev[1], s), "rec");
     launch_correct(T, d_phi, c->mk, nullptr, nullptr, c->cval, s);
     ck(cudaEventRecord(ev[2], s), "rec");
@@ -967,8 +966,7 @@ kfbi_status kfbi_profile_apply(kfbi_ctx* c, const double* d_phi, double* d_out, 
     ck(cudaEventRecord(ev[4], s), "rec");
     launch_inverse_sparse(T, c->spec, c->hsep, c->vsten, s);
     ck(cudaEventRecord(ev[5], s), "rec");
-    launch_hole_coeffs(T, c->hole_off, c->hole_M, c->hole_delta, c->nh, d_phi, c->ahole, s);
-    ck(cudaEventRecord(ev[6], s), "rec");
+    ck(cudaEventRecord(ev[6], s), "rec");   // hole coefficients are fused into the spline launch
     launch_interp(T, d_phi, c->mk, nullptr, nullptr, c->vsten, c->nh, c->nh ? c->wg : nullptr, c->ahole, d_out, s);
     ck(cudaEventRecord(ev[7], s), "rec");
     ck(cudaEventSynchronize(ev[7]), "sync");

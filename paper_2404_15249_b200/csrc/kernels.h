@@ -7,7 +7,10 @@
 namespace kfbi {
 
 // A1: periodic cubic-spline second-derivative knots of φ (M threads).
-void launch_spline(const DevTables& T, const double* phi, double* mk, cudaStream_t s);
+// spline knots of φ; with nh > 0 also the hole-completion coefficients a_h (R27) in extra blocks
+void launch_spline(const DevTables& T, const double* phi, double* mk, cudaStream_t s, const int* hole_off = nullptr,
+                   const int* hole_M = nullptr, const double* hole_delta = nullptr, int nh = 0,
+                   double* ahole = nullptr);
 // A2+A3: jumps at intersections + correction at irregular nodes (one thread per node).
 //   phi/mk may be NULL (Φ ≡ 0); fq = [F] at intersections or NULL; jq_given (nq×6) replaces
 //   the jump computation (test path).  Output cval[n] = h² × (correction of f̃ at node n).

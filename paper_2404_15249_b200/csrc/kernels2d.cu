@@ -105,18 +105,31 @@ __device__ __forceinline__ void block_reduce(double (&v)[NV], double* scratch) {
 }
 
 // ------------------------------------------------------------------------------ A1
-__global__ void k_spline(DevTables T, const double* __restrict__ phi, double* __restrict__ mk) {
+// blocks [0, nsb): one thread per control point; blocks nsb + h: the hole-completion coefficient
+// a_h = Δs_h Σ_{Γ_h} φ (reading R27) by a deterministic block reduction (saves a launch per apply)
+__global__ void k_spline(DevTables T, const double* __restrict__ phi, double* __restrict__ mk, int nsb,
+                         const int* __restrict__ hoff, const int* __restrict__ hcnt,
+                         const double* __restrict__ hdelta, double* __restrict__ ahole) {
+  if ((int)blockIdx.x >= nsb) {
+    __shared__ double scratch[32];
+    const int hh = blockIdx.x - nsb;
+    double v[1] = {0.0};
+    for (int m = threadIdx.x; m < hcnt[hh]; m += blockDim.x) v[0] += phi[hoff[hh] + m];
+    block_reduce<1>(v, scratch);
+    if (threadIdx.x == 0) ahole[hh] = hdelta[hh] * v[0];
+    return;
+  }
   int m = blockIdx.x * blockDim.x + threadIdx.x;
   if (m >= T.M) return;
   int c = T.z_comp[m], ml = T.z_knot[m];
   int off = T.c_off[c], Mc = T.c_M[c], nt = T.sp_ntaps[c], first = T.sp_first[c];
   const double* b = T.sp_coef + T.sp_coef_off[c];
   double acc = 0.0;
+  int idx = (ml + first) % Mc;   // one modulo, then wrap by compare (periodic knots)
+  if (idx < 0) idx += Mc;
   for (int r = 0; r < nt; ++r) {
-    int idx = ml + first + r;
-    idx %= Mc;
-    if (idx < 0) idx += Mc;
     acc = fma(b[r], phi[off + idx], acc);
+    if (++idx == Mc) idx = 0;
   }
   mk[m] = acc;
 }
@@ -1026,8 +1039,10 @@ inline int cdiv(long a, long b) { return (int)((a + b - 1) / b); }
 
 // ============================================================================== launchers
 long long g_launches = 0;
-void launch_spline(const DevTables& T, const double* phi, double* mk, cudaStream_t s) {
-  { ++g_launches; k_spline<<<cdiv(T.M, 256), 256, 0, s>>>(T, phi, mk); }
+void launch_spline(const DevTables& T, const double* phi, double* mk, cudaStream_t s, const int* hole_off,
+                   const int* hole_M, const double* hole_delta, int nh, double* ahole) {
+  const int nsb = cdiv(T.M, 256);
+  { ++g_launches; k_spline<<<nsb + nh, 256, 0, s>>>(T, phi, mk, nsb, hole_off, hole_M, hole_delta, ahole); }
 }
 
 void launch_correct(const DevTables& T, const double* phi, const double* mk, const double* fq,

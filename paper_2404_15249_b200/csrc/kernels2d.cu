@@ -1892,7 +1892,15 @@ __global__ void __launch_bounds__(256) k_zeval3(DevTables3 T, const double* __re
     if (wn < T.w_hi) load(wn, nxt);
     const size_t rbase = (size_t)T.zrow_id[w] * N;
     const int e1 = T.zrow_ptr[w + 1];
-    for (int e = T.zrow_ptr[w]; e < e1; ++e) {
+    for (int e0 = T.zrow_ptr[w]; e0 < e1; e0 += 8) {   // 8 nodes per transpose-reduction
+    double vv[8];
+#pragma unroll
+    for (int nd = 0; nd < 8; ++nd) {
+      const int e = e0 + nd;
+      if (e >= e1) {
+        vv[nd] = 0.0;
+        continue;
+      }
       const int b = T.znode_b[e];
       const double2 w1 = __ldg(tw + b);                                   // e^{iθ}
       const double2 wz = __ldg(tw + ((32 * U * b) & (2 * N - 1)));        // e^{i·32Uθ}
@@ -1916,10 +1924,11 @@ __global__ void __launch_bounds__(256) k_zeval3(DevTables3 T, const double* __re
         tr += w1.x * sr[1] - w1.y * si[1];
         ti += w1.x * si[1] + w1.y * sr[1];
       }
-      double v = wl.y * tr + wl.x * ti;
-#pragma unroll
-      for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-      if (lane == 0) work[rbase + b] = scale * v;
+      vv[nd] = wl.y * tr + wl.x * ti;
+    }
+    const double tot = warp_transpose_reduce8(vv);   // lane l: node 4·(l>>4&1) + 2·(l>>3&1) + (l>>2&1)
+    const int nd = ((lane >> 4) & 1) * 4 + ((lane >> 3) & 1) * 2 + ((lane >> 2) & 1);
+    if ((lane & 3) == 0 && e0 + nd < e1) work[rbase + T.znode_b[e0 + nd]] = scale * tot;
     }
 #pragma unroll
     for (int s = 0; s < S; ++s)

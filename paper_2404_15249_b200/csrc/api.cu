@@ -435,7 +435,10 @@ void apply_Y3(kfbi_ctx* c, const double* fgrid, const double* fq, const double* 
   launch_base3(c->T3, fgrid, c->work, s);
   launch_correct3(c->T3, nullptr, nullptr, fq, nullptr, c->work, s);
   forward3(c, s);
-  inverse3(c, nullptr, s);
+  // only the stencil nodes are read: the K_D path's sparse inverse (y-rows, z at the nodes)
+  const double sc = 2.0 / c->T3.N;
+  launch_sparse3(c->T3, 1, c->work, c->hsep, sc, c->work2, s);
+  launch_sparse3(c->T3, 2, c->work2, nullptr, sc, c->work, s);
   launch_interp3(c->T3, nullptr, nullptr, fz, nullptr, c->work, out, s);
 }
 void final_field3(kfbi_ctx* c, const double* phi, const double* fgrid, const double* fq, double* u, cudaStream_t s) {

@@ -367,8 +367,11 @@ void final_field2(kfbi_ctx* c, const double* phi, const double* fgrid, const dou
 }
 
 // --- 3D interface solves (control points = intersection nodes, R12) -------------------
-void forward3(kfbi_ctx* c, cudaStream_t s) {   // rows: DST along z, transpose, DST along y
-  launch_dst_rows3(c->T3, 0, c->work, nullptr, 1.0, nullptr, s);
+// rows: DST along z (source h²·f·1_Ω + compact corrections built on load), transpose, DST along y
+// (from_work: the source is already in the working array, e.g. the test entry points)
+void forward3(kfbi_ctx* c, const double* fgrid, cudaStream_t s, bool from_work = false) {
+  if (from_work) launch_dst_rows3(c->T3, 0, c->work, nullptr, 1.0, nullptr, s);
+  else launch_dst_rows3(c->T3, 3, c->work, nullptr, 1.0, nullptr, s, fgrid, c->corr);
   launch_transpose3(c->T3, c->work, s);
   launch_dst_rows3(c->T3, 0, c->work, nullptr, 1.0, nullptr, s);
   launch_sweep3(c->T3, c->work, c->zfirst, c->fsep, s);
@@ -432,9 +435,8 @@ void apply_KD3(kfbi_ctx* c, const double* phi, double* out, cudaStream_t s) {
   launch_sum_parts(M, c->world, c->parts, out, s);
 }
 void apply_Y3(kfbi_ctx* c, const double* fgrid, const double* fq, const double* fz, double* out, cudaStream_t s) {
-  launch_base3(c->T3, fgrid, c->work, s);
-  launch_correct3(c->T3, nullptr, nullptr, fq, nullptr, c->work, s);
-  forward3(c, s);
+  launch_correct3(c->T3, nullptr, nullptr, fq, nullptr, nullptr, s, c->corr);
+  forward3(c, fgrid, s);
   // only the stencil nodes are read: the K_D path's sparse inverse (y-rows, z at the nodes)
   const double sc = 2.0 / c->T3.N;
   launch_sparse3(c->T3, 1, c->work, c->hsep, sc, c->work2, s);
@@ -443,9 +445,8 @@ void apply_Y3(kfbi_ctx* c, const double* fgrid, const double* fq, const double* 
 }
 void final_field3(kfbi_ctx* c, const double* phi, const double* fgrid, const double* fq, double* u, cudaStream_t s) {
   launch_lsq3(c->T3, phi, c->dphi, s);
-  launch_base3(c->T3, fgrid, c->work, s);
-  launch_correct3(c->T3, phi, c->dphi, fq, nullptr, c->work, s);
-  forward3(c, s);
+  launch_correct3(c->T3, phi, c->dphi, fq, nullptr, nullptr, s, c->corr);
+  forward3(c, fgrid, s);
   inverse3(c, u, s);
 }
 
@@ -1009,7 +1010,7 @@ kfbi_status kfbi_test_fast_solve(kfbi_ctx* c, const double* d_rhs, double* d_v, 
   cudaStream_t s = pick(c, stream);
   if (c->dim == 3) {
     launch_base3(c->T3, d_rhs, c->work, s);   // note: masked by Ω (test inputs are Ω-supported or use 2D)
-    forward3(c, s);
+    forward3(c, nullptr, s, true);
     inverse3(c, d_v, s);
     ck(cudaGetLastError(), "fast solve 3D");
     return KFBI_OK;
@@ -1036,7 +1037,7 @@ kfbi_status kfbi_test_interface_solve(kfbi_ctx* c, const double* d_base, const d
   if (c->dim == 3) {
     launch_base3(c->T3, d_base, c->work, s);
     launch_correct3(c->T3, nullptr, nullptr, nullptr, d_jq, c->work, s);
-    forward3(c, s);
+    forward3(c, nullptr, s, true);
     if (d_v) {
       inverse3(c, d_v, s);
     } else {
@@ -1046,7 +1047,7 @@ kfbi_status kfbi_test_interface_solve(kfbi_ctx* c, const double* d_base, const d
       if (d_v) {   // the field went to d_v: recompute the working copy for the interpolation
         launch_base3(c->T3, d_base, c->work, s);
         launch_correct3(c->T3, nullptr, nullptr, nullptr, d_jq, c->work, s);
-        forward3(c, s);
+        forward3(c, nullptr, s, true);
         inverse3(c, nullptr, s);
       }
       launch_interp3(c->T3, nullptr, nullptr, nullptr, d_jz, c->work, d_vplus, s);

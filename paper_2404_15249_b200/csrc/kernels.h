@@ -87,8 +87,9 @@ void launch_sparse3(const DevTables3& T, int which, const double* src, const dou
 // batched in-place DST-I of the (N−1)·N rows of the working array: mode 0 plain (× scale);
 // mode 1 inverse with the arrowhead fix-up on load (rows = (i, ll), modes m = ll·N + kk);
 // mode 2 final store into a full (N+1)^3 grid (× scale)
+// mode 3: forward from h²·f·1_Ω (src = full (N+1)³ grid, or NULL) + the compact corrections `corr`
 void launch_dst_rows3(const DevTables3& T, int mode, double* work, const double* hsep, double scale, double* out,
-                      cudaStream_t s);
+                      cudaStream_t s, const double* src = nullptr, const double* corr = nullptr);
 void launch_transpose3(const DevTables3& T, double* work, cudaStream_t s);
 void launch_sweep3(const DevTables3& T, double* work, double* zB, double* zA, cudaStream_t s);
 void launch_reduced3(const DevTables3& T, const double* zB, const double* zA, double* hsep, cudaStream_t s);

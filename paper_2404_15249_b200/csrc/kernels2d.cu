@@ -1698,9 +1698,13 @@ __device__ __forceinline__ void load_fixed_row(const DevTables3& T, const double
 
 // batched DST-I of the rows of length N (index 0 ≡ 0): one row per N/32 lanes, 8192/N rows per CTA.
 // MODE 0: in place (× scale); 1: in place from the fixed-up spectral rows; 2: into the (N+1)³ grid u.
+// MODE 3: the forward source is built on load — h²·f·1_Ω from the full grid `src` plus the row's
+// compact corrections (the dense base is never written).
 template <int MODE, int N>
 __global__ void __launch_bounds__(256, 2) k_dst_rows3t(DevTables3 T, double* work, const double* __restrict__ hsep,
-                                                       double scale, double* __restrict__ out) {
+                                                       double scale, double* __restrict__ out,
+                                                       const double* __restrict__ src,
+                                                       const double* __restrict__ corr) {
   constexpr int NTL = N / 32, RPC = 256 / NTL, ZS = N / 2 + N / 32 + 1;
   extern __shared__ double2 smz[];
   const int rl = threadIdx.x / NTL, tid = threadIdx.x % NTL;
@@ -1712,6 +1716,28 @@ __global__ void __launch_bounds__(256, 2) k_dst_rows3t(DevTables3 T, double* wor
   double* rp = work + row * N;
   if (MODE == 1 && live) {
     load_fixed_row<N>(T, work, hsep, i, (size_t)a * N, z, tid);
+  } else if (MODE == 3) {
+    const int W = N + 1;
+    const double h2 = T.h * T.h;
+    const size_t gbase = ((size_t)i * W + a) * W;
+#pragma unroll
+    for (int s = 0; s < 16; ++s) {
+      const int m = tid + s * NTL;
+      double v0 = 0.0, v1 = 0.0;
+      if (live && a > 0 && src) {
+        if (m > 0 && T.side[gbase + 2 * m]) v0 = h2 * src[gbase + 2 * m];
+        if (T.side[gbase + 2 * m + 1]) v1 = h2 * src[gbase + 2 * m + 1];
+      }
+      z[zpad(m)] = make_double2(v0, v1);
+    }
+    __syncwarp();
+    if (live && a > 0 && corr) {   // the row's irregular nodes (distinct z indices)
+      double* fz = reinterpret_cast<double*>(z);
+      for (int e = T.irr_row_ptr[row] + tid; e < T.irr_row_ptr[row + 1]; e += NTL) {
+        const int b = (int)(T.irr_lin[e] & (N - 1));
+        fz[2 * zpad(b >> 1) + (b & 1)] += corr[e];
+      }
+    }
   } else {
 #pragma unroll
     for (int s = 0; s < 16; ++s) {
@@ -2087,7 +2113,7 @@ void launch_correct3(const DevTables3& T, const double* phi, const double* dphi,
 }
 template <int N>
 static void dst_rows3_n(const DevTables3& T, int mode, double* work, const double* hsep, double scale, double* out,
-                        cudaStream_t s) {
+                        cudaStream_t s, const double* src, const double* corr) {
   constexpr int RPC = 256 / (N / 32);
   const size_t sm = (size_t)RPC * (N / 2 + N / 32 + 1) * sizeof(double2);
   const int grid = cdiv3((long)(N - 1) * N, RPC);
@@ -2096,21 +2122,23 @@ static void dst_rows3_n(const DevTables3& T, int mode, double* work, const doubl
     cudaFuncSetAttribute(k_dst_rows3t<0, N>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
     cudaFuncSetAttribute(k_dst_rows3t<1, N>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
     cudaFuncSetAttribute(k_dst_rows3t<2, N>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    cudaFuncSetAttribute(k_dst_rows3t<3, N>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
     attr = true;
   }
-  if (mode == 0) k_dst_rows3t<0, N><<<grid, 256, sm, s>>>(T, work, hsep, scale, out);
-  else if (mode == 1) k_dst_rows3t<1, N><<<grid, 256, sm, s>>>(T, work, hsep, scale, out);
-  else k_dst_rows3t<2, N><<<grid, 256, sm, s>>>(T, work, hsep, scale, out);
+  if (mode == 0) k_dst_rows3t<0, N><<<grid, 256, sm, s>>>(T, work, hsep, scale, out, src, corr);
+  else if (mode == 1) k_dst_rows3t<1, N><<<grid, 256, sm, s>>>(T, work, hsep, scale, out, src, corr);
+  else if (mode == 2) k_dst_rows3t<2, N><<<grid, 256, sm, s>>>(T, work, hsep, scale, out, src, corr);
+  else k_dst_rows3t<3, N><<<grid, 256, sm, s>>>(T, work, hsep, scale, out, src, corr);
 }
 void launch_dst_rows3(const DevTables3& T, int mode, double* work, const double* hsep, double scale, double* out,
-                      cudaStream_t s) {
+                      cudaStream_t s, const double* src, const double* corr) {
   ++g_launches;
   switch (T.N) {
-    case 32: dst_rows3_n<32>(T, mode, work, hsep, scale, out, s); break;
-    case 64: dst_rows3_n<64>(T, mode, work, hsep, scale, out, s); break;
-    case 128: dst_rows3_n<128>(T, mode, work, hsep, scale, out, s); break;
-    case 256: dst_rows3_n<256>(T, mode, work, hsep, scale, out, s); break;
-    default: dst_rows3_n<512>(T, mode, work, hsep, scale, out, s); break;
+    case 32: dst_rows3_n<32>(T, mode, work, hsep, scale, out, s, src, corr); break;
+    case 64: dst_rows3_n<64>(T, mode, work, hsep, scale, out, s, src, corr); break;
+    case 128: dst_rows3_n<128>(T, mode, work, hsep, scale, out, s, src, corr); break;
+    case 256: dst_rows3_n<256>(T, mode, work, hsep, scale, out, s, src, corr); break;
+    default: dst_rows3_n<512>(T, mode, work, hsep, scale, out, s, src, corr); break;
   }
 }
 template <int N>

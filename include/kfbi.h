@@ -198,6 +198,21 @@ kfbi_status kfbi_apply_model(const kfbi_ctx* ctx, double* bytes_sweep, double* b
 
 kfbi_status kfbi_destroy(kfbi_ctx* ctx);
 
+/* Gray–Scott reaction–diffusion (readings R40, R41): one
+ * Strang step R(Δt/2) ∘ D(Δt) ∘ R(Δt/2) of u_t = ε₁Δu + (1/ε₀)[γ(1−u) − uv²],
+ * v_t = ε₂Δv + (1/ε₀)[uv² − (γ+κ_r)v] with ∂_n u = ∂_n v = 0, in place on the full node grids
+ * d_u, d_v ((N+1)² doubles, device).  R: explicit midpoint rule at every node.  D: Crank–Nicolson
+ * per species as one Neumann solve (Δ − κ)y = −κw, ∂_n y = 0, w ← 2y − w, the boundary data of
+ * the source by bilinear interpolation of w at the intersection and control points.
+ *   ctx_u, ctx_v  2D Neumann contexts on the same geometry with κ = 2/(ε₁Δt) and 2/(ε₂Δt)
+ *   d_psi_u/v     densities (M doubles each): GMRES warm start when warm ≠ 0, updated in place
+ *   d_scratch     2(N+1)² + nq + 2M doubles of device scratch
+ *   params5       host {γ, κ_r, ε₀, ε₁, ε₂};  tol  GMRES tolerance;  iters2  host out, 2 ints
+ * Synchronous (two kfbi_solve calls). */
+kfbi_status kfbi_gray_scott_step(kfbi_ctx* ctx_u, kfbi_ctx* ctx_v, double* d_u, double* d_v, double* d_psi_u,
+                                 double* d_psi_v, int32_t warm, double* d_scratch, double dt,
+                                 const double* params5, double tol, int32_t* iters2, void* stream);
+
 /* Device time of each kernel of one kfbi_apply, averaged over `reps` applies, from CUDA
  * events recorded on `stream` between the launches (bench/roofline use; synchronous).
  * ms_out[8] = {spline (+ hole coefficients), correct, sweep, reduced, inverse, 0, interp, whole

@@ -180,14 +180,21 @@ class Oracle2D:
             return bicgstab(K, ghat, x0=phi0, tol=tol, max_iter=restart * max_restarts)
         return gmres(K, ghat, x0=phi0, tol=tol, restart=restart, max_restarts=max_restarts)
 
-    def solve(self, g, f=None, tol=1e-8, restart=30, max_restarts=50, phi0=None, method="gmres", gamma=1.0):
-        """Procedures 2-3: ĝ = g − (Yf)⁺, GMRES on K φ = ĝ, final field."""
+    def solve(self, g, f=None, tol=1e-8, restart=30, max_restarts=50, phi0=None, method="gmres", gamma=1.0,
+              fdata=None):
+        """Procedures 2-3: ĝ = g − (Yf)⁺, GMRES on K φ = ĝ, final field.
+        f: callable f(x, y), or fdata = (f at the interior nodes (N−1)², f at intersections, f at
+        control points) when f is only known as data (e.g. the Gray–Scott diffusion substeps)."""
         n = self.st.n
-        if f is not None:
-            px, py = self.isect_points()
-            zx, zy = self.ctrl_points()
-            fg = f(self.X[1:n, 1:n], self.Y[1:n, 1:n])
-            fq, fz = f(px, py), f(zx, zy)
+        if f is not None or fdata is not None:
+            if fdata is not None:
+                fg, fq, fz = fdata
+                f = True
+            else:
+                px, py = self.isect_points()
+                zx, zy = self.ctrl_points()
+                fg = f(self.X[1:n, 1:n], self.Y[1:n, 1:n])
+                fq, fz = f(px, py), f(zx, zy)
             ghat = g - self.apply_Y(fg, fq, fz) if not self.neumann else None
         else:
             fg = fq = fz = None

@@ -7,3 +7,4 @@
 """
 from .kfbi import (KFBI, KfbiError, Stats, load, launch_count, unique_id, broadcast_unique_id,  # noqa: F401
                    LIB_PATH, EXPORTS)
+from .grayscott import GrayScott  # noqa: F401,E402

@@ -109,6 +109,7 @@ void layout(kfbi_ctx* c, Arena& A) {
   T.q_axis = A.table(S.q_axis); T.q_comp = A.table(S.q_comp); T.q_knot = A.table(S.q_knot);
   T.q_t = A.table(S.q_t); T.q_t1 = A.table(S.q_t1); T.q_t2 = A.table(S.q_t2);
   T.q_p1 = A.table(S.q_p1); T.q_p2 = A.table(S.q_p2);
+  T.q_x = A.table(S.q_x); T.q_y = A.table(S.q_y); T.z_x = A.table(S.z_x); T.z_y = A.table(S.z_y);
   T.irr_j = A.table(S.irr_j); T.irr_ptr = A.table(S.irr_ptr); T.pair_q = A.table(S.pair_q);
   T.col_ptr = A.table(S.col_ptr); T.col_mid = A.table(S.col_mid); T.irr_side = A.table(S.irr_side); T.pair_d = A.table(S.pair_d);
   T.z_comp = A.table(S.z_comp); T.z_knot = A.table(S.z_knot);
@@ -986,6 +987,50 @@ kfbi_status kfbi_profile_apply(kfbi_ctx* c, const double* d_phi, double* d_out, 
   for (int q = 0; q < 8; ++q) ms[q] = acc[q] / reps;
   for (auto& e : ev) cudaEventDestroy(e);
   KFBI_CATCH(c)
+  return KFBI_OK;
+}
+
+kfbi_status kfbi_gray_scott_step(kfbi_ctx* cu, kfbi_ctx* cv, double* d_u, double* d_v, double* d_psi_u,
+                                 double* d_psi_v, int32_t warm, double* d_scratch, double dt, const double* params5,
+                                 double tol, int32_t* iters2, void* stream) {
+  if (!cu || !cv || !d_u || !d_v || !d_psi_u || !d_psi_v || !d_scratch || !params5 || !(dt > 0) || !(tol > 0))
+    return KFBI_EINVAL;
+  if (cu->dim != 2 || cv->dim != 2 || !cu->S.neumann || !cv->S.neumann || cu->S.N != cv->S.N ||
+      cu->S.M != cv->S.M || cu->S.nq != cv->S.nq)
+    return fail(cu, KFBI_EINVAL, "Gray-Scott needs two 2D Neumann contexts on the same geometry");
+  const double eps[2] = {params5[3], params5[4]};
+  kfbi_ctx* cs[2] = {cu, cv};
+  for (int q = 0; q < 2; ++q)
+    if (std::fabs(cs[q]->S.kappa - 2.0 / (eps[q] * dt)) > 1e-12 * cs[q]->S.kappa)
+      return fail(cu, KFBI_EINVAL, "context kappa must be 2/(eps dt) (Crank-Nicolson, reading R40)");
+  KFBI_TRY(cu)
+  need_ws(cu);
+  need_ws(cv);
+  cudaStream_t s = pick(cu, stream);
+  const long nn = (long)(cu->S.N + 1) * (cu->S.N + 1);
+  const int M = cu->S.M, nq = cu->S.nq;
+  double* fg = d_scratch;
+  double* fq = fg + nn;
+  double* fz = fq + nq;
+  double* y = fz + M;
+  double* g0 = y + nn;
+  const GsParams p{params5[0], params5[1], params5[2]};
+  launch_fill(g0, M, 0.0, s);   // homogeneous Neumann data
+  launch_gs_reaction(d_u, d_v, nn, 0.5 * dt, p, s);
+  double* w[2] = {d_u, d_v};
+  double* psi[2] = {d_psi_u, d_psi_v};
+  for (int q = 0; q < 2; ++q) {
+    launch_gs_rhs(cs[q]->T, w[q], fg, fq, fz, s);
+    kfbi_solve_opts o{tol, 30, 50, KFBI_GMRES, 1.0};
+    kfbi_solve_stats st{};
+    const kfbi_status r = kfbi_solve(cs[q], g0, fg, fq, fz, warm ? psi[q] : nullptr, y, psi[q], &o, &st, s);
+    if (r != KFBI_OK) return r;
+    if (iters2) iters2[q] = st.iters;
+    launch_gs_combine(w[q], y, nn, s);
+  }
+  launch_gs_reaction(d_u, d_v, nn, 0.5 * dt, p, s);
+  ck(cudaGetLastError(), "gray-scott step");
+  KFBI_CATCH(cu)
   return KFBI_OK;
 }
 

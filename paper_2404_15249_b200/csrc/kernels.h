@@ -18,6 +18,14 @@ void launch_correct(const DevTables& T, const double* phi, const double* mk, con
                     const double* jq_given, double* cval, cudaStream_t s);
 // A4 (dense input only): forward DST-I of rows i = 1..N−1 of a full-grid base
 //   f̃ = mask·f (+ Σ_h a_h b_h), written to spec[(i−1)·N + k].
+struct GsParams {   // Gray–Scott: feed γ, removal κ_r, ε₀
+  double gamma, kr, eps0;
+};
+void launch_gs_reaction(double* u, double* v, long n, double dt, const GsParams& p, cudaStream_t s);
+void launch_gs_rhs(const DevTables& T, const double* w, double* fg, double* fq, double* fz, cudaStream_t s);
+void launch_gs_combine(double* w, const double* y, long n, cudaStream_t s);
+void launch_fill(double* x, long n, double val, cudaStream_t s);
+
 struct BumpParams {
   int nh;
   double cx[4], cy[4], rad[4];

@@ -831,6 +831,51 @@ __global__ void k_hole_coeffs(const int* __restrict__ off, const int* __restrict
   if (threadIdx.x == 0) a[hh] = delta[hh] * v[0];
 }
 
+// ------------------------------------------------------------------------------ Gray–Scott (NEXT-2)
+// pointwise reaction by the explicit midpoint rule (reading R40), rates (1/ε₀)[γ(1−u) − uv², uv² − (γ+κ_r)v]
+__device__ __forceinline__ void gs_rates(double u, double v, const GsParams& p, double& du, double& dv) {
+  const double uv2 = u * v * v;
+  du = (p.gamma * (1.0 - u) - uv2) / p.eps0;
+  dv = (uv2 - (p.gamma + p.kr) * v) / p.eps0;
+}
+__global__ void k_gs_reaction(double* __restrict__ u, double* __restrict__ v, long n, double dt, GsParams p) {
+  for (long i = (long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long)gridDim.x * blockDim.x) {
+    const double u0 = u[i], v0 = v[i];
+    double du, dv;
+    gs_rates(u0, v0, p, du, dv);
+    const double um = u0 + 0.5 * dt * du, vm = v0 + 0.5 * dt * dv;
+    gs_rates(um, vm, p, du, dv);
+    u[i] = u0 + dt * du;
+    v[i] = v0 + dt * dv;
+  }
+}
+__device__ __forceinline__ double bilinear(const double* __restrict__ w, int N, double lo, double h, double px,
+                                           double py) {
+  const double sx = (px - lo) / h, sy = (py - lo) / h;
+  const int i = (int)floor(sx), j = (int)floor(sy);
+  const double tx = sx - i, ty = sy - j;
+  const size_t W = (size_t)N + 1, b = (size_t)i * W + j;
+  return (1 - tx) * (1 - ty) * w[b] + tx * (1 - ty) * w[b + W] + (1 - tx) * ty * w[b + 1] + tx * ty * w[b + W + 1];
+}
+// diffusion source f = −κ w at the full grid, the intersections and the control points (R41: bilinear)
+__global__ void k_gs_rhs(DevTables T, const double* __restrict__ w, double* __restrict__ fg,
+                         double* __restrict__ fq, double* __restrict__ fz) {
+  const long nn = (long)(T.N + 1) * (T.N + 1);
+  const double k = T.kappa;
+  for (long i = (long)blockIdx.x * blockDim.x + threadIdx.x; i < nn + T.nq + T.M; i += (long)gridDim.x * blockDim.x) {
+    if (i < nn) fg[i] = -k * w[i];
+    else if (i < nn + T.nq) fq[i - nn] = -k * bilinear(w, T.N, T.lo, T.h, T.q_x[i - nn], T.q_y[i - nn]);
+    else fz[i - nn - T.nq] = -k * bilinear(w, T.N, T.lo, T.h, T.z_x[i - nn - T.nq], T.z_y[i - nn - T.nq]);
+  }
+}
+__global__ void k_gs_combine(double* __restrict__ w, const double* __restrict__ y, long n) {
+  for (long i = (long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long)gridDim.x * blockDim.x)
+    w[i] = 2.0 * y[i] - w[i];   // Crank–Nicolson: (I − aΔ)^{-1}(I + aΔ) w = 2y − w
+}
+__global__ void k_fill(double* __restrict__ x, long n, double val) {
+  for (long i = (long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long)gridDim.x * blockDim.x) x[i] = val;
+}
+
 // ------------------------------------------------------------------------------ FFT building blocks
 // (register DFTs, padded shared-memory slots; the DST-I cores are with the 2D/3D row kernels below)
 
@@ -2241,6 +2286,25 @@ void launch_inverse_dense(const DevTables& T, const double* spec, const double* 
                           cudaStream_t s) {
   BumpParams bp{};
   dense_dispatch<1>(T, spec, 0, bp, hsep, vgrid, s);
+}
+
+void launch_gs_reaction(double* u, double* v, long n, double dt, const GsParams& p, cudaStream_t s) {
+  ++g_launches;
+  k_gs_reaction<<<(int)std::min<long>((n + 255) / 256, 8L * num_sms()), 256, 0, s>>>(u, v, n, dt, p);
+}
+void launch_gs_rhs(const DevTables& T, const double* w, double* fg, double* fq, double* fz, cudaStream_t s) {
+  const long n = (long)(T.N + 1) * (T.N + 1) + T.nq + T.M;
+  ++g_launches;
+  k_gs_rhs<<<(int)std::min<long>((n + 255) / 256, 8L * num_sms()), 256, 0, s>>>(T, w, fg, fq, fz);
+}
+void launch_gs_combine(double* w, const double* y, long n, cudaStream_t s) {
+  ++g_launches;
+  k_gs_combine<<<(int)std::min<long>((n + 255) / 256, 8L * num_sms()), 256, 0, s>>>(w, y, n);
+}
+void launch_fill(double* x, long n, double val, cudaStream_t s) {
+  if (n <= 0) return;
+  ++g_launches;
+  k_fill<<<(int)std::min<long>((n + 255) / 256, 8L * num_sms()), 256, 0, s>>>(x, n, val);
 }
 
 }  // namespace kfbi

@@ -186,6 +186,7 @@ struct DevTables {
   // intersections
   const int32_t *q_axis, *q_comp, *q_knot;
   const double *q_t, *q_t1, *q_t2, *q_p1, *q_p2;
+  const double *q_x, *q_y, *z_x, *z_y;   // point coordinates (bilinear sampling, NEXT-2)
   // irregular nodes
   const int32_t *irr_j, *irr_ptr, *pair_q, *col_ptr, *col_mid;
   const int8_t* irr_side;

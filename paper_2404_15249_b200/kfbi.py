@@ -22,7 +22,7 @@ EXPORTS = ["kfbi_version", "kfbi_last_error", "kfbi_last_setup_error", "kfbi_get
            "kfbi_workspace_size", "kfbi_set_workspace", "kfbi_sizes", "kfbi_points", "kfbi_node_mask",
            "kfbi_apply", "kfbi_solve", "kfbi_apply_model", "kfbi_destroy", "kfbi_test_fast_solve",
            "kfbi_test_interface_solve", "kfbi_test_setup_dump", "kfbi_profile_apply", "kfbi_launch_count",
-           "kfbi_slab"]
+           "kfbi_slab", "kfbi_gray_scott_step"]
 
 
 class KfbiError(RuntimeError):
@@ -98,6 +98,8 @@ def load(path: str = LIB_PATH):
     lib.kfbi_profile_apply.argtypes = [vp, vp, vp, i32, dp, vp]
     lib.kfbi_launch_count.argtypes = [i64p]
     lib.kfbi_slab.argtypes = [vp, i32, i64p]
+    lib.kfbi_gray_scott_step.argtypes = [vp, vp, vp, vp, vp, vp, i32, vp, C.c_double, dp, C.c_double,
+                                         C.POINTER(C.c_int32), vp]
     for name in EXPORTS:
         getattr(lib, name).restype = C.c_char_p if name in ("kfbi_version", "kfbi_last_error",
                                                             "kfbi_last_setup_error") else C.c_int32

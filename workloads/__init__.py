@@ -168,3 +168,20 @@ def smooth_density(comp_counts: Sequence[int]) -> np.ndarray:
         u = np.arange(mc) / mc
         out.append(np.cos(2 * np.pi * u) + 0.5 * np.sin(6 * np.pi * u))
     return np.concatenate(out)
+
+
+# --- Gray–Scott workload: parameters, initial data, problems ---
+GS_PARAMS = dict(gamma=0.024, kr=0.06, eps0=0.01, eps1=0.008, eps2=0.004)
+
+
+def gray_scott_initial(X, Y):
+    """v = ¼ sin²(4πx) sin²(4πy) on |x|, |y| ≤ 0.25 (0 elsewhere), u = 1 − 2v."""
+    sq = (np.abs(X) <= 0.25) & (np.abs(Y) <= 0.25)
+    v = np.where(sq, 0.25 * np.sin(4 * np.pi * X) ** 2 * np.sin(4 * np.pi * Y) ** 2, 0.0)
+    return 1.0 - 2.0 * v, v
+
+
+def gray_scott_problem(n, eps, dt):
+    """One species' diffusion substep: Neumann modified Helmholtz with κ = 2/(εΔt) on the disk r = 1.8
+    in B = (−2, 2)² (P:299, P:320)."""
+    return problem(f"gray-scott-{eps:g}", 2, n, [circle(1.8)], 2.0 / (eps * dt), lo=-2.0, hi=2.0, bc=NEUMANN)

@@ -67,6 +67,8 @@ struct kfbi_ctx {
   // GMRES
   double *V = nullptr, *gx = nullptr, *gr = nullptr, *ghat = nullptr, *tmp = nullptr;
   double *partial = nullptr, *hcol = nullptr, *ycoef = nullptr, *scal = nullptr;
+  double *spec_f = nullptr, *spec_bump = nullptr;   // cached spectra (final field by linearity)
+  bool spec_f_valid = false;
   double* hcol_host = nullptr;   // host-mapped (written by k_copy, read after a stream sync)
   double* hcol_map = nullptr;    // its device alias
   // host staging of small tables (kept alive for the async uploads)
@@ -150,6 +152,10 @@ void layout(kfbi_ctx* c, Arena& A) {
   c->wg = A.take<double>((size_t)std::max(c->nh, 1) * S.M);
   // scratch
   c->spec = A.take<double>((N - 1) * N);
+  // spectra reused by the final field (linearity): DST(f·1_Ω) from the solve's Y apply, DST(b_h) of the
+  // hole bumps from setup — the final field's dense forward becomes spec_f + Σ a_h spec_bump_h
+  c->spec_f = A.take<double>((N - 1) * N);
+  c->spec_bump = A.take<double>((size_t)std::max(c->nh, 1) * (N - 1) * N);
   c->zfirst = A.take<double>(P * N);
   c->zlast = A.take<double>(P * N);
   c->fsep = A.take<double>(std::max<size_t>(P - 1, 1) * N);
@@ -346,6 +352,8 @@ void apply_Y2(kfbi_ctx* c, const double* fgrid, const double* fq, const double* 
   const DevTables& T = c->T;
   BumpParams none{};
   dst_forward2(c, fgrid, true, none, s);
+  launch_copy((int)((long)(T.N - 1) * T.N), c->spec, c->spec_f, s);   // kept for the final field
+  c->spec_f_valid = true;
   launch_correct(T, nullptr, nullptr, fq, nullptr, c->cval, s);
   spectral2(c, c->cval, true, s);
   interp2(c, nullptr, fz, nullptr, false, out, s);
@@ -357,7 +365,13 @@ void final_field2(kfbi_ctx* c, const double* phi, const double* fgrid, const dou
   bp.a = c->ahole;
   launch_hole_coeffs(T, c->hole_off, c->hole_M, c->hole_delta, c->nh, phi, c->ahole, s);
   const bool dense = fgrid || c->nh;
-  if (dense) dst_forward2(c, fgrid, true, bp, s);
+  if (dense && (!fgrid || c->spec_f_valid)) {   // by linearity from the cached spectra
+    const long nspec = (long)(T.N - 1) * T.N;
+    launch_combine(nspec, fgrid ? c->spec_f : nullptr, c->nh, c->spec_bump, nspec, c->ahole, c->spec, s);
+  } else if (dense) {
+    dst_forward2(c, fgrid, true, bp, s);
+  }
+  c->spec_f_valid = false;
   launch_spline(T, phi, c->mk, s);
   launch_correct(T, phi, c->mk, fq, nullptr, c->cval, s);
   spectral2(c, c->cval, dense, s);
@@ -588,6 +602,8 @@ kfbi_status kfbi_set_workspace(kfbi_ctx* c, void* d_ws, size_t bytes) {
     BumpParams bp = c->bump;
     bp.a = c->onehot + (size_t)h * c->nh;
     dst_forward2(c, nullptr, false, bp, s);
+    const long nspec = (long)(c->S.N - 1) * c->S.N;
+    launch_copy((int)nspec, c->spec, c->spec_bump + (size_t)h * nspec, s);
     spectral2(c, nullptr, true, s);
     interp2(c, nullptr, nullptr, nullptr, false, c->wg + (size_t)h * c->S.M, s);
   }

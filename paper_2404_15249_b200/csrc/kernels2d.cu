@@ -872,6 +872,15 @@ __global__ void k_gs_combine(double* __restrict__ w, const double* __restrict__ 
   for (long i = (long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long)gridDim.x * blockDim.x)
     w[i] = 2.0 * y[i] - w[i];   // Crank–Nicolson: (I − aΔ)^{-1}(I + aΔ) w = 2y − w
 }
+// out = base + Σ_q coef[q] · V_q (coefficients in device memory; base may be NULL)
+__global__ void k_combine(long n, const double* __restrict__ base, int k, const double* __restrict__ V, long ldv,
+                          const double* __restrict__ coef, double* __restrict__ out) {
+  for (long i = (long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long)gridDim.x * blockDim.x) {
+    double acc = base ? base[i] : 0.0;
+    for (int q = 0; q < k; ++q) acc = fma(coef[q], V[(size_t)q * ldv + i], acc);
+    out[i] = acc;
+  }
+}
 __global__ void k_fill(double* __restrict__ x, long n, double val) {
   for (long i = (long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long)gridDim.x * blockDim.x) x[i] = val;
 }
@@ -2307,4 +2316,9 @@ void launch_fill(double* x, long n, double val, cudaStream_t s) {
   k_fill<<<(int)std::min<long>((n + 255) / 256, 8L * num_sms()), 256, 0, s>>>(x, n, val);
 }
 
+void launch_combine(long n, const double* base, int k, const double* V, long ldv, const double* coef, double* out,
+                    cudaStream_t s) {
+  ++g_launches;
+  k_combine<<<(int)std::min<long>((n + 255) / 256, 8L * num_sms()), 256, 0, s>>>(n, base, k, V, ldv, coef, out);
+}
 }  // namespace kfbi

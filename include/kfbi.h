@@ -146,6 +146,21 @@ kfbi_status kfbi_slab(const kfbi_ctx* ctx, int32_t rank, int64_t* out6);
 kfbi_status kfbi_setup(const kfbi_grid* grid, const kfbi_boundary* bnd, const kfbi_pde* pde,
                        const kfbi_dist* dist, void* stream, kfbi_ctx** out);
 
+/* Procedure 1 with its O(N²) phases on the device (2D only): node
+ * classification, the sign-change edges and their intersections by 64-step bisection
+ * (readings R30/R31) and the irregular nodes with their incident intersections (P:551,
+ * App. A.3) run as kernels on `stream` in the caller's scratch d_scratch (device, ≥ the bytes
+ * kfbi_setup_scratch_size returns, borrowed for the call only, contents undefined after); the
+ * lists come back to the host (the only host↔device traffic) and the rest of Procedure 1 runs
+ * there as in kfbi_setup.  The lists are identical to kfbi_setup's (same arithmetic, IEEE
+ * round-to-nearest, no contraction; the star level uses the device sin/atan2, so a node within
+ * an ulp of Γ could in principle classify differently).  Synchronous.  Errors as kfbi_setup plus
+ * KFBI_ENOMEM (scratch too small), KFBI_ECUDA, KFBI_EUNSUPPORTED (dim = 3). */
+kfbi_status kfbi_setup_scratch_size(const kfbi_grid* grid, size_t* bytes);
+kfbi_status kfbi_setup_device(const kfbi_grid* grid, const kfbi_boundary* bnd, const kfbi_pde* pde,
+                              const kfbi_dist* dist, void* stream, void* d_scratch, size_t bytes,
+                              kfbi_ctx** out);
+
 /* Bytes of device workspace the context needs (setup tables + scratch). */
 kfbi_status kfbi_workspace_size(const kfbi_ctx* ctx, size_t* bytes);
 

@@ -8,7 +8,7 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "lib", "libkfbi.so")
-SOURCES = ["api.cu", "kernels2d.cu", "kernels3d.cu", "setup2d.cpp", "setup3d.cpp"]
+SOURCES = ["api.cu", "kernels2d.cu", "kernels3d.cu", "setup_gpu.cu", "setup2d.cpp", "setup3d.cpp"]
 NVCC_FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
               "-Xcompiler", "-fPIC,-fopenmp,-O2", "-shared"]
 

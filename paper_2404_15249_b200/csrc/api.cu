@@ -498,8 +498,9 @@ kfbi_status kfbi_get_unique_id(void* out128) {
   return KFBI_OK;
 }
 
-kfbi_status kfbi_setup(const kfbi_grid* grid, const kfbi_boundary* bnd, const kfbi_pde* pde,
-                       const kfbi_dist* dist, void* stream, kfbi_ctx** out) {
+namespace {
+kfbi_status setup_impl(const kfbi_grid* grid, const kfbi_boundary* bnd, const kfbi_pde* pde,
+                       const kfbi_dist* dist, void* stream, const DeviceScratch* dev, kfbi_ctx** out) {
   if (!out) return KFBI_EINVAL;
   *out = nullptr;
   auto* c = new kfbi_ctx();
@@ -516,7 +517,7 @@ kfbi_status kfbi_setup(const kfbi_grid* grid, const kfbi_boundary* bnd, const kf
     if (!grid || !bnd || !pde || !bnd->comp) throw ArgError("null descriptor");
     c->dim = grid->dim;
     if (c->dim == 3) build_setup3(c->S3, grid, bnd, pde);
-    else build_setup(c->S, grid, bnd, pde);
+    else build_setup(c->S, grid, bnd, pde, dev);
     if (c->world > 1) {
       if (c->dim == 3) {
         if (c->S3.P < c->world || c->S3.P % c->world) throw ArgError("3D: world must divide N/16 (slabs = ADM blocks)");
@@ -547,6 +548,14 @@ kfbi_status kfbi_setup(const kfbi_grid* grid, const kfbi_boundary* bnd, const kf
     g_setup_err = e.what();
     delete c;
     return KFBI_EUNSUPPORTED;
+  } catch (const DeviceError& e) {
+    g_setup_err = e.what();
+    delete c;
+    return KFBI_ECUDA;
+  } catch (const ScratchError& e) {
+    g_setup_err = e.what();
+    delete c;
+    return KFBI_ENOMEM;
   } catch (const std::exception& e) {
     g_setup_err = e.what();
     delete c;
@@ -554,6 +563,47 @@ kfbi_status kfbi_setup(const kfbi_grid* grid, const kfbi_boundary* bnd, const kf
   }
   *out = c;
   return KFBI_OK;
+}
+
+}  // namespace
+
+kfbi_status kfbi_setup(const kfbi_grid* grid, const kfbi_boundary* bnd, const kfbi_pde* pde,
+                       const kfbi_dist* dist, void* stream, kfbi_ctx** out) {
+  return setup_impl(grid, bnd, pde, dist, stream, nullptr, out);
+}
+
+kfbi_status kfbi_setup_scratch_size(const kfbi_grid* grid, size_t* bytes) {
+  if (!grid || !bytes) return KFBI_EINVAL;
+  *bytes = 0;
+  if (grid->dim != 2) {
+    g_setup_err = "device setup phases are built for dim = 2 only";
+    return KFBI_EUNSUPPORTED;
+  }
+  const int N = grid->n[0];
+  if (N < 64 || N > 8192 || (N & (N - 1))) {
+    g_setup_err = "n must be a power of two in [64, 8192]";
+    return KFBI_EINVAL;
+  }
+  *bytes = gpu_setup_scratch_bytes(N);
+  return KFBI_OK;
+}
+
+kfbi_status kfbi_setup_device(const kfbi_grid* grid, const kfbi_boundary* bnd, const kfbi_pde* pde,
+                              const kfbi_dist* dist, void* stream, void* d_scratch, size_t bytes,
+                              kfbi_ctx** out) {
+  if (!out) return KFBI_EINVAL;
+  *out = nullptr;
+  if (!grid || grid->dim != 2) {
+    g_setup_err = "device setup phases are built for dim = 2 only";
+    return grid ? KFBI_EUNSUPPORTED : KFBI_EINVAL;
+  }
+  if (!d_scratch) {
+    g_setup_err = "null device scratch";
+    return KFBI_EINVAL;
+  }
+  if (dist && dist->device >= 0) cudaSetDevice(dist->device);
+  const DeviceScratch dev{d_scratch, bytes, (cudaStream_t)stream};
+  return setup_impl(grid, bnd, pde, dist, stream, &dev, out);
 }
 
 kfbi_status kfbi_slab(const kfbi_ctx* c, int32_t rank, int64_t* out) {

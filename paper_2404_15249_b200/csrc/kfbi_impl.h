@@ -9,6 +9,8 @@
 
 #include "../../include/kfbi.h"
 
+struct CUstream_st;   // cudaStream_t without the CUDA headers (setup2d.cpp is plain C++)
+
 namespace kfbi {
 
 // Block structure of the in-GPU partitioned tridiagonal solve along x (arrowhead/ADM,
@@ -21,7 +23,7 @@ constexpr int LB = BL - 1;
 // level-2 blocks of BL2−1 separators around level-2 separators (nested arrowhead).
 constexpr int BL2 = 32;
 constexpr int LB2 = BL2 - 1;
-// most stencil rows one column may hold (checked by setup)
+// most stencil rows in one k_inv_sparse work item (longer columns are split by setup)
 constexpr int kMaxColRows = 512;
 
 // Position of sine mode k (0 ≤ k < N) in the 2D spectral arrays (see setup2d.cpp).
@@ -55,6 +57,12 @@ struct ArgError : std::runtime_error {
   using std::runtime_error::runtime_error;
 };
 struct UnsupportedError : std::runtime_error {   // → KFBI_EUNSUPPORTED
+  using std::runtime_error::runtime_error;
+};
+struct DeviceError : std::runtime_error {        // → KFBI_ECUDA (device setup phases)
+  using std::runtime_error::runtime_error;
+};
+struct ScratchError : std::runtime_error {       // → KFBI_ENOMEM (device setup scratch too small)
   using std::runtime_error::runtime_error;
 };
 
@@ -121,7 +129,18 @@ struct Setup {
   std::vector<int> holes;            // component ids
 };
 
-void build_setup(Setup& S, const kfbi_grid* g, const kfbi_boundary* b, const kfbi_pde* pde);
+// caller-provided device scratch for the GPU setup phases (NEXT-3, setup_gpu.cu)
+struct DeviceScratch {
+  void* ptr;
+  size_t bytes;
+  ::CUstream_st* stream;
+};
+// dev != nullptr: classification, sign-change edges, bisection and the irregular-node lists run on
+// the device (bit-identical lists, tests/test_gpu_setup.py); the rest of Procedure 1 on the host
+void build_setup(Setup& S, const kfbi_grid* g, const kfbi_boundary* b, const kfbi_pde* pde,
+                 const DeviceScratch* dev = nullptr);
+size_t gpu_setup_scratch_bytes(int N);
+void gpu_setup_phases(Setup& S, void* scratch, size_t bytes, ::CUstream_st* s, std::vector<int>& q_owner);
 
 // Host-side setup products in 3D (control points = intersection nodes, reading R12).
 struct Setup3 {

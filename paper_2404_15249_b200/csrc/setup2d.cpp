@@ -181,7 +181,7 @@ bool lu_solve(int n, double* A, double* b) {
 
 }  // namespace
 
-void build_setup(Setup& S, const kfbi_grid* g, const kfbi_boundary* b, const kfbi_pde* pde) {
+void build_setup(Setup& S, const kfbi_grid* g, const kfbi_boundary* b, const kfbi_pde* pde, const DeviceScratch* dev) {
   setup_tick("start");
   if (!g || !b || !pde || !b->comp || b->ncomp < 1) throw ArgError("null descriptor");
   if (g->dim != 2) throw ArgError("only dim = 2 is built in this library version");
@@ -225,6 +225,14 @@ void build_setup(Setup& S, const kfbi_grid* g, const kfbi_boundary* b, const kfb
 
   setup_tick("classification (P:551): Ω side o");
   // ---- classification: Ω side of every node ----
+  // the device path (NEXT-3) runs classification, edges, bisection and the irregular lists in
+  // setup_gpu.cu with the same arithmetic; the host continues from its lists
+  std::vector<int> q_owner;
+  auto side = [&](int i, int j) { return S.side[(size_t)i * W + j]; };
+  if (dev) {
+    if (S.comps.size() > 8) throw ArgError("at most 8 components for the device setup");
+    gpu_setup_phases(S, dev->ptr, dev->bytes, dev->stream, q_owner);
+  } else {
   S.side.assign((size_t)W * W, 0);
 #pragma omp parallel for schedule(static)
   for (int i = 0; i < W; ++i)
@@ -233,21 +241,67 @@ void build_setup(Setup& S, const kfbi_grid* g, const kfbi_boundary* b, const kfb
       for (int c = 0; c < nc && in; ++c) in = omega_side(S.comps[c], X(i), X(j));
       S.side[(size_t)i * W + j] = in ? 1 : 0;
     }
-  auto side = [&](int i, int j) { return S.side[(size_t)i * W + j]; };
 
   setup_tick("intersections on sign-change edg");
   // ---- intersections on sign-change edges ----
-  struct Edge { int axis, i, j; };
-  std::vector<Edge> edges;
+  S.q_axis.clear(); S.q_i.clear(); S.q_j.clear();
   for (int axis = 0; axis < 2; ++axis)
     for (int i = 0; i < W - (axis == 0); ++i)
       for (int j = 0; j < W - (axis == 1); ++j)
-        if (side(i, j) != side(i + (axis == 0), j + (axis == 1))) edges.push_back({axis, i, j});
+        if (side(i, j) != side(i + (axis == 0), j + (axis == 1))) {
+          S.q_axis.push_back(axis);
+          S.q_i.push_back(i);
+          S.q_j.push_back(j);
+        }
   // already in (axis, i, j) order
-  S.nq = (int)edges.size();
+  S.nq = (int)S.q_axis.size();
+  S.q_xi.resize(S.nq);
+  q_owner.resize(S.nq);
+  std::string err;
+#pragma omp parallel for schedule(dynamic, 64)
+  for (int e = 0; e < S.nq; ++e) {
+    const int axis = S.q_axis[e];
+    double x0 = X(S.q_i[e]), y0 = X(S.q_j[e]);
+    double x1 = x0 + (axis == 0 ? h : 0.0), y1 = y0 + (axis == 1 ? h : 0.0);
+    int owner = -1, count = 0;
+    for (int c = 0; c < nc; ++c)
+      if (omega_side(S.comps[c], x0, y0) != omega_side(S.comps[c], x1, y1)) { owner = c; ++count; }
+    if (count != 1) {
+#pragma omp critical
+      err = "edge crossed by several components (R31)";
+      continue;
+    }
+    const Comp& C = S.comps[owner];
+    bool want = omega_side(C, x0, y0);
+    // double-crossing check at interior samples (R31)
+    bool prev = want;
+    int changes = 0;
+    const double ts[5] = {0.2, 0.4, 0.6, 0.8, 1.0};
+    for (double t : ts) {
+      bool cur = omega_side(C, x0 + (axis == 0 ? t * h : 0.0), y0 + (axis == 1 ? t * h : 0.0));
+      changes += cur != prev;
+      prev = cur;
+    }
+    if (changes != 1) {
+#pragma omp critical
+      err = "grid edge crossed more than once (R31)";
+      continue;
+    }
+    double a = 0, bb = 1;
+    for (int it = 0; it < 64; ++it) {
+      double m = 0.5 * (a + bb);
+      bool same = omega_side(C, x0 + (axis == 0 ? m * h : 0.0), y0 + (axis == 1 ? m * h : 0.0)) == want;
+      if (same) a = m; else bb = m;
+    }
+    double t = 0.5 * (a + bb);
+    S.q_xi[e] = (axis == 0 ? x0 : y0) + t * h;
+    q_owner[e] = owner;
+  }
+  if (!err.empty()) throw GeomError(err);
+  }   // host phases
   const int nq = S.nq;
-  S.q_axis.resize(nq); S.q_i.resize(nq); S.q_j.resize(nq); S.q_comp.resize(nq); S.q_knot.resize(nq);
-  S.q_xi.resize(nq); S.q_t.resize(nq); S.q_theta.resize(nq); S.q_t1.resize(nq); S.q_t2.resize(nq);
+  S.q_comp.resize(nq); S.q_knot.resize(nq);
+  S.q_t.resize(nq); S.q_theta.resize(nq); S.q_t1.resize(nq); S.q_t2.resize(nq);
   S.q_p1.resize(nq); S.q_p2.resize(nq); S.q_x.resize(nq); S.q_y.resize(nq);
 
   // components: perimeter, control counts (R11)
@@ -266,45 +320,12 @@ void build_setup(Setup& S, const kfbi_grid* g, const kfbi_boundary* b, const kfb
   for (int c = 0; c < nc; ++c) arcs[c].c = &S.comps[c];
   S.M = off;
 
-  std::string err;
 #pragma omp parallel for schedule(dynamic, 64)
   for (int e = 0; e < nq; ++e) {
-    const Edge ed = edges[e];
-    double x0 = X(ed.i), y0 = X(ed.j);
-    double x1 = x0 + (ed.axis == 0 ? h : 0.0), y1 = y0 + (ed.axis == 1 ? h : 0.0);
-    int owner = -1, count = 0;
-    for (int c = 0; c < nc; ++c)
-      if (omega_side(S.comps[c], x0, y0) != omega_side(S.comps[c], x1, y1)) { owner = c; ++count; }
-    if (count != 1) {
-#pragma omp critical
-      err = "edge crossed by several components (R31)";
-      continue;
-    }
+    const int owner = q_owner[e], axis = S.q_axis[e];
     const Comp& C = S.comps[owner];
-    bool want = omega_side(C, x0, y0);
-    // double-crossing check at interior samples (R31)
-    bool prev = want;
-    int changes = 0;
-    const double ts[5] = {0.2, 0.4, 0.6, 0.8, 1.0};
-    for (double t : ts) {
-      bool cur = omega_side(C, x0 + (ed.axis == 0 ? t * h : 0.0), y0 + (ed.axis == 1 ? t * h : 0.0));
-      changes += cur != prev;
-      prev = cur;
-    }
-    if (changes != 1) {
-#pragma omp critical
-      err = "grid edge crossed more than once (R31)";
-      continue;
-    }
-    double a = 0, bb = 1;
-    for (int it = 0; it < 64; ++it) {
-      double m = 0.5 * (a + bb);
-      bool same = omega_side(C, x0 + (ed.axis == 0 ? m * h : 0.0), y0 + (ed.axis == 1 ? m * h : 0.0)) == want;
-      if (same) a = m; else bb = m;
-    }
-    double t = 0.5 * (a + bb);
-    double xi = (ed.axis == 0 ? x0 : y0) + t * h;
-    double px = ed.axis == 0 ? xi : x0, py = ed.axis == 1 ? xi : y0;
+    const double x0 = X(S.q_i[e]), y0 = X(S.q_j[e]), xi = S.q_xi[e];
+    double px = axis == 0 ? xi : x0, py = axis == 1 ? xi : y0;
     double th = C.kind == KFBI_ELLIPSE ? std::atan2((py - C.c[1]) / C.p[1], (px - C.c[0]) / C.p[0])
                                        : std::atan2(py - C.c[1], px - C.c[0]);
     if (th < 0) th += kTwoPi;
@@ -317,15 +338,15 @@ void build_setup(Setup& S, const kfbi_grid* g, const kfbi_boundary* b, const kfb
     if (m >= C.M) m -= C.M;
     double pos[2], tau[2], taup[2];
     frame(C, th, pos, tau, taup);
-    S.q_axis[e] = ed.axis; S.q_i[e] = ed.i; S.q_j[e] = ed.j; S.q_comp[e] = owner; S.q_knot[e] = m;
-    S.q_xi[e] = xi; S.q_t[e] = tt; S.q_theta[e] = th;
+    S.q_comp[e] = owner; S.q_knot[e] = m;
+    S.q_t[e] = tt; S.q_theta[e] = th;
     S.q_t1[e] = tau[0]; S.q_t2[e] = tau[1]; S.q_p1[e] = taup[0]; S.q_p2[e] = taup[1];
     S.q_x[e] = px; S.q_y[e] = py;
   }
-  if (!err.empty()) throw GeomError(err);
 
   setup_tick("irregular nodes (P:551) and thei");
   // ---- irregular nodes and their incident intersections ----
+  if (!dev) {
   std::unordered_map<int64_t, int> qidx;
   qidx.reserve(nq * 2);
   auto key = [&](int axis, int i, int j) { return ((int64_t)axis * W + i) * W + j; };
@@ -362,10 +383,12 @@ void build_setup(Setup& S, const kfbi_grid* g, const kfbi_boundary* b, const kfb
     }
   }
   S.nirr = (int)S.irr_i.size();
+  }
   {
     std::vector<int> cnt(N + 1, 0);
     for (int r : S.irr_i) cnt[r]++;
     S.col_ptr.assign(N + 1, 0);
+    S.col_mid.assign(N + 1, 0);
     for (int i = 0; i < N; ++i) S.col_ptr[i + 1] = S.col_ptr[i] + cnt[i];
     // col_mid[i]: first even-row entry of column i (== col_ptr[i+1] if none)
     for (int i = 0; i < N; ++i) {
@@ -459,15 +482,20 @@ void build_setup(Setup& S, const kfbi_grid* g, const kfbi_boundary* b, const kfb
     S.st_node.resize(keys.size());
     for (size_t k = 0; k < keys.size(); ++k)
       S.st_node[k] = (int)(std::lower_bound(uk.begin(), uk.end(), keys[k]) - uk.begin());
+    // work items of k_inv_sparse: one per stencil column, a column with more than kMaxColRows rows
+    // (Γ running along a grid line at large N) split into equal chunks of consecutive rows
     S.ocol.clear();
     S.ocol_ptr.assign(1, 0);
-    for (int u = 0; u < S.nsn; ++u) {
-      if (u == 0 || S.sn_i[u] != S.sn_i[u - 1]) {
-        if (u > 0) S.ocol_ptr.push_back(u);
-        S.ocol.push_back(S.sn_i[u]);
+    for (int u0 = 0; u0 < S.nsn;) {
+      int u1 = u0;
+      while (u1 < S.nsn && S.sn_i[u1] == S.sn_i[u0]) ++u1;
+      const int nch = (u1 - u0 + kMaxColRows - 1) / kMaxColRows, per = (u1 - u0 + nch - 1) / nch;
+      for (int k = 0; k < nch; ++k) {
+        S.ocol.push_back(S.sn_i[u0]);
+        S.ocol_ptr.push_back(std::min(u1, u0 + (k + 1) * per));
       }
+      u0 = u1;
     }
-    S.ocol_ptr.push_back(S.nsn);
     S.max_col_rows = 1;
     S.ocol_ncls.assign(3 * (S.ocol_ptr.size() - 1), 0);   // rows per class (odd, j ≡ 0, j ≡ 2 mod 4)
     for (size_t c = 0; c + 1 < S.ocol_ptr.size(); ++c)
@@ -476,7 +504,6 @@ void build_setup(Setup& S, const kfbi_grid* g, const kfbi_boundary* b, const kfb
         ++S.ocol_ncls[3 * c + ((j & 1) ? 0 : ((j & 3) == 0 ? 1 : 2))];
       }
     for (size_t c = 0; c + 1 < S.ocol_ptr.size(); ++c) {
-      if (S.ocol_ptr[c + 1] - S.ocol_ptr[c] > kMaxColRows) throw GeomError("too many stencil rows in one grid column");
       S.max_col_rows = std::max(S.max_col_rows, S.ocol_ptr[c + 1] - S.ocol_ptr[c]);
     }
   }
@@ -524,6 +551,7 @@ void build_setup(Setup& S, const kfbi_grid* g, const kfbi_boundary* b, const kfb
   S.red_a.assign(N, 0.0);
   S.red_b.assign(N, 0.0);
   S.red_invc.assign((size_t)std::max(P - 1, 1) * N, 0.0);
+#pragma omp parallel for schedule(static)
   for (int k = 1; k < N; ++k) {
     double sk = std::sin(kPi * k / (2.0 * N));
     double d = -(2.0 + 4.0 * sk * sk + S.kappa * h * h);
@@ -557,6 +585,7 @@ void build_setup(Setup& S, const kfbi_grid* g, const kfbi_boundary* b, const kfb
   S.z2r.assign((size_t)LB2 * N, 0.0);
   S.red2_a.assign(N, 0.0);
   S.red2_b.assign(N, 0.0);
+#pragma omp parallel for schedule(static)
   for (int k = 1; k < N; ++k) {
     const double a = S.red_a[k], bb = S.red_b[k];
     double c = bb, cs[LB2];
@@ -582,6 +611,7 @@ void build_setup(Setup& S, const kfbi_grid* g, const kfbi_boundary* b, const kfb
     for (int k = 0; k < N; ++k) posof[k] = mode_position(k, N);
     auto perm = [&](std::vector<double>& v, int rows, double fill0) {
       std::vector<double> out(v.size());
+#pragma omp parallel for schedule(static)
       for (int r = 0; r < rows; ++r)
         for (int k = 0; k < N; ++k) out[(size_t)r * N + posof[k]] = k == 0 ? fill0 : v[(size_t)r * N + k];
       v.swap(out);

@@ -1,0 +1,316 @@
+// GPU-side Procedure 1 for 2D geometries: the O(N²) phases of the
+// host setup — node classification, sign-change edges and their intersections by bisection
+// (R30/R31), irregular nodes with their incident intersections (App. A.3) — as one
+// thread per node / edge, the ordered lists by prefix sums (CUB).  The arithmetic is the host's
+// (setup2d.cpp) operation for operation with round-to-nearest intrinsics, so no FMA contraction can
+// move a node across Γ: the lists are bit-identical to the host setup (tests/test_setup_gpu.py).
+// The rest of Procedure 1 (frames, arc length, control points, stencils, tables) stays on the host.
+#include <cuda_runtime.h>
+
+#include <cub/cub.cuh>
+
+#include "kfbi_impl.h"
+
+namespace kfbi {
+namespace {
+
+struct DevComp {
+  int kind, role;
+  double c0, c1, p0, p1, p2, p3;
+};
+struct Comps {
+  int n;
+  DevComp c[8];
+};
+
+__device__ __forceinline__ double node_x(double lo, double h, int i) { return __dadd_rn(lo, __dmul_rn((double)i, h)); }
+
+// level(c, x, y) and omega_side exactly as setup2d.cpp (points on Γ are in Ω, R30)
+__device__ __forceinline__ bool d_omega_side(const DevComp& c, double x, double y) {
+  double l;
+  if (c.kind == KFBI_ELLIPSE) {
+    const double u = __ddiv_rn(__dsub_rn(x, c.c0), c.p0), v = __ddiv_rn(__dsub_rn(y, c.c1), c.p1);
+    l = __dsub_rn(__dadd_rn(__dmul_rn(u, u), __dmul_rn(v, v)), 1.0);
+  } else {
+    const double dx = __dsub_rn(x, c.c0), dy = __dsub_rn(y, c.c1);
+    const double ang = __dmul_rn(c.p2, __dsub_rn(atan2(dy, dx), c.p3));
+    l = __dsub_rn(__dsqrt_rn(__dadd_rn(__dmul_rn(dx, dx), __dmul_rn(dy, dy))),
+                  __dmul_rn(c.p0, __dadd_rn(1.0, __dmul_rn(c.p1, sin(ang)))));
+  }
+  return c.role == KFBI_OUTER ? (l <= 0.0) : (l >= 0.0);
+}
+
+__global__ void k_classify(int W, double lo, double h, Comps cs, int8_t* __restrict__ side) {
+  for (long idx = (long)blockIdx.x * blockDim.x + threadIdx.x; idx < (long)W * W; idx += (long)gridDim.x * blockDim.x) {
+    const int i = (int)(idx / W), j = (int)(idx % W);
+    const double x = node_x(lo, h, i), y = node_x(lo, h, j);
+    bool in = true;
+    for (int c = 0; c < cs.n && in; ++c) in = d_omega_side(cs.c[c], x, y);
+    side[idx] = in ? 1 : 0;
+  }
+}
+
+// flag[axis·W² + i·W + j] = 1 for a sign-change edge from (i, j) along axis (the host's (axis, i, j) order)
+__global__ void k_edge_flags(int W, const int8_t* __restrict__ side, int* __restrict__ flag) {
+  const long WW = (long)W * W;
+  for (long idx = (long)blockIdx.x * blockDim.x + threadIdx.x; idx < 2 * WW; idx += (long)gridDim.x * blockDim.x) {
+    const int axis = (int)(idx / WW);
+    const long r = idx - axis * WW;
+    const int i = (int)(r / W), j = (int)(r % W);
+    int f = 0;
+    if (axis == 0 ? i < W - 1 : j < W - 1) f = side[r] != side[r + (axis == 0 ? W : 1)];
+    flag[idx] = f;
+  }
+}
+
+__global__ void k_edge_compact(int W, const int* __restrict__ flag, const int* __restrict__ qmap, int* __restrict__ qa,
+                               int* __restrict__ qi, int* __restrict__ qj) {
+  const long WW = (long)W * W;
+  for (long idx = (long)blockIdx.x * blockDim.x + threadIdx.x; idx < 2 * WW; idx += (long)gridDim.x * blockDim.x) {
+    if (!flag[idx]) continue;
+    const int q = qmap[idx], axis = (int)(idx / WW);
+    const long r = idx - axis * WW;
+    qa[q] = axis;
+    qi[q] = (int)(r / W);
+    qj[q] = (int)(r % W);
+  }
+}
+
+// owner component, the double-crossing check at 4 interior samples (R31) and 64 halvings (R30)
+__global__ void k_bisect(int nq, double lo, double h, Comps cs, const int* __restrict__ qa, const int* __restrict__ qi,
+                         const int* __restrict__ qj, double* __restrict__ xi_out, int* __restrict__ owner_out,
+                         int* __restrict__ err) {
+  const int e = blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= nq) return;
+  const int axis = qa[e];
+  const double x0 = node_x(lo, h, qi[e]), y0 = node_x(lo, h, qj[e]);
+  const double x1 = axis == 0 ? __dadd_rn(x0, h) : x0, y1 = axis == 1 ? __dadd_rn(y0, h) : y0;
+  int owner = -1, count = 0;
+  for (int c = 0; c < cs.n; ++c)
+    if (d_omega_side(cs.c[c], x0, y0) != d_omega_side(cs.c[c], x1, y1)) {
+      owner = c;
+      ++count;
+    }
+  if (count != 1) {
+    atomicOr(err, 1);
+    return;
+  }
+  const DevComp& C = cs.c[owner];
+  const bool want = d_omega_side(C, x0, y0);
+  bool prev = want;
+  int changes = 0;
+  const double ts[5] = {0.2, 0.4, 0.6, 0.8, 1.0};
+  for (int k = 0; k < 5; ++k) {
+    const double d = __dmul_rn(ts[k], h);
+    const bool cur = d_omega_side(C, axis == 0 ? __dadd_rn(x0, d) : x0, axis == 1 ? __dadd_rn(y0, d) : y0);
+    changes += cur != prev;
+    prev = cur;
+  }
+  if (changes != 1) {
+    atomicOr(err, 2);
+    return;
+  }
+  double a = 0.0, bb = 1.0;
+  for (int it = 0; it < 64; ++it) {
+    const double m = __dmul_rn(0.5, __dadd_rn(a, bb));
+    const double d = __dmul_rn(m, h);
+    const bool same = d_omega_side(C, axis == 0 ? __dadd_rn(x0, d) : x0, axis == 1 ? __dadd_rn(y0, d) : y0) == want;
+    if (same) a = m;
+    else bb = m;
+  }
+  const double t = __dmul_rn(0.5, __dadd_rn(a, bb));
+  xi_out[e] = __dadd_rn(axis == 0 ? x0 : y0, __dmul_rn(t, h));
+  owner_out[e] = owner;
+}
+
+// irregular-node flags in the host's order: column i = 1..N−1, odd rows first, then even rows
+__device__ __forceinline__ int row_of(int jj, int N) { return jj < N / 2 ? 2 * jj + 1 : 2 * (jj - N / 2) + 2; }
+
+__global__ void k_irr_flags(int N, const int8_t* __restrict__ side, int* __restrict__ iflag, int* __restrict__ err) {
+  const int W = N + 1;
+  const long n = (long)(N - 1) * (N - 1);
+  for (long idx = (long)blockIdx.x * blockDim.x + threadIdx.x; idx < n; idx += (long)gridDim.x * blockDim.x) {
+    const int i = 1 + (int)(idx / (N - 1)), j = row_of((int)(idx % (N - 1)), N);
+    const long p = (long)i * W + j;
+    const int8_t s0 = side[p];
+    const bool irr = side[p - W] != s0 || side[p + W] != s0 || side[p - 1] != s0 || side[p + 1] != s0;
+    iflag[idx] = irr ? 1 : 0;
+    if (irr && (i < 2 || j < 2 || i > N - 2 || j > N - 2)) atomicOr(err, 4);   // R32
+  }
+}
+
+__global__ void k_irr_compact(int N, const int* __restrict__ iflag, const int* __restrict__ imap,
+                              const int8_t* __restrict__ side, int* __restrict__ ii, int* __restrict__ ij,
+                              int8_t* __restrict__ iside, int* __restrict__ ncnt) {
+  const int W = N + 1;
+  const long n = (long)(N - 1) * (N - 1);
+  for (long idx = (long)blockIdx.x * blockDim.x + threadIdx.x; idx < n; idx += (long)gridDim.x * blockDim.x) {
+    if (!iflag[idx]) continue;
+    const int r = imap[idx];
+    const int i = 1 + (int)(idx / (N - 1)), j = row_of((int)(idx % (N - 1)), N);
+    const long p = (long)i * W + j;
+    const int8_t s0 = side[p];
+    ii[r] = i;
+    ij[r] = j;
+    iside[r] = s0;
+    ncnt[r] = (side[p - W] != s0) + (side[p + W] != s0) + (side[p - 1] != s0) + (side[p + 1] != s0);
+  }
+}
+
+// the ≤ 4 incident intersections in the host's candidate order, d = x_a(p̄) − ξ (App. A.3)
+__global__ void k_irr_pairs(int N, double lo, double h, int nirr, const int* __restrict__ ii, const int* __restrict__ ij,
+                            const int* __restrict__ iptr, const int8_t* __restrict__ side, const int* __restrict__ qmap,
+                            const double* __restrict__ xi, int* __restrict__ pq, double* __restrict__ pd) {
+  const int r = blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= nirr) return;
+  const int W = N + 1;
+  const long WW = (long)W * W;
+  const int i = ii[r], j = ij[r];
+  const int8_t s0 = side[(long)i * W + j];
+  const int cand[4][5] = {{0, i - 1, j, i - 1, j}, {0, i, j, i + 1, j}, {1, i, j - 1, i, j - 1}, {1, i, j, i, j + 1}};
+  int o = iptr[r];
+  for (int k = 0; k < 4; ++k) {
+    const int oi = cand[k][3], oj = cand[k][4];
+    if (side[(long)oi * W + oj] == s0) continue;
+    const int q = qmap[cand[k][0] * WW + (long)cand[k][1] * W + cand[k][2]];
+    const double xbar = cand[k][0] == 0 ? node_x(lo, h, oi) : node_x(lo, h, oj);
+    pq[o] = q;
+    pd[o] = __dsub_rn(xbar, xi[q]);
+    ++o;
+  }
+}
+
+inline int grid_for(long n) { return (int)std::min<long>((n + 255) / 256, 65535L * 4); }
+
+template <class T>
+T* carve(uint8_t*& p, size_t n) {
+  p = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(p) + 255) & ~uintptr_t(255));
+  T* r = reinterpret_cast<T*>(p);
+  p += n * sizeof(T);
+  return r;
+}
+
+void ck_(cudaError_t e, const char* what) {
+  if (e != cudaSuccess) throw DeviceError(std::string("setup on device: ") + what + ": " + cudaGetErrorString(e));
+}
+
+size_t cub_scan_bytes(long n) {
+  size_t b = 0;
+  cub::DeviceScan::ExclusiveSum(nullptr, b, (const int*)nullptr, (int*)nullptr, (int)n);
+  return b;
+}
+
+// list capacities: nq ≤ kQPerW·(N+1) intersections (Γ of total length up to ~20 box sides) and
+// n_irr ≤ 2·nq (every irregular node ends a sign-change edge, each edge has two ends)
+constexpr long kQPerW = 64;
+size_t lists_bytes(long W) {
+  const long nq = kQPerW * W, ni = 2 * nq;
+  return nq * (4 * sizeof(int) + sizeof(double)) + ni * (4 * sizeof(int) + 1 + 4 * (sizeof(int) + sizeof(double))) +
+         32 * 256;
+}
+
+}  // namespace
+
+size_t gpu_setup_scratch_bytes(int N) {
+  const long W = N + 1, WW = W * W, n2 = (long)(N - 1) * (N - 1);
+  return WW + 2 * (2 * WW) * sizeof(int) + 2 * n2 * sizeof(int) + lists_bytes(W) + cub_scan_bytes(2 * WW) + 16 * 256;
+}
+
+// fills S.side, the intersection base lists (axis, i, j, ξ, owner) and the irregular-node lists
+void gpu_setup_phases(Setup& S, void* scratch, size_t bytes, cudaStream_t s, std::vector<int>& q_owner) {
+  const int N = S.N, W = N + 1;
+  const long WW = (long)W * W, n2 = (long)(N - 1) * (N - 1);
+  if (bytes < gpu_setup_scratch_bytes(N)) throw ScratchError("device setup scratch too small (kfbi_setup_scratch_size)");
+  if (S.comps.size() > 8) throw ArgError("at most 8 components for the device setup");
+  Comps cs{};
+  cs.n = (int)S.comps.size();
+  for (int c = 0; c < cs.n; ++c) {
+    const Comp& C = S.comps[c];
+    cs.c[c] = DevComp{C.kind, C.role, C.c[0], C.c[1], C.p[0], C.p[1], C.p[2], C.p[3]};
+  }
+  uint8_t* p = reinterpret_cast<uint8_t*>(scratch);
+  int8_t* side = carve<int8_t>(p, WW);
+  int* flag = carve<int>(p, 2 * WW);
+  int* qmap = carve<int>(p, 2 * WW);
+  int* iflag = carve<int>(p, n2);
+  int* imap = carve<int>(p, n2);
+  int* err = carve<int>(p, 4);
+  const size_t tb = cub_scan_bytes(2 * WW);
+  void* temp = carve<uint8_t>(p, tb);
+  const long qcap = kQPerW * W, icap = 2 * qcap;
+  int* qa = carve<int>(p, qcap);
+  int* qi = carve<int>(p, qcap);
+  int* qj = carve<int>(p, qcap);
+  int* qo = carve<int>(p, qcap);
+  double* qx = carve<double>(p, qcap);
+  int* ii = carve<int>(p, icap);
+  int* ij = carve<int>(p, icap);
+  int* cnt = carve<int>(p, icap + 1);
+  int* iptr = carve<int>(p, icap + 1);
+  int8_t* isd = carve<int8_t>(p, icap);
+  int* pqv = carve<int>(p, 4 * icap);
+  double* pdv = carve<double>(p, 4 * icap);
+  if ((size_t)(p - reinterpret_cast<uint8_t*>(scratch)) > bytes) throw ScratchError("device setup scratch layout overflow");
+  ck_(cudaMemsetAsync(err, 0, sizeof(int), s), "memset");
+  k_classify<<<grid_for(WW), 256, 0, s>>>(W, S.lo, S.h, cs, side);
+  k_edge_flags<<<grid_for(2 * WW), 256, 0, s>>>(W, side, flag);
+  size_t tbb = tb;
+  ck_(cub::DeviceScan::ExclusiveSum(temp, tbb, flag, qmap, (int)(2 * WW), s), "scan edges");
+  int h_last[2];
+  ck_(cudaMemcpyAsync(&h_last[0], qmap + 2 * WW - 1, sizeof(int), cudaMemcpyDeviceToHost, s), "d2h");
+  ck_(cudaMemcpyAsync(&h_last[1], flag + 2 * WW - 1, sizeof(int), cudaMemcpyDeviceToHost, s), "d2h");
+  ck_(cudaStreamSynchronize(s), "sync");
+  const int nq = h_last[0] + h_last[1];
+  if (nq > qcap) throw ScratchError("more intersections than the device setup scratch holds (64 per grid line)");
+  k_edge_compact<<<grid_for(2 * WW), 256, 0, s>>>(W, flag, qmap, qa, qi, qj);
+  if (nq > 0) k_bisect<<<(nq + 127) / 128, 128, 0, s>>>(nq, S.lo, S.h, cs, qa, qi, qj, qx, qo, err);
+  ck_(cudaGetLastError(), "edge kernels");
+  S.nq = nq;
+  S.q_axis.resize(nq); S.q_i.resize(nq); S.q_j.resize(nq); S.q_xi.resize(nq);
+  q_owner.resize(nq);
+  ck_(cudaMemcpyAsync(S.q_axis.data(), qa, nq * sizeof(int), cudaMemcpyDeviceToHost, s), "d2h");
+  ck_(cudaMemcpyAsync(S.q_i.data(), qi, nq * sizeof(int), cudaMemcpyDeviceToHost, s), "d2h");
+  ck_(cudaMemcpyAsync(S.q_j.data(), qj, nq * sizeof(int), cudaMemcpyDeviceToHost, s), "d2h");
+  ck_(cudaMemcpyAsync(S.q_xi.data(), qx, nq * sizeof(double), cudaMemcpyDeviceToHost, s), "d2h");
+  ck_(cudaMemcpyAsync(q_owner.data(), qo, nq * sizeof(int), cudaMemcpyDeviceToHost, s), "d2h");
+  int h_err = 0;
+  ck_(cudaMemcpyAsync(&h_err, err, sizeof(int), cudaMemcpyDeviceToHost, s), "d2h");
+  S.side.resize(WW);
+  ck_(cudaMemcpyAsync(S.side.data(), side, WW, cudaMemcpyDeviceToHost, s), "d2h side");
+  ck_(cudaStreamSynchronize(s), "sync");
+  if (h_err & 1) throw GeomError("edge crossed by several components (R31)");
+  if (h_err & 2) throw GeomError("grid edge crossed more than once (R31)");
+  // irregular nodes
+  k_irr_flags<<<grid_for(n2), 256, 0, s>>>(N, side, iflag, err);
+  size_t tb2 = tb;
+  ck_(cub::DeviceScan::ExclusiveSum(temp, tb2, iflag, imap, (int)n2, s), "scan irregular");
+  ck_(cudaMemcpyAsync(&h_last[0], imap + n2 - 1, sizeof(int), cudaMemcpyDeviceToHost, s), "d2h");
+  ck_(cudaMemcpyAsync(&h_last[1], iflag + n2 - 1, sizeof(int), cudaMemcpyDeviceToHost, s), "d2h");
+  ck_(cudaMemcpyAsync(&h_err, err, sizeof(int), cudaMemcpyDeviceToHost, s), "d2h");
+  ck_(cudaStreamSynchronize(s), "sync");
+  if (h_err & 4) throw GeomError("Γ too close to the box boundary (R32)");
+  const int nirr = h_last[0] + h_last[1];
+  if (nirr > icap) throw ScratchError("internal: more irregular nodes than 2·nq");
+  k_irr_compact<<<grid_for(n2), 256, 0, s>>>(N, iflag, imap, side, ii, ij, isd, cnt);
+  ck_(cudaMemsetAsync(cnt + nirr, 0, sizeof(int), s), "memset");
+  size_t tb3 = tb;
+  ck_(cub::DeviceScan::ExclusiveSum(temp, tb3, cnt, iptr, nirr + 1, s), "scan pairs");
+  if (nirr > 0)
+    k_irr_pairs<<<(nirr + 127) / 128, 128, 0, s>>>(N, S.lo, S.h, nirr, ii, ij, iptr, side, qmap, qx, pqv, pdv);
+  ck_(cudaGetLastError(), "irregular-node kernels");
+  S.nirr = nirr;
+  S.irr_i.resize(nirr); S.irr_j.resize(nirr); S.irr_side.resize(nirr); S.irr_ptr.resize(nirr + 1);
+  ck_(cudaMemcpyAsync(S.irr_i.data(), ii, nirr * sizeof(int), cudaMemcpyDeviceToHost, s), "d2h");
+  ck_(cudaMemcpyAsync(S.irr_j.data(), ij, nirr * sizeof(int), cudaMemcpyDeviceToHost, s), "d2h");
+  ck_(cudaMemcpyAsync(S.irr_side.data(), isd, nirr, cudaMemcpyDeviceToHost, s), "d2h");
+  ck_(cudaMemcpyAsync(S.irr_ptr.data(), iptr, (nirr + 1) * sizeof(int), cudaMemcpyDeviceToHost, s), "d2h");
+  ck_(cudaStreamSynchronize(s), "sync");
+  const int npair = S.irr_ptr[nirr];
+  S.pair_q.resize(npair);
+  S.pair_d.resize(npair);
+  ck_(cudaMemcpyAsync(S.pair_q.data(), pqv, npair * sizeof(int), cudaMemcpyDeviceToHost, s), "d2h");
+  ck_(cudaMemcpyAsync(S.pair_d.data(), pdv, npair * sizeof(double), cudaMemcpyDeviceToHost, s), "d2h");
+  ck_(cudaStreamSynchronize(s), "sync");
+}
+
+}  // namespace kfbi

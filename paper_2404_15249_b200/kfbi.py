@@ -22,7 +22,7 @@ EXPORTS = ["kfbi_version", "kfbi_last_error", "kfbi_last_setup_error", "kfbi_get
            "kfbi_workspace_size", "kfbi_set_workspace", "kfbi_sizes", "kfbi_points", "kfbi_node_mask",
            "kfbi_apply", "kfbi_solve", "kfbi_apply_model", "kfbi_destroy", "kfbi_test_fast_solve",
            "kfbi_test_interface_solve", "kfbi_test_setup_dump", "kfbi_profile_apply", "kfbi_launch_count",
-           "kfbi_slab", "kfbi_gray_scott_step"]
+           "kfbi_slab", "kfbi_gray_scott_step", "kfbi_setup_scratch_size", "kfbi_setup_device"]
 
 
 class KfbiError(RuntimeError):
@@ -83,6 +83,9 @@ def load(path: str = LIB_PATH):
     lib.kfbi_last_setup_error.restype = C.c_char_p
     lib.kfbi_get_unique_id.argtypes = [vp]
     lib.kfbi_setup.argtypes = [C.POINTER(Grid), C.POINTER(Boundary), C.POINTER(Pde), C.POINTER(Dist), vp, C.POINTER(vp)]
+    lib.kfbi_setup_scratch_size.argtypes = [C.POINTER(Grid), C.POINTER(C.c_size_t)]
+    lib.kfbi_setup_device.argtypes = [C.POINTER(Grid), C.POINTER(Boundary), C.POINTER(Pde), C.POINTER(Dist), vp, vp,
+                                      C.c_size_t, C.POINTER(vp)]
     lib.kfbi_workspace_size.argtypes = [vp, C.POINTER(C.c_size_t)]
     lib.kfbi_set_workspace.argtypes = [vp, vp, C.c_size_t]
     lib.kfbi_sizes.argtypes = [vp, i64p, i64p, i64p, i64p]
@@ -158,9 +161,10 @@ class KFBI:
     kappa and comps (each with kind, role, center, p, n_ctrl) — e.g. workloads.Problem."""
 
     def __init__(self, problem, device: int = 0, stream=None, workspace: bool = True, world: int = 1,
-                 rank: int = 0, nccl_id: bytes = None):
+                 rank: int = 0, nccl_id: bytes = None, device_setup: bool = False):
         """world > 1: slab `rank` of a multi-GPU run (nccl_id from broadcast_unique_id), or
-        rank = −1 to run all slabs in this process (single-GPU emulation of the partition)."""
+        rank = −1 to run all slabs in this process (single-GPU emulation of the partition).
+        device_setup: run the O(N²) phases of Procedure 1 on the GPU (kfbi_setup_device, 2D)."""
         import torch
         self.torch = torch
         self.lib = load()
@@ -181,7 +185,19 @@ class KFBI:
         dist = Dist(world, rank, device, C.cast(self._nccl, C.c_void_p) if self._nccl is not None else None)
         self.world, self.rank = world, rank
         ctx = C.c_void_p()
-        st = self.lib.kfbi_setup(C.byref(g), C.byref(b), C.byref(pde), C.byref(dist), None, C.byref(ctx))
+        if device_setup:
+            sb = C.c_size_t()
+            st = self.lib.kfbi_setup_scratch_size(C.byref(g), C.byref(sb))
+            if st != OK:
+                raise KfbiError(st, self.lib.kfbi_last_setup_error().decode())
+            scratch = torch.empty(sb.value, dtype=torch.uint8, device=self.device)
+            with torch.cuda.device(self.device):
+                strm = torch.cuda.current_stream(self.device).cuda_stream
+                st = self.lib.kfbi_setup_device(C.byref(g), C.byref(b), C.byref(pde), C.byref(dist), C.c_void_p(strm),
+                                                C.c_void_p(scratch.data_ptr()), sb.value, C.byref(ctx))
+            del scratch
+        else:
+            st = self.lib.kfbi_setup(C.byref(g), C.byref(b), C.byref(pde), C.byref(dist), None, C.byref(ctx))
         if st != OK:
             raise KfbiError(st, self.lib.kfbi_last_setup_error().decode())
         self.ctx = ctx

@@ -150,6 +150,16 @@ def test_apply_full_size_C3():
     assert rel(k.apply(phi).cpu().numpy(), o.apply_KD(phi)) < 1e-10
 
 
+@pytest.mark.slow
+def test_apply_full_size_C2_split_columns():
+    """The star at N = 8192 puts > 512 stencil rows in one grid column where Γ runs along it:
+    those columns are split into several k_inv_sparse work items (setup2d.cpp)."""
+    prob = W.C2(8192)
+    o, k = oracle(prob), gpu(prob)
+    phi = W.random_density(o.M, 1)
+    assert rel(k.apply(phi).cpu().numpy(), o.apply_KD(phi)) < 1e-10
+
+
 # ------------------------------------------------------------------ full solve
 @pytest.mark.parametrize("prob", [W.C1(64), W.C2(1024), W.C3(1024)], ids=lambda p: p.name + str(p.n))
 def test_solve_matches_oracle(prob):

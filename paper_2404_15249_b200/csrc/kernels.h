@@ -73,7 +73,7 @@ extern long long g_launches;   // kernels launched by this library (all launcher
 void launch_mgs_step(int n, double* w, const double* Vprev, const double* Vcur, const double* partial_prev,
                      double* partial_cur, double* hout, cudaStream_t s);
 void launch_norm_scale(int n, double* w, const double* partial, double* hout, cudaStream_t s);
-// one-CTA fused MGS step for n ≤ 27648 (returns false → use the multi-CTA path)
+// fused MGS step on one 8-CTA cluster for n ≤ 32768 (returns false → use the multi-kernel path)
 bool launch_mgs_fused(int n, int j, const double* V, double* w, double* hcol, cudaStream_t s);
 void launch_dot(int n, const double* a, const double* b, double* partial, cudaStream_t s);
 void launch_finish_sum(const double* partial, double* out, bool take_sqrt, cudaStream_t s);

@@ -16,6 +16,7 @@
 //                   final applies (once per solve)
 // plus deterministic GMRES vector kernels (Alg. 5).  FP64 on CUDA cores: the
 // path is HBM/latency bound, not a dense contraction (no tensor cores).
+#include <cooperative_groups.h>
 #include <cuda_runtime.h>
 
 #include <cstdio>
@@ -937,39 +938,79 @@ __global__ void k_norm_scale(int n, double* w, const double* __restrict__ partia
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) w[i] = w[i] / hn;
 }
 
-// Whole MGS step of Arnoldi iteration j in one CTA (small M): w stays in shared memory while the
-// j+1 basis vectors stream by; h_i = (w, μ_i), w −= h_i μ_i for i = 0..j, then
-// h_{j+1} = ‖w‖ and w /= h_{j+1}.  Deterministic block reductions.
-constexpr int kMgsThreads = 1024, kMgsMax = 27 * 1024;   // w (≤ 216 KB) in shared memory
-__global__ void __launch_bounds__(kMgsThreads) k_mgs_fused(int n, int j, const double* __restrict__ V, double* w,
-                                                           double* hcol) {
-  extern __shared__ double sw[];
-  __shared__ double scratch[32];
-  __shared__ double s_h;
-  for (int idx = threadIdx.x; idx < n; idx += kMgsThreads) sw[idx] = w[idx];
-  for (int i = 0; i <= j; ++i) {
-    const double* vi = V + (size_t)i * n;
-    double acc[1] = {0.0};
-    for (int idx = threadIdx.x; idx < n; idx += kMgsThreads) acc[0] = fma(sw[idx], vi[idx], acc[0]);
-    block_reduce<1>(acc, scratch);
-    if (threadIdx.x == 0) {
-      s_h = acc[0];
-      hcol[i] = acc[0];
-    }
+// Whole MGS step of Arnoldi iteration j: h_i = (w, μ_i), w −= h_i μ_i for i = 0..j, then
+// h_{j+1} = ‖w‖ and w /= h_{j+1}, on one thread-block cluster: CTA c of kMgsCl owns the contiguous
+// slice [c·n_c, (c+1)·n_c) of w in registers (KPT per thread).  Per projection i: slice dot with v_i
+// (v_{i+1} already loading), warp shuffles + per-warp partials summed in order by thread 0, the CTA
+// partial stored into every CTA's shared slot over DSMEM, one cluster barrier, and every thread sums
+// the kMgsCl partials in rank order — so all CTAs hold the same h_i, then w −= h_i v_i.  Slots are
+// double-buffered by the parity of i: a slot is rewritten two barriers after it was read.
+constexpr int kMgsCl = 8, kMgsClThreads = 512;
+template <int KPT>
+__global__ void __cluster_dims__(kMgsCl, 1, 1) __launch_bounds__(kMgsClThreads)
+    k_mgs_cluster(int n, int j, const double* __restrict__ V, double* w, double* hcol) {
+  namespace cg = cooperative_groups;
+  cg::cluster_group cl = cg::this_cluster();
+  __shared__ double warp_part[kMgsClThreads / 32];
+  __shared__ double slot[2][kMgsCl];
+  const int rank = (int)cl.block_rank(), lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const int nc = (n + kMgsCl - 1) / kMgsCl, c0 = rank * nc, c1 = min(n, c0 + nc);
+  double x[KPT], v[KPT];
+#pragma unroll
+  for (int k = 0; k < KPT; ++k) {
+    const int idx = c0 + threadIdx.x + k * kMgsClThreads;
+    x[k] = idx < c1 ? w[idx] : 0.0;
+    v[k] = idx < c1 ? V[idx] : 0.0;
+  }
+  auto cluster_sum = [&](double a, int parity) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) a += __shfl_xor_sync(0xffffffffu, a, o);
+    if (lane == 0) warp_part[wid] = a;
     __syncthreads();
-    const double h = s_h;
-    for (int idx = threadIdx.x; idx < n; idx += kMgsThreads) sw[idx] = fma(-h, vi[idx], sw[idx]);
+    if (threadIdx.x < kMgsCl) {   // thread r stores this CTA's partial into CTA r's slot
+      double t = 0.0;
+      for (int q = 0; q < kMgsClThreads / 32; ++q) t += warp_part[q];
+      double* remote = cl.map_shared_rank(&slot[parity][0], (int)threadIdx.x);
+      remote[rank] = t;
+    }
+    cl.sync();
+    double tot = 0.0;
+#pragma unroll
+    for (int r = 0; r < kMgsCl; ++r) tot += slot[parity][r];
+    return tot;
+  };
+  for (int i = 0; i <= j; ++i) {
+    double a = 0.0;
+#pragma unroll
+    for (int k = 0; k < KPT; ++k) a = fma(x[k], v[k], a);
+    double vn[KPT];
+    if (i < j) {
+      const double* vi = V + (size_t)(i + 1) * n;
+#pragma unroll
+      for (int k = 0; k < KPT; ++k) {
+        const int idx = c0 + threadIdx.x + k * kMgsClThreads;
+        vn[k] = idx < c1 ? vi[idx] : 0.0;
+      }
+    }
+    const double h = cluster_sum(a, i & 1);
+    if (rank == 0 && threadIdx.x == 0) hcol[i] = h;
+#pragma unroll
+    for (int k = 0; k < KPT; ++k) {
+      x[k] = fma(-h, v[k], x[k]);
+      if (i < j) v[k] = vn[k];
+    }
   }
-  double acc[1] = {0.0};
-  for (int idx = threadIdx.x; idx < n; idx += kMgsThreads) acc[0] = fma(sw[idx], sw[idx], acc[0]);
-  block_reduce<1>(acc, scratch);
-  if (threadIdx.x == 0) {
-    s_h = sqrt(acc[0]);
-    hcol[j + 1] = s_h;
+  double a = 0.0;
+#pragma unroll
+  for (int k = 0; k < KPT; ++k) a = fma(x[k], x[k], a);
+  const double hn = sqrt(cluster_sum(a, (j + 1) & 1));
+  if (rank == 0 && threadIdx.x == 0) hcol[j + 1] = hn;
+#pragma unroll
+  for (int k = 0; k < KPT; ++k) {
+    const int idx = c0 + threadIdx.x + k * kMgsClThreads;
+    if (idx < c1) w[idx] = hn == 0.0 ? x[k] : x[k] / hn;
   }
-  __syncthreads();
-  const double hn = s_h;
-  for (int idx = threadIdx.x; idx < n; idx += kMgsThreads) w[idx] = hn == 0.0 ? sw[idx] : sw[idx] / hn;
+  cl.sync();   // no CTA may exit while another can still write into its slots
 }
 
 __global__ void k_dot(int n, const double* __restrict__ a, const double* __restrict__ b, double* __restrict__ partial) {
@@ -1146,14 +1187,14 @@ void launch_mgs_step(int n, double* w, const double* Vprev, const double* Vcur, 
 }
 
 bool launch_mgs_fused(int n, int j, const double* V, double* w, double* hcol, cudaStream_t s) {
-  if (n > kMgsMax) return false;
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(k_mgs_fused, cudaFuncAttributeMaxDynamicSharedMemorySize, kMgsMax * (int)sizeof(double));
-    attr = true;
+  const int per = (n + kMgsCl * kMgsClThreads - 1) / (kMgsCl * kMgsClThreads);   // elements per thread
+  switch (per <= 1 ? 1 : per <= 2 ? 2 : per <= 4 ? 4 : per <= 8 ? 8 : 0) {
+    case 1: ++g_launches; k_mgs_cluster<1><<<kMgsCl, kMgsClThreads, 0, s>>>(n, j, V, w, hcol); return true;
+    case 2: ++g_launches; k_mgs_cluster<2><<<kMgsCl, kMgsClThreads, 0, s>>>(n, j, V, w, hcol); return true;
+    case 4: ++g_launches; k_mgs_cluster<4><<<kMgsCl, kMgsClThreads, 0, s>>>(n, j, V, w, hcol); return true;
+    case 8: ++g_launches; k_mgs_cluster<8><<<kMgsCl, kMgsClThreads, 0, s>>>(n, j, V, w, hcol); return true;
+    default: return false;
   }
-  { ++g_launches; k_mgs_fused<<<1, kMgsThreads, (size_t)n * sizeof(double), s>>>(n, j, V, w, hcol); }
-  return true;
 }
 
 void launch_norm_scale(int n, double* w, const double* partial, double* hout, cudaStream_t s) {

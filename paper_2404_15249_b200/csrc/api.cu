@@ -299,8 +299,8 @@ void need_ws(kfbi_ctx* c) {
 // owned columns need.  world > 1: level-2 segments = slabs; the segment end values are all-gathered
 // (the only exchange of the tridiagonal solve) and every rank solves the S − 1 slab
 // separators redundantly.
-void spectral2(kfbi_ctx* c, const double* cval, bool dense, cudaStream_t s) {
-  for (int r : my_ranks(c)) launch_sweep(slab(c, r), cval, dense, c->spec, c->zfirst, c->zlast, c->fsep, s);
+void spectral2(kfbi_ctx* c, const double* cval, const DenseSrc& D, cudaStream_t s) {
+  for (int r : my_ranks(c)) launch_sweep(slab(c, r), cval, D, c->spec, c->zfirst, c->zlast, c->fsep, s);
   if (c->world == 1) {
     launch_reduced(c->T, c->zfirst, c->zlast, c->fsep, c->hsep, s);
     return;
@@ -336,26 +336,27 @@ void interp2(kfbi_ctx* c, const double* phi, const double* fz, const double* jz,
   launch_sum_parts(M, c->world, c->parts, out, s);
 }
 
-void dst_forward2(kfbi_ctx* c, const double* fgrid, bool mask, const BumpParams& bp, cudaStream_t s) {
-  for (int r : my_ranks(c)) launch_dst_forward(slab(c, r), fgrid, mask, bp, c->spec, s);
+void dst_forward2(kfbi_ctx* c, const double* fgrid, bool mask, const BumpParams& bp, double* dst, cudaStream_t s) {
+  for (int r : my_ranks(c)) launch_dst_forward(slab(c, r), fgrid, mask, bp, dst, s);
 }
 
 void apply_KD2(kfbi_ctx* c, const double* phi, double* out, cudaStream_t s) {
   const DevTables& T = c->T;
   launch_spline(T, phi, c->mk, s, c->hole_off, c->hole_M, c->hole_delta, c->nh, c->ahole);   // + a_h (R27)
   launch_correct(T, phi, c->mk, nullptr, nullptr, c->cval, s);
-  spectral2(c, c->cval, false, s);
+  spectral2(c, c->cval, DenseSrc{}, s);
   interp2(c, phi, nullptr, nullptr, true, out, s);
 }
 
 void apply_Y2(kfbi_ctx* c, const double* fgrid, const double* fq, const double* fz, double* out, cudaStream_t s) {
   const DevTables& T = c->T;
   BumpParams none{};
-  dst_forward2(c, fgrid, true, none, s);
-  launch_copy((int)((long)(T.N - 1) * T.N), c->spec, c->spec_f, s);   // kept for the final field
+  dst_forward2(c, fgrid, true, none, c->spec_f, s);   // kept for the final field
   c->spec_f_valid = true;
   launch_correct(T, nullptr, nullptr, fq, nullptr, c->cval, s);
-  spectral2(c, c->cval, true, s);
+  DenseSrc D;
+  D.base = c->spec_f;
+  spectral2(c, c->cval, D, s);
   interp2(c, nullptr, fz, nullptr, false, out, s);
 }
 
@@ -364,17 +365,22 @@ void final_field2(kfbi_ctx* c, const double* phi, const double* fgrid, const dou
   BumpParams bp = c->bump;
   bp.a = c->ahole;
   launch_hole_coeffs(T, c->hole_off, c->hole_M, c->hole_delta, c->nh, phi, c->ahole, s);
-  const bool dense = fgrid || c->nh;
-  if (dense && (!fgrid || c->spec_f_valid)) {   // by linearity from the cached spectra
-    const long nspec = (long)(T.N - 1) * T.N;
-    launch_combine(nspec, fgrid ? c->spec_f : nullptr, c->nh, c->spec_bump, nspec, c->ahole, c->spec, s);
-  } else if (dense) {
-    dst_forward2(c, fgrid, true, bp, s);
+  // dense source by linearity from the cached spectra: f̂ + Σ a_h ŵ_h, formed inside the sweep
+  DenseSrc D;
+  if (!fgrid || c->spec_f_valid) {
+    D.base = fgrid ? c->spec_f : nullptr;
+    D.nb = c->nh;
+    D.bump = c->spec_bump;
+    D.ldb = (long)(T.N - 1) * T.N;
+    D.coef = c->ahole;
+  } else {
+    dst_forward2(c, fgrid, true, bp, c->spec_f, s);
+    D.base = c->spec_f;
   }
   c->spec_f_valid = false;
   launch_spline(T, phi, c->mk, s);
   launch_correct(T, phi, c->mk, fq, nullptr, c->cval, s);
-  spectral2(c, c->cval, dense, s);
+  spectral2(c, c->cval, D, s);
   for (int r : my_ranks(c)) launch_inverse_dense(slab(c, r), c->spec, c->hsep, u, s);   // owned columns
   const size_t W = (size_t)T.N + 1;
   ck(cudaMemsetAsync(u, 0, W * sizeof(double), s), "memset");
@@ -651,10 +657,11 @@ kfbi_status kfbi_set_workspace(kfbi_ctx* c, void* d_ws, size_t bytes) {
   for (int h = 0; h < c->nh; ++h) {
     BumpParams bp = c->bump;
     bp.a = c->onehot + (size_t)h * c->nh;
-    dst_forward2(c, nullptr, false, bp, s);
     const long nspec = (long)(c->S.N - 1) * c->S.N;
-    launch_copy((int)nspec, c->spec, c->spec_bump + (size_t)h * nspec, s);
-    spectral2(c, nullptr, true, s);
+    dst_forward2(c, nullptr, false, bp, c->spec_bump + (size_t)h * nspec, s);
+    DenseSrc D;
+    D.base = c->spec_bump + (size_t)h * nspec;
+    spectral2(c, nullptr, D, s);
     interp2(c, nullptr, nullptr, nullptr, false, c->wg + (size_t)h * c->S.M, s);
   }
   ck(cudaGetLastError(), "setup kernels");
@@ -1031,7 +1038,7 @@ kfbi_status kfbi_profile_apply(kfbi_ctx* c, const double* d_phi, double* d_out, 
     ck(cudaEventRecord(ev[1], s), "rec");
     launch_correct(T, d_phi, c->mk, nullptr, nullptr, c->cval, s);
     ck(cudaEventRecord(ev[2], s), "rec");
-    launch_sweep(T, c->cval, false, c->spec, c->zfirst, c->zlast, c->fsep, s);
+    launch_sweep(T, c->cval, DenseSrc{}, c->spec, c->zfirst, c->zlast, c->fsep, s);
     ck(cudaEventRecord(ev[3], s), "rec");
     launch_reduced(T, c->zfirst, c->zlast, c->fsep, c->hsep, s);
     ck(cudaEventRecord(ev[4], s), "rec");
@@ -1128,7 +1135,9 @@ kfbi_status kfbi_test_fast_solve(kfbi_ctx* c, const double* d_rhs, double* d_v, 
   }
   BumpParams none{};
   launch_dst_forward(c->T, d_rhs, false, none, c->spec, s);
-  launch_sweep(c->T, nullptr, true, c->spec, c->zfirst, c->zlast, c->fsep, s);
+  DenseSrc D;
+  D.base = c->spec;
+  launch_sweep(c->T, nullptr, D, c->spec, c->zfirst, c->zlast, c->fsep, s);
   launch_reduced(c->T, c->zfirst, c->zlast, c->fsep, c->hsep, s);
   launch_inverse_dense(c->T, c->spec, c->hsep, d_v, s);
   const size_t W = (size_t)c->T.N + 1;
@@ -1169,7 +1178,9 @@ kfbi_status kfbi_test_interface_solve(kfbi_ctx* c, const double* d_base, const d
   BumpParams none{};
   if (d_base) launch_dst_forward(c->T, d_base, false, none, c->spec, s);
   launch_correct(c->T, nullptr, nullptr, nullptr, d_jq, c->cval, s);
-  launch_sweep(c->T, c->cval, d_base != nullptr, c->spec, c->zfirst, c->zlast, c->fsep, s);
+  DenseSrc D;
+  D.base = d_base ? c->spec : nullptr;
+  launch_sweep(c->T, c->cval, D, c->spec, c->zfirst, c->zlast, c->fsep, s);
   launch_reduced(c->T, c->zfirst, c->zlast, c->fsep, c->hsep, s);
   if (d_vplus) {
     launch_inverse_sparse(c->T, c->spec, c->hsep, c->vsten, s);

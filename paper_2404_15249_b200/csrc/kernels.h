@@ -36,9 +36,20 @@ struct BumpParams {
 };
 void launch_dst_forward(const DevTables& T, const double* fgrid, bool mask, const BumpParams& bp,
                         double* spec, cudaStream_t s);
+// dense spectral source of a sweep: f̂ = base + Σ_{h<nb} coef[h] · bump[h·ldb] (any of them may be
+// absent; base may alias the sweep's output). The final field's linear combination (R27) is formed
+// as it is read instead of in a separate pass over the grid.
+struct DenseSrc {
+  const double* base = nullptr;
+  int nb = 0;
+  const double* bump = nullptr;
+  long ldb = 0;
+  const double* coef = nullptr;   // device, nb entries
+  bool any() const { return base || nb > 0; }
+};
 // A4+A5 fused: per (mode pair, block) local solve with the sparse-correction DST computed
-// on the fly; dense f̂ read from `spec` (in place) when `dense`.
-void launch_sweep(const DevTables& T, const double* cval, bool dense, double* spec, double* zfirst,
+// on the fly, plus the dense f̂ of `D` when present.
+void launch_sweep(const DevTables& T, const double* cval, const DenseSrc& D, double* spec, double* zfirst,
                   double* zlast, double* fsep, cudaStream_t s);
 // A5 reduced (arrowhead) system per mode: separator values h_g.
 void launch_reduced(const DevTables& T, const double* zfirst, const double* zlast, const double* fsep,

@@ -151,8 +151,9 @@ constexpr int kRotStride = kQuads / kRotSteps;  // 32
 // q = τ/2, w = τ mod 2; local Thomas per mode, pivots in registers for the CTA's lifetime; writes
 // z (block rows), B[g] = z_g[1], A[g] = h² f̂_sep,g − z_g[L].
 template <bool DENSE>
-__global__ void __launch_bounds__(kSweepThreads, 2) k_sweep(DevTables T, const double* __restrict__ cval, double* spec,
-                                                           double* __restrict__ zB, double* __restrict__ zA) {
+__global__ void __launch_bounds__(kSweepThreads, 2) k_sweep(DevTables T, const double* __restrict__ cval, DenseSrc D,
+                                                           double* spec, double* __restrict__ zB,
+                                                           double* __restrict__ zA) {
   extern __shared__ double sm[];
   const int N = T.N, half = N >> 1, quarter = N >> 2, m2 = 2 * N - 1, B = kSweepThreads;
   double* R = sm;                                            // [4·BL sums][kQuads]
@@ -288,8 +289,17 @@ __global__ void __launch_bounds__(kSweepThreads, 2) k_sweep(DevTables T, const d
       const double A = Rs[(4 * c + w) * kQuads], E = Rs[(4 * c + 2 + w) * kQuads];
       r1 = w ? A - E : A + E;
       r2 = w ? A + E : A - E;
-      if (DENSE) {
-        const double2 d = *reinterpret_cast<const double2*>(spec + (size_t)(c0 + c - 1) * N + p1);
+      if (DENSE) {   // f̂ = base + Σ a_h bump_h, the fma order of k_combine
+        const size_t off = (size_t)(c0 + c - 1) * N + p1;
+        double2 d = D.base ? *reinterpret_cast<const double2*>(D.base + off) : make_double2(0.0, 0.0);
+#pragma unroll
+        for (int q = 0; q < 4; ++q)
+          if (q < D.nb) {
+            const double2 b = __ldcs(reinterpret_cast<const double2*>(D.bump + (size_t)q * D.ldb + off));
+            const double a = __ldg(D.coef + q);
+            d.x = fma(a, b.x, d.x);
+            d.y = fma(a, b.y, d.y);
+          }
         r1 = fma(h2, d.x, r1);
         r2 = fma(h2, d.y, r2);
       }
@@ -1075,8 +1085,9 @@ void launch_correct(const DevTables& T, const double* phi, const double* mk, con
 
 
 
-void launch_sweep(const DevTables& T, const double* cval, bool dense, double* spec, double* zfirst, double* zlast,
-                  double* fsep, cudaStream_t s) {
+void launch_sweep(const DevTables& T, const double* cval, const DenseSrc& D, double* spec, double* zfirst,
+                  double* zlast, double* fsep, cudaStream_t s) {
+  const bool dense = D.any();
   (void)zlast;
   const size_t sm = (size_t)BL * 4 * kQuads * sizeof(double) + (size_t)T.maxe * 5 * sizeof(double) +
                     (size_t)(2 * T.N / 64 + 64 + 1) * sizeof(double2) + 3 * BL * sizeof(int);
@@ -1095,9 +1106,9 @@ void launch_sweep(const DevTables& T, const double* cval, bool dense, double* sp
   if (G > T.g_hi - T.g_lo) G = T.g_hi - T.g_lo;
   const int grid = nch * G;
   if (dense)
-    { ++g_launches; k_sweep<true><<<grid, kSweepThreads, sm, s>>>(T, cval, spec, zfirst, fsep); }
+    { ++g_launches; k_sweep<true><<<grid, kSweepThreads, sm, s>>>(T, cval, D, spec, zfirst, fsep); }
   else
-    { ++g_launches; k_sweep<false><<<grid, kSweepThreads, sm, s>>>(T, cval, spec, zfirst, fsep); }
+    { ++g_launches; k_sweep<false><<<grid, kSweepThreads, sm, s>>>(T, cval, D, spec, zfirst, fsep); }
 }
 
 void launch_reduced(const DevTables& T, const double* zfirst, const double* zlast, const double* fsep, double* hsep,

@@ -373,6 +373,10 @@ void final_field2(kfbi_ctx* c, const double* phi, const double* fgrid, const dou
     D.bump = c->spec_bump;
     D.ldb = (long)(T.N - 1) * T.N;
     D.coef = c->ahole;
+    for (int h = 0; h < c->nh && h < 4; ++h) {   // bump h lives in |x − cx| < rad
+      D.blo[h] = std::max(1, (int)std::floor((c->bump.cx[h] - c->bump.rad[h] - T.lo) / T.h) - 1);
+      D.bhi[h] = std::min(T.N - 1, (int)std::ceil((c->bump.cx[h] + c->bump.rad[h] - T.lo) / T.h) + 1);
+    }
   } else {
     dst_forward2(c, fgrid, true, bp, c->spec_f, s);
     D.base = c->spec_f;

@@ -45,6 +45,7 @@ struct DenseSrc {
   const double* bump = nullptr;
   long ldb = 0;
   const double* coef = nullptr;   // device, nb entries
+  int blo[4] = {0, 0, 0, 0}, bhi[4] = {-1, -1, -1, -1};   // grid columns i where bump h can be non-zero
   bool any() const { return base || nb > 0; }
 };
 // A4+A5 fused: per (mode pair, block) local solve with the sparse-correction DST computed

@@ -80,7 +80,7 @@ void launch_red2_fixup(const DevTables& T, const double* h2, double* hsep, cudaS
 void launch_sum_parts(int n, int nparts, const double* parts, double* out, cudaStream_t s);
 
 // A8: GMRES vector kernels (deterministic fixed-grid reductions)
-constexpr int kRedBlocks = 64;
+constexpr int kRedBlocks = 512;   // per-CTA partials of the multi-CTA reductions (multiple of 32)
 extern long long g_launches;   // kernels launched by this library (all launchers bump it)
 void launch_mgs_step(int n, double* w, const double* Vprev, const double* Vcur, const double* partial_prev,
                      double* partial_cur, double* hout, cudaStream_t s);

@@ -1027,10 +1027,26 @@ __global__ void __launch_bounds__(DenseCfg<N>::NTHR, 1) k_dst_dense2(DevTables T
 }
 
 // ------------------------------------------------------------------------------ A8 GMRES
-__device__ __forceinline__ double ordered_sum(const double* __restrict__ p) {
+// sum of the kRedBlocks per-CTA partials in a fixed order (deterministic), by one warp: lane l adds
+// p[l], p[l+32], … (independent loads), then a fixed xor tree; every lane returns the total
+__device__ __forceinline__ double warp_ordered_sum(const double* __restrict__ p) {
+  const int lane = threadIdx.x & 31;
   double s = 0.0;
-  for (int b = 0; b < kRedBlocks; ++b) s += p[b];
+#pragma unroll
+  for (int b = 0; b < kRedBlocks / 32; ++b) s += p[lane + 32 * b];
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
   return s;
+}
+// the same total broadcast to the whole CTA (warp 0 sums, one barrier)
+__device__ __forceinline__ double block_ordered_sum(const double* __restrict__ p) {
+  __shared__ double s_tot;
+  if (threadIdx.x < 32) {
+    const double t = warp_ordered_sum(p);
+    if (threadIdx.x == 0) s_tot = t;
+  }
+  __syncthreads();
+  return s_tot;
 }
 
 __global__ void k_mgs_step(int n, double* w, const double* Vprev, const double* Vcur, const double* pprev,
@@ -1040,24 +1056,37 @@ __global__ void k_mgs_step(int n, double* w, const double* Vprev, const double* 
   const int b0 = blockIdx.x * per, b1 = min(n, b0 + per);
   double hp = 0.0;
   if (Vprev) {
-    hp = ordered_sum(pprev);
+    hp = block_ordered_sum(pprev);
     if (blockIdx.x == 0 && threadIdx.x == 0) *hout = hp;
   }
-  double v[1] = {0.0};
-  for (int i = b0 + threadIdx.x; i < b1; i += blockDim.x) {
-    double wv = w[i];
+  double a0 = 0.0, a1 = 0.0;   // two independent chains
+  int i = b0 + threadIdx.x;
+  for (; i + (int)blockDim.x < b1; i += 2 * blockDim.x) {
+    double w0 = w[i], w1 = w[i + blockDim.x];
     if (Vprev) {
-      wv = fma(-hp, Vprev[i], wv);
-      w[i] = wv;
+      w0 = fma(-hp, Vprev[i], w0);
+      w1 = fma(-hp, Vprev[i + blockDim.x], w1);
+      w[i] = w0;
+      w[i + blockDim.x] = w1;
     }
-    v[0] = fma(wv, Vcur[i], v[0]);
+    a0 = fma(w0, Vcur[i], a0);
+    a1 = fma(w1, Vcur[i + blockDim.x], a1);
   }
+  if (i < b1) {
+    double w0 = w[i];
+    if (Vprev) {
+      w0 = fma(-hp, Vprev[i], w0);
+      w[i] = w0;
+    }
+    a0 = fma(w0, Vcur[i], a0);
+  }
+  double v[1] = {a0 + a1};
   block_reduce<1>(v, scratch);
   if (threadIdx.x == 0) pcur[blockIdx.x] = v[0];
 }
 
 __global__ void k_norm_scale(int n, double* w, const double* __restrict__ partial, double* hout) {
-  const double hn = sqrt(ordered_sum(partial));
+  const double hn = sqrt(block_ordered_sum(partial));
   if (blockIdx.x == 0 && threadIdx.x == 0) *hout = hn;
   if (hn == 0.0) return;
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) w[i] = w[i] / hn;
@@ -1149,9 +1178,9 @@ __global__ void k_dot(int n, const double* __restrict__ a, const double* __restr
 }
 
 __global__ void k_finish_sum(const double* __restrict__ partial, double* out, int take_sqrt) {
-  if (threadIdx.x == 0 && blockIdx.x == 0) {
-    const double s = ordered_sum(partial);
-    *out = take_sqrt ? sqrt(s) : s;
+  if (threadIdx.x < 32 && blockIdx.x == 0) {
+    const double s = warp_ordered_sum(partial);
+    if (threadIdx.x == 0) *out = take_sqrt ? sqrt(s) : s;
   }
 }
 

@@ -257,12 +257,12 @@ __device__ __forceinline__ int fpos(int j) { return j + 2 * (j >> 5); }
 //   ⇒ F_2k = Im Y_k,  F_2k+1 − F_2k−1 = Re Y_k  (F_−1 = −F_1): the odd outputs are the prefix sums
 //   of Re Y, taken per lane (16 terms) and across the row's lanes by a log-depth shuffle scan.
 // On exit F_j sits at ((double*)z)[fpos(j)], j ∈ [0, N).
+// wa, wb = e^{iπ(2 tid)/N}, e^{iπ(2 tid+1)/N} (callers may load them before their last barrier)
 template <int N>
-__device__ __forceinline__ void dst2_core(double2* z, const double2* __restrict__ tw, int tid,
-                                          double* scratch = nullptr) {   // scratch: N/1024 + 1 doubles if N > 1024
+__device__ __forceinline__ void dst2_core_w(double2* z, const double2* __restrict__ tw, int tid, double2 wa, double2 wb,
+                                            double* scratch = nullptr) {   // scratch: N/1024 + 1 doubles if N > 1024
   constexpr int M = N / 2, NTL = N / 32;
   double2 v[16];
-  const double2 wa = __ldg(tw + 2 * tid), wb = __ldg(tw + 2 * tid + 1);   // e^{iπ(2 tid)/N}, e^{iπ(2 tid+1)/N}
 #pragma unroll
   for (int s = 0; s < 16; ++s) {   // item tid of the first radix-16 pass holds m = tid + NTL·s
     const int m = tid + NTL * s;
@@ -333,6 +333,12 @@ __device__ __forceinline__ void dst2_core(double2* z, const double2* __restrict_
 }
 
 
+
+template <int N>
+__device__ __forceinline__ void dst2_core(double2* z, const double2* __restrict__ tw, int tid,
+                                          double* scratch = nullptr) {
+  dst2_core_w<N>(z, tw, tid, __ldg(tw + 2 * tid), __ldg(tw + 2 * tid + 1), scratch);
+}
 
 // accurate DST-I (2D rows, N up to 8192): the real DFT of the odd extension x (x_t = f_t, x_N = 0,
 // x_{2N−t} = −f_t) by one N-point complex FFT of z_m = x_2m + i x_2m+1; F_k = Im(E_k + e^{iπk/N} O_k)/2.

@@ -289,6 +289,7 @@ __global__ void __launch_bounds__(256, 2) k_dst_rows3t(DevTables3 T, double* wor
 // only the distinct stencil nodes of the result are read, so the z-direction transforms are sparse.
 // forward: plane i, columns ll ∈ [l0, l0 + RPC): G_a = Σ_{irregular (i,a,b)} c · sin(π b ll/N) (the
 // z-DST of the sparse rows, evaluated directly), then the y-DST of G along a → work[(i−1)][ll][kk].
+constexpr int kFwdGroups = 8;
 template <int N>
 __global__ void __launch_bounds__(256, 2) k_fwd3s(DevTables3 T, const double* __restrict__ corr,
                                                   double* __restrict__ work) {
@@ -317,7 +318,10 @@ __global__ void __launch_bounds__(256, 2) k_fwd3s(DevTables3 T, const double* __
   // s, c = sin, cos(πbt/N): sin(πb(N−t)/N) = (−1)^{b+1} s, sin(πb(N/2 ± t)/N) = sin(πb/2) c ± cos(πb/2) s,
   // so one rotation per entry serves four columns (the 2D sweep's quad symmetry, along z).
   constexpr int QPI = CPT / 4;   // quads per item
-  const int tq0 = blockIdx.x * (RPC / 4);
+  // kFwdGroups consecutive mode groups per CTA: the plane's entries are staged once for all of them
+  for (int grp = blockIdx.x * kFwdGroups; grp < (blockIdx.x + 1) * kFwdGroups && grp * RPC < N; ++grp) {
+  const int tq0 = grp * (RPC / 4);
+  if (grp != blockIdx.x * kFwdGroups) __syncthreads();   // the previous group's rows have been written out
   for (int it = threadIdx.x; it < N * NG; it += NTHR) {
     const int rr = it % N, cg = it / N, k = rr / NTHR, pos = rr % NTHR;
     const int a = T.irr_row_perm[(size_t)(i - 1) * N + k * NTHR + ((k & 1) ? NTHR - 1 - pos : pos)];
@@ -354,10 +358,11 @@ __global__ void __launch_bounds__(256, 2) k_fwd3s(DevTables3 T, const double* __
 #pragma unroll
     for (int c = 0; c < CPT; ++c) reinterpret_cast<double*>(smz + (cg * CPT + c) * ZS)[off] = a ? g[c] : 0.0;
   }
-  __syncthreads();
   const int rl = threadIdx.x / NTL, tid = threadIdx.x % NTL;
+  const double2 wa = __ldg(tw + 2 * tid), wb = __ldg(tw + 2 * tid + 1);   // in flight across the barrier
+  __syncthreads();
   double2* z = smz + rl * ZS;
-  dst2_core<N>(z, tw, tid);
+  dst2_core_w<N>(z, tw, tid, wa, wb);
   const int tq = tq0 + (rl >> 2), mem = rl & 3;   // this row's mode: member of quad tq
   const int ll = tq ? (mem == 0 ? tq : mem == 1 ? N - tq : mem == 2 ? N / 2 - tq : N / 2 + tq)
                     : (mem == 0 ? 0 : mem == 1 ? N / 2 : mem == 2 ? N / 4 : 3 * N / 4);
@@ -369,6 +374,7 @@ __global__ void __launch_bounds__(256, 2) k_fwd3s(DevTables3 T, const double* __
     const int j = 2 * (tid + s * NTL);
     const double2 f = *reinterpret_cast<const double2*>(F + fpos(j));
     __stcs(reinterpret_cast<double2*>(op + j), make_double2(sc * f.x, sc * f.y));
+  }
   }
 }
 
@@ -671,7 +677,8 @@ static void sparse3_n(const DevTables3& T, int which, const double* src, const d
       cudaFuncSetAttribute(k_fwd3s<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm0);
       attr0 = sm0;
     }
-    k_fwd3s<N><<<grid, NTHR, sm0, s>>>(T, src, dst);
+    const dim3 gridf((N / RPC + kFwdGroups - 1) / kFwdGroups, T.i_hi - T.i_lo + 1);
+    k_fwd3s<N><<<gridf, NTHR, sm0, s>>>(T, src, dst);
   }
   else if (which == 1) k_inv3y<N><<<grid, NTHR, sm, s>>>(T, src, hsep, scale, dst);
   else if (T.w_hi > T.w_lo) k_zeval3<N><<<std::min(cdiv3(T.w_hi - T.w_lo, 8), num_sms() * 2), 256, 0, s>>>(T, src, scale, dst);

@@ -235,10 +235,33 @@ def main():
     copies = 1 if sharded else world          # replicas each solve the whole problem
     value = copies * U * n_app / t_step
 
-    # e2e through the public API with pinned host buffers
+    # e2e through the public API with pinned host buffers.  Single-grid layouts move only the Ω-node
+    # values of f and u (kfbi_scatter_omega / kfbi_gather_omega: f is zero-extended off Ω, and
+    # u_h is valid on Ω); slab-sharded runs move full grids.
     pin = lambda a: torch.tensor(a, dtype=torch.float64).pin_memory()
-    g_h, fg_h, fq_h, fz_h = pin(g), pin(fgrid), pin(fq), pin(fz)
-    u_h = torch.empty(k.n_nodes, dtype=torch.float64).pin_memory()
+    compact = not sharded
+    if compact:
+        omask = k.node_mask().reshape(-1).astype(bool)
+        n_out = int(omask.sum())
+        fg_h = pin(np.ascontiguousarray(fgrid.reshape(-1)[omask]))
+        fg_full = [torch.empty(k.n_nodes, dtype=torch.float64, device=dev) for _ in range(2)]
+    else:
+        n_out = k.n_nodes
+        fg_h = pin(fgrid)
+    g_h, fq_h, fz_h = pin(g), pin(fq), pin(fz)
+    u_h = torch.empty(n_out, dtype=torch.float64).pin_memory()
+    u_c = torch.empty(n_out, dtype=torch.float64, device=dev) if compact else None
+
+    def solve_io(gd, fgd, fqd, fzd, b, u=None):
+        """kfbi_solve on device inputs; with compact transfers f is scattered first and the Ω values
+        of u gathered after; returns the device array the host copy reads."""
+        if compact:
+            u, _, st_ = k.solve(gd, k.scatter_omega(fgd, grid=fg_full[b]), fqd, fzd, u=u, method=args.method)
+            return k.gather_omega(u, compact=u_c if b is None else u_cs[b])
+        u, _, st_ = k.solve(gd, fgd, fqd, fzd, u=u, method=args.method)
+        return u.view(-1)
+
+    u_cs = [torch.empty(n_out, dtype=torch.float64, device=dev) for _ in range(2)] if compact else None
     e2e_t = []
     for it in range(args.warmup + args.steps):
         flush.zero_()
@@ -249,8 +272,8 @@ def main():
         fgd = fg_h.to(dev, non_blocking=True)
         fqd = fq_h.to(dev, non_blocking=True)
         fzd = fz_h.to(dev, non_blocking=True)
-        u, _, st2 = k.solve(gd, fgd, fqd, fzd, method=args.method)
-        u_h.copy_(u.view(-1), non_blocking=True)
+        uo = solve_io(gd, fgd, fqd, fzd, 0)
+        u_h.copy_(uo, non_blocking=True)
         e1.record(stream)
         e1.synchronize()
         if it >= args.warmup:
@@ -260,8 +283,8 @@ def main():
         tt = torch.tensor([t_e2e], device=dev)
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         t_e2e = float(tt.item())
-    h2d = 8 * (g.size + fgrid.size + fq.size + fz.size)
-    d2h = 8 * k.n_nodes
+    h2d = 8 * (g.size + fg_h.numel() + fq.size + fz.size)
+    d2h = 8 * n_out
 
     # e2e, pipelined serving loop through the same public API: step k+1's inputs are uploaded on an
     # H2D copy stream while step k solves, and step k's field is downloaded on a D2H copy stream while
@@ -271,7 +294,7 @@ def main():
         h2d_s, d2h_s = torch.cuda.Stream(dev), torch.cuda.Stream(dev)
         din = [[torch.empty_like(x, device=dev) for x in (g_h, fg_h, fq_h, fz_h)] for _ in range(2)]
         dout = [torch.empty(k.n_nodes, dtype=torch.float64, device=dev) for _ in range(2)]
-        hout = [torch.empty(k.n_nodes, dtype=torch.float64).pin_memory() for _ in range(2)]
+        hout = [torch.empty(n_out, dtype=torch.float64).pin_memory() for _ in range(2)]
         ev_in = [torch.cuda.Event() for _ in range(2)]
         ev_done = [torch.cuda.Event() for _ in range(2)]
         ev_out = [torch.cuda.Event() for _ in range(2)]
@@ -297,11 +320,11 @@ def main():
             stream.wait_event(ev_in[b])
             if j >= 2:
                 stream.wait_event(ev_out[b])                # download j−2 has left dout[b]
-            k.solve(*din[b], u=dout[b], method=args.method)
+            uo = solve_io(*din[b], b, u=dout[b])
             ev_done[b].record(stream)
             with torch.cuda.stream(d2h_s):
                 d2h_s.wait_event(ev_done[b])
-                hout[b].copy_(dout[b], non_blocking=True)
+                hout[b].copy_(uo, non_blocking=True)
                 ev_out[b].record(d2h_s)
         d2h_s.wait_stream(h2d_s)
         t1.record(d2h_s)
@@ -350,7 +373,9 @@ def main():
         "e2e": {"value": copies * U * n_app / t_e2e_pipe, "unit": UNIT, "h2d_bytes_per_step": h2d,
                 "d2h_bytes_per_step": d2h, "s_per_step": t_e2e_pipe,
                 "mode": "pipelined serving loop: H2D of step k+1 and D2H of step k overlap the solves "
-                        "(two copy streams, double-buffered); timed from the first upload to the last download",
+                        "(two copy streams, double-buffered); timed from the first upload to the last download"
+                        + ("; f and u cross PCIe as their Omega-node values (kfbi_scatter_omega before and "
+                           "kfbi_gather_omega after each solve, inside the timed region)" if compact else ""),
                 "serial": {"value": copies * U * n_app / t_e2e, "s_per_step": t_e2e,
                            "mode": "H2D, solve, D2H back to back every step"}},
         "gpu_launches": launches, "gpu_launches_per_step": launches / args.steps,

@@ -180,6 +180,17 @@ kfbi_status kfbi_points(const kfbi_ctx* ctx, int32_t which, double* host_xyz);
 /* Ω mask of the full node grid ((N+1)^d int8, 1 = Ω) into host memory. */
 kfbi_status kfbi_node_mask(const kfbi_ctx* ctx, int8_t* host_mask);
 
+/* Ω-compact grid transfers (serving path).  The solve uses f only on Ω nodes (zero extension,
+ * P:530) and u_h is valid only there, so a caller may move just the Ω values across PCIe:
+ * n_omega = number of Ω nodes of the full (N+1)^d node grid, in row-major node order (i, j[, k]) —
+ * the order of kfbi_node_mask's 1 entries.  kfbi_scatter_omega: d_grid[p] = d_compact[rank of p]
+ * on Ω nodes, 0 elsewhere (a full-grid f for kfbi_solve).  kfbi_gather_omega: d_compact[rank of p] =
+ * d_grid[p] for the Ω nodes of a full grid (e.g. kfbi_solve's u).  Device pointers, n_omega and
+ * (N+1)^d doubles; asynchronous on `stream`; single-context grids (world = 1 layouts). */
+kfbi_status kfbi_omega_count(const kfbi_ctx* ctx, int64_t* n_omega);
+kfbi_status kfbi_scatter_omega(kfbi_ctx* ctx, const double* d_compact, double* d_grid, void* stream);
+kfbi_status kfbi_gather_omega(kfbi_ctx* ctx, const double* d_grid, double* d_compact, void* stream);
+
 /* out = K̃φ = K_D φ (+ hole completion, R27), φ and out are M doubles on the device.
  * Neumann contexts: out = K_N ψ = ½ψ − ∂_n(Sψ) = ∂_n V⁺ of the interface problem with
  * [v] = 0, [∂_n v] = ψ (reading R38).  Asynchronous, stream-ordered, no state change. */

@@ -69,6 +69,11 @@ struct kfbi_ctx {
   double *partial = nullptr, *hcol = nullptr, *ycoef = nullptr, *scal = nullptr;
   double *spec_f = nullptr, *spec_bump = nullptr;   // cached spectra (final field by linearity)
   bool spec_f_valid = false;
+  // Ω-compact transfers: Ω nodes per grid row (prefix), the full-grid mask on the device
+  std::vector<int64_t> om_ptr;
+  const int64_t* d_om_ptr = nullptr;
+  const int8_t* d_side = nullptr;
+  int64_t om_rows = 0, om_width = 0;
   double* hcol_host = nullptr;   // host-mapped (written by k_copy, read after a stream sync)
   double* hcol_map = nullptr;    // its device alias
   // host staging of small tables (kept alive for the async uploads)
@@ -100,6 +105,20 @@ struct Arena {
 };
 
 DevTables slab(const kfbi_ctx* c, int r);
+
+// Ω nodes before each grid row of `width` nodes (rows × width = the full node grid, row-major)
+void omega_rows(kfbi_ctx* c, const std::vector<int8_t>& side, int64_t rows, int64_t width) {
+  if (c->om_rows == rows && (int64_t)c->om_ptr.size() == rows + 1) return;
+  c->om_rows = rows;
+  c->om_width = width;
+  c->om_ptr.assign(rows + 1, 0);
+  for (int64_t r = 0; r < rows; ++r) {
+    int64_t n = 0;
+    const int8_t* row = side.data() + r * width;
+    for (int64_t j = 0; j < width; ++j) n += row[j] != 0;
+    c->om_ptr[r + 1] = c->om_ptr[r] + n;
+  }
+}
 
 void layout(kfbi_ctx* c, Arena& A) {
   Setup& S = c->S;
@@ -135,6 +154,9 @@ void layout(kfbi_ctx* c, Arena& A) {
   T.maxe = S.maxe;
   T.mcr = S.max_col_rows;
   T.side = A.table(S.side);
+  omega_rows(c, S.side, (int64_t)S.N + 1, (int64_t)S.N + 1);
+  c->d_om_ptr = A.table(c->om_ptr);
+  c->d_side = T.side;
   // holes
   auto& hoff = c->hoff; auto& hM = c->hM; auto& hdel = c->hdel; auto& oneh = c->oneh;
   hoff.clear(); hM.clear(); hdel.clear(); oneh.clear();
@@ -196,6 +218,9 @@ void layout3(kfbi_ctx* c, Arena& A) {
   T.st_wn = A.table(S.st_wn); T.neumann = S.neumann ? 1 : 0;
   T.sin_tab = A.table(S.sin_tab); T.dk = A.table(S.dk); T.zr = A.table(S.zr); T.red_a = A.table(S.red_a);
   T.red_b = A.table(S.red_b); T.side = A.table(S.side);
+  omega_rows(c, S.side, ((int64_t)S.N + 1) * ((int64_t)S.N + 1), (int64_t)S.N + 1);
+  c->d_om_ptr = A.table(c->om_ptr);
+  c->d_side = T.side;
   T.tw = A.table(S.tw);
   T.irr_row_perm = A.table(S.irr_row_perm);
   T.max_plane_irr = S.max_plane_irr;
@@ -719,6 +744,32 @@ kfbi_status kfbi_node_mask(const kfbi_ctx* c, int8_t* mask) {
   if (!c || !mask) return KFBI_EINVAL;
   const auto& sd = c->dim == 3 ? c->S3.side : c->S.side;
   std::memcpy(mask, sd.data(), sd.size());
+  return KFBI_OK;
+}
+
+kfbi_status kfbi_omega_count(const kfbi_ctx* c, int64_t* n_omega) {
+  if (!c || !n_omega || c->om_ptr.empty()) return KFBI_EINVAL;
+  *n_omega = c->om_ptr.back();
+  return KFBI_OK;
+}
+
+kfbi_status kfbi_scatter_omega(kfbi_ctx* c, const double* d_compact, double* d_grid, void* stream) {
+  if (!c || !d_compact || !d_grid) return fail(c, KFBI_EINVAL, "null pointer");
+  KFBI_TRY(c)
+  need_ws(c);
+  launch_omega_map(c->om_rows, c->om_width, c->d_side, c->d_om_ptr, d_compact, d_grid, true, pick(c, stream));
+  ck(cudaGetLastError(), "kfbi_scatter_omega launch");
+  KFBI_CATCH(c)
+  return KFBI_OK;
+}
+
+kfbi_status kfbi_gather_omega(kfbi_ctx* c, const double* d_grid, double* d_compact, void* stream) {
+  if (!c || !d_compact || !d_grid) return fail(c, KFBI_EINVAL, "null pointer");
+  KFBI_TRY(c)
+  need_ws(c);
+  launch_omega_map(c->om_rows, c->om_width, c->d_side, c->d_om_ptr, d_grid, d_compact, false, pick(c, stream));
+  ck(cudaGetLastError(), "kfbi_gather_omega launch");
+  KFBI_CATCH(c)
   return KFBI_OK;
 }
 

@@ -25,6 +25,10 @@ void launch_gs_reaction(double* u, double* v, long n, double dt, const GsParams&
 void launch_gs_rhs(const DevTables& T, const double* w, double* fg, double* fq, double* fz, cudaStream_t s);
 void launch_gs_combine(double* w, const double* y, long n, cudaStream_t s);
 void launch_fill(double* x, long n, double val, cudaStream_t s);
+// Ω-compact ↔ full grid (rows × width nodes, row-major; om_ptr = Ω nodes before each row):
+// scatter: grid[p] = compact[rank of p] on Ω nodes, 0 elsewhere; gather: compact[rank of p] = grid[p]
+void launch_omega_map(long rows, long width, const int8_t* side, const int64_t* om_ptr, const double* src,
+                      double* dst, bool scatter, cudaStream_t s);
 // out = base + Σ_q coef[q]·V_q, coef on the device (base may be NULL)
 void launch_combine(long n, const double* base, int k, const double* V, long ldv, const double* coef, double* out,
                     cudaStream_t s);

@@ -17,6 +17,7 @@
 // plus deterministic GMRES vector kernels (Alg. 5).  FP64 on CUDA cores: the
 // path is HBM/latency bound, not a dense contraction (no tensor cores).
 #include <cooperative_groups.h>
+#include <cub/cub.cuh>
 #include <cuda_runtime.h>
 
 #include <cstdio>
@@ -1443,6 +1444,54 @@ void launch_gs_combine(double* w, const double* y, long n, cudaStream_t s) {
   ++g_launches;
   k_gs_combine<<<(int)std::min<long>((n + 255) / 256, 8L * num_sms()), 256, 0, s>>>(w, y, n);
 }
+// one CTA per grid row, 256 consecutive nodes per pass (coalesced): ballot + popc ranks within each
+// warp, the 8 warp counts through shared memory, a running offset along the row
+constexpr int kOmThreads = 256;
+template <bool SCATTER>
+__global__ void __launch_bounds__(kOmThreads) k_omega_map(long rows, long width, const int8_t* __restrict__ side,
+                                                          const int64_t* __restrict__ om_ptr,
+                                                          const double* __restrict__ src, double* __restrict__ dst) {
+  __shared__ int s_w[2][kOmThreads / 32];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const unsigned lt = (1u << lane) - 1u;
+  int par = 0;
+  for (long r = blockIdx.x; r < rows; r += gridDim.x) {
+    const int8_t* m = side + r * width;
+    long run = om_ptr[r];
+    for (long base = 0; base < width; base += kOmThreads) {
+      const long j = base + threadIdx.x;
+      const bool in = j < width && m[j] != 0;
+      const unsigned bal = __ballot_sync(0xffffffffu, in);
+      if (lane == 0) s_w[par][wid] = __popc(bal);
+      __syncthreads();
+      int off = 0, tot = 0;
+#pragma unroll
+      for (int w = 0; w < kOmThreads / 32; ++w) {
+        const int c = s_w[par][w];
+        off += w < wid ? c : 0;
+        tot += c;
+      }
+      const long q = run + off + __popc(bal & lt);
+      if (SCATTER) {
+        if (j < width) dst[r * width + j] = in ? src[q] : 0.0;
+      } else if (in) {
+        dst[q] = src[r * width + j];
+      }
+      run += tot;
+      par ^= 1;   // double-buffered counts: the next pass writes the other slot, one barrier per pass
+    }
+  }
+}
+
+void launch_omega_map(long rows, long width, const int8_t* side, const int64_t* om_ptr, const double* src,
+                      double* dst, bool scatter, cudaStream_t s) {
+  if (rows <= 0) return;
+  const int grid = (int)std::min<long>(rows, 8L * num_sms());
+  ++g_launches;
+  if (scatter) k_omega_map<true><<<grid, kOmThreads, 0, s>>>(rows, width, side, om_ptr, src, dst);
+  else k_omega_map<false><<<grid, kOmThreads, 0, s>>>(rows, width, side, om_ptr, src, dst);
+}
+
 void launch_fill(double* x, long n, double val, cudaStream_t s) {
   if (n <= 0) return;
   ++g_launches;

@@ -22,7 +22,8 @@ EXPORTS = ["kfbi_version", "kfbi_last_error", "kfbi_last_setup_error", "kfbi_get
            "kfbi_workspace_size", "kfbi_set_workspace", "kfbi_sizes", "kfbi_points", "kfbi_node_mask",
            "kfbi_apply", "kfbi_solve", "kfbi_apply_model", "kfbi_destroy", "kfbi_test_fast_solve",
            "kfbi_test_interface_solve", "kfbi_test_setup_dump", "kfbi_profile_apply", "kfbi_launch_count",
-           "kfbi_slab", "kfbi_gray_scott_step", "kfbi_setup_scratch_size", "kfbi_setup_device"]
+           "kfbi_slab", "kfbi_gray_scott_step", "kfbi_setup_scratch_size", "kfbi_setup_device",
+           "kfbi_omega_count", "kfbi_scatter_omega", "kfbi_gather_omega"]
 
 
 class KfbiError(RuntimeError):
@@ -83,6 +84,9 @@ def load(path: str = LIB_PATH):
     lib.kfbi_last_setup_error.restype = C.c_char_p
     lib.kfbi_get_unique_id.argtypes = [vp]
     lib.kfbi_setup.argtypes = [C.POINTER(Grid), C.POINTER(Boundary), C.POINTER(Pde), C.POINTER(Dist), vp, C.POINTER(vp)]
+    lib.kfbi_omega_count.argtypes = [vp, i64p]
+    lib.kfbi_scatter_omega.argtypes = [vp, vp, vp, vp]
+    lib.kfbi_gather_omega.argtypes = [vp, vp, vp, vp]
     lib.kfbi_setup_scratch_size.argtypes = [C.POINTER(Grid), C.POINTER(C.c_size_t)]
     lib.kfbi_setup_device.argtypes = [C.POINTER(Grid), C.POINTER(Boundary), C.POINTER(Pde), C.POINTER(Dist), vp, vp,
                                       C.c_size_t, C.POINTER(vp)]
@@ -253,6 +257,25 @@ class KFBI:
         out = np.zeros((n, self.problem.dim))
         self._check(self.lib.kfbi_points(self.ctx, code, out.ctypes.data_as(C.POINTER(C.c_double))))
         return out
+
+    def omega_count(self):
+        n = C.c_int64()
+        self._check(self.lib.kfbi_omega_count(self.ctx, C.byref(n)))
+        return n.value
+
+    def scatter_omega(self, compact, grid=None, stream=None):
+        """Full (N+1)^d grid from the Ω-node values (0 off Ω) — kfbi_scatter_omega."""
+        t = self.torch
+        grid = t.empty(self.n_nodes, dtype=t.float64, device=self.device) if grid is None else grid
+        self._check(self.lib.kfbi_scatter_omega(self.ctx, _ptr(compact), _ptr(grid), self._stream(stream)))
+        return grid
+
+    def gather_omega(self, grid, compact=None, stream=None):
+        """Ω-node values of a full grid — kfbi_gather_omega."""
+        t = self.torch
+        compact = t.empty(self.omega_count(), dtype=t.float64, device=self.device) if compact is None else compact
+        self._check(self.lib.kfbi_gather_omega(self.ctx, _ptr(grid), _ptr(compact), self._stream(stream)))
+        return compact
 
     def node_mask(self):
         out = np.zeros(self.n_nodes, dtype=np.int8)

@@ -74,3 +74,12 @@ def test_host_setup3d_matches_oracle(lib, prob):
     assert np.array_equal(k.setup_dump(2), grid3d.stencil(st))
     assert np.array_equal(k.node_mask().astype(bool), st.side)
     np.testing.assert_allclose(k.points("ctrl"), st.q_pos, atol=1e-13 * st.h)
+
+
+def test_omega_count_matches_mask():
+    """kfbi_omega_count = number of Ω nodes of the node mask (host setup only, no GPU)."""
+    import workloads as W
+    from paper_2404_15249_b200 import KFBI
+    for prob in (W.C1(64), W.C3(256), W.C4(32)):
+        k = KFBI(prob, workspace=False)
+        assert k.omega_count() == int(k.node_mask().astype(bool).sum())

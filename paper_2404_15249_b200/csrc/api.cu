@@ -225,7 +225,7 @@ void layout3(kfbi_ctx* c, Arena& A) {
   T.irr_row_perm = A.table(S.irr_row_perm);
   T.max_plane_irr = S.max_plane_irr;
   T.irr_row_ptr = A.table(S.irr_row_ptr); T.zrow_id = A.table(S.zrow_id); T.zrow_ptr = A.table(S.zrow_ptr);
-  T.znode_b = A.table(S.znode_b); T.nzrow = (int)S.zrow_id.size();
+  T.znode_b = A.table(S.znode_b); T.nzrow = (int)S.zrow_id.size(); T.zrow_need = A.table(S.zrow_need);
   c->nh = 0;
   c->work = A.take<double>((N - 1) * K);
   c->work2 = A.take<double>((N - 1) * K);
@@ -1030,7 +1030,8 @@ kfbi_status kfbi_apply_model(const kfbi_ctx* c, double* bytes_sweep, double* byt
   if (c->dim == 3) {
     const double N = c->S3.N, U = (N - 1) * (N - 1) * (N - 1), F = (N - 1) * N * N;
     if (bytes_sweep) *bytes_sweep = 8.0 * F;         // k_fwd3s: writes the spectrum (sparse source on chip)
-    if (bytes_inverse) *bytes_inverse = 16.0 * F;    // k_inv3y: reads the spectrum, writes the y-inverse rows
+    // k_inv3y: reads the spectrum, writes the y-inverse rows that hold stencil nodes
+    if (bytes_inverse) *bytes_inverse = 8.0 * F + 8.0 * N * (double)c->S3.zrow_id.size();
     if (unknowns) *unknowns = U;
     return KFBI_OK;
   }

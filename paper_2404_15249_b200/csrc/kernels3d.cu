@@ -391,12 +391,17 @@ __global__ void __launch_bounds__(256, 2) k_inv3y(DevTables3 T, const double* __
   const int rl = threadIdx.x / NTL, tid = threadIdx.x % NTL;
   double2* z = smz + rl * ZS;
   const size_t m0 = (size_t)(l0 + rl) * N;
+  __shared__ uint8_t s_need[N];   // visible after the barrier below
+  for (int a = threadIdx.x; a < N; a += NTHR) s_need[a] = T.zrow_need[(size_t)(i - 1) * N + a];
   load_fixed_row<N>(T, spec, hsep, i, m0, z, tid);
   __syncwarp();
   dst2_core<N>(z, tw, tid);
   __syncthreads();
+  // only the grid rows (i, a) that hold stencil nodes are read by the z-evaluation: the others are
+  // not stored (≈ 80 % of the y-inverse's writes at C5)
   for (int idx = threadIdx.x; idx < N * RPC; idx += NTHR) {
     const int c = idx % RPC, a = idx / RPC;
+    if (!s_need[a]) continue;
     const double v = (a == 0 || l0 + c == 0) ? 0.0 : scale * reinterpret_cast<const double*>(smz + c * ZS)[fpos(a)];
     out[((size_t)(i - 1) * N + a) * N + l0 + c] = v;
   }

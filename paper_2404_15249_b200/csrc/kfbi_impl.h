@@ -169,6 +169,7 @@ struct Setup3 {
   std::vector<int16_t> irr_row_perm; // (N−1)·N: per plane, rows j by descending irregular count
   int max_plane_irr = 0;
   std::vector<int32_t> zrow_id, zrow_ptr, znode_b;   // distinct stencil nodes grouped by grid row
+  std::vector<uint8_t> zrow_need;                    // (N−1)·N: 1 if grid row (i−1)·N + a holds stencil nodes
 };
 void build_setup3(Setup3& S, const kfbi_grid* g, const kfbi_boundary* b, const kfbi_pde* pde);
 
@@ -189,6 +190,7 @@ struct DevTables3 {
   const double *sin_tab, *dk, *zr, *red_a, *red_b;
   const double* tw;   // 2N × (cos, sin)
   const int32_t *irr_row_ptr, *zrow_id, *zrow_ptr, *znode_b;
+  const uint8_t* zrow_need;   // rows the z-evaluation reads (the y-inverse writes only those)
   const int16_t* irr_row_perm;
   int max_plane_irr;
   // slab of this rank (multi-GPU): ADM blocks [b_lo, b_hi), x-planes [i_lo, i_hi],

@@ -362,6 +362,8 @@ void build_setup3(Setup3& S, const kfbi_grid* g, const kfbi_boundary* b, const k
       S.znode_b.push_back((int32_t)(nodes[e] % N));
     }
     S.zrow_ptr.push_back((int32_t)nodes.size());
+    S.zrow_need.assign((size_t)(N - 1) * N, 0);
+    for (int32_t r : S.zrow_id) S.zrow_need[r] = 1;
   }
 
   // fast-solver tables: modes m = ll·N + kk (DST along z → ll, along y → kk), tridiagonal along x

@@ -222,7 +222,7 @@ void layout3(kfbi_ctx* c, Arena& A) {
   c->d_om_ptr = A.table(c->om_ptr);
   c->d_side = T.side;
   T.tw = A.table(S.tw);
-  T.irr_row_perm = A.table(S.irr_row_perm);
+  T.irr_row_perm = A.table(S.irr_row_perm); T.irr_row_nheavy = A.table(S.irr_row_nheavy);
   T.max_plane_irr = S.max_plane_irr;
   T.irr_row_ptr = A.table(S.irr_row_ptr); T.zrow_id = A.table(S.zrow_id); T.zrow_ptr = A.table(S.zrow_ptr);
   T.znode_b = A.table(S.znode_b); T.nzrow = (int)S.zrow_id.size(); T.zrow_need = A.table(S.zrow_need);

@@ -322,41 +322,70 @@ __global__ void __launch_bounds__(256, 2) k_fwd3s(DevTables3 T, const double* __
   for (int grp = blockIdx.x * kFwdGroups; grp < (blockIdx.x + 1) * kFwdGroups && grp * RPC < N; ++grp) {
   const int tq0 = grp * (RPC / 4);
   if (grp != blockIdx.x * kFwdGroups) __syncthreads();   // the previous group's rows have been written out
-  for (int it = threadIdx.x; it < N * NG; it += NTHR) {
-    const int rr = it % N, cg = it / N, k = rr / NTHR, pos = rr % NTHR;
-    const int a = T.irr_row_perm[(size_t)(i - 1) * N + k * NTHR + ((k & 1) ? NTHR - 1 - pos : pos)];
-    double g[CPT];
+  // G rows: entries e of grid row a (sorted by count) → CPT mode sums.  Rows with more than
+  // kHeavyRow entries (the first H of the plane's order) are split over 8 lanes and summed by a fixed
+  // xor tree; the rest take one thread each.  Keeps the longest per-thread chain near the mean.
+  auto accumulate = [&](int e, int t0, double (&g)[CPT]) {
+    const double v = s_val[e];
+    const int b = s_b[e];
+    const double sg1 = (b & 1) ? v : -v;                                   // (−1)^{b+1} v
+    const double sg2 = ((b & 3) == 0 || (b & 3) == 3) ? -v : v, sg3 = (b & 3) <= 1 ? v : -v;
+    const int r0 = (b * t0) & (2 * N - 1);
+    double2 w = make_double2(sin_lookup(s_q, (r0 + N / 2) & (2 * N - 1), N), sin_lookup(s_q, r0, N));
+    const double2 d = make_double2(sin_lookup(s_q, (b + N / 2) & (2 * N - 1), N), sin_lookup(s_q, b, N));
 #pragma unroll
-    for (int c = 0; c < CPT; ++c) g[c] = 0.0;
-    const int e1 = s_ptr[a + 1];
-    const int t0 = tq0 + cg * QPI;
-    for (int e = s_ptr[a]; e < e1; ++e) {
-      const double v = s_val[e];
-      const int b = s_b[e];
-      const double sg1 = (b & 1) ? v : -v;                                   // (−1)^{b+1} v
-      const double sg2 = ((b & 3) == 0 || (b & 3) == 3) ? -v : v, sg3 = (b & 3) <= 1 ? v : -v;
-      const int r0 = (b * t0) & (2 * N - 1);
-      double2 w = make_double2(sin_lookup(s_q, (r0 + N / 2) & (2 * N - 1), N), sin_lookup(s_q, r0, N));
-      const double2 d = make_double2(sin_lookup(s_q, (b + N / 2) & (2 * N - 1), N), sin_lookup(s_q, b, N));
-#pragma unroll
-      for (int u = 0; u < QPI; ++u) {
-        const double sv = w.y, cv = w.x, A = (b & 1) ? cv : sv;
-        if (t0 + u == 0) {   // special quad: modes 0 (unused), N/2, N/4, 3N/4
-          g[4 * u + 1] = fma(v, sin_lookup(s_q, (b * (N / 2)) & (2 * N - 1), N), g[4 * u + 1]);
-          g[4 * u + 2] = fma(v, sin_lookup(s_q, (b * (N / 4)) & (2 * N - 1), N), g[4 * u + 2]);
-          g[4 * u + 3] = fma(v, sin_lookup(s_q, (b * (3 * N / 4)) & (2 * N - 1), N), g[4 * u + 3]);
-        } else {
-          g[4 * u + 0] = fma(v, sv, g[4 * u + 0]);
-          g[4 * u + 1] = fma(sg1, sv, g[4 * u + 1]);
-          g[4 * u + 2] = fma(sg2, A, g[4 * u + 2]);
-          g[4 * u + 3] = fma(sg3, A, g[4 * u + 3]);
-        }
-        if (u + 1 < QPI) w = cmul(w, d);
+    for (int u = 0; u < QPI; ++u) {
+      const double sv = w.y, cv = w.x, A = (b & 1) ? cv : sv;
+      if (t0 + u == 0) {   // special quad: modes 0 (unused), N/2, N/4, 3N/4
+        g[4 * u + 1] = fma(v, sin_lookup(s_q, (b * (N / 2)) & (2 * N - 1), N), g[4 * u + 1]);
+        g[4 * u + 2] = fma(v, sin_lookup(s_q, (b * (N / 4)) & (2 * N - 1), N), g[4 * u + 2]);
+        g[4 * u + 3] = fma(v, sin_lookup(s_q, (b * (3 * N / 4)) & (2 * N - 1), N), g[4 * u + 3]);
+      } else {
+        g[4 * u + 0] = fma(v, sv, g[4 * u + 0]);
+        g[4 * u + 1] = fma(sg1, sv, g[4 * u + 1]);
+        g[4 * u + 2] = fma(sg2, A, g[4 * u + 2]);
+        g[4 * u + 3] = fma(sg3, A, g[4 * u + 3]);
       }
+      if (u + 1 < QPI) w = cmul(w, d);
     }
+  };
+  auto store = [&](int a, int cg, const double (&g)[CPT]) {
     const int off = 2 * zpad(a >> 1) + (a & 1);
 #pragma unroll
     for (int c = 0; c < CPT; ++c) reinterpret_cast<double*>(smz + (cg * CPT + c) * ZS)[off] = a ? g[c] : 0.0;
+  };
+  const int16_t* perm = T.irr_row_perm + (size_t)(i - 1) * N;
+  const int H = T.irr_row_nheavy[i - 1];
+  {   // heavy rows: 4 per warp per round, warp-uniform trip count (all lanes take part in the shuffles)
+    const int lane = threadIdx.x & 31, sub = lane & 7;
+    const int nitem = H * NG;
+    for (int base = (threadIdx.x >> 5) * 4; base < nitem; base += NTHR / 8) {
+      const int hi = base + (lane >> 3);
+      const bool act = hi < nitem;
+      const int cg = act ? hi / H : 0, a = act ? perm[hi % H] : 0;
+      double g[CPT];
+#pragma unroll
+      for (int c = 0; c < CPT; ++c) g[c] = 0.0;
+      if (act) {
+        const int e1 = s_ptr[a + 1], t0 = tq0 + cg * QPI;
+        for (int e = s_ptr[a] + sub; e < e1; e += 8) accumulate(e, t0, g);
+      }
+#pragma unroll
+      for (int o = 4; o > 0; o >>= 1)
+#pragma unroll
+        for (int c = 0; c < CPT; ++c) g[c] += __shfl_xor_sync(0xffffffffu, g[c], o);
+      if (act && sub == 0) store(a, cg, g);
+    }
+  }
+  const int NL = N - H;   // light rows (≤ kHeavyRow entries, incl. the empty ones): one thread each
+  for (int it = threadIdx.x; it < NL * NG; it += NTHR) {
+    const int cg = it / NL, a = perm[H + it % NL];
+    double g[CPT];
+#pragma unroll
+    for (int c = 0; c < CPT; ++c) g[c] = 0.0;
+    const int e1 = s_ptr[a + 1], t0 = tq0 + cg * QPI;
+    for (int e = s_ptr[a]; e < e1; ++e) accumulate(e, t0, g);
+    store(a, cg, g);
   }
   const int rl = threadIdx.x / NTL, tid = threadIdx.x % NTL;
   const double2 wa = __ldg(tw + 2 * tid), wb = __ldg(tw + 2 * tid + 1);   // in flight across the barrier

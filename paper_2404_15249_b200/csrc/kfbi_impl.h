@@ -25,6 +25,8 @@ constexpr int BL2 = 32;
 constexpr int LB2 = BL2 - 1;
 // most stencil rows in one k_inv_sparse work item (longer columns are split by setup)
 constexpr int kMaxColRows = 512;
+// 3D forward: grid rows with more irregular entries than this are split over 8 lanes
+constexpr int kHeavyRow = 6;
 
 // Position of sine mode k (0 ≤ k < N) in the 2D spectral arrays (see setup2d.cpp).
 #ifdef __CUDACC__
@@ -167,6 +169,7 @@ struct Setup3 {
   std::vector<double> tw;            // 2N complex: (cos, sin)(π m / N), m = 0..2N−1
   std::vector<int32_t> irr_row_ptr;  // (N−1)·N + 1: irregular nodes of grid row (i−1)·N + j
   std::vector<int16_t> irr_row_perm; // (N−1)·N: per plane, rows j by descending irregular count
+  std::vector<int32_t> irr_row_nheavy;   // N−1: rows of the plane with more than kHeavyRow entries
   int max_plane_irr = 0;
   std::vector<int32_t> zrow_id, zrow_ptr, znode_b;   // distinct stencil nodes grouped by grid row
   std::vector<uint8_t> zrow_need;                    // (N−1)·N: 1 if grid row (i−1)·N + a holds stencil nodes
@@ -192,6 +195,7 @@ struct DevTables3 {
   const int32_t *irr_row_ptr, *zrow_id, *zrow_ptr, *znode_b;
   const uint8_t* zrow_need;   // rows the z-evaluation reads (the y-inverse writes only those)
   const int16_t* irr_row_perm;
+  const int32_t* irr_row_nheavy;
   int max_plane_irr;
   // slab of this rank (multi-GPU): ADM blocks [b_lo, b_hi), x-planes [i_lo, i_hi],
   // stencil-node rows [w_lo, w_hi) of the zrow list; the whole problem when world = 1

@@ -346,6 +346,15 @@ void build_setup3(Setup3& S, const kfbi_grid* g, const kfbi_boundary* b, const k
       const int32_t* rp = &S.irr_row_ptr[(size_t)i * N];
       std::stable_sort(pr, pr + N, [&](int16_t x, int16_t y) { return rp[x + 1] - rp[x] > rp[y + 1] - rp[y]; });
     }
+    // rows with more than kHeavyRow entries come first in each plane's order; the forward kernel
+    // splits each of them over 8 lanes
+    S.irr_row_nheavy.assign(N - 1, 0);
+    for (int i = 0; i < N - 1; ++i) {
+      const int32_t* rp = &S.irr_row_ptr[(size_t)i * N];
+      int h = 0;
+      for (int a = 0; a < N; ++a) h += rp[a + 1] - rp[a] > kHeavyRow;
+      S.irr_row_nheavy[i] = h;
+    }
     std::vector<int64_t> nodes(10 * (size_t)nq);
     for (size_t e = 0; e < 10 * (size_t)nq; ++e)
       nodes[e] = (int64_t)(S.st_nodes_ij[3 * e] - 1) * N * N + (int64_t)S.st_nodes_ij[3 * e + 1] * N +

@@ -26,7 +26,7 @@ constexpr int LB2 = BL2 - 1;
 // most stencil rows in one k_inv_sparse work item (longer columns are split by setup)
 constexpr int kMaxColRows = 512;
 // 3D forward: grid rows with more irregular entries than this are split over 8 lanes
-constexpr int kHeavyRow = 6;
+constexpr int kHeavyRow = 9;
 
 // Position of sine mode k (0 ≤ k < N) in the 2D spectral arrays (see setup2d.cpp).
 #ifdef __CUDACC__

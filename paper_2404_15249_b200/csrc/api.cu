@@ -402,6 +402,16 @@ void final_field2(kfbi_ctx* c, const double* phi, const double* fgrid, const dou
       D.blo[h] = std::max(1, (int)std::floor((c->bump.cx[h] - c->bump.rad[h] - T.lo) / T.h) - 1);
       D.bhi[h] = std::min(T.N - 1, (int)std::ceil((c->bump.cx[h] + c->bump.rad[h] - T.lo) / T.h) + 1);
     }
+    if (fgrid && c->world == 1) {
+      // spec_f is not needed after the final field: add a_h ŵ_h into it on the bumps' support columns
+      // only (in place, k_combine's fma order), then a base-only dense sweep
+      for (int h = 0; h < c->nh && h < 4; ++h) {
+        const size_t off = (size_t)(D.blo[h] - 1) * T.N;
+        const long n = (long)(D.bhi[h] - D.blo[h] + 1) * T.N;
+        launch_axpy_dcoef(n, c->ahole + h, c->spec_bump + (size_t)h * D.ldb + off, c->spec_f + off, s);
+      }
+      D.nb = 0;
+    }
   } else {
     dst_forward2(c, fgrid, true, bp, c->spec_f, s);
     D.base = c->spec_f;

@@ -25,6 +25,8 @@ void launch_gs_reaction(double* u, double* v, long n, double dt, const GsParams&
 void launch_gs_rhs(const DevTables& T, const double* w, double* fg, double* fq, double* fz, cudaStream_t s);
 void launch_gs_combine(double* w, const double* y, long n, cudaStream_t s);
 void launch_fill(double* x, long n, double val, cudaStream_t s);
+// y += (*coef) · x over n elements (coef on the device)
+void launch_axpy_dcoef(long n, const double* coef, const double* x, double* y, cudaStream_t s);
 // Ω-compact ↔ full grid (rows × width nodes, row-major; om_ptr = Ω nodes before each row):
 // scatter: grid[p] = compact[rank of p] on Ω nodes, 0 elsewhere; gather: compact[rank of p] = grid[p]
 void launch_omega_map(long rows, long width, const int8_t* side, const int64_t* om_ptr, const double* src,

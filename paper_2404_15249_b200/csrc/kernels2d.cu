@@ -1498,6 +1498,17 @@ void launch_fill(double* x, long n, double val, cudaStream_t s) {
   k_fill<<<(int)std::min<long>((n + 255) / 256, 8L * num_sms()), 256, 0, s>>>(x, n, val);
 }
 
+__global__ void k_axpy_dcoef(long n, const double* __restrict__ coef, const double* __restrict__ x,
+                             double* __restrict__ y) {
+  const double a = *coef;
+  for (long i = (long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long)gridDim.x * blockDim.x)
+    y[i] = fma(a, __ldcs(x + i), y[i]);
+}
+void launch_axpy_dcoef(long n, const double* coef, const double* x, double* y, cudaStream_t s) {
+  if (n <= 0) return;
+  ++g_launches;
+  k_axpy_dcoef<<<(int)std::min<long>((n + 255) / 256, 8L * num_sms()), 256, 0, s>>>(n, coef, x, y);
+}
 void launch_combine(long n, const double* base, int k, const double* V, long ldv, const double* coef, double* out,
                     cudaStream_t s) {
   ++g_launches;

@@ -4,6 +4,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <climits>
 #include <chrono>
 #include <cmath>
 #include <cstring>
@@ -71,7 +72,9 @@ struct kfbi_ctx {
   bool spec_f_valid = false;
   // Ω-compact transfers: Ω nodes per grid row (prefix), the full-grid mask on the device
   std::vector<int64_t> om_ptr;
+  std::vector<int32_t> om_seg;   // Ω nodes before each 32-node segment of each row
   const int64_t* d_om_ptr = nullptr;
+  const int32_t* d_om_seg = nullptr;
   const int8_t* d_side = nullptr;
   int64_t om_rows = 0, om_width = 0;
   double* hcol_host = nullptr;   // host-mapped (written by k_copy, read after a stream sync)
@@ -112,12 +115,18 @@ void omega_rows(kfbi_ctx* c, const std::vector<int8_t>& side, int64_t rows, int6
   c->om_rows = rows;
   c->om_width = width;
   c->om_ptr.assign(rows + 1, 0);
+  const int64_t nseg = (width + 31) / 32;
+  c->om_seg.assign(rows * nseg, 0);
   for (int64_t r = 0; r < rows; ++r) {
     int64_t n = 0;
     const int8_t* row = side.data() + r * width;
-    for (int64_t j = 0; j < width; ++j) n += row[j] != 0;
+    for (int64_t j = 0; j < width; ++j) {
+      if ((j & 31) == 0) c->om_seg[r * nseg + (j >> 5)] = (int32_t)(c->om_ptr[r] + n);
+      n += row[j] != 0;
+    }
     c->om_ptr[r + 1] = c->om_ptr[r] + n;
   }
+  if (c->om_ptr.back() > INT32_MAX) throw ArgError("too many Ω nodes for the compact transfers");
 }
 
 void layout(kfbi_ctx* c, Arena& A) {
@@ -156,6 +165,7 @@ void layout(kfbi_ctx* c, Arena& A) {
   T.side = A.table(S.side);
   omega_rows(c, S.side, (int64_t)S.N + 1, (int64_t)S.N + 1);
   c->d_om_ptr = A.table(c->om_ptr);
+  c->d_om_seg = A.table(c->om_seg);
   c->d_side = T.side;
   // holes
   auto& hoff = c->hoff; auto& hM = c->hM; auto& hdel = c->hdel; auto& oneh = c->oneh;
@@ -220,6 +230,7 @@ void layout3(kfbi_ctx* c, Arena& A) {
   T.red_b = A.table(S.red_b); T.side = A.table(S.side);
   omega_rows(c, S.side, ((int64_t)S.N + 1) * ((int64_t)S.N + 1), (int64_t)S.N + 1);
   c->d_om_ptr = A.table(c->om_ptr);
+  c->d_om_seg = A.table(c->om_seg);
   c->d_side = T.side;
   T.tw = A.table(S.tw);
   T.irr_row_perm = A.table(S.irr_row_perm); T.irr_row_nheavy = A.table(S.irr_row_nheavy);
@@ -767,7 +778,7 @@ kfbi_status kfbi_scatter_omega(kfbi_ctx* c, const double* d_compact, double* d_g
   if (!c || !d_compact || !d_grid) return fail(c, KFBI_EINVAL, "null pointer");
   KFBI_TRY(c)
   need_ws(c);
-  launch_omega_map(c->om_rows, c->om_width, c->d_side, c->d_om_ptr, d_compact, d_grid, true, pick(c, stream));
+  launch_omega_map(c->om_rows, c->om_width, c->d_side, c->d_om_seg, d_compact, d_grid, true, pick(c, stream));
   ck(cudaGetLastError(), "kfbi_scatter_omega launch");
   KFBI_CATCH(c)
   return KFBI_OK;
@@ -777,7 +788,7 @@ kfbi_status kfbi_gather_omega(kfbi_ctx* c, const double* d_grid, double* d_compa
   if (!c || !d_compact || !d_grid) return fail(c, KFBI_EINVAL, "null pointer");
   KFBI_TRY(c)
   need_ws(c);
-  launch_omega_map(c->om_rows, c->om_width, c->d_side, c->d_om_ptr, d_grid, d_compact, false, pick(c, stream));
+  launch_omega_map(c->om_rows, c->om_width, c->d_side, c->d_om_seg, d_grid, d_compact, false, pick(c, stream));
   ck(cudaGetLastError(), "kfbi_gather_omega launch");
   KFBI_CATCH(c)
   return KFBI_OK;

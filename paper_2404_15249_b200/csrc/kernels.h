@@ -27,9 +27,10 @@ void launch_gs_combine(double* w, const double* y, long n, cudaStream_t s);
 void launch_fill(double* x, long n, double val, cudaStream_t s);
 // y += (*coef) · x over n elements (coef on the device)
 void launch_axpy_dcoef(long n, const double* coef, const double* x, double* y, cudaStream_t s);
-// Ω-compact ↔ full grid (rows × width nodes, row-major; om_ptr = Ω nodes before each row):
-// scatter: grid[p] = compact[rank of p] on Ω nodes, 0 elsewhere; gather: compact[rank of p] = grid[p]
-void launch_omega_map(long rows, long width, const int8_t* side, const int64_t* om_ptr, const double* src,
+// Ω-compact ↔ full grid (rows × width nodes, row-major; om_seg = Ω nodes before each 32-node
+// segment of each row): scatter: grid[p] = compact[rank of p] on Ω nodes, 0 elsewhere;
+// gather: compact[rank of p] = grid[p]
+void launch_omega_map(long rows, long width, const int8_t* side, const int32_t* om_seg, const double* src,
                       double* dst, bool scatter, cudaStream_t s);
 // out = base + Σ_q coef[q]·V_q, coef on the device (base may be NULL)
 void launch_combine(long n, const double* base, int k, const double* V, long ldv, const double* coef, double* out,

@@ -566,8 +566,18 @@ __global__ void __launch_bounds__(kInvThreads, 2) k_inv_sparse(DevTables T, cons
     const double v = tab[idx + (idx >> 4)];
     return (r & N) ? -v : v;
   };
-  // persistent over the owned stencil columns: the sine table is staged once per CTA
-  for (int b = T.o_lo + blockIdx.x; b < T.o_hi; b += gridDim.x) {
+  // persistent over the owned stencil columns: the sine table is staged once per CTA.  Items are
+  // taken in descending row count (setup order `ocol_order`), dealt in snake order over the CTAs:
+  // a few columns along which Γ runs hold up to ~200 rows against a mean of 12, and a plain
+  // round-robin left the CTAs that drew them as the kernel's tail.
+  const int G = gridDim.x, nit = T.nocol;
+  auto item = [&](int r) {   // item of round r for this CTA (−1: none)
+    const int kk = r * G + ((r & 1) ? G - 1 - (int)blockIdx.x : (int)blockIdx.x);
+    return kk < nit ? T.ocol_order[kk] : -1;
+  };
+  for (int rnd = 0; rnd * G < nit; ++rnd) {
+  const int b = item(rnd);
+  if (b < T.o_lo || b >= T.o_hi) continue;   // CTA-uniform
   __syncthreads();
   const int i = T.ocol[b];
   const int u0 = T.ocol_ptr[b], u1 = T.ocol_ptr[b + 1];
@@ -582,8 +592,8 @@ __global__ void __launch_bounds__(kInvThreads, 2) k_inv_sparse(DevTables T, cons
   const double* zl = T.zr + (size_t)(sep ? 0 : LB - rr) * N;     // Z_L[p] = Z_R[LB−1−p], p = rr − 1
   const double* zrr = T.zr + (size_t)(sep ? 0 : rr - 1) * N;
   {   // warm L2 with the next column's spectral row while this one is evaluated
-    const int bn = b + gridDim.x;
-    if (bn < T.o_hi) {
+    const int bn = item(rnd + 1);
+    if (bn >= T.o_lo && bn < T.o_hi) {
       const int in = T.ocol[bn], qn = in / BL, rn = in - qn * BL;
       const double* nrow = rn == 0 ? hsep + (size_t)(qn - 1) * N : spec + (size_t)(in - 1) * N;
       for (int o = threadIdx.x * 16; o < N; o += B * 16)

@@ -506,6 +506,11 @@ void build_setup(Setup& S, const kfbi_grid* g, const kfbi_boundary* b, const kfb
     for (size_t c = 0; c + 1 < S.ocol_ptr.size(); ++c) {
       S.max_col_rows = std::max(S.max_col_rows, S.ocol_ptr[c + 1] - S.ocol_ptr[c]);
     }
+    S.ocol_order.resize(S.ocol.size());
+    for (size_t c = 0; c < S.ocol.size(); ++c) S.ocol_order[c] = (int32_t)c;
+    std::stable_sort(S.ocol_order.begin(), S.ocol_order.end(), [&](int32_t x, int32_t y) {
+      return S.ocol_ptr[x + 1] - S.ocol_ptr[x] > S.ocol_ptr[y + 1] - S.ocol_ptr[y];
+    });
   }
 
   setup_tick("spline filters (reading R10; SUR");

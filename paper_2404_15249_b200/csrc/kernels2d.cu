@@ -189,7 +189,14 @@ __global__ void __launch_bounds__(kSweepThreads, 2) k_sweep(DevTables T, const d
   const double h2 = T.h * T.h;
   const int slot = threadIdx.x >> 1;
   double* Rs = R + slot;           // Rs[(4c + u)·kQuads], u: 0 A_o, 1 B_o, 2 A_e, 3 B_e
-  for (int g = T.g_lo + blockIdx.x / nch; g < T.g_hi; g += G) {
+  // blocks in descending count of sparse entries (setup order `blk_order`), snake-dealt over the
+  // G block groups so that the groups that draw the blocks where Γ runs along x are not the tail
+  const int grp = blockIdx.x / nch;
+  for (int rnd = 0; rnd * G < T.P; ++rnd) {
+  const int kk = rnd * G + ((rnd & 1) ? G - 1 - grp : grp);
+  if (kk >= T.P) continue;
+  const int g = T.blk_order[kk];
+  if (g < T.g_lo || g >= T.g_hi) continue;   // CTA-uniform
     const int c0 = BL * g + 1;
     const int e0 = T.col_ptr[c0];
     const int ncol = g < T.P - 1 ? BL : LB;   // block columns + separator column

@@ -632,12 +632,18 @@ void build_setup(Setup& S, const kfbi_grid* g, const kfbi_boundary* b, const kfb
     perm(S.red2_a, 1, 0.0);
     perm(S.red2_b, 1, 1.0);
   }
-  // largest number of sparse corrections staged by one sweep work item (block + separator)
+  // largest number of sparse corrections staged by one sweep work item (block + separator), and the
+  // blocks by descending count (the sweep's work order)
   S.maxe = 1;
+  std::vector<int> bcnt(P);
   for (int gg = 0; gg < P; ++gg) {
     const int last = std::min(BL * gg + BL, N - 1);
-    S.maxe = std::max(S.maxe, S.col_ptr[last + 1] - S.col_ptr[BL * gg + 1]);
+    bcnt[gg] = S.col_ptr[last + 1] - S.col_ptr[BL * gg + 1];
+    S.maxe = std::max(S.maxe, bcnt[gg]);
   }
+  S.blk_order.resize(P);
+  for (int gg = 0; gg < P; ++gg) S.blk_order[gg] = gg;
+  std::stable_sort(S.blk_order.begin(), S.blk_order.end(), [&](int32_t x, int32_t y) { return bcnt[x] > bcnt[y]; });
   S.holes.clear();
   if (S.kappa == 0.0)
     for (int c = 0; c < nc; ++c)

@@ -99,3 +99,22 @@ def test_device_setup_errors():
     assert st == K.ENOMEM and not ctx.value
     g3 = K.Grid(3, (C.c_double * 3)(-1.2, -1.2, -1.2), (C.c_double * 3)(1.2, 1.2, 1.2), (C.c_int32 * 3)(64, 64, 64))
     assert lib.kfbi_setup_scratch_size(C.byref(g3), C.byref(need)) == K.EUNSUPPORTED
+
+
+@pytest.mark.parametrize("make,n", [(W.C1, 64), (W.C2, 1024), (W.C3, 1024)])
+def test_device_setup_matches_oracle(make, n):
+    """The device phases against the oracle's own Procedure 1 (oracle/grid.py), as the host setup is
+    in tests/test_abi.py: integer lists bit for bit, intersection points to 1e-13·h."""
+    from oracle import grid
+    from paper_2404_15249_b200 import KFBI
+    prob = make(n)
+    k = KFBI(prob, device_setup=True)
+    st = grid.build(prob)
+    assert k.M == st.M and k.nq == st.q_xi.size
+    assert np.array_equal(k.setup_dump(0), np.argwhere(st.irregular))
+    assert np.array_equal(k.setup_dump(1), np.stack([st.q_axis, st.q_i, st.q_j], -1))
+    assert np.array_equal(k.setup_dump(2), grid.stencil(st))
+    assert np.array_equal(k.node_mask().astype(bool), st.side)
+    px = np.where(st.q_axis == 0, st.q_xi, st.x[st.q_i])
+    py = np.where(st.q_axis == 1, st.q_xi, st.x[st.q_j])
+    np.testing.assert_allclose(k.points("isect"), np.stack([px, py], -1), atol=1e-13 * st.h)

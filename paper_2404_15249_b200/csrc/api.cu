@@ -415,7 +415,7 @@ void final_field2(kfbi_ctx* c, const double* phi, const double* fgrid, const dou
     }
     if (fgrid && c->world == 1) {
       // spec_f is not needed after the final field: add a_h ŵ_h into it on the bumps' support columns
-      // only (in place, k_combine's fma order), then a base-only dense sweep
+      // only (in place, one fma per bump in order), then a base-only dense sweep
       for (int h = 0; h < c->nh && h < 4; ++h) {
         const size_t off = (size_t)(D.blo[h] - 1) * T.N;
         const long n = (long)(D.bhi[h] - D.blo[h] + 1) * T.N;

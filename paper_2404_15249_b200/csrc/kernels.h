@@ -32,9 +32,7 @@ void launch_axpy_dcoef(long n, const double* coef, const double* x, double* y, c
 // gather: compact[rank of p] = grid[p]
 void launch_omega_map(long rows, long width, const int8_t* side, const int32_t* om_seg, const double* src,
                       double* dst, bool scatter, cudaStream_t s);
-// out = base + Σ_q coef[q]·V_q, coef on the device (base may be NULL)
-void launch_combine(long n, const double* base, int k, const double* V, long ldv, const double* coef, double* out,
-                    cudaStream_t s);
+
 
 struct BumpParams {
   int nh;

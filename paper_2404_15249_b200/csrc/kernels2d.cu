@@ -297,7 +297,7 @@ __global__ void __launch_bounds__(kSweepThreads, 2) k_sweep(DevTables T, const d
       const double A = Rs[(4 * c + w) * kQuads], E = Rs[(4 * c + 2 + w) * kQuads];
       r1 = w ? A - E : A + E;
       r2 = w ? A + E : A - E;
-      if (DENSE) {   // f̂ = base + Σ a_h bump_h, the fma order of k_combine
+      if (DENSE) {   // f̂ = base + Σ a_h bump_h, one fma per bump in order
         const size_t off = (size_t)(c0 + c - 1) * N + p1;
         double2 d = DENSE == 1 || D.base ? *reinterpret_cast<const double2*>(D.base + off) : make_double2(0.0, 0.0);
         if (DENSE == 2) {
@@ -840,14 +840,6 @@ __global__ void k_gs_combine(double* __restrict__ w, const double* __restrict__ 
     w[i] = 2.0 * y[i] - w[i];   // Crank–Nicolson: (I − aΔ)^{-1}(I + aΔ) w = 2y − w
 }
 // out = base + Σ_q coef[q] · V_q (coefficients in device memory; base may be NULL)
-__global__ void k_combine(long n, const double* __restrict__ base, int k, const double* __restrict__ V, long ldv,
-                          const double* __restrict__ coef, double* __restrict__ out) {
-  for (long i = (long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long)gridDim.x * blockDim.x) {
-    double acc = base ? base[i] : 0.0;
-    for (int q = 0; q < k; ++q) acc = fma(coef[q], V[(size_t)q * ldv + i], acc);
-    out[i] = acc;
-  }
-}
 __global__ void k_fill(double* __restrict__ x, long n, double val) {
   for (long i = (long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long)gridDim.x * blockDim.x) x[i] = val;
 }
@@ -1511,11 +1503,6 @@ void launch_axpy_dcoef(long n, const double* coef, const double* x, double* y, c
   if (n <= 0) return;
   ++g_launches;
   k_axpy_dcoef<<<(int)std::min<long>((n + 255) / 256, 8L * num_sms()), 256, 0, s>>>(n, coef, x, y);
-}
-void launch_combine(long n, const double* base, int k, const double* V, long ldv, const double* coef, double* out,
-                    cudaStream_t s) {
-  ++g_launches;
-  k_combine<<<(int)std::min<long>((n + 255) / 256, 8L * num_sms()), 256, 0, s>>>(n, base, k, V, ldv, coef, out);
 }
 }  // namespace kfbi
 

@@ -23,8 +23,9 @@ constexpr int LB = BL - 1;
 // level-2 blocks of BL2−1 separators around level-2 separators (nested arrowhead).
 constexpr int BL2 = 32;
 constexpr int LB2 = BL2 - 1;
-// most stencil rows in one k_inv_sparse work item (longer columns are split by setup)
-constexpr int kMaxColRows = 512;
+// most stencil rows in one k_inv_sparse work item: longer columns are split by setup (load balance:
+// rows per column reach ~200 at C3 and the cap of a few hundred on the 8192² star, mean 12)
+constexpr int kMaxColRows = 64;
 // 3D forward: grid rows with more irregular entries than this are split over 8 lanes
 constexpr int kHeavyRow = 9;
 

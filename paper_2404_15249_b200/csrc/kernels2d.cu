@@ -137,6 +137,7 @@ __global__ void k_correct(DevTables T, const double* __restrict__ phi, const dou
 // Outputs: z at the block rows, B[g] = z_g[1], A[g] = h² f̂_sep,g − z_g[L] (reduced-system
 // right-hand side pieces).
 constexpr int kSweepThreads = 256;
+constexpr int kEntCap = 768;                 // sparse entries staged per pass (k_sweep shared memory)
 constexpr int kQuads = kSweepThreads / 2;   // 128 quads {t, N−t, N/2−t, N/2+t} per CTA chunk
 constexpr int kRotSteps = 4;                 // quads per phase-1 item (t = base + kRotStride·s)
 constexpr int kRotStride = kQuads / kRotSteps;  // 32
@@ -160,8 +161,9 @@ __global__ void __launch_bounds__(kSweepThreads, 2) k_sweep(DevTables T, const d
   double* R = sm;                                            // [4·BL sums][kQuads]
   double4* ent = reinterpret_cast<double4*>(R + (size_t)BL * 4 * kQuads);   // (c, j, cos Δ, sin Δ)
   // ent = (c, c·sin(πj/2) (odd j) or c·cos(πj/2) (even j), cos Δ, sin Δ), Δ = π·kRotStride·j/N
-  int* ent_j = reinterpret_cast<int*>(ent + T.maxe);
-  double2* th = reinterpret_cast<double2*>(ent_j + ((T.maxe + 3) & ~3));   // e^{iπ 64k/N}
+  const int ecap = T.maxe < kEntCap ? T.maxe : kEntCap;     // entries staged per pass
+  int* ent_j = reinterpret_cast<int*>(ent + ecap);
+  double2* th = reinterpret_cast<double2*>(ent_j + ((ecap + 3) & ~3));   // e^{iπ 64k/N}
   double2* tl = th + 2 * N / 64;                              // e^{iπ l/N}, l < 64
   int* s_cnt = reinterpret_cast<int*>(tl + 64);               // per-column [start, mid, end)
   build_eipi(T.sin_tab, N, th, tl);
@@ -201,21 +203,26 @@ __global__ void __launch_bounds__(kSweepThreads, 2) k_sweep(DevTables T, const d
     const int e0 = T.col_ptr[c0];
     const int ncol = g < T.P - 1 ? BL : LB;   // block columns + separator column
     const int e1 = cval ? T.col_ptr[c0 + ncol] : e0;
+    // the block's entries are staged kEntCap at a time (a block where Γ runs along x holds up to
+    // ~1,700 on the 8192² star: staging them all would leave one CTA per SM); later passes add into R
+    for (int cb = e0, pass = 0; pass == 0 || cb < e1; cb += kEntCap, ++pass) {
+    const int ce = e1 - cb < kEntCap ? e1 : cb + kEntCap;
     __syncthreads();
-    for (int e = e0 + threadIdx.x; e < e1; e += B) {
+    for (int e = cb + threadIdx.x; e < ce; e += B) {
       const int j = T.irr_j[e];
       const int rd = (j * kRotStride) & m2;
       const double c = cval[e];
       // odd j: sin(πj/2) = ±1; even j: cos(πj/2) = ±1
       const bool neg = (j >> 1) & 1;
-      ent[e - e0] = make_double4(c, neg ? -c : c, sin_lookup(T.sin_tab, (rd + half) & m2, N), sin_lookup(T.sin_tab, rd, N));
-      ent_j[e - e0] = j;
+      ent[e - cb] = make_double4(c, neg ? -c : c, sin_lookup(T.sin_tab, (rd + half) & m2, N), sin_lookup(T.sin_tab, rd, N));
+      ent_j[e - cb] = j;
     }
     if (threadIdx.x < ncol) {
       const int i = c0 + threadIdx.x;
-      s_cnt[3 * threadIdx.x] = (cval ? T.col_ptr[i] : e0) - e0;
-      s_cnt[3 * threadIdx.x + 1] = (cval ? T.col_mid[i] : e0) - e0;
-      s_cnt[3 * threadIdx.x + 2] = (cval ? T.col_ptr[i + 1] : e0) - e0;
+      auto clampc = [&](int v) { return (v < cb ? cb : v > ce ? ce : v) - cb; };   // this pass's part
+      s_cnt[3 * threadIdx.x] = cval ? clampc(T.col_ptr[i]) : 0;
+      s_cnt[3 * threadIdx.x + 1] = cval ? clampc(T.col_mid[i]) : 0;
+      s_cnt[3 * threadIdx.x + 2] = cval ? clampc(T.col_ptr[i + 1]) : 0;
     }
     __syncthreads();
     // ---- phase 1: sparse DST of every column, 8 quads per item by rotation ----
@@ -257,16 +264,17 @@ __global__ void __launch_bounds__(kSweepThreads, 2) k_sweep(DevTables T, const d
 #pragma unroll
       for (int q = 0; q < kRotSteps; ++q) {
         const int sl = qg + kRotStride * q;
-        R[(4 * c + 0) * kQuads + sl] = Ao[q];
-        R[(4 * c + 1) * kQuads + sl] = Bo[q];
-        R[(4 * c + 2) * kQuads + sl] = Ae[q];
-        R[(4 * c + 3) * kQuads + sl] = Be[q];
+        if (ch == 0 && sl == 0) continue;     // quad slot 0 of chunk 0: the special modes below
+        double* r = R + 4 * c * kQuads + sl;   // only this item writes these slots: no barrier needed
+        r[0] = pass ? r[0] + Ao[q] : Ao[q];
+        r[kQuads] = pass ? r[kQuads] + Bo[q] : Bo[q];
+        r[2 * kQuads] = pass ? r[2 * kQuads] + Ae[q] : Ae[q];
+        r[3 * kQuads] = pass ? r[3 * kQuads] + Be[q] : Be[q];
       }
     }
-    __syncthreads();
     if (ch == 0) {   // CTA-uniform: all lanes take part in the shuffles
       // quad slot 0 holds modes {0, N/2, N/4, 3N/4}: r_{N/2} = Σ c sin(πj/2), r_{N/4}, r_{3N/4};
-      // 16 lanes per column (strided entries, fixed shuffle tree: deterministic)
+      // 16 lanes per column (strided entries, fixed shuffle tree), pass sums added in pass order
       const int c = threadIdx.x >> 4, sub = threadIdx.x & 15;
       double rh = 0.0, rq = 0.0, r3 = 0.0;
       for (int e = s_cnt[3 * c] + sub; c < ncol && e < s_cnt[3 * c + 2]; e += 16) {
@@ -283,12 +291,16 @@ __global__ void __launch_bounds__(kSweepThreads, 2) k_sweep(DevTables T, const d
         r3 += __shfl_xor_sync(0xffffffffu, r3, o);
       }
       if (sub == 0 && c < ncol) {
-        R[(4 * c + 0) * kQuads] = 0.5 * rh;          // (A_o + A_e, A_o − A_e) = (0, r_{N/2})
-        R[(4 * c + 2) * kQuads] = -0.5 * rh;
-        R[(4 * c + 1) * kQuads] = 0.5 * (rq + r3);   // (B_o − B_e, B_o + B_e) = (r_{N/4}, r_{3N/4})
-        R[(4 * c + 3) * kQuads] = 0.5 * (r3 - rq);
+        double* r = R + 4 * c * kQuads;
+        const double v0 = 0.5 * rh, v2 = -0.5 * rh;                   // (A_o + A_e, A_o − A_e) = (0, r_{N/2})
+        const double v1 = 0.5 * (rq + r3), v3 = 0.5 * (r3 - rq);     // (B_o − B_e, B_o + B_e) = (r_{N/4}, r_{3N/4})
+        r[0] = pass ? r[0] + v0 : v0;
+        r[kQuads] = pass ? r[kQuads] + v1 : v1;
+        r[2 * kQuads] = pass ? r[2 * kQuads] + v2 : v2;
+        r[3 * kQuads] = pass ? r[3 * kQuads] + v3 : v3;
       }
     }
+    }   // entry passes
     __syncthreads();
     if (!active) continue;
     // ---- phase 2: local Thomas, y_p = r_p − y_{p−1}/c_{p−1}, z_p = (y_p − z_{p+1})/c_p ----
@@ -1243,7 +1255,7 @@ void launch_sweep(const DevTables& T, const double* cval, const DenseSrc& D, dou
                   double* zlast, double* fsep, cudaStream_t s) {
   const int dense = !D.any() ? 0 : D.nb > 0 ? 2 : 1;
   (void)zlast;
-  const size_t sm = (size_t)BL * 4 * kQuads * sizeof(double) + (size_t)T.maxe * 5 * sizeof(double) +
+  const size_t sm = (size_t)BL * 4 * kQuads * sizeof(double) + (size_t)std::min(T.maxe, kEntCap) * 5 * sizeof(double) +
                     (size_t)(2 * T.N / 64 + 64 + 1) * sizeof(double2) + 3 * BL * sizeof(int);
   static bool attr = false;
   if (!attr) {

@@ -14,8 +14,10 @@
 //   k_interp        A7  jump-corrected six-point interpolation (Alg. 3)
 //   k_dst_dense2    A4/A6 dense rows (FFT-based DST-I in shared memory) for the volume and
 //                   final applies (once per solve)
-// plus deterministic GMRES vector kernels (Alg. 5).  FP64 on CUDA cores: the
-// path is HBM/latency bound, not a dense contraction (no tensor cores).
+// plus deterministic GMRES vector kernels (Alg. 5: k_mgs_cluster, one thread-block
+// cluster per MGS step with DSMEM partial sums; k_mgs_step/k_norm_scale for large M) and the
+// Ω-compact serving transfers (k_omega_map).  FP64 on CUDA cores: the path is HBM/latency bound,
+// not a dense contraction (no tensor cores).
 #include <cooperative_groups.h>
 #include <cub/cub.cuh>
 #include <cuda_runtime.h>

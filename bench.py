@@ -252,13 +252,16 @@ def main():
     u_h = torch.empty(n_out, dtype=torch.float64).pin_memory()
     u_c = torch.empty(n_out, dtype=torch.float64, device=dev) if compact else None
 
-    def solve_io(gd, fgd, fqd, fzd, b, u=None):
+    def solve_io(gd, fgd, fqd, fzd, b, u=None, async_final=False):
         """kfbi_solve on device inputs; with compact transfers f is scattered first and the Ω values
-        of u gathered after; returns the device array the host copy reads."""
+        of u gathered after; returns the device array the host copy reads.  async_final: the solve
+        returns with its final field still running on the stream (the serving loop's next host work
+        overlaps it; every later use is stream-ordered)."""
         if compact:
-            u, _, st_ = k.solve(gd, k.scatter_omega(fgd, grid=fg_full[b]), fqd, fzd, u=u, method=args.method)
+            u, _, st_ = k.solve(gd, k.scatter_omega(fgd, grid=fg_full[b]), fqd, fzd, u=u, method=args.method,
+                                async_final=async_final)
             return k.gather_omega(u, compact=u_c if b is None else u_cs[b])
-        u, _, st_ = k.solve(gd, fgd, fqd, fzd, u=u, method=args.method)
+        u, _, st_ = k.solve(gd, fgd, fqd, fzd, u=u, method=args.method, async_final=async_final)
         return u.view(-1)
 
     u_cs = [torch.empty(n_out, dtype=torch.float64, device=dev) for _ in range(2)] if compact else None
@@ -320,7 +323,7 @@ def main():
             stream.wait_event(ev_in[b])
             if j >= 2:
                 stream.wait_event(ev_out[b])                # download j−2 has left dout[b]
-            uo = solve_io(*din[b], b, u=dout[b])
+            uo = solve_io(*din[b], b, u=dout[b], async_final=True)
             ev_done[b].record(stream)
             with torch.cuda.stream(d2h_s):
                 d2h_s.wait_event(ev_done[b])

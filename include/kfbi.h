@@ -103,6 +103,10 @@ typedef struct {
                             KFBI_BICGSTAB (textbook, 2 applies per iteration); the last two run
                             at most restart × max_restarts iterations (reading R39)            */
   double gamma;          /* Richardson relaxation γ ∈ (0, 1], default 1               */
+  int32_t async_final;   /* 0 (default): return after the final field is computed; 1: return once
+                            the iteration has converged and the final field (u) is enqueued on
+                            `stream` — d_u / d_phi_out are complete when the stream reaches that
+                            point (serving loops overlap their next host work with it)          */
 } kfbi_solve_opts;
 enum { KFBI_GMRES = 0, KFBI_RICHARDSON = 1, KFBI_BICGSTAB = 2 };
 
@@ -208,7 +212,8 @@ kfbi_status kfbi_apply(kfbi_ctx* ctx, const double* d_phi, double* d_out, void* 
  *   d_phi0     initial density (M) or NULL for φ₀ = 0
  *   d_u        out: full node grid; u_h on Ω nodes, the interface solution elsewhere
  *   d_phi_out  out: converged density (M) or NULL
- * Synchronous (one host sync per Arnoldi step, as P:782). */
+ * Synchronous (one host sync per Arnoldi step, as P:782), except that with opts->async_final the
+ * final-field work is left running on `stream`. */
 kfbi_status kfbi_solve(kfbi_ctx* ctx, const double* d_g, const double* d_f_grid,
                        const double* d_f_isect, const double* d_f_ctrl, const double* d_phi0,
                        double* d_u, double* d_phi_out, const kfbi_solve_opts* opts,

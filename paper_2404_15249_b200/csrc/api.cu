@@ -935,7 +935,7 @@ kfbi_status kfbi_solve(kfbi_ctx* c, const double* d_g, const double* d_f_grid, c
   if (!c || !d_g || !d_u) return fail(c, KFBI_EINVAL, "null pointer");
   if ((d_f_grid == nullptr) != (d_f_isect == nullptr) || (d_f_grid == nullptr) != (d_f_ctrl == nullptr))
     return fail(c, KFBI_EINVAL, "f_grid, f_isect, f_ctrl must all be given or all NULL");
-  kfbi_solve_opts o{1e-8, 30, 50, KFBI_GMRES, 1.0};
+  kfbi_solve_opts o{1e-8, 30, 50, KFBI_GMRES, 1.0, 0};
   if (opts) o = *opts;
   if (o.restart < 1 || o.restart > kMaxRestart || o.max_restarts < 1 || !(o.tol > 0) || o.method < 0 ||
       o.method > KFBI_BICGSTAB || (o.method == KFBI_RICHARDSON && !(o.gamma > 0 && o.gamma <= 1)))
@@ -1038,7 +1038,7 @@ kfbi_status kfbi_solve(kfbi_ctx* c, const double* d_g, const double* d_f_grid, c
   final_field(c, c->gx, d_f_grid, d_f_isect, d_u, s);
   st.n_applies++;
   ck(cudaGetLastError(), "solve kernels");
-  ck(cudaStreamSynchronize(s), "solve sync");
+  if (!o.async_final) ck(cudaStreamSynchronize(s), "solve sync");
   KFBI_CATCH(c)
   st.converged = converged ? 1 : 0;
   st.t_solve_s = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
@@ -1171,7 +1171,7 @@ kfbi_status kfbi_gray_scott_step(kfbi_ctx* cu, kfbi_ctx* cv, double* d_u, double
   double* psi[2] = {d_psi_u, d_psi_v};
   for (int q = 0; q < 2; ++q) {
     launch_gs_rhs(cs[q]->T, w[q], fg, fq, fz, s);
-    kfbi_solve_opts o{tol, 30, 50, KFBI_GMRES, 1.0};
+    kfbi_solve_opts o{tol, 30, 50, KFBI_GMRES, 1.0, 0};
     kfbi_solve_stats st{};
     const kfbi_status r = kfbi_solve(cs[q], g0, fg, fq, fz, warm ? psi[q] : nullptr, y, psi[q], &o, &st, s);
     if (r != KFBI_OK) return r;

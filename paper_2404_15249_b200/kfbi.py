@@ -55,7 +55,7 @@ class Dist(C.Structure):
 
 class SolveOpts(C.Structure):
     _fields_ = [("tol", C.c_double), ("restart", C.c_int32), ("max_restarts", C.c_int32),
-                ("method", C.c_int32), ("gamma", C.c_double)]
+                ("method", C.c_int32), ("gamma", C.c_double), ("async_final", C.c_int32)]
 
 
 METHODS = {"gmres": 0, "richardson": 1, "bicgstab": 2}
@@ -289,7 +289,8 @@ class KFBI:
         return out
 
     def solve(self, g, f_grid=None, f_isect=None, f_ctrl=None, phi0=None, tol=1e-8, restart=30,
-              max_restarts=50, u=None, stream=None, raise_on_noconv=True, method="gmres", gamma=1.0):
+              max_restarts=50, u=None, stream=None, raise_on_noconv=True, method="gmres", gamma=1.0,
+              async_final=False):
         t = self.torch
         g = self._dev(g, self.M)
         fg = self._dev(f_grid, self.n_nodes)
@@ -298,7 +299,7 @@ class KFBI:
         p0 = self._dev(phi0, self.M)
         u = t.empty(self.n_nodes, dtype=t.float64, device=self.device) if u is None else u
         phi = t.empty(self.M, dtype=t.float64, device=self.device)
-        opts = SolveOpts(tol, restart, max_restarts, METHODS[method], gamma)
+        opts = SolveOpts(tol, restart, max_restarts, METHODS[method], gamma, 1 if async_final else 0)
         st = SolveStats()
         code = self.lib.kfbi_solve(self.ctx, _ptr(g), _ptr(fg), _ptr(fq), _ptr(fz), _ptr(p0), _ptr(u), _ptr(phi),
                                    C.byref(opts), C.byref(st), self._stream(stream))

@@ -47,3 +47,20 @@ def test_compact_solve_matches_full():
     b = k.gather_omega(u2).cpu().numpy()
     assert np.array_equal(a, b)                           # f off Ω is never read (zero extension)
     assert np.array_equal(a, u_full.cpu().numpy().reshape(-1)[mask])
+
+
+def test_async_final_matches_sync():
+    """opts.async_final: kfbi_solve returns with the final field still on the stream; after the
+    stream is synchronised u and φ equal the synchronous solve bit for bit."""
+    prob = W.C3(1024)
+    k = _k(prob)
+    pz, pq = k.points("ctrl"), k.points("isect")
+    x = prob.lo + np.arange(prob.n + 1) * prob.h
+    X, Y = np.meshgrid(x, x, indexing="ij")
+    dev = lambda a: torch.tensor(np.ascontiguousarray(a), device="cuda")
+    args = (dev(W.u_exact(*pz.T)), dev(W.f_exact(prob.kappa, X, Y).ravel()), dev(W.f_exact(prob.kappa, *pq.T)),
+            dev(W.f_exact(prob.kappa, *pz.T)))
+    u1, p1, s1 = k.solve(*args)
+    u2, p2, s2 = k.solve(*args, async_final=True)
+    torch.cuda.synchronize()
+    assert torch.equal(u1, u2) and torch.equal(p1, p2) and s1.iters == s2.iters

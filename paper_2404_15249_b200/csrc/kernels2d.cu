@@ -621,27 +621,10 @@ __global__ void __launch_bounds__(kInvThreads, 2) k_inv_sparse(DevTables T, cons
         asm volatile("prefetch.global.L2 [%0];" ::"l"(nrow + o));
     }
   }
-  auto X4 = [&](int t, double (&x)[4]) {
-    const double2* xp = reinterpret_cast<const double2*>(xrow + 4 * t);
-    const double2 a = xp[0], b2 = xp[1];
-    x[0] = a.x; x[1] = a.y; x[2] = b2.x; x[3] = b2.y;
-    if (hl) {
-      const double2* hp = reinterpret_cast<const double2*>(hl + 4 * t);
-      const double2* zp = reinterpret_cast<const double2*>(zl + 4 * t);
-      const double2 h0 = hp[0], h1 = hp[1], z0 = __ldg(zp), z1 = __ldg(zp + 1);
-      x[0] = fma(-h0.x, z0.x, x[0]); x[1] = fma(-h0.y, z0.y, x[1]);
-      x[2] = fma(-h1.x, z1.x, x[2]); x[3] = fma(-h1.y, z1.y, x[3]);
-    }
-    if (hr) {
-      const double2* hp = reinterpret_cast<const double2*>(hr + 4 * t);
-      const double2* zp = reinterpret_cast<const double2*>(zrr + 4 * t);
-      const double2 h0 = hp[0], h1 = hp[1], z0 = __ldg(zp), z1 = __ldg(zp + 1);
-      x[0] = fma(-h0.x, z0.x, x[0]); x[1] = fma(-h0.y, z0.y, x[1]);
-      x[2] = fma(-h1.x, z1.x, x[2]); x[3] = fma(-h1.y, z1.y, x[3]);
-    }
-  };
   double Pv[QPT], Qp[QPT], Qm[QPT], Rv[QPT];
   double xq1 = 0.0, xq2 = 0.0, xq3 = 0.0;   // modes N/4, N/2, 3N/4 (quad slot 0)
+  // the row's own quads are loaded first, all QPT of them (their registers are the final ones), and
+  // the fix-up rows after: more loads in flight per thread than quad-by-quad X4 (L2-latency bound)
 #pragma unroll
   for (int s = 0; s < QPT; ++s) {
     const int t = threadIdx.x + s * B;
@@ -649,15 +632,35 @@ __global__ void __launch_bounds__(kInvThreads, 2) k_inv_sparse(DevTables T, cons
       Pv[s] = Qp[s] = Qm[s] = Rv[s] = 0.0;
       continue;
     }
-    double x[4];
-    X4(t, x);
+    const double2* xp = reinterpret_cast<const double2*>(xrow + 4 * t);
+    const double2 a = xp[0], b2 = xp[1];
+    Pv[s] = a.x; Qp[s] = a.y; Qm[s] = b2.x; Rv[s] = b2.y;
+  }
+  auto fix = [&](const double* hrow, const double* zrow) {
+#pragma unroll
+    for (int s = 0; s < QPT; ++s) {
+      const int t = threadIdx.x + s * B;
+      if (t >= quarter) continue;
+      const double2* hp = reinterpret_cast<const double2*>(hrow + 4 * t);
+      const double2* zp = reinterpret_cast<const double2*>(zrow + 4 * t);
+      const double2 h0 = hp[0], h1 = hp[1], z0 = __ldg(zp), z1 = __ldg(zp + 1);
+      Pv[s] = fma(-h0.x, z0.x, Pv[s]); Qp[s] = fma(-h0.y, z0.y, Qp[s]);
+      Qm[s] = fma(-h1.x, z1.x, Qm[s]); Rv[s] = fma(-h1.y, z1.y, Rv[s]);
+    }
+  };
+  if (hl) fix(hl, zl);
+  if (hr) fix(hr, zrr);
+#pragma unroll
+  for (int s = 0; s < QPT; ++s) {
+    const int t = threadIdx.x + s * B;
+    if (t >= quarter) continue;
     if (t == 0) {   // positions 0..3 = modes 0, N/2, N/4, 3N/4
-      xq2 = x[1];
-      xq1 = x[2];
-      xq3 = x[3];
+      xq2 = Qp[s];
+      xq1 = Qm[s];
+      xq3 = Rv[s];
       Pv[s] = Qp[s] = Qm[s] = Rv[s] = 0.0;
     } else {
-      const double a = x[0], bb = x[1], c = x[2], d = x[3];
+      const double a = Pv[s], bb = Qp[s], c = Qm[s], d = Rv[s];
       Pv[s] = a + bb;
       Rv[s] = c + d;
       Qp[s] = (a - bb) + (d - c);

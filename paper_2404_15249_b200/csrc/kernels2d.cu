@@ -572,6 +572,7 @@ __device__ __forceinline__ double fixup(const DevTables& T, const double* __rest
 // follow by rotation with the per-row step e^{iπjB/N}.  Rows come grouped by class (odd,
 // j ≡ 0, j ≡ 2 mod 4; setup order) and are processed up to four at a time.
 constexpr int kInvThreads = 256;
+static_assert(kMaxColRows <= kInvThreads, "k_inv_sparse stages a column's rows one per thread");
 
 template <int QPT>
 __global__ void __launch_bounds__(kInvThreads, 2) k_inv_sparse(DevTables T, const double* __restrict__ spec,
@@ -596,13 +597,19 @@ __global__ void __launch_bounds__(kInvThreads, 2) k_inv_sparse(DevTables T, cons
     const int kk = r * G + ((r & 1) ? G - 1 - (int)blockIdx.x : (int)blockIdx.x);
     return kk < nit ? T.ocol_order[kk] : -1;
   };
+  // the next item's indices are loaded one round ahead, so that the column's row loads do not wait
+  // behind the dependent chain ocol_order → ocol / ocol_ptr
+  auto in_range = [&](int bb) { return bb >= T.o_lo && bb < T.o_hi; };
+  int nb = item(0), ni = 0, nu0 = 0, nu1 = 0;
+  if (in_range(nb)) { ni = T.ocol[nb]; nu0 = T.ocol_ptr[nb]; nu1 = T.ocol_ptr[nb + 1]; }
   for (int rnd = 0; rnd * G < nit; ++rnd) {
-  const int b = item(rnd);
-  if (b < T.o_lo || b >= T.o_hi) continue;   // CTA-uniform
+  const int b = nb, i = ni, u0 = nu0, u1 = nu1;
+  nb = item(rnd + 1);
+  if (in_range(nb)) { ni = T.ocol[nb]; nu0 = T.ocol_ptr[nb]; nu1 = T.ocol_ptr[nb + 1]; }
+  if (!in_range(b)) continue;   // CTA-uniform
   __syncthreads();
-  const int i = T.ocol[b];
-  const int u0 = T.ocol_ptr[b], u1 = T.ocol_ptr[b + 1];
-  for (int u = u0 + threadIdx.x; u < u1; u += B) s_rows[u - u0] = T.sn_j[u];
+  // row indices: loaded now, stored to shared memory after the row loads (kMaxColRows ≤ B)
+  const int srow = u0 + (int)threadIdx.x < u1 ? T.sn_j[u0 + threadIdx.x] : 0;
   // column i: separator → x = h; block row → x = z − h_{g−1} Z_L[p] − h_g Z_R[p].
   // Spectral positions 4t..4t+3 hold the quad {t, N−t, N/2−t, N/2+t}: two 16-byte loads per array.
   const int q = i / BL, rr = i - q * BL;
@@ -612,15 +619,6 @@ __global__ void __launch_bounds__(kInvThreads, 2) k_inv_sparse(DevTables T, cons
   const double* hr = (!sep && q < P - 1) ? hsep + (size_t)q * N : nullptr;
   const double* zl = T.zr + (size_t)(sep ? 0 : LB - rr) * N;     // Z_L[p] = Z_R[LB−1−p], p = rr − 1
   const double* zrr = T.zr + (size_t)(sep ? 0 : rr - 1) * N;
-  {   // warm L2 with the next column's spectral row while this one is evaluated
-    const int bn = item(rnd + 1);
-    if (bn >= T.o_lo && bn < T.o_hi) {
-      const int in = T.ocol[bn], qn = in / BL, rn = in - qn * BL;
-      const double* nrow = rn == 0 ? hsep + (size_t)(qn - 1) * N : spec + (size_t)(in - 1) * N;
-      for (int o = threadIdx.x * 16; o < N; o += B * 16)
-        asm volatile("prefetch.global.L2 [%0];" ::"l"(nrow + o));
-    }
-  }
   double Pv[QPT], Qp[QPT], Qm[QPT], Rv[QPT];
   double xq1 = 0.0, xq2 = 0.0, xq3 = 0.0;   // modes N/4, N/2, 3N/4 (quad slot 0)
   // the row's own quads are loaded first, all QPT of them (their registers are the final ones), and
@@ -667,6 +665,15 @@ __global__ void __launch_bounds__(kInvThreads, 2) k_inv_sparse(DevTables T, cons
       Qm[s] = (a - bb) - (d - c);
     }
   }
+  {   // warm L2 with the next column's spectral row while this one is evaluated
+    if (in_range(nb)) {
+      const int qn = ni / BL, rn = ni - qn * BL;
+      const double* nrow = rn == 0 ? hsep + (size_t)(qn - 1) * N : spec + (size_t)(ni - 1) * N;
+      for (int o = threadIdx.x * 16; o < N; o += B * 16)
+        asm volatile("prefetch.global.L2 [%0];" ::"l"(nrow + o));
+    }
+  }
+  if (u0 + (int)threadIdx.x < u1) s_rows[threadIdx.x] = srow;
   __syncthreads();
   const double scale = 2.0 / N;
   const int nrows = u1 - u0;

@@ -75,6 +75,89 @@ def test_frames_sphere_closed_form():
     np.testing.assert_allclose(np.linalg.det(np.stack([e1, e2, n], 1)), 1.0, atol=1e-13)
 
 
+def _torus_angles(p, R):
+    """(u, v) of points on the torus about z: x = (R + r cos v)(cos u, sin u), z = r sin v."""
+    rho = np.hypot(p[:, 0], p[:, 1])
+    return np.arctan2(p[:, 1], p[:, 0]), np.arctan2(p[:, 2], rho - R)
+
+
+def test_frames_torus_closed_form():
+    """Torus (R, r): the outward normal is (cos v cos u, cos v sin u, sin v) and the principal normal
+    curvatures are 1/r (meridian) and cos v/(R + r cos v) (parallel) (textbook differential geometry
+    of the torus).  With κ_ab = −e_aᵀD²ℓe_b/|∇ℓ| (sphere: −δ_ab/r) the eigenvalues of κ_ab
+    are −1/r and −cos v/(R + r cos v).  Geometry: C5 (reading R28), P:330-333 for the 3D box."""
+    R, r = 0.7, 0.3
+    comp = W.torus(R, r)
+    p = _surface_points(comp, m=400, seed=11)
+    u, v = _torus_angles(p, R)
+    n, e1, e2, kab = grid3d.frames(comp, p)
+    np.testing.assert_allclose(n, np.stack([np.cos(v) * np.cos(u), np.cos(v) * np.sin(u), np.sin(v)], -1),
+                               atol=1e-13)
+    ev = np.sort(np.linalg.eigvalsh(kab), axis=1)
+    want = np.sort(np.stack([np.full_like(v, -1.0 / r), -np.cos(v) / (R + r * np.cos(v))], -1), axis=1)
+    np.testing.assert_allclose(ev, want, atol=1e-12)
+    # the parallel direction (−sin u, cos u, 0) is a principal direction with curvature −cos v/(R + r cos v)
+    t = np.stack([-np.sin(u), np.cos(u), np.zeros_like(u)], -1)
+    tc = np.stack([(t * e1).sum(1), (t * e2).sum(1)], -1)
+    np.testing.assert_allclose(np.einsum("ma,mab,mb->m", tc, kab, tc), -np.cos(v) / (R + r * np.cos(v)), atol=1e-12)
+
+
+def test_frames_ellipsoid_gauss_and_mean_curvature():
+    """Ellipsoid (a, b, c): Gaussian curvature K = 1/(a²b²c² W⁴) and mean curvature
+    H = (|x|² − a² − b² − c²)/(2a²b²c² W³), W² = x²/a⁴ + y²/b⁴ + z²/c⁴ (textbook closed forms; H is
+    −1/r on the sphere, matching κ_ab = −I/r).  So det κ_ab = K and tr κ_ab = 2H.  Geometry: C4
+    (P:330-333)."""
+    a, b, c = 1.0, 0.8, 0.6
+    comp = W.ellipsoid(a, b, c)
+    p = _surface_points(comp, m=400, seed=12)
+    _, _, _, kab = grid3d.frames(comp, p)
+    x, y, z = p.T
+    W2 = x * x / a ** 4 + y * y / b ** 4 + z * z / c ** 4
+    K = 1.0 / (a * a * b * b * c * c * W2 ** 2)
+    H = ((p * p).sum(1) - a * a - b * b - c * c) / (2 * a * a * b * b * c * c * W2 ** 1.5)
+    np.testing.assert_allclose(np.linalg.det(kab), K, rtol=1e-12)
+    np.testing.assert_allclose(np.trace(kab, axis1=1, axis2=2), 2 * H, rtol=1e-12)
+
+
+def _level_exact(name, x):
+    """Implicit surface equations written out here (not the oracle's): ellipsoid Σ(x_a/r_a)² − 1,
+    torus (√(x² + y²) − R)² + z² − r² (SURVEY O2 / reading R28)."""
+    if name == "ellipsoid":
+        return (x[..., 0] / 1.0) ** 2 + (x[..., 1] / 0.8) ** 2 + (x[..., 2] / 0.6) ** 2 - 1.0
+    return (np.hypot(x[..., 0], x[..., 1]) - 0.7) ** 2 + x[..., 2] ** 2 - 0.09
+
+
+@pytest.mark.parametrize("name", ["ellipsoid", "torus"])
+def test_frames_monge_patch_definition(name):
+    """κ_ab by its definition: Γ is x = x₀ + t_a e_a + ½ κ_ab t_a t_b n + O(t³).
+    Each surface point over x₀ + ε(w₁e₁ + w₂e₂) is found on the normal line by bisection of the
+    implicit equation alone; the symmetric second difference (s(εw) + s(−εw))/2 = ½ε² wᵀκw + O(ε⁴)
+    must match the oracle's κ_ab, and |s(εw) − s(−εw)| = O(ε³) checks n ⟂ Γ."""
+    comp = SURF[name]
+    p = _surface_points(comp, m=60, seed=13)
+    n, e1, e2, kab = grid3d.frames(comp, p)
+    eps = 1e-3
+    rng = np.random.default_rng(14)
+    for _ in range(3):
+        w = rng.normal(size=(len(p), 2))
+        w /= np.linalg.norm(w, axis=1)[:, None]
+        s = []
+        for sg in (1.0, -1.0):
+            base = p + sg * eps * (w[:, :1] * e1 + w[:, 1:] * e2)
+            lo, hi = np.full(len(p), -1e-3), np.full(len(p), 1e-3)
+            flo = _level_exact(name, base + lo[:, None] * n)
+            assert np.all(flo * _level_exact(name, base + hi[:, None] * n) < 0)
+            for _ in range(80):
+                mid = 0.5 * (lo + hi)
+                fm = _level_exact(name, base + mid[:, None] * n)
+                same = np.sign(fm) == np.sign(flo)
+                lo, hi = np.where(same, mid, lo), np.where(same, hi, mid)
+            s.append(0.5 * (lo + hi))
+        want = 0.5 * eps ** 2 * np.einsum("ma,mab,mb->m", w, kab, w)
+        np.testing.assert_allclose(0.5 * (s[0] + s[1]), want, atol=5e-11)   # O(ε⁴) ≈ 1e-12·κ³
+        assert np.abs(s[0] - s[1]).max() < 1e-8                              # O(ε³)
+
+
 def test_lsq_fit_constants_and_convergence():
     errs = []
     q, gq, H = _quad3(3)
@@ -158,13 +241,25 @@ def test_KD3d_constant_density():
 
 
 @pytest.mark.slow
-def test_second_order_3d():
+@pytest.mark.parametrize("geom", ["sphere", "C4-ellipsoid", "C5-torus"])
+def test_second_order_3d(geom):
+    """Second-order convergence (P:4, "second-order accurate") of the Dirichlet BVP on the sphere and
+    on the C4 ellipsoid (κ = 0) and C5 torus (κ = 1) geometries, which exercise the non-spherical
+    κ_ab of App. A.2: e∞ and e₂ between N and 2N.  The ellipsoid's e∞ sits at its x tips (principal
+    radii 0.64 and 0.36 = 4.8h at N = 32) and is pre-asymptotic below N = 64 (measured e∞ 3.5e-4,
+    2.2e-4, 2.3e-5 at N = 32, 64, 128; e₂ converges at order 2 throughout), so it runs 64 → 128."""
     errs = []
-    for nn in (32, 64):
-        prob = W.problem("sphere", 3, nn, [W.ellipsoid(1, 1, 1)], 0.0)
+    sizes = (64, 128) if geom == "C4-ellipsoid" else (32, 64)
+    for nn in sizes:
+        if geom == "sphere":
+            prob = W.problem("sphere", 3, nn, [W.ellipsoid(1, 1, 1)], 0.0)
+        elif geom == "C4-ellipsoid":
+            prob = W.C4(nn)
+        else:
+            prob = W.C5(nn)
         o = Oracle3D(prob)
         X, Y, Z = np.meshgrid(o.st.x, o.st.x, o.st.x, indexing="ij")
-        v, phi, s = o.solve(W.u_exact(*o.points().T), lambda a, b, c: W.f_exact(0.0, a, b, c))
+        v, phi, s = o.solve(W.u_exact(*o.points().T), lambda a, b, c: W.f_exact(prob.kappa, a, b, c))
         assert s.converged
         errs.append(o.errors(v, W.u_exact(X, Y, Z)))
     e = np.array(errs)

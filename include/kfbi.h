@@ -25,6 +25,8 @@
  * memory: the caller queries kfbi_workspace_size() and hands a device buffer (e.g. a
  * torch.uint8 tensor) to kfbi_set_workspace(); the context borrows it until destroyed.
  * Streams are cudaStream_t passed as void* (NULL = legacy default stream).
+ * Devices: a context lives on kfbi_dist.device (the current device if dist is NULL or
+ * device < 0); every entry point runs on that device and restores the caller's current device.
  *
  * Errors: every call returns a kfbi_status; no exceptions or exit() cross the ABI.
  * kfbi_last_error(ctx) / kfbi_last_setup_error() return a message for the last failure.
@@ -46,12 +48,17 @@ typedef int32_t kfbi_status;
 enum {
   KFBI_OK = 0,
   KFBI_EINVAL = 1,       /* bad sizes, κ < 0, unequal h, null pointer, N not a power of two */
-  KFBI_EGEOM = 2,        /* Γ leaves the box / within 2h of ∂B, edge crossed twice (R31, R32) */
+  KFBI_EGEOM = 2,        /* Γ leaves the box, an edge crossed twice or by two components
+                            (R31), or an irregular node outside [2, N−2] on some axis — the
+                            clearance reading R32 as built: every interpolation
+                            stencil node is then an unknown node                               */
   KFBI_ENOCONV = 3,      /* GMRES hit max_restarts; outputs hold the last iterate + stats   */
   KFBI_ECUDA = 4,
   KFBI_ENCCL = 5,
   KFBI_ENOMEM = 6,       /* workspace missing or too small                                  */
-  KFBI_EUNSUPPORTED = 7  /* feature not built (e.g. 3D, Neumann)                            */
+  KFBI_EUNSUPPORTED = 7, /* feature not built (e.g. device setup in 3D, Neumann with κ = 0)   */
+  KFBI_EBREAKDOWN = 8    /* kfbi_solve: a residual became NaN/Inf (non-finite inputs or a
+                            breakdown of the iteration); outputs are undefined                  */
 };
 
 /* geometry kinds (2D curves parametrised CCW by θ ∈ [0, 2π)) */

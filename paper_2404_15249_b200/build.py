@@ -10,7 +10,7 @@ CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "lib", "libkfbi.so")
 SOURCES = ["api.cu", "kernels2d.cu", "kernels3d.cu", "setup_gpu.cu", "setup2d.cpp", "setup3d.cpp"]
 NVCC_FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
-              "-Xcompiler", "-fPIC,-fopenmp,-O2", "-shared"]
+              "-Xcompiler", "-fPIC,-fopenmp,-O2"]
 
 
 def nvcc() -> str:
@@ -42,11 +42,28 @@ def nccl_paths():
 
 
 def build(force: bool = False, verbose: bool = False) -> str:
+    """Each source compiles to an object in parallel (no relocatable device code), then one link."""
     if not force and not stale():
         return LIB
     os.makedirs(os.path.dirname(LIB), exist_ok=True)
-    cmd = ([nvcc()] + NVCC_FLAGS + ["-o", LIB + ".tmp"] + [os.path.join(CSRC, s) for s in SOURCES] + ["-lgomp"]
-           + nccl_paths())
+    objdir = os.path.join(HERE, "lib", "obj")
+    os.makedirs(objdir, exist_ok=True)
+    inc = nccl_paths()
+    inc = [a for a in inc if a.startswith("-I")]
+
+    def compile_one(src):
+        obj = os.path.join(objdir, src + ".o")
+        cmd = [nvcc()] + NVCC_FLAGS + inc + ["-c", "-o", obj, os.path.join(CSRC, src)]
+        if verbose:
+            print(" ".join(cmd), file=sys.stderr)
+        subprocess.run(cmd, check=True, cwd=CSRC)
+        return obj
+
+    from concurrent.futures import ThreadPoolExecutor
+    with ThreadPoolExecutor(max_workers=len(SOURCES)) as ex:
+        objs = list(ex.map(compile_one, SOURCES))
+    cmd = ([nvcc(), "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-o", LIB + ".tmp"] + objs
+           + ["-lgomp"] + nccl_paths())
     if verbose:
         print(" ".join(cmd), file=sys.stderr)
     subprocess.run(cmd, check=True, cwd=CSRC)

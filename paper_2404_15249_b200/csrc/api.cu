@@ -32,6 +32,21 @@ inline void ck(cudaError_t e, const char* what) {
 struct NcclError : std::runtime_error {
   using std::runtime_error::runtime_error;
 };
+// a non-finite residual in an iterative solve (NaN/Inf in the inputs, or a breakdown): KFBI_EBREAKDOWN
+struct BreakdownError : std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
+// the entry point runs on the context's device and restores the caller's current device on return
+struct DeviceGuard {
+  int prev = -1;
+  explicit DeviceGuard(int dev) {
+    int cur = 0;
+    if (dev >= 0 && cudaGetDevice(&cur) == cudaSuccess && cur != dev && cudaSetDevice(dev) == cudaSuccess) prev = cur;
+  }
+  ~DeviceGuard() {
+    if (prev >= 0) cudaSetDevice(prev);
+  }
+};
 inline void ckn(ncclResult_t e, const char* what) {
   if (e != ncclSuccess) throw NcclError(std::string(what) + ": " + ncclGetErrorString(e));
 }
@@ -314,6 +329,7 @@ kfbi_status fail(kfbi_ctx* c, kfbi_status st, const std::string& msg) {
 }
 
 #define KFBI_TRY(ctx)                                                  \
+  DeviceGuard kfbi_device_guard_((ctx)->device);                       \
   try {
 #define KFBI_CATCH(ctx)                                                \
   }                                                                    \
@@ -321,6 +337,7 @@ kfbi_status fail(kfbi_ctx* c, kfbi_status st, const std::string& msg) {
   catch (const NcclError& e) { return fail(ctx, KFBI_ENCCL, e.what()); } \
   catch (const GeomError& e) { return fail(ctx, KFBI_EGEOM, e.what()); } \
   catch (const ArgError& e) { return fail(ctx, KFBI_EINVAL, e.what()); } \
+  catch (const BreakdownError& e) { return fail(ctx, KFBI_EBREAKDOWN, e.what()); } \
   catch (const std::exception& e) { return fail(ctx, KFBI_EINVAL, e.what()); }
 
 cudaStream_t pick(kfbi_ctx* c, void* s) { return s ? (cudaStream_t)s : c->stream; }
@@ -583,7 +600,8 @@ kfbi_status setup_impl(const kfbi_grid* grid, const kfbi_boundary* bnd, const kf
       }
     }
     c->stream = (cudaStream_t)stream;
-    c->device = dist ? dist->device : 0;
+    c->device = (dist && dist->device >= 0) ? dist->device : 0;
+    if (!dist || dist->device < 0) cudaGetDevice(&c->device);
     Arena A{nullptr, 0, false};
     if (c->dim == 3) layout3(c, A);
     else layout(c, A);
@@ -687,7 +705,6 @@ kfbi_status kfbi_set_workspace(kfbi_ctx* c, void* d_ws, size_t bytes) {
   if (bytes < c->ws_need) return fail(c, KFBI_ENOMEM, "workspace too small");
   if (((uintptr_t)d_ws) & 255) return fail(c, KFBI_EINVAL, "workspace must be 256-byte aligned");
   KFBI_TRY(c)
-  ck(cudaSetDevice(c->device), "cudaSetDevice");
   c->ws = (uint8_t*)d_ws;
   c->ws_bytes = bytes;
   Arena A{c->ws, 0, true};
@@ -699,8 +716,7 @@ kfbi_status kfbi_set_workspace(kfbi_ctx* c, void* d_ws, size_t bytes) {
     ck(cudaHostAlloc(&c->hcol_host, (kMaxRestart + 2) * sizeof(double), cudaHostAllocMapped), "cudaHostAlloc");
     ck(cudaHostGetDevicePointer((void**)&c->hcol_map, c->hcol_host, 0), "cudaHostGetDevicePointer");
   }
-  if (c->use_nccl) {
-    ck(cudaSetDevice(c->device), "cudaSetDevice");
+  if (c->use_nccl && !c->comm) {   // a second kfbi_set_workspace keeps the communicator
     ckn(ncclCommInitRank(&c->comm, c->world, c->nccl_id, c->rank), "ncclCommInitRank");
   }
   // hole completion fields w_h|Γ (reading R27): plain fast solve of the bump, no jumps
@@ -842,7 +858,7 @@ bool solve_richardson(kfbi_ctx* c, const kfbi_solve_opts& o, bool have_x0, kfbi_
       launch_sub(M, c->ghat, c->tmp, c->gr, s);
     }
     const double nr = norm2(c, c->gr, s);
-    if (!std::isfinite(nr)) throw std::runtime_error("non-finite residual");
+    if (!std::isfinite(nr)) throw BreakdownError("non-finite residual");
     if (r0 < 0) r0 = nr;
     st.rel_residual = r0 > 0 ? nr / r0 : 0.0;
     if (nr <= o.tol * r0 || r0 == 0.0) return true;
@@ -867,7 +883,7 @@ bool solve_bicgstab(kfbi_ctx* c, const kfbi_solve_opts& o, bool have_x0, kfbi_so
   }
   launch_copy(M, r, rhat, s);
   const double n0 = norm2(c, r, s);
-  if (!std::isfinite(n0)) throw std::runtime_error("non-finite residual");
+  if (!std::isfinite(n0)) throw BreakdownError("non-finite residual");
   st.rel_residual = n0 > 0 ? 1.0 : 0.0;
   if (n0 == 0.0) return true;
   double rho_prev = 1.0, alpha = 1.0, omega = 1.0;
@@ -901,7 +917,7 @@ bool solve_bicgstab(kfbi_ctx* c, const kfbi_solve_opts& o, bool have_x0, kfbi_so
     axpy(c, -alpha, v, sv, s);
     st.iters++;
     const double ns = norm2(c, sv, s);
-    if (!std::isfinite(ns)) throw std::runtime_error("non-finite BiCGSTAB residual");
+    if (!std::isfinite(ns)) throw BreakdownError("non-finite BiCGSTAB residual");
     if (ns <= o.tol * n0) {
       axpy(c, alpha, p, c->gx, s);
       st.rel_residual = ns / n0;
@@ -980,7 +996,7 @@ kfbi_status kfbi_solve(kfbi_ctx* c, const double* d_g, const double* d_f_grid, c
     launch_copy(1, c->scal, c->hcol_map, s);   // β into host-mapped memory (no copy engine)
     ck(cudaStreamSynchronize(s), "sync beta");
     const double beta = c->hcol_host[0];
-    if (!std::isfinite(beta)) throw std::runtime_error("non-finite residual");
+    if (!std::isfinite(beta)) throw BreakdownError("non-finite residual");
     if (beta0 < 0) beta0 = beta;
     st.rel_residual = beta0 > 0 ? beta / beta0 : 0.0;
     if (beta <= o.tol * beta0 || beta0 == 0.0) { converged = true; break; }
@@ -1021,7 +1037,7 @@ kfbi_status kfbi_solve(kfbi_ctx* c, const double* d_g, const double* d_f_grid, c
       Hc(j + 1, j) = 0.0;
       gv[j + 1] = -sn[j] * gv[j];
       gv[j] = cs[j] * gv[j];
-      if (!std::isfinite(gv[j + 1])) throw std::runtime_error("non-finite GMRES residual");
+      if (!std::isfinite(gv[j + 1])) throw BreakdownError("non-finite GMRES residual");
       if (std::fabs(gv[j + 1]) <= o.tol * beta0 || hnext <= 1e-14 * beta0) { jlast = j; break; }
     }
     const int k = jlast + 1;
@@ -1192,6 +1208,7 @@ kfbi_status kfbi_launch_count(int64_t* count) {
 
 kfbi_status kfbi_destroy(kfbi_ctx* c) {
   if (!c) return KFBI_OK;
+  DeviceGuard g(c->device);
   if (c->comm) ncclCommDestroy(c->comm);
   if (c->hcol_host) cudaFreeHost(c->hcol_host);
   delete c;

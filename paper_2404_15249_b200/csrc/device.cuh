@@ -5,6 +5,11 @@
 #pragma once
 #include <cuda_runtime.h>
 
+#include <map>
+#include <mutex>
+#include <tuple>
+#include <utility>
+
 #include "kernels.h"
 
 namespace kfbi {
@@ -379,15 +384,53 @@ __device__ __forceinline__ void dst1_core(double2* z, const double2* __restrict_
 }
 
 
+// Host-side launch caches, kept per device: the shared-memory opt-in of a kernel, its occupancy and
+// the SM count belong to one device, and one process may drive contexts on several GPUs.
+inline int cur_device() {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  return dev;
+}
+
 inline int num_sms() {
-  static int n = 0;
-  if (!n) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
-    if (n <= 0) n = 148;
+  static std::mutex mu;
+  static std::map<int, int> n;
+  const int dev = cur_device();
+  std::lock_guard<std::mutex> g(mu);
+  int& v = n[dev];
+  if (v <= 0) {
+    cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
+    if (v <= 0) v = 148;
   }
-  return n;
+  return v;
+}
+
+// raise a kernel's dynamic shared-memory limit on the current device to at least `bytes`
+inline void smem_optin(const void* fn, size_t bytes) {
+  static std::mutex mu;
+  static std::map<std::pair<int, const void*>, size_t> done;
+  const int dev = cur_device();
+  std::lock_guard<std::mutex> g(mu);
+  size_t& v = done[{dev, fn}];
+  if (v < bytes) {
+    cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+    v = bytes;
+  }
+}
+
+// resident CTAs per SM of `fn` at (threads, dynamic smem) on the current device (≥ 1)
+inline int occupancy(const void* fn, int threads, size_t sm) {
+  static std::mutex mu;
+  static std::map<std::tuple<int, const void*, int, size_t>, int> done;
+  const auto key = std::make_tuple(cur_device(), fn, threads, sm);
+  std::lock_guard<std::mutex> g(mu);
+  auto it = done.find(key);
+  if (it != done.end()) return it->second;
+  int per = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, fn, threads, sm);
+  if (per < 1) per = 1;
+  done[key] = per;
+  return per;
 }
 
 }  // namespace

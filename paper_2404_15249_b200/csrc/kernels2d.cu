@@ -1269,17 +1269,11 @@ void launch_sweep(const DevTables& T, const double* cval, const DenseSrc& D, dou
   (void)zlast;
   const size_t sm = (size_t)BL * 4 * kQuads * sizeof(double) + (size_t)std::min(T.maxe, kEntCap) * 5 * sizeof(double) +
                     (size_t)(2 * T.N / 64 + 64 + 1) * sizeof(double2) + 3 * BL * sizeof(int);
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(k_sweep<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
-    cudaFuncSetAttribute(k_sweep<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
-    cudaFuncSetAttribute(k_sweep<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
-    attr = true;
-  }
+  smem_optin((const void*)k_sweep<0>, 227 * 1024);
+  smem_optin((const void*)k_sweep<1>, 227 * 1024);
+  smem_optin((const void*)k_sweep<2>, 227 * 1024);
   const int nch = (T.N / 4 + kQuads - 1) / kQuads;
-  int per = 0;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_sweep<0>, kSweepThreads, sm);
-  if (per < 1) per = 1;
+  const int per = occupancy((const void*)k_sweep<0>, kSweepThreads, sm);
   int G = num_sms() * per / nch;
   if (G < 1) G = 1;
   if (G > T.g_hi - T.g_lo) G = T.g_hi - T.g_lo;
@@ -1311,14 +1305,10 @@ void launch_inverse_sparse(const DevTables& T, const double* spec, const double*
   const size_t sm = (size_t)(T.N + T.N / 16 + 1) * sizeof(double) +
                     (size_t)(kInvThreads / 32) * 2 * T.mcr * sizeof(double);
   const int grid = ncols < 2 * num_sms() ? ncols : 2 * num_sms();
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(k_inv_sparse<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-    cudaFuncSetAttribute(k_inv_sparse<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-    cudaFuncSetAttribute(k_inv_sparse<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-    cudaFuncSetAttribute(k_inv_sparse<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-    attr = true;
-  }
+  smem_optin((const void*)k_inv_sparse<1>, 200 * 1024);
+  smem_optin((const void*)k_inv_sparse<2>, 200 * 1024);
+  smem_optin((const void*)k_inv_sparse<4>, 200 * 1024);
+  smem_optin((const void*)k_inv_sparse<8>, 200 * 1024);
   switch (qpt) {
     case 1: ++g_launches; k_inv_sparse<1><<<grid, kInvThreads, sm, s>>>(T, spec, hsep, vsten); break;
     case 2: ++g_launches; k_inv_sparse<2><<<grid, kInvThreads, sm, s>>>(T, spec, hsep, vsten); break;
@@ -1423,17 +1413,9 @@ static void dense_n(const DevTables& T, const double* src, int mask, const BumpP
                     double* dst, cudaStream_t s) {
   using C = DenseCfg<N>;
   const size_t sm = C::smem(C::STAGE && MODE == 0);
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(k_dst_dense2<MODE, N>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-    attr = true;
-  }
+  smem_optin((const void*)k_dst_dense2<MODE, N>, sm);
   const int rows = T.col_hi - T.col_lo + 1;
-  static int per = 0;
-  if (!per) {
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_dst_dense2<MODE, N>, C::NTHR, sm);
-    if (per < 1) per = 1;
-  }
+  const int per = occupancy((const void*)k_dst_dense2<MODE, N>, C::NTHR, sm);
   const int groups = (rows + C::RPC - 1) / C::RPC;
   const int grid = groups < per * num_sms() ? groups : per * num_sms();
   k_dst_dense2<MODE, N><<<grid, C::NTHR, sm, s>>>(T, src, mask, bp, hsep, dst);

@@ -669,14 +669,10 @@ static void dst_rows3_n(const DevTables3& T, int mode, double* work, const doubl
   constexpr int RPC = 256 / (N / 32);
   const size_t sm = (size_t)RPC * (N / 2 + N / 32 + 1) * sizeof(double2);
   const int grid = cdiv3((long)(N - 1) * N, RPC);
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(k_dst_rows3t<0, N>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-    cudaFuncSetAttribute(k_dst_rows3t<1, N>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-    cudaFuncSetAttribute(k_dst_rows3t<2, N>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-    cudaFuncSetAttribute(k_dst_rows3t<3, N>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-    attr = true;
-  }
+  smem_optin((const void*)k_dst_rows3t<0, N>, sm);
+  smem_optin((const void*)k_dst_rows3t<1, N>, sm);
+  smem_optin((const void*)k_dst_rows3t<2, N>, sm);
+  smem_optin((const void*)k_dst_rows3t<3, N>, sm);
   if (mode == 0) k_dst_rows3t<0, N><<<grid, 256, sm, s>>>(T, work, hsep, scale, out, src, corr);
   else if (mode == 1) k_dst_rows3t<1, N><<<grid, 256, sm, s>>>(T, work, hsep, scale, out, src, corr);
   else if (mode == 2) k_dst_rows3t<2, N><<<grid, 256, sm, s>>>(T, work, hsep, scale, out, src, corr);
@@ -698,19 +694,11 @@ static void sparse3_n(const DevTables3& T, int which, const double* src, const d
                       double* dst, cudaStream_t s) {
   constexpr int RPC = 256 / (N / 32) < N ? 256 / (N / 32) : N, NTHR = RPC * (N / 32);
   const size_t sm = (size_t)RPC * (N / 2 + N / 32 + 1) * sizeof(double2);
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(k_inv3y<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-    attr = true;
-  }
+  smem_optin((const void*)k_inv3y<N>, sm);
   const dim3 grid(N / RPC, T.i_hi - T.i_lo + 1);
   if (which == 0) {
     const size_t sm0 = sm + (size_t)T.max_plane_irr * (sizeof(double) + sizeof(int16_t));
-    static size_t attr0 = 0;
-    if (sm0 > attr0) {
-      cudaFuncSetAttribute(k_fwd3s<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm0);
-      attr0 = sm0;
-    }
+    smem_optin((const void*)k_fwd3s<N>, sm0);
     const dim3 gridf((N / RPC + kFwdGroups - 1) / kFwdGroups, T.i_hi - T.i_lo + 1);
     k_fwd3s<N><<<gridf, NTHR, sm0, s>>>(T, src, dst);
   }

@@ -15,8 +15,9 @@ import numpy as np
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "lib", "libkfbi.so")
 
-OK, EINVAL, EGEOM, ENOCONV, ECUDA, ENCCL, ENOMEM, EUNSUPPORTED = range(8)
-_NAMES = {0: "OK", 1: "EINVAL", 2: "EGEOM", 3: "ENOCONV", 4: "ECUDA", 5: "ENCCL", 6: "ENOMEM", 7: "EUNSUPPORTED"}
+OK, EINVAL, EGEOM, ENOCONV, ECUDA, ENCCL, ENOMEM, EUNSUPPORTED, EBREAKDOWN = range(9)
+_NAMES = {0: "OK", 1: "EINVAL", 2: "EGEOM", 3: "ENOCONV", 4: "ECUDA", 5: "ENCCL", 6: "ENOMEM", 7: "EUNSUPPORTED",
+          8: "EBREAKDOWN"}
 
 EXPORTS = ["kfbi_version", "kfbi_last_error", "kfbi_last_setup_error", "kfbi_get_unique_id", "kfbi_setup",
            "kfbi_workspace_size", "kfbi_set_workspace", "kfbi_sizes", "kfbi_points", "kfbi_node_mask",
@@ -223,8 +224,29 @@ class KFBI:
             raise KfbiError(st, self.lib.kfbi_last_error(self.ctx).decode())
 
     def _stream(self, stream):
-        s = stream if stream is not None else self.torch.cuda.current_stream(self.device)
-        return C.c_void_p(s.cuda_stream)
+        """cudaStream_t for a call.  Inputs are converted on torch's current stream, so an explicit
+        other stream first waits on it (no read of a half-copied input)."""
+        cur = self.torch.cuda.current_stream(self.device)
+        if stream is not None and stream != cur:
+            stream.wait_stream(cur)
+        return C.c_void_p((stream if stream is not None else cur).cuda_stream)
+
+    def _keep(self, stream, *tensors):
+        """Tensors read or written by work still queued on an explicit non-current stream stay
+        allocated until that work is done (caching-allocator record_stream)."""
+        if stream is None or stream == self.torch.cuda.current_stream(self.device):
+            return
+        for x in tensors:
+            if x is not None:
+                x.record_stream(stream)
+
+    def _out(self, x, n, name):
+        """A caller-supplied output buffer: float64, contiguous, on the context's device, n values."""
+        t = self.torch
+        if (not isinstance(x, t.Tensor) or x.dtype != t.float64 or x.device != self.device
+                or not x.is_contiguous() or x.numel() != n):
+            raise ValueError(f"{name} must be a contiguous float64 tensor of {n} values on {self.device}")
+        return x
 
     def _dev(self, x, n=None):
         t = self.torch
@@ -266,15 +288,23 @@ class KFBI:
     def scatter_omega(self, compact, grid=None, stream=None):
         """Full (N+1)^d grid from the Ω-node values (0 off Ω) — kfbi_scatter_omega."""
         t = self.torch
-        grid = t.empty(self.n_nodes, dtype=t.float64, device=self.device) if grid is None else grid
-        self._check(self.lib.kfbi_scatter_omega(self.ctx, _ptr(compact), _ptr(grid), self._stream(stream)))
+        compact = self._out(compact, self.omega_count(), "compact")
+        grid = (t.empty(self.n_nodes, dtype=t.float64, device=self.device) if grid is None
+                else self._out(grid, self.n_nodes, "grid"))
+        with t.cuda.device(self.device):
+            self._check(self.lib.kfbi_scatter_omega(self.ctx, _ptr(compact), _ptr(grid), self._stream(stream)))
+        self._keep(stream, compact, grid)
         return grid
 
     def gather_omega(self, grid, compact=None, stream=None):
         """Ω-node values of a full grid — kfbi_gather_omega."""
         t = self.torch
-        compact = t.empty(self.omega_count(), dtype=t.float64, device=self.device) if compact is None else compact
-        self._check(self.lib.kfbi_gather_omega(self.ctx, _ptr(grid), _ptr(compact), self._stream(stream)))
+        grid = self._out(grid.reshape(-1) if grid.is_contiguous() else grid, self.n_nodes, "grid")
+        compact = (t.empty(self.omega_count(), dtype=t.float64, device=self.device) if compact is None
+                   else self._out(compact, self.omega_count(), "compact"))
+        with t.cuda.device(self.device):
+            self._check(self.lib.kfbi_gather_omega(self.ctx, _ptr(grid), _ptr(compact), self._stream(stream)))
+        self._keep(stream, grid, compact)
         return compact
 
     def node_mask(self):
@@ -284,8 +314,10 @@ class KFBI:
 
     def apply(self, phi, out=None, stream=None):
         phi = self._dev(phi, self.M)
-        out = self.torch.empty_like(phi) if out is None else out
-        self._check(self.lib.kfbi_apply(self.ctx, _ptr(phi), _ptr(out), self._stream(stream)))
+        out = self.torch.empty_like(phi) if out is None else self._out(out, self.M, "out")
+        with self.torch.cuda.device(self.device):
+            self._check(self.lib.kfbi_apply(self.ctx, _ptr(phi), _ptr(out), self._stream(stream)))
+        self._keep(stream, phi, out)
         return out
 
     def solve(self, g, f_grid=None, f_isect=None, f_ctrl=None, phi0=None, tol=1e-8, restart=30,
@@ -297,12 +329,15 @@ class KFBI:
         fq = self._dev(f_isect, self.nq)
         fz = self._dev(f_ctrl, self.M)
         p0 = self._dev(phi0, self.M)
-        u = t.empty(self.n_nodes, dtype=t.float64, device=self.device) if u is None else u
+        u = (t.empty(self.n_nodes, dtype=t.float64, device=self.device) if u is None
+             else self._out(u.reshape(-1) if isinstance(u, t.Tensor) and u.is_contiguous() else u, self.n_nodes, "u"))
         phi = t.empty(self.M, dtype=t.float64, device=self.device)
         opts = SolveOpts(tol, restart, max_restarts, METHODS[method], gamma, 1 if async_final else 0)
         st = SolveStats()
-        code = self.lib.kfbi_solve(self.ctx, _ptr(g), _ptr(fg), _ptr(fq), _ptr(fz), _ptr(p0), _ptr(u), _ptr(phi),
-                                   C.byref(opts), C.byref(st), self._stream(stream))
+        with t.cuda.device(self.device):
+            code = self.lib.kfbi_solve(self.ctx, _ptr(g), _ptr(fg), _ptr(fq), _ptr(fz), _ptr(p0), _ptr(u), _ptr(phi),
+                                       C.byref(opts), C.byref(st), self._stream(stream))
+        self._keep(stream, g, fg, fq, fz, p0, u, phi)
         if code != OK and (code != ENOCONV or raise_on_noconv):
             self._check(code)
         stats = Stats(st.iters, st.restarts, st.n_applies, bool(st.converged), st.rel_residual, st.t_solve_s)

@@ -55,10 +55,10 @@ def test_setup_errors(lib):
     with pytest.raises(KfbiError) as e:   # Neumann at κ = 0: constant null space
         KFBI(W.neumann(W.C1(64)), workspace=False)
     assert e.value.code == 7
-    with pytest.raises(KfbiError) as e:   # 3D Neumann not built
+    with pytest.raises(KfbiError) as e:   # 3D Neumann at κ = 0 (C4): constant null space
         KFBI(W.neumann(W.C4(32)), workspace=False)
     assert e.value.code == 7
-    with pytest.raises(KfbiError) as e:   # Γ within 2h of ∂B (R32)
+    with pytest.raises(KfbiError) as e:   # an irregular node outside [2, N−2] (R32 as built)
         KFBI(W.problem("near-box", 2, 64, [W.circle(1.18)], 0.0), workspace=False)
     assert e.value.code == 2
 

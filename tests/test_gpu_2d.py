@@ -181,6 +181,32 @@ def test_solve_matches_oracle(prob):
     assert np.abs(u[m] - W.u_exact(X, Y)[m]).max() < 50 * prob.h ** 2
 
 
+@pytest.mark.slow
+def test_solve_full_size_C3():
+    """The bench workload itself: C3 8192² (κ = 0, two holes, hole completion R27) solved by
+    kfbi_solve against the oracle's Alg. 5 GMRES on the same inputs — world-1 in-place bump axpy into
+    the final spectrum and the k_dst_dense2<·, 8192> final field included."""
+    prob = W.C3(8192)
+    o, k = oracle(prob), gpu(prob)
+    n = prob.n
+    f = lambda x, y: W.f_exact(prob.kappa, x, y)
+    zx, zy = o.ctrl_points()
+    u_ref, phi_ref, s_ref = o.solve(W.u_exact(zx, zy), f)
+    pz, pq = k.points("ctrl"), k.points("isect")
+    x = prob.lo + np.arange(n + 1) * prob.h
+    X, Y = np.meshgrid(x, x, indexing="ij")
+    fg = f(X, Y)
+    del X, Y
+    u, phi, s = k.solve(W.u_exact(pz[:, 0], pz[:, 1]), fg, f(pq[:, 0], pq[:, 1]), f(pz[:, 0], pz[:, 1]))
+    u = u.cpu().numpy()
+    m = o.st.side
+    assert s.converged and abs(s.iters - s_ref.iters) <= 1, (s.iters, s_ref.iters)
+    assert rel(u[m], u_ref[m]) < 1e-8
+    assert rel(phi.cpu().numpy(), phi_ref) < 1e-8
+    _OR.pop(prob, None)
+    _GPU.pop(prob, None)
+
+
 def test_solve_second_order_on_gpu():
     errs = []
     for n in (256, 512, 1024, 2048):

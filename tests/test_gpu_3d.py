@@ -107,6 +107,28 @@ def test_interface_solve3d_full_size_C5():
     test_interface_solve3d_piecewise_quadratic(W.C5(512))
 
 
+@pytest.mark.slow
+def test_apply3d_full_size_C5():
+    """The K_D apply that bench.py --config C5 times (512³: k_fwd3s<512>, k_sweep3, k_reduced3,
+    k_inv3y<512>, k_zeval3<512>) against the oracle's plain Alg. 4 path, seeds 0 and 1."""
+    prob = W.C5(512)
+    o, k = oracle(prob), gpu(prob)
+    for seed in (0, 1):
+        phi = W.random_density(o.M, seed)
+        assert rel(k.apply(phi).cpu().numpy(), o.apply_KD(phi)) < 1e-10
+    _OR.pop(prob, None)
+    _GPU.pop(prob, None)
+
+
+@pytest.mark.slow
+def test_solve3d_C5_256():
+    """C5 geometry (torus, κ = 1) solved at 256³ against the oracle's GMRES."""
+    prob = W.C5(256)
+    test_solve3d_matches_oracle(prob)
+    _OR.pop(prob, None)
+    _GPU.pop(prob, None)
+
+
 # ------------------------------------------------------------------ multi-GPU partition (emulated)
 @pytest.mark.parametrize("prob,world", [(W.C4(64), 2), (W.C4(64), 4), (W.C5(128), 8)], ids=["C4-64x2", "C4-64x4", "C5-128x8"])
 def test_partitioned_apply3d_matches_single(prob, world):

@@ -76,3 +76,48 @@ def test_bad_solve_options(opts):
     with pytest.raises(KfbiError) as e:
         k.solve(W.u_exact(pz[:, 0], pz[:, 1]), **opts)
     assert e.value.code == 1                                     # KFBI_EINVAL
+
+
+def test_nonfinite_input_is_a_breakdown():
+    """A NaN in g makes the first residual non-finite: KFBI_EBREAKDOWN, not EINVAL."""
+    k = gpu(W.C1(64))
+    g = W.u_exact(*k.points("ctrl").T)
+    g[3] = np.nan
+    with pytest.raises(KfbiError) as e:
+        k.solve(g)
+    assert e.value.code == 8                                     # KFBI_EBREAKDOWN
+
+
+def test_output_buffers_are_validated():
+    k = gpu(W.C1(64))
+    phi = np.zeros(k.M)
+    for bad in (torch.empty(k.M, dtype=torch.float32, device="cuda"), torch.empty(k.M + 1, dtype=torch.float64,
+                device="cuda"), torch.empty(2 * k.M, dtype=torch.float64, device="cuda")[::2]):
+        with pytest.raises(ValueError):
+            k.apply(phi, out=bad)
+    with pytest.raises(ValueError):
+        k.solve(W.u_exact(*k.points("ctrl").T), u=torch.empty(k.n_nodes - 1, dtype=torch.float64, device="cuda"))
+
+
+def test_explicit_stream_matches_current_stream():
+    """Work on an explicit side stream waits for the inputs converted on the current stream."""
+    prob = W.C2(256)
+    k = gpu(prob)
+    phi = W.random_density(k.M, 4)
+    ref = k.apply(phi).cpu()
+    s = torch.cuda.Stream()
+    out = k.apply(phi, stream=s)
+    s.synchronize()
+    assert torch.equal(out.cpu(), ref)
+
+
+@pytest.mark.skipif(not torch.cuda.is_available() or torch.cuda.device_count() < 2, reason="needs two GPUs")
+def test_context_on_second_device():
+    """A context on device 1 created and used while device 0 is current (per-device launch caches)."""
+    prob = W.C3(1024)
+    k0 = gpu(prob)
+    with torch.cuda.device(0):
+        k1 = KFBI(prob, device=1)
+        phi = W.random_density(k0.M, 5)
+        assert torch.equal(k1.apply(phi).cpu(), k0.apply(phi).cpu())
+        assert torch.cuda.current_device() == 0

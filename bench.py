@@ -9,8 +9,10 @@ value  = grid points per second per interface solve = U · n_applies / t_step,
 e2e    = the same metric through the public API with pinned HOST inputs/outputs: the H2D
          copy of g, f (grid, intersections, control points) and the D2H copy of u inside
          the timed region.
---impl reference: the CPU oracle (oracle/) as it stands, one K_D apply of the same
-         workload per step, on the host cores (rank 0 only).
+cpu_baseline: the CPU oracle (oracle/) as it stands, one full solve of the same workload on all
+         host cores (scipy.fft workers; BASELINE.md's CPU plan), rank 0 at N = 1.
+--impl reference: the CPU oracle as it stands, one K_D apply of the same workload per step, on
+         all host cores (rank 0 only).
 """
 from __future__ import annotations
 
@@ -107,48 +109,77 @@ def make_inputs(k, prob):
     return (g, f(*G).ravel(), f(*pq.T), f(*pz.T))
 
 
-def cpu_oracle_apply_rate(prob, reps=1):
-    """Oracle (as it stands) on the host: one K_D apply of the same workload."""
+def host_cpu():
+    """Host description for the CPU baselines (nproc, lscpu model and sockets)."""
+    info = {"nproc": os.cpu_count()}
+    try:
+        out = subprocess.run(["lscpu"], capture_output=True, text=True, timeout=10).stdout
+        for l in out.splitlines():
+            k, _, v = l.partition(":")
+            if k.strip() in ("Model name", "Socket(s)", "Core(s) per socket", "Thread(s) per core"):
+                info[k.strip()] = v.strip()
+    except Exception:
+        pass
+    return info
+
+
+def oracle_workers():
+    """The oracle runs as it stands; only its library primitives get the host's cores: scipy.fft's
+    worker pool (its DST-I passes) and the BLAS thread pool.  NumPy element-wise work stays serial."""
+    import scipy.fft
+    return scipy.fft.set_workers(os.cpu_count() or 1)
+
+
+def cpu_oracle_solve_rate(prob):
+    """The oracle's full Dirichlet solve (Y apply, Alg. 5 GMRES, final field) of the
+    workload on all host cores, as BASELINE.md plans the CPU column: U × interface solves / seconds."""
     from oracle.bie import Oracle2D
     from oracle.bie3d import Oracle3D
-    t0 = time.time()
-    o = Oracle2D(prob) if prob.dim == 2 else Oracle3D(prob)
-    t_setup = time.time() - t0
-    phi = W.random_density(o.M, 0)
-    ts = []
-    for _ in range(reps):
+    with oracle_workers():
         t0 = time.perf_counter()
-        o.apply_K(phi) if prob.dim == 2 else o.apply_KD(phi)
-        ts.append(time.perf_counter() - t0)
-    return o, ts, t_setup
+        o = Oracle2D(prob) if prob.dim == 2 else Oracle3D(prob)
+        t_setup = time.perf_counter() - t0
+        f = lambda *a: W.f_exact(prob.kappa, *a)
+        g = W.u_exact(*(o.ctrl_points() if prob.dim == 2 else o.points().T))
+        t0 = time.perf_counter()
+        _, _, st = o.solve(g, f)
+        t = time.perf_counter() - t0
+    n_solves = st.n_applies + 2          # + the Y apply and the final field (as kfbi_solve counts)
+    return prob.unknowns * n_solves / t, t, t_setup, st
 
 
 def run_reference(args, prob):
+    """The base contract's reference arm for this tier: the CPU oracle as it stands, one K_D apply of
+    the workload per step, on all host cores (scipy.fft workers), rank 0 only."""
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
     from oracle.bie import Oracle2D
     from oracle.bie3d import Oracle3D
     U = prob.unknowns
-    o = Oracle2D(prob) if prob.dim == 2 else Oracle3D(prob)
-    phi = W.random_density(o.M, 0)
-    apply = o.apply_K if prob.dim == 2 else o.apply_KD
-    for _ in range(args.warmup):
-        apply(phi)
-    ts = []
-    for _ in range(args.steps):
-        t0 = time.perf_counter()
-        apply(phi)
-        ts.append(time.perf_counter() - t0)
+    with oracle_workers():
+        o = Oracle2D(prob) if prob.dim == 2 else Oracle3D(prob)
+        phi = W.random_density(o.M, 0)
+        apply = o.apply_K if prob.dim == 2 else o.apply_KD
+        for _ in range(args.warmup):
+            apply(phi)
+        ts = []
+        for _ in range(args.steps):
+            t0 = time.perf_counter()
+            apply(phi)
+            ts.append(time.perf_counter() - t0)
     t = float(np.mean(ts))
     v = U / t
-    sample = f"one K_D apply (interface solve) of {prob.name} N={prob.n} per step"
+    cpu = host_cpu()
+    sample = (f"one K_D apply (interface solve) of {prob.name} N={prob.n} per step; scipy.fft workers = "
+              f"{cpu['nproc']} host cores, NumPy element-wise serial")
     print(json.dumps({
         "impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": 1e3 * t, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": {"workload": prob.name, "grid": prob.n, "kappa": prob.kappa, "M": o.M},
-        "cpu_baseline": {"value": v, "unit": UNIT, "cores": 1, "kind": "oracle", "sample": sample},
+        "cpu_baseline": {"value": v, "unit": UNIT, "cores": cpu["nproc"], "kind": "oracle", "sample": sample,
+                         "host": cpu},
         "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}))
 
 
@@ -192,6 +223,14 @@ def main():
     # multi-GPU: slabs along x over NCCL when the world size divides the slab units
     # (2D: level-2 segments, N/512; 3D: ADM blocks, N/16); otherwise independent replicas
     sharded = world > 1 and (prob.n % (512 * world) == 0 if prob.dim == 2 else prob.n % (16 * world) == 0)
+    if world > 1 and not sharded:
+        # the path shards (slabs of level-2 segments / ADM blocks): N replicas of the whole
+        # problem would read as scaling, so a world size that does not divide the slab units is refused
+        if rank == 0:
+            print(json.dumps({"metric": METRIC, "error": f"world {world} does not divide {prob.name} N={prob.n} into "
+                              f"slabs ({'N/512 segments' if prob.dim == 2 else 'N/16 ADM blocks'})"}))
+        dist.destroy_process_group()
+        raise SystemExit(2)
     if sharded:
         k = KFBI(prob, device=local, world=world, rank=rank, nccl_id=broadcast_unique_id())
     else:
@@ -232,7 +271,7 @@ def main():
         t_step = float(tt.item())
     U = prob.unknowns
     n_app = stats.n_applies
-    copies = 1 if sharded else world          # replicas each solve the whole problem
+    copies = 1
     value = copies * U * n_app / t_step
 
     # e2e through the public API with pinned host buffers.  Single-grid layouts move only the Ω-node
@@ -386,9 +425,14 @@ def main():
         "clocks": clk.summary(),
     }
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        o, ts, t_setup = cpu_oracle_apply_rate(prob)
-        line["cpu_baseline"] = {"value": U / ts[0], "unit": UNIT, "cores": 1, "kind": "oracle",
-                                "sample": f"one K_D apply of {prob.name} N={prob.n} (oracle setup {t_setup:.0f}s untimed)"}
+        v, t, t_setup, st = cpu_oracle_solve_rate(prob)
+        cpu = host_cpu()
+        line["cpu_baseline"] = {"value": v, "unit": UNIT, "cores": cpu["nproc"], "kind": "oracle",
+                                "sample": f"one full oracle solve of {prob.name} N={prob.n} ({t:.1f} s, "
+                                          f"{st.iters} GMRES iterations, {st.n_applies + 2} interface solves; "
+                                          f"setup {t_setup:.0f} s untimed); scipy.fft workers = {cpu['nproc']} "
+                                          f"host cores, NumPy element-wise serial",
+                                "host": cpu, "solve_s": t, "gpu_speedup_solve": t / t_step}
     if rank == 0:
         print(json.dumps(line))
     if world > 1:

@@ -31,6 +31,21 @@ __device__ __forceinline__ double2 cmul(double2 a, double2 b) {
 __device__ __forceinline__ double2 eipi(const double2* th, const double2* tl, int r) {
   return cmul(th[r >> 6], tl[r & 63]);
 }
+// the same two tables with one 16-byte pad slot after every 8 entries (th: 2N/64 + 2N/512 + 1 slots,
+// tl: 72): lanes whose indices agree mod 8 (even multipliers j) then fall in different bank groups
+__device__ __forceinline__ int eipi_pad(int y) { return y + (y >> 3); }
+__device__ __forceinline__ double2 eipi_p(const double2* th, const double2* tl, int r) {
+  return cmul(th[eipi_pad(r >> 6)], tl[eipi_pad(r & 63)]);
+}
+__device__ __forceinline__ void build_eipi_p(const double* __restrict__ sin_tab, int N, double2* th, double2* tl) {
+  const int m2 = 2 * N - 1;
+  for (int k = threadIdx.x; k < 2 * N / 64; k += blockDim.x) {
+    const int r = 64 * k;
+    th[eipi_pad(k)] = make_double2(sin_lookup(sin_tab, (r + N / 2) & m2, N), sin_lookup(sin_tab, r & m2, N));
+  }
+  for (int l = threadIdx.x; l < 64; l += blockDim.x)
+    tl[eipi_pad(l)] = make_double2(sin_lookup(sin_tab, (l + N / 2) & m2, N), sin_lookup(sin_tab, l & m2, N));
+}
 __device__ __forceinline__ void build_eipi(const double* __restrict__ sin_tab, int N, double2* th, double2* tl) {
   const int m2 = 2 * N - 1;
   for (int k = threadIdx.x; k < 2 * N / 64; k += blockDim.x) {

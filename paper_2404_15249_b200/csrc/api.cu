@@ -221,7 +221,7 @@ void layout(kfbi_ctx* c, Arena& A) {
   c->ycoef = A.take<double>(kMaxRestart + 1);
   c->scal = A.take<double>(8);
   const size_t nseg = S.P >= 2 * BL2 ? S.P / BL2 : 1;
-  c->segbuf = A.take<double>(nseg * 3 * N);
+  c->segbuf = A.take<double>(nseg * 4 * N);
   c->h2 = A.take<double>(nseg * N);
   c->parts = A.take<double>((size_t)std::max(c->world, 1) * M);
   T.sn_i = A.table(S.sn_i);
@@ -252,6 +252,13 @@ void layout3(kfbi_ctx* c, Arena& A) {
   T.max_plane_irr = S.max_plane_irr;
   T.irr_row_ptr = A.table(S.irr_row_ptr); T.zrow_id = A.table(S.zrow_id); T.zrow_ptr = A.table(S.zrow_ptr);
   T.znode_b = A.table(S.znode_b); T.nzrow = (int)S.zrow_id.size(); T.zrow_need = A.table(S.zrow_need);
+  T.world = c->world; T.L3 = S.L3;
+  T.rinv3 = S.L3 >= 0 ? A.table(S.rinv3) : nullptr; T.z3r = S.L3 >= 0 ? A.table(S.z3r) : nullptr;
+  T.red3_a = S.L3 >= 0 ? A.table(S.red3_a) : nullptr; T.red3_b = S.L3 >= 0 ? A.table(S.red3_b) : nullptr;
+  if (c->world > 1) {
+    c->segbuf = A.take<double>((size_t)c->world * 4 * K);   // per slab: first, last, zA_sep, zB_first
+    c->h2 = A.take<double>((size_t)c->world * K);
+  }
   c->nh = 0;
   c->work = A.take<double>((N - 1) * K);
   c->work2 = A.take<double>((N - 1) * K);
@@ -315,6 +322,43 @@ DevTables3 slab3(const kfbi_ctx* c, int r) {
   return T;
 }
 
+// level-2 arrowhead tables of the 3D reduced system tridiag(a, b, a) (P − 1 separators per mode) for
+// slabs of L3 + 1 blocks: the L3 interior separators of a slab are eliminated locally (pivots and the
+// right spike S₂⁻¹e_L), leaving tridiag(A2, B2, A2) on the world − 1 slab separators (App. A.5 applied
+// to the reduced system).  L3 = 0: the slab separators are the whole reduced system.
+void level2_tables3(Setup3& S, int L3) {
+  const size_t K = (size_t)S.N * S.N;
+  S.L3 = L3;
+  S.rinv3.assign((size_t)std::max(L3, 1) * K, 0.0);
+  S.z3r.assign((size_t)std::max(L3, 1) * K, 0.0);
+  S.red3_a.assign(K, 0.0);
+  S.red3_b.assign(K, 1.0);
+#pragma omp parallel for schedule(static)
+  for (long m = 0; m < (long)K; ++m) {
+    const double a = S.red_a[m], bb = S.red_b[m];
+    if (L3 == 0) {
+      S.red3_a[m] = a;
+      S.red3_b[m] = bb;
+      continue;
+    }
+    std::vector<double> cs(L3);
+    double cc = bb;
+    for (int p = 0; p < L3; ++p) {
+      if (p > 0) cc = bb - a * a / cc;
+      cs[p] = cc;
+      S.rinv3[(size_t)p * K + m] = 1.0 / cc;
+    }
+    double x = 1.0 / cs[L3 - 1];   // S₂⁻¹e_L: x_L = 1/c_L, x_p = −a x_{p+1}/c_p
+    S.z3r[(size_t)(L3 - 1) * K + m] = x;
+    for (int p = L3 - 2; p >= 0; --p) {
+      x = -a * x / cs[p];
+      S.z3r[(size_t)p * K + m] = x;
+    }
+    S.red3_a[m] = -a * a * S.z3r[m];
+    S.red3_b[m] = bb - 2.0 * a * a * S.z3r[(size_t)(L3 - 1) * K + m];
+  }
+}
+
 std::vector<int> my_ranks(const kfbi_ctx* c) {
   std::vector<int> v;
   if (c->rank >= 0) v.push_back(c->rank);
@@ -361,8 +405,8 @@ void spectral2(kfbi_ctx* c, const double* cval, const DenseSrc& D, cudaStream_t 
   for (int r : my_ranks(c)) launch_red2_local(slab(c, r), c->zfirst, c->fsep, c->hsep, c->segbuf, s);
   if (c->use_nccl) {
     const DevTables T = slab(c, c->rank);
-    const size_t cnt = (size_t)(T.seg_hi - T.seg_lo) * 3 * T.N;
-    ckn(ncclAllGather(c->segbuf + (size_t)T.seg_lo * 3 * T.N, c->segbuf, cnt, ncclDouble, c->comm, s), "allgather");
+    const size_t cnt = (size_t)(T.seg_hi - T.seg_lo) * 4 * T.N;
+    ckn(ncclAllGather(c->segbuf + (size_t)T.seg_lo * 4 * T.N, c->segbuf, cnt, ncclDouble, c->comm, s), "allgather");
   }
   launch_red2_solve(c->T, c->segbuf, c->h2, s);
   for (int r : my_ranks(c)) launch_red2_fixup(slab(c, r), c->h2, c->hsep, s);
@@ -484,6 +528,25 @@ void inverse3(kfbi_ctx* c, double* u, cudaStream_t s) {   // u == NULL: result s
 // and the z-evaluation of its own slab; the block end values (zB, zA: P/world rows each) are
 // all-gathered, every rank solves the (cheap) reduced system for all modes, and the interpolation
 // partial sums (plane owner contributes) are all-reduced.  rank = −1 emulates all slabs in one ctx.
+// reduced (separator) system of the sweeps just run.  world > 1: every slab eliminates its interior
+// separators, publishes 4 values per mode (first, last, its boundary separator's zA, its first
+// block's zB), one all-gather (4·K doubles per rank; the 2D path's level-2 scheme), every
+// rank solves the world − 1 slab separators per mode, and fixes up its own interior separators.
+void reduced3_dist(kfbi_ctx* c, cudaStream_t s) {
+  const DevTables3& T = c->T3;
+  if (c->world == 1) {
+    launch_reduced3(T, c->zfirst, c->fsep, c->hsep, s);
+    return;
+  }
+  for (int r : my_ranks(c)) launch_red3_local(slab3(c, r), c->zfirst, c->fsep, c->hsep, c->segbuf, s);
+  if (c->use_nccl) {
+    const size_t cnt = (size_t)4 * T.N * T.N;
+    ckn(ncclAllGather(c->segbuf + (size_t)c->rank * cnt, c->segbuf, cnt, ncclDouble, c->comm, s), "allgather");
+  }
+  launch_red3_solve(T, c->segbuf, c->h2, s);
+  for (int r : my_ranks(c)) launch_red3_fixup(slab3(c, r), c->h2, c->hsep, s);
+}
+
 void apply_KD3(kfbi_ctx* c, const double* phi, double* out, cudaStream_t s) {
   const DevTables3& T = c->T3;
   const double sc = 2.0 / T.N;
@@ -494,15 +557,7 @@ void apply_KD3(kfbi_ctx* c, const double* phi, double* out, cudaStream_t s) {
     launch_sparse3(Ts, 0, c->corr, nullptr, 1.0, c->work, s);
     launch_sweep3(Ts, c->work, c->zfirst, c->fsep, s);
   }
-  if (c->use_nccl) {
-    const DevTables3 Ts = slab3(c, c->rank);
-    const size_t K = (size_t)T.N * T.N, cnt = (size_t)(Ts.b_hi - Ts.b_lo) * K;
-    ckn(ncclGroupStart(), "group");
-    ckn(ncclAllGather(c->zfirst + (size_t)Ts.b_lo * K, c->zfirst, cnt, ncclDouble, c->comm, s), "allgather zB");
-    ckn(ncclAllGather(c->fsep + (size_t)Ts.b_lo * K, c->fsep, cnt, ncclDouble, c->comm, s), "allgather zA");
-    ckn(ncclGroupEnd(), "group");
-  }
-  launch_reduced3(T, c->zfirst, c->fsep, c->hsep, s);
+  reduced3_dist(c, s);
   for (int r : my_ranks(c)) {
     const DevTables3 Ts = slab3(c, r);
     launch_sparse3(Ts, 1, c->work, c->hsep, sc, c->work2, s);
@@ -594,6 +649,7 @@ kfbi_status setup_impl(const kfbi_grid* grid, const kfbi_boundary* bnd, const kf
     if (c->world > 1) {
       if (c->dim == 3) {
         if (c->S3.P < c->world || c->S3.P % c->world) throw ArgError("3D: world must divide N/16 (slabs = ADM blocks)");
+        level2_tables3(c->S3, c->S3.P / c->world - 1);
       } else {
         const int nseg = c->S.P >= 2 * BL2 ? c->S.P / BL2 : 1;
         if (nseg < c->world || nseg % c->world) throw ArgError("world must divide N/512 (slabs = level-2 segments)");

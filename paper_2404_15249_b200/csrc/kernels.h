@@ -75,7 +75,8 @@ void launch_interp(const DevTables& T, const double* phi, const double* mk, cons
                    const double* jz_given, const double* vsten, int nh, const double* wg, const double* a,
                    double* out, cudaStream_t s, bool partial = false);
 // multi-GPU split of the level-2 reduced solve (segments = slabs): local segment solves for the
-// owned segments [seg_lo, seg_hi) → seg buffer [seg][3][N] (first, last, separator rhs); level-2 solve
+// owned segments [seg_lo, seg_hi) → seg buffer [seg][4][N] (first, last, zA of the segment's boundary
+// separator, zB of its first block); level-2 solve
 // for all segments (after the all-gather) → h2 [seg][N]; fix-up of the owned segments' separators
 void launch_red2_local(const DevTables& T, const double* zB, const double* zA, double* hsep, double* segbuf,
                        cudaStream_t s);
@@ -121,6 +122,13 @@ void launch_dst_rows3(const DevTables3& T, int mode, double* work, const double*
 void launch_transpose3(const DevTables3& T, double* work, cudaStream_t s);
 void launch_sweep3(const DevTables3& T, double* work, double* zB, double* zA, cudaStream_t s);
 void launch_reduced3(const DevTables3& T, const double* zB, const double* zA, double* hsep, cudaStream_t s);
+// multi-GPU level-2 split of the 3D reduced system (slab = P/world blocks): interior separators of the
+// slab [b_lo, b_hi) → hsep + segbuf[rank][4][K]; level-2 solve of the world − 1 slab separators → h2;
+// fix-up of the slab's interior separators and its boundary separators in hsep
+void launch_red3_local(const DevTables3& T, const double* zB, const double* zA, double* hsep, double* segbuf,
+                       cudaStream_t s);
+void launch_red3_solve(const DevTables3& T, const double* segbuf, double* h2, cudaStream_t s);
+void launch_red3_fixup(const DevTables3& T, const double* h2, double* hsep, cudaStream_t s);
 // partial: only stencil nodes in the slab's planes [i_lo, i_hi] contribute (multi-GPU partial sums)
 void launch_interp3(const DevTables3& T, const double* phi, const double* dphi, const double* fz,
                     const double* jz_given, const double* work, double* out, cudaStream_t s, bool partial = false);

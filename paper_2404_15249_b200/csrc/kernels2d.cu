@@ -467,7 +467,10 @@ __global__ void __launch_bounds__(512) k_reduced2(DevTables T, const double* __r
 }
 
 // ---- multi-GPU split of k_reduced2: the level-2 segments are the slabs' separator groups ----
-// (1) owned segments: local level-2 block solve, z kept in hsep, (first, last, rhs_sep) → segbuf
+// (1) owned segments: local level-2 block solve, z kept in hsep; segbuf[sg][4][N] = (first z, last z,
+// zA of the segment's right boundary separator, zB of its first block).  The boundary separator's
+// right-hand side zA[gs] − zB[gs + 1] joins one value from each side of a slab cut, so it is formed
+// after the exchange from rows both owners publish (no rank reads another slab's blocks).
 __global__ void k_red2_local(DevTables T, const double* __restrict__ zB, const double* __restrict__ zA,
                              double* __restrict__ hsep, double* __restrict__ segbuf) {
   const int N = T.N, S = T.nseg;
@@ -480,21 +483,20 @@ __global__ void k_red2_local(DevTables T, const double* __restrict__ zB, const d
 #pragma unroll
   for (int p = 0; p < LB2; ++p) {
     const int g = gbase + p;
-    const double r = zA[(size_t)g * N + k] - zB[(size_t)(g + 1) * N + k];
-    z[p] = p ? fma(-a * z[p - 1], T.rinv2[(size_t)(p - 1) * N + k], r) : r;
+    z[p] = zA[(size_t)g * N + k] - zB[(size_t)(g + 1) * N + k];
   }
+#pragma unroll
+  for (int p = 1; p < LB2; ++p) z[p] = fma(-a * z[p - 1], T.rinv2[(size_t)(p - 1) * N + k], z[p]);
   z[LB2 - 1] *= T.rinv2[(size_t)(LB2 - 1) * N + k];
 #pragma unroll
   for (int p = LB2 - 2; p >= 0; --p) z[p] = (z[p] - a * z[p + 1]) * T.rinv2[(size_t)p * N + k];
 #pragma unroll
   for (int p = 0; p < LB2; ++p) hsep[(size_t)(gbase + p) * N + k] = z[p];
-  double* sb = segbuf + (size_t)sg * 3 * N;
+  double* sb = segbuf + (size_t)sg * 4 * N;
   sb[k] = z[0];
   sb[N + k] = z[LB2 - 1];
-  if (sg < S - 1) {
-    const int gs = gbase + LB2;
-    sb[2 * N + k] = zA[(size_t)gs * N + k] - zB[(size_t)(gs + 1) * N + k];
-  }
+  sb[2 * N + k] = sg < S - 1 ? zA[(size_t)(gbase + LB2) * N + k] : 0.0;
+  sb[3 * N + k] = zB[(size_t)gbase * N + k];
 }
 
 // (2) every rank: the level-2 tridiagonal system of the S − 1 slab separators per mode
@@ -505,9 +507,9 @@ __global__ void k_red2_solve(DevTables T, const double* __restrict__ segbuf, dou
   const double a = T.red_a[k], A2 = T.red2_a[k], B2 = T.red2_b[k];
   double c = B2, yprev = 0.0, ciprev = 0.0;
   for (int q = 0; q < S - 1; ++q) {
-    const double* sq = segbuf + (size_t)q * 3 * N;
-    const double* sn = segbuf + (size_t)(q + 1) * 3 * N;
-    const double r = sq[2 * N + k] - a * sq[N + k] - a * sn[k];
+    const double* sq = segbuf + (size_t)q * 4 * N;
+    const double* sn = segbuf + (size_t)(q + 1) * 4 * N;
+    const double r = (sq[2 * N + k] - sn[3 * N + k]) - a * sq[N + k] - a * sn[k];
     if (q) c = B2 - A2 * A2 * ciprev;
     const double ci = 1.0 / c;
     const double y = q ? r - A2 * yprev * ciprev : r;

@@ -614,6 +614,109 @@ __global__ void k_reduced3(DevTables3 T, const double* __restrict__ zB, const do
   }
 }
 
+// ---- multi-GPU level-2 split of the reduced system (slab r = blocks [b_lo, b_hi), see api.cu) ----
+// (1) the slab's L3 interior separators b_lo .. b_hi − 2 (right-hand sides zA[g] − zB[g + 1] from the
+// slab's own blocks) by Thomas with the level-2 pivots; segbuf[r] = (first, last, zA[b_hi − 1], zB[b_lo])
+__global__ void k_red3_local(DevTables3 T, const double* __restrict__ zB, const double* __restrict__ zA,
+                             double* __restrict__ hsep, double* __restrict__ segbuf) {
+  const int N = T.N, L3 = T.L3, g0 = T.b_lo;
+  const size_t K = (size_t)N * N;
+  const size_t m = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (m >= K) return;
+  double* sb = segbuf + (size_t)T.rank * 4 * K;
+  const int ll = (int)(m / N), kk = (int)(m % N);
+  if (ll == 0 || kk == 0) {   // not a mode (k_sweep3 leaves these rows untouched)
+    for (int p = 0; p < L3; ++p) hsep[(size_t)(g0 + p) * K + m] = 0.0;
+    sb[m] = sb[K + m] = sb[2 * K + m] = sb[3 * K + m] = 0.0;
+    return;
+  }
+  const double a = T.red_a[m];
+  double z = 0.0;
+  for (int p = 0; p < L3; ++p) {
+    const int g = g0 + p;
+    const double r = zA[(size_t)g * K + m] - zB[(size_t)(g + 1) * K + m];
+    z = p ? fma(-a * z, T.rinv3[(size_t)(p - 1) * K + m], r) : r;
+    hsep[(size_t)g * K + m] = z;
+  }
+  double first = 0.0, last = 0.0;
+  if (L3 > 0) {
+    z *= T.rinv3[(size_t)(L3 - 1) * K + m];
+    last = z;
+    hsep[(size_t)(g0 + L3 - 1) * K + m] = z;
+    for (int p = L3 - 2; p >= 0; --p) {
+      z = (hsep[(size_t)(g0 + p) * K + m] - a * z) * T.rinv3[(size_t)p * K + m];
+      hsep[(size_t)(g0 + p) * K + m] = z;
+    }
+    first = z;
+  }
+  sb[m] = first;
+  sb[K + m] = last;
+  sb[2 * K + m] = T.b_hi < T.P ? zA[(size_t)(T.b_hi - 1) * K + m] : 0.0;
+  sb[3 * K + m] = zB[(size_t)g0 * K + m];
+}
+
+// (2) every rank: tridiag(A2, B2, A2) on the world − 1 slab separators per mode, right-hand side
+// zA[s] − zB[s + 1] − a·last_q − a·first_{q+1} (the two halves from the slabs on either side)
+__global__ void k_red3_solve(DevTables3 T, const double* __restrict__ segbuf, double* __restrict__ h2) {
+  const int N = T.N, W = T.world, L3 = T.L3;
+  const size_t K = (size_t)N * N;
+  const size_t m = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (m >= K || W < 2) return;
+  const int ll = (int)(m / N), kk = (int)(m % N);
+  if (ll == 0 || kk == 0) {
+    for (int q = 0; q < W - 1; ++q) h2[(size_t)q * K + m] = 0.0;
+    return;
+  }
+  const double a = T.red_a[m], A2 = T.red3_a[m], B2 = T.red3_b[m];
+  double c = B2, y = 0.0, ci = 0.0;
+  for (int q = 0; q < W - 1; ++q) {
+    const double* sq = segbuf + (size_t)q * 4 * K;
+    const double* sn = segbuf + (size_t)(q + 1) * 4 * K;
+    double r = sq[2 * K + m] - sn[3 * K + m];
+    if (L3 > 0) r -= a * sq[K + m] + a * sn[m];
+    if (q) c = B2 - A2 * A2 * ci;
+    y = q ? r - A2 * y * ci : r;
+    ci = 1.0 / c;
+    h2[(size_t)q * K + m] = y;
+  }
+  double cinv[64];   // world ≤ 64
+  double cc = B2;
+  for (int q = 0; q < W - 1; ++q) {
+    if (q) cc = B2 - A2 * A2 * cinv[q - 1];
+    cinv[q] = 1.0 / cc;
+  }
+  double hn = h2[(size_t)(W - 2) * K + m] * cinv[W - 2];
+  h2[(size_t)(W - 2) * K + m] = hn;
+  for (int q = W - 3; q >= 0; --q) {
+    hn = (h2[(size_t)q * K + m] - A2 * hn) * cinv[q];
+    h2[(size_t)q * K + m] = hn;
+  }
+}
+
+// (3) the slab's interior separators x = z − a h2_{r−1} Z2_L[p] − a h2_r Z2_R[p], and its two slab
+// separators (the values the fixed-up inverse of the slab's planes reads)
+__global__ void k_red3_fixup(DevTables3 T, const double* __restrict__ h2, double* __restrict__ hsep) {
+  const int N = T.N, W = T.world, L3 = T.L3, r = T.rank, g0 = T.b_lo;
+  const size_t K = (size_t)N * N;
+  const size_t m = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (m >= K) return;
+  const int ll = (int)(m / N), kk = (int)(m % N);
+  const bool mode = ll != 0 && kk != 0;
+  const double a = mode ? T.red_a[m] : 0.0;
+  const double hl = r > 0 ? a * h2[(size_t)(r - 1) * K + m] : 0.0;
+  const double hr = r < W - 1 ? a * h2[(size_t)r * K + m] : 0.0;
+  for (int p = 0; p < L3; ++p) {
+    double x = hsep[(size_t)(g0 + p) * K + m];
+    if (mode) {
+      x = fma(-hl, T.z3r[(size_t)(L3 - 1 - p) * K + m], x);   // Z2_L[p] = Z2_R[L3 − 1 − p]
+      x = fma(-hr, T.z3r[(size_t)p * K + m], x);
+    }
+    hsep[(size_t)(g0 + p) * K + m] = x;
+  }
+  if (r < W - 1) hsep[(size_t)(T.b_hi - 1) * K + m] = mode ? h2[(size_t)r * K + m] : 0.0;
+  if (r > 0) hsep[(size_t)(g0 - 1) * K + m] = mode ? h2[(size_t)(r - 1) * K + m] : 0.0;
+}
+
 // A7 (3D): ten-point interpolation at the control points
 __global__ void k_interp3(DevTables3 T, const double* __restrict__ phi, const double* __restrict__ dphi,
                           const double* __restrict__ fz, const double* __restrict__ jg, const double* __restrict__ work,
@@ -731,6 +834,19 @@ void launch_reduced3(const DevTables3& T, const double* zB, const double* zA, do
   if (T.P < 2) return;
   ++g_launches;
   k_reduced3<<<cdiv3((long)T.N * T.N, 128), 128, 0, s>>>(T, zB, zA, hsep);
+}
+void launch_red3_local(const DevTables3& T, const double* zB, const double* zA, double* hsep, double* segbuf,
+                       cudaStream_t s) {
+  ++g_launches;
+  k_red3_local<<<cdiv3((long)T.N * T.N, 128), 128, 0, s>>>(T, zB, zA, hsep, segbuf);
+}
+void launch_red3_solve(const DevTables3& T, const double* segbuf, double* h2, cudaStream_t s) {
+  ++g_launches;
+  k_red3_solve<<<cdiv3((long)T.N * T.N, 128), 128, 0, s>>>(T, segbuf, h2);
+}
+void launch_red3_fixup(const DevTables3& T, const double* h2, double* hsep, cudaStream_t s) {
+  ++g_launches;
+  k_red3_fixup<<<cdiv3((long)T.N * T.N, 128), 128, 0, s>>>(T, h2, hsep);
 }
 void launch_interp3(const DevTables3& T, const double* phi, const double* dphi, const double* fz,
                     const double* jz_given, const double* work, double* out, cudaStream_t s, bool partial) {

@@ -176,6 +176,11 @@ struct Setup3 {
   int max_plane_irr = 0;
   std::vector<int32_t> zrow_id, zrow_ptr, znode_b;   // distinct stencil nodes grouped by grid row
   std::vector<uint8_t> zrow_need;                    // (N−1)·N: 1 if grid row (i−1)·N + a holds stencil nodes
+  // multi-GPU level-2 split of the reduced system (world > 1): slabs of P/world blocks hold
+  // L3 = P/world − 1 interior separators each (pivots rinv3, spike z3r: L3 × K), the world − 1 slab
+  // separators solve tridiag(red3_a, red3_b, red3_a) per mode after the exchange
+  int L3 = -1;
+  std::vector<double> rinv3, z3r, red3_a, red3_b;
 };
 void build_setup3(Setup3& S, const kfbi_grid* g, const kfbi_boundary* b, const kfbi_pde* pde);
 
@@ -205,6 +210,8 @@ struct DevTables3 {
   int rank, b_lo, b_hi, i_lo, i_hi, w_lo, w_hi;
   int nzrow;
   const int8_t* side;
+  int world, L3;   // level-2 split of the reduced system (world > 1)
+  const double *rinv3, *z3r, *red3_a, *red3_b;
 };
 
 // ---- device views -------------------------------------------------------------------

@@ -130,10 +130,13 @@ def test_solve3d_C5_256():
 
 
 # ------------------------------------------------------------------ multi-GPU partition (emulated)
-@pytest.mark.parametrize("prob,world", [(W.C4(64), 2), (W.C4(64), 4), (W.C5(128), 8)], ids=["C4-64x2", "C4-64x4", "C5-128x8"])
+@pytest.mark.parametrize("prob,world", [(W.C4(64), 2), (W.C4(64), 4), (W.C5(128), 8), (W.C5(128), 2), (W.C5(256), 4)],
+                         ids=["C4-64x2", "C4-64x4", "C5-128x8", "C5-128x2", "C5-256x4"])
 def test_partitioned_apply3d_matches_single(prob, world):
-    """All slabs in one context (rank = −1): block sweeps per slab, the gathered reduced system and the
-    disjoint partial interpolation sums reproduce world = 1 (to summation order) and the oracle."""
+    """All slabs in one context (rank = −1): block sweeps per slab, the level-2 split of the reduced
+    system (slab interior separators eliminated locally, L3 = P/world − 1 = 1, 0, 0, 3, 3 here; the
+    world − 1 slab separators solved after the 4-row exchange) and the disjoint partial interpolation
+    sums reproduce world = 1 (to summation order) and the oracle."""
     k1 = gpu(prob)
     kw = KFBI(prob, world=world, rank=-1)
     for seed in (0, 1):

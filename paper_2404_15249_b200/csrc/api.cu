@@ -253,6 +253,8 @@ void layout3(kfbi_ctx* c, Arena& A) {
   T.irr_row_ptr = A.table(S.irr_row_ptr); T.zrow_id = A.table(S.zrow_id); T.zrow_ptr = A.table(S.zrow_ptr);
   T.znode_b = A.table(S.znode_b); T.nzrow = (int)S.zrow_id.size(); T.zrow_need = A.table(S.zrow_need);
   T.world = c->world; T.L3 = S.L3;
+  T.q_lo[0] = 0; T.q_hi[0] = S.nq; T.q_lo[1] = T.q_hi[1] = T.q_lo[2] = T.q_hi[2] = S.nq;
+  T.n_lo = 0; T.n_hi = S.nirr;
   T.rinv3 = S.L3 >= 0 ? A.table(S.rinv3) : nullptr; T.z3r = S.L3 >= 0 ? A.table(S.z3r) : nullptr;
   T.red3_a = S.L3 >= 0 ? A.table(S.red3_a) : nullptr; T.red3_b = S.L3 >= 0 ? A.table(S.red3_b) : nullptr;
   if (c->world > 1) {
@@ -311,7 +313,7 @@ DevTables3 slab3(const kfbi_ctx* c, int r) {
   const Setup3& S = c->S3;
   const int world = c->world;
   T.rank = r;
-  if (world == 1) return T;
+  if (world == 1) return T;   // c->T3 holds the full ranges (layout3)
   T.b_lo = r * S.P / world;
   T.b_hi = (r + 1) * S.P / world;
   T.i_lo = BL * T.b_lo + 1;
@@ -319,6 +321,26 @@ DevTables3 slab3(const kfbi_ctx* c, int r) {
   auto row0 = [&](int i) { return (int32_t)((int64_t)(i - 1) * S.N); };
   T.w_lo = (int)(std::lower_bound(S.zrow_id.begin(), S.zrow_id.end(), row0(T.i_lo)) - S.zrow_id.begin());
   T.w_hi = (int)(std::lower_bound(S.zrow_id.begin(), S.zrow_id.end(), row0(T.i_hi + 1)) - S.zrow_id.begin());
+  // point work of the slab: the control points whose LSQ derivatives the slab's corrections and
+  // partial interpolation sums use (intersections of its irregular nodes' edges: low-end plane
+  // i − 1 … i; stencil nodes c ± 1 of a control point in the slab: low-end plane ≥ i_lo − 2)
+  for (int a = 0; a < 3; ++a) {
+    auto key_lt = [&](int q, int i) { return S.q_axis[q] < a || (S.q_axis[q] == a && S.q_i[q] < i); };
+    int lo = 0, hi = S.nq;
+    while (lo < hi) { const int mid = (lo + hi) / 2; if (key_lt(mid, T.i_lo - 2)) lo = mid + 1; else hi = mid; }
+    T.q_lo[a] = lo;
+    hi = S.nq;
+    while (lo < hi) { const int mid = (lo + hi) / 2; if (key_lt(mid, T.i_hi + 3)) lo = mid + 1; else hi = mid; }
+    T.q_hi[a] = lo;
+  }
+  {
+    int lo = 0, hi = S.nirr;
+    while (lo < hi) { const int mid = (lo + hi) / 2; if (S.irr_ijk[3 * mid] < T.i_lo) lo = mid + 1; else hi = mid; }
+    T.n_lo = lo;
+    hi = S.nirr;
+    while (lo < hi) { const int mid = (lo + hi) / 2; if (S.irr_ijk[3 * mid] <= T.i_hi) lo = mid + 1; else hi = mid; }
+    T.n_hi = lo;
+  }
   return T;
 }
 
@@ -501,27 +523,58 @@ void final_field2(kfbi_ctx* c, const double* phi, const double* fgrid, const dou
 // --- 3D interface solves (control points = intersection nodes, R12) -------------------
 // rows: DST along z (source h²·f·1_Ω + compact corrections built on load), transpose, DST along y
 // (from_work: the source is already in the working array, e.g. the test entry points)
+void reduced3_dist(kfbi_ctx* c, cudaStream_t s);
+// dense forward of the slab planes (all of them for world = 1 or the emulation): z-DST of the rows with
+// the source built on load, transpose, y-DST, block sweeps, then the (distributed) reduced system
 void forward3(kfbi_ctx* c, const double* fgrid, cudaStream_t s, bool from_work = false) {
-  if (from_work) launch_dst_rows3(c->T3, 0, c->work, nullptr, 1.0, nullptr, s);
-  else launch_dst_rows3(c->T3, 3, c->work, nullptr, 1.0, nullptr, s, fgrid, c->corr);
-  launch_transpose3(c->T3, c->work, s);
-  launch_dst_rows3(c->T3, 0, c->work, nullptr, 1.0, nullptr, s);
-  launch_sweep3(c->T3, c->work, c->zfirst, c->fsep, s);
-  launch_reduced3(c->T3, c->zfirst, c->fsep, c->hsep, s);
+  for (int r : my_ranks(c)) {
+    const DevTables3 Ts = slab3(c, r);
+    if (from_work) launch_dst_rows3(Ts, 0, c->work, nullptr, 1.0, nullptr, s);
+    else launch_dst_rows3(Ts, 3, c->work, nullptr, 1.0, nullptr, s, fgrid, c->corr);
+    launch_transpose3(Ts, c->work, s);
+    launch_dst_rows3(Ts, 0, c->work, nullptr, 1.0, nullptr, s);
+    launch_sweep3(Ts, c->work, c->zfirst, c->fsep, s);
+  }
+  reduced3_dist(c, s);
 }
 void inverse3(kfbi_ctx* c, double* u, cudaStream_t s) {   // u == NULL: result stays in work
   const double sc = 2.0 / c->T3.N;
-  launch_dst_rows3(c->T3, 1, c->work, c->hsep, sc, nullptr, s);
-  launch_transpose3(c->T3, c->work, s);
-  if (!u) {
-    launch_dst_rows3(c->T3, 0, c->work, nullptr, sc, nullptr, s);
-    return;
+  for (int r : my_ranks(c)) {
+    const DevTables3 Ts = slab3(c, r);
+    launch_dst_rows3(Ts, 1, c->work, c->hsep, sc, nullptr, s);
+    launch_transpose3(Ts, c->work, s);
+    if (!u) launch_dst_rows3(Ts, 0, c->work, nullptr, sc, nullptr, s);
+    else launch_dst_rows3(Ts, 2, c->work, nullptr, sc, u, s);   // the slab's planes of u
   }
-  launch_dst_rows3(c->T3, 2, c->work, nullptr, sc, u, s);
+  if (!u) return;
   const size_t W = (size_t)c->T3.N + 1;
   ck(cudaMemsetAsync(u, 0, W * W * sizeof(double), s), "memset");
   ck(cudaMemsetAsync(u + (size_t)c->T3.N * W * W, 0, W * W * sizeof(double), s), "memset");
   ck(cudaMemset2DAsync(u + (W + c->T3.N) * W, W * W * sizeof(double), 0, W * sizeof(double), c->T3.N - 1, s), "memset");
+}
+// the slab's sparse inverse (y-rows, z at the stencil nodes) and the interpolation (partial sums of the
+// slabs, all-reduced) — shared by the K_D and Y applies
+void interp3_dist(kfbi_ctx* c, const double* phi, const double* fz, double* out, cudaStream_t s) {
+  const DevTables3& T = c->T3;
+  const double sc = 2.0 / T.N;
+  for (int r : my_ranks(c)) {
+    const DevTables3 Ts = slab3(c, r);
+    launch_sparse3(Ts, 1, c->work, c->hsep, sc, c->work2, s);
+    launch_sparse3(Ts, 2, c->work2, nullptr, sc, c->work, s);
+  }
+  if (c->world == 1) {
+    launch_interp3(T, phi, c->dphi, fz, nullptr, c->work, out, s);
+    return;
+  }
+  const int M = T.nq;
+  if (c->use_nccl) {
+    launch_interp3(slab3(c, c->rank), phi, c->dphi, fz, nullptr, c->work, c->parts, s, true);
+    ckn(ncclAllReduce(c->parts, out, M, ncclDouble, ncclSum, c->comm, s), "allreduce");
+    return;
+  }
+  for (int r : my_ranks(c))
+    launch_interp3(slab3(c, r), phi, c->dphi, fz, nullptr, c->work, c->parts + (size_t)r * M, s, true);
+  launch_sum_parts(M, c->world, c->parts, out, s);
 }
 // K_D (the GMRES operator): sparse source, sparse read-out — no dense z-direction transforms
 // Multi-GPU: each rank runs the sparse forward, the block sweeps, the y-inverse
@@ -548,47 +601,30 @@ void reduced3_dist(kfbi_ctx* c, cudaStream_t s) {
 }
 
 void apply_KD3(kfbi_ctx* c, const double* phi, double* out, cudaStream_t s) {
-  const DevTables3& T = c->T3;
-  const double sc = 2.0 / T.N;
-  launch_lsq3(T, phi, c->dphi, s);
-  launch_correct3(T, phi, c->dphi, nullptr, nullptr, nullptr, s, c->corr);
+  for (int r : my_ranks(c)) {   // the slab's control points and irregular nodes only
+    const DevTables3 Ts = slab3(c, r);
+    launch_lsq3(Ts, phi, c->dphi, s);
+    launch_correct3(Ts, phi, c->dphi, nullptr, nullptr, nullptr, s, c->corr);
+  }
   for (int r : my_ranks(c)) {
     const DevTables3 Ts = slab3(c, r);
     launch_sparse3(Ts, 0, c->corr, nullptr, 1.0, c->work, s);
     launch_sweep3(Ts, c->work, c->zfirst, c->fsep, s);
   }
   reduced3_dist(c, s);
-  for (int r : my_ranks(c)) {
-    const DevTables3 Ts = slab3(c, r);
-    launch_sparse3(Ts, 1, c->work, c->hsep, sc, c->work2, s);
-    launch_sparse3(Ts, 2, c->work2, nullptr, sc, c->work, s);
-  }
-  if (c->world == 1) {
-    launch_interp3(T, phi, c->dphi, nullptr, nullptr, c->work, out, s);
-    return;
-  }
-  const int M = T.nq;
-  if (c->use_nccl) {
-    launch_interp3(slab3(c, c->rank), phi, c->dphi, nullptr, nullptr, c->work, c->parts, s, true);
-    ckn(ncclAllReduce(c->parts, out, M, ncclDouble, ncclSum, c->comm, s), "allreduce");
-    return;
-  }
-  for (int r : my_ranks(c))
-    launch_interp3(slab3(c, r), phi, c->dphi, nullptr, nullptr, c->work, c->parts + (size_t)r * M, s, true);
-  launch_sum_parts(M, c->world, c->parts, out, s);
+  interp3_dist(c, phi, nullptr, out, s);
 }
 void apply_Y3(kfbi_ctx* c, const double* fgrid, const double* fq, const double* fz, double* out, cudaStream_t s) {
-  launch_correct3(c->T3, nullptr, nullptr, fq, nullptr, nullptr, s, c->corr);
+  for (int r : my_ranks(c)) launch_correct3(slab3(c, r), nullptr, nullptr, fq, nullptr, nullptr, s, c->corr);
   forward3(c, fgrid, s);
-  // only the stencil nodes are read: the K_D path's sparse inverse (y-rows, z at the nodes)
-  const double sc = 2.0 / c->T3.N;
-  launch_sparse3(c->T3, 1, c->work, c->hsep, sc, c->work2, s);
-  launch_sparse3(c->T3, 2, c->work2, nullptr, sc, c->work, s);
-  launch_interp3(c->T3, nullptr, nullptr, fz, nullptr, c->work, out, s);
+  interp3_dist(c, nullptr, fz, out, s);   // only the stencil nodes are read
 }
 void final_field3(kfbi_ctx* c, const double* phi, const double* fgrid, const double* fq, double* u, cudaStream_t s) {
-  launch_lsq3(c->T3, phi, c->dphi, s);
-  launch_correct3(c->T3, phi, c->dphi, fq, nullptr, nullptr, s, c->corr);
+  for (int r : my_ranks(c)) {
+    const DevTables3 Ts = slab3(c, r);
+    launch_lsq3(Ts, phi, c->dphi, s);
+    launch_correct3(Ts, phi, c->dphi, fq, nullptr, nullptr, s, c->corr);
+  }
   forward3(c, fgrid, s);
   inverse3(c, u, s);
 }

@@ -80,8 +80,11 @@ __device__ __forceinline__ void load_jump3(const DevTables3& T, int q, const dou
 
 // A1 (3D): tangent-plane LSQ fit (reading R12) with the precomputed scaled normal-matrix inverse.
 __global__ void k_lsq3(DevTables3 T, const double* __restrict__ phi, double* __restrict__ dphi) {
-  const int e = blockIdx.x * blockDim.x + threadIdx.x;
-  if (e >= T.nq) return;
+  // thread t → the t-th control point of the slab's three per-axis ranges
+  int e = blockIdx.x * blockDim.x + threadIdx.x;
+  const int n0 = T.q_hi[0] - T.q_lo[0], n1 = T.q_hi[1] - T.q_lo[1], n2 = T.q_hi[2] - T.q_lo[2];
+  if (e >= n0 + n1 + n2) return;
+  e = e < n0 ? T.q_lo[0] + e : (e < n0 + n1 ? T.q_lo[1] + e - n0 : T.q_lo[2] + e - n0 - n1);
   const double ih = 1.0 / T.h;
   const double x0 = T.q_pos[3 * e], y0 = T.q_pos[3 * e + 1], z0 = T.q_pos[3 * e + 2];
   const double* e1 = T.q_e1 + 3 * e;
@@ -142,8 +145,8 @@ __global__ void k_base3(DevTables3 T, const double* __restrict__ f, double* __re
 __global__ void k_correct3(DevTables3 T, const double* __restrict__ phi, const double* __restrict__ dphi,
                            const double* __restrict__ fq, const double* __restrict__ jg, double* __restrict__ work,
                            double* __restrict__ corr) {
-  const int n = blockIdx.x * blockDim.x + threadIdx.x;
-  if (n >= T.nirr) return;
+  const int n = T.n_lo + blockIdx.x * blockDim.x + threadIdx.x;   // the slab's irregular nodes
+  if (n >= T.n_hi) return;
   double acc = 0.0;
   for (int e = T.irr_ptr[n]; e < T.irr_ptr[n + 1]; ++e) {
     const int q = T.pair_q[e];
@@ -222,8 +225,8 @@ __global__ void __launch_bounds__(256, 2) k_dst_rows3t(DevTables3 T, double* wor
   const int rl = threadIdx.x / NTL, tid = threadIdx.x % NTL;
   double2* z = smz + rl * ZS;
   const double2* __restrict__ tw = reinterpret_cast<const double2*>(T.tw);
-  const size_t row = (size_t)blockIdx.x * RPC + rl;   // (i−1)·N + a
-  const bool live = row < (size_t)(N - 1) * N;
+  const size_t row = (size_t)(T.i_lo - 1) * N + (size_t)blockIdx.x * RPC + rl;   // (i−1)·N + a, slab planes
+  const bool live = row < (size_t)T.i_hi * N;
   const int i = (int)(row / N) + 1, a = (int)(row % N);
   double* rp = work + row * N;
   if (MODE == 1 && live) {
@@ -724,9 +727,13 @@ __global__ void k_interp3(DevTables3 T, const double* __restrict__ phi, const do
   const int e = blockIdx.x * blockDim.x + threadIdx.x;
   if (e >= T.nq) return;
   const int N = T.N;
+  const int c0 = T.st_c[3 * e], c1 = T.st_c[3 * e + 1], c2 = T.st_c[3 * e + 2];
+  if (partial && (c0 + 1 < T.i_lo || c0 - 1 > T.i_hi)) {   // no stencil node in the slab
+    out[e] = 0.0;
+    return;
+  }
   Jump10 J;
   load_jump3(T, e, phi, dphi, fz, jg, J);
-  const int c0 = T.st_c[3 * e], c1 = T.st_c[3 * e + 1], c2 = T.st_c[3 * e + 2];
   const int code = T.st_code[e];
   const int s0 = (code >> 10) & 1 ? 1 : -1, s1 = (code >> 11) & 1 ? 1 : -1, s2 = (code >> 12) & 1 ? 1 : -1;
   const int off[10][3] = {{0, 0, 0}, {1, 0, 0}, {-1, 0, 0}, {0, 1, 0}, {0, -1, 0}, {0, 0, 1}, {0, 0, -1},
@@ -753,8 +760,10 @@ inline int cdiv3(long a, long b) { return (int)((a + b - 1) / b); }
 }  // namespace
 
 void launch_lsq3(const DevTables3& T, const double* phi, double* dphi, cudaStream_t s) {
+  const int n = T.q_hi[0] - T.q_lo[0] + T.q_hi[1] - T.q_lo[1] + T.q_hi[2] - T.q_lo[2];
+  if (n <= 0) return;
   ++g_launches;
-  k_lsq3<<<cdiv3(T.nq, 128), 128, 0, s>>>(T, phi, dphi);
+  k_lsq3<<<cdiv3(n, 128), 128, 0, s>>>(T, phi, dphi);
 }
 void launch_base3(const DevTables3& T, const double* fgrid, double* work, cudaStream_t s) {
   ++g_launches;
@@ -762,16 +771,16 @@ void launch_base3(const DevTables3& T, const double* fgrid, double* work, cudaSt
 }
 void launch_correct3(const DevTables3& T, const double* phi, const double* dphi, const double* fq,
                      const double* jq_given, double* work, cudaStream_t s, double* corr) {
-  if (!T.nirr) return;
+  if (T.n_hi <= T.n_lo) return;
   ++g_launches;
-  k_correct3<<<cdiv3(T.nirr, 128), 128, 0, s>>>(T, phi, dphi, fq, jq_given, work, corr);
+  k_correct3<<<cdiv3(T.n_hi - T.n_lo, 128), 128, 0, s>>>(T, phi, dphi, fq, jq_given, work, corr);
 }
 template <int N>
 static void dst_rows3_n(const DevTables3& T, int mode, double* work, const double* hsep, double scale, double* out,
                         cudaStream_t s, const double* src, const double* corr) {
   constexpr int RPC = 256 / (N / 32);
   const size_t sm = (size_t)RPC * (N / 2 + N / 32 + 1) * sizeof(double2);
-  const int grid = cdiv3((long)(N - 1) * N, RPC);
+  const int grid = cdiv3((long)(T.i_hi - T.i_lo + 1) * N, RPC);
   smem_optin((const void*)k_dst_rows3t<0, N>, sm);
   smem_optin((const void*)k_dst_rows3t<1, N>, sm);
   smem_optin((const void*)k_dst_rows3t<2, N>, sm);
@@ -822,9 +831,9 @@ void launch_sparse3(const DevTables3& T, int which, const double* src, const dou
 }
 void launch_transpose3(const DevTables3& T, double* work, cudaStream_t s) {
   const int t = T.N / 32;
-  dim3 grid(t * (t + 1) / 2, T.N - 1);
+  dim3 grid(t * (t + 1) / 2, T.i_hi - T.i_lo + 1);   // the slab's planes
   ++g_launches;
-  k_transpose3<<<grid, dim3(32, 8), 0, s>>>(T.N, work);
+  k_transpose3<<<grid, dim3(32, 8), 0, s>>>(T.N, work + (size_t)(T.i_lo - 1) * T.N * T.N);
 }
 void launch_sweep3(const DevTables3& T, double* work, double* zB, double* zA, cudaStream_t s) {
   ++g_launches;

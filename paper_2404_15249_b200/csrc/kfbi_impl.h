@@ -211,6 +211,9 @@ struct DevTables3 {
   int nzrow;
   const int8_t* side;
   int world, L3;   // level-2 split of the reduced system (world > 1)
+  // the slab's point work: control points (= intersections, sorted by axis, i) with low-end plane in
+  // [i_lo − 2, i_hi + 2], per axis [q_lo[a], q_hi[a]); irregular nodes of its planes [n_lo, n_hi)
+  int q_lo[3], q_hi[3], n_lo, n_hi;
   const double *rinv3, *z3r, *red3_a, *red3_b;
 };
 

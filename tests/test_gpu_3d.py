@@ -148,10 +148,13 @@ def test_partitioned_apply3d_matches_single(prob, world):
         assert rel(kw.apply(phi).cpu().numpy(), o.apply_KD(phi)) < 1e-10
 
 
-def test_partitioned_solve3d_matches_oracle():
+@pytest.mark.parametrize("world", [2, 4])
+def test_partitioned_solve3d_matches_oracle(world):
+    """The whole solve with every stage sharded by slab: the LSQ fits, corrections and point work of
+    each slab, the dense Y apply and final field of its planes, the level-2 reduced system."""
     prob = W.C4(64)
     o = oracle(prob)
-    kw = KFBI(prob, world=2, rank=-1)
+    kw = KFBI(prob, world=world, rank=-1)
     f = lambda a, b, c: W.f_exact(prob.kappa, a, b, c)
     u_ref, phi_ref, s_ref = o.solve(W.u_exact(*o.points().T), f)
     X, Y, Z = _grid(prob)

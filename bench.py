@@ -236,9 +236,11 @@ def main():
     else:
         k = KFBI(prob, device=local)
     g, fgrid, fq, fz = make_inputs(k, prob)
+    if sharded:   # one rank per process: f and u are the rank's node slab (kfbi_local_slab)
+        fgrid = np.ascontiguousarray(fgrid.reshape((prob.n + 1,) * prob.dim)[k.local_slice()]).reshape(-1)
     t = lambda a: torch.tensor(a, dtype=torch.float64, device=dev)
     g_d, fg_d, fq_d, fz_d = t(g), t(fgrid), t(fq), t(fz)
-    u_d = torch.empty(k.n_nodes, dtype=torch.float64, device=dev)
+    u_d = torch.empty(k.local_nodes, dtype=torch.float64, device=dev)
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)   # > 126 MB L2
     stream = torch.cuda.current_stream(dev)
 
@@ -276,7 +278,7 @@ def main():
 
     # e2e through the public API with pinned host buffers.  Single-grid layouts move only the Ω-node
     # values of f and u (kfbi_scatter_omega / kfbi_gather_omega: f is zero-extended off Ω, and
-    # u_h is valid on Ω); slab-sharded runs move full grids.
+    # u_h is valid on Ω); slab-sharded runs move each rank's node slab of f and u.
     pin = lambda a: torch.tensor(a, dtype=torch.float64).pin_memory()
     compact = not sharded
     if compact:
@@ -285,7 +287,7 @@ def main():
         fg_h = pin(np.ascontiguousarray(fgrid.reshape(-1)[omask]))
         fg_full = [torch.empty(k.n_nodes, dtype=torch.float64, device=dev) for _ in range(2)]
     else:
-        n_out = k.n_nodes
+        n_out = k.local_nodes
         fg_h = pin(fgrid)
     g_h, fq_h, fz_h = pin(g), pin(fq), pin(fz)
     u_h = torch.empty(n_out, dtype=torch.float64).pin_memory()
@@ -335,7 +337,7 @@ def main():
     def e2e_pipelined(nsteps):
         h2d_s, d2h_s = torch.cuda.Stream(dev), torch.cuda.Stream(dev)
         din = [[torch.empty_like(x, device=dev) for x in (g_h, fg_h, fq_h, fz_h)] for _ in range(2)]
-        dout = [torch.empty(k.n_nodes, dtype=torch.float64, device=dev) for _ in range(2)]
+        dout = [torch.empty(k.local_nodes, dtype=torch.float64, device=dev) for _ in range(2)]
         hout = [torch.empty(n_out, dtype=torch.float64).pin_memory() for _ in range(2)]
         ev_in = [torch.cuda.Event() for _ in range(2)]
         ev_done = [torch.cuda.Event() for _ in range(2)]

@@ -183,6 +183,17 @@ kfbi_status kfbi_set_workspace(kfbi_ctx* ctx, void* d_ws, size_t bytes);
  * nodes, n_nodes = (N+1)^d grid nodes of a full field. */
 kfbi_status kfbi_sizes(const kfbi_ctx* ctx, int64_t* M, int64_t* nq, int64_t* n_irr, int64_t* n_nodes);
 
+/* The node box this context reads f from and writes u to (memory is the paper's
+ * reason for going multi-GPU).  world = 1, or rank = −1 (all slabs in one context):
+ * the full grid, local_shape = (N+1, N+1, 1) in 2D / (N+1)³ in 3D, offset 0.  One rank per process
+ * (world > 1, rank ≥ 0): the rank's slab of grid columns / x-planes i ∈ [local_offset[0],
+ * local_offset[0] + local_shape[0]) with all j (and k): 2D shape (n_i, N+1, 1), 3D (n_i, N+1, N+1).
+ * kfbi_solve's d_f_grid and d_u are then arrays of that shape (row-major, last index contiguous), u is
+ * valid on the slab's Ω nodes, and the context's spectral / working arrays hold the slab only (the
+ * workspace shrinks ∝ 1/world).  kfbi_scatter_omega, kfbi_gather_omega, kfbi_gray_scott_step and the
+ * kfbi_test_* entry points are full-grid only (KFBI_EUNSUPPORTED on a one-rank-per-process context). */
+kfbi_status kfbi_local_slab(const kfbi_ctx* ctx, int64_t local_shape[3], int64_t local_offset[3]);
+
 /* Host copies of point coordinates so the caller can evaluate g and f there:
  * which = 0: control points (M × dim, interleaved), 1: intersection nodes (nq × dim),
  * 2: outward unit normals at the control points (M × dim; Neumann data g_N = n·∇u). */

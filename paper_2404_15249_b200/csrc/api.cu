@@ -84,6 +84,11 @@ struct kfbi_ctx {
   double *V = nullptr, *gx = nullptr, *gr = nullptr, *ghat = nullptr, *tmp = nullptr;
   double *partial = nullptr, *hcol = nullptr, *ycoef = nullptr, *scal = nullptr;
   double *spec_f = nullptr, *spec_bump = nullptr;   // cached spectra (final field by linearity)
+  size_t spec_ld = 0;                                 // stride between the hole bumps' spectra
+  // local-slab I/O (world > 1 with one rank per process): f and u are the rank's node slab
+  // [loc_off, loc_off + loc_shape) of the full grid; the spectral and working arrays hold the slab only
+  bool local_io = false;
+  int64_t loc_shape[3] = {0, 0, 0}, loc_off[3] = {0, 0, 0};
   bool spec_f_valid = false;
   // Ω-compact transfers: Ω nodes per grid row (prefix), the full-grid mask on the device
   std::vector<int64_t> om_ptr;
@@ -113,6 +118,13 @@ struct Arena {
     T* p = assign ? reinterpret_cast<T*>(base + off) : nullptr;
     off += n * sizeof(T);
     return p;
+  }
+  // n elements addressed by global index [i0, i0 + n): the returned pointer is the buffer shifted by
+  // −i0 (slab-local buffers indexed with global row numbers by the kernels)
+  template <class T>
+  T* take_rows(size_t n, size_t i0) {
+    T* p = take<T>(n);
+    return assign ? p - i0 : nullptr;
   }
   template <class T>
   const T* table(const std::vector<T>& v) {
@@ -198,11 +210,27 @@ void layout(kfbi_ctx* c, Arena& A) {
   c->ahole = A.take<double>(std::max(c->nh, 1));
   c->wg = A.take<double>((size_t)std::max(c->nh, 1) * S.M);
   // scratch
-  c->spec = A.take<double>((N - 1) * N);
+  // spectral rows (row i − 1 = grid column i): the whole grid, or the rank's slab columns
+  // [col_lo, col_hi] when it runs alone in its process (local-slab I/O, memory ∝ 1/world)
+  size_t row0 = 0, nloc = N - 1;
+  c->local_io = c->world > 1 && c->rank >= 0;
+  if (c->local_io) {
+    const int nseg = S.P >= 2 * BL2 ? S.P / BL2 : 1;
+    const int g_lo = c->rank * nseg / c->world * BL2, g_hi = (c->rank + 1) * nseg / c->world * BL2;
+    const int col_lo = BL * g_lo + 1, col_hi = std::min(BL * g_hi, S.N - 1);
+    row0 = col_lo - 1;
+    nloc = col_hi - col_lo + 1;
+    c->loc_off[0] = col_lo; c->loc_shape[0] = nloc;
+  } else {
+    c->loc_off[0] = 0; c->loc_shape[0] = N + 1;
+  }
+  c->loc_off[1] = 0; c->loc_shape[1] = N + 1; c->loc_off[2] = 0; c->loc_shape[2] = 1;
+  c->spec = A.take_rows<double>(nloc * N, row0 * N);
   // spectra reused by the final field (linearity): DST(f·1_Ω) from the solve's Y apply, DST(b_h) of the
   // hole bumps from setup — the final field's dense forward becomes spec_f + Σ a_h spec_bump_h
-  c->spec_f = A.take<double>((N - 1) * N);
-  c->spec_bump = A.take<double>((size_t)std::max(c->nh, 1) * (N - 1) * N);
+  c->spec_f = A.take_rows<double>(nloc * N, row0 * N);
+  c->spec_ld = nloc * N;
+  c->spec_bump = A.take_rows<double>((size_t)std::max(c->nh, 1) * nloc * N, row0 * N);
   c->zfirst = A.take<double>(P * N);
   c->zlast = A.take<double>(P * N);
   c->fsep = A.take<double>(std::max<size_t>(P - 1, 1) * N);
@@ -262,8 +290,21 @@ void layout3(kfbi_ctx* c, Arena& A) {
     c->h2 = A.take<double>((size_t)c->world * K);
   }
   c->nh = 0;
-  c->work = A.take<double>((N - 1) * K);
-  c->work2 = A.take<double>((N - 1) * K);
+  // working arrays: all N − 1 planes, or the rank's slab planes [i_lo, i_hi] (local-slab I/O)
+  size_t pl0 = 0, npl = N - 1;
+  c->local_io = c->world > 1 && c->rank >= 0;
+  if (c->local_io) {
+    const int b_lo = c->rank * S.P / c->world, b_hi = (c->rank + 1) * S.P / c->world;
+    const int i_lo = BL * b_lo + 1, i_hi = std::min(BL * b_hi, S.N - 1);
+    pl0 = i_lo - 1;
+    npl = i_hi - i_lo + 1;
+    c->loc_off[0] = i_lo; c->loc_shape[0] = npl;
+  } else {
+    c->loc_off[0] = 0; c->loc_shape[0] = N + 1;
+  }
+  c->loc_off[1] = c->loc_off[2] = 0; c->loc_shape[1] = c->loc_shape[2] = N + 1;
+  c->work = A.take_rows<double>(npl * K, pl0 * K);
+  c->work2 = A.take_rows<double>(npl * K, pl0 * K);
   c->zfirst = A.take<double>(P * K);
   c->corr = A.take<double>(std::max(S.nirr, 1));
   c->fsep = A.take<double>(P * K);   // P rows (not P − 1): equal all-gather slices per rank
@@ -490,7 +531,7 @@ void final_field2(kfbi_ctx* c, const double* phi, const double* fgrid, const dou
     D.base = fgrid ? c->spec_f : nullptr;
     D.nb = c->nh;
     D.bump = c->spec_bump;
-    D.ldb = (long)(T.N - 1) * T.N;
+    D.ldb = (long)c->spec_ld;
     D.coef = c->ahole;
     for (int h = 0; h < c->nh && h < 4; ++h) {   // bump h lives in |x − cx| < rad
       D.blo[h] = std::max(1, (int)std::floor((c->bump.cx[h] - c->bump.rad[h] - T.lo) / T.h) - 1);
@@ -515,6 +556,7 @@ void final_field2(kfbi_ctx* c, const double* phi, const double* fgrid, const dou
   launch_correct(T, phi, c->mk, fq, nullptr, c->cval, s);
   spectral2(c, c->cval, D, s);
   for (int r : my_ranks(c)) launch_inverse_dense(slab(c, r), c->spec, c->hsep, u, s);   // owned columns
+  if (c->local_io) return;   // the box rows 0 and N belong to no slab
   const size_t W = (size_t)T.N + 1;
   ck(cudaMemsetAsync(u, 0, W * sizeof(double), s), "memset");
   ck(cudaMemsetAsync(u + (size_t)T.N * W, 0, W * sizeof(double), s), "memset");
@@ -548,6 +590,12 @@ void inverse3(kfbi_ctx* c, double* u, cudaStream_t s) {   // u == NULL: result s
   }
   if (!u) return;
   const size_t W = (size_t)c->T3.N + 1;
+  if (c->local_io) {   // the slab's planes: only their a = N faces (the box planes 0, N belong to no slab)
+    const DevTables3 Ts = slab3(c, c->rank);
+    ck(cudaMemset2DAsync(u + ((size_t)Ts.i_lo * W + c->T3.N) * W, W * W * sizeof(double), 0, W * sizeof(double),
+                         Ts.i_hi - Ts.i_lo + 1, s), "memset");
+    return;
+  }
   ck(cudaMemsetAsync(u, 0, W * W * sizeof(double), s), "memset");
   ck(cudaMemsetAsync(u + (size_t)c->T3.N * W * W, 0, W * W * sizeof(double), s), "memset");
   ck(cudaMemset2DAsync(u + (W + c->T3.N) * W, W * W * sizeof(double), 0, W * sizeof(double), c->T3.N - 1, s), "memset");
@@ -815,7 +863,7 @@ kfbi_status kfbi_set_workspace(kfbi_ctx* c, void* d_ws, size_t bytes) {
   for (int h = 0; h < c->nh; ++h) {
     BumpParams bp = c->bump;
     bp.a = c->onehot + (size_t)h * c->nh;
-    const long nspec = (long)(c->S.N - 1) * c->S.N;
+    const long nspec = (long)c->spec_ld;
     dst_forward2(c, nullptr, false, bp, c->spec_bump + (size_t)h * nspec, s);
     DenseSrc D;
     D.base = c->spec_bump + (size_t)h * nspec;
@@ -842,6 +890,15 @@ kfbi_status kfbi_sizes(const kfbi_ctx* c, int64_t* M, int64_t* nq, int64_t* nirr
   if (nq) *nq = c->S.nq;
   if (nirr) *nirr = c->S.nirr;
   if (nn) *nn = (int64_t)(c->S.N + 1) * (c->S.N + 1);
+  return KFBI_OK;
+}
+
+kfbi_status kfbi_local_slab(const kfbi_ctx* c, int64_t local_shape[3], int64_t local_offset[3]) {
+  if (!c || !local_shape || !local_offset) return KFBI_EINVAL;
+  for (int a = 0; a < 3; ++a) {
+    local_shape[a] = c->loc_shape[a];
+    local_offset[a] = c->loc_off[a];
+  }
   return KFBI_OK;
 }
 
@@ -884,6 +941,7 @@ kfbi_status kfbi_omega_count(const kfbi_ctx* c, int64_t* n_omega) {
 
 kfbi_status kfbi_scatter_omega(kfbi_ctx* c, const double* d_compact, double* d_grid, void* stream) {
   if (!c || !d_compact || !d_grid) return fail(c, KFBI_EINVAL, "null pointer");
+  if (c->local_io) return fail(c, KFBI_EUNSUPPORTED, "Omega transfers are full-grid (world = 1 or the emulation)");
   KFBI_TRY(c)
   need_ws(c);
   launch_omega_map(c->om_rows, c->om_width, c->d_side, c->d_om_seg, d_compact, d_grid, true, pick(c, stream));
@@ -894,6 +952,7 @@ kfbi_status kfbi_scatter_omega(kfbi_ctx* c, const double* d_compact, double* d_g
 
 kfbi_status kfbi_gather_omega(kfbi_ctx* c, const double* d_grid, double* d_compact, void* stream) {
   if (!c || !d_compact || !d_grid) return fail(c, KFBI_EINVAL, "null pointer");
+  if (c->local_io) return fail(c, KFBI_EUNSUPPORTED, "Omega transfers are full-grid (world = 1 or the emulation)");
   KFBI_TRY(c)
   need_ws(c);
   launch_omega_map(c->om_rows, c->om_width, c->d_side, c->d_om_seg, d_grid, d_compact, false, pick(c, stream));
@@ -1053,6 +1112,11 @@ kfbi_status kfbi_solve(kfbi_ctx* c, const double* d_g, const double* d_f_grid, c
   bool converged = false;
   KFBI_TRY(c)
   need_ws(c);
+  if (c->local_io) {   // the rank's node slab: the kernels index with global node numbers
+    const size_t row = c->dim == 3 ? (size_t)(c->S3.N + 1) * (c->S3.N + 1) : (size_t)c->S.N + 1;
+    if (d_f_grid) d_f_grid -= (size_t)c->loc_off[0] * row;
+    d_u -= (size_t)c->loc_off[0] * row;
+  }
   cudaStream_t s = pick(c, stream);
   const int M = nctrl(c);
   const size_t bM = (size_t)M * sizeof(double);
@@ -1261,6 +1325,7 @@ kfbi_status kfbi_gray_scott_step(kfbi_ctx* cu, kfbi_ctx* cv, double* d_u, double
   for (int q = 0; q < 2; ++q)
     if (std::fabs(cs[q]->S.kappa - 2.0 / (eps[q] * dt)) > 1e-12 * cs[q]->S.kappa)
       return fail(cu, KFBI_EINVAL, "context kappa must be 2/(eps dt) (Crank-Nicolson, reading R40)");
+  if (cu && cu->local_io) return fail(cu, KFBI_EUNSUPPORTED, "full-grid entry point (world = 1 or the emulation)");
   KFBI_TRY(cu)
   need_ws(cu);
   need_ws(cv);
@@ -1309,6 +1374,7 @@ kfbi_status kfbi_destroy(kfbi_ctx* c) {
 
 kfbi_status kfbi_test_fast_solve(kfbi_ctx* c, const double* d_rhs, double* d_v, void* stream) {
   if (!c || !d_rhs || !d_v) return KFBI_EINVAL;
+  if (c && c->local_io) return fail(c, KFBI_EUNSUPPORTED, "full-grid entry point (world = 1 or the emulation)");
   KFBI_TRY(c)
   need_ws(c);
   cudaStream_t s = pick(c, stream);
@@ -1337,6 +1403,7 @@ kfbi_status kfbi_test_fast_solve(kfbi_ctx* c, const double* d_rhs, double* d_v, 
 kfbi_status kfbi_test_interface_solve(kfbi_ctx* c, const double* d_base, const double* d_jq, const double* d_jz,
                                       double* d_v, double* d_vplus, void* stream) {
   if (!c || !d_jq || !d_jz) return KFBI_EINVAL;
+  if (c && c->local_io) return fail(c, KFBI_EUNSUPPORTED, "full-grid entry point (world = 1 or the emulation)");
   KFBI_TRY(c)
   need_ws(c);
   cudaStream_t s = pick(c, stream);

@@ -24,7 +24,7 @@ EXPORTS = ["kfbi_version", "kfbi_last_error", "kfbi_last_setup_error", "kfbi_get
            "kfbi_apply", "kfbi_solve", "kfbi_apply_model", "kfbi_destroy", "kfbi_test_fast_solve",
            "kfbi_test_interface_solve", "kfbi_test_setup_dump", "kfbi_profile_apply", "kfbi_launch_count",
            "kfbi_slab", "kfbi_gray_scott_step", "kfbi_setup_scratch_size", "kfbi_setup_device",
-           "kfbi_omega_count", "kfbi_scatter_omega", "kfbi_gather_omega"]
+           "kfbi_omega_count", "kfbi_scatter_omega", "kfbi_gather_omega", "kfbi_local_slab"]
 
 
 class KfbiError(RuntimeError):
@@ -94,6 +94,7 @@ def load(path: str = LIB_PATH):
     lib.kfbi_workspace_size.argtypes = [vp, C.POINTER(C.c_size_t)]
     lib.kfbi_set_workspace.argtypes = [vp, vp, C.c_size_t]
     lib.kfbi_sizes.argtypes = [vp, i64p, i64p, i64p, i64p]
+    lib.kfbi_local_slab.argtypes = [vp, i64p, i64p]
     lib.kfbi_points.argtypes = [vp, i32, dp]
     lib.kfbi_node_mask.argtypes = [vp, C.POINTER(C.c_int8)]
     lib.kfbi_apply.argtypes = [vp, vp, vp, vp]
@@ -217,6 +218,12 @@ class KFBI:
         self._check(self.lib.kfbi_sizes(ctx, C.byref(M), C.byref(nq), C.byref(nirr), C.byref(nn)))
         self.M, self.nq, self.nirr, self.n_nodes = M.value, nq.value, nirr.value, nn.value
         self.n = problem.n
+        shp, off = (C.c_int64 * 3)(), (C.c_int64 * 3)()
+        self._check(self.lib.kfbi_local_slab(ctx, shp, off))
+        d = problem.dim
+        self.local_shape = tuple(shp[:d])          # f and u of kfbi_solve (the full grid unless one
+        self.local_offset = tuple(off[:d])         # rank per process, see include/kfbi.h)
+        self.local_nodes = int(np.prod(self.local_shape))
 
     # ------------------------------------------------------------------ helpers
     def _check(self, st):
@@ -325,12 +332,12 @@ class KFBI:
               async_final=False):
         t = self.torch
         g = self._dev(g, self.M)
-        fg = self._dev(f_grid, self.n_nodes)
+        fg = self._dev(f_grid, self.local_nodes)
         fq = self._dev(f_isect, self.nq)
         fz = self._dev(f_ctrl, self.M)
         p0 = self._dev(phi0, self.M)
-        u = (t.empty(self.n_nodes, dtype=t.float64, device=self.device) if u is None
-             else self._out(u.reshape(-1) if isinstance(u, t.Tensor) and u.is_contiguous() else u, self.n_nodes, "u"))
+        u = (t.empty(self.local_nodes, dtype=t.float64, device=self.device) if u is None
+             else self._out(u.reshape(-1) if isinstance(u, t.Tensor) and u.is_contiguous() else u, self.local_nodes, "u"))
         phi = t.empty(self.M, dtype=t.float64, device=self.device)
         opts = SolveOpts(tol, restart, max_restarts, METHODS[method], gamma, 1 if async_final else 0)
         st = SolveStats()
@@ -341,7 +348,11 @@ class KFBI:
         if code != OK and (code != ENOCONV or raise_on_noconv):
             self._check(code)
         stats = Stats(st.iters, st.restarts, st.n_applies, bool(st.converged), st.rel_residual, st.t_solve_s)
-        return u.view((self.n + 1,) * self.problem.dim), phi, stats
+        return u.view(self.local_shape), phi, stats
+
+    def local_slice(self):
+        """numpy index of this context's node slab in the full grid (f and u of solve())."""
+        return tuple(slice(o, o + n) for o, n in zip(self.local_offset, self.local_shape))
 
     def slab(self, rank=None):
         out = (C.c_int64 * 6)()

@@ -31,7 +31,9 @@ def _worker(rank, world, port, q):
         stencil = k.setup_dump(2).reshape(-1, 2)[:, 0]           # columns of all stencil nodes
         owned = int(((stencil >= sl["col_lo"]) & (stencil <= sl["col_hi"])).sum())
         out = [None] * world
-        dist.all_gather_object(out, (nid, sl, owned, int(stencil.size)))
+        k1 = KFBI(W.C3(2048), workspace=False)
+        dist.all_gather_object(out, (nid, sl, owned, int(stencil.size), k.local_offset, k.local_shape,
+                                     k.workspace_bytes, k1.workspace_bytes))
         if rank == 0:
             q.put(out)
     finally:
@@ -63,6 +65,12 @@ def test_slab_partition_and_id_bootstrap(world):
         assert (a["g_hi"] * 16) == a["col_hi"]                       # slab ends on a level-2 separator
     # every stencil node is owned by exactly one rank (partial interpolation sums are disjoint)
     assert sum(r[2] for r in res) == res[0][3]
+    # local-slab I/O (kfbi_local_slab): each rank's f/u box is its slab's grid columns, all j; the boxes
+    # tile the unknown columns 1..N−1, and the workspace of a rank holds its slab's spectra only
+    for r, sl in zip(res, slabs):
+        assert r[4] == (sl["col_lo"], 0) and r[5] == (sl["col_hi"] - sl["col_lo"] + 1, n + 1)
+    assert sum(r[5][0] for r in res) == n - 1
+    assert all(r[6] < 0.75 * r[7] for r in res)
 
 
 def _worker3(rank, world, port, q):
@@ -77,7 +85,9 @@ def _worker3(rank, world, port, q):
         planes = k.setup_dump(2).reshape(-1, 3)[:, 0]            # x-planes of all stencil nodes
         owned = int(((planes >= sl["i_lo"]) & (planes <= sl["i_hi"])).sum())
         out = [None] * world
-        dist.all_gather_object(out, (sl, owned, int(planes.size)))
+        k1 = KFBI(W.C4(64), workspace=False)
+        dist.all_gather_object(out, (sl, owned, int(planes.size), k.local_offset, k.local_shape,
+                                     k.workspace_bytes, k1.workspace_bytes))
         if rank == 0:
             q.put(out)
     finally:
@@ -105,3 +115,8 @@ def test_slab_partition_3d(world):
         assert a["b_hi"] == b["b_lo"] and a["i_hi"] + 1 == b["i_lo"] and a["w_hi"] == b["w_lo"]
         assert a["b_hi"] * 16 == a["i_hi"]                            # slab ends on a block separator
     assert sum(r[1] for r in res) == res[0][2]                        # stencil nodes owned once
+    for r, sl in zip(res, slabs):   # local-slab I/O boxes = the slab's x-planes (all j, k)
+        assert r[3] == (sl["i_lo"], 0, 0) and r[4] == (sl["i_hi"] - sl["i_lo"] + 1, n + 1, n + 1)
+    assert sum(r[4][0] for r in res) == n - 1
+    # the two (N−1)·N² working arrays shrink to the slab's planes (≤ 20 N² doubles of level-2 tables added)
+    assert all(r[5] <= r[6] - 2 * (n - 1 - r[4][0]) * n * n * 8 + 20 * n * n * 8 for r in res)

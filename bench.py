@@ -401,6 +401,22 @@ def main():
             roofline["traffic"] = json.load(open(ncu_csv)).get(f"{prob.name}:{prob.n}:k_{dom}")
         except Exception:
             pass
+    # the FP64 side of the same kernels: ncu's executed FP64 FLOPs per launch (2·DFMA + DADD + DMUL,
+    # profiles/ncu_fp64.json) over the live CUDA-event time, against the measured FP64 peak
+    # (profiles/fp64_peak.json, tools/fp64_peak.cu)
+    try:
+        fl = json.load(open(os.path.join(ROOT, "profiles", "ncu_fp64.json")))
+        pk = json.load(open(os.path.join(ROOT, "profiles", "fp64_peak.json")))["fp64_tflops"]
+        fp = {}
+        for n in ("sweep", "inverse"):
+            f = fl.get(f"{prob.name}:{prob.n}:k_{n}")
+            if f:
+                a = f / (prof[n] * 1e-3) / 1e12
+                fp[f"k_{n}"] = {"achieved": a, "peak": pk, "unit": "TFLOP/s", "frac": a / pk, "flops_per_launch": f}
+        if fp:
+            roofline["fp64"] = fp
+    except Exception:
+        pass
 
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,

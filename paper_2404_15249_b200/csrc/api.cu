@@ -335,6 +335,7 @@ DevTables slab(const kfbi_ctx* c, int r) {
   if (world == 1) {
     T.g_lo = 0; T.g_hi = S.P; T.seg_lo = 0; T.seg_hi = T.nseg;
     T.col_lo = 1; T.col_hi = S.N - 1; T.o_lo = 0; T.o_hi = (int)S.ocol.size();
+    T.irr_lo = 0; T.irr_hi = S.nirr;
     return T;
   }
   T.seg_lo = r * T.nseg / world;
@@ -345,6 +346,8 @@ DevTables slab(const kfbi_ctx* c, int r) {
   T.col_hi = std::min(BL * T.g_hi, S.N - 1);
   T.o_lo = (int)(std::lower_bound(S.ocol.begin(), S.ocol.end(), T.col_lo) - S.ocol.begin());
   T.o_hi = (int)(std::upper_bound(S.ocol.begin(), S.ocol.end(), T.col_hi) - S.ocol.begin());
+  T.irr_lo = S.col_ptr[T.col_lo];
+  T.irr_hi = S.col_ptr[T.col_hi + 1];
   return T;
 }
 
@@ -503,17 +506,16 @@ void dst_forward2(kfbi_ctx* c, const double* fgrid, bool mask, const BumpParams&
 void apply_KD2(kfbi_ctx* c, const double* phi, double* out, cudaStream_t s) {
   const DevTables& T = c->T;
   launch_spline(T, phi, c->mk, s, c->hole_off, c->hole_M, c->hole_delta, c->nh, c->ahole);   // + a_h (R27)
-  launch_correct(T, phi, c->mk, nullptr, nullptr, c->cval, s);
+  for (int r : my_ranks(c)) launch_correct(slab(c, r), phi, c->mk, nullptr, nullptr, c->cval, s);   // slab's nodes
   spectral2(c, c->cval, DenseSrc{}, s);
   interp2(c, phi, nullptr, nullptr, true, out, s);
 }
 
 void apply_Y2(kfbi_ctx* c, const double* fgrid, const double* fq, const double* fz, double* out, cudaStream_t s) {
-  const DevTables& T = c->T;
   BumpParams none{};
   dst_forward2(c, fgrid, true, none, c->spec_f, s);   // kept for the final field
   c->spec_f_valid = true;
-  launch_correct(T, nullptr, nullptr, fq, nullptr, c->cval, s);
+  for (int r : my_ranks(c)) launch_correct(slab(c, r), nullptr, nullptr, fq, nullptr, c->cval, s);
   DenseSrc D;
   D.base = c->spec_f;
   spectral2(c, c->cval, D, s);
@@ -553,7 +555,7 @@ void final_field2(kfbi_ctx* c, const double* phi, const double* fgrid, const dou
   }
   c->spec_f_valid = false;
   launch_spline(T, phi, c->mk, s);
-  launch_correct(T, phi, c->mk, fq, nullptr, c->cval, s);
+  for (int r : my_ranks(c)) launch_correct(slab(c, r), phi, c->mk, fq, nullptr, c->cval, s);
   spectral2(c, c->cval, D, s);
   for (int r : my_ranks(c)) launch_inverse_dense(slab(c, r), c->spec, c->hsep, u, s);   // owned columns
   if (c->local_io) return;   // the box rows 0 and N belong to no slab
@@ -1285,7 +1287,7 @@ kfbi_status kfbi_profile_apply(kfbi_ctx* c, const double* d_phi, double* d_out, 
     ck(cudaEventRecord(ev[0], s), "rec");
     launch_spline(T, d_phi, c->mk, s, c->hole_off, c->hole_M, c->hole_delta, c->nh, c->ahole);
     ck(cudaEventRecord(ev[1], s), "rec");
-    launch_correct(T, d_phi, c->mk, nullptr, nullptr, c->cval, s);
+    for (int r : my_ranks(c)) launch_correct(slab(c, r), d_phi, c->mk, nullptr, nullptr, c->cval, s);
     ck(cudaEventRecord(ev[2], s), "rec");
     launch_sweep(T, c->cval, DenseSrc{}, c->spec, c->zfirst, c->zlast, c->fsep, s);
     ck(cudaEventRecord(ev[3], s), "rec");
@@ -1430,7 +1432,7 @@ kfbi_status kfbi_test_interface_solve(kfbi_ctx* c, const double* d_base, const d
   }
   BumpParams none{};
   if (d_base) launch_dst_forward(c->T, d_base, false, none, c->spec, s);
-  launch_correct(c->T, nullptr, nullptr, nullptr, d_jq, c->cval, s);
+  for (int r : my_ranks(c)) launch_correct(slab(c, r), nullptr, nullptr, nullptr, d_jq, c->cval, s);
   DenseSrc D;
   D.base = d_base ? c->spec : nullptr;
   launch_sweep(c->T, c->cval, D, c->spec, c->zfirst, c->zlast, c->fsep, s);

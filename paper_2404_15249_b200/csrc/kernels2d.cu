@@ -97,8 +97,8 @@ __global__ void k_spline(DevTables T, const double* __restrict__ phi, double* __
 // ------------------------------------------------------------------------------ A2+A3
 __global__ void k_correct(DevTables T, const double* __restrict__ phi, const double* __restrict__ mk,
                           const double* __restrict__ fq, const double* __restrict__ jqg, double* __restrict__ cval) {
-  int n = blockIdx.x * blockDim.x + threadIdx.x;
-  if (n >= T.nirr) return;
+  int n = T.irr_lo + blockIdx.x * blockDim.x + threadIdx.x;   // the slab's irregular nodes
+  if (n >= T.irr_hi) return;
   double acc = 0.0;
   for (int e = T.irr_ptr[n]; e < T.irr_ptr[n + 1]; ++e) {
     int q = T.pair_q[e];
@@ -1075,6 +1075,13 @@ __global__ void k_interp(DevTables T, const double* __restrict__ phi, const doub
                          const double* __restrict__ ahole, double* __restrict__ out, int partial) {
   const int m = blockIdx.x * blockDim.x + threadIdx.x;
   if (m >= T.M) return;
+  if (partial) {   // multi-GPU: a control point whose stencil columns c − 1 … c + 1 miss the slab adds 0
+    const int col = T.sn_i[T.st_node[m * 6]];
+    if (col + 1 < T.col_lo || col - 1 > T.col_hi) {
+      out[m] = 0.0;
+      return;
+    }
+  }
   Jump6 J;
   if (jzg) {
     J.v = jzg[m * 6];
@@ -1559,8 +1566,8 @@ void launch_spline(const DevTables& T, const double* phi, double* mk, cudaStream
 
 void launch_correct(const DevTables& T, const double* phi, const double* mk, const double* fq,
                     const double* jq_given, double* cval, cudaStream_t s) {
-  if (T.nirr == 0) return;
-  { ++g_launches; k_correct<<<cdiv(T.nirr, 128), 128, 0, s>>>(T, phi, mk, fq, jq_given, cval); }
+  if (T.irr_hi <= T.irr_lo) return;
+  { ++g_launches; k_correct<<<cdiv(T.irr_hi - T.irr_lo, 128), 128, 0, s>>>(T, phi, mk, fq, jq_given, cval); }
 }
 
 

@@ -250,6 +250,7 @@ struct DevTables {
   // slab of the executing rank (multi-GPU): blocks [g_lo, g_hi), level-2 segments
   // [seg_lo, seg_hi) of nseg, owned columns [col_lo, col_hi], owned stencil columns [o_lo, o_hi)
   int g_lo, g_hi, seg_lo, seg_hi, nseg, col_lo, col_hi, o_lo, o_hi, rank;
+  int irr_lo, irr_hi;   // the slab's irregular nodes (sorted by column): the corrections its sweep reads
 };
 
 }  // namespace kfbi

@@ -53,7 +53,8 @@ def build(force: bool = False, verbose: bool = False) -> str:
 
     def compile_one(src):
         obj = os.path.join(objdir, src + ".o")
-        cmd = [nvcc()] + NVCC_FLAGS + inc + ["-c", "-o", obj, os.path.join(CSRC, src)]
+        extra = os.environ.get("KFBI_NVCC_EXTRA", "").split()   # e.g. -DKFBI_BOUNDS (device index checks)
+        cmd = [nvcc()] + NVCC_FLAGS + extra + inc + ["-c", "-o", obj, os.path.join(CSRC, src)]
         if verbose:
             print(" ".join(cmd), file=sys.stderr)
         subprocess.run(cmd, check=True, cwd=CSRC)

@@ -61,6 +61,7 @@ struct kfbi_ctx {
   ncclUniqueId nccl_id{};
   ncclComm_t comm = nullptr;
   double *segbuf = nullptr, *h2 = nullptr, *parts = nullptr;
+  double *seg3 = nullptr, *seg3_in = nullptr, *h3_out = nullptr, *h3_in = nullptr;   // 3D level-2 exchange
   Setup S;
   DevTables T{};
   Setup3 S3;
@@ -285,9 +286,12 @@ void layout3(kfbi_ctx* c, Arena& A) {
   T.n_lo = 0; T.n_hi = S.nirr;
   T.rinv3 = S.L3 >= 0 ? A.table(S.rinv3) : nullptr; T.z3r = S.L3 >= 0 ? A.table(S.z3r) : nullptr;
   T.red3_a = S.L3 >= 0 ? A.table(S.red3_a) : nullptr; T.red3_b = S.L3 >= 0 ? A.table(S.red3_b) : nullptr;
-  if (c->world > 1) {
-    c->segbuf = A.take<double>((size_t)c->world * 4 * K);   // per slab: first, last, zA_sep, zB_first
-    c->h2 = A.take<double>((size_t)c->world * K);
+  if (c->world > 1) {   // level-2 exchange buffers (reduced3_dist); the emulation holds every slab's
+    const size_t W = c->world, Kq = (K + W - 1) / W, sl = c->rank >= 0 ? 1 : W;
+    c->seg3 = A.take<double>(sl * W * 4 * Kq);    // from local: [slab][q][4][Kq]
+    c->seg3_in = A.take<double>(W * 4 * Kq);      // owner's input [r][4][Kq] (NCCL)
+    c->h3_out = A.take<double>(sl * W * 2 * Kq);  // owner's output [owner][r][2][Kq] (emulation) / [r][2][Kq]
+    c->h3_in = A.take<double>(sl * W * 2 * Kq);   // slab's fix-up input [slab][q][2][Kq]
   }
   c->nh = 0;
   // working arrays: all N − 1 planes, or the rank's slab planes [i_lo, i_hi] (local-slab I/O)
@@ -632,22 +636,53 @@ void interp3_dist(kfbi_ctx* c, const double* phi, const double* fz, double* out,
 // all-gathered, every rank solves the (cheap) reduced system for all modes, and the interpolation
 // partial sums (plane owner contributes) are all-reduced.  rank = −1 emulates all slabs in one ctx.
 // reduced (separator) system of the sweeps just run.  world > 1: every slab eliminates its interior
-// separators, publishes 4 values per mode (first, last, its boundary separator's zA, its first
-// block's zB), one all-gather (4·K doubles per rank; the 2D path's level-2 scheme), every
-// rank solves the world − 1 slab separators per mode, and fixes up its own interior separators.
+// separators and publishes 4 values per mode (first, last, its boundary separator's zA, its first
+// block's zB); the level-2 system of the world − 1 slab separators is solved mode-partitioned (owner q
+// of K/W modes; all-to-all of the 4 rows, all-to-all of the 2 rows each slab needs back: ≈ 6·K doubles
+// sent per rank); every slab then fixes up its own interior separators.
 void reduced3_dist(kfbi_ctx* c, cudaStream_t s) {
   const DevTables3& T = c->T3;
   if (c->world == 1) {
     launch_reduced3(T, c->zfirst, c->fsep, c->hsep, s);
     return;
   }
-  for (int r : my_ranks(c)) launch_red3_local(slab3(c, r), c->zfirst, c->fsep, c->hsep, c->segbuf, s);
+  const size_t W = c->world, K = (size_t)T.N * T.N, Kq = (K + W - 1) / W;
   if (c->use_nccl) {
-    const size_t cnt = (size_t)4 * T.N * T.N;
-    ckn(ncclAllGather(c->segbuf + (size_t)c->rank * cnt, c->segbuf, cnt, ncclDouble, c->comm, s), "allgather");
+    const int me = c->rank;
+    const DevTables3 Ts = slab3(c, me);
+    launch_red3_local(Ts, c->zfirst, c->fsep, c->hsep, c->seg3, (int)Kq, s);
+    // all-to-all: owner q gets every slab's 4 rows of its modes
+    ckn(ncclGroupStart(), "group");
+    for (int q = 0; q < (int)W; ++q) {
+      if (q == me) continue;
+      ckn(ncclSend(c->seg3 + (size_t)q * 4 * Kq, 4 * Kq, ncclDouble, q, c->comm, s), "send seg");
+      ckn(ncclRecv(c->seg3_in + (size_t)q * 4 * Kq, 4 * Kq, ncclDouble, q, c->comm, s), "recv seg");
+    }
+    ckn(ncclGroupEnd(), "group");
+    ck(cudaMemcpyAsync(c->seg3_in + (size_t)me * 4 * Kq, c->seg3 + (size_t)me * 4 * Kq, 4 * Kq * sizeof(double),
+                       cudaMemcpyDeviceToDevice, s), "self rows");
+    launch_red3_solve(Ts, c->seg3_in, 4 * Kq, c->h3_out, 2 * Kq, (int)Kq, s);
+    // all-to-all back: slab r gets (h_{r−1}, h_r) of every owner's modes
+    ckn(ncclGroupStart(), "group");
+    for (int r = 0; r < (int)W; ++r) {
+      if (r == me) continue;
+      ckn(ncclSend(c->h3_out + (size_t)r * 2 * Kq, 2 * Kq, ncclDouble, r, c->comm, s), "send h");
+      ckn(ncclRecv(c->h3_in + (size_t)r * 2 * Kq, 2 * Kq, ncclDouble, r, c->comm, s), "recv h");
+    }
+    ckn(ncclGroupEnd(), "group");
+    ck(cudaMemcpyAsync(c->h3_in + (size_t)me * 2 * Kq, c->h3_out + (size_t)me * 2 * Kq, 2 * Kq * sizeof(double),
+                       cudaMemcpyDeviceToDevice, s), "self h");
+    launch_red3_fixup(Ts, c->h3_in, c->hsep, (int)Kq, s);
+    return;
   }
-  launch_red3_solve(T, c->segbuf, c->h2, s);
-  for (int r : my_ranks(c)) launch_red3_fixup(slab3(c, r), c->h2, c->hsep, s);
+  // emulation (every slab in this context): the exchanges are strided reads of the other slabs' buffers —
+  // owner q reads slab r's rows at seg3[r][q] (stride W·4·Kq) and writes slab r's rows to h3_in[r][q]
+  for (int r = 0; r < (int)W; ++r)
+    launch_red3_local(slab3(c, r), c->zfirst, c->fsep, c->hsep, c->seg3 + (size_t)r * W * 4 * Kq, (int)Kq, s);
+  for (int q = 0; q < (int)W; ++q)
+    launch_red3_solve(slab3(c, q), c->seg3 + (size_t)q * 4 * Kq, W * 4 * Kq, c->h3_in + (size_t)q * 2 * Kq,
+                      W * 2 * Kq, (int)Kq, s);
+  for (int r = 0; r < (int)W; ++r) launch_red3_fixup(slab3(c, r), c->h3_in + (size_t)r * W * 2 * Kq, c->hsep, (int)Kq, s);
 }
 
 void apply_KD3(kfbi_ctx* c, const double* phi, double* out, cudaStream_t s) {

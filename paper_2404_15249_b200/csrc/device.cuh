@@ -12,6 +12,25 @@
 
 #include "kernels.h"
 
+// Bounds checks of the hot kernels' computed indices (compute-sanitizer is closed on this GPU pool):
+// built with -DKFBI_BOUNDS (KFBI_NVCC_EXTRA=-DKFBI_BOUNDS python -m paper_2404_15249_b200.build --force),
+// a violated check prints the kernel, line and values and traps; compiled out otherwise.
+#ifdef KFBI_BOUNDS
+#include <cstdio>
+#define KFBI_CHECK(cond, a, b)                                                                            \
+  do {                                                                                                     \
+    if (!(cond)) {                                                                                         \
+      printf("KFBI_CHECK failed %s:%d (%s): %lld %lld block %d thread %d\n", __FILE__, __LINE__, #cond,  \
+             (long long)(a), (long long)(b), (int)blockIdx.x, (int)threadIdx.x);                           \
+      __trap();                                                                                            \
+    }                                                                                                      \
+  } while (0)
+#else
+#define KFBI_CHECK(cond, a, b) \
+  do {                         \
+  } while (0)
+#endif
+
 namespace kfbi {
 namespace {
 

@@ -122,13 +122,15 @@ void launch_dst_rows3(const DevTables3& T, int mode, double* work, const double*
 void launch_transpose3(const DevTables3& T, double* work, cudaStream_t s);
 void launch_sweep3(const DevTables3& T, double* work, double* zB, double* zA, cudaStream_t s);
 void launch_reduced3(const DevTables3& T, const double* zB, const double* zA, double* hsep, cudaStream_t s);
-// multi-GPU level-2 split of the 3D reduced system (slab = P/world blocks): interior separators of the
-// slab [b_lo, b_hi) → hsep + segbuf[rank][4][K]; level-2 solve of the world − 1 slab separators → h2;
-// fix-up of the slab's interior separators and its boundary separators in hsep
-void launch_red3_local(const DevTables3& T, const double* zB, const double* zA, double* hsep, double* segbuf,
+// multi-GPU level-2 split of the 3D reduced system (slab = P/world blocks), mode-partitioned: the slab's
+// interior separators → hsep and its 4 rows per mode in chunk-major layout seg[q][4][Kq]; owner T.rank
+// of modes [rank·Kq, (rank+1)·Kq) solves the world − 1 slab separators from in[r·in_r] ([4][Kq] per slab)
+// into out[r·out_r] ([2][Kq] per slab: h_{r−1}, h_r); each slab fixes up from its [q][2][Kq] rows
+void launch_red3_local(const DevTables3& T, const double* zB, const double* zA, double* hsep, double* seg, int Kq,
                        cudaStream_t s);
-void launch_red3_solve(const DevTables3& T, const double* segbuf, double* h2, cudaStream_t s);
-void launch_red3_fixup(const DevTables3& T, const double* h2, double* hsep, cudaStream_t s);
+void launch_red3_solve(const DevTables3& T, const double* in, size_t in_r, double* out, size_t out_r, int Kq,
+                       cudaStream_t s);
+void launch_red3_fixup(const DevTables3& T, const double* hin, double* hsep, int Kq, cudaStream_t s);
 // partial: only stencil nodes in the slab's planes [i_lo, i_hi] contribute (multi-GPU partial sums)
 void launch_interp3(const DevTables3& T, const double* phi, const double* dphi, const double* fz,
                     const double* jz_given, const double* work, double* out, cudaStream_t s, bool partial = false);

@@ -102,6 +102,7 @@ __global__ void k_correct(DevTables T, const double* __restrict__ phi, const dou
   double acc = 0.0;
   for (int e = T.irr_ptr[n]; e < T.irr_ptr[n + 1]; ++e) {
     int q = T.pair_q[e];
+    KFBI_CHECK(q >= 0 && q < T.nq, q, T.nq);
     double d = T.pair_d[e];
     int ax = T.q_axis[q];
     double v, va, vaa;
@@ -206,6 +207,7 @@ __global__ void __launch_bounds__(kSweepThreads, 2) k_sweep(DevTables T, const d
   const int g = T.blk_order[kk];
   if (g < T.g_lo || g >= T.g_hi) continue;   // CTA-uniform
     const int c0 = BL * g + 1;
+    KFBI_CHECK(c0 - 1 >= T.col_lo - 1 && c0 - 1 + LB - 1 <= T.col_hi - 1, c0, T.col_hi);   // spectral rows of the slab
     const int e0 = T.col_ptr[c0];
     const int ncol = g < T.P - 1 ? BL : LB;   // block columns + separator column
     const int e1 = cval ? T.col_ptr[c0 + ncol] : e0;
@@ -215,7 +217,9 @@ __global__ void __launch_bounds__(kSweepThreads, 2) k_sweep(DevTables T, const d
     const int ce = e1 - cb < kEntCap ? e1 : cb + kEntCap;
     __syncthreads();
     for (int e = cb + threadIdx.x; e < ce; e += B) {
+      KFBI_CHECK(e >= 0 && e < T.nirr, e, T.nirr);
       const int j = T.irr_j[e];
+      KFBI_CHECK(j >= 1 && j < N, j, N);
       const int rd = (j * kRotStride) & m2;
       const double c = cval[e];
       // odd j: sin(πj/2) = ±1; even j: cos(πj/2) = ±1
@@ -663,6 +667,7 @@ __global__ void __launch_bounds__(kInvThreads, 2) k_inv_sparse(DevTables T, cons
   // Spectral positions 4t..4t+3 hold the quad {t, N−t, N/2−t, N/2+t}: two 16-byte loads per array.
   const int q = i / BL, rr = i - q * BL;
   const bool sep = rr == 0;
+  KFBI_CHECK(i >= T.col_lo && i <= T.col_hi && u1 - u0 <= T.mcr, i, u1 - u0);
   const double* xrow = ASYNC ? xs : own_row(i);
   const double* hl = (!sep && q > 0) ? hsep + (size_t)(q - 1) * N : nullptr;
   const double* hr = (!sep && q < P - 1) ? hsep + (size_t)q * N : nullptr;
@@ -831,6 +836,7 @@ __global__ void __launch_bounds__(kInvThreads, 2) k_inv_sparse(DevTables T, cons
     }
     const int j = s_rows[t];
     const double sig = ((j >> 1) & 1) ? -1.0 : 1.0;   // σ_j = sin(πj/2) for odd j
+    KFBI_CHECK(u0 + t < T.nsn && j >= 1 && j < N, u0 + t, j);
     vsten[u0 + t] = scale * ((j & 1) ? s1 + sig * s2 : s1);
   }
   }
@@ -1078,7 +1084,10 @@ __global__ void k_interp(DevTables T, const double* __restrict__ phi, const doub
   if (partial) {   // multi-GPU: a control point whose stencil columns c − 1 … c + 1 miss the slab adds 0
     const int col = T.sn_i[T.st_node[m * 6]];
     if (col + 1 < T.col_lo || col - 1 > T.col_hi) {
-      out[m] = 0.0;
+      double acc = 0.0;   // rank 0 still adds the hole-completion term (R27) of every control point
+      if (T.rank == 0)
+        for (int hh = 0; hh < nh; ++hh) acc = fma(ahole[hh], wg[(size_t)hh * T.M + m], acc);
+      out[m] = acc;
       return;
     }
   }
@@ -1104,6 +1113,7 @@ __global__ void k_interp(DevTables T, const double* __restrict__ phi, const doub
   for (int p = 0; p < 6; ++p) {
     const int idx = m * 6 + p;
     const int sn = T.st_node[idx];
+    KFBI_CHECK(sn >= 0 && sn < T.nsn, sn, T.nsn);
     if (partial) {   // multi-GPU: only stencil nodes in the owned columns contribute (partial sum)
       const int col = T.sn_i[sn];
       if (col < T.col_lo || col > T.col_hi) continue;

@@ -150,6 +150,7 @@ __global__ void k_correct3(DevTables3 T, const double* __restrict__ phi, const d
   double acc = 0.0;
   for (int e = T.irr_ptr[n]; e < T.irr_ptr[n + 1]; ++e) {
     const int q = T.pair_q[e];
+    KFBI_CHECK(q >= 0 && q < T.nq, q, T.nq);
     const double d = T.pair_d[e];
     const int ax = T.q_axis[q];
     Jump10 J;
@@ -400,6 +401,7 @@ __global__ void __launch_bounds__(256, 2) k_fwd3s(DevTables3 T, const double* __
                     : (mem == 0 ? 0 : mem == 1 ? N / 2 : mem == 2 ? N / 4 : 3 * N / 4);
   const double sc = ll ? 1.0 : 0.0;
   const double* F = reinterpret_cast<const double*>(z);
+  KFBI_CHECK(i >= T.i_lo && i <= T.i_hi && ll >= 0 && ll < N, i, ll);
   double* op = work + ((size_t)(i - 1) * N + ll) * N;
 #pragma unroll
   for (int s = 0; s < 16; ++s) {
@@ -472,6 +474,7 @@ __global__ void __launch_bounds__(256) k_zeval3(DevTables3 T, const double* __re
     double nxt[S][U];
     if (wn < T.w_hi) load(wn, nxt);
     const size_t rbase = (size_t)T.zrow_id[w] * N;
+    KFBI_CHECK(T.zrow_id[w] / N + 1 >= T.i_lo && T.zrow_id[w] / N + 1 <= T.i_hi, T.zrow_id[w], w);
     const int e1 = T.zrow_ptr[w + 1];
     for (int e0 = T.zrow_ptr[w]; e0 < e1; e0 += 8) {   // 8 nodes per transpose-reduction
     double vv[8];
@@ -618,19 +621,26 @@ __global__ void k_reduced3(DevTables3 T, const double* __restrict__ zB, const do
 }
 
 // ---- multi-GPU level-2 split of the reduced system (slab r = blocks [b_lo, b_hi), see api.cu) ----
+// The world − 1 slab separators' level-2 system is solved mode-partitioned: owner q of
+// the modes [q·Kq, (q+1)·Kq) receives 4 rows per mode from every slab and returns each slab the 2 rows
+// it needs — two all-to-alls of 4·K and 2·K doubles in total per rank instead of an all-gather.
+// Buffer layouts (Kq = ⌈K / W⌉, m' = m − q·Kq): seg (from local) [q][4][Kq] per slab; the owner's input
+// [r][4][Kq] (slab r's rows at stride `in_r`); the owner's output [r][2][Kq] (slab r's (h_{r−1}, h_r)
+// at stride `out_r`); a slab's fix-up input [q][2][Kq].
 // (1) the slab's L3 interior separators b_lo .. b_hi − 2 (right-hand sides zA[g] − zB[g + 1] from the
-// slab's own blocks) by Thomas with the level-2 pivots; segbuf[r] = (first, last, zA[b_hi − 1], zB[b_lo])
+// slab's own blocks) by Thomas with the level-2 pivots; rows (first, last, zA[b_hi − 1], zB[b_lo])
 __global__ void k_red3_local(DevTables3 T, const double* __restrict__ zB, const double* __restrict__ zA,
-                             double* __restrict__ hsep, double* __restrict__ segbuf) {
+                             double* __restrict__ hsep, double* __restrict__ seg, int Kq) {
   const int N = T.N, L3 = T.L3, g0 = T.b_lo;
   const size_t K = (size_t)N * N;
   const size_t m = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (m >= K) return;
-  double* sb = segbuf + (size_t)T.rank * 4 * K;
+  const int q = (int)(m / Kq), mp = (int)(m - (size_t)q * Kq);
+  double* sb = seg + (size_t)q * 4 * Kq + mp;
   const int ll = (int)(m / N), kk = (int)(m % N);
   if (ll == 0 || kk == 0) {   // not a mode (k_sweep3 leaves these rows untouched)
     for (int p = 0; p < L3; ++p) hsep[(size_t)(g0 + p) * K + m] = 0.0;
-    sb[m] = sb[K + m] = sb[2 * K + m] = sb[3 * K + m] = 0.0;
+    sb[0] = sb[Kq] = sb[2 * Kq] = sb[3 * Kq] = 0.0;
     return;
   }
   const double a = T.red_a[m];
@@ -652,62 +662,63 @@ __global__ void k_red3_local(DevTables3 T, const double* __restrict__ zB, const 
     }
     first = z;
   }
-  sb[m] = first;
-  sb[K + m] = last;
-  sb[2 * K + m] = T.b_hi < T.P ? zA[(size_t)(T.b_hi - 1) * K + m] : 0.0;
-  sb[3 * K + m] = zB[(size_t)g0 * K + m];
+  sb[0] = first;
+  sb[Kq] = last;
+  sb[2 * Kq] = T.b_hi < T.P ? zA[(size_t)(T.b_hi - 1) * K + m] : 0.0;
+  sb[3 * Kq] = zB[(size_t)g0 * K + m];
 }
 
-// (2) every rank: tridiag(A2, B2, A2) on the world − 1 slab separators per mode, right-hand side
-// zA[s] − zB[s + 1] − a·last_q − a·first_{q+1} (the two halves from the slabs on either side)
-__global__ void k_red3_solve(DevTables3 T, const double* __restrict__ segbuf, double* __restrict__ h2) {
-  const int N = T.N, W = T.world, L3 = T.L3;
+// (2) owner q (= T.rank): tridiag(A2, B2, A2) on the world − 1 slab separators for its modes, right-hand
+// side zA[s] − zB[s + 1] − a·last_s − a·first_{s+1} (slab s and s + 1 rows); separator s goes to slab s
+// as its h_r and to slab s + 1 as its h_{r−1}
+__global__ void k_red3_solve(DevTables3 T, const double* __restrict__ in, size_t in_r, double* __restrict__ out,
+                             size_t out_r, int Kq) {
+  const int N = T.N, W = T.world, L3 = T.L3, q = T.rank;
   const size_t K = (size_t)N * N;
-  const size_t m = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (m >= K || W < 2) return;
+  const int mp = blockIdx.x * blockDim.x + threadIdx.x;
+  const size_t m = (size_t)q * Kq + mp;
+  if (mp >= Kq || m >= K || W < 2) return;
   const int ll = (int)(m / N), kk = (int)(m % N);
-  if (ll == 0 || kk == 0) {
-    for (int q = 0; q < W - 1; ++q) h2[(size_t)q * K + m] = 0.0;
-    return;
-  }
-  const double a = T.red_a[m], A2 = T.red3_a[m], B2 = T.red3_b[m];
+  const bool mode = ll != 0 && kk != 0;
+  const double a = mode ? T.red_a[m] : 0.0, A2 = mode ? T.red3_a[m] : 0.0, B2 = mode ? T.red3_b[m] : 1.0;
   double c = B2, y = 0.0, ci = 0.0;
-  for (int q = 0; q < W - 1; ++q) {
-    const double* sq = segbuf + (size_t)q * 4 * K;
-    const double* sn = segbuf + (size_t)(q + 1) * 4 * K;
-    double r = sq[2 * K + m] - sn[3 * K + m];
-    if (L3 > 0) r -= a * sq[K + m] + a * sn[m];
-    if (q) c = B2 - A2 * A2 * ci;
-    y = q ? r - A2 * y * ci : r;
+  double cinv[64], yv[64];   // world ≤ 64
+  for (int s = 0; s < W - 1; ++s) {
+    const double* sl = in + s * in_r + mp;          // slab s: (first, last, zA_sep, zB_first) at stride Kq
+    const double* sr = in + (s + 1) * in_r + mp;
+    double r = sl[2 * Kq] - sr[3 * Kq];
+    if (L3 > 0) r -= a * sl[Kq] + a * sr[0];
+    if (s) c = B2 - A2 * A2 * ci;
+    y = s ? r - A2 * y * ci : r;
     ci = 1.0 / c;
-    h2[(size_t)q * K + m] = y;
+    cinv[s] = ci;
+    yv[s] = y;
   }
-  double cinv[64];   // world ≤ 64
-  double cc = B2;
-  for (int q = 0; q < W - 1; ++q) {
-    if (q) cc = B2 - A2 * A2 * cinv[q - 1];
-    cinv[q] = 1.0 / cc;
+  double hn = 0.0;
+  for (int s = W - 2; s >= 0; --s) {
+    hn = s == W - 2 ? yv[s] * cinv[s] : (yv[s] - A2 * hn) * cinv[s];
+    if (!mode) hn = 0.0;
+    out[s * out_r + Kq + mp] = hn;              // slab s: h_r
+    out[(s + 1) * out_r + mp] = hn;             // slab s + 1: h_{r−1}
   }
-  double hn = h2[(size_t)(W - 2) * K + m] * cinv[W - 2];
-  h2[(size_t)(W - 2) * K + m] = hn;
-  for (int q = W - 3; q >= 0; --q) {
-    hn = (h2[(size_t)q * K + m] - A2 * hn) * cinv[q];
-    h2[(size_t)q * K + m] = hn;
-  }
+  out[mp] = 0.0;                                // slab 0 has no left slab separator
+  out[(W - 1) * out_r + Kq + mp] = 0.0;         // the last slab has no right one
 }
 
-// (3) the slab's interior separators x = z − a h2_{r−1} Z2_L[p] − a h2_r Z2_R[p], and its two slab
-// separators (the values the fixed-up inverse of the slab's planes reads)
-__global__ void k_red3_fixup(DevTables3 T, const double* __restrict__ h2, double* __restrict__ hsep) {
+// (3) slab r: interior separators x = z − a h_{r−1} Z2_L[p] − a h_r Z2_R[p], and its two slab
+// separators (the values the fixed-up inverse of the slab's planes reads); hin = [q][2][Kq]
+__global__ void k_red3_fixup(DevTables3 T, const double* __restrict__ hin, double* __restrict__ hsep, int Kq) {
   const int N = T.N, W = T.world, L3 = T.L3, r = T.rank, g0 = T.b_lo;
   const size_t K = (size_t)N * N;
   const size_t m = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (m >= K) return;
+  const int q = (int)(m / Kq), mp = (int)(m - (size_t)q * Kq);
+  const double hlv = hin[(size_t)q * 2 * Kq + mp], hrv = hin[(size_t)q * 2 * Kq + Kq + mp];
   const int ll = (int)(m / N), kk = (int)(m % N);
   const bool mode = ll != 0 && kk != 0;
   const double a = mode ? T.red_a[m] : 0.0;
-  const double hl = r > 0 ? a * h2[(size_t)(r - 1) * K + m] : 0.0;
-  const double hr = r < W - 1 ? a * h2[(size_t)r * K + m] : 0.0;
+  const double hl = r > 0 ? a * hlv : 0.0;
+  const double hr = r < W - 1 ? a * hrv : 0.0;
   for (int p = 0; p < L3; ++p) {
     double x = hsep[(size_t)(g0 + p) * K + m];
     if (mode) {
@@ -716,8 +727,8 @@ __global__ void k_red3_fixup(DevTables3 T, const double* __restrict__ h2, double
     }
     hsep[(size_t)(g0 + p) * K + m] = x;
   }
-  if (r < W - 1) hsep[(size_t)(T.b_hi - 1) * K + m] = mode ? h2[(size_t)r * K + m] : 0.0;
-  if (r > 0) hsep[(size_t)(g0 - 1) * K + m] = mode ? h2[(size_t)(r - 1) * K + m] : 0.0;
+  if (r < W - 1) hsep[(size_t)(T.b_hi - 1) * K + m] = mode ? hrv : 0.0;
+  if (r > 0) hsep[(size_t)(g0 - 1) * K + m] = mode ? hlv : 0.0;
 }
 
 // A7 (3D): ten-point interpolation at the control points
@@ -744,6 +755,7 @@ __global__ void k_interp3(DevTables3 T, const double* __restrict__ phi, const do
   for (int p = 0; p < 10; ++p) {
     const int ni = c0 + off[p][0], nj = c1 + off[p][1], nk = c2 + off[p][2];
     if (partial && (ni < T.i_lo || ni > T.i_hi)) continue;   // multi-GPU: the plane owner contributes
+    KFBI_CHECK(ni >= 1 && ni < N && nj >= 1 && nj < N && nk >= 1 && nk < N, ni, (long long)nj * N + nk);
     double v = work[(size_t)(ni - 1) * N * N + (size_t)nj * N + nk];
     if ((code >> p) & 1) {
       const double dx = T.lo + ni * T.h - zx, dy = T.lo + nj * T.h - zy, dz = T.lo + nk * T.h - zz;
@@ -844,18 +856,19 @@ void launch_reduced3(const DevTables3& T, const double* zB, const double* zA, do
   ++g_launches;
   k_reduced3<<<cdiv3((long)T.N * T.N, 128), 128, 0, s>>>(T, zB, zA, hsep);
 }
-void launch_red3_local(const DevTables3& T, const double* zB, const double* zA, double* hsep, double* segbuf,
+void launch_red3_local(const DevTables3& T, const double* zB, const double* zA, double* hsep, double* seg, int Kq,
                        cudaStream_t s) {
   ++g_launches;
-  k_red3_local<<<cdiv3((long)T.N * T.N, 128), 128, 0, s>>>(T, zB, zA, hsep, segbuf);
+  k_red3_local<<<cdiv3((long)T.N * T.N, 128), 128, 0, s>>>(T, zB, zA, hsep, seg, Kq);
 }
-void launch_red3_solve(const DevTables3& T, const double* segbuf, double* h2, cudaStream_t s) {
+void launch_red3_solve(const DevTables3& T, const double* in, size_t in_r, double* out, size_t out_r, int Kq,
+                       cudaStream_t s) {
   ++g_launches;
-  k_red3_solve<<<cdiv3((long)T.N * T.N, 128), 128, 0, s>>>(T, segbuf, h2);
+  k_red3_solve<<<cdiv3(Kq, 128), 128, 0, s>>>(T, in, in_r, out, out_r, Kq);
 }
-void launch_red3_fixup(const DevTables3& T, const double* h2, double* hsep, cudaStream_t s) {
+void launch_red3_fixup(const DevTables3& T, const double* hin, double* hsep, int Kq, cudaStream_t s) {
   ++g_launches;
-  k_red3_fixup<<<cdiv3((long)T.N * T.N, 128), 128, 0, s>>>(T, h2, hsep);
+  k_red3_fixup<<<cdiv3((long)T.N * T.N, 128), 128, 0, s>>>(T, hin, hsep, Kq);
 }
 void launch_interp3(const DevTables3& T, const double* phi, const double* dphi, const double* fz,
                     const double* jz_given, const double* work, double* out, cudaStream_t s, bool partial) {

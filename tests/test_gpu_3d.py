@@ -135,8 +135,9 @@ def test_solve3d_C5_256():
 def test_partitioned_apply3d_matches_single(prob, world):
     """All slabs in one context (rank = −1): block sweeps per slab, the level-2 split of the reduced
     system (slab interior separators eliminated locally, L3 = P/world − 1 = 1, 0, 0, 3, 3 here; the
-    world − 1 slab separators solved after the 4-row exchange) and the disjoint partial interpolation
-    sums reproduce world = 1 (to summation order) and the oracle."""
+    world − 1 slab separators solved mode-partitioned, each owner reading the slabs' rows of its K/world
+    modes as the all-to-all delivers them) and the disjoint partial interpolation sums reproduce
+    world = 1 (to summation order) and the oracle."""
     k1 = gpu(prob)
     kw = KFBI(prob, world=world, rank=-1)
     for seed in (0, 1):

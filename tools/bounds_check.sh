@@ -5,4 +5,4 @@ export PYTHONPATH=.
 python tools/sanitize_run.py > gpurun_out/r2_bounds_workload.log 2>&1; echo "workload rc=$?" >> gpurun_out/r2_bounds_workload.log
 python -m pytest tests -m gpu -x -q > gpurun_out/r2_bounds_tests.log 2>&1; echo "tests rc=$?" >> gpurun_out/r2_bounds_tests.log
 grep -h "KFBI_CHECK" gpurun_out/r2_bounds_*.log | head
-tail -3 gpurun_out/r2_bounds_workload.log gpurun_out/r2_bounds_tests.log
+tail -n 3 gpurun_out/r2_bounds_workload.log; tail -n 3 gpurun_out/r2_bounds_tests.log

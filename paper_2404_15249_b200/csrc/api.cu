@@ -62,6 +62,7 @@ struct kfbi_ctx {
   ncclComm_t comm = nullptr;
   double *segbuf = nullptr, *h2 = nullptr, *parts = nullptr;
   double *seg3 = nullptr, *seg3_in = nullptr, *h3_out = nullptr, *h3_in = nullptr;   // 3D level-2 exchange
+  std::vector<DevTables> slabs;   // per-rank slab tables (2D), rebuilt with the workspace layout
   Setup S;
   DevTables T{};
   Setup3 S3;
@@ -136,6 +137,7 @@ struct Arena {
 };
 
 DevTables slab(const kfbi_ctx* c, int r);
+DevTables slab_build(const kfbi_ctx* c, int r);
 
 // Ω nodes before each grid row of `width` nodes (rows × width = the full node grid, row-major)
 void omega_rows(kfbi_ctx* c, const std::vector<int8_t>& side, int64_t rows, int64_t width) {
@@ -254,7 +256,9 @@ void layout(kfbi_ctx* c, Arena& A) {
   c->h2 = A.take<double>(nseg * N);
   c->parts = A.take<double>((size_t)std::max(c->world, 1) * M);
   T.sn_i = A.table(S.sn_i);
-  c->T = slab(c, c->rank >= 0 ? c->rank : 0);
+  c->slabs.clear();
+  c->T = slab_build(c, c->rank >= 0 ? c->rank : 0);
+  for (int r = 0; r < std::max(c->world, 1); ++r) c->slabs.push_back(slab_build(c, r));
 }
 
 void layout3(kfbi_ctx* c, Arena& A) {
@@ -330,7 +334,7 @@ void layout3(kfbi_ctx* c, Arena& A) {
 int nctrl(const kfbi_ctx* c) { return c->dim == 3 ? c->S3.nq : c->S.M; }
 
 // DevTables restricted to the slab of rank r of `world` (full domain when world == 1)
-DevTables slab(const kfbi_ctx* c, int r) {
+DevTables slab_build(const kfbi_ctx* c, int r) {
   DevTables T = c->T;
   const Setup& S = c->S;
   const int world = c->world;
@@ -353,6 +357,12 @@ DevTables slab(const kfbi_ctx* c, int r) {
   T.irr_lo = S.col_ptr[T.col_lo];
   T.irr_hi = S.col_ptr[T.col_hi + 1];
   return T;
+}
+
+// the slab tables of rank r, built once per workspace (slab_build walks the stencil-column items)
+DevTables slab(const kfbi_ctx* c, int r) {
+  if (r >= 0 && r < (int)c->slabs.size()) return c->slabs[r];
+  return slab_build(c, r);
 }
 
 // 3D slab of rank r: whole ADM blocks (15 planes + separator), P / world per rank

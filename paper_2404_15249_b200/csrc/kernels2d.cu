@@ -143,8 +143,8 @@ __global__ void k_correct(DevTables T, const double* __restrict__ phi, const dou
 constexpr int kSweepThreads = 256;
 constexpr int kEntCap = 768;                 // sparse entries staged per pass (k_sweep shared memory)
 constexpr int kQuads = kSweepThreads / 2;   // 128 quads {t, N−t, N/2−t, N/2+t} per CTA chunk
-constexpr int kRotSteps = 4;                 // quads per phase-1 item (t = base + kRotStride·s)
-constexpr int kRotStride = kQuads / kRotSteps;  // 32
+constexpr int kRotSteps = 8;                 // quads per phase-1 item (t = base + kRotStride·s)
+constexpr int kRotStride = kQuads / kRotSteps;  // 16
 // Persistent CTAs, each owning a fixed chunk of 256 quads of sine modes {t, N−t, N/2−t, N/2+t}
 // (spectral positions 4t..4t+3, see mode_position) and iterating over blocks g of BL−1 columns
 // (+ the separator column).  Phase 1 (A4, DST of the staged sparse corrections): with
@@ -180,21 +180,11 @@ __global__ void __launch_bounds__(kSweepThreads, 2) k_sweep(DevTables T, const d
   // sectors; the bank-conflict-free mapping w = τ/128 measured 12% slower: half-sector stores)
   const int qq = q0 + (threadIdx.x >> 1), w = threadIdx.x & 1;
   const bool active = qq < quarter;
-  const int p1 = active ? 4 * qq + 2 * w : 1, p2 = p1 + 1;   // spectral positions of this thread
-  double ic1[LB], ic2[LB];   // 1/c_p for both modes, fixed for the CTA lifetime
-  {
-    const double d1 = T.dk[p1], d2 = T.dk[p2];
-    double c1 = d1, c2 = d2;
-#pragma unroll
-    for (int p = 0; p < LB; ++p) {
-      if (p) {
-        c1 = d1 - ic1[p - 1];
-        c2 = d2 - ic2[p - 1];
-      }
-      ic1[p] = 1.0 / c1;
-      ic2[p] = 1.0 / c2;
-    }
-  }
+  const int p1 = active ? 4 * qq + 2 * w : 0, p2 = p1 + 1;   // spectral positions of this thread
+  // block pivots 1/c_p of this thread's two modes from the setup table (bitwise the recurrence
+  // c_1 = d, c_p = d − 1/c_{p−1}); read per block from L1/L2 instead of held in 60 registers, which
+  // phase 1's eight-quad items use
+  auto icp = [&](int p) { return __ldg(reinterpret_cast<const double2*>(T.invc + (size_t)p * N + p1)); };
   const double h2 = T.h * T.h;
   const int slot = threadIdx.x >> 1;
   double* Rs = R + slot;           // Rs[(4c + u)·kQuads], u: 0 A_o, 1 B_o, 2 A_e, 3 B_e
@@ -338,6 +328,9 @@ __global__ void __launch_bounds__(kSweepThreads, 2) k_sweep(DevTables T, const d
       }
     };
     // y_p overwrites this thread's own two sum slots of row p (the partner thread owns the others)
+    double2 ic[LB];
+#pragma unroll
+    for (int p = 0; p < LB; ++p) ic[p] = icp(p);
     double y1, y2;
     rhs(0, y1, y2);
     Rs[w * kQuads] = y1;
@@ -346,20 +339,20 @@ __global__ void __launch_bounds__(kSweepThreads, 2) k_sweep(DevTables T, const d
     for (int p = 1; p < LB; ++p) {
       double r1, r2;
       rhs(p, r1, r2);
-      y1 = fma(-y1, ic1[p - 1], r1);
-      y2 = fma(-y2, ic2[p - 1], r2);
+      y1 = fma(-y1, ic[p - 1].x, r1);
+      y2 = fma(-y2, ic[p - 1].y, r2);
       Rs[(4 * p + w) * kQuads] = y1;
       Rs[(4 * p + 2 + w) * kQuads] = y2;
     }
     double sep1 = 0.0, sep2 = 0.0;
     if (g < T.P - 1) rhs(LB, sep1, sep2);
-    double z1 = y1 * ic1[LB - 1], z2 = y2 * ic2[LB - 1];
+    double z1 = y1 * ic[LB - 1].x, z2 = y2 * ic[LB - 1].y;
     const double zl1 = z1, zl2 = z2;
     *reinterpret_cast<double2*>(spec + (size_t)(c0 - 1 + LB - 1) * N + p1) = make_double2(z1, z2);
 #pragma unroll
     for (int p = LB - 2; p >= 0; --p) {
-      z1 = (Rs[(4 * p + w) * kQuads] - z1) * ic1[p];
-      z2 = (Rs[(4 * p + 2 + w) * kQuads] - z2) * ic2[p];
+      z1 = (Rs[(4 * p + w) * kQuads] - z1) * ic[p].x;
+      z2 = (Rs[(4 * p + 2 + w) * kQuads] - z2) * ic[p].y;
       *reinterpret_cast<double2*>(spec + (size_t)(c0 - 1 + p) * N + p1) = make_double2(z1, z2);
     }
     *reinterpret_cast<double2*>(zB + (size_t)g * N + p1) = make_double2(z1, z2);

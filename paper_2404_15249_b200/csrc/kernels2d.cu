@@ -328,31 +328,28 @@ __global__ void __launch_bounds__(kSweepThreads, 2) k_sweep(DevTables T, const d
       }
     };
     // y_p overwrites this thread's own two sum slots of row p (the partner thread owns the others)
-    double2 ic[LB];
-#pragma unroll
-    for (int p = 0; p < LB; ++p) ic[p] = icp(p);
-    double y1, y2;
-    rhs(0, y1, y2);
-    Rs[w * kQuads] = y1;
-    Rs[(2 + w) * kQuads] = y2;
+    // the forward values y stay in registers (no shared-memory round trip); pivots per step
+    double y1[LB], y2[LB];
+    rhs(0, y1[0], y2[0]);
 #pragma unroll
     for (int p = 1; p < LB; ++p) {
       double r1, r2;
       rhs(p, r1, r2);
-      y1 = fma(-y1, ic[p - 1].x, r1);
-      y2 = fma(-y2, ic[p - 1].y, r2);
-      Rs[(4 * p + w) * kQuads] = y1;
-      Rs[(4 * p + 2 + w) * kQuads] = y2;
+      const double2 c = icp(p - 1);
+      y1[p] = fma(-y1[p - 1], c.x, r1);
+      y2[p] = fma(-y2[p - 1], c.y, r2);
     }
     double sep1 = 0.0, sep2 = 0.0;
     if (g < T.P - 1) rhs(LB, sep1, sep2);
-    double z1 = y1 * ic[LB - 1].x, z2 = y2 * ic[LB - 1].y;
+    const double2 cl = icp(LB - 1);
+    double z1 = y1[LB - 1] * cl.x, z2 = y2[LB - 1] * cl.y;
     const double zl1 = z1, zl2 = z2;
     *reinterpret_cast<double2*>(spec + (size_t)(c0 - 1 + LB - 1) * N + p1) = make_double2(z1, z2);
 #pragma unroll
     for (int p = LB - 2; p >= 0; --p) {
-      z1 = (Rs[(4 * p + w) * kQuads] - z1) * ic[p].x;
-      z2 = (Rs[(4 * p + 2 + w) * kQuads] - z2) * ic[p].y;
+      const double2 c = icp(p);
+      z1 = (y1[p] - z1) * c.x;
+      z2 = (y2[p] - z2) * c.y;
       *reinterpret_cast<double2*>(spec + (size_t)(c0 - 1 + p) * N + p1) = make_double2(z1, z2);
     }
     *reinterpret_cast<double2*>(zB + (size_t)g * N + p1) = make_double2(z1, z2);

@@ -143,6 +143,8 @@ __global__ void k_correct(DevTables T, const double* __restrict__ phi, const dou
 constexpr int kSweepThreads = 256;
 constexpr int kEntCap = 768;                 // sparse entries staged per pass (k_sweep shared memory)
 constexpr int kQuads = kSweepThreads / 2;   // 128 quads {t, N−t, N/2−t, N/2+t} per CTA chunk
+constexpr int kRs = kQuads + 8;              // sum-row stride: rows 2r and 2r + 1 start 16 banks apart,
+                                             // so phase 2's paired reads (w = 0, 1) do not conflict
 constexpr int kRotSteps = 8;                 // quads per phase-1 item (t = base + kRotStride·s)
 constexpr int kRotStride = kQuads / kRotSteps;  // 16
 // Persistent CTAs, each owning a fixed chunk of 256 quads of sine modes {t, N−t, N/2−t, N/2+t}
@@ -162,8 +164,8 @@ __global__ void __launch_bounds__(kSweepThreads, 2) k_sweep(DevTables T, const d
                                                            double* __restrict__ zA) {
   extern __shared__ double sm[];
   const int N = T.N, half = N >> 1, quarter = N >> 2, m2 = 2 * N - 1, B = kSweepThreads;
-  double* R = sm;                                            // [4·BL sums][kQuads]
-  double4* ent = reinterpret_cast<double4*>(R + (size_t)BL * 4 * kQuads);   // (c, j, cos Δ, sin Δ)
+  double* R = sm;                                            // [4·BL sums][kRs]
+  double4* ent = reinterpret_cast<double4*>(R + (size_t)BL * 4 * kRs);   // (c, j, cos Δ, sin Δ)
   // ent = (c, c·sin(πj/2) (odd j) or c·cos(πj/2) (even j), cos Δ, sin Δ), Δ = π·kRotStride·j/N
   const int ecap = T.maxe < kEntCap ? T.maxe : kEntCap;     // entries staged per pass
   int* ent_j = reinterpret_cast<int*>(ent + ecap);
@@ -187,7 +189,7 @@ __global__ void __launch_bounds__(kSweepThreads, 2) k_sweep(DevTables T, const d
   auto icp = [&](int p) { return __ldg(reinterpret_cast<const double2*>(T.invc + (size_t)p * N + p1)); };
   const double h2 = T.h * T.h;
   const int slot = threadIdx.x >> 1;
-  double* Rs = R + slot;           // Rs[(4c + u)·kQuads], u: 0 A_o, 1 B_o, 2 A_e, 3 B_e
+  double* Rs = R + slot;           // Rs[(4c + u)·kRs], u: 0 A_o, 1 B_o, 2 A_e, 3 B_e
   // blocks in descending count of sparse entries (setup order `blk_order`), snake-dealt over the
   // G block groups so that the groups that draw the blocks where Γ runs along x are not the tail
   const int grp = blockIdx.x / nch;
@@ -265,11 +267,11 @@ __global__ void __launch_bounds__(kSweepThreads, 2) k_sweep(DevTables T, const d
       for (int q = 0; q < kRotSteps; ++q) {
         const int sl = qg + kRotStride * q;
         if (ch == 0 && sl == 0) continue;     // quad slot 0 of chunk 0: the special modes below
-        double* r = R + 4 * c * kQuads + sl;   // only this item writes these slots: no barrier needed
+        double* r = R + 4 * c * kRs + sl;   // only this item writes these slots: no barrier needed
         r[0] = pass ? r[0] + Ao[q] : Ao[q];
-        r[kQuads] = pass ? r[kQuads] + Bo[q] : Bo[q];
-        r[2 * kQuads] = pass ? r[2 * kQuads] + Ae[q] : Ae[q];
-        r[3 * kQuads] = pass ? r[3 * kQuads] + Be[q] : Be[q];
+        r[kRs] = pass ? r[kRs] + Bo[q] : Bo[q];
+        r[2 * kRs] = pass ? r[2 * kRs] + Ae[q] : Ae[q];
+        r[3 * kRs] = pass ? r[3 * kRs] + Be[q] : Be[q];
       }
     }
     if (ch == 0) {   // CTA-uniform: all lanes take part in the shuffles
@@ -291,13 +293,13 @@ __global__ void __launch_bounds__(kSweepThreads, 2) k_sweep(DevTables T, const d
         r3 += __shfl_xor_sync(0xffffffffu, r3, o);
       }
       if (sub == 0 && c < ncol) {
-        double* r = R + 4 * c * kQuads;
+        double* r = R + 4 * c * kRs;
         const double v0 = 0.5 * rh, v2 = -0.5 * rh;                   // (A_o + A_e, A_o − A_e) = (0, r_{N/2})
         const double v1 = 0.5 * (rq + r3), v3 = 0.5 * (r3 - rq);     // (B_o − B_e, B_o + B_e) = (r_{N/4}, r_{3N/4})
         r[0] = pass ? r[0] + v0 : v0;
-        r[kQuads] = pass ? r[kQuads] + v1 : v1;
-        r[2 * kQuads] = pass ? r[2 * kQuads] + v2 : v2;
-        r[3 * kQuads] = pass ? r[3 * kQuads] + v3 : v3;
+        r[kRs] = pass ? r[kRs] + v1 : v1;
+        r[2 * kRs] = pass ? r[2 * kRs] + v2 : v2;
+        r[3 * kRs] = pass ? r[3 * kRs] + v3 : v3;
       }
     }
     }   // entry passes
@@ -306,7 +308,7 @@ __global__ void __launch_bounds__(kSweepThreads, 2) k_sweep(DevTables T, const d
     // ---- phase 2: local Thomas, y_p = r_p − y_{p−1}/c_{p−1}, z_p = (y_p − z_{p+1})/c_p ----
     // this thread's two right-hand sides from the quad sums (w = 0: t, N−t; w = 1: N/2−t, N/2+t)
     auto rhs = [&](int c, double& r1, double& r2) {
-      const double A = Rs[(4 * c + w) * kQuads], E = Rs[(4 * c + 2 + w) * kQuads];
+      const double A = Rs[(4 * c + w) * kRs], E = Rs[(4 * c + 2 + w) * kRs];
       r1 = w ? A - E : A + E;
       r2 = w ? A + E : A - E;
       if (DENSE) {   // f̂ = base + Σ a_h bump_h, one fma per bump in order
@@ -1576,7 +1578,7 @@ void launch_sweep(const DevTables& T, const double* cval, const DenseSrc& D, dou
                   double* zlast, double* fsep, cudaStream_t s) {
   const int dense = !D.any() ? 0 : D.nb > 0 ? 2 : 1;
   (void)zlast;
-  const size_t sm = (size_t)BL * 4 * kQuads * sizeof(double) + (size_t)std::min(T.maxe, kEntCap) * 5 * sizeof(double) +
+  const size_t sm = (size_t)BL * 4 * kRs * sizeof(double) + (size_t)std::min(T.maxe, kEntCap) * 5 * sizeof(double) +
                     (size_t)(2 * T.N / 64 + 2 * T.N / 512 + 2 + 72 + 1) * sizeof(double2) + 3 * BL * sizeof(int);
   smem_optin((const void*)k_sweep<0>, 227 * 1024);
   smem_optin((const void*)k_sweep<1>, 227 * 1024);

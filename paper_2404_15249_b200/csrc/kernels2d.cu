@@ -182,7 +182,7 @@ __global__ void __launch_bounds__(kSweepThreads, 2) k_sweep(DevTables T, const d
   // sectors; the bank-conflict-free mapping w = τ/128 measured 12% slower: half-sector stores)
   const int qq = q0 + (threadIdx.x >> 1), w = threadIdx.x & 1;
   const bool active = qq < quarter;
-  const int p1 = active ? 4 * qq + 2 * w : 0, p2 = p1 + 1;   // spectral positions of this thread
+  const int p1 = active ? 4 * qq + 2 * w : 0;   // spectral positions p1, p1 + 1 of this thread
   // block pivots 1/c_p of this thread's two modes from the setup table (bitwise the recurrence
   // c_1 = d, c_p = d − 1/c_{p−1}); read per block from L1/L2 instead of held in 60 registers, which
   // phase 1's eight-quad items use
@@ -594,6 +594,7 @@ __global__ void __launch_bounds__(kInvThreads, 2) k_inv_sparse(DevTables T, cons
   extern __shared__ double smx[];
   __shared__ int s_rows[kMaxColRows];
   __shared__ double2 s_step[kMaxColRows];   // (cos, sin)(πjB/N) of each row: the recurrence step
+  __shared__ double s_xq[3];                // modes N/4, N/2, 3N/4 of the column (thread 0's quad slot)
   const int N = T.N, half = N >> 1, quarter = N >> 2, m2 = 2 * N - 1, B = kInvThreads, P = T.P;
   // ASYNC: e^{iπr/N} from two small tables (th, tl: 5 KB) and the next item's own spectral row
   // streamed into `xs` by cp.async while this one is evaluated; else the 64 KB sine table
@@ -731,6 +732,11 @@ __global__ void __launch_bounds__(kInvThreads, 2) k_inv_sparse(DevTables T, cons
     const int rd = (srow * B) & m2;
     s_step[threadIdx.x] = make_double2(cosr(rd), sinr(rd));
   }
+  if (threadIdx.x == 0) {
+    s_xq[0] = xq1;
+    s_xq[1] = xq2;
+    s_xq[2] = xq3;
+  }
   __syncthreads();
   const double scale = 2.0 / N;
   const int nrows = u1 - u0;
@@ -803,14 +809,6 @@ __global__ void __launch_bounds__(kInvThreads, 2) k_inv_sparse(DevTables T, cons
         acc[k] = accs[k];
         acc[4 + k] = accc[k];
       }
-      if (threadIdx.x == 0) {
-#pragma unroll
-        for (int k = 0; k < 4; ++k) {
-          const int j = js[k];
-          acc[k] += xq1 * sinr((j * quarter) & m2) + xq2 * sinr((j * half) & m2) +
-                    xq3 * sinr((j * (half + quarter)) & m2);
-        }
-      }
       const double ws = warp_transpose_reduce8(acc);
       if ((lane & 3) == 0) {   // value index v = 4·(lane>>4 & 1) + 2·(lane>>3 & 1) + (lane>>2 & 1): acc[v]
         const int v = ((lane >> 4) & 1) * 4 + ((lane >> 3) & 1) * 2 + ((lane >> 2) & 1);
@@ -827,6 +825,9 @@ __global__ void __launch_bounds__(kInvThreads, 2) k_inv_sparse(DevTables T, cons
       s2 += red[(size_t)w * 2 * T.mcr + 2 * t + 1];
     }
     const int j = s_rows[t];
+    // the special modes, per row here rather than by thread 0 inside every group (no warp-0 divergence)
+    s1 += s_xq[0] * sinr((j * quarter) & m2) + s_xq[1] * sinr((j * half) & m2) +
+          s_xq[2] * sinr((j * (half + quarter)) & m2);
     const double sig = ((j >> 1) & 1) ? -1.0 : 1.0;   // σ_j = sin(πj/2) for odd j
     KFBI_CHECK(u0 + t < T.nsn && j >= 1 && j < N, u0 + t, j);
     vsten[u0 + t] = scale * ((j & 1) ? s1 + sig * s2 : s1);

@@ -562,17 +562,6 @@ __device__ __forceinline__ double fixup_staged(const DevTables& T, const double*
   if (g < P - 1) x = fma(-hsep[(size_t)g * N + k], __ldg(T.zr + (size_t)p * N + k), x);
   return x;
 }
-__device__ __forceinline__ double fixup(const DevTables& T, const double* __restrict__ spec,
-                                        const double* __restrict__ hsep, int i, int k) {
-  const int N = T.N, P = T.P;
-  const int q = i / BL, r = i - q * BL;
-  if (r == 0) return hsep[(size_t)(q - 1) * N + k];
-  const int p = r - 1, g = q;
-  double x = spec[(size_t)(i - 1) * N + k];
-  if (g > 0) x = fma(-hsep[(size_t)(g - 1) * N + k], __ldg(T.zr + (size_t)(LB - 1 - p) * N + k), x);
-  if (g < P - 1) x = fma(-hsep[(size_t)g * N + k], __ldg(T.zr + (size_t)p * N + k), x);
-  return x;
-}
 
 // ------------------------------------------------------------------------------ A6 sparse
 // One CTA per column holding stencil nodes: v_j = (2/N) Σ_k v̂_k sin(πjk/N) at those rows.
@@ -1347,9 +1336,45 @@ __global__ void __launch_bounds__(DenseCfg<N>::NTHR, 1) k_dst_dense2(DevTables T
     }
   } else {   // spectral positions → modes (coalesced reads, scattered shared-memory writes), then pairs
     double* f = reinterpret_cast<double*>(z);
-    for (int p = tid; p < N; p += NTH) {
-      const int k = position_mode(p, N);
-      f[k] = (live && k) ? (staged ? fixup_staged(T, stage, hsep, i, p) : fixup(T, src, hsep, i, p)) : 0.0;
+    if (!staged) {
+      // a quad of positions {t, N−t, N/2−t, N/2+t} per step: two 16-byte loads per row (x, h_{g−1},
+      // Z_L[p], h_g, Z_R[p]), fixed up and scattered to the four modes
+      const int q = i / BL, rr = i - q * BL;
+      const bool sep = rr == 0;
+      const double* xrow = sep ? hsep + (size_t)(q - 1) * N : src + (size_t)(i - 1) * N;
+      const double* hl = (!sep && q > 0) ? hsep + (size_t)(q - 1) * N : nullptr;
+      const double* hr = (!sep && q < T.P - 1) ? hsep + (size_t)q * N : nullptr;
+      const double* zl = T.zr + (size_t)(sep ? 0 : LB - rr) * N;   // Z_L[p] = Z_R[LB−1−p], p = rr − 1
+      const double* zrr = T.zr + (size_t)(sep ? 0 : rr - 1) * N;
+      for (int t = tid; t < N / 4; t += NTH) {
+        double2 a = make_double2(0.0, 0.0), b = a;
+        if (live) {
+          a = reinterpret_cast<const double2*>(xrow + 4 * t)[0];
+          b = reinterpret_cast<const double2*>(xrow + 4 * t)[1];
+          if (hl) {
+            const double2 h0 = reinterpret_cast<const double2*>(hl + 4 * t)[0], h1 = reinterpret_cast<const double2*>(hl + 4 * t)[1];
+            const double2 z0 = __ldg(reinterpret_cast<const double2*>(zl + 4 * t)), z1 = __ldg(reinterpret_cast<const double2*>(zl + 4 * t) + 1);
+            a.x = fma(-h0.x, z0.x, a.x); a.y = fma(-h0.y, z0.y, a.y);
+            b.x = fma(-h1.x, z1.x, b.x); b.y = fma(-h1.y, z1.y, b.y);
+          }
+          if (hr) {
+            const double2 h0 = reinterpret_cast<const double2*>(hr + 4 * t)[0], h1 = reinterpret_cast<const double2*>(hr + 4 * t)[1];
+            const double2 z0 = __ldg(reinterpret_cast<const double2*>(zrr + 4 * t)), z1 = __ldg(reinterpret_cast<const double2*>(zrr + 4 * t) + 1);
+            a.x = fma(-h0.x, z0.x, a.x); a.y = fma(-h0.y, z0.y, a.y);
+            b.x = fma(-h1.x, z1.x, b.x); b.y = fma(-h1.y, z1.y, b.y);
+          }
+        }
+        const int p = 4 * t;
+        f[position_mode(p, N)] = position_mode(p, N) ? a.x : 0.0;   // mode 0 (t = 0, r = 0) is not a mode
+        f[position_mode(p + 1, N)] = a.y;
+        f[position_mode(p + 2, N)] = b.x;
+        f[position_mode(p + 3, N)] = b.y;
+      }
+    } else {
+      for (int p = tid; p < N; p += NTH) {
+        const int k = position_mode(p, N);
+        f[k] = (live && k) ? fixup_staged(T, stage, hsep, i, p) : 0.0;
+      }
     }
     rsync<NTH>();
     if (staged && threadIdx.x == 0 && i + step <= T.col_hi) issue(i + step);

@@ -137,13 +137,17 @@ const char* kfbi_last_setup_error(void);
  * broadcasts it (e.g. as a torch.uint8[128] tensor over torch.distributed) and passes it in
  * kfbi_dist.nccl_id on every rank.  Multi-GPU layout: 2D grids
  * are split along x into `world` slabs of whole level-2 arrowhead segments (512 columns each), so
- * `world` must divide N/512.  Per apply the ranks exchange the segment end values of the reduced
- * system (one ncclAllGather) and sum disjoint partial interpolations (one ncclAllReduce); φ, the
- * outputs and GMRES are replicated.  3D grids are split along x into slabs of whole ADM blocks
- * (15 planes + separator), `world` must divide N/16; per K_D apply the block end values are
- * all-gathered (two ncclAllGather in one group), the reduced system is solved redundantly, and the
- * interpolation partial sums are all-reduced; the once-per-solve dense applies are replicated.  kfbi_dist.rank = −1 with world > 1 runs all ranks' slabs in
- * this one context (single-GPU emulation of the partition, collectives done in device memory). */
+ * `world` must divide N/512; 3D grids into slabs of whole ADM blocks (15 planes + separator), so
+ * `world` must divide N/16.  Each slab solves its blocks, eliminates its interior separators and
+ * publishes 4 values per mode (first, last, its boundary separator's zA, its first block's zB).
+ * Per apply the ranks exchange those rows — 2D: one ncclAllGather, every rank solves the slab
+ * separators; 3D: mode-partitioned, one grouped ncclSend/ncclRecv all-to-all to the owner of
+ * K/world modes and one back with the two rows each slab needs — and sum disjoint partial
+ * interpolations (one ncclAllReduce).  Corrections, LSQ fits, transforms, the once-per-solve dense
+ * applies and the final field run on each rank's slab only (kfbi_local_slab); φ, the outputs and
+ * GMRES are replicated.  kfbi_dist.rank = −1 with world > 1 runs all ranks' slabs in this one
+ * context (single-GPU emulation of the partition; the exchanges become reads of the other slabs'
+ * buffers). */
 kfbi_status kfbi_get_unique_id(void* out128);
 
 /* Slab of `rank` (host): out6 = {first block, end block, first column, last column, first
@@ -157,16 +161,16 @@ kfbi_status kfbi_slab(const kfbi_ctx* ctx, int32_t rank, int64_t* out6);
 kfbi_status kfbi_setup(const kfbi_grid* grid, const kfbi_boundary* bnd, const kfbi_pde* pde,
                        const kfbi_dist* dist, void* stream, kfbi_ctx** out);
 
-/* Procedure 1 with its O(N²) phases on the device (2D only): node
+/* Procedure 1 with its O(N^d) phases on the device (2D and 3D): node
  * classification, the sign-change edges and their intersections by 64-step bisection
  * (readings R30/R31) and the irregular nodes with their incident intersections (P:551,
  * App. A.3) run as kernels on `stream` in the caller's scratch d_scratch (device, ≥ the bytes
- * kfbi_setup_scratch_size returns, borrowed for the call only, contents undefined after); the
- * lists come back to the host (the only host↔device traffic) and the rest of Procedure 1 runs
- * there as in kfbi_setup.  The lists are identical to kfbi_setup's (same arithmetic, IEEE
- * round-to-nearest, no contraction; the star level uses the device sin/atan2, so a node within
- * an ulp of Γ could in principle classify differently).  Synchronous.  Errors as kfbi_setup plus
- * KFBI_ENOMEM (scratch too small), KFBI_ECUDA, KFBI_EUNSUPPORTED (dim = 3). */
+ * kfbi_setup_scratch_size returns — ≈ 5 GB at 512³ — borrowed for the call only, contents undefined
+ * after); the lists come back to the host (the only host↔device traffic) and the rest of Procedure 1
+ * (frames, control points, LSQ neighbourhoods, stencils, per-mode tables) runs there as in kfbi_setup.
+ * The lists are identical to kfbi_setup's (same arithmetic, IEEE round-to-nearest, no contraction; the
+ * star level uses the device sin/atan2, so a node within an ulp of Γ could in principle classify
+ * differently).  Synchronous.  Errors as kfbi_setup plus KFBI_ENOMEM (scratch too small), KFBI_ECUDA. */
 kfbi_status kfbi_setup_scratch_size(const kfbi_grid* grid, size_t* bytes);
 kfbi_status kfbi_setup_device(const kfbi_grid* grid, const kfbi_boundary* bnd, const kfbi_pde* pde,
                               const kfbi_dist* dist, void* stream, void* d_scratch, size_t bytes,

@@ -775,7 +775,7 @@ kfbi_status setup_impl(const kfbi_grid* grid, const kfbi_boundary* bnd, const kf
     }
     if (!grid || !bnd || !pde || !bnd->comp) throw ArgError("null descriptor");
     c->dim = grid->dim;
-    if (c->dim == 3) build_setup3(c->S3, grid, bnd, pde);
+    if (c->dim == 3) build_setup3(c->S3, grid, bnd, pde, dev);
     else build_setup(c->S, grid, bnd, pde, dev);
     if (c->world > 1) {
       if (c->dim == 3) {
@@ -836,11 +836,19 @@ kfbi_status kfbi_setup(const kfbi_grid* grid, const kfbi_boundary* bnd, const kf
 kfbi_status kfbi_setup_scratch_size(const kfbi_grid* grid, size_t* bytes) {
   if (!grid || !bytes) return KFBI_EINVAL;
   *bytes = 0;
-  if (grid->dim != 2) {
-    g_setup_err = "device setup phases are built for dim = 2 only";
-    return KFBI_EUNSUPPORTED;
-  }
   const int N = grid->n[0];
+  if (grid->dim == 3) {
+    if (N < 32 || N > 512 || (N & (N - 1))) {
+      g_setup_err = "3D: n must be a power of two in [32, 512]";
+      return KFBI_EINVAL;
+    }
+    *bytes = gpu_setup_scratch_bytes3(N);
+    return KFBI_OK;
+  }
+  if (grid->dim != 2) {
+    g_setup_err = "dim must be 2 or 3";
+    return KFBI_EINVAL;
+  }
   if (N < 64 || N > 8192 || (N & (N - 1))) {
     g_setup_err = "n must be a power of two in [64, 8192]";
     return KFBI_EINVAL;
@@ -854,9 +862,9 @@ kfbi_status kfbi_setup_device(const kfbi_grid* grid, const kfbi_boundary* bnd, c
                               kfbi_ctx** out) {
   if (!out) return KFBI_EINVAL;
   *out = nullptr;
-  if (!grid || grid->dim != 2) {
-    g_setup_err = "device setup phases are built for dim = 2 only";
-    return grid ? KFBI_EUNSUPPORTED : KFBI_EINVAL;
+  if (!grid || (grid->dim != 2 && grid->dim != 3)) {
+    g_setup_err = "dim must be 2 or 3";
+    return KFBI_EINVAL;
   }
   if (!d_scratch) {
     g_setup_err = "null device scratch";

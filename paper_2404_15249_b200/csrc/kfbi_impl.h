@@ -182,7 +182,10 @@ struct Setup3 {
   int L3 = -1;
   std::vector<double> rinv3, z3r, red3_a, red3_b;
 };
-void build_setup3(Setup3& S, const kfbi_grid* g, const kfbi_boundary* b, const kfbi_pde* pde);
+void build_setup3(Setup3& S, const kfbi_grid* g, const kfbi_boundary* b, const kfbi_pde* pde,
+                  const DeviceScratch* dev = nullptr);
+size_t gpu_setup_scratch_bytes3(int N);
+void gpu_setup_phases3(Setup3& S, void* scratch, size_t bytes, ::CUstream_st* s);
 
 struct DevTables3 {
   int N, P, nq, nirr;

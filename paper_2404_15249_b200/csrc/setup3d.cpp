@@ -73,7 +73,7 @@ bool lu_solve_n(int n, double* A, double* b) {
 
 }  // namespace
 
-void build_setup3(Setup3& S, const kfbi_grid* g, const kfbi_boundary* b, const kfbi_pde* pde) {
+void build_setup3(Setup3& S, const kfbi_grid* g, const kfbi_boundary* b, const kfbi_pde* pde, const DeviceScratch* dev) {
   if (b->ncomp != 1) throw ArgError("3D: exactly one (outer) surface is supported");
   const kfbi_component& in = b->comp[0];
   if (in.kind != KFBI_ELLIPSOID && in.kind != KFBI_TORUS) throw ArgError("3D surfaces: ellipsoid or torus");
@@ -104,62 +104,111 @@ void build_setup3(Setup3& S, const kfbi_grid* g, const kfbi_boundary* b, const k
   auto X = [&](int i) { return lo + i * h; };
   auto lin = [&](int i, int j, int k) { return ((size_t)i * W + j) * W + k; };
 
-  // classification
-  S.side.assign((size_t)W * W * W, 0);
-#pragma omp parallel for schedule(static)
-  for (int i = 0; i < W; ++i)
-    for (int j = 0; j < W; ++j)
-      for (int k = 0; k < W; ++k) S.side[lin(i, j, k)] = inside3(C, X(i), X(j), X(k)) ? 1 : 0;
-  auto side = [&](int i, int j, int k) { return S.side[lin(i, j, k)]; };
-
-  // intersections on sign-change edges, sorted by (axis, i, j, k)
-  struct E { int axis, i, j, k; };
-  std::vector<E> edges;
-  for (int axis = 0; axis < 3; ++axis) {
-    std::vector<std::vector<E>> part(W);
-#pragma omp parallel for schedule(dynamic, 4)
+  if (dev) {   // classification, edges, bisection and the irregular-node lists on the GPU (NEXT-3)
+    gpu_setup_phases3(S, dev->ptr, dev->bytes, dev->stream);
+  } else {
+    // classification
+    S.side.assign((size_t)W * W * W, 0);
+  #pragma omp parallel for schedule(static)
     for (int i = 0; i < W; ++i)
       for (int j = 0; j < W; ++j)
-        for (int k = 0; k < W; ++k) {
-          const int i1 = i + (axis == 0), j1 = j + (axis == 1), k1 = k + (axis == 2);
-          if (i1 > N || j1 > N || k1 > N) continue;
-          if (side(i, j, k) != side(i1, j1, k1)) part[i].push_back({axis, i, j, k});
+        for (int k = 0; k < W; ++k) S.side[lin(i, j, k)] = inside3(C, X(i), X(j), X(k)) ? 1 : 0;
+    auto side = [&](int i, int j, int k) { return S.side[lin(i, j, k)]; };
+
+    // intersections on sign-change edges, sorted by (axis, i, j, k)
+    struct E { int axis, i, j, k; };
+    std::vector<E> edges;
+    for (int axis = 0; axis < 3; ++axis) {
+      std::vector<std::vector<E>> part(W);
+  #pragma omp parallel for schedule(dynamic, 4)
+      for (int i = 0; i < W; ++i)
+        for (int j = 0; j < W; ++j)
+          for (int k = 0; k < W; ++k) {
+            const int i1 = i + (axis == 0), j1 = j + (axis == 1), k1 = k + (axis == 2);
+            if (i1 > N || j1 > N || k1 > N) continue;
+            if (side(i, j, k) != side(i1, j1, k1)) part[i].push_back({axis, i, j, k});
+          }
+      for (auto& p : part) edges.insert(edges.end(), p.begin(), p.end());
+    }
+    const int nq = (int)edges.size();
+    S.nq = nq;
+    S.q_axis.resize(nq); S.q_i.resize(nq); S.q_j.resize(nq); S.q_k.resize(nq);
+    S.q_xi.resize(nq);
+    bool bad = false;
+  #pragma omp parallel for schedule(dynamic, 256)
+    for (int e = 0; e < nq; ++e) {
+      const E ed = edges[e];
+      double p0[3] = {X(ed.i), X(ed.j), X(ed.k)};
+      const bool want = inside3(C, p0[0], p0[1], p0[2]);
+      bool prev = want;
+      int changes = 0;
+      for (double t : {0.2, 0.4, 0.6, 0.8, 1.0}) {
+        double p[3] = {p0[0], p0[1], p0[2]};
+        p[ed.axis] += t * h;
+        const bool cur = inside3(C, p[0], p[1], p[2]);
+        changes += cur != prev;
+        prev = cur;
+      }
+      if (changes != 1) bad = true;
+      double a = 0, bb = 1;
+      for (int it = 0; it < 64; ++it) {
+        const double m = 0.5 * (a + bb);
+        double p[3] = {p0[0], p0[1], p0[2]};
+        p[ed.axis] += m * h;
+        if (inside3(C, p[0], p[1], p[2]) == want) a = m; else bb = m;
+      }
+      const double t = 0.5 * (a + bb);
+      double pos[3] = {p0[0], p0[1], p0[2]};
+      pos[ed.axis] += t * h;
+      S.q_axis[e] = ed.axis; S.q_i[e] = ed.i; S.q_j[e] = ed.j; S.q_k[e] = ed.k;
+      S.q_xi[e] = pos[ed.axis];
+    }
+    if (bad) throw GeomError("grid edge crossed more than once (R31)");
+    // irregular nodes (6 neighbours) sorted by (i, j, k), CSR to their incident intersections
+    std::unordered_map<int64_t, int> qidx;
+    qidx.reserve(2 * (size_t)nq);
+    auto key = [&](int axis, int i, int j, int k) { return (int64_t)axis * W * W * W + (int64_t)lin(i, j, k); };
+    for (int e = 0; e < nq; ++e) qidx[key(S.q_axis[e], S.q_i[e], S.q_j[e], S.q_k[e])] = e;
+    S.irr_lin.clear(); S.irr_side.clear(); S.irr_ptr.assign(1, 0); S.pair_q.clear(); S.pair_d.clear();
+    S.irr_ijk.clear();
+    for (int i = 1; i < N; ++i)
+      for (int j = 1; j < N; ++j)
+        for (int k = 1; k < N; ++k) {
+          const int s0 = side(i, j, k);
+          const int nb[6][3] = {{i - 1, j, k}, {i + 1, j, k}, {i, j - 1, k}, {i, j + 1, k}, {i, j, k - 1}, {i, j, k + 1}};
+          bool irr = false;
+          for (auto& q : nb) irr |= side(q[0], q[1], q[2]) != s0;
+          if (!irr) continue;
+          if (i < 2 || j < 2 || k < 2 || i > N - 2 || j > N - 2 || k > N - 2)
+            throw GeomError("Γ too close to the box boundary (R32)");
+          S.irr_lin.push_back((int64_t)(i - 1) * N * N + (int64_t)j * N + k);
+          S.irr_ijk.push_back(i); S.irr_ijk.push_back(j); S.irr_ijk.push_back(k);
+          S.irr_side.push_back((int8_t)s0);
+          for (int q = 0; q < 6; ++q) {
+            const int oi = nb[q][0], oj = nb[q][1], ok = nb[q][2];
+            if (side(oi, oj, ok) == s0) continue;
+            const int axis = q / 2;
+            const int li = std::min(i, oi), lj = std::min(j, oj), lk = std::min(k, ok);
+            auto it = qidx.find(key(axis, li, lj, lk));
+            if (it == qidx.end()) throw GeomError("internal: missing intersection");
+            const int e = it->second;
+            const double xbar = axis == 0 ? X(oi) : axis == 1 ? X(oj) : X(ok);
+            S.pair_q.push_back(e);
+            S.pair_d.push_back(xbar - S.q_xi[e]);
+          }
+          S.irr_ptr.push_back((int)S.pair_q.size());
         }
-    for (auto& p : part) edges.insert(edges.end(), p.begin(), p.end());
+    S.nirr = (int)S.irr_lin.size();
   }
-  const int nq = (int)edges.size();
-  S.nq = nq;
-  S.q_axis.resize(nq); S.q_i.resize(nq); S.q_j.resize(nq); S.q_k.resize(nq);
-  S.q_xi.resize(nq); S.q_pos.resize(3 * (size_t)nq); S.q_n.resize(3 * (size_t)nq);
-  S.q_e1.resize(3 * (size_t)nq); S.q_e2.resize(3 * (size_t)nq); S.q_kab.resize(3 * (size_t)nq);
-  bool bad = false;
-#pragma omp parallel for schedule(dynamic, 256)
-  for (int e = 0; e < nq; ++e) {
-    const E ed = edges[e];
-    double p0[3] = {X(ed.i), X(ed.j), X(ed.k)};
-    const bool want = inside3(C, p0[0], p0[1], p0[2]);
-    bool prev = want;
-    int changes = 0;
-    for (double t : {0.2, 0.4, 0.6, 0.8, 1.0}) {
-      double p[3] = {p0[0], p0[1], p0[2]};
-      p[ed.axis] += t * h;
-      const bool cur = inside3(C, p[0], p[1], p[2]);
-      changes += cur != prev;
-      prev = cur;
-    }
-    if (changes != 1) bad = true;
-    double a = 0, bb = 1;
-    for (int it = 0; it < 64; ++it) {
-      const double m = 0.5 * (a + bb);
-      double p[3] = {p0[0], p0[1], p0[2]};
-      p[ed.axis] += m * h;
-      if (inside3(C, p[0], p[1], p[2]) == want) a = m; else bb = m;
-    }
-    const double t = 0.5 * (a + bb);
-    double pos[3] = {p0[0], p0[1], p0[2]};
-    pos[ed.axis] += t * h;
-    S.q_axis[e] = ed.axis; S.q_i[e] = ed.i; S.q_j[e] = ed.j; S.q_k[e] = ed.k;
-    S.q_xi[e] = pos[ed.axis];
+  // frames at the intersections (common to the host and device paths): the node coordinates with the
+  // edge axis replaced by ξ
+  const int nqf = S.nq;
+  S.q_pos.resize(3 * (size_t)nqf); S.q_n.resize(3 * (size_t)nqf);
+  S.q_e1.resize(3 * (size_t)nqf); S.q_e2.resize(3 * (size_t)nqf); S.q_kab.resize(3 * (size_t)nqf);
+#pragma omp parallel for schedule(static)
+  for (int e = 0; e < nqf; ++e) {
+    double pos[3] = {X(S.q_i[e]), X(S.q_j[e]), X(S.q_k[e])};
+    pos[S.q_axis[e]] = S.q_xi[e];
     // frame: n = ∇ℓ/|∇ℓ|, e1 = normalize(n × u*), e2 = n × e1, κ_ab = −e_aᵀ D²ℓ e_b / |∇ℓ|
     double gr[3], H[3][3];
     grad_hess(C, pos, gr, H);
@@ -190,43 +239,9 @@ void build_setup3(Setup3& S, const kfbi_grid* g, const kfbi_boundary* b, const k
     S.q_kab[3 * e + 1] = -quad(e1, e2) / gn;
     S.q_kab[3 * e + 2] = -quad(e2, e2) / gn;
   }
-  if (bad) throw GeomError("grid edge crossed more than once (R31)");
-
-  // irregular nodes (6 neighbours) sorted by (i, j, k), CSR to their incident intersections
-  std::unordered_map<int64_t, int> qidx;
-  qidx.reserve(2 * (size_t)nq);
-  auto key = [&](int axis, int i, int j, int k) { return (int64_t)axis * W * W * W + (int64_t)lin(i, j, k); };
-  for (int e = 0; e < nq; ++e) qidx[key(S.q_axis[e], S.q_i[e], S.q_j[e], S.q_k[e])] = e;
-  S.irr_lin.clear(); S.irr_side.clear(); S.irr_ptr.assign(1, 0); S.pair_q.clear(); S.pair_d.clear();
-  S.irr_ijk.clear();
-  for (int i = 1; i < N; ++i)
-    for (int j = 1; j < N; ++j)
-      for (int k = 1; k < N; ++k) {
-        const int s0 = side(i, j, k);
-        const int nb[6][3] = {{i - 1, j, k}, {i + 1, j, k}, {i, j - 1, k}, {i, j + 1, k}, {i, j, k - 1}, {i, j, k + 1}};
-        bool irr = false;
-        for (auto& q : nb) irr |= side(q[0], q[1], q[2]) != s0;
-        if (!irr) continue;
-        if (i < 2 || j < 2 || k < 2 || i > N - 2 || j > N - 2 || k > N - 2)
-          throw GeomError("Γ too close to the box boundary (R32)");
-        S.irr_lin.push_back((int64_t)(i - 1) * N * N + (int64_t)j * N + k);
-        S.irr_ijk.push_back(i); S.irr_ijk.push_back(j); S.irr_ijk.push_back(k);
-        S.irr_side.push_back((int8_t)s0);
-        for (int q = 0; q < 6; ++q) {
-          const int oi = nb[q][0], oj = nb[q][1], ok = nb[q][2];
-          if (side(oi, oj, ok) == s0) continue;
-          const int axis = q / 2;
-          const int li = std::min(i, oi), lj = std::min(j, oj), lk = std::min(k, ok);
-          auto it = qidx.find(key(axis, li, lj, lk));
-          if (it == qidx.end()) throw GeomError("internal: missing intersection");
-          const int e = it->second;
-          const double xbar = axis == 0 ? X(oi) : axis == 1 ? X(oj) : X(ok);
-          S.pair_q.push_back(e);
-          S.pair_d.push_back(xbar - S.q_xi[e]);
-        }
-        S.irr_ptr.push_back((int)S.pair_q.size());
-      }
-  S.nirr = (int)S.irr_lin.size();
+  const int nq = S.nq;
+  auto side = [&](int i, int j, int k) { return S.side[lin(i, j, k)]; };
+  bool bad = false;
 
   // LSQ neighbours: 5×5×5 block of edge low-end nodes; scaled normal matrix inverse
   std::unordered_map<int64_t, std::vector<int>> bucket;

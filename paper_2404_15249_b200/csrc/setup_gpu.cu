@@ -1,4 +1,4 @@
-// GPU-side Procedure 1 for 2D geometries: the O(N²) phases of the
+// GPU-side Procedure 1 for 2D and 3D geometries: the O(N^d) phases of the
 // host setup — node classification, sign-change edges and their intersections by bisection
 // (R30/R31), irregular nodes with their incident intersections (App. A.3) — as one
 // thread per node / edge, the ordered lists by prefix sums (CUB).  The arithmetic is the host's
@@ -209,11 +209,259 @@ size_t lists_bytes(long W) {
          32 * 256;
 }
 
+// ---------------------------------------------------------------------------------------- 3D
+// The same phases for the 3D surfaces (setup3d.cpp): level3 / inside3 with round-to-nearest intrinsics
+// in the host's operation order, edges in (axis, i, j, k) order, irregular nodes in (i, j, k) order
+// with their ≤ 6 incident intersections in the host's neighbour order.
+struct DevComp3 {
+  int kind;
+  double c0, c1, c2, p0, p1, p2;
+};
+__device__ __forceinline__ bool d_inside3(const DevComp3& c, double x, double y, double z) {
+  const double dx = __dsub_rn(x, c.c0), dy = __dsub_rn(y, c.c1), dz = __dsub_rn(z, c.c2);
+  double l;
+  if (c.kind == KFBI_ELLIPSOID) {
+    const double u = __ddiv_rn(dx, c.p0), v = __ddiv_rn(dy, c.p1), w = __ddiv_rn(dz, c.p2);
+    l = __dsub_rn(__dadd_rn(__dadd_rn(__dmul_rn(u, u), __dmul_rn(v, v)), __dmul_rn(w, w)), 1.0);
+  } else {
+    const double q = __dsub_rn(__dsqrt_rn(__dadd_rn(__dmul_rn(dx, dx), __dmul_rn(dy, dy))), c.p0);
+    l = __dsub_rn(__dadd_rn(__dmul_rn(q, q), __dmul_rn(dz, dz)), __dmul_rn(c.p1, c.p1));
+  }
+  return l <= 0.0;
+}
+
+__global__ void k_classify3(int W, double lo, double h, DevComp3 c, int8_t* __restrict__ side) {
+  const long WWW = (long)W * W * W;
+  for (long idx = (long)blockIdx.x * blockDim.x + threadIdx.x; idx < WWW; idx += (long)gridDim.x * blockDim.x) {
+    const int i = (int)(idx / ((long)W * W)), j = (int)((idx / W) % W), k = (int)(idx % W);
+    side[idx] = d_inside3(c, node_x(lo, h, i), node_x(lo, h, j), node_x(lo, h, k)) ? 1 : 0;
+  }
+}
+
+// flag[axis·W³ + lin(i, j, k)] = 1 for a sign-change edge from (i, j, k) along axis
+__global__ void k_edge_flags3(int W, const int8_t* __restrict__ side, int* __restrict__ flag) {
+  const long WWW = (long)W * W * W;
+  for (long idx = (long)blockIdx.x * blockDim.x + threadIdx.x; idx < 3 * WWW; idx += (long)gridDim.x * blockDim.x) {
+    const int axis = (int)(idx / WWW);
+    const long r = idx - axis * WWW;
+    const int i = (int)(r / ((long)W * W)), j = (int)((r / W) % W), k = (int)(r % W);
+    const bool ok = axis == 0 ? i < W - 1 : axis == 1 ? j < W - 1 : k < W - 1;
+    const long st = axis == 0 ? (long)W * W : axis == 1 ? W : 1;
+    flag[idx] = ok && side[r] != side[r + st] ? 1 : 0;
+  }
+}
+
+__global__ void k_edge_compact3(int W, const int* __restrict__ flag, const int* __restrict__ qmap, int* __restrict__ qa,
+                                int* __restrict__ qi, int* __restrict__ qj, int* __restrict__ qk) {
+  const long WWW = (long)W * W * W;
+  for (long idx = (long)blockIdx.x * blockDim.x + threadIdx.x; idx < 3 * WWW; idx += (long)gridDim.x * blockDim.x) {
+    if (!flag[idx]) continue;
+    const int q = qmap[idx], axis = (int)(idx / WWW);
+    const long r = idx - axis * WWW;
+    qa[q] = axis;
+    qi[q] = (int)(r / ((long)W * W));
+    qj[q] = (int)((r / W) % W);
+    qk[q] = (int)(r % W);
+  }
+}
+
+// the double-crossing check at 5 samples (R31) and 64 halvings (R30), as setup3d.cpp
+__global__ void k_bisect3(int nq, double lo, double h, DevComp3 c, const int* __restrict__ qa, const int* __restrict__ qi,
+                          const int* __restrict__ qj, const int* __restrict__ qk, double* __restrict__ xi_out,
+                          int* __restrict__ err) {
+  const int e = blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= nq) return;
+  const int axis = qa[e];
+  const double p0[3] = {node_x(lo, h, qi[e]), node_x(lo, h, qj[e]), node_x(lo, h, qk[e])};
+  auto at = [&](double t) {
+    double p[3] = {p0[0], p0[1], p0[2]};
+    p[axis] = __dadd_rn(p[axis], __dmul_rn(t, h));
+    return d_inside3(c, p[0], p[1], p[2]);
+  };
+  const bool want = d_inside3(c, p0[0], p0[1], p0[2]);
+  bool prev = want;
+  int changes = 0;
+  const double ts[5] = {0.2, 0.4, 0.6, 0.8, 1.0};
+  for (int s = 0; s < 5; ++s) {
+    const bool cur = at(ts[s]);
+    changes += cur != prev;
+    prev = cur;
+  }
+  if (changes != 1) atomicOr(err, 2);
+  double a = 0.0, bb = 1.0;
+  for (int it = 0; it < 64; ++it) {
+    const double m = __dmul_rn(0.5, __dadd_rn(a, bb));
+    if (at(m) == want) a = m;
+    else bb = m;
+  }
+  const double t = __dmul_rn(0.5, __dadd_rn(a, bb));
+  xi_out[e] = __dadd_rn(p0[axis], __dmul_rn(t, h));
+}
+
+__global__ void k_irr_flags3(int N, const int8_t* __restrict__ side, int* __restrict__ iflag, int* __restrict__ err) {
+  const long W = N + 1, WW = W * W, M = N - 1, n = M * M * M;
+  for (long idx = (long)blockIdx.x * blockDim.x + threadIdx.x; idx < n; idx += (long)gridDim.x * blockDim.x) {
+    const int i = 1 + (int)(idx / (M * M)), j = 1 + (int)((idx / M) % M), k = 1 + (int)(idx % M);
+    const long p = ((long)i * W + j) * W + k;
+    const int8_t s0 = side[p];
+    const bool irr = side[p - WW] != s0 || side[p + WW] != s0 || side[p - W] != s0 || side[p + W] != s0 ||
+                     side[p - 1] != s0 || side[p + 1] != s0;
+    iflag[idx] = irr ? 1 : 0;
+    if (irr && (i < 2 || j < 2 || k < 2 || i > N - 2 || j > N - 2 || k > N - 2)) atomicOr(err, 4);   // R32
+  }
+}
+
+__global__ void k_irr_compact3(int N, const int* __restrict__ iflag, const int* __restrict__ imap,
+                               const int8_t* __restrict__ side, int64_t* __restrict__ ilin, int* __restrict__ ijk,
+                               int8_t* __restrict__ iside, int* __restrict__ ncnt) {
+  const long W = N + 1, WW = W * W, M = N - 1, n = M * M * M;
+  for (long idx = (long)blockIdx.x * blockDim.x + threadIdx.x; idx < n; idx += (long)gridDim.x * blockDim.x) {
+    if (!iflag[idx]) continue;
+    const int r = imap[idx];
+    const int i = 1 + (int)(idx / (M * M)), j = 1 + (int)((idx / M) % M), k = 1 + (int)(idx % M);
+    const long p = ((long)i * W + j) * W + k;
+    const int8_t s0 = side[p];
+    ilin[r] = (int64_t)(i - 1) * N * N + (int64_t)j * N + k;
+    ijk[3 * r] = i;
+    ijk[3 * r + 1] = j;
+    ijk[3 * r + 2] = k;
+    iside[r] = s0;
+    ncnt[r] = (side[p - WW] != s0) + (side[p + WW] != s0) + (side[p - W] != s0) + (side[p + W] != s0) +
+              (side[p - 1] != s0) + (side[p + 1] != s0);
+  }
+}
+
+__global__ void k_irr_pairs3(int N, double lo, double h, int nirr, const int* __restrict__ ijk,
+                             const int* __restrict__ iptr, const int8_t* __restrict__ side, const int* __restrict__ qmap,
+                             const double* __restrict__ xi, int* __restrict__ pq, double* __restrict__ pd) {
+  const int r = blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= nirr) return;
+  const long W = N + 1, WWW = W * W * W;
+  const int i = ijk[3 * r], j = ijk[3 * r + 1], k = ijk[3 * r + 2];
+  auto lin = [&](int a, int b, int cc) { return ((long)a * W + b) * W + cc; };
+  const int8_t s0 = side[lin(i, j, k)];
+  const int nb[6][3] = {{i - 1, j, k}, {i + 1, j, k}, {i, j - 1, k}, {i, j + 1, k}, {i, j, k - 1}, {i, j, k + 1}};
+  int o = iptr[r];
+  for (int q = 0; q < 6; ++q) {
+    const int oi = nb[q][0], oj = nb[q][1], ok = nb[q][2];
+    if (side[lin(oi, oj, ok)] == s0) continue;
+    const int axis = q / 2;
+    const int li = min(i, oi), lj = min(j, oj), lk = min(k, ok);
+    const int e = qmap[axis * WWW + lin(li, lj, lk)];
+    const double xbar = axis == 0 ? node_x(lo, h, oi) : axis == 1 ? node_x(lo, h, oj) : node_x(lo, h, ok);
+    pq[o] = e;
+    pd[o] = __dsub_rn(xbar, xi[e]);
+    ++o;
+  }
+}
+
+// list capacities (3D): nq ≤ kQPerW2·W² intersections, n_irr ≤ 2·nq
+constexpr long kQPerW2 = 16;
+size_t lists_bytes3(long W) {
+  const long nq = kQPerW2 * W * W, ni = 2 * nq;
+  return nq * (4 * sizeof(int) + sizeof(double)) + ni * (sizeof(int64_t) + 3 * sizeof(int) + 3 * sizeof(int) + 1 +
+                                                         6 * (sizeof(int) + sizeof(double))) + 32 * 256;
+}
+
 }  // namespace
 
 size_t gpu_setup_scratch_bytes(int N) {
   const long W = N + 1, WW = W * W, n2 = (long)(N - 1) * (N - 1);
   return WW + 2 * (2 * WW) * sizeof(int) + 2 * n2 * sizeof(int) + lists_bytes(W) + cub_scan_bytes(2 * WW) + 16 * 256;
+}
+
+size_t gpu_setup_scratch_bytes3(int N) {
+  const long W = N + 1, WWW = W * W * W, n3 = (long)(N - 1) * (N - 1) * (N - 1);
+  return WWW + 2 * (3 * WWW) * sizeof(int) + 2 * n3 * sizeof(int) + lists_bytes3(W) + cub_scan_bytes(3 * WWW) +
+         16 * 256;
+}
+
+// fills S.side, the intersection lists (axis, i, j, k, ξ) and the irregular-node lists of the 3D setup
+void gpu_setup_phases3(Setup3& S, void* scratch, size_t bytes, cudaStream_t s) {
+  const int N = S.N, W = N + 1;
+  const long WWW = (long)W * W * W, n3 = (long)(N - 1) * (N - 1) * (N - 1);
+  if (bytes < gpu_setup_scratch_bytes3(N)) throw ScratchError("device setup scratch too small (kfbi_setup_scratch_size)");
+  const Comp& C = S.comp;
+  const DevComp3 c{C.kind, C.c[0], C.c[1], C.c[2], C.p[0], C.p[1], C.p[2]};
+  uint8_t* p = reinterpret_cast<uint8_t*>(scratch);
+  int8_t* side = carve<int8_t>(p, WWW);
+  int* flag = carve<int>(p, 3 * WWW);
+  int* qmap = carve<int>(p, 3 * WWW);
+  int* iflag = carve<int>(p, n3);
+  int* imap = carve<int>(p, n3);
+  int* err = carve<int>(p, 4);
+  const size_t tb = cub_scan_bytes(3 * WWW);
+  void* temp = carve<uint8_t>(p, tb);
+  const long qcap = kQPerW2 * W * W, icap = 2 * qcap;
+  int* qa = carve<int>(p, qcap);
+  int* qi = carve<int>(p, qcap);
+  int* qj = carve<int>(p, qcap);
+  int* qk = carve<int>(p, qcap);
+  double* qx = carve<double>(p, qcap);
+  int64_t* ilin = carve<int64_t>(p, icap);
+  int* ijk = carve<int>(p, 3 * icap);
+  int* cnt = carve<int>(p, icap + 1);
+  int* iptr = carve<int>(p, icap + 1);
+  int8_t* isd = carve<int8_t>(p, icap);
+  int* pqv = carve<int>(p, 6 * icap);
+  double* pdv = carve<double>(p, 6 * icap);
+  if ((size_t)(p - reinterpret_cast<uint8_t*>(scratch)) > bytes) throw ScratchError("device setup scratch layout overflow");
+  ck_(cudaMemsetAsync(err, 0, sizeof(int), s), "memset");
+  k_classify3<<<grid_for(WWW), 256, 0, s>>>(W, S.lo, S.h, c, side);
+  k_edge_flags3<<<grid_for(3 * WWW), 256, 0, s>>>(W, side, flag);
+  size_t tbb = tb;
+  ck_(cub::DeviceScan::ExclusiveSum(temp, tbb, flag, qmap, (int)(3 * WWW), s), "scan edges");
+  int h_last[2];
+  ck_(cudaMemcpyAsync(&h_last[0], qmap + 3 * WWW - 1, sizeof(int), cudaMemcpyDeviceToHost, s), "d2h");
+  ck_(cudaMemcpyAsync(&h_last[1], flag + 3 * WWW - 1, sizeof(int), cudaMemcpyDeviceToHost, s), "d2h");
+  ck_(cudaStreamSynchronize(s), "sync");
+  const int nq = h_last[0] + h_last[1];
+  if (nq > qcap) throw ScratchError("more intersections than the device setup scratch holds (16 per grid plane line)");
+  k_edge_compact3<<<grid_for(3 * WWW), 256, 0, s>>>(W, flag, qmap, qa, qi, qj, qk);
+  if (nq > 0) k_bisect3<<<(nq + 127) / 128, 128, 0, s>>>(nq, S.lo, S.h, c, qa, qi, qj, qk, qx, err);
+  ck_(cudaGetLastError(), "edge kernels");
+  S.nq = nq;
+  S.q_axis.resize(nq); S.q_i.resize(nq); S.q_j.resize(nq); S.q_k.resize(nq); S.q_xi.resize(nq);
+  ck_(cudaMemcpyAsync(S.q_axis.data(), qa, nq * sizeof(int), cudaMemcpyDeviceToHost, s), "d2h");
+  ck_(cudaMemcpyAsync(S.q_i.data(), qi, nq * sizeof(int), cudaMemcpyDeviceToHost, s), "d2h");
+  ck_(cudaMemcpyAsync(S.q_j.data(), qj, nq * sizeof(int), cudaMemcpyDeviceToHost, s), "d2h");
+  ck_(cudaMemcpyAsync(S.q_k.data(), qk, nq * sizeof(int), cudaMemcpyDeviceToHost, s), "d2h");
+  ck_(cudaMemcpyAsync(S.q_xi.data(), qx, nq * sizeof(double), cudaMemcpyDeviceToHost, s), "d2h");
+  int h_err = 0;
+  ck_(cudaMemcpyAsync(&h_err, err, sizeof(int), cudaMemcpyDeviceToHost, s), "d2h");
+  S.side.resize(WWW);
+  ck_(cudaMemcpyAsync(S.side.data(), side, WWW, cudaMemcpyDeviceToHost, s), "d2h side");
+  ck_(cudaStreamSynchronize(s), "sync");
+  if (h_err & 2) throw GeomError("grid edge crossed more than once (R31)");
+  k_irr_flags3<<<grid_for(n3), 256, 0, s>>>(N, side, iflag, err);
+  size_t tb2 = tb;
+  ck_(cub::DeviceScan::ExclusiveSum(temp, tb2, iflag, imap, (int)n3, s), "scan irregular");
+  ck_(cudaMemcpyAsync(&h_last[0], imap + n3 - 1, sizeof(int), cudaMemcpyDeviceToHost, s), "d2h");
+  ck_(cudaMemcpyAsync(&h_last[1], iflag + n3 - 1, sizeof(int), cudaMemcpyDeviceToHost, s), "d2h");
+  ck_(cudaMemcpyAsync(&h_err, err, sizeof(int), cudaMemcpyDeviceToHost, s), "d2h");
+  ck_(cudaStreamSynchronize(s), "sync");
+  if (h_err & 4) throw GeomError("Γ too close to the box boundary (R32)");
+  const int nirr = h_last[0] + h_last[1];
+  if (nirr > icap) throw ScratchError("internal: more irregular nodes than 2·nq");
+  k_irr_compact3<<<grid_for(n3), 256, 0, s>>>(N, iflag, imap, side, ilin, ijk, isd, cnt);
+  ck_(cudaMemsetAsync(cnt + nirr, 0, sizeof(int), s), "memset");
+  size_t tb3 = tb;
+  ck_(cub::DeviceScan::ExclusiveSum(temp, tb3, cnt, iptr, nirr + 1, s), "scan pairs");
+  if (nirr > 0) k_irr_pairs3<<<(nirr + 127) / 128, 128, 0, s>>>(N, S.lo, S.h, nirr, ijk, iptr, side, qmap, qx, pqv, pdv);
+  ck_(cudaGetLastError(), "irregular-node kernels");
+  S.nirr = nirr;
+  S.irr_lin.resize(nirr); S.irr_ijk.resize(3 * (size_t)nirr); S.irr_side.resize(nirr); S.irr_ptr.resize(nirr + 1);
+  ck_(cudaMemcpyAsync(S.irr_lin.data(), ilin, nirr * sizeof(int64_t), cudaMemcpyDeviceToHost, s), "d2h");
+  ck_(cudaMemcpyAsync(S.irr_ijk.data(), ijk, 3 * (size_t)nirr * sizeof(int), cudaMemcpyDeviceToHost, s), "d2h");
+  ck_(cudaMemcpyAsync(S.irr_side.data(), isd, nirr, cudaMemcpyDeviceToHost, s), "d2h");
+  ck_(cudaMemcpyAsync(S.irr_ptr.data(), iptr, (nirr + 1) * sizeof(int), cudaMemcpyDeviceToHost, s), "d2h");
+  ck_(cudaStreamSynchronize(s), "sync");
+  const int npair = S.irr_ptr[nirr];
+  S.pair_q.resize(npair);
+  S.pair_d.resize(npair);
+  ck_(cudaMemcpyAsync(S.pair_q.data(), pqv, npair * sizeof(int), cudaMemcpyDeviceToHost, s), "d2h");
+  ck_(cudaMemcpyAsync(S.pair_d.data(), pdv, npair * sizeof(double), cudaMemcpyDeviceToHost, s), "d2h");
+  ck_(cudaStreamSynchronize(s), "sync");
 }
 
 // fills S.side, the intersection base lists (axis, i, j, ξ, owner) and the irregular-node lists

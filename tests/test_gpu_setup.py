@@ -82,7 +82,7 @@ def test_device_setup_errors():
     with pytest.raises(KfbiError) as e:
         KFBI(prob)
     assert e.value.code == K.EGEOM
-    # scratch too small → ENOMEM; 3D → EUNSUPPORTED
+    # scratch too small → ENOMEM; 3D sizes: powers of two in [32, 512], ≈ 5 GB of scratch at 512³
     import ctypes as C
     lib = K.load()
     g = K.Grid(2, (C.c_double * 3)(-1.2, -1.2, 0), (C.c_double * 3)(1.2, 1.2, 0), (C.c_int32 * 3)(256, 256, 0))
@@ -98,7 +98,9 @@ def test_device_setup_errors():
                                C.c_void_p(small.data_ptr()), need.value // 4, C.byref(ctx))
     assert st == K.ENOMEM and not ctx.value
     g3 = K.Grid(3, (C.c_double * 3)(-1.2, -1.2, -1.2), (C.c_double * 3)(1.2, 1.2, 1.2), (C.c_int32 * 3)(64, 64, 64))
-    assert lib.kfbi_setup_scratch_size(C.byref(g3), C.byref(need)) == K.EUNSUPPORTED
+    assert lib.kfbi_setup_scratch_size(C.byref(g3), C.byref(need)) == K.OK and need.value > 0
+    g3b = K.Grid(3, (C.c_double * 3)(-1.2, -1.2, -1.2), (C.c_double * 3)(1.2, 1.2, 1.2), (C.c_int32 * 3)(1024, 1024, 1024))
+    assert lib.kfbi_setup_scratch_size(C.byref(g3b), C.byref(need)) == K.EINVAL
 
 
 @pytest.mark.parametrize("make,n", [(W.C1, 64), (W.C2, 1024), (W.C3, 1024)])
@@ -118,3 +120,38 @@ def test_device_setup_matches_oracle(make, n):
     px = np.where(st.q_axis == 0, st.q_xi, st.x[st.q_i])
     py = np.where(st.q_axis == 1, st.q_xi, st.x[st.q_j])
     np.testing.assert_allclose(k.points("isect"), np.stack([px, py], -1), atol=1e-13 * st.h)
+
+
+@pytest.mark.parametrize("make,n", [(W.C4, 32), (W.C4, 128), (W.C5, 64), (W.C5, 512)])
+def test_device_setup3d_lists_match_host(make, n):
+    """3D (NEXT-3): classification, the (axis, i, j, k) sign-change edges with their bisected ξ and the
+    (i, j, k) irregular nodes with their ≤ 6 incident intersections on the device — bit-identical to the
+    host setup (ellipsoid and torus levels use only +, −, ×, ÷, √ on both sides); the host setup is pinned
+    to the oracle's lists by tests/test_abi.py::test_host_setup3d_matches_oracle."""
+    prob = make(n)
+    host, dev, th, td = _pair(prob)
+    print(f"{prob.name} N={n}: host setup {th:.3f} s, device-phase setup {td:.3f} s")
+    assert (host.M, host.nq, host.nirr) == (dev.M, dev.nq, dev.nirr)
+    assert np.array_equal(host.node_mask(), dev.node_mask())
+    for which in (0, 1, 2):                      # irregular nodes, intersections, stencil nodes
+        assert np.array_equal(host.setup_dump(which), dev.setup_dump(which)), which
+    assert np.array_equal(host.points("ctrl"), dev.points("ctrl"))
+    assert np.array_equal(host.points("normal"), dev.points("normal"))
+    phi = W.random_density(host.M, 3)
+    assert np.array_equal(host.apply(phi).cpu().numpy(), dev.apply(phi).cpu().numpy())
+
+
+@pytest.mark.parametrize("make,n", [(W.C4, 32), (W.C5, 64)])
+def test_device_setup3d_matches_oracle(make, n):
+    """The 3D device phases against the oracle's 3D Procedure 1 (oracle/grid3d.py)."""
+    from oracle import grid3d
+    from paper_2404_15249_b200 import KFBI
+    prob = make(n)
+    k = KFBI(prob, device_setup=True)
+    st = grid3d.build(prob)
+    assert k.M == st.M and k.nq == st.M
+    assert np.array_equal(k.setup_dump(0), np.argwhere(st.irregular))
+    assert np.array_equal(k.setup_dump(1), np.stack([st.q_axis, st.q_i, st.q_j, st.q_k], -1))
+    assert np.array_equal(k.setup_dump(2), grid3d.stencil(st))
+    assert np.array_equal(k.node_mask().astype(bool), st.side)
+    np.testing.assert_allclose(k.points("ctrl"), st.q_pos, atol=1e-13 * st.h)

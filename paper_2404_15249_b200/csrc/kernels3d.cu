@@ -382,7 +382,12 @@ __global__ void __launch_bounds__(256, 2) k_fwd3s(DevTables3 T, const double* __
     }
   }
   const int NL = N - H;   // light rows (≤ kHeavyRow entries, incl. the empty ones): one thread each
-  for (int it = threadIdx.x; it < NL * NG; it += NTHR) {
+  // rows in descending entry count, dealt in snake order over the threads (thread t takes the t-th and
+  // the (2·NTHR − 1 − t)-th heaviest, …): the barrier below waits for the slowest thread
+  for (int it0 = threadIdx.x; it0 < NL * NG; it0 += NTHR) {
+    const int rnd = it0 / NTHR, pos = it0 - rnd * NTHR;
+    const int rem = min(NTHR, NL * NG - rnd * NTHR);   // items in this round
+    const int it = (rnd & 1) ? rnd * NTHR + (rem - 1 - pos) : it0;
     const int cg = it / NL, a = perm[H + it % NL];
     double g[CPT];
 #pragma unroll

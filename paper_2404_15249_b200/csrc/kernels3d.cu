@@ -589,6 +589,9 @@ __global__ void __launch_bounds__(256) k_sweep3(DevTables3 T, double* spec, doub
 
 __global__ void k_reduced3(DevTables3 T, const double* __restrict__ zB, const double* __restrict__ zA,
                            double* __restrict__ hsep) {
+  // thread per mode: the P − 1 ≤ 31 right-hand sides loaded in one batch, the forward values kept in
+  // registers (no re-read of hsep), pivots recomputed for the backward pass
+  constexpr int PM = 31;
   const int N = T.N, P = T.P;
   const size_t K = (size_t)N * N;
   const size_t m = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -599,29 +602,35 @@ __global__ void k_reduced3(DevTables3 T, const double* __restrict__ zB, const do
     return;
   }
   const double a = T.red_a[m], b = T.red_b[m];
-  double c = b, y = 0.0, ci = 0.0;
-  for (int g = 0; g < P - 1; ++g) {
-    const double r = zA[(size_t)g * K + m] - zB[(size_t)(g + 1) * K + m];
-    if (g) c = b - a * a * ci;
-    y = g ? r - a * y * ci : r;
+  double y[PM];
+#pragma unroll
+  for (int g = 0; g < PM; ++g)
+    if (g < P - 1) y[g] = zA[(size_t)g * K + m] - zB[(size_t)(g + 1) * K + m];
+  double c = b, ci = 0.0;
+#pragma unroll
+  for (int g = 0; g < PM; ++g) {
+    if (g >= P - 1) break;
+    if (g) {
+      c = b - a * a * ci;
+      y[g] = y[g] - a * y[g - 1] * ci;
+    }
     ci = 1.0 / c;
-    hsep[(size_t)g * K + m] = y;
   }
-  // backward: h_g = (y_g − a h_{g+1}) / c_g — recompute the pivots forward into registers
-  double hn = y * ci;
-  hsep[(size_t)(P - 2) * K + m] = hn;
-  if (P > 2) {
-    // pivots are needed in reverse: regenerate them (P − 1 ≤ 32 entries) in a local array
-    double cinv[64];
-    double cc = b;
-    for (int g = 0; g < P - 1; ++g) {
-      if (g) cc = b - a * a * cinv[g - 1];
-      cinv[g] = 1.0 / cc;
-    }
-    for (int g = P - 3; g >= 0; --g) {
-      hn = (hsep[(size_t)g * K + m] - a * hn) * cinv[g];
-      hsep[(size_t)g * K + m] = hn;
-    }
+  // backward: h_g = (y_g − a h_{g+1}) / c_g with the pivots regenerated from the top
+  double cinv[PM];
+  double cc = b;
+#pragma unroll
+  for (int g = 0; g < PM; ++g) {
+    if (g >= P - 1) break;
+    if (g) cc = b - a * a * cinv[g - 1];
+    cinv[g] = 1.0 / cc;
+  }
+  double hn = 0.0;
+#pragma unroll
+  for (int g = PM - 1; g >= 0; --g) {
+    if (g >= P - 1) continue;
+    hn = g == P - 2 ? y[g] * cinv[g] : (y[g] - a * hn) * cinv[g];
+    hsep[(size_t)g * K + m] = hn;
   }
 }
 

@@ -272,6 +272,7 @@ void layout3(kfbi_ctx* c, Arena& A) {
   T.irr_lin = A.table(S.irr_lin); T.irr_side = A.table(S.irr_side); T.irr_ptr = A.table(S.irr_ptr);
   T.pair_q = A.table(S.pair_q); T.pair_d = A.table(S.pair_d);
   T.lsq_ptr = A.table(S.lsq_ptr); T.lsq_nb = A.table(S.lsq_nb); T.lsq_G = A.table(S.lsq_G);
+  T.lsq_t = A.table(S.lsq_t);
   T.st_c = A.table(S.st_c); T.st_code = A.table(S.st_code); T.st_w = A.table(S.st_w);
   T.st_wn = A.table(S.st_wn); T.neumann = S.neumann ? 1 : 0;
   T.sin_tab = A.table(S.sin_tab); T.dk = A.table(S.dk); T.zr = A.table(S.zr); T.red_a = A.table(S.red_a);

@@ -78,30 +78,38 @@ __device__ __forceinline__ void load_jump3(const DevTables3& T, int q, const dou
               T.q_kab + 3 * q);
 }
 
-// A1 (3D): tangent-plane LSQ fit (reading R12) with the precomputed scaled normal-matrix inverse.
+// A1 (3D): tangent-plane LSQ fit (reading R12) with the precomputed scaled normal-matrix inverse and the
+// neighbours' tangent coordinates from setup (streamed; only φ is gathered).  Eight lanes per control
+// point stride over its ~30 neighbours; the five moments are summed by a fixed xor tree.
+constexpr int kLsqLanes = 8;
 __global__ void k_lsq3(DevTables3 T, const double* __restrict__ phi, double* __restrict__ dphi) {
-  // thread t → the t-th control point of the slab's three per-axis ranges
-  int e = blockIdx.x * blockDim.x + threadIdx.x;
+  // point p → the p-th control point of the slab's three per-axis ranges
+  const int gt = blockIdx.x * blockDim.x + threadIdx.x;
+  int e = gt / kLsqLanes;
+  const int sub = gt % kLsqLanes;
   const int n0 = T.q_hi[0] - T.q_lo[0], n1 = T.q_hi[1] - T.q_lo[1], n2 = T.q_hi[2] - T.q_lo[2];
-  if (e >= n0 + n1 + n2) return;
-  e = e < n0 ? T.q_lo[0] + e : (e < n0 + n1 ? T.q_lo[1] + e - n0 : T.q_lo[2] + e - n0 - n1);
-  const double ih = 1.0 / T.h;
-  const double x0 = T.q_pos[3 * e], y0 = T.q_pos[3 * e + 1], z0 = T.q_pos[3 * e + 2];
-  const double* e1 = T.q_e1 + 3 * e;
-  const double* e2 = T.q_e2 + 3 * e;
-  const double f0 = phi[e];
+  const bool valid = e < n0 + n1 + n2;
+  e = !valid ? 0 : (e < n0 ? T.q_lo[0] + e : (e < n0 + n1 ? T.q_lo[1] + e - n0 : T.q_lo[2] + e - n0 - n1));
   double b[5] = {0, 0, 0, 0, 0};
-  for (int u = T.lsq_ptr[e]; u < T.lsq_ptr[e + 1]; ++u) {
-    const int q = T.lsq_nb[u];
-    const double dx = (T.q_pos[3 * q] - x0) * ih, dy = (T.q_pos[3 * q + 1] - y0) * ih, dz = (T.q_pos[3 * q + 2] - z0) * ih;
-    const double t1 = e1[0] * dx + e1[1] * dy + e1[2] * dz, t2 = e2[0] * dx + e2[1] * dy + e2[2] * dz;
-    const double df = phi[q] - f0;
-    b[0] = fma(t1, df, b[0]);
-    b[1] = fma(t2, df, b[1]);
-    b[2] = fma(0.5 * t1 * t1, df, b[2]);
-    b[3] = fma(t1 * t2, df, b[3]);
-    b[4] = fma(0.5 * t2 * t2, df, b[4]);
+  if (valid) {
+    const double f0 = phi[e];
+    const double2* __restrict__ tt = reinterpret_cast<const double2*>(T.lsq_t);
+    for (int u = T.lsq_ptr[e] + sub; u < T.lsq_ptr[e + 1]; u += kLsqLanes) {
+      const double2 t = tt[u];
+      const double df = phi[T.lsq_nb[u]] - f0;
+      b[0] = fma(t.x, df, b[0]);
+      b[1] = fma(t.y, df, b[1]);
+      b[2] = fma(0.5 * t.x * t.x, df, b[2]);
+      b[3] = fma(t.x * t.y, df, b[3]);
+      b[4] = fma(0.5 * t.y * t.y, df, b[4]);
+    }
   }
+#pragma unroll
+  for (int o = kLsqLanes / 2; o > 0; o >>= 1)
+#pragma unroll
+    for (int r = 0; r < 5; ++r) b[r] += __shfl_xor_sync(0xffffffffu, b[r], o);
+  if (!valid || sub) return;
+  const double ih = 1.0 / T.h;
   const double* G = T.lsq_G + 15 * (size_t)e;
   // symmetric 5×5 from its upper triangle
   const double g[5][5] = {{G[0], G[1], G[2], G[3], G[4]},
@@ -789,7 +797,7 @@ void launch_lsq3(const DevTables3& T, const double* phi, double* dphi, cudaStrea
   const int n = T.q_hi[0] - T.q_lo[0] + T.q_hi[1] - T.q_lo[1] + T.q_hi[2] - T.q_lo[2];
   if (n <= 0) return;
   ++g_launches;
-  k_lsq3<<<cdiv3(n, 128), 128, 0, s>>>(T, phi, dphi);
+  k_lsq3<<<cdiv3((long)n * kLsqLanes, 256), 256, 0, s>>>(T, phi, dphi);
 }
 void launch_base3(const DevTables3& T, const double* fgrid, double* work, cudaStream_t s) {
   ++g_launches;

@@ -163,6 +163,7 @@ struct Setup3 {
   std::vector<double> pair_d;
   std::vector<int32_t> lsq_ptr, lsq_nb;   // LSQ neighbours (CSR)
   std::vector<double> lsq_G;              // 15 per point: (ÂᵀÂ)⁻¹ upper triangle, Â scaled by 1/h
+  std::vector<double> lsq_t;              // 2 per neighbour: tangent coordinates (t1, t2)/h of the fit
   std::vector<int32_t> st_c, st_code;     // stencil centre (3) and sign/exterior code
   std::vector<double> st_w;               // 10 per point: row 0 of the inverse local system
   std::vector<double> st_wn;              // 10 per point: normal-derivative row (Neumann, R38)
@@ -197,6 +198,7 @@ struct DevTables3 {
   const int32_t *irr_ptr, *pair_q;
   const double* pair_d;
   const int32_t *lsq_ptr, *lsq_nb;
+  const double* lsq_t;
   const double* lsq_G;
   const int32_t *st_c, *st_code;
   const double *st_w, *st_wn;

@@ -270,9 +270,11 @@ void build_setup3(Setup3& S, const kfbi_grid* g, const kfbi_boundary* b, const k
     S.lsq_ptr.push_back((int)S.lsq_nb.size());
   }
   S.lsq_G.assign(15 * (size_t)nq, 0.0);
+  S.lsq_t.assign(2 * S.lsq_nb.size(), 0.0);
 #pragma omp parallel for schedule(dynamic, 256)
   for (int e = 0; e < nq; ++e) {
     const auto& L = nbl[e];
+    int slot = S.lsq_ptr[e];
     if (L.size() < 8) { bad = true; continue; }
     // Â columns (t1/h, t2/h, ½(t1/h)², (t1/h)(t2/h), ½(t2/h)²); G = ÂᵀÂ
     double G[25] = {0};
@@ -281,6 +283,9 @@ void build_setup3(Setup3& S, const kfbi_grid* g, const kfbi_boundary* b, const k
       for (int r = 0; r < 3; ++r) d[r] = (S.q_pos[3 * q + r] - S.q_pos[3 * e + r]) / h;
       double t1 = 0, t2 = 0;
       for (int r = 0; r < 3; ++r) { t1 += S.q_e1[3 * e + r] * d[r]; t2 += S.q_e2[3 * e + r] * d[r]; }
+      S.lsq_t[2 * (size_t)slot] = t1;   // the fit's tangent coordinates (/h), streamed by k_lsq3
+      S.lsq_t[2 * (size_t)slot + 1] = t2;
+      ++slot;
       const double a[5] = {t1, t2, 0.5 * t1 * t1, t1 * t2, 0.5 * t2 * t2};
       for (int r = 0; r < 5; ++r)
         for (int c2 = 0; c2 < 5; ++c2) G[r * 5 + c2] += a[r] * a[c2];

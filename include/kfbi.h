@@ -206,6 +206,11 @@ kfbi_status kfbi_points(const kfbi_ctx* ctx, int32_t which, double* host_xyz);
 /* Ω mask of the full node grid ((N+1)^d int8, 1 = Ω) into host memory. */
 kfbi_status kfbi_node_mask(const kfbi_ctx* ctx, int8_t* host_mask);
 
+/* Ω mask of this context's node slab (kfbi_local_slab: the full grid unless one rank per process) into
+ * device memory d_mask (int8, local_shape elements, row-major), enqueued on `stream` (a device-to-device
+ * copy of the context's classification; needs the workspace). */
+kfbi_status kfbi_node_mask_device(kfbi_ctx* ctx, int8_t* d_mask, void* stream);
+
 /* Ω-compact grid transfers (serving path).  The solve uses f only on Ω nodes (zero extension,
  * P:530) and u_h is valid only there, so a caller may move just the Ω values across PCIe:
  * n_omega = number of Ω nodes of the full (N+1)^d node grid, in row-major node order (i, j[, k]) —

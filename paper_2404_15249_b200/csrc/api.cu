@@ -989,6 +989,18 @@ kfbi_status kfbi_node_mask(const kfbi_ctx* c, int8_t* mask) {
   return KFBI_OK;
 }
 
+kfbi_status kfbi_node_mask_device(kfbi_ctx* c, int8_t* d_mask, void* stream) {
+  if (!c || !d_mask) return fail(c, KFBI_EINVAL, "null pointer");
+  KFBI_TRY(c)
+  need_ws(c);
+  const size_t row = c->dim == 3 ? (size_t)(c->S3.N + 1) * (c->S3.N + 1) : (size_t)c->S.N + 1;
+  const size_t off = (size_t)c->loc_off[0] * row;
+  const size_t n = (size_t)c->loc_shape[0] * row;
+  ck(cudaMemcpyAsync(d_mask, c->d_side + off, n, cudaMemcpyDeviceToDevice, pick(c, stream)), "mask copy");
+  KFBI_CATCH(c)
+  return KFBI_OK;
+}
+
 kfbi_status kfbi_omega_count(const kfbi_ctx* c, int64_t* n_omega) {
   if (!c || !n_omega || c->om_ptr.empty()) return KFBI_EINVAL;
   *n_omega = c->om_ptr.back();

@@ -24,7 +24,8 @@ EXPORTS = ["kfbi_version", "kfbi_last_error", "kfbi_last_setup_error", "kfbi_get
            "kfbi_apply", "kfbi_solve", "kfbi_apply_model", "kfbi_destroy", "kfbi_test_fast_solve",
            "kfbi_test_interface_solve", "kfbi_test_setup_dump", "kfbi_profile_apply", "kfbi_launch_count",
            "kfbi_slab", "kfbi_gray_scott_step", "kfbi_setup_scratch_size", "kfbi_setup_device",
-           "kfbi_omega_count", "kfbi_scatter_omega", "kfbi_gather_omega", "kfbi_local_slab"]
+           "kfbi_omega_count", "kfbi_scatter_omega", "kfbi_gather_omega", "kfbi_local_slab",
+           "kfbi_node_mask_device"]
 
 
 class KfbiError(RuntimeError):
@@ -97,6 +98,7 @@ def load(path: str = LIB_PATH):
     lib.kfbi_local_slab.argtypes = [vp, i64p, i64p]
     lib.kfbi_points.argtypes = [vp, i32, dp]
     lib.kfbi_node_mask.argtypes = [vp, C.POINTER(C.c_int8)]
+    lib.kfbi_node_mask_device.argtypes = [vp, vp, vp]
     lib.kfbi_apply.argtypes = [vp, vp, vp, vp]
     lib.kfbi_solve.argtypes = [vp, vp, vp, vp, vp, vp, vp, vp, C.POINTER(SolveOpts), C.POINTER(SolveStats), vp]
     lib.kfbi_apply_model.argtypes = [vp, dp, dp, dp]
@@ -313,6 +315,15 @@ class KFBI:
             self._check(self.lib.kfbi_gather_omega(self.ctx, _ptr(grid), _ptr(compact), self._stream(stream)))
         self._keep(stream, grid, compact)
         return compact
+
+    def node_mask_device(self, stream=None):
+        """Ω mask of this context's node slab as a device int8 tensor (kfbi_node_mask_device)."""
+        t = self.torch
+        out = t.empty(self.local_nodes, dtype=t.int8, device=self.device)
+        with t.cuda.device(self.device):
+            self._check(self.lib.kfbi_node_mask_device(self.ctx, _ptr(out), self._stream(stream)))
+        self._keep(stream, out)
+        return out.view(self.local_shape)
 
     def node_mask(self):
         out = np.zeros(self.n_nodes, dtype=np.int8)

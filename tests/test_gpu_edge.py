@@ -121,3 +121,9 @@ def test_context_on_second_device():
         phi = W.random_density(k0.M, 5)
         assert torch.equal(k1.apply(phi).cpu(), k0.apply(phi).cpu())
         assert torch.cuda.current_device() == 0
+
+
+@pytest.mark.parametrize("prob,world", [(W.C1(64), 1), (W.C4(32), 1), (W.C3(1024), 2)], ids=["C1", "C4", "C3x2-emul"])
+def test_node_mask_device_matches_host(prob, world):
+    k = KFBI(prob, world=world, rank=-1) if world > 1 else gpu(prob)
+    assert np.array_equal(k.node_mask_device().cpu().numpy(), k.node_mask()[k.local_slice()])

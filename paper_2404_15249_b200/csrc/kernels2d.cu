@@ -196,13 +196,13 @@ __global__ void __launch_bounds__(kSweepThreads, 2) k_sweep(DevTables T, const d
   for (int rnd = 0; rnd * G < T.P; ++rnd) {
   const int kk = rnd * G + ((rnd & 1) ? G - 1 - grp : grp);
   if (kk >= T.P) continue;
-  const int g = T.blk_order[kk];
+  const int g = T.blk_meta[3 * kk];
   if (g < T.g_lo || g >= T.g_hi) continue;   // CTA-uniform
     const int c0 = BL * g + 1;
     KFBI_CHECK(c0 - 1 >= T.col_lo - 1 && c0 - 1 + LB - 1 <= T.col_hi - 1, c0, T.col_hi);   // spectral rows of the slab
-    const int e0 = T.col_ptr[c0];
+    const int e0 = T.blk_meta[3 * kk + 1];
     const int ncol = g < T.P - 1 ? BL : LB;   // block columns + separator column
-    const int e1 = cval ? T.col_ptr[c0 + ncol] : e0;
+    const int e1 = cval ? T.blk_meta[3 * kk + 2] : e0;
     // the block's entries are staged kEntCap at a time (a block where Γ runs along x holds up to
     // ~1,700 on the 8192² star: staging them all would leave one CTA per SM); later passes add into R
     for (int cb = e0, pass = 0; pass == 0 || cb < e1; cb += kEntCap, ++pass) {
@@ -216,7 +216,8 @@ __global__ void __launch_bounds__(kSweepThreads, 2) k_sweep(DevTables T, const d
       const double c = cval[e];
       // odd j: sin(πj/2) = ±1; even j: cos(πj/2) = ±1
       const bool neg = (j >> 1) & 1;
-      ent[e - cb] = make_double4(c, neg ? -c : c, sin_lookup(T.sin_tab, (rd + half) & m2, N), sin_lookup(T.sin_tab, rd, N));
+      const double2 dr = E(rd);   // e^{iπ·kRotStride·j/N} from the shared tables (no global lookups)
+      ent[e - cb] = make_double4(c, neg ? -c : c, dr.x, dr.y);
       ent_j[e - cb] = j;
     }
     if (threadIdx.x < ncol) {

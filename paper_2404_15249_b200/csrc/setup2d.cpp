@@ -644,6 +644,14 @@ void build_setup(Setup& S, const kfbi_grid* g, const kfbi_boundary* b, const kfb
   S.blk_order.resize(P);
   for (int gg = 0; gg < P; ++gg) S.blk_order[gg] = gg;
   std::stable_sort(S.blk_order.begin(), S.blk_order.end(), [&](int32_t x, int32_t y) { return bcnt[x] > bcnt[y]; });
+  // per position of that order: (block, first entry, end entry) — one load instead of blk_order → col_ptr
+  S.blk_meta.resize(3 * (size_t)P);
+  for (int kk = 0; kk < P; ++kk) {
+    const int gg = S.blk_order[kk], c0 = BL * gg + 1, ncol = gg < P - 1 ? BL : LB;
+    S.blk_meta[3 * kk] = gg;
+    S.blk_meta[3 * kk + 1] = S.col_ptr[c0];
+    S.blk_meta[3 * kk + 2] = S.col_ptr[c0 + ncol];
+  }
   S.holes.clear();
   if (S.kappa == 0.0)
     for (int c = 0; c < nc; ++c)

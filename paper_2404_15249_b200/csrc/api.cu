@@ -176,7 +176,7 @@ void layout(kfbi_ctx* c, Arena& A) {
   T.z_t1 = A.table(S.z_t1); T.z_t2 = A.table(S.z_t2); T.z_p1 = A.table(S.z_p1); T.z_p2 = A.table(S.z_p2);
   T.sn_j = A.table(S.sn_j); T.ocol = A.table(S.ocol); T.ocol_ptr = A.table(S.ocol_ptr);
   T.ocol_ncls = A.table(S.ocol_ncls); T.ocol_order = A.table(S.ocol_order); T.blk_order = A.table(S.blk_order);
-  T.blk_meta = A.table(S.blk_meta);
+  T.blk_meta = A.table(S.blk_meta); T.ocol_meta = A.table(S.ocol_meta);
   T.st_node = A.table(S.st_node); T.st_ext = A.table(S.st_ext);
   T.st_w = A.table(S.st_w); T.st_dx = A.table(S.st_dx); T.st_dy = A.table(S.st_dy);
   T.st_wn = A.table(S.st_wn); T.neumann = S.neumann ? 1 : 0;

@@ -577,72 +577,46 @@ __device__ __forceinline__ double fixup_staged(const DevTables& T, const double*
 constexpr int kInvThreads = 256;
 static_assert(kMaxColRows <= kInvThreads, "k_inv_sparse stages a column's rows one per thread");
 
-template <int QPT, bool ASYNC>
+template <int QPT>
 __global__ void __launch_bounds__(kInvThreads, 2) k_inv_sparse(DevTables T, const double* __restrict__ spec,
-                                                               const double* __restrict__ hsep, double* __restrict__ vsten,
-                                                               int abl) {
+                                                               const double* __restrict__ hsep, double* __restrict__ vsten) {
   extern __shared__ double smx[];
   __shared__ int s_rows[kMaxColRows];
   __shared__ double2 s_step[kMaxColRows];   // (cos, sin)(πjB/N) of each row: the recurrence step
   __shared__ double s_xq[3];                // modes N/4, N/2, 3N/4 of the column (thread 0's quad slot)
   const int N = T.N, half = N >> 1, quarter = N >> 2, m2 = 2 * N - 1, B = kInvThreads, P = T.P;
-  // ASYNC: e^{iπr/N} from two small tables (th, tl: 5 KB) and the next item's own spectral row
-  // streamed into `xs` by cp.async while this one is evaluated; else the 64 KB sine table
   double* tab = smx;   // sin(πr/N), r ∈ [0, N), at r + r/16
-  double2* th = reinterpret_cast<double2*>(smx);   // e^{iπ 64k/N}, k < 2N/64
-  double2* tl = th + 2 * N / 64;                   // e^{iπ l/N}, l < 64
-  double* xs = reinterpret_cast<double*>(tl + 64); // [N]: the own row in flight (ASYNC)
-  double* red = ASYNC ? xs + N : smx + N + N / 16 + 1;   // [warp][2·row]: per-warp partials of the rows
-  if (ASYNC) build_eipi(T.sin_tab, N, th, tl);
-  else
-    for (int r = threadIdx.x; r < N; r += B) tab[r + (r >> 4)] = sin_lookup(T.sin_tab, r, N);
+  double* red = smx + N + N / 16 + 1;   // [warp][2·row]: per-warp partial sums of the column's rows
+  for (int r = threadIdx.x; r < N; r += B) tab[r + (r >> 4)] = sin_lookup(T.sin_tab, r, N);
   auto sinr = [&](int r) {   // sin(πr/N), r ∈ [0, 2N)
-    if (ASYNC) return eipi(th, tl, r).y;
     const int idx = r & (N - 1);
     const double v = tab[idx + (idx >> 4)];
     return (r & N) ? -v : v;
   };
-  auto cosr = [&](int r) {   // cos(πr/N)
-    if (ASYNC) return eipi(th, tl, r).x;
-    return sinr((r + half) & m2);
-  };
-  auto own_row = [&](int ii) {
-    const int qq = ii / BL, r2 = ii - qq * BL;
-    return r2 == 0 ? hsep + (size_t)(qq - 1) * N : spec + (size_t)(ii - 1) * N;
-  };
-  auto prefetch_row = [&](int ii) {   // cp.async of this thread's quads of the row into xs
-    const double* src = own_row(ii);
-#pragma unroll
-    for (int s = 0; s < QPT; ++s) {
-      const int t = threadIdx.x + s * B;
-      if (t >= quarter) continue;
-      const unsigned dst = (unsigned)__cvta_generic_to_shared(xs + 4 * t);
-      asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(src + 4 * t));
-      asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst + 16), "l"(src + 4 * t + 2));
-    }
-    asm volatile("cp.async.commit_group;" ::: "memory");
-  };
-  int pf = -1;   // item whose own row is in xs (ASYNC)
   // persistent over the owned stencil columns: the sine table is staged once per CTA.  Items are
   // taken in descending row count (setup order `ocol_order`), dealt in snake order over the CTAs:
   // a few columns along which Γ runs hold up to ~200 rows against a mean of 12, and a plain
   // round-robin left the CTAs that drew them as the kernel's tail.
   const int G = gridDim.x, nit = T.nocol;
-  auto item = [&](int r) {   // item of round r for this CTA (−1: none)
+  // the next item's (column, row range, class counts) are loaded one round ahead from the per-position
+  // table ocol_meta (one load level), so that the column's row loads do not wait behind an index chain
+  struct Item { int b, i, u0, u1, ncl0, ncl1; };
+  auto item = [&](int r) {   // item of round r for this CTA (b = −1: none)
+    Item it{-1, 0, 0, 0, 0, 0};
     const int kk = r * G + ((r & 1) ? G - 1 - (int)blockIdx.x : (int)blockIdx.x);
-    return kk < nit ? T.ocol_order[kk] : -1;
+    if (kk >= nit) return it;
+    const int2* m = reinterpret_cast<const int2*>(T.ocol_meta + 6 * (size_t)kk);
+    const int2 m0 = m[0], m1 = m[1], m2v = m[2];
+    it.b = m0.x; it.i = m0.y; it.u0 = m1.x; it.u1 = m1.y; it.ncl0 = m2v.x; it.ncl1 = m2v.y;
+    if (it.b < T.o_lo || it.b >= T.o_hi) it.b = -1;
+    return it;
   };
-  // the next item's indices are loaded one round ahead, so that the column's row loads do not wait
-  // behind the dependent chain ocol_order → ocol / ocol_ptr
-  auto in_range = [&](int bb) { return bb >= T.o_lo && bb < T.o_hi; };
-  int nb = item(0), ni = 0, nu0 = 0, nu1 = 0;
-  if (in_range(nb)) { ni = T.ocol[nb]; nu0 = T.ocol_ptr[nb]; nu1 = T.ocol_ptr[nb + 1]; }
+  Item nx = item(0);
   for (int rnd = 0; rnd * G < nit; ++rnd) {
-  const int b = nb, i = ni, u0 = nu0, u1 = nu1;
-  nb = item(rnd + 1);
-  if (in_range(nb)) { ni = T.ocol[nb]; nu0 = T.ocol_ptr[nb]; nu1 = T.ocol_ptr[nb + 1]; }
-  if (!in_range(b)) continue;   // CTA-uniform
-  if (ASYNC && pf != b) prefetch_row(i);
+  const Item cur = nx;
+  nx = item(rnd + 1);
+  if (cur.b < 0) continue;   // CTA-uniform
+  const int i = cur.i, u0 = cur.u0, u1 = cur.u1;
   __syncthreads();
   // row indices: loaded now, stored to shared memory after the row loads (kMaxColRows ≤ B)
   const int srow = u0 + (int)threadIdx.x < u1 ? T.sn_j[u0 + threadIdx.x] : 0;
@@ -651,7 +625,7 @@ __global__ void __launch_bounds__(kInvThreads, 2) k_inv_sparse(DevTables T, cons
   const int q = i / BL, rr = i - q * BL;
   const bool sep = rr == 0;
   KFBI_CHECK(i >= T.col_lo && i <= T.col_hi && u1 - u0 <= T.mcr, i, u1 - u0);
-  const double* xrow = ASYNC ? xs : own_row(i);
+  const double* xrow = sep ? hsep + (size_t)(q - 1) * N : spec + (size_t)(i - 1) * N;
   const double* hl = (!sep && q > 0) ? hsep + (size_t)(q - 1) * N : nullptr;
   const double* hr = (!sep && q < P - 1) ? hsep + (size_t)q * N : nullptr;
   const double* zl = T.zr + (size_t)(sep ? 0 : LB - rr) * N;     // Z_L[p] = Z_R[LB−1−p], p = rr − 1
@@ -667,14 +641,9 @@ __global__ void __launch_bounds__(kInvThreads, 2) k_inv_sparse(DevTables T, cons
       Pv[s] = Qp[s] = Qm[s] = Rv[s] = 0.0;
       continue;
     }
-    if (ASYNC && s == 0) asm volatile("cp.async.wait_all;" ::: "memory");   // this thread's own copies
     const double2* xp = reinterpret_cast<const double2*>(xrow + 4 * t);
     const double2 a = xp[0], b2 = xp[1];
     Pv[s] = a.x; Qp[s] = a.y; Qm[s] = b2.x; Rv[s] = b2.y;
-  }
-  if (ASYNC) {   // the next item's own row streams in while this one is fixed up and evaluated
-    pf = in_range(nb) ? nb : -1;
-    if (pf >= 0) prefetch_row(ni);
   }
   auto fix = [&](const double* hrow, const double* zrow) {
 #pragma unroll
@@ -688,10 +657,8 @@ __global__ void __launch_bounds__(kInvThreads, 2) k_inv_sparse(DevTables T, cons
       Qm[s] = fma(-h1.x, z1.x, Qm[s]); Rv[s] = fma(-h1.y, z1.y, Rv[s]);
     }
   };
-  if (abl != 2) {
-    if (hl) fix(hl, zl);
-    if (hr) fix(hr, zrr);
-  }
+  if (hl) fix(hl, zl);
+  if (hr) fix(hr, zrr);
 #pragma unroll
   for (int s = 0; s < QPT; ++s) {
     const int t = threadIdx.x + s * B;
@@ -709,10 +676,10 @@ __global__ void __launch_bounds__(kInvThreads, 2) k_inv_sparse(DevTables T, cons
       Qm[s] = (a - bb) - (d - c);
     }
   }
-  if (!ASYNC) {   // warm L2 with the next column's spectral row while this one is evaluated
-    if (in_range(nb)) {
-      const int qn = ni / BL, rn = ni - qn * BL;
-      const double* nrow = rn == 0 ? hsep + (size_t)(qn - 1) * N : spec + (size_t)(ni - 1) * N;
+  {   // warm L2 with the next column's spectral row while this one is evaluated
+    if (nx.b >= 0) {
+      const int qn = nx.i / BL, rn = nx.i - qn * BL;
+      const double* nrow = rn == 0 ? hsep + (size_t)(qn - 1) * N : spec + (size_t)(nx.i - 1) * N;
       for (int o = threadIdx.x * 16; o < N; o += B * 16)
         asm volatile("prefetch.global.L2 [%0];" ::"l"(nrow + o));
     }
@@ -720,7 +687,7 @@ __global__ void __launch_bounds__(kInvThreads, 2) k_inv_sparse(DevTables T, cons
   if (u0 + (int)threadIdx.x < u1) {
     s_rows[threadIdx.x] = srow;
     const int rd = (srow * B) & m2;
-    s_step[threadIdx.x] = make_double2(cosr(rd), sinr(rd));
+    s_step[threadIdx.x] = make_double2(sinr((rd + half) & m2), sinr(rd));
   }
   if (threadIdx.x == 0) {
     s_xq[0] = xq1;
@@ -734,9 +701,9 @@ __global__ void __launch_bounds__(kInvThreads, 2) k_inv_sparse(DevTables T, cons
   // rows come sorted by class (odd, j ≡ 0, j ≡ 2 mod 4): groups of ≤ 4 rows of one class.  Sines along
   // the thread's quads t = tid + s·B by the three-term recurrence S_{s+1} = 2 cos(πjB/N) S_s − S_{s−1}
   // (one FMA per step; cosines likewise for odd rows).
-  const int ncl0 = T.ocol_ncls[3 * b], ncl1 = T.ocol_ncls[3 * b + 1];
+  const int ncl0 = cur.ncl0, ncl1 = cur.ncl1;
 #pragma unroll 1
-  for (int c0 = 0; c0 < (abl == 1 ? 0 : 3); ++c0) {
+  for (int c0 = 0; c0 < 3; ++c0) {
     const int cbeg = c0 == 0 ? 0 : (c0 == 1 ? ncl0 : ncl0 + ncl1);
     const int cend = c0 == 0 ? ncl0 : (c0 == 1 ? ncl0 + ncl1 : nrows);
 #pragma unroll 1
@@ -750,15 +717,7 @@ __global__ void __launch_bounds__(kInvThreads, 2) k_inv_sparse(DevTables T, cons
         js[k] = k < nr ? s_rows[u + k] : 0;
         const int r0 = (js[k] * (int)threadIdx.x) & m2;
         const double2 st = s_step[k < nr ? u + k : u];
-        double s0, c0v;
-        if (ASYNC) {
-          const double2 e = eipi(th, tl, r0);
-          s0 = e.y;
-          c0v = e.x;
-        } else {
-          s0 = sinr(r0);
-          c0v = sinr((r0 + half) & m2);
-        }
+        const double s0 = sinr(r0), c0v = sinr((r0 + half) & m2);
         const double sd = st.y, cd = st.x;
         S[k] = s0;
         C[k] = c0v;
@@ -822,238 +781,6 @@ __global__ void __launch_bounds__(kInvThreads, 2) k_inv_sparse(DevTables T, cons
     KFBI_CHECK(u0 + t < T.nsn && j >= 1 && j < N, u0 + t, j);
     vsten[u0 + t] = scale * ((j & 1) ? s1 + sig * s2 : s1);
   }
-  }
-}
-
-// ---- warp-specialised form of the same inverse (one CTA per SM, 8 producer + 8 consumer warps) ----
-// Producers (threads 256..511) load the next item's spectral row and its four fix-up rows
-// into registers while the consumers evaluate the current item, then publish the fixed-up quad
-// combinations (P, Q+D, Q−D, R per quad, see above) and the per-row step rotations e^{iπjB/N} in
-// shared memory.  Consumers (threads 0..255) copy the quads into registers, release the buffer and
-// evaluate the rows exactly as k_inv_sparse does.  Named barriers: FULL (producers arrive, consumers
-// wait), EMPTY (consumers arrive after their register copy, producers wait before overwriting), PROD
-// (producers only), CONS (consumers only).
-constexpr int kWsCons = 256, kWsProd = 256, kWsThreads = kWsCons + kWsProd;
-constexpr int kBarFull = 1, kBarEmpty = 2, kBarProd = 3, kBarCons = 4;
-__device__ __forceinline__ void bar_sync(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
-__device__ __forceinline__ void bar_arrive(int id, int n) { asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(n) : "memory"); }
-
-struct WsRow {      // per stencil row of the current item
-  double cd, sd;   // cos, sin(πjB/N): the recurrence step along a thread's quads (B = kWsCons)
-  double extra;    // modes N/4, N/2, 3N/4: xq1 sin(πj/4) + xq2 sin(πj/2) + xq3 sin(3πj/4)
-  int j, pad;
-};
-struct WsMeta {
-  int nrows, u0, ncl0, ncl1;
-  double xq1, xq2, xq3, pad;
-};
-
-template <int QPT>
-__global__ void __launch_bounds__(kWsThreads, 1) k_inv_ws(DevTables T, const double* __restrict__ spec,
-                                                         const double* __restrict__ hsep, double* __restrict__ vsten,
-                                                         int abl) {
-  extern __shared__ double smx[];
-  const int N = T.N, half = N >> 1, quarter = N >> 2, m2 = 2 * N - 1, P = T.P;
-  double* tab = smx;                                            // sin(πr/N), r ∈ [0, N), at r + r/16
-  double4* xq = reinterpret_cast<double4*>(smx + ((N + N / 16 + 1 + 3) & ~3));   // [quarter] quads
-  WsRow* rinfo = reinterpret_cast<WsRow*>(xq + quarter);         // [2][kMaxColRows]
-  WsMeta* meta = reinterpret_cast<WsMeta*>(rinfo + 2 * kMaxColRows);   // [2]
-  double* red = reinterpret_cast<double*>(meta + 2);             // [8 warps][2·mcr]
-  for (int r = threadIdx.x; r < N; r += kWsThreads) tab[r + (r >> 4)] = sin_lookup(T.sin_tab, r, N);
-  __syncthreads();
-  auto sinr = [&](int r) {   // sin(πr/N), r ∈ [0, 2N)
-    const int idx = r & (N - 1);
-    const double v = tab[idx + (idx >> 4)];
-    return (r & N) ? -v : v;
-  };
-  // this CTA's items: rounds r of a snake deal over the CTAs, in descending row count (ocol_order)
-  const int G = gridDim.x, nit = T.nocol;
-  auto item = [&](int r) {
-    const int kk = r * G + ((r & 1) ? G - 1 - (int)blockIdx.x : (int)blockIdx.x);
-    const int b = kk < nit ? T.ocol_order[kk] : -1;
-    return (b >= T.o_lo && b < T.o_hi) ? b : -1;
-  };
-  int nmine = 0;
-  for (int r = 0; r * G < nit; ++r) nmine += item(r) >= 0;
-  if (nmine == 0) return;   // CTA-uniform
-
-  if (threadIdx.x >= kWsCons) {
-    // ================================================================ producers
-    const int pt = threadIdx.x - kWsCons;
-    int n = 0;
-    for (int rnd = 0; rnd * G < nit; ++rnd) {
-      const int b = item(rnd);
-      if (b < 0) continue;
-      const int i = T.ocol[b], u0 = T.ocol_ptr[b], u1 = T.ocol_ptr[b + 1];
-      const int q = i / BL, rr = i - q * BL;
-      const bool sep = rr == 0;
-      const double* xrow = sep ? hsep + (size_t)(q - 1) * N : spec + (size_t)(i - 1) * N;
-      const double* hl = (!sep && q > 0) ? hsep + (size_t)(q - 1) * N : nullptr;
-      const double* hr = (!sep && q < P - 1) ? hsep + (size_t)q * N : nullptr;
-      const double* zl = T.zr + (size_t)(sep ? 0 : LB - rr) * N;   // Z_L[p] = Z_R[LB−1−p], p = rr − 1
-      const double* zrr = T.zr + (size_t)(sep ? 0 : rr - 1) * N;
-      double Pv[QPT], Qp[QPT], Qm[QPT], Rv[QPT];
-#pragma unroll
-      for (int s = 0; s < QPT; ++s) {
-        const int t = pt + s * kWsProd;
-        if (t >= quarter) { Pv[s] = Qp[s] = Qm[s] = Rv[s] = 0.0; continue; }
-        const double2* xp = reinterpret_cast<const double2*>(xrow + 4 * t);
-        const double2 a = xp[0], b2 = xp[1];
-        Pv[s] = a.x; Qp[s] = a.y; Qm[s] = b2.x; Rv[s] = b2.y;
-      }
-      auto fix = [&](const double* hrow, const double* zrow) {
-#pragma unroll
-        for (int s = 0; s < QPT; ++s) {
-          const int t = pt + s * kWsProd;
-          if (t >= quarter) continue;
-          const double2* hp = reinterpret_cast<const double2*>(hrow + 4 * t);
-          const double2* zp = reinterpret_cast<const double2*>(zrow + 4 * t);
-          const double2 h0 = hp[0], h1 = hp[1], z0 = __ldg(zp), z1 = __ldg(zp + 1);
-          Pv[s] = fma(-h0.x, z0.x, Pv[s]); Qp[s] = fma(-h0.y, z0.y, Qp[s]);
-          Qm[s] = fma(-h1.x, z1.x, Qm[s]); Rv[s] = fma(-h1.y, z1.y, Rv[s]);
-        }
-      };
-      if (abl != 2) {
-        if (hl) fix(hl, zl);
-        if (hr) fix(hr, zrr);
-      }
-      const int jrow = u0 + pt < u1 ? T.sn_j[u0 + pt] : 0;
-      const int bf = n & 1;
-      if (n > 0) bar_sync(kBarEmpty, kWsThreads);   // consumers hold item n − 1 in registers
-#pragma unroll
-      for (int s = 0; s < QPT; ++s) {
-        const int t = pt + s * kWsProd;
-        if (t >= quarter) continue;
-        if (t == 0) {   // positions 0..3 = modes 0, N/2, N/4, 3N/4
-          meta[bf].xq2 = Qp[s];
-          meta[bf].xq1 = Qm[s];
-          meta[bf].xq3 = Rv[s];
-          xq[0] = make_double4(0.0, 0.0, 0.0, 0.0);
-        } else {
-          const double a = Pv[s], bb = Qp[s], c = Qm[s], d = Rv[s];
-          xq[t] = make_double4(a + bb, (a - bb) + (d - c), (a - bb) - (d - c), c + d);
-        }
-      }
-      if (pt == 0) {
-        meta[bf].nrows = u1 - u0;
-        meta[bf].u0 = u0;
-        meta[bf].ncl0 = T.ocol_ncls[3 * b];
-        meta[bf].ncl1 = T.ocol_ncls[3 * b + 1];
-      }
-      bar_sync(kBarProd, kWsProd);   // xq1..3 visible to the row threads
-      if (u0 + pt < u1) {
-        const int j = jrow, rd = (j * kWsCons) & m2;
-        WsRow w;
-        w.j = j;
-        w.pad = 0;
-        w.sd = sin_lookup(T.sin_tab, rd, N);
-        w.cd = sin_lookup(T.sin_tab, (rd + half) & m2, N);
-        w.extra = meta[bf].xq1 * sin_lookup(T.sin_tab, (j * quarter) & m2, N) +
-                  meta[bf].xq2 * sin_lookup(T.sin_tab, (j * half) & m2, N) +
-                  meta[bf].xq3 * sin_lookup(T.sin_tab, (j * (half + quarter)) & m2, N);
-        rinfo[bf * kMaxColRows + pt] = w;
-      }
-      __threadfence_block();
-      bar_arrive(kBarFull, kWsThreads);
-      ++n;
-    }
-    return;
-  }
-  // ================================================================== consumers
-  const double scale = 2.0 / N;
-  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = kWsCons >> 5;
-  for (int n = 0; n < nmine; ++n) {
-    const int bf = n & 1;
-    bar_sync(kBarFull, kWsThreads);
-    double Pv[QPT], Qp[QPT], Qm[QPT], Rv[QPT];
-#pragma unroll
-    for (int s = 0; s < QPT; ++s) {
-      const int t = threadIdx.x + s * kWsCons;
-      if (t >= quarter) { Pv[s] = Qp[s] = Qm[s] = Rv[s] = 0.0; continue; }
-      const double4 v = xq[t];
-      Pv[s] = v.x; Qp[s] = v.y; Qm[s] = v.z; Rv[s] = v.w;
-    }
-    const WsMeta mt = meta[bf];
-    if (n + 1 < nmine) bar_arrive(kBarEmpty, kWsThreads);   // the quads are in registers: release xq
-    const WsRow* ri = rinfo + bf * kMaxColRows;
-    const int nrows = mt.nrows;
-#pragma unroll 1
-    for (int c0 = 0; c0 < (abl == 1 ? 0 : 3); ++c0) {
-      const int cbeg = c0 == 0 ? 0 : (c0 == 1 ? mt.ncl0 : mt.ncl0 + mt.ncl1);
-      const int cend = c0 == 0 ? mt.ncl0 : (c0 == 1 ? mt.ncl0 + mt.ncl1 : nrows);
-#pragma unroll 1
-      for (int u = cbeg; u < cend; u += 4) {
-        const int nr = cend - u < 4 ? cend - u : 4;
-        double accs[4] = {0.0, 0.0, 0.0, 0.0}, accc[4] = {0.0, 0.0, 0.0, 0.0};
-        double S[4], Sm[4], C[4], Cm[4], twocd[4];
-#pragma unroll
-        for (int k = 0; k < 4; ++k) {
-          const WsRow& w = ri[k < nr ? u + k : u];
-          const int r0 = (w.j * (int)threadIdx.x) & m2;
-          const double s0 = sinr(r0), c0v = sinr((r0 + half) & m2), sd = w.sd, cd = w.cd;
-          S[k] = s0;
-          C[k] = c0v;
-          Sm[k] = fma(s0, cd, -c0v * sd);   // angle − πjB/N
-          Cm[k] = fma(c0v, cd, s0 * sd);
-          twocd[k] = 2.0 * cd;
-        }
-        if (c0 == 0) {
-#pragma unroll
-          for (int s = 0; s < QPT; ++s) {
-#pragma unroll
-            for (int k = 0; k < 4; ++k) {
-              accs[k] = fma(Pv[s], S[k], accs[k]);
-              accc[k] = fma(Rv[s], C[k], accc[k]);
-              const double sn = fma(twocd[k], S[k], -Sm[k]), cn = fma(twocd[k], C[k], -Cm[k]);
-              Sm[k] = S[k];
-              S[k] = sn;
-              Cm[k] = C[k];
-              C[k] = cn;
-            }
-          }
-        } else {
-#pragma unroll
-          for (int s = 0; s < QPT; ++s) {
-            const double xv = c0 == 1 ? Qp[s] : Qm[s];
-#pragma unroll
-            for (int k = 0; k < 4; ++k) {
-              accs[k] = fma(xv, S[k], accs[k]);
-              const double sn = fma(twocd[k], S[k], -Sm[k]);
-              Sm[k] = S[k];
-              S[k] = sn;
-            }
-          }
-        }
-        double acc[8];
-#pragma unroll
-        for (int k = 0; k < 4; ++k) {
-          acc[k] = accs[k];
-          acc[4 + k] = accc[k];
-        }
-        if (threadIdx.x == 0) {
-#pragma unroll
-          for (int k = 0; k < 4; ++k) acc[k] += ri[k < nr ? u + k : u].extra;
-        }
-        const double ws = warp_transpose_reduce8(acc);
-        if ((lane & 3) == 0) {
-          const int v = ((lane >> 4) & 1) * 4 + ((lane >> 3) & 1) * 2 + ((lane >> 2) & 1);
-          const int k = v & 3;
-          if (k < nr) red[(size_t)wid * 2 * T.mcr + 2 * (u + k) + (v >> 2)] = ws;
-        }
-      }
-    }
-    bar_sync(kBarCons, kWsCons);   // the warps' partials of every row are in `red`
-    for (int t = threadIdx.x; t < nrows; t += kWsCons) {
-      double s1 = 0.0, s2 = 0.0;
-      for (int w = 0; w < nw; ++w) {
-        s1 += red[(size_t)w * 2 * T.mcr + 2 * t];
-        s2 += red[(size_t)w * 2 * T.mcr + 2 * t + 1];
-      }
-      const int j = ri[t].j;
-      const double sig = ((j >> 1) & 1) ? -1.0 : 1.0;   // σ_j = sin(πj/2) for odd j
-      vsten[mt.u0 + t] = scale * ((j & 1) ? s1 + sig * s2 : s1);
-    }
-    // the next item's FULL barrier (all 512 threads) orders these reads of `red` before its writes
   }
 }
 
@@ -1640,44 +1367,15 @@ void launch_inverse_sparse(const DevTables& T, const double* spec, const double*
   if (ncols <= 0) return;
   const int quarter = T.N / 4;
   const int qpt = (quarter + kInvThreads - 1) / kInvThreads;
-  // KFBI_INV = ws | sync | async (default sync): A/B switch for the measurements in DESIGN.md §7
-  static const char* mode_env = std::getenv("KFBI_INV");
-  static const int mode = !mode_env ? 1 : (mode_env[0] == 'w' ? 0 : (mode_env[0] == 's' ? 1 : 2));
-  static const int abl = std::getenv("KFBI_WS_ABL") ? std::atoi(std::getenv("KFBI_WS_ABL")) : 0;
-  const int grid = ncols < 2 * num_sms() ? ncols : 2 * num_sms();
-  ++g_launches;
-  if (mode == 0) {
-    const size_t smw = (size_t)((T.N + T.N / 16 + 1 + 3) & ~3) * sizeof(double) + (size_t)quarter * sizeof(double4) +
-                       2 * kMaxColRows * sizeof(WsRow) + 2 * sizeof(WsMeta) +
-                       (size_t)(kWsCons / 32) * 2 * T.mcr * sizeof(double);
-    const int gw = ncols < num_sms() ? ncols : num_sms();
-    switch (qpt) {
-      case 1: smem_optin((const void*)k_inv_ws<1>, smw); k_inv_ws<1><<<gw, kWsThreads, smw, s>>>(T, spec, hsep, vsten, abl); break;
-      case 2: smem_optin((const void*)k_inv_ws<2>, smw); k_inv_ws<2><<<gw, kWsThreads, smw, s>>>(T, spec, hsep, vsten, abl); break;
-      case 4: smem_optin((const void*)k_inv_ws<4>, smw); k_inv_ws<4><<<gw, kWsThreads, smw, s>>>(T, spec, hsep, vsten, abl); break;
-      case 8: smem_optin((const void*)k_inv_ws<8>, smw); k_inv_ws<8><<<gw, kWsThreads, smw, s>>>(T, spec, hsep, vsten, abl); break;
-      default: break;
-    }
-    return;
-  }
   const size_t red_b = (size_t)(kInvThreads / 32) * 2 * T.mcr * sizeof(double);
-  if (mode == 1) {
-    const size_t sm = (size_t)(T.N + T.N / 16 + 1) * sizeof(double) + red_b;
-    switch (qpt) {
-      case 1: smem_optin((const void*)k_inv_sparse<1, false>, sm); k_inv_sparse<1, false><<<grid, kInvThreads, sm, s>>>(T, spec, hsep, vsten, abl); break;
-      case 2: smem_optin((const void*)k_inv_sparse<2, false>, sm); k_inv_sparse<2, false><<<grid, kInvThreads, sm, s>>>(T, spec, hsep, vsten, abl); break;
-      case 4: smem_optin((const void*)k_inv_sparse<4, false>, sm); k_inv_sparse<4, false><<<grid, kInvThreads, sm, s>>>(T, spec, hsep, vsten, abl); break;
-      case 8: smem_optin((const void*)k_inv_sparse<8, false>, sm); k_inv_sparse<8, false><<<grid, kInvThreads, sm, s>>>(T, spec, hsep, vsten, abl); break;
-      default: break;
-    }
-    return;
-  }
-  const size_t sm = (size_t)(2 * T.N / 64 + 64) * sizeof(double2) + (size_t)T.N * sizeof(double) + red_b;
+  const int grid = ncols < 2 * num_sms() ? ncols : 2 * num_sms();
+  const size_t sm = (size_t)(T.N + T.N / 16 + 1) * sizeof(double) + red_b;
+  ++g_launches;
   switch (qpt) {
-    case 1: smem_optin((const void*)k_inv_sparse<1, true>, sm); k_inv_sparse<1, true><<<grid, kInvThreads, sm, s>>>(T, spec, hsep, vsten, abl); break;
-    case 2: smem_optin((const void*)k_inv_sparse<2, true>, sm); k_inv_sparse<2, true><<<grid, kInvThreads, sm, s>>>(T, spec, hsep, vsten, abl); break;
-    case 4: smem_optin((const void*)k_inv_sparse<4, true>, sm); k_inv_sparse<4, true><<<grid, kInvThreads, sm, s>>>(T, spec, hsep, vsten, abl); break;
-    case 8: smem_optin((const void*)k_inv_sparse<8, true>, sm); k_inv_sparse<8, true><<<grid, kInvThreads, sm, s>>>(T, spec, hsep, vsten, abl); break;
+    case 1: smem_optin((const void*)k_inv_sparse<1>, sm); k_inv_sparse<1><<<grid, kInvThreads, sm, s>>>(T, spec, hsep, vsten); break;
+    case 2: smem_optin((const void*)k_inv_sparse<2>, sm); k_inv_sparse<2><<<grid, kInvThreads, sm, s>>>(T, spec, hsep, vsten); break;
+    case 4: smem_optin((const void*)k_inv_sparse<4>, sm); k_inv_sparse<4><<<grid, kInvThreads, sm, s>>>(T, spec, hsep, vsten); break;
+    case 8: smem_optin((const void*)k_inv_sparse<8>, sm); k_inv_sparse<8><<<grid, kInvThreads, sm, s>>>(T, spec, hsep, vsten); break;
     default: break;
   }
 }

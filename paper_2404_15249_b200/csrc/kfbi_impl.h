@@ -110,6 +110,7 @@ struct Setup {
   std::vector<int32_t> ocol_order;       // stencil-column items by descending row count (k_inv_sparse)
   std::vector<int32_t> blk_order;        // ADM blocks by descending sparse-entry count (k_sweep)
   std::vector<int32_t> blk_meta;         // 3 per position of blk_order: block, first entry, end entry
+  std::vector<int32_t> ocol_meta;        // 6 per position of ocol_order: item, column, row range, class counts
   std::vector<int32_t> st_node;          // M*6 → unique stencil node index
   std::vector<int8_t> st_ext;            // M*6: 1 if the node is in Ω^c
   std::vector<double> st_w, st_dx, st_dy;   // M*6: row 0 of the inverse local system, offsets
@@ -239,7 +240,7 @@ struct DevTables {
   const int32_t *z_comp, *z_knot;
   const double *z_t1, *z_t2, *z_p1, *z_p2;
   // stencils
-  const int32_t *sn_j, *ocol, *ocol_ptr, *st_node, *ocol_ncls, *ocol_order, *blk_order, *blk_meta;
+  const int32_t *sn_j, *ocol, *ocol_ptr, *st_node, *ocol_ncls, *ocol_order, *blk_order, *blk_meta, *ocol_meta;
   const int8_t* st_ext;
   const double *st_w, *st_dx, *st_dy, *st_wn;
   int neumann;   // K_N: density = ψ (Φ = 0, Ψ = ψ) and the normal-derivative interpolation

@@ -511,6 +511,13 @@ void build_setup(Setup& S, const kfbi_grid* g, const kfbi_boundary* b, const kfb
     std::stable_sort(S.ocol_order.begin(), S.ocol_order.end(), [&](int32_t x, int32_t y) {
       return S.ocol_ptr[x + 1] - S.ocol_ptr[x] > S.ocol_ptr[y + 1] - S.ocol_ptr[y];
     });
+    // per work position: (item, column, first row, end row, odd rows, j ≡ 0 rows) — one load per item
+    S.ocol_meta.resize(6 * S.ocol_order.size());
+    for (size_t kk = 0; kk < S.ocol_order.size(); ++kk) {
+      const int32_t b = S.ocol_order[kk];
+      const int32_t v[6] = {b, S.ocol[b], S.ocol_ptr[b], S.ocol_ptr[b + 1], S.ocol_ncls[3 * b], S.ocol_ncls[3 * b + 1]};
+      std::copy(v, v + 6, S.ocol_meta.begin() + 6 * kk);
+    }
   }
 
   setup_tick("spline filters (reading R10; SUR");

@@ -193,16 +193,25 @@ __global__ void __launch_bounds__(kSweepThreads, 2) k_sweep(DevTables T, const d
   // blocks in descending count of sparse entries (setup order `blk_order`), snake-dealt over the
   // G block groups so that the groups that draw the blocks where Γ runs along x are not the tail
   const int grp = blockIdx.x / nch;
+  // the next block's (block, entry range) is loaded one round ahead (three registers)
+  auto meta = [&](int rnd, int& g, int& e0, int& e1) {
+    const int kk = rnd * G + ((rnd & 1) ? G - 1 - grp : grp);
+    g = -1;
+    if (kk >= T.P) return;
+    g = T.blk_meta[3 * kk];
+    e0 = T.blk_meta[3 * kk + 1];
+    e1 = T.blk_meta[3 * kk + 2];
+  };
+  int ng = -1, ne0 = 0, ne1 = 0;
+  meta(0, ng, ne0, ne1);
   for (int rnd = 0; rnd * G < T.P; ++rnd) {
-  const int kk = rnd * G + ((rnd & 1) ? G - 1 - grp : grp);
-  if (kk >= T.P) continue;
-  const int g = T.blk_meta[3 * kk];
-  if (g < T.g_lo || g >= T.g_hi) continue;   // CTA-uniform
+  const int g = ng, e0 = ne0, e1m = ne1;
+  meta(rnd + 1, ng, ne0, ne1);
+  if (g < T.g_lo || g >= T.g_hi) continue;   // CTA-uniform (g = −1: no block)
     const int c0 = BL * g + 1;
     KFBI_CHECK(c0 - 1 >= T.col_lo - 1 && c0 - 1 + LB - 1 <= T.col_hi - 1, c0, T.col_hi);   // spectral rows of the slab
-    const int e0 = T.blk_meta[3 * kk + 1];
     const int ncol = g < T.P - 1 ? BL : LB;   // block columns + separator column
-    const int e1 = cval ? T.blk_meta[3 * kk + 2] : e0;
+    const int e1 = cval ? e1m : e0;
     // the block's entries are staged kEntCap at a time (a block where Γ runs along x holds up to
     // ~1,700 on the 8192² star: staging them all would leave one CTA per SM); later passes add into R
     for (int cb = e0, pass = 0; pass == 0 || cb < e1; cb += kEntCap, ++pass) {

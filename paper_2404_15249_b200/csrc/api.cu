@@ -63,6 +63,8 @@ struct kfbi_ctx {
   double *segbuf = nullptr, *h2 = nullptr, *parts = nullptr;
   double *seg3 = nullptr, *seg3_in = nullptr, *h3_out = nullptr, *h3_in = nullptr;   // 3D level-2 exchange
   std::vector<DevTables> slabs;   // per-rank slab tables (2D), rebuilt with the workspace layout
+  std::vector<int32_t> q_g01, z_g01;   // spline knot pairs of the intersections / control points
+  std::vector<double> q_dl, z_dl;
   Setup S;
   DevTables T{};
   Setup3 S3;
@@ -185,6 +187,25 @@ void layout(kfbi_ctx* c, Arena& A) {
   coff.clear(); cM.clear(); cdel.clear();
   for (auto& cc : S.comps) { coff.push_back(cc.off); cM.push_back(cc.M); cdel.push_back(cc.delta); }
   T.c_off = A.table(coff); T.c_M = A.table(cM); T.c_delta = A.table(cdel);
+  // the two spline knots (global density indices) and Δs of every intersection and control point: one
+  // load level for the jump kernels instead of point → component → offset, size
+  auto knots = [&](const std::vector<int32_t>& comp, const std::vector<int32_t>& knot, std::vector<int32_t>& g01,
+                   std::vector<double>& dl) {
+    const size_t n = comp.size();
+    g01.resize(2 * n);
+    dl.resize(n);
+    for (size_t k = 0; k < n; ++k) {
+      const Comp& cc = S.comps[comp[k]];
+      const int m = knot[k], m1 = m + 1 == cc.M ? 0 : m + 1;
+      g01[2 * k] = cc.off + m;
+      g01[2 * k + 1] = cc.off + m1;
+      dl[k] = cc.delta;
+    }
+  };
+  knots(S.q_comp, S.q_knot, c->q_g01, c->q_dl);
+  knots(S.z_comp, S.z_knot, c->z_g01, c->z_dl);
+  T.q_g01 = A.table(c->q_g01); T.q_dl = A.table(c->q_dl);
+  T.z_g01 = A.table(c->z_g01); T.z_dl = A.table(c->z_dl);
   T.sp_ntaps = A.table(S.sp_ntaps); T.sp_first = A.table(S.sp_first); T.sp_coef_off = A.table(S.sp_coef_off);
   T.sp_coef = A.table(S.sp_coef);
   T.sin_tab = A.table(S.sin_tab); T.dk = A.table(S.dk); T.invc = A.table(S.invc); T.zr = A.table(S.zr);

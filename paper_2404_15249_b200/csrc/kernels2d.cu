@@ -31,13 +31,12 @@
 namespace kfbi {
 namespace {
 
-__device__ __forceinline__ void spline_eval(const double* __restrict__ phi, const double* __restrict__ mk, int off,
-                                            int Mc, double delta, int m, double t, double& g, double& gp,
-                                            double& gpp) {
-  // SURVEY App. A.7 on [s_m, s_{m+1}], t = (s − s_m)/Δ
-  int m1 = (m + 1 == Mc) ? 0 : m + 1;
-  double g0 = phi[off + m], g1 = phi[off + m1], a = mk[off + m], b = mk[off + m1];
-  double w = 1.0 - t;
+// the density and its arc-length derivatives on [s_m, s_{m+1}] (t = (s − s_m)/Δ) from the
+// point's precomputed knot pair (global density indices of knots m and m + 1)
+__device__ __forceinline__ void spline_eval2(const double* __restrict__ phi, const double* __restrict__ mk, int2 g01,
+                                             double delta, double t, double& g, double& gp, double& gpp) {
+  const double g0 = phi[g01.x], g1 = phi[g01.y], a = mk[g01.x], b = mk[g01.y];
+  const double w = 1.0 - t;
   g = w * g0 + t * g1 + (delta * delta / 6.0) * ((w * w * w - w) * a + (t * t * t - t) * b);
   gp = (g1 - g0) / delta + (delta / 6.0) * (-(3.0 * w * w - 1.0) * a + (3.0 * t * t - 1.0) * b);
   gpp = w * a + t * b;
@@ -113,8 +112,7 @@ __global__ void k_correct(DevTables T, const double* __restrict__ phi, const dou
     } else {
       double Phi = 0, Phis = 0, Phiss = 0;
       if (phi) {
-        int c = T.q_comp[q];
-        spline_eval(phi, mk, T.c_off[c], T.c_M[c], T.c_delta[c], T.q_knot[q], T.q_t[q], Phi, Phis, Phiss);
+        spline_eval2(phi, mk, reinterpret_cast<const int2*>(T.q_g01)[q], T.q_dl[q], T.q_t[q], Phi, Phis, Phiss);
       }
       double F = fq ? fq[q] : 0.0;
       // Neumann (R38): the density is ψ = [∂_n v] with [v] = 0
@@ -821,8 +819,7 @@ __global__ void k_interp(DevTables T, const double* __restrict__ phi, const doub
   } else {
     double Phi = 0, Phis = 0, Phiss = 0;
     if (phi) {
-      const int c = T.z_comp[m];
-      spline_eval(phi, mk, T.c_off[c], T.c_M[c], T.c_delta[c], T.z_knot[m], 0.0, Phi, Phis, Phiss);
+      spline_eval2(phi, mk, reinterpret_cast<const int2*>(T.z_g01)[m], T.z_dl[m], 0.0, Phi, Phis, Phiss);
     }
     J = T.neumann ? jumps2d(0.0, 0.0, 0.0, Phi, Phis, fz ? fz[m] : 0.0, T.kappa, T.z_t1[m], T.z_t2[m], T.z_p1[m], T.z_p2[m])
                   : jumps2d(Phi, Phis, Phiss, 0.0, 0.0, fz ? fz[m] : 0.0, T.kappa, T.z_t1[m], T.z_t2[m], T.z_p1[m], T.z_p2[m]);

@@ -238,6 +238,8 @@ struct DevTables {
   const double* pair_d;
   // control points
   const int32_t *z_comp, *z_knot;
+  const int32_t *q_g01, *z_g01;   // global density indices of the knots m, m + 1 of each point
+  const double *q_dl, *z_dl;      // Δs of the point's component
   const double *z_t1, *z_t2, *z_p1, *z_p2;
   // stencils
   const int32_t *sn_j, *ocol, *ocol_ptr, *st_node, *ocol_ncls, *ocol_order, *blk_order, *blk_meta, *ocol_meta;

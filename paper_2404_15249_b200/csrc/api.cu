@@ -65,6 +65,7 @@ struct kfbi_ctx {
   std::vector<DevTables> slabs;   // per-rank slab tables (2D), rebuilt with the workspace layout
   std::vector<int32_t> q_g01, z_g01;   // spline knot pairs of the intersections / control points
   std::vector<double> q_dl, z_dl;
+  std::vector<uint8_t> row_omega;
   Setup S;
   DevTables T{};
   Setup3 S3;
@@ -219,6 +220,9 @@ void layout(kfbi_ctx* c, Arena& A) {
   c->d_om_ptr = A.table(c->om_ptr);
   c->d_om_seg = A.table(c->om_seg);
   c->d_side = T.side;
+  c->row_omega.assign(S.N + 1, 0);
+  for (int i = 0; i <= S.N; ++i) c->row_omega[i] = c->om_ptr[i + 1] > c->om_ptr[i] ? 1 : 0;
+  T.row_omega = A.table(c->row_omega);
   // holes
   auto& hoff = c->hoff; auto& hM = c->hM; auto& hdel = c->hdel; auto& oneh = c->oneh;
   hoff.clear(); hM.clear(); hdel.clear(); oneh.clear();

@@ -1116,12 +1116,15 @@ __global__ void __launch_bounds__(DenseCfg<N>::NTHR, 1) k_dst_dense2(DevTables T
     for (int s = 0; s < 8; ++s) fp[s] = reinterpret_cast<const double2*>(f)[tid + NTH * s];
     rsync<NTH>();
   }
-  dst1_core<N>(z, tw, tid, fp);
+  // a forward row of f·1_Ω with no Ω node (a grid column outside Γ's x-extent) has a zero spectrum:
+  // no transform (CTA-uniform when a CTA holds one row, N ≥ 2048)
+  const bool empty = MODE == 0 && RPC == 1 && mask_omega && bp.nh == 0 && live && !T.row_omega[i];
+  if (!empty) dst1_core<N>(z, tw, tid, fp);
   if (!live) continue;
   if (MODE == 0) {
     for (int p = tid; p < N; p += NTH) {   // modes → spectral positions
       const int k = position_mode(p, N);
-      __stcs(dst + (size_t)(i - 1) * N + p, k ? z[zpad(k)].x : 0.0);
+      __stcs(dst + (size_t)(i - 1) * N + p, (k && !empty) ? z[zpad(k)].x : 0.0);
     }
   } else {
     const double sc = 2.0 / N;

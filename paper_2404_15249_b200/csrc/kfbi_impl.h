@@ -239,6 +239,7 @@ struct DevTables {
   // control points
   const int32_t *z_comp, *z_knot;
   const int32_t *q_g01, *z_g01;   // global density indices of the knots m, m + 1 of each point
+  const uint8_t* row_omega;       // grid column i holds Ω nodes
   const double *q_dl, *z_dl;      // Δs of the point's component
   const double *z_t1, *z_t2, *z_p1, *z_p2;
   // stencils

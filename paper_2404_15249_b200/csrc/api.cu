@@ -1342,7 +1342,8 @@ kfbi_status kfbi_profile_apply(kfbi_ctx* c, const double* d_phi, double* d_out, 
   for (auto& e : ev) ck(cudaEventCreate(&e), "event");
   double acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
   if (c->dim == 3) {
-    const DevTables3& T3 = c->T3;
+    // one rank per process: this rank's slab (its working arrays hold the slab's planes only)
+    const DevTables3 T3 = c->local_io ? slab3(c, c->rank) : c->T3;
     const double sc = 2.0 / T3.N;
     for (int r = 0; r < reps; ++r) {
       ck(cudaEventRecord(ev[0], s), "rec");
@@ -1359,7 +1360,7 @@ kfbi_status kfbi_profile_apply(kfbi_ctx* c, const double* d_phi, double* d_out, 
       ck(cudaEventRecord(ev[5], s), "rec");
       launch_sparse3(T3, 2, c->work2, nullptr, sc, c->work, s);
       ck(cudaEventRecord(ev[6], s), "rec");
-      launch_interp3(T3, d_phi, c->dphi, nullptr, nullptr, c->work, d_out, s);
+      launch_interp3(T3, d_phi, c->dphi, nullptr, nullptr, c->work, d_out, s, c->local_io);
       ck(cudaEventRecord(ev[7], s), "rec");
       ck(cudaEventSynchronize(ev[7]), "sync");
       for (int q = 0; q < 7; ++q) {

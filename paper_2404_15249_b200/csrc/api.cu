@@ -311,7 +311,7 @@ void layout3(kfbi_ctx* c, Arena& A) {
   T.irr_row_perm = A.table(S.irr_row_perm); T.irr_row_nheavy = A.table(S.irr_row_nheavy);
   T.max_plane_irr = S.max_plane_irr;
   T.irr_row_ptr = A.table(S.irr_row_ptr); T.zrow_id = A.table(S.zrow_id); T.zrow_ptr = A.table(S.zrow_ptr);
-  T.znode_b = A.table(S.znode_b); T.nzrow = (int)S.zrow_id.size(); T.zrow_need = A.table(S.zrow_need);
+  T.znode_b = A.table(S.znode_b); T.nzrow = (int)S.zrow_id.size(); T.zplane_ptr = A.table(S.zplane_ptr);
   T.world = c->world; T.L3 = S.L3;
   T.q_lo[0] = 0; T.q_hi[0] = S.nq; T.q_lo[1] = T.q_hi[1] = T.q_lo[2] = T.q_hi[2] = S.nq;
   T.n_lo = 0; T.n_hi = S.nirr;

@@ -428,7 +428,10 @@ __global__ void __launch_bounds__(256, 2) k_fwd3s(DevTables3 T, const double* __
 // inverse along y: spectral rows (i, ll) fixed up with the separators (R20), DST along kk → a, stored
 // transposed to out[(i−1)][a][ll] so that the z-direction evaluation reads contiguous rows.
 template <int N>
-__global__ void __launch_bounds__(256, 2) k_inv3y(DevTables3 T, const double* __restrict__ spec,
+#ifndef KFBI_INV3Y_MINB
+#define KFBI_INV3Y_MINB 2
+#endif
+__global__ void __launch_bounds__(256, KFBI_INV3Y_MINB) k_inv3y(DevTables3 T, const double* __restrict__ spec,
                                                   const double* __restrict__ hsep, double scale,
                                                   double* __restrict__ out) {
   constexpr int NTL = N / 32, RPC = 256 / NTL < N ? 256 / NTL : N, NTHR = RPC * NTL, ZS = N / 2 + N / 32 + 1;
@@ -438,17 +441,17 @@ __global__ void __launch_bounds__(256, 2) k_inv3y(DevTables3 T, const double* __
   const int rl = threadIdx.x / NTL, tid = threadIdx.x % NTL;
   double2* z = smz + rl * ZS;
   const size_t m0 = (size_t)(l0 + rl) * N;
-  __shared__ uint8_t s_need[N];   // visible after the barrier below
-  for (int a = threadIdx.x; a < N; a += NTHR) s_need[a] = T.zrow_need[(size_t)(i - 1) * N + a];
+  __shared__ int16_t s_row[N];   // visible after the barrier below
+  const int w0 = T.zplane_ptr[i - 1], nn = T.zplane_ptr[i] - w0;
+  for (int w = threadIdx.x; w < nn; w += NTHR) s_row[w] = (int16_t)(T.zrow_id[w0 + w] - (i - 1) * N);
   load_fixed_row<N>(T, spec, hsep, i, m0, z, tid);
   __syncwarp();
   dst2_core<N>(z, tw, tid);
   __syncthreads();
   // only the grid rows (i, a) that hold stencil nodes are read by the z-evaluation: the others are
   // not stored (≈ 80 % of the y-inverse's writes at C5)
-  for (int idx = threadIdx.x; idx < N * RPC; idx += NTHR) {
-    const int c = idx % RPC, a = idx / RPC;
-    if (!s_need[a]) continue;
+  for (int idx = threadIdx.x; idx < nn * RPC; idx += NTHR) {
+    const int c = idx % RPC, a = s_row[idx / RPC];
     const double v = (a == 0 || l0 + c == 0) ? 0.0 : scale * reinterpret_cast<const double*>(smz + c * ZS)[fpos(a)];
     out[((size_t)(i - 1) * N + a) * N + l0 + c] = v;
   }

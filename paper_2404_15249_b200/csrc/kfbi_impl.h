@@ -178,7 +178,7 @@ struct Setup3 {
   std::vector<int32_t> irr_row_nheavy;   // N−1: rows of the plane with more than kHeavyRow entries
   int max_plane_irr = 0;
   std::vector<int32_t> zrow_id, zrow_ptr, znode_b;   // distinct stencil nodes grouped by grid row
-  std::vector<uint8_t> zrow_need;                    // (N−1)·N: 1 if grid row (i−1)·N + a holds stencil nodes
+  std::vector<int32_t> zplane_ptr;                   // N: zrow_id[zplane_ptr[i−1] .. zplane_ptr[i]) lie in plane i
   // multi-GPU level-2 split of the reduced system (world > 1): slabs of P/world blocks hold
   // L3 = P/world − 1 interior separators each (pivots rinv3, spike z3r: L3 × K), the world − 1 slab
   // separators solve tridiag(red3_a, red3_b, red3_a) per mode after the exchange
@@ -208,7 +208,7 @@ struct DevTables3 {
   const double *sin_tab, *dk, *zr, *red_a, *red_b;
   const double* tw;   // 2N × (cos, sin)
   const int32_t *irr_row_ptr, *zrow_id, *zrow_ptr, *znode_b;
-  const uint8_t* zrow_need;   // rows the z-evaluation reads (the y-inverse writes only those)
+  const int32_t* zplane_ptr;   // per plane, the rows the z-evaluation reads (the y-inverse writes only those)
   const int16_t* irr_row_perm;
   const int32_t* irr_row_nheavy;
   int max_plane_irr;

@@ -391,8 +391,10 @@ void build_setup3(Setup3& S, const kfbi_grid* g, const kfbi_boundary* b, const k
       S.znode_b.push_back((int32_t)(nodes[e] % N));
     }
     S.zrow_ptr.push_back((int32_t)nodes.size());
-    S.zrow_need.assign((size_t)(N - 1) * N, 0);
-    for (int32_t r : S.zrow_id) S.zrow_need[r] = 1;
+    S.zplane_ptr.assign(N, 0);
+    for (int i = 1; i <= N; ++i)
+      S.zplane_ptr[i - 1] = (int32_t)(std::lower_bound(S.zrow_id.begin(), S.zrow_id.end(), (i - 1) * N) -
+                                      S.zrow_id.begin());
   }
 
   // fast-solver tables: modes m = ll·N + kk (DST along z → ll, along y → kk), tridiagonal along x

@@ -548,7 +548,9 @@ void apply_KD2(kfbi_ctx* c, const double* phi, double* out, cudaStream_t s) {
   const DevTables& T = c->T;
   launch_spline(T, phi, c->mk, s, c->hole_off, c->hole_M, c->hole_delta, c->nh, c->ahole);   // + a_h (R27)
   for (int r : my_ranks(c)) launch_correct(slab(c, r), phi, c->mk, nullptr, nullptr, c->cval, s);   // slab's nodes
-  spectral2(c, c->cval, DenseSrc{}, s);
+  DenseSrc D;
+  D.stencil_only = true;
+  spectral2(c, c->cval, D, s);
   interp2(c, phi, nullptr, nullptr, true, out, s);
 }
 
@@ -559,6 +561,7 @@ void apply_Y2(kfbi_ctx* c, const double* fgrid, const double* fq, const double* 
   for (int r : my_ranks(c)) launch_correct(slab(c, r), nullptr, nullptr, fq, nullptr, c->cval, s);
   DenseSrc D;
   D.base = c->spec_f;
+  D.stencil_only = true;
   spectral2(c, c->cval, D, s);
   interp2(c, nullptr, fz, nullptr, false, out, s);
 }
@@ -949,6 +952,7 @@ kfbi_status kfbi_set_workspace(kfbi_ctx* c, void* d_ws, size_t bytes) {
     dst_forward2(c, nullptr, false, bp, c->spec_bump + (size_t)h * nspec, s);
     DenseSrc D;
     D.base = c->spec_bump + (size_t)h * nspec;
+    D.stencil_only = true;
     spectral2(c, nullptr, D, s);
     interp2(c, nullptr, nullptr, nullptr, false, c->wg + (size_t)h * c->S.M, s);
   }
@@ -1382,7 +1386,9 @@ kfbi_status kfbi_profile_apply(kfbi_ctx* c, const double* d_phi, double* d_out, 
     ck(cudaEventRecord(ev[1], s), "rec");
     for (int r : my_ranks(c)) launch_correct(slab(c, r), d_phi, c->mk, nullptr, nullptr, c->cval, s);
     ck(cudaEventRecord(ev[2], s), "rec");
-    launch_sweep(T, c->cval, DenseSrc{}, c->spec, c->zfirst, c->zlast, c->fsep, s);
+    DenseSrc D;
+    D.stencil_only = true;
+    launch_sweep(T, c->cval, D, c->spec, c->zfirst, c->zlast, c->fsep, s);
     ck(cudaEventRecord(ev[3], s), "rec");
     launch_reduced(T, c->zfirst, c->zlast, c->fsep, c->hsep, s);
     ck(cudaEventRecord(ev[4], s), "rec");

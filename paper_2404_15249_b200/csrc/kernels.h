@@ -50,6 +50,7 @@ struct DenseSrc {
   const double* bump = nullptr;
   long ldb = 0;
   const double* coef = nullptr;   // device, nb entries
+  bool stencil_only = false;      // the sweep stores only the spectral rows of stencil columns (sparse inverse follows)
   int blo[4] = {0, 0, 0, 0}, bhi[4] = {-1, -1, -1, -1};   // grid columns i where bump h can be non-zero
   bool any() const { return base || nb > 0; }
 };

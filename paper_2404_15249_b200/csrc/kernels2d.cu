@@ -192,19 +192,18 @@ __global__ void __launch_bounds__(kSweepThreads, 2) k_sweep(DevTables T, const d
   // G block groups so that the groups that draw the blocks where Γ runs along x are not the tail
   const int grp = blockIdx.x / nch;
   // the next block's (block, entry range) is loaded one round ahead (three registers)
-  auto meta = [&](int rnd, int& g, int& e0, int& e1) {
+  auto meta = [&](int rnd, int4& m) {
     const int kk = rnd * G + ((rnd & 1) ? G - 1 - grp : grp);
-    g = -1;
+    m.x = -1;
     if (kk >= T.P) return;
-    g = T.blk_meta[3 * kk];
-    e0 = T.blk_meta[3 * kk + 1];
-    e1 = T.blk_meta[3 * kk + 2];
+    m = __ldg(reinterpret_cast<const int4*>(T.blk_meta) + kk);
   };
-  int ng = -1, ne0 = 0, ne1 = 0;
-  meta(0, ng, ne0, ne1);
+  int4 nm = make_int4(-1, 0, 0, 0);
+  meta(0, nm);
   for (int rnd = 0; rnd * G < T.P; ++rnd) {
-  const int g = ng, e0 = ne0, e1m = ne1;
-  meta(rnd + 1, ng, ne0, ne1);
+  const int g = nm.x, e0 = nm.y, e1m = nm.z;
+  const int keep = D.stencil_only ? nm.w : 0x7fff;   // positions whose spectral rows are stored
+  meta(rnd + 1, nm);
   if (g < T.g_lo || g >= T.g_hi) continue;   // CTA-uniform (g = −1: no block)
     const int c0 = BL * g + 1;
     KFBI_CHECK(c0 - 1 >= T.col_lo - 1 && c0 - 1 + LB - 1 <= T.col_hi - 1, c0, T.col_hi);   // spectral rows of the slab
@@ -354,13 +353,14 @@ __global__ void __launch_bounds__(kSweepThreads, 2) k_sweep(DevTables T, const d
     const double2 cl = icp(LB - 1);
     double z1 = y1[LB - 1] * cl.x, z2 = y2[LB - 1] * cl.y;
     const double zl1 = z1, zl2 = z2;
-    *reinterpret_cast<double2*>(spec + (size_t)(c0 - 1 + LB - 1) * N + p1) = make_double2(z1, z2);
+    if ((keep >> (LB - 1)) & 1)
+      *reinterpret_cast<double2*>(spec + (size_t)(c0 - 1 + LB - 1) * N + p1) = make_double2(z1, z2);
 #pragma unroll
     for (int p = LB - 2; p >= 0; --p) {
       const double2 c = icp(p);
       z1 = (y1[p] - z1) * c.x;
       z2 = (y2[p] - z2) * c.y;
-      *reinterpret_cast<double2*>(spec + (size_t)(c0 - 1 + p) * N + p1) = make_double2(z1, z2);
+      if ((keep >> p) & 1) *reinterpret_cast<double2*>(spec + (size_t)(c0 - 1 + p) * N + p1) = make_double2(z1, z2);
     }
     *reinterpret_cast<double2*>(zB + (size_t)g * N + p1) = make_double2(z1, z2);
     if (g < T.P - 1) *reinterpret_cast<double2*>(zA + (size_t)g * N + p1) = make_double2(sep1 - zl1, sep2 - zl2);

@@ -109,7 +109,7 @@ struct Setup {
   std::vector<int32_t> ocol_ncls;        // 3 per stencil column: rows of class odd, j≡0, j≡2 (mod 4)
   std::vector<int32_t> ocol_order;       // stencil-column items by descending row count (k_inv_sparse)
   std::vector<int32_t> blk_order;        // ADM blocks by descending sparse-entry count (k_sweep)
-  std::vector<int32_t> blk_meta;         // 3 per position of blk_order: block, first entry, end entry
+  std::vector<int32_t> blk_meta;         // 4 per position of blk_order: block, first entry, end entry, stencil-column mask
   std::vector<int32_t> ocol_meta;        // 6 per position of ocol_order: item, column, row range, class counts
   std::vector<int32_t> st_node;          // M*6 → unique stencil node index
   std::vector<int8_t> st_ext;            // M*6: 1 if the node is in Ω^c

@@ -651,13 +651,20 @@ void build_setup(Setup& S, const kfbi_grid* g, const kfbi_boundary* b, const kfb
   S.blk_order.resize(P);
   for (int gg = 0; gg < P; ++gg) S.blk_order[gg] = gg;
   std::stable_sort(S.blk_order.begin(), S.blk_order.end(), [&](int32_t x, int32_t y) { return bcnt[x] > bcnt[y]; });
-  // per position of that order: (block, first entry, end entry) — one load instead of blk_order → col_ptr
-  S.blk_meta.resize(3 * (size_t)P);
+  // per position of that order: (block, first entry, end entry, stencil-column mask) — one load
+  // instead of blk_order → col_ptr; mask bit p: grid column BL·g + 1 + p holds stencil nodes (the
+  // sparse apply's inverse reads only those spectral rows, so the sweep stores only those)
+  std::vector<uint8_t> scol(N + 1, 0);
+  for (int u = 0; u < S.nsn; ++u) scol[S.sn_i[u]] = 1;
+  S.blk_meta.resize(4 * (size_t)P);
   for (int kk = 0; kk < P; ++kk) {
     const int gg = S.blk_order[kk], c0 = BL * gg + 1, ncol = gg < P - 1 ? BL : LB;
-    S.blk_meta[3 * kk] = gg;
-    S.blk_meta[3 * kk + 1] = S.col_ptr[c0];
-    S.blk_meta[3 * kk + 2] = S.col_ptr[c0 + ncol];
+    int msk = 0;
+    for (int p = 0; p < LB; ++p) msk |= (int)scol[c0 + p] << p;
+    S.blk_meta[4 * kk] = gg;
+    S.blk_meta[4 * kk + 1] = S.col_ptr[c0];
+    S.blk_meta[4 * kk + 2] = S.col_ptr[c0 + ncol];
+    S.blk_meta[4 * kk + 3] = msk;
   }
   S.holes.clear();
   if (S.kappa == 0.0)

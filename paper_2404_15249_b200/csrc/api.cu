@@ -312,6 +312,7 @@ void layout3(kfbi_ctx* c, Arena& A) {
   T.max_plane_irr = S.max_plane_irr;
   T.irr_row_ptr = A.table(S.irr_row_ptr); T.zrow_id = A.table(S.zrow_id); T.zrow_ptr = A.table(S.zrow_ptr);
   T.znode_b = A.table(S.znode_b); T.nzrow = (int)S.zrow_id.size(); T.zplane_ptr = A.table(S.zplane_ptr);
+  T.plane_flags = A.table(S.plane_flags);
   T.world = c->world; T.L3 = S.L3;
   T.q_lo[0] = 0; T.q_hi[0] = S.nq; T.q_lo[1] = T.q_hi[1] = T.q_lo[2] = T.q_hi[2] = S.nq;
   T.n_lo = 0; T.n_hi = S.nirr;
@@ -734,7 +735,7 @@ void apply_KD3(kfbi_ctx* c, const double* phi, double* out, cudaStream_t s) {
   for (int r : my_ranks(c)) {
     const DevTables3 Ts = slab3(c, r);
     launch_sparse3(Ts, 0, c->corr, nullptr, 1.0, c->work, s);
-    launch_sweep3(Ts, c->work, c->zfirst, c->fsep, s);
+    launch_sweep3(Ts, c->work, c->zfirst, c->fsep, s, true);
   }
   reduced3_dist(c, s);
   interp3_dist(c, phi, nullptr, out, s);
@@ -1357,7 +1358,7 @@ kfbi_status kfbi_profile_apply(kfbi_ctx* c, const double* d_phi, double* d_out, 
       ck(cudaEventRecord(ev[2], s), "rec");
       launch_sparse3(T3, 0, c->corr, nullptr, 1.0, c->work, s);
       ck(cudaEventRecord(ev[3], s), "rec");
-      launch_sweep3(T3, c->work, c->zfirst, c->fsep, s);
+      launch_sweep3(T3, c->work, c->zfirst, c->fsep, s, true);
       launch_reduced3(T3, c->zfirst, c->fsep, c->hsep, s);
       ck(cudaEventRecord(ev[4], s), "rec");
       launch_sparse3(T3, 1, c->work, c->hsep, sc, c->work2, s);

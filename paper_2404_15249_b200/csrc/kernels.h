@@ -121,7 +121,9 @@ void launch_sparse3(const DevTables3& T, int which, const double* src, const dou
 void launch_dst_rows3(const DevTables3& T, int mode, double* work, const double* hsep, double scale, double* out,
                       cudaStream_t s, const double* src = nullptr, const double* corr = nullptr);
 void launch_transpose3(const DevTables3& T, double* work, cudaStream_t s);
-void launch_sweep3(const DevTables3& T, double* work, double* zB, double* zA, cudaStream_t s);
+// sparse: the source came from k_fwd3s (planes without irregular nodes are zero and not written; the
+// planes the y-inverse does not read are not stored)
+void launch_sweep3(const DevTables3& T, double* work, double* zB, double* zA, cudaStream_t s, bool sparse = false);
 void launch_reduced3(const DevTables3& T, const double* zB, const double* zA, double* hsep, cudaStream_t s);
 // multi-GPU level-2 split of the 3D reduced system (slab = P/world blocks), mode-partitioned: the slab's
 // interior separators → hsep and its 4 rows per mode in chunk-major layout seg[q][4][Kq]; owner T.rank

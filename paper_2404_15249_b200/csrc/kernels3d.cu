@@ -310,6 +310,7 @@ __global__ void __launch_bounds__(256, 2) k_fwd3s(DevTables3 T, const double* __
   extern __shared__ double2 smz[];
   const double2* __restrict__ tw = reinterpret_cast<const double2*>(T.tw);
   const int i = blockIdx.y + T.i_lo;
+  if (!(T.plane_flags[i] & 1)) return;   // no irregular node in the plane: k_sweep3 reads it as zero
   __shared__ int s_ptr[N + 1];
   __shared__ double s_q[N / 2 + 1];   // quarter-wave sin(π r/N): staging rotations from smem, not L1/L2
   for (int r = threadIdx.x; r <= N / 2; r += NTHR) s_q[r] = T.sin_tab[r];
@@ -443,6 +444,7 @@ __global__ void __launch_bounds__(256, KFBI_INV3Y_MINB) k_inv3y(DevTables3 T, co
   const size_t m0 = (size_t)(l0 + rl) * N;
   __shared__ int16_t s_row[N];   // visible after the barrier below
   const int w0 = T.zplane_ptr[i - 1], nn = T.zplane_ptr[i] - w0;
+  if (nn == 0) return;   // no stencil row in the plane (CTA-uniform, before any barrier)
   for (int w = threadIdx.x; w < nn; w += NTHR) s_row[w] = (int16_t)(T.zrow_id[w0 + w] - (i - 1) * N);
   load_fixed_row<N>(T, spec, hsep, i, m0, z, tid);
   __syncwarp();
@@ -564,7 +566,7 @@ __global__ void k_transpose3(int N, double* work) {
 
 // A5 (3D): per mode m, all P blocks of BL−1 rows in turn; pivots in registers
 __global__ void __launch_bounds__(256) k_sweep3(DevTables3 T, double* spec, double* __restrict__ zB,
-                                                double* __restrict__ zA) {
+                                                double* __restrict__ zA, bool sparse) {
   const int N = T.N, P = T.P;
   const size_t K = (size_t)N * N;
   const size_t m = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -584,17 +586,21 @@ __global__ void __launch_bounds__(256) k_sweep3(DevTables3 T, double* spec, doub
   for (int g = T.b_lo; g < T.b_hi; ++g) {
     double y[LB];
 #pragma unroll
-    for (int p = 0; p < LB; ++p) {
-      const double r = spec[(size_t)(BL * g + p) * K + m];
+    for (int p = 0; p < LB; ++p) {   // plane-uniform branches (flags of grid plane BL·g + p + 1)
+      const double r = sparse && !(T.plane_flags[BL * g + p + 1] & 1) ? 0.0 : spec[(size_t)(BL * g + p) * K + m];
       y[p] = p ? fma(-y[p - 1], ic[p - 1], r) : r;
     }
     y[LB - 1] *= ic[LB - 1];
 #pragma unroll
     for (int p = LB - 2; p >= 0; --p) y[p] = (y[p] - y[p + 1]) * ic[p];
 #pragma unroll
-    for (int p = 0; p < LB; ++p) spec[(size_t)(BL * g + p) * K + m] = y[p];
+    for (int p = 0; p < LB; ++p)
+      if (!sparse || (T.plane_flags[BL * g + p + 1] & 2)) spec[(size_t)(BL * g + p) * K + m] = y[p];
     zB[(size_t)g * K + m] = y[0];
-    if (g < P - 1) zA[(size_t)g * K + m] = spec[(size_t)(BL * g + LB) * K + m] - y[LB - 1];
+    if (g < P - 1) {
+      const double sep = sparse && !(T.plane_flags[BL * g + LB + 1] & 1) ? 0.0 : spec[(size_t)(BL * g + LB) * K + m];
+      zA[(size_t)g * K + m] = sep - y[LB - 1];
+    }
   }
 }
 
@@ -872,9 +878,9 @@ void launch_transpose3(const DevTables3& T, double* work, cudaStream_t s) {
   ++g_launches;
   k_transpose3<<<grid, dim3(32, 8), 0, s>>>(T.N, work + (size_t)(T.i_lo - 1) * T.N * T.N);
 }
-void launch_sweep3(const DevTables3& T, double* work, double* zB, double* zA, cudaStream_t s) {
+void launch_sweep3(const DevTables3& T, double* work, double* zB, double* zA, cudaStream_t s, bool sparse) {
   ++g_launches;
-  k_sweep3<<<cdiv3((long)T.N * T.N, 256), 256, 0, s>>>(T, work, zB, zA);
+  k_sweep3<<<cdiv3((long)T.N * T.N, 256), 256, 0, s>>>(T, work, zB, zA, sparse);
 }
 void launch_reduced3(const DevTables3& T, const double* zB, const double* zA, double* hsep, cudaStream_t s) {
   if (T.P < 2) return;

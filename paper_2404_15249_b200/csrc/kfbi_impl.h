@@ -179,6 +179,7 @@ struct Setup3 {
   int max_plane_irr = 0;
   std::vector<int32_t> zrow_id, zrow_ptr, znode_b;   // distinct stencil nodes grouped by grid row
   std::vector<int32_t> zplane_ptr;                   // N: zrow_id[zplane_ptr[i−1] .. zplane_ptr[i]) lie in plane i
+  std::vector<uint8_t> plane_flags;                  // N+1: bit 0 irregular nodes in plane i, bit 1 stencil rows
   // multi-GPU level-2 split of the reduced system (world > 1): slabs of P/world blocks hold
   // L3 = P/world − 1 interior separators each (pivots rinv3, spike z3r: L3 × K), the world − 1 slab
   // separators solve tridiag(red3_a, red3_b, red3_a) per mode after the exchange
@@ -209,6 +210,7 @@ struct DevTables3 {
   const double* tw;   // 2N × (cos, sin)
   const int32_t *irr_row_ptr, *zrow_id, *zrow_ptr, *znode_b;
   const int32_t* zplane_ptr;   // per plane, the rows the z-evaluation reads (the y-inverse writes only those)
+  const uint8_t* plane_flags;  // per grid plane: bit 0 non-zero sparse source, bit 1 read by the y-inverse
   const int16_t* irr_row_perm;
   const int32_t* irr_row_nheavy;
   int max_plane_irr;

@@ -395,6 +395,12 @@ void build_setup3(Setup3& S, const kfbi_grid* g, const kfbi_boundary* b, const k
     for (int i = 1; i <= N; ++i)
       S.zplane_ptr[i - 1] = (int32_t)(std::lower_bound(S.zrow_id.begin(), S.zrow_id.end(), (i - 1) * N) -
                                       S.zrow_id.begin());
+    // per grid plane i ∈ [1, N): bit 0 the sparse forward source is non-zero (irregular nodes in the
+    // plane), bit 1 the y-inverse reads the plane (stencil rows): the sparse K_D apply skips the rest
+    S.plane_flags.assign(N + 1, 0);
+    for (int i = 1; i < N; ++i)
+      S.plane_flags[i] = (uint8_t)((S.irr_row_ptr[(size_t)i * N] > S.irr_row_ptr[(size_t)(i - 1) * N] ? 1 : 0) |
+                                   (S.zplane_ptr[i] > S.zplane_ptr[i - 1] ? 2 : 0));
   }
 
   // fast-solver tables: modes m = ll·N + kk (DST along z → ll, along y → kk), tridiagonal along x

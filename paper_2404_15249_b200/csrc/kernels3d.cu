@@ -565,8 +565,12 @@ __global__ void k_transpose3(int N, double* work) {
 }
 
 // A5 (3D): per mode m, all P blocks of BL−1 rows in turn; pivots in registers
-__global__ void __launch_bounds__(256) k_sweep3(DevTables3 T, double* spec, double* __restrict__ zB,
-                                                double* __restrict__ zA, bool sparse) {
+#ifndef KFBI_SWEEP3_SPLIT
+#define KFBI_SWEEP3_SPLIT 4
+#endif
+constexpr int kSweep3Threads = 128;
+__global__ void __launch_bounds__(kSweep3Threads) k_sweep3(DevTables3 T, double* spec, double* __restrict__ zB,
+                                                          double* __restrict__ zA, bool sparse) {
   const int N = T.N, P = T.P;
   const size_t K = (size_t)N * N;
   const size_t m = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -583,24 +587,35 @@ __global__ void __launch_bounds__(256) k_sweep3(DevTables3 T, double* spec, doub
       ic[p] = 1.0 / c;
     }
   }
-  for (int g = T.b_lo; g < T.b_hi; ++g) {
-    double y[LB];
+  // the next block's LB source planes and its separator plane are loaded while this block is solved
+  // and stored (software pipelining: twice the loads in flight per thread)
+  auto load = [&](int g, double (&x)[BL]) {
 #pragma unroll
-    for (int p = 0; p < LB; ++p) {   // plane-uniform branches (flags of grid plane BL·g + p + 1)
-      const double r = sparse && !(T.plane_flags[BL * g + p + 1] & 1) ? 0.0 : spec[(size_t)(BL * g + p) * K + m];
-      y[p] = p ? fma(-y[p - 1], ic[p - 1], r) : r;
+    for (int p = 0; p < BL; ++p) {   // plane-uniform branches (flags of grid plane BL·g + p + 1)
+      const bool live = (p < LB || g < P - 1) && !(sparse && !(T.plane_flags[BL * g + p + 1] & 1));
+      x[p] = live ? __ldcs(spec + (size_t)(BL * g + p) * K + m) : 0.0;
     }
+  };
+  // blockIdx.y: a contiguous share of the slab's blocks (more, shorter CTAs: a smaller last wave)
+  const int nb = T.b_hi - T.b_lo;
+  const int g0 = T.b_lo + (int)((long)nb * blockIdx.y / gridDim.y), g1 = T.b_lo + (int)((long)nb * (blockIdx.y + 1) / gridDim.y);
+  double nx[BL];
+  if (g0 < g1) load(g0, nx);
+  for (int g = g0; g < g1; ++g) {
+    double y[BL];
+#pragma unroll
+    for (int p = 0; p < BL; ++p) y[p] = nx[p];
+    if (g + 1 < g1) load(g + 1, nx);
+#pragma unroll
+    for (int p = 1; p < LB; ++p) y[p] = fma(-y[p - 1], ic[p - 1], y[p]);
     y[LB - 1] *= ic[LB - 1];
 #pragma unroll
     for (int p = LB - 2; p >= 0; --p) y[p] = (y[p] - y[p + 1]) * ic[p];
 #pragma unroll
     for (int p = 0; p < LB; ++p)
-      if (!sparse || (T.plane_flags[BL * g + p + 1] & 2)) spec[(size_t)(BL * g + p) * K + m] = y[p];
+      if (!sparse || (T.plane_flags[BL * g + p + 1] & 2)) __stcs(spec + (size_t)(BL * g + p) * K + m, y[p]);
     zB[(size_t)g * K + m] = y[0];
-    if (g < P - 1) {
-      const double sep = sparse && !(T.plane_flags[BL * g + LB + 1] & 1) ? 0.0 : spec[(size_t)(BL * g + LB) * K + m];
-      zA[(size_t)g * K + m] = sep - y[LB - 1];
-    }
+    if (g < P - 1) zA[(size_t)g * K + m] = y[LB] - y[LB - 1];
   }
 }
 
@@ -880,7 +895,7 @@ void launch_transpose3(const DevTables3& T, double* work, cudaStream_t s) {
 }
 void launch_sweep3(const DevTables3& T, double* work, double* zB, double* zA, cudaStream_t s, bool sparse) {
   ++g_launches;
-  k_sweep3<<<cdiv3((long)T.N * T.N, 256), 256, 0, s>>>(T, work, zB, zA, sparse);
+  k_sweep3<<<dim3(cdiv3((long)T.N * T.N, kSweep3Threads), std::max(1, std::min(KFBI_SWEEP3_SPLIT, T.b_hi - T.b_lo))), kSweep3Threads, 0, s>>>(T, work, zB, zA, sparse);
 }
 void launch_reduced3(const DevTables3& T, const double* zB, const double* zA, double* hsep, cudaStream_t s) {
   if (T.P < 2) return;

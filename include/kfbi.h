@@ -247,9 +247,11 @@ kfbi_status kfbi_solve(kfbi_ctx* ctx, const double* d_g, const double* d_f_grid,
                        kfbi_solve_stats* stats, void* stream);
 
 /* Algorithmic HBM bytes per launch of the two dominant kernels (model of DESIGN.md §6):
- * 2D: bytes_sweep = k_sweep (spectrum written, 8 B per block-row value), bytes_inverse =
- * k_inv_sparse (spectral columns of the stencil columns read); 3D: bytes_sweep = k_fwd3s
- * (spectrum written), bytes_inverse = k_inv3y (spectrum read + y-inverse rows written).
+ * 2D: bytes_sweep = k_sweep (the spectral rows of the block columns that hold stencil nodes
+ * written, 8 B per mode), bytes_inverse = k_inv_sparse (the spectral rows of the distinct stencil
+ * columns read); 3D: bytes_sweep = k_fwd3s (spectrum of the planes with irregular nodes written),
+ * bytes_inverse = k_inv3y (spectrum of the planes with stencil rows read + the y-inverse rows that
+ * hold stencil nodes written).
  * unknowns = interior grid points.  Host-only, no GPU work. */
 kfbi_status kfbi_apply_model(const kfbi_ctx* ctx, double* bytes_sweep, double* bytes_inverse,
                              double* unknowns);

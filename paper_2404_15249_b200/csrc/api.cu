@@ -1320,18 +1320,33 @@ kfbi_status kfbi_solve(kfbi_ctx* c, const double* d_g, const double* d_f_grid, c
 kfbi_status kfbi_apply_model(const kfbi_ctx* c, double* bytes_sweep, double* bytes_inverse, double* unknowns) {
   if (!c) return KFBI_EINVAL;
   if (c->dim == 3) {
-    const double N = c->S3.N, U = (N - 1) * (N - 1) * (N - 1), F = (N - 1) * N * N;
-    if (bytes_sweep) *bytes_sweep = 8.0 * F;         // k_fwd3s: writes the spectrum (sparse source on chip)
-    // k_inv3y: reads the spectrum, writes the y-inverse rows that hold stencil nodes
-    if (bytes_inverse) *bytes_inverse = 8.0 * F + 8.0 * N * (double)c->S3.zrow_id.size();
+    const double N = c->S3.N, U = (N - 1) * (N - 1) * (N - 1);
+    double nf = 0, ni = 0;   // planes with irregular nodes (non-zero source) / with stencil rows
+    for (size_t i = 1; i < c->S3.plane_flags.size(); ++i) {
+      nf += c->S3.plane_flags[i] & 1;
+      ni += (c->S3.plane_flags[i] >> 1) & 1;
+    }
+    // k_fwd3s: writes the spectrum of the planes with a non-zero sparse source (computed on chip)
+    if (bytes_sweep) *bytes_sweep = 8.0 * nf * N * N;
+    // k_inv3y: reads the spectrum of the planes with stencil rows, writes the y-inverse rows that hold
+    // stencil nodes
+    if (bytes_inverse) *bytes_inverse = 8.0 * ni * N * N + 8.0 * N * (double)c->S3.zrow_id.size();
     if (unknowns) *unknowns = U;
     return KFBI_OK;
   }
-  const double N = c->S.N, P = c->S.P;
-  // sweep: writes v̂ at the block rows of every mode (8 B per value); reads are on-chip
-  if (bytes_sweep) *bytes_sweep = 8.0 * (N - P) * (N - 1);
-  // sparse inverse: reads v̂ rows of the columns that hold stencil nodes
-  if (bytes_inverse) *bytes_inverse = 8.0 * (double)c->S.ocol.size() * (N - 1);
+  const double N = c->S.N;
+  // distinct grid columns holding stencil nodes; those inside ADM blocks (not separators) are the
+  // spectral rows the sparse apply's sweep stores (8 B per mode) and its inverse reads
+  std::vector<int32_t> cols(c->S.sn_i.begin(), c->S.sn_i.end());
+  std::sort(cols.begin(), cols.end());
+  cols.erase(std::unique(cols.begin(), cols.end()), cols.end());
+  double ncol = 0, nblk = 0;
+  for (int32_t i : cols) {
+    ncol += 1;
+    nblk += (i % BL) != 0;
+  }
+  if (bytes_sweep) *bytes_sweep = 8.0 * nblk * (N - 1);
+  if (bytes_inverse) *bytes_inverse = 8.0 * ncol * (N - 1);
   if (unknowns) *unknowns = (N - 1) * (N - 1);
   return KFBI_OK;
 }

@@ -66,31 +66,55 @@ __device__ __forceinline__ Jump6 jumps2d(double Phi, double Phis, double Phiss, 
 // ------------------------------------------------------------------------------ A1
 // blocks [0, nsb): one thread per control point; blocks nsb + h: the hole-completion coefficient
 // a_h = Δs_h Σ_{Γ_h} φ (reading R27) by a deterministic block reduction (saves a launch per apply)
-__global__ void k_spline(DevTables T, const double* __restrict__ phi, double* __restrict__ mk, int nsb,
+constexpr int kSplineLanes = 8;
+__global__ void k_spline(DevTables T, const double* __restrict__ phi, double* __restrict__ mk, int nh,
                          const int* __restrict__ hoff, const int* __restrict__ hcnt,
                          const double* __restrict__ hdelta, double* __restrict__ ahole) {
-  if ((int)blockIdx.x >= nsb) {
+  if ((int)blockIdx.x < nh) {   // hole blocks first: they are the longest, the spline blocks fill in
     __shared__ double scratch[32];
-    const int hh = blockIdx.x - nsb;
+    const int hh = blockIdx.x;
+    const int cnt = hcnt[hh], o = hoff[hh];
     double v[1] = {0.0};
-    for (int m = threadIdx.x; m < hcnt[hh]; m += blockDim.x) v[0] += phi[hoff[hh] + m];
+    for (int m = threadIdx.x; m < cnt; m += 4 * blockDim.x) {   // four loads in flight, summed in order
+      double x[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) x[u] = m + u * (int)blockDim.x < cnt ? phi[o + m + u * blockDim.x] : 0.0;
+#pragma unroll
+      for (int u = 0; u < 4; ++u) v[0] += x[u];
+    }
     block_reduce<1>(v, scratch);
     if (threadIdx.x == 0) ahole[hh] = hdelta[hh] * v[0];
     return;
   }
-  int m = blockIdx.x * blockDim.x + threadIdx.x;
-  if (m >= T.M) return;
-  int c = T.z_comp[m], ml = T.z_knot[m];
-  int off = T.c_off[c], Mc = T.c_M[c], nt = T.sp_ntaps[c], first = T.sp_first[c];
-  const double* b = T.sp_coef + T.sp_coef_off[c];
+  // kSplineLanes lanes per control point, each with ≤ 64 / kSplineLanes taps whose loads are all issued
+  // before the FMAs (the one-thread loop waited on one phi load per tap); a fixed xor tree sums the lanes
+  const int gt = (blockIdx.x - nh) * blockDim.x + threadIdx.x;
+  const int m = gt / kSplineLanes, sub = gt % kSplineLanes;
   double acc = 0.0;
-  int idx = (ml + first) % Mc;   // one modulo, then wrap by compare (periodic knots)
-  if (idx < 0) idx += Mc;
-  for (int r = 0; r < nt; ++r) {
-    acc = fma(b[r], phi[off + idx], acc);
-    if (++idx == Mc) idx = 0;
+  if (m < T.M) {
+    const int c = T.z_comp[m], ml = T.z_knot[m];
+    const int off = T.c_off[c], Mc = T.c_M[c], nt = T.sp_ntaps[c], first = T.sp_first[c];
+    const double* b = T.sp_coef + T.sp_coef_off[c];
+    int base = (ml + first + sub) % Mc;   // periodic knots
+    if (base < 0) base += Mc;
+    constexpr int U = 64 / kSplineLanes;
+    double bv[U], pv[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int r = sub + kSplineLanes * u;
+      bv[u] = 0.0;
+      pv[u] = 0.0;
+      if (r < nt) {
+        bv[u] = b[r];
+        pv[u] = phi[off + (base + kSplineLanes * u) % Mc];
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) acc = fma(bv[u], pv[u], acc);
   }
-  mk[m] = acc;
+#pragma unroll
+  for (int o = kSplineLanes / 2; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+  if (m < T.M && sub == 0) mk[m] = acc;
 }
 
 // ------------------------------------------------------------------------------ A2+A3
@@ -808,6 +832,32 @@ __global__ void k_interp(DevTables T, const double* __restrict__ phi, const doub
       return;
     }
   }
+  // the stencil's loads (node ids → values, weights, offsets) and the hole terms are issued before the
+  // jump chain (spline knots → φ, M → jumps), so the two dependent load chains overlap
+  int sn[6];
+  double v[6], wt[6], dx[6], dy[6];
+  bool ext[6];
+#pragma unroll
+  for (int p = 0; p < 6; ++p) {
+    const int idx = m * 6 + p;
+    sn[p] = T.st_node[idx];
+    ext[p] = T.st_ext[idx];
+    dx[p] = T.st_dx[idx];
+    dy[p] = T.st_dy[idx];
+    wt[p] = T.neumann ? T.st_wn[idx] : T.st_w[idx];   // V⁺ or ∂_n V⁺ (Neumann, R38)
+  }
+#pragma unroll
+  for (int p = 0; p < 6; ++p) {
+    KFBI_CHECK(sn[p] >= 0 && sn[p] < T.nsn, sn[p], T.nsn);
+    v[p] = vsten[sn[p]];
+    if (partial) {   // multi-GPU: only stencil nodes in the owned columns contribute (partial sum)
+      const int col = T.sn_i[sn[p]];
+      if (col < T.col_lo || col > T.col_hi) wt[p] = 0.0, v[p] = 0.0, ext[p] = false;
+    }
+  }
+  double hole = 0.0;
+  if (!partial || T.rank == 0)
+    for (int hh = 0; hh < nh; ++hh) hole = fma(ahole[hh], wg[(size_t)hh * T.M + m], hole);
   Jump6 J;
   if (jzg) {
     J.v = jzg[m * 6];
@@ -827,23 +877,13 @@ __global__ void k_interp(DevTables T, const double* __restrict__ phi, const doub
   double acc = 0.0;
 #pragma unroll
   for (int p = 0; p < 6; ++p) {
-    const int idx = m * 6 + p;
-    const int sn = T.st_node[idx];
-    KFBI_CHECK(sn >= 0 && sn < T.nsn, sn, T.nsn);
-    if (partial) {   // multi-GPU: only stencil nodes in the owned columns contribute (partial sum)
-      const int col = T.sn_i[sn];
-      if (col < T.col_lo || col > T.col_hi) continue;
-    }
-    double v = vsten[sn];
-    if (T.st_ext[idx]) {   // exterior node: shift by the jump Taylor polynomial
-      const double dx = T.st_dx[idx], dy = T.st_dy[idx];
-      v += J.v + J.vx * dx + J.vy * dy + 0.5 * J.vxx * dx * dx + J.vxy * dx * dy + 0.5 * J.vyy * dy * dy;
-    }
-    acc = fma(T.neumann ? T.st_wn[idx] : T.st_w[idx], v, acc);   // V⁺ or ∂_n V⁺ (Neumann, R38)
+    double vp = v[p];
+    if (ext[p])   // exterior node: shift by the jump Taylor polynomial
+      vp += J.v + J.vx * dx[p] + J.vy * dy[p] + 0.5 * J.vxx * dx[p] * dx[p] + J.vxy * dx[p] * dy[p] +
+            0.5 * J.vyy * dy[p] * dy[p];
+    acc = fma(wt[p], vp, acc);
   }
-  if (!partial || T.rank == 0)
-    for (int hh = 0; hh < nh; ++hh) acc = fma(ahole[hh], wg[(size_t)hh * T.M + m], acc);
-  out[m] = acc;
+  out[m] = acc + hole;
 }
 
 __global__ void k_hole_coeffs(const int* __restrict__ off, const int* __restrict__ cnt,
@@ -1325,8 +1365,8 @@ inline int cdiv(long a, long b) { return (int)((a + b - 1) / b); }
 long long g_launches = 0;
 void launch_spline(const DevTables& T, const double* phi, double* mk, cudaStream_t s, const int* hole_off,
                    const int* hole_M, const double* hole_delta, int nh, double* ahole) {
-  const int nsb = cdiv(T.M, 256);
-  { ++g_launches; k_spline<<<nsb + nh, 256, 0, s>>>(T, phi, mk, nsb, hole_off, hole_M, hole_delta, ahole); }
+  const int nsb = cdiv(T.M * kSplineLanes, 256);
+  { ++g_launches; k_spline<<<nsb + nh, 256, 0, s>>>(T, phi, mk, nh, hole_off, hole_M, hole_delta, ahole); }
 }
 
 void launch_correct(const DevTables& T, const double* phi, const double* mk, const double* fq,

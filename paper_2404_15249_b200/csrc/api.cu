@@ -213,6 +213,7 @@ void layout(kfbi_ctx* c, Arena& A) {
   T.tw = A.table(S.tw);
   T.red_a = A.table(S.red_a); T.red_b = A.table(S.red_b); T.red_invc = A.table(S.red_invc);
   T.rinv2 = A.table(S.rinv2); T.z2r = A.table(S.z2r); T.red2_a = A.table(S.red2_a); T.red2_b = A.table(S.red2_b);
+  T.red2_ci = A.table(S.red2_ci);
   T.maxe = S.maxe;
   T.mcr = S.max_col_rows;
   T.side = A.table(S.side);

@@ -420,13 +420,17 @@ __global__ void k_reduced_small(DevTables T, const double* __restrict__ zB, cons
 // thread (mode lane, segment σ) solves its BL2−1 separators locally in registers, the S−1
 // level-2 separators per mode are solved from shared memory, then each segment is fixed up
 // with the level-2 spikes (z − a h2_{σ−1} Z2_L − a h2_σ Z2_R).
-__global__ void __launch_bounds__(512) k_reduced2(DevTables T, const double* __restrict__ zB,
+#ifndef KFBI_RED2_MODES
+#define KFBI_RED2_MODES 32
+#endif
+constexpr int kRed2Modes = KFBI_RED2_MODES;   // modes per CTA (× one thread per level-2 segment)
+__global__ void __launch_bounds__(kRed2Modes * kMaxSeg) k_reduced2(DevTables T, const double* __restrict__ zB,
                                                   const double* __restrict__ zA, double* __restrict__ hsep) {
-  __shared__ double s_first[16][32], s_last[16][32], s_rs[16][32], s_h2[16][32];
-  __shared__ double s_rinv[LB2][32], s_z2r[LB2][32];   // the CTA's 32 modes of the level-2 tables
+  __shared__ double s_first[kMaxSeg][kRed2Modes], s_last[kMaxSeg][kRed2Modes], s_rs[kMaxSeg][kRed2Modes], s_h2[kMaxSeg][kRed2Modes];
+  __shared__ double s_rinv[LB2][kRed2Modes], s_z2r[LB2][kRed2Modes];   // the CTA's modes of the level-2 tables
   const int N = T.N, P = T.P, S = P / BL2;
   const int lane = threadIdx.x, sg = threadIdx.y;
-  const int k = blockIdx.x * 32 + lane + 1;
+  const int k = blockIdx.x * kRed2Modes + lane + 1;
   const bool ok = k < N;
   const int kk = ok ? k : 1;
   const double a = T.red_a[kk];
@@ -461,17 +465,20 @@ __global__ void __launch_bounds__(512) k_reduced2(DevTables T, const double* __r
   if (sg == 0 && S > 1) {
     // level-2 reduced system: tridiag(A2, B2, A2), rhs = r_s − a z_σ[L] − a z_{σ+1}[1];
     // pivots → s_rs, forward values → s_h2 (in place, per lane)
-    const double A2 = T.red2_a[kk], B2 = T.red2_b[kk];
-    double c = B2, yprev = 0.0, ciprev = 0.0;
-    for (int q = 0; q < S - 1; ++q) {
+    // pivots 1/c_q from the setup table (no divisions on the critical path), loaded up front
+    const double A2 = T.red2_a[kk];
+    double cis[kMaxSeg - 1];
+#pragma unroll
+    for (int q = 0; q < kMaxSeg - 1; ++q) cis[q] = q < S - 1 ? T.red2_ci[(size_t)q * N + kk] : 1.0;
+    double yprev = 0.0;
+#pragma unroll
+    for (int q = 0; q < kMaxSeg - 1; ++q) {
+      if (q >= S - 1) break;
       const double r = s_rs[q][lane] - a * s_last[q][lane] - a * s_first[q + 1][lane];
-      if (q) c = B2 - A2 * A2 * ciprev;
-      const double ci = 1.0 / c;
-      const double y = q ? r - A2 * yprev * ciprev : r;
-      s_rs[q][lane] = ci;
+      const double y = q ? r - A2 * yprev * cis[q - 1] : r;
+      s_rs[q][lane] = cis[q];
       s_h2[q][lane] = y;
       yprev = y;
-      ciprev = ci;
     }
     double hn = s_h2[S - 2][lane] * s_rs[S - 2][lane];
     s_h2[S - 2][lane] = hn;
@@ -1402,9 +1409,9 @@ void launch_reduced(const DevTables& T, const double* zfirst, const double* zlas
                     cudaStream_t s) {
   (void)zlast;
   if (T.P < 2) return;
-  if (T.P >= 2 * BL2 && T.P % BL2 == 0 && T.P / BL2 <= 16) {
-    dim3 blk(32, T.P / BL2);
-    { ++g_launches; k_reduced2<<<cdiv(T.N - 1, 32), blk, 0, s>>>(T, zfirst, fsep, hsep); }
+  if (T.P >= 2 * BL2 && T.P % BL2 == 0 && T.P / BL2 <= kMaxSeg) {
+    dim3 blk(kRed2Modes, T.P / BL2);
+    { ++g_launches; k_reduced2<<<cdiv(T.N - 1, kRed2Modes), blk, 0, s>>>(T, zfirst, fsep, hsep); }
   } else {
     { ++g_launches; k_reduced_small<<<cdiv(T.N - 1, 64), 64, 0, s>>>(T, zfirst, fsep, hsep); }
   }

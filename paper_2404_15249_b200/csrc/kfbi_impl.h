@@ -23,6 +23,7 @@ constexpr int LB = BL - 1;
 // level-2 blocks of BL2−1 separators around level-2 separators (nested arrowhead).
 constexpr int BL2 = 32;
 constexpr int LB2 = BL2 - 1;
+constexpr int kMaxSeg = 16;   // level-2 segments per mode handled by k_reduced2 (P ≤ kMaxSeg · BL2)
 // most stencil rows in one k_inv_sparse work item: longer columns are split by setup (load balance:
 // rows per column reach ~200 at C3 and the cap of a few hundred on the 8192² star, mean 12)
 constexpr int kMaxColRows = 64;
@@ -130,6 +131,7 @@ struct Setup {
   std::vector<double> red_invc;      // (P−1) × N
   std::vector<double> rinv2, z2r;    // LB2 × N: level-2 block pivots / spike
   std::vector<double> red2_a, red2_b;  // N: level-2 reduced system coefficients
+  std::vector<double> red2_ci;         // (kMaxSeg − 1) × N: level-2 pivots 1/c_q
   int maxe = 1;                      // max sparse entries per sweep work item
   int max_col_rows = 1;              // max stencil rows in one grid column
   // holes (κ = 0 completion, reading R27)
@@ -255,7 +257,7 @@ struct DevTables {
   // fast solver
   const double *sin_tab, *dk, *invc, *zr, *red_a, *red_b, *red_invc;
   const double* tw;   // 2N × (cos, sin)(π m/N)
-  const double *rinv2, *z2r, *red2_a, *red2_b;
+  const double *rinv2, *z2r, *red2_a, *red2_b, *red2_ci;
   int maxe;
   const int8_t* side;
   const int32_t* sn_i;

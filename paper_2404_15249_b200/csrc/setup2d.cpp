@@ -597,6 +597,7 @@ void build_setup(Setup& S, const kfbi_grid* g, const kfbi_boundary* b, const kfb
   S.z2r.assign((size_t)LB2 * N, 0.0);
   S.red2_a.assign(N, 0.0);
   S.red2_b.assign(N, 0.0);
+  S.red2_ci.assign((size_t)(kMaxSeg - 1) * N, 1.0);
 #pragma omp parallel for schedule(static)
   for (int k = 1; k < N; ++k) {
     const double a = S.red_a[k], bb = S.red_b[k];
@@ -614,6 +615,13 @@ void build_setup(Setup& S, const kfbi_grid* g, const kfbi_boundary* b, const kfb
     }
     S.red2_a[k] = -a * a * S.z2r[k];
     S.red2_b[k] = bb - 2.0 * a * a * S.z2r[(size_t)(LB2 - 1) * N + k];
+    // level-2 pivots 1/c_q of tridiag(A2, B2, A2) (c_0 = B2, c_q = B2 − A2² / c_{q−1}), q < kMaxSeg − 1
+    const double A2 = S.red2_a[k], B2 = S.red2_b[k];
+    double c2 = B2;
+    for (int q = 0; q < kMaxSeg - 1; ++q) {
+      if (q) c2 = B2 - A2 * A2 * S.red2_ci[(size_t)(q - 1) * N + k];
+      S.red2_ci[(size_t)q * N + k] = 1.0 / c2;
+    }
   }
   // spectral mode order: quad {t, N−t, N/2−t, N/2+t} at positions 4t..4t+3 (t ∈ [1, N/4)), and
   // {0, N/2, N/4, 3N/4} at 0..3, so that the inverse transform loads a quad as two 16-byte words
@@ -638,6 +646,7 @@ void build_setup(Setup& S, const kfbi_grid* g, const kfbi_boundary* b, const kfb
     perm(S.z2r, LB2, 0.0);
     perm(S.red2_a, 1, 0.0);
     perm(S.red2_b, 1, 1.0);
+    perm(S.red2_ci, kMaxSeg - 1, 1.0);
   }
   // largest number of sparse corrections staged by one sweep work item (block + separator), and the
   // blocks by descending count (the sweep's work order)

@@ -344,7 +344,7 @@ void layout3(kfbi_ctx* c, Arena& A) {
   c->work2 = A.take_rows<double>(npl * K, pl0 * K);
   c->zfirst = A.take<double>(P * K);
   c->corr = A.take<double>(std::max(S.nirr, 1));
-  c->fsep = A.take<double>(P * K);   // P rows (not P − 1): equal all-gather slices per rank
+  c->fsep = A.take<double>(P * K);   // zA: one row per block (the last block's is unused)
   c->hsep = A.take<double>(std::max<size_t>(P - 1, 1) * K);
   c->dphi = A.take<double>(5 * M);
   c->parts = A.take<double>((size_t)std::max(c->world, 1) * M);
@@ -674,9 +674,10 @@ void interp3_dist(kfbi_ctx* c, const double* phi, const double* fz, double* out,
 }
 // K_D (the GMRES operator): sparse source, sparse read-out — no dense z-direction transforms
 // Multi-GPU: each rank runs the sparse forward, the block sweeps, the y-inverse
-// and the z-evaluation of its own slab; the block end values (zB, zA: P/world rows each) are
-// all-gathered, every rank solves the (cheap) reduced system for all modes, and the interpolation
-// partial sums (plane owner contributes) are all-reduced.  rank = −1 emulates all slabs in one ctx.
+// and the z-evaluation of its own slab; the reduced system goes through reduced3_dist (below: slab-
+// local elimination, mode-partitioned level-2 solve over two grouped all-to-alls), and the
+// interpolation partial sums (plane owner contributes) are all-reduced.  rank = −1 emulates all slabs
+// in one ctx.
 // reduced (separator) system of the sweeps just run.  world > 1: every slab eliminates its interior
 // separators and publishes 4 values per mode (first, last, its boundary separator's zA, its first
 // block's zB); the level-2 system of the world − 1 slab separators is solved mode-partitioned (owner q

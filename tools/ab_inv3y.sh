@@ -1,4 +1,5 @@
 # A/B of the y-inverse: plane-pair k_inv3yp (default build) vs one plane per CTA (-DKFBI_INV3Y_SINGLE),
+# (the plane-pair variant was removed after this A/B: DESIGN.md §7, k_inv3y)
 # the 3D GPU tests (incl. the full-size C5 apply) on the default
 export PYTHONPATH=.
 for v in pair single; do

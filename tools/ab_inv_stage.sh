@@ -1,4 +1,5 @@
 # A/B of k_inv_sparse: staged spectral row (bulk copy, default) vs unstaged (KFBI_INV_STAGE=0),
+# (the staged variant was removed after this A/B: DESIGN.md §7 "Round 2 experiments")
 # the 2D GPU tests on both
 export PYTHONPATH=.
 for v in 1 0; do

@@ -281,6 +281,7 @@ def main():
     # u_h is valid on Ω); slab-sharded runs move each rank's node slab of f and u.
     pin = lambda a: torch.tensor(a, dtype=torch.float64).pin_memory()
     compact = not sharded
+    omega_io = compact and prob.dim == 2   # kfbi_solve_opts.omega_io (2D single-context grids)
     if compact:
         omask = k.node_mask().reshape(-1).astype(bool)
         n_out = int(omask.sum())
@@ -298,6 +299,10 @@ def main():
         of u gathered after; returns the device array the host copy reads.  async_final: the solve
         returns with its final field still running on the stream (the serving loop's next host work
         overlaps it; every later use is stream-ordered)."""
+        if compact and omega_io:   # 2D: the solve reads f and writes u as Ω-node values itself
+            u, _, st_ = k.solve(gd, fgd, fqd, fzd, u=u_c if b is None else u_cs[b], method=args.method,
+                                async_final=async_final, omega_io=True)
+            return u
         if compact:
             u, _, st_ = k.solve(gd, k.scatter_omega(fgd, grid=fg_full[b]), fqd, fzd, u=u, method=args.method,
                                 async_final=async_final)
@@ -437,7 +442,9 @@ def main():
                 "d2h_bytes_per_step": d2h, "s_per_step": t_e2e_pipe, "steps": n_e2e,
                 "mode": "pipelined serving loop: H2D of step k+1 and D2H of step k overlap the solves "
                         "(two copy streams, double-buffered); timed from the first upload to the last download"
-                        + ("; f and u cross PCIe as their Omega-node values (kfbi_scatter_omega before and "
+                        + ("; f and u cross PCIe as their Omega-node values, which kfbi_solve reads and writes "
+                           "directly (opts.omega_io)" if omega_io else
+                           "; f and u cross PCIe as their Omega-node values (kfbi_scatter_omega before and "
                            "kfbi_gather_omega after each solve, inside the timed region)" if compact else ""),
                 "serial": {"value": copies * U * n_app / t_e2e, "s_per_step": t_e2e,
                            "mode": "H2D, solve, D2H back to back every step"}},

@@ -100,6 +100,9 @@ struct kfbi_ctx {
   std::vector<int32_t> om_seg;   // Ω nodes before each 32-node segment of each row
   const int64_t* d_om_ptr = nullptr;
   const int32_t* d_om_seg = nullptr;
+  std::vector<int32_t> om_row32;   // 2D: Ω nodes before each grid row (N + 2)
+  std::vector<uint32_t> om_info;   // 2D: per row, the padded segment bitmasks then the in-row counts
+  bool io_compact = false;         // inside kfbi_solve with opts.omega_io: f and u are Ω-compact
   const int8_t* d_side = nullptr;
   int64_t om_rows = 0, om_width = 0;
   double* hcol_host = nullptr;   // host-mapped (written by k_copy, read after a stream sync)
@@ -221,6 +224,21 @@ void layout(kfbi_ctx* c, Arena& A) {
   c->d_om_ptr = A.table(c->om_ptr);
   c->d_om_seg = A.table(c->om_seg);
   c->d_side = T.side;
+  {   // Ω-compact rows for the dense forward / final field (kfbi_solve_opts.omega_io)
+    const int64_t W = (int64_t)S.N + 1, nseg = (W + 31) / 32, nsegp = (nseg + 3) / 4 * 4;
+    c->om_row32.assign(c->om_ptr.begin(), c->om_ptr.end());
+    c->om_info.assign((size_t)W * 2 * nsegp, 0u);
+    for (int64_t r = 0; r < W; ++r) {
+      uint32_t* info = c->om_info.data() + (size_t)r * 2 * nsegp;
+      for (int64_t j = 0; j < W; ++j)
+        if (S.side[(size_t)(r * W + j)]) info[j >> 5] |= 1u << (j & 31);
+      for (int64_t g = 0; g < nseg; ++g)
+        info[nsegp + g] = (uint32_t)(c->om_seg[r * nseg + g] - c->om_ptr[r]);
+    }
+    T.om_row = A.table(c->om_row32);
+    T.om_info = A.table(c->om_info);
+    T.om_nsegp = (int)nsegp;
+  }
   c->row_omega.assign(S.N + 1, 0);
   for (int i = 0; i <= S.N; ++i) c->row_omega[i] = c->om_ptr[i + 1] > c->om_ptr[i] ? 1 : 0;
   T.row_omega = A.table(c->row_omega);
@@ -543,7 +561,8 @@ void interp2(kfbi_ctx* c, const double* phi, const double* fz, const double* jz,
 }
 
 void dst_forward2(kfbi_ctx* c, const double* fgrid, bool mask, const BumpParams& bp, double* dst, cudaStream_t s) {
-  for (int r : my_ranks(c)) launch_dst_forward(slab(c, r), fgrid, mask, bp, dst, s);
+  const bool compact = c->io_compact && fgrid != nullptr;   // world = 1 only (kfbi_solve checks)
+  for (int r : my_ranks(c)) launch_dst_forward(slab(c, r), fgrid, mask, bp, dst, s, compact);
 }
 
 void apply_KD2(kfbi_ctx* c, const double* phi, double* out, cudaStream_t s) {
@@ -603,8 +622,8 @@ void final_field2(kfbi_ctx* c, const double* phi, const double* fgrid, const dou
   launch_spline(T, phi, c->mk, s);
   for (int r : my_ranks(c)) launch_correct(slab(c, r), phi, c->mk, fq, nullptr, c->cval, s);
   spectral2(c, c->cval, D, s);
-  for (int r : my_ranks(c)) launch_inverse_dense(slab(c, r), c->spec, c->hsep, u, s);   // owned columns
-  if (c->local_io) return;   // the box rows 0 and N belong to no slab
+  for (int r : my_ranks(c)) launch_inverse_dense(slab(c, r), c->spec, c->hsep, u, s, c->io_compact);   // owned columns
+  if (c->local_io || c->io_compact) return;   // the box rows 0 and N belong to no slab / hold no Ω node
   const size_t W = (size_t)T.N + 1;
   ck(cudaMemsetAsync(u, 0, W * sizeof(double), s), "memset");
   ck(cudaMemsetAsync(u + (size_t)T.N * W, 0, W * sizeof(double), s), "memset");
@@ -1203,8 +1222,10 @@ kfbi_status kfbi_solve(kfbi_ctx* c, const double* d_g, const double* d_f_grid, c
   if (!c || !d_g || !d_u) return fail(c, KFBI_EINVAL, "null pointer");
   if ((d_f_grid == nullptr) != (d_f_isect == nullptr) || (d_f_grid == nullptr) != (d_f_ctrl == nullptr))
     return fail(c, KFBI_EINVAL, "f_grid, f_isect, f_ctrl must all be given or all NULL");
-  kfbi_solve_opts o{1e-8, 30, 50, KFBI_GMRES, 1.0, 0};
+  kfbi_solve_opts o{1e-8, 30, 50, KFBI_GMRES, 1.0, 0, 0};
   if (opts) o = *opts;
+  if (o.omega_io && (c->dim != 2 || c->local_io || c->world != 1))
+    return fail(c, KFBI_EUNSUPPORTED, "omega_io: 2D single-context grids only");
   if (o.restart < 1 || o.restart > kMaxRestart || o.max_restarts < 1 || !(o.tol > 0) || o.method < 0 ||
       o.method > KFBI_BICGSTAB || (o.method == KFBI_RICHARDSON && !(o.gamma > 0 && o.gamma <= 1)))
     return fail(c, KFBI_EINVAL, "bad solve options");
@@ -1213,6 +1234,11 @@ kfbi_status kfbi_solve(kfbi_ctx* c, const double* d_g, const double* d_f_grid, c
   bool converged = false;
   KFBI_TRY(c)
   need_ws(c);
+  struct CompactIO {   // f and u Ω-compact for this solve only (reset on every exit path)
+    kfbi_ctx* c;
+    CompactIO(kfbi_ctx* c_, bool on) : c(c_) { c->io_compact = on; }
+    ~CompactIO() { c->io_compact = false; }
+  } compact_io(c, o.omega_io != 0);
   if (c->local_io) {   // the rank's node slab: the kernels index with global node numbers
     const size_t row = c->dim == 3 ? (size_t)(c->S3.N + 1) * (c->S3.N + 1) : (size_t)c->S.N + 1;
     if (d_f_grid) d_f_grid -= (size_t)c->loc_off[0] * row;

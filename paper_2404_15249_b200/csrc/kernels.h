@@ -39,8 +39,9 @@ struct BumpParams {
   double cx[4], cy[4], rad[4];
   const double* a;   // device, nh coefficients
 };
+// compact: fgrid holds f at the Ω nodes only (row-major ranks, kfbi_omega_count values; mask implied)
 void launch_dst_forward(const DevTables& T, const double* fgrid, bool mask, const BumpParams& bp,
-                        double* spec, cudaStream_t s);
+                        double* spec, cudaStream_t s, bool compact = false);
 // dense spectral source of a sweep: f̂ = base + Σ_{h<nb} coef[h] · bump[h·ldb] (any of them may be
 // absent; base may alias the sweep's output). The final field's linear combination (R27) is formed
 // as it is read instead of in a separate pass over the grid.
@@ -65,8 +66,9 @@ void launch_reduced(const DevTables& T, const double* zfirst, const double* zlas
 void launch_inverse_sparse(const DevTables& T, const double* spec, const double* hsep, double* vsten,
                            cudaStream_t s);
 // A6 dense: inverse DST-I of every row into a full (N+1)^2 grid (fix-up fused).
+// compact: vgrid receives the field at the Ω nodes only (row-major ranks)
 void launch_inverse_dense(const DevTables& T, const double* spec, const double* hsep, double* vgrid,
-                          cudaStream_t s);
+                          cudaStream_t s, bool compact = false);
 // hole coefficients a_h = Δ_h Σ_{m∈Γ_h} φ_m (reading R27), one block per hole
 void launch_hole_coeffs(const DevTables& T, const int* hole_off, const int* hole_M, const double* hole_delta,
                         int nh, const double* phi, double* a, cudaStream_t s);

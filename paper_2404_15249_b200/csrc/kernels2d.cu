@@ -959,7 +959,13 @@ __device__ __forceinline__ double dense_src(const DevTables& T, const double* __
   double v = 0.0;
   if (j == 0) return v;
   const size_t idx = (size_t)i * (N + 1) + j;
-  if (src && (!mask_omega || T.side[idx])) v = src[idx];
+  if (src && mask_omega == 2) {   // Ω-compact input: the node's rank among the Ω nodes (row-major)
+    const uint32_t* info = T.om_info + (size_t)i * 2 * T.om_nsegp;
+    const uint32_t bits = info[j >> 5];
+    if ((bits >> (j & 31)) & 1u) v = src[T.om_row[i] + (int)info[T.om_nsegp + (j >> 5)] + __popc(bits & ((1u << (j & 31)) - 1u))];
+  } else if (src && (!mask_omega || T.side[idx])) {
+    v = src[idx];
+  }
   if (bp.nh) {
     const double x = T.lo + i * T.h, yy = T.lo + j * T.h;
     for (int hh = 0; hh < bp.nh; ++hh) {
@@ -979,7 +985,8 @@ struct DenseCfg {
   // while the current row is transformed
   static constexpr bool STAGE = RPC == 1;
   static constexpr int STAGE_D = N + 2;            // doubles: one row (+1 for 8-byte misalignment)
-  static constexpr int STAGE_B = N + 1 + 32;       // bytes of the Ω-mask row (+ alignment)
+  static constexpr int STAGE_B = N + 1 + 32;       // bytes of the Ω-mask row (+ alignment), or the
+                                                   // Ω-compact row's segment bits and counts (2·nsegp words)
   static constexpr size_t smem(bool staged) {
     return (size_t)RPC * ZS * 16 + (staged ? (size_t)STAGE_D * 8 + STAGE_B + 16 : 0);
   }
@@ -1002,10 +1009,11 @@ __device__ __forceinline__ void bulk_load(uint64_t* bar, void* dst0, const void*
                                           const void* src1, uint32_t n1) {
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");   // earlier generic reads of the buffer
   asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(n0 + n1) : "memory");
-  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-                   smem_u32(dst0)),
-               "l"(src0), "r"(n0), "r"(smem_u32(bar))
-               : "memory");
+  if (n0)
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                     smem_u32(dst0)),
+                 "l"(src0), "r"(n0), "r"(smem_u32(bar))
+                 : "memory");
   if (n1)
     asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
                      smem_u32(dst1)),
@@ -1037,8 +1045,18 @@ __global__ void __launch_bounds__(DenseCfg<N>::NTHR, 1) k_dst_dense2(DevTables T
   const bool staged = C::STAGE && MODE == 0 && src != nullptr;
   const int step = gridDim.x * RPC;
   // bulk copies of row `in`'s primary input; returns nothing, offsets recomputed by the reader
+  const bool compact = mask_omega == 2;   // MODE 0: src holds f at the Ω nodes only (row-major ranks)
   auto issue = [&](int in) {
-    if (MODE == 0) {
+    if (MODE == 0 && compact) {
+      // the row's Ω values are contiguous: [om_row[in], om_row[in + 1]); the copy is rounded down to
+      // whole 16-byte words (the last value, if cut, is read from global memory), plus the row's
+      // segment bits and counts
+      const char* a = reinterpret_cast<const char*>(src + T.om_row[in]);
+      const char* al = reinterpret_cast<const char*>(reinterpret_cast<uintptr_t>(a) & ~uintptr_t(15));
+      const uint32_t n0 = (uint32_t)(((a - al) + (size_t)(T.om_row[in + 1] - T.om_row[in]) * 8) & ~size_t(15));
+      const uint32_t* info = T.om_info + (size_t)in * 2 * T.om_nsegp;
+      bulk_load(&bar, stage, al, n0, smask, info, (uint32_t)T.om_nsegp * 8u);
+    } else if (MODE == 0) {
       const char* a = reinterpret_cast<const char*>(src + (size_t)in * (N + 1));
       const char* al = reinterpret_cast<const char*>(reinterpret_cast<uintptr_t>(a) & ~uintptr_t(15));
       const uint32_t n0 = (uint32_t)((((a - al) + (N + 1) * 8) + 15) & ~15);
@@ -1067,7 +1085,11 @@ __global__ void __launch_bounds__(DenseCfg<N>::NTHR, 1) k_dst_dense2(DevTables T
   if (!staged) {
     const int in = i + step;
     if (in <= T.col_hi && src) {
-      if (MODE == 0) {
+      if (MODE == 0 && compact) {
+        const double* row = src + T.om_row[in];
+        for (int o = 16 * tid; o < T.om_row[in + 1] - T.om_row[in]; o += 16 * NTH)
+          asm volatile("prefetch.global.L2 [%0];" ::"l"(row + o));
+      } else if (MODE == 0) {
         const double* row = src + (size_t)in * (N + 1);
         for (int o = 16 * tid; o <= N; o += 16 * NTH) asm volatile("prefetch.global.L2 [%0];" ::"l"(row + o));
         if (mask_omega && tid < (N + 128) / 128)
@@ -1086,7 +1108,31 @@ __global__ void __launch_bounds__(DenseCfg<N>::NTHR, 1) k_dst_dense2(DevTables T
   }
   double2 fp[8];
   if (MODE == 0) {
-    if (staged) {   // the row and its mask from shared memory (8-byte / byte offsets of the aligned copies)
+    if (staged && compact) {   // Ω values from the staged compact row (segment bits / counts staged too)
+      const int r0 = T.om_row[i], nv = T.om_row[i + 1] - r0;
+      const int off = (int)((reinterpret_cast<uintptr_t>(src + r0) & 15) >> 3);
+      const int nst = ((off + nv) & ~1) - off;   // values held by the stage
+      const uint32_t* bits = reinterpret_cast<const uint32_t*>(smask);
+      const uint32_t* cnt = bits + T.om_nsegp;
+      auto val = [&](int j) {
+        const uint32_t b = bits[j >> 5];
+        if (!((b >> (j & 31)) & 1u)) return 0.0;
+        const int r = (int)cnt[j >> 5] + __popc(b & ((1u << (j & 31)) - 1u));
+        return r < nst ? stage[off + r] : src[r0 + r];
+      };
+#pragma unroll
+      for (int s = 0; s < 8; ++s) {
+        const int m = tid + NTH * s;
+        double v0 = m ? val(2 * m) : 0.0, v1 = val(2 * m + 1);
+        if (bp.nh) {
+          v0 += dense_src(T, nullptr, 0, bp, i, 2 * m);
+          v1 += dense_src(T, nullptr, 0, bp, i, 2 * m + 1);
+        }
+        fp[s] = make_double2(v0, v1);
+      }
+      __syncthreads();   // every read of the staging buffer is done: stream the next row in
+      if (threadIdx.x == 0 && i + step <= T.col_hi) issue(i + step);
+    } else if (staged) {   // the row and its mask from shared memory (8-byte / byte offsets of the aligned copies)
       const size_t a = reinterpret_cast<uintptr_t>(src + (size_t)i * (N + 1));
       const double* row = stage + ((a & 15) >> 3);
       const uint8_t* mrow = smask + (reinterpret_cast<uintptr_t>(T.side + (size_t)i * (N + 1)) & 15);
@@ -1175,8 +1221,18 @@ __global__ void __launch_bounds__(DenseCfg<N>::NTHR, 1) k_dst_dense2(DevTables T
     }
   } else {
     const double sc = 2.0 / N;
-    for (int j = tid; j <= N; j += NTH)
-      __stcs(dst + (size_t)i * (N + 1) + j, (j == 0 || j == N) ? 0.0 : sc * z[zpad(j)].x);
+    if (mask_omega == 2) {   // Ω-compact output: u at the row's Ω nodes only (never j = 0, N)
+      const uint32_t* info = T.om_info + (size_t)i * 2 * T.om_nsegp;
+      const int r0 = T.om_row[i];
+      for (int j = tid; j <= N; j += NTH) {
+        const uint32_t b = info[j >> 5];
+        if ((b >> (j & 31)) & 1u)
+          __stcs(dst + r0 + (int)info[T.om_nsegp + (j >> 5)] + __popc(b & ((1u << (j & 31)) - 1u)), sc * z[zpad(j)].x);
+      }
+    } else {
+      for (int j = tid; j <= N; j += NTH)
+        __stcs(dst + (size_t)i * (N + 1) + j, (j == 0 || j == N) ? 0.0 : sc * z[zpad(j)].x);
+    }
   }
   }
 }
@@ -1554,14 +1610,14 @@ static void dense_dispatch(const DevTables& T, const double* src, int mask, cons
   }
 }
 void launch_dst_forward(const DevTables& T, const double* fgrid, bool mask, const BumpParams& bp, double* spec,
-                        cudaStream_t s) {
-  dense_dispatch<0>(T, fgrid, mask ? 1 : 0, bp, nullptr, spec, s);
+                        cudaStream_t s, bool compact) {
+  dense_dispatch<0>(T, fgrid, compact ? 2 : (mask ? 1 : 0), bp, nullptr, spec, s);
 }
 
 void launch_inverse_dense(const DevTables& T, const double* spec, const double* hsep, double* vgrid,
-                          cudaStream_t s) {
+                          cudaStream_t s, bool compact) {
   BumpParams bp{};
-  dense_dispatch<1>(T, spec, 0, bp, hsep, vgrid, s);
+  dense_dispatch<1>(T, spec, compact ? 2 : 0, bp, hsep, vgrid, s);
 }
 
 void launch_gs_reaction(double* u, double* v, long n, double dt, const GsParams& p, cudaStream_t s) {

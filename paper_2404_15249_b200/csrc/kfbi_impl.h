@@ -244,6 +244,11 @@ struct DevTables {
   const int32_t *z_comp, *z_knot;
   const int32_t *q_g01, *z_g01;   // global density indices of the knots m, m + 1 of each point
   const uint8_t* row_omega;       // grid column i holds Ω nodes
+  // Ω-compact rows: om_row[i] = Ω nodes before grid row i (N + 2 entries); om_info row i = the
+  // om_nsegp 32-node segment bitmasks of the row, then the Ω counts before each segment in the row
+  const int32_t* om_row;
+  const uint32_t* om_info;
+  int om_nsegp;
   const double *q_dl, *z_dl;      // Δs of the point's component
   const double *z_t1, *z_t2, *z_p1, *z_p2;
   // stencils

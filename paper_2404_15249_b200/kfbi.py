@@ -57,7 +57,7 @@ class Dist(C.Structure):
 
 class SolveOpts(C.Structure):
     _fields_ = [("tol", C.c_double), ("restart", C.c_int32), ("max_restarts", C.c_int32),
-                ("method", C.c_int32), ("gamma", C.c_double), ("async_final", C.c_int32)]
+                ("method", C.c_int32), ("gamma", C.c_double), ("async_final", C.c_int32), ("omega_io", C.c_int32)]
 
 
 METHODS = {"gmres": 0, "richardson": 1, "bicgstab": 2}
@@ -340,17 +340,21 @@ class KFBI:
 
     def solve(self, g, f_grid=None, f_isect=None, f_ctrl=None, phi0=None, tol=1e-8, restart=30,
               max_restarts=50, u=None, stream=None, raise_on_noconv=True, method="gmres", gamma=1.0,
-              async_final=False):
+              async_final=False, omega_io=False):
+        """omega_io: f_grid and u hold the Ω-node values only (omega_count() entries, row-major node
+        order; 2D single-context grids) and u is returned flat in that layout."""
         t = self.torch
+        nf = self.omega_count() if omega_io else self.local_nodes
         g = self._dev(g, self.M)
-        fg = self._dev(f_grid, self.local_nodes)
+        fg = self._dev(f_grid, nf)
         fq = self._dev(f_isect, self.nq)
         fz = self._dev(f_ctrl, self.M)
         p0 = self._dev(phi0, self.M)
-        u = (t.empty(self.local_nodes, dtype=t.float64, device=self.device) if u is None
-             else self._out(u.reshape(-1) if isinstance(u, t.Tensor) and u.is_contiguous() else u, self.local_nodes, "u"))
+        u = (t.empty(nf, dtype=t.float64, device=self.device) if u is None
+             else self._out(u.reshape(-1) if isinstance(u, t.Tensor) and u.is_contiguous() else u, nf, "u"))
         phi = t.empty(self.M, dtype=t.float64, device=self.device)
-        opts = SolveOpts(tol, restart, max_restarts, METHODS[method], gamma, 1 if async_final else 0)
+        opts = SolveOpts(tol, restart, max_restarts, METHODS[method], gamma, 1 if async_final else 0,
+                         1 if omega_io else 0)
         st = SolveStats()
         with t.cuda.device(self.device):
             code = self.lib.kfbi_solve(self.ctx, _ptr(g), _ptr(fg), _ptr(fq), _ptr(fz), _ptr(p0), _ptr(u), _ptr(phi),
@@ -359,7 +363,7 @@ class KFBI:
         if code != OK and (code != ENOCONV or raise_on_noconv):
             self._check(code)
         stats = Stats(st.iters, st.restarts, st.n_applies, bool(st.converged), st.rel_residual, st.t_solve_s)
-        return u.view(self.local_shape), phi, stats
+        return (u if omega_io else u.view(self.local_shape)), phi, stats
 
     def local_slice(self):
         """numpy index of this context's node slab in the full grid (f and u of solve())."""

@@ -64,3 +64,35 @@ def test_async_final_matches_sync():
     u2, p2, s2 = k.solve(*args, async_final=True)
     torch.cuda.synchronize()
     assert torch.equal(u1, u2) and torch.equal(p1, p2) and s1.iters == s2.iters
+
+
+@pytest.mark.parametrize("prob", [W.C1(64), W.C2(512), W.C3(1024), W.C3(2048)], ids=lambda p: f"{p.name}{p.n}")
+def test_omega_io_solve_bit_exact(prob):
+    """kfbi_solve_opts.omega_io: f in and u out as Ω-node values only.  The dense forward reads f at
+    the Ω nodes through the row bitmasks (staged row copies at N ≥ 1024, global gathers below) and
+    the final field writes u there; both equal the full-grid solve bit for bit (f off Ω is never read,
+    P:530; u_h on Ω), and a 3D context refuses the option."""
+    k = _k(prob)
+    pz, pq = k.points("ctrl"), k.points("isect")
+    x = prob.lo + np.arange(prob.n + 1) * prob.h
+    X, Y = np.meshgrid(x, x, indexing="ij")
+    f = W.f_exact(prob.kappa, X, Y).ravel()
+    dev = lambda a: torch.tensor(np.ascontiguousarray(a), device="cuda")
+    g, fq, fz = dev(W.u_exact(*pz.T)), dev(W.f_exact(prob.kappa, *pq.T)), dev(W.f_exact(prob.kappa, *pz.T))
+    u_full, phi_full, st_full = k.solve(g, dev(f), fq, fz)
+    mask = k.node_mask().reshape(-1).astype(bool)
+    u_c, phi_c, st_c = k.solve(g, dev(f[mask]), fq, fz, omega_io=True)
+    assert u_c.numel() == k.omega_count() and st_c.iters == st_full.iters
+    assert torch.equal(phi_c, phi_full)
+    assert np.array_equal(u_c.cpu().numpy(), u_full.cpu().numpy().reshape(-1)[mask])
+
+
+def test_omega_io_refused_in_3d():
+    from paper_2404_15249_b200 import KfbiError
+    k = _k(W.C4(64))
+    pz = k.points("ctrl")
+    g = torch.tensor(W.u_exact(*pz.T), device="cuda")
+    with pytest.raises(KfbiError):
+        k.solve(g, torch.zeros(k.omega_count(), dtype=torch.float64, device="cuda"),
+                torch.zeros(k.nq, dtype=torch.float64, device="cuda"),
+                torch.zeros(k.M, dtype=torch.float64, device="cuda"), omega_io=True)

@@ -1082,6 +1082,9 @@ __global__ void __launch_bounds__(DenseCfg<N>::NTHR, 1) k_dst_dense2(DevTables T
   for (int rb = blockIdx.x; T.col_lo + rb * RPC <= T.col_hi; rb += gridDim.x) {
   const int i = T.col_lo + rb * RPC + rl;
   const bool live = i <= T.col_hi;
+  // MODE 1 with Ω-compact output: a grid row without Ω nodes has no output — its loads, transform and
+  // stores are skipped
+  const bool skip1 = MODE == 1 && compact && live && !T.row_omega[i];
   if (!staged) {
     const int in = i + step;
     if (in <= T.col_hi && src) {
@@ -1175,7 +1178,7 @@ __global__ void __launch_bounds__(DenseCfg<N>::NTHR, 1) k_dst_dense2(DevTables T
       const double* zrr = T.zr + (size_t)(sep ? 0 : rr - 1) * N;
       for (int t = tid; t < N / 4; t += NTH) {
         double2 a = make_double2(0.0, 0.0), b = a;
-        if (live) {
+        if (live && !skip1) {
           a = reinterpret_cast<const double2*>(xrow + 4 * t)[0];
           b = reinterpret_cast<const double2*>(xrow + 4 * t)[1];
           if (hl) {
@@ -1211,7 +1214,8 @@ __global__ void __launch_bounds__(DenseCfg<N>::NTHR, 1) k_dst_dense2(DevTables T
   }
   // a forward row of f·1_Ω with no Ω node (a grid column outside Γ's x-extent) has a zero spectrum:
   // no transform (CTA-uniform when a CTA holds one row, N ≥ 2048)
-  const bool empty = MODE == 0 && RPC == 1 && mask_omega && bp.nh == 0 && live && !T.row_omega[i];
+  const bool empty = (MODE == 0 && RPC == 1 && mask_omega && bp.nh == 0 && live && !T.row_omega[i]) ||
+                     (RPC == 1 && skip1);
   if (!empty) dst1_core<N>(z, tw, tid, fp);
   if (!live) continue;
   if (MODE == 0) {

@@ -301,7 +301,10 @@ __global__ void __launch_bounds__(256, 2) k_dst_rows3t(DevTables3 T, double* wor
 // only the distinct stencil nodes of the result are read, so the z-direction transforms are sparse.
 // forward: plane i, columns ll ∈ [l0, l0 + RPC): G_a = Σ_{irregular (i,a,b)} c · sin(π b ll/N) (the
 // z-DST of the sparse rows, evaluated directly), then the y-DST of G along a → work[(i−1)][ll][kk].
-constexpr int kFwdGroups = 8;
+#ifndef KFBI_FWD_GROUPS
+#define KFBI_FWD_GROUPS 8
+#endif
+constexpr int kFwdGroups = KFBI_FWD_GROUPS;
 template <int N>
 __global__ void __launch_bounds__(256, 2) k_fwd3s(DevTables3 T, const double* __restrict__ corr,
                                                   double* __restrict__ work) {

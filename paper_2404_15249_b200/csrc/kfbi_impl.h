@@ -150,6 +150,8 @@ void build_setup(Setup& S, const kfbi_grid* g, const kfbi_boundary* b, const kfb
                  const DeviceScratch* dev = nullptr);
 size_t gpu_setup_scratch_bytes(int N);
 void gpu_setup_phases(Setup& S, void* scratch, size_t bytes, ::CUstream_st* s, std::vector<int>& q_owner);
+// 2D stencils (nodes, LU weights, unique sorted stencil nodes) on the device, after the control points
+void gpu_stencil_phase(Setup& S, void* scratch, size_t bytes, ::CUstream_st* s);
 
 // Host-side setup products in 3D (control points = intersection nodes, reading R12).
 struct Setup3 {

@@ -421,6 +421,9 @@ void build_setup(Setup& S, const kfbi_grid* g, const kfbi_boundary* b, const kfb
   setup_tick("six-point stencils + inverse row");
   // ---- six-point stencils + inverse rows (R14, R16) ----
   const int M = S.M;
+  if (dev) {   // NEXT-3: the same stencils and LU solves on the device (setup_gpu.cu, bit-identical)
+    gpu_stencil_phase(S, dev->ptr, dev->bytes, dev->stream);
+  } else {
   std::vector<int64_t> nodes((size_t)M * 6 * 2);
   S.st_ext.assign((size_t)M * 6, 0);
   S.st_w.assign((size_t)M * 6, 0);
@@ -482,6 +485,9 @@ void build_setup(Setup& S, const kfbi_grid* g, const kfbi_boundary* b, const kfb
     S.st_node.resize(keys.size());
     for (size_t k = 0; k < keys.size(); ++k)
       S.st_node[k] = (int)(std::lower_bound(uk.begin(), uk.end(), keys[k]) - uk.begin());
+  }
+  }
+  {
     // work items of k_inv_sparse: one per stencil column, a column with more than kMaxColRows rows
     // (Γ running along a grid line at large N) split into equal chunks of consecutive rows
     S.ocol.clear();

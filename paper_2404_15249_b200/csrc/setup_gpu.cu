@@ -3,10 +3,14 @@
 // (R30/R31), irregular nodes with their incident intersections (App. A.3) — as one
 // thread per node / edge, the ordered lists by prefix sums (CUB).  The arithmetic is the host's
 // (setup2d.cpp) operation for operation with round-to-nearest intrinsics, so no FMA contraction can
-// move a node across Γ: the lists are bit-identical to the host setup (tests/test_setup_gpu.py).
-// The rest of Procedure 1 (frames, arc length, control points, stencils, tables) stays on the host.
+// move a node across Γ: the lists are bit-identical to the host setup (tests/test_gpu_setup.py).
+// 2D also builds the interpolation stencils on the device (the six nodes, the local 6×6 Vandermonde
+// solves by LU with partial pivoting — SURVEY §8(f) NEXT-3 "stencil LU on device" — and the sorted
+// unique stencil-node list by a radix sort); frames, arc length, control points and the per-mode
+// tables stay on the host.
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cub/cub.cuh>
 
 #include "kfbi_impl.h"
@@ -207,6 +211,100 @@ size_t lists_bytes(long W) {
   const long nq = kQPerW * W, ni = 2 * nq;
   return nq * (4 * sizeof(int) + sizeof(double)) + ni * (4 * sizeof(int) + 1 + 4 * (sizeof(int) + sizeof(double))) +
          32 * 256;
+}
+
+// ---------------------------------------------------------------------------------------- 2D stencils
+// The host's lu_solve (setup2d.cpp) operation for operation: partial pivoting on |a|, elimination
+// a_ij −= f·a_kj with f = a_ik / a_kk, back substitution — round-to-nearest intrinsics, no contraction.
+__device__ bool d_lu_solve6(double* A, double* b) {
+  constexpr int n = 6;
+  for (int k = 0; k < n; ++k) {
+    int piv = k;
+    for (int i = k + 1; i < n; ++i)
+      if (fabs(A[i * n + k]) > fabs(A[piv * n + k])) piv = i;
+    if (fabs(A[piv * n + k]) < 1e-300) return false;
+    if (piv != k) {
+      for (int j = 0; j < n; ++j) {
+        const double t = A[k * n + j];
+        A[k * n + j] = A[piv * n + j];
+        A[piv * n + j] = t;
+      }
+      const double t = b[k];
+      b[k] = b[piv];
+      b[piv] = t;
+    }
+    for (int i = k + 1; i < n; ++i) {
+      const double f = __ddiv_rn(A[i * n + k], A[k * n + k]);
+      for (int j = k; j < n; ++j) A[i * n + j] = __dsub_rn(A[i * n + j], __dmul_rn(f, A[k * n + j]));
+      b[i] = __dsub_rn(b[i], __dmul_rn(f, b[k]));
+    }
+  }
+  for (int i = n - 1; i >= 0; --i) {
+    double sacc = b[i];
+    for (int j = i + 1; j < n; ++j) sacc = __dsub_rn(sacc, __dmul_rn(A[i * n + j], b[j]));
+    b[i] = __ddiv_rn(sacc, A[i * n + i]);
+  }
+  return true;
+}
+
+// thread per control point: the six stencil nodes (R14), offsets, exterior flags, row 0 of
+// the inverse local system (V⁺ weights) and the normal-derivative row (Neumann, R38), and each node's
+// sort key (column, row class, row) — setup2d.cpp's stencil loop with the same arithmetic
+__global__ void k_stencil2(int M, int N, double lo, double h, const double* __restrict__ zx, const double* __restrict__ zy,
+                           const double* __restrict__ t1, const double* __restrict__ t2, const int8_t* __restrict__ side,
+                           int64_t* __restrict__ nodes, int8_t* __restrict__ ext, double* __restrict__ w,
+                           double* __restrict__ wn, double* __restrict__ sdx, double* __restrict__ sdy,
+                           int64_t* __restrict__ keys, int* __restrict__ err) {
+  const int m = blockIdx.x * blockDim.x + threadIdx.x;
+  if (m >= M) return;
+  const int W = N + 1;
+  const double z[2] = {zx[m], zy[m]};
+  int c[2], sg[2];
+  for (int a = 0; a < 2; ++a) {
+    c[a] = (int)floor(__dadd_rn(__ddiv_rn(__dsub_rn(z[a], lo), h), 0.5));
+    sg[a] = z[a] >= node_x(lo, h, c[a]) ? 1 : -1;
+  }
+  const int off6[6][2] = {{0, 0}, {1, 0}, {-1, 0}, {0, 1}, {0, -1}, {sg[0], sg[1]}};
+  double A[36], A2[36], wv[6], wnv[6];
+  for (int p = 0; p < 6; ++p) {
+    const int ni = c[0] + off6[p][0], nj = c[1] + off6[p][1];
+    if (ni < 1 || nj < 1 || ni > N - 1 || nj > N - 1) atomicOr(err, 1);
+    nodes[((size_t)m * 6 + p) * 2] = ni;
+    nodes[((size_t)m * 6 + p) * 2 + 1] = nj;
+    const double dx = __dsub_rn(node_x(lo, h, ni), z[0]), dy = __dsub_rn(node_x(lo, h, nj), z[1]);
+    sdx[m * 6 + p] = dx;
+    sdy[m * 6 + p] = dy;
+    ext[m * 6 + p] = (ni >= 0 && ni <= N && nj >= 0 && nj <= N && side[(size_t)ni * W + nj]) ? 0 : 1;
+    const double row[6] = {1.0, dx, dy, __dmul_rn(__dmul_rn(0.5, dx), dx), __dmul_rn(dx, dy),
+                           __dmul_rn(__dmul_rn(0.5, dy), dy)};
+    for (int q = 0; q < 6; ++q) A[q * 6 + p] = A2[q * 6 + p] = row[q];
+    wv[p] = p == 0 ? 1.0 : 0.0;
+    wnv[p] = 0.0;
+    const int64_t cls = (nj & 1) ? 0 : ((nj & 3) == 0 ? 1 : 2);
+    keys[(size_t)m * 6 + p] = ((int64_t)ni * 3 + cls) * W + nj;
+  }
+  wnv[1] = t2[m];
+  wnv[2] = -t1[m];
+  if (!d_lu_solve6(A, wv) || !d_lu_solve6(A2, wnv)) atomicOr(err, 2);
+  for (int p = 0; p < 6; ++p) {
+    w[m * 6 + p] = wv[p];
+    wn[m * 6 + p] = wnv[p];
+  }
+}
+
+// st_node[k] = position of keys[k] in the sorted unique list uk[0, nu) (lower bound)
+__global__ void k_stencil_rank(long n, const int64_t* __restrict__ keys, const int64_t* __restrict__ uk,
+                               const int* __restrict__ nu, int32_t* __restrict__ st_node) {
+  const long k = (long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= n) return;
+  const int64_t key = keys[k];
+  int a = 0, b = *nu;
+  while (a < b) {
+    const int mid = (a + b) >> 1;
+    if (uk[mid] < key) a = mid + 1;
+    else b = mid;
+  }
+  st_node[k] = a;
 }
 
 // ---------------------------------------------------------------------------------------- 3D
@@ -559,6 +657,76 @@ void gpu_setup_phases(Setup& S, void* scratch, size_t bytes, cudaStream_t s, std
   ck_(cudaMemcpyAsync(S.pair_q.data(), pqv, npair * sizeof(int), cudaMemcpyDeviceToHost, s), "d2h");
   ck_(cudaMemcpyAsync(S.pair_d.data(), pdv, npair * sizeof(double), cudaMemcpyDeviceToHost, s), "d2h");
   ck_(cudaStreamSynchronize(s), "sync");
+}
+
+// 2D stencils on the device (after the host's control points): fills S.st_nodes_ij, st_ext, st_w,
+// st_wn, st_dx, st_dy, the unique stencil nodes (nsn, sn_i, sn_j) and st_node.  The Ω side array of
+// gpu_setup_phases is still at the head of the scratch (same carve order).
+void gpu_stencil_phase(Setup& S, void* scratch, size_t bytes, cudaStream_t s) {
+  const int N = S.N, W = N + 1, M = S.M;
+  const long WW = (long)W * W, n6 = 6L * M;
+  uint8_t* p = reinterpret_cast<uint8_t*>(scratch);
+  const int8_t* side = carve<int8_t>(p, WW);
+  double* zx = carve<double>(p, M);
+  double* zy = carve<double>(p, M);
+  double* t1 = carve<double>(p, M);
+  double* t2 = carve<double>(p, M);
+  int64_t* nodes = carve<int64_t>(p, 2 * n6);
+  int8_t* ext = carve<int8_t>(p, n6);
+  double* w = carve<double>(p, n6);
+  double* wn = carve<double>(p, n6);
+  double* sdx = carve<double>(p, n6);
+  double* sdy = carve<double>(p, n6);
+  int64_t* keys = carve<int64_t>(p, n6);
+  int64_t* sorted = carve<int64_t>(p, n6);
+  int64_t* uk = carve<int64_t>(p, n6);
+  int32_t* st_node = carve<int32_t>(p, n6);
+  int* nu = carve<int>(p, 1);
+  int* err = carve<int>(p, 1);
+  size_t tb_sort = 0, tb_uniq = 0;
+  cub::DeviceRadixSort::SortKeys(nullptr, tb_sort, keys, sorted, (int)n6, 0, 64, s);
+  cub::DeviceSelect::Unique(nullptr, tb_uniq, sorted, uk, nu, (int)n6, s);
+  const size_t tb = std::max(tb_sort, tb_uniq);
+  void* temp = carve<uint8_t>(p, tb);
+  if ((size_t)(p - reinterpret_cast<uint8_t*>(scratch)) > bytes) throw ScratchError("device setup scratch too small for the stencils");
+  ck_(cudaMemcpyAsync(zx, S.z_x.data(), M * sizeof(double), cudaMemcpyHostToDevice, s), "h2d");
+  ck_(cudaMemcpyAsync(zy, S.z_y.data(), M * sizeof(double), cudaMemcpyHostToDevice, s), "h2d");
+  ck_(cudaMemcpyAsync(t1, S.z_t1.data(), M * sizeof(double), cudaMemcpyHostToDevice, s), "h2d");
+  ck_(cudaMemcpyAsync(t2, S.z_t2.data(), M * sizeof(double), cudaMemcpyHostToDevice, s), "h2d");
+  ck_(cudaMemsetAsync(err, 0, sizeof(int), s), "memset");
+  if (M > 0)
+    k_stencil2<<<(M + 127) / 128, 128, 0, s>>>(M, N, S.lo, S.h, zx, zy, t1, t2, side, nodes, ext, w, wn, sdx, sdy, keys, err);
+  size_t tbs = tb;
+  ck_(cub::DeviceRadixSort::SortKeys(temp, tbs, keys, sorted, (int)n6, 0, 64, s), "sort stencil keys");
+  size_t tbu = tb;
+  ck_(cub::DeviceSelect::Unique(temp, tbu, sorted, uk, nu, (int)n6, s), "unique stencil keys");
+  if (n6 > 0) k_stencil_rank<<<grid_for(n6), 256, 0, s>>>(n6, keys, uk, nu, st_node);
+  ck_(cudaGetLastError(), "stencil kernels");
+  int h_nu = 0, h_err = 0;
+  ck_(cudaMemcpyAsync(&h_nu, nu, sizeof(int), cudaMemcpyDeviceToHost, s), "d2h");
+  ck_(cudaMemcpyAsync(&h_err, err, sizeof(int), cudaMemcpyDeviceToHost, s), "d2h");
+  S.st_nodes_ij.resize(2 * n6);
+  S.st_ext.resize(n6); S.st_w.resize(n6); S.st_wn.resize(n6); S.st_dx.resize(n6); S.st_dy.resize(n6);
+  S.st_node.resize(n6);
+  ck_(cudaMemcpyAsync(S.st_nodes_ij.data(), nodes, 2 * n6 * sizeof(int64_t), cudaMemcpyDeviceToHost, s), "d2h");
+  ck_(cudaMemcpyAsync(S.st_ext.data(), ext, n6, cudaMemcpyDeviceToHost, s), "d2h");
+  ck_(cudaMemcpyAsync(S.st_w.data(), w, n6 * sizeof(double), cudaMemcpyDeviceToHost, s), "d2h");
+  ck_(cudaMemcpyAsync(S.st_wn.data(), wn, n6 * sizeof(double), cudaMemcpyDeviceToHost, s), "d2h");
+  ck_(cudaMemcpyAsync(S.st_dx.data(), sdx, n6 * sizeof(double), cudaMemcpyDeviceToHost, s), "d2h");
+  ck_(cudaMemcpyAsync(S.st_dy.data(), sdy, n6 * sizeof(double), cudaMemcpyDeviceToHost, s), "d2h");
+  ck_(cudaMemcpyAsync(S.st_node.data(), st_node, n6 * sizeof(int32_t), cudaMemcpyDeviceToHost, s), "d2h");
+  ck_(cudaStreamSynchronize(s), "sync");
+  if (h_err) throw GeomError("interpolation stencil leaves the grid or is singular");
+  std::vector<int64_t> hu(h_nu);
+  ck_(cudaMemcpyAsync(hu.data(), uk, h_nu * sizeof(int64_t), cudaMemcpyDeviceToHost, s), "d2h");
+  ck_(cudaStreamSynchronize(s), "sync");
+  S.nsn = h_nu;
+  S.sn_i.resize(h_nu);
+  S.sn_j.resize(h_nu);
+  for (int u = 0; u < h_nu; ++u) {
+    S.sn_i[u] = (int)(hu[u] / W / 3);
+    S.sn_j[u] = (int)(hu[u] % W);
+  }
 }
 
 }  // namespace kfbi

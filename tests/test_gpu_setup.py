@@ -1,8 +1,9 @@
 """GPU-side Procedure 1 phases (kfbi_setup_device) against the host setup.
 
-Classification, the sign-change edges with their bisected intersections (R30/R31)
-and the irregular-node lists (App. A.3) come from setup_gpu.cu; everything downstream of
-them from the same host code, so the two setups must agree on every list.  Integer lists and
+Classification, the sign-change edges with their bisected intersections (R30/R31),
+the irregular-node lists (App. A.3) and, in 2D, the six-point stencils with their LU-solved
+weight rows (R14, R16, R38) and the sorted unique stencil-node list come from setup_gpu.cu;
+everything else from the same host code, so the two setups must agree on every list.  Integer lists and
 the Ω mask are compared bit-exactly; ξ is bit-exact for ellipses (only +, −, ×, ÷ on both sides)
 and within 1e-13 for stars (device sin/atan2 vs libm inside the level function, amplified where Γ
 grazes a grid line, R30).  The
@@ -68,6 +69,19 @@ def test_device_setup_apply_matches_host(make, n):
         assert err == 0.0
     else:   # Δξ ≤ 1e-13 enters the corrections through d/h² (App. A.3): well inside the 1e-10 apply bar
         assert err <= 1e-11
+
+
+@pytest.mark.parametrize("n", [64, 1024])
+def test_device_stencils_neumann_apply_matches_host(n):
+    """The device LU of the normal-derivative rows (st_wn, R38) equals the host's bit for bit: the
+    K_N apply (Neumann, κ = 1) of an ellipse built on either setup is identical."""
+    import torch
+    prob = W.neumann(W.problem("ellipse-k1", 2, n, [W.ellipse(1.0, 0.8)], 1.0))
+    host, dev, _, _ = _pair(prob)
+    phi = torch.tensor(W.random_density(host.M, seed=3), dtype=torch.float64, device="cuda")
+    a, b = host.apply(phi), dev.apply(phi)
+    torch.cuda.synchronize()
+    assert torch.equal(a, b)
 
 
 def test_device_setup_errors():

@@ -194,6 +194,8 @@ void build_setup3(Setup3& S, const kfbi_grid* g, const kfbi_boundary* b, const k
                   const DeviceScratch* dev = nullptr);
 size_t gpu_setup_scratch_bytes3(int N);
 void gpu_setup_phases3(Setup3& S, void* scratch, size_t bytes, ::CUstream_st* s);
+// 3D ten-point stencils (nodes, LU weight rows, centre and sign/exterior code) on the device
+void gpu_stencil_phase3(Setup3& S, void* scratch, size_t bytes, ::CUstream_st* s);
 
 struct DevTables3 {
   int N, P, nq, nirr;

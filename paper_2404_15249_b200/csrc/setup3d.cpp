@@ -304,7 +304,11 @@ void build_setup3(Setup3& S, const kfbi_grid* g, const kfbi_boundary* b, const k
   }
   if (bad) throw GeomError("LSQ fit needs ≥ 8 non-degenerate neighbours (R12)");
 
-  // ten-point stencils + row 0 of the inverse local system (R14, R16)
+  // ten-point stencils + row 0 of the inverse local system (R14, R16); NEXT-3: on the device
+  // with the same arithmetic when the setup runs there (setup_gpu.cu, bit-identical)
+  if (dev) {
+    gpu_stencil_phase3(S, dev->ptr, dev->bytes, dev->stream);
+  } else {
   S.st_c.assign(3 * (size_t)nq, 0);
   S.st_code.assign(nq, 0);
   S.st_w.assign(10 * (size_t)nq, 0.0);
@@ -346,6 +350,7 @@ void build_setup3(Setup3& S, const kfbi_grid* g, const kfbi_boundary* b, const k
     S.st_code[e] = ext | ((sg[0] > 0) << 10) | ((sg[1] > 0) << 11) | ((sg[2] > 0) << 12);
   }
   if (bad) throw GeomError("interpolation stencil leaves the grid or is singular");
+  }
 
   // sparse K_D path: irregular nodes by grid row (i−1)·N + j, and the distinct stencil nodes by row
   {

@@ -292,6 +292,92 @@ __global__ void k_stencil2(int M, int N, double lo, double h, const double* __re
   }
 }
 
+// the host's lu_solve_n (setup3d.cpp) for the 10×10 systems, same operation order, round-to-nearest
+__device__ bool d_lu_solve10(double* A, double* b) {
+  constexpr int n = 10;
+  for (int k = 0; k < n; ++k) {
+    int piv = k;
+    for (int i = k + 1; i < n; ++i)
+      if (fabs(A[i * n + k]) > fabs(A[piv * n + k])) piv = i;
+    if (fabs(A[piv * n + k]) < 1e-300) return false;
+    if (piv != k) {
+      for (int j = 0; j < n; ++j) {
+        const double t = A[k * n + j];
+        A[k * n + j] = A[piv * n + j];
+        A[piv * n + j] = t;
+      }
+      const double t = b[k];
+      b[k] = b[piv];
+      b[piv] = t;
+    }
+    for (int i = k + 1; i < n; ++i) {
+      const double f = __ddiv_rn(A[i * n + k], A[k * n + k]);
+      for (int j = k; j < n; ++j) A[i * n + j] = __dsub_rn(A[i * n + j], __dmul_rn(f, A[k * n + j]));
+      b[i] = __dsub_rn(b[i], __dmul_rn(f, b[k]));
+    }
+  }
+  for (int i = n - 1; i >= 0; --i) {
+    double sacc = b[i];
+    for (int j = i + 1; j < n; ++j) sacc = __dsub_rn(sacc, __dmul_rn(A[i * n + j], b[j]));
+    b[i] = __ddiv_rn(sacc, A[i * n + i]);
+  }
+  return true;
+}
+
+// thread per 3D control point (intersection node): the ten-point stencil {c, c ± e_a, c + σ_x e_x +
+// σ_y e_y, c + σ_x e_x + σ_z e_z, c + σ_y e_y + σ_z e_z} (R14, R16), row 0 of the inverse local
+// system and the Neumann normal-derivative row (R38), centre and sign/exterior code — setup3d.cpp's
+// stencil loop with the same arithmetic
+__global__ void k_stencil3(int nq, int N, double lo, double h, const double* __restrict__ qpos,
+                           const double* __restrict__ qn, const int8_t* __restrict__ side,
+                           int64_t* __restrict__ nodes, double* __restrict__ w, double* __restrict__ wn,
+                           int32_t* __restrict__ stc, int32_t* __restrict__ code, int* __restrict__ err) {
+  const int e = blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= nq) return;
+  const int W = N + 1;
+  const double z[3] = {qpos[3 * (size_t)e], qpos[3 * (size_t)e + 1], qpos[3 * (size_t)e + 2]};
+  int c[3], sg[3];
+  for (int a = 0; a < 3; ++a) {
+    c[a] = (int)floor(__dadd_rn(__ddiv_rn(__dsub_rn(z[a], lo), h), 0.5));
+    sg[a] = z[a] >= node_x(lo, h, c[a]) ? 1 : -1;
+  }
+  const int off[10][3] = {{0, 0, 0}, {1, 0, 0}, {-1, 0, 0}, {0, 1, 0}, {0, -1, 0}, {0, 0, 1}, {0, 0, -1},
+                          {sg[0], sg[1], 0}, {sg[0], 0, sg[2]}, {0, sg[1], sg[2]}};
+  double A[100], A2[100], wv[10], wnv[10];
+  int ext = 0;
+  bool bad = false;
+  for (int p = 0; p < 10; ++p) {
+    const int ni = c[0] + off[p][0], nj = c[1] + off[p][1], nk = c[2] + off[p][2];
+    wv[p] = p == 0 ? 1.0 : 0.0;
+    wnv[p] = 0.0;
+    if (ni < 1 || nj < 1 || nk < 1 || ni > N - 1 || nj > N - 1 || nk > N - 1) {
+      bad = true;
+      continue;
+    }
+    nodes[30 * (size_t)e + 3 * p] = ni;
+    nodes[30 * (size_t)e + 3 * p + 1] = nj;
+    nodes[30 * (size_t)e + 3 * p + 2] = nk;
+    if (!side[((size_t)ni * W + nj) * W + nk]) ext |= 1 << p;
+    const double dx = __dsub_rn(node_x(lo, h, ni), z[0]), dy = __dsub_rn(node_x(lo, h, nj), z[1]),
+                 dz = __dsub_rn(node_x(lo, h, nk), z[2]);
+    const double row[10] = {1.0, dx, dy, dz, __dmul_rn(__dmul_rn(0.5, dx), dx), __dmul_rn(__dmul_rn(0.5, dy), dy),
+                            __dmul_rn(__dmul_rn(0.5, dz), dz), __dmul_rn(dx, dy), __dmul_rn(dx, dz), __dmul_rn(dy, dz)};
+    for (int q = 0; q < 10; ++q) A[q * 10 + p] = A2[q * 10 + p] = row[q];
+  }
+  if (bad) {
+    atomicOr(err, 1);
+    return;
+  }
+  for (int a = 0; a < 3; ++a) wnv[1 + a] = qn[3 * (size_t)e + a];
+  if (!d_lu_solve10(A, wv) || !d_lu_solve10(A2, wnv)) atomicOr(err, 2);
+  for (int p = 0; p < 10; ++p) {
+    w[10 * (size_t)e + p] = wv[p];
+    wn[10 * (size_t)e + p] = wnv[p];
+  }
+  for (int a = 0; a < 3; ++a) stc[3 * (size_t)e + a] = c[a];
+  code[e] = ext | ((sg[0] > 0) << 10) | ((sg[1] > 0) << 11) | ((sg[2] > 0) << 12);
+}
+
 // st_node[k] = position of keys[k] in the sorted unique list uk[0, nu) (lower bound)
 __global__ void k_stencil_rank(long n, const int64_t* __restrict__ keys, const int64_t* __restrict__ uk,
                                const int* __restrict__ nu, int32_t* __restrict__ st_node) {
@@ -727,6 +813,44 @@ void gpu_stencil_phase(Setup& S, void* scratch, size_t bytes, cudaStream_t s) {
     S.sn_i[u] = (int)(hu[u] / W / 3);
     S.sn_j[u] = (int)(hu[u] % W);
   }
+}
+
+// 3D ten-point stencils on the device (after the host's frames): fills S.st_nodes_ij, st_w, st_wn, st_c,
+// st_code.  The Ω side array of gpu_setup_phases3 is still at the head of the scratch.
+void gpu_stencil_phase3(Setup3& S, void* scratch, size_t bytes, cudaStream_t s) {
+  const int N = S.N, W = N + 1, nq = S.nq;
+  const long WWW = (long)W * W * W;
+  uint8_t* p = reinterpret_cast<uint8_t*>(scratch);
+  const int8_t* side = carve<int8_t>(p, WWW);
+  double* qpos = carve<double>(p, 3L * nq);
+  double* qn = carve<double>(p, 3L * nq);
+  int64_t* nodes = carve<int64_t>(p, 30L * nq);
+  double* w = carve<double>(p, 10L * nq);
+  double* wn = carve<double>(p, 10L * nq);
+  int32_t* stc = carve<int32_t>(p, 3L * nq);
+  int32_t* code = carve<int32_t>(p, nq);
+  int* err = carve<int>(p, 1);
+  if ((size_t)(p - reinterpret_cast<uint8_t*>(scratch)) > bytes) throw ScratchError("device setup scratch too small for the stencils");
+  ck_(cudaMemcpyAsync(qpos, S.q_pos.data(), 3L * nq * sizeof(double), cudaMemcpyHostToDevice, s), "h2d");
+  ck_(cudaMemcpyAsync(qn, S.q_n.data(), 3L * nq * sizeof(double), cudaMemcpyHostToDevice, s), "h2d");
+  ck_(cudaMemsetAsync(nodes, 0, 30L * nq * sizeof(int64_t), s), "memset");
+  ck_(cudaMemsetAsync(err, 0, sizeof(int), s), "memset");
+  if (nq > 0) k_stencil3<<<(nq + 127) / 128, 128, 0, s>>>(nq, N, S.lo, S.h, qpos, qn, side, nodes, w, wn, stc, code, err);
+  ck_(cudaGetLastError(), "stencil kernel");
+  int h_err = 0;
+  ck_(cudaMemcpyAsync(&h_err, err, sizeof(int), cudaMemcpyDeviceToHost, s), "d2h");
+  S.st_nodes_ij.resize(30L * nq);
+  S.st_w.resize(10L * nq);
+  S.st_wn.resize(10L * nq);
+  S.st_c.resize(3L * nq);
+  S.st_code.resize(nq);
+  ck_(cudaMemcpyAsync(S.st_nodes_ij.data(), nodes, 30L * nq * sizeof(int64_t), cudaMemcpyDeviceToHost, s), "d2h");
+  ck_(cudaMemcpyAsync(S.st_w.data(), w, 10L * nq * sizeof(double), cudaMemcpyDeviceToHost, s), "d2h");
+  ck_(cudaMemcpyAsync(S.st_wn.data(), wn, 10L * nq * sizeof(double), cudaMemcpyDeviceToHost, s), "d2h");
+  ck_(cudaMemcpyAsync(S.st_c.data(), stc, 3L * nq * sizeof(int32_t), cudaMemcpyDeviceToHost, s), "d2h");
+  ck_(cudaMemcpyAsync(S.st_code.data(), code, nq * sizeof(int32_t), cudaMemcpyDeviceToHost, s), "d2h");
+  ck_(cudaStreamSynchronize(s), "sync");
+  if (h_err) throw GeomError("interpolation stencil leaves the grid or is singular");
 }
 
 }  // namespace kfbi

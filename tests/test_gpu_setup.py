@@ -138,8 +138,9 @@ def test_device_setup_matches_oracle(make, n):
 
 @pytest.mark.parametrize("make,n", [(W.C4, 32), (W.C4, 128), (W.C5, 64), (W.C5, 512)])
 def test_device_setup3d_lists_match_host(make, n):
-    """3D (NEXT-3): classification, the (axis, i, j, k) sign-change edges with their bisected ξ and the
-    (i, j, k) irregular nodes with their ≤ 6 incident intersections on the device — bit-identical to the
+    """3D (NEXT-3): classification, the (axis, i, j, k) sign-change edges with their bisected ξ, the
+    (i, j, k) irregular nodes with their ≤ 6 incident intersections and the ten-point stencils with
+    their LU-solved weight rows on the device — bit-identical to the
     host setup (ellipsoid and torus levels use only +, −, ×, ÷, √ on both sides); the host setup is pinned
     to the oracle's lists by tests/test_abi.py::test_host_setup3d_matches_oracle."""
     prob = make(n)
@@ -152,6 +153,17 @@ def test_device_setup3d_lists_match_host(make, n):
     assert np.array_equal(host.points("ctrl"), dev.points("ctrl"))
     assert np.array_equal(host.points("normal"), dev.points("normal"))
     phi = W.random_density(host.M, 3)
+    assert np.array_equal(host.apply(phi).cpu().numpy(), dev.apply(phi).cpu().numpy())
+
+
+def test_device_stencils3d_neumann_apply_matches_host():
+    """3D ten-point stencils on the device (NEXT-3 stencil LU): the Neumann normal-derivative rows
+    (R38) equal the host's bit for bit — the K_N apply of the C4 ellipsoid (κ = 1) built on either
+    setup is identical."""
+    import torch
+    prob = W.neumann(W.problem("C4-ellipsoid-k1", 3, 64, list(W.C4(64).comps), 1.0))
+    host, dev, _, _ = _pair(prob)
+    phi = W.random_density(host.M, 5)
     assert np.array_equal(host.apply(phi).cpu().numpy(), dev.apply(phi).cpu().numpy())
 
 

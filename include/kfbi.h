@@ -173,8 +173,11 @@ kfbi_status kfbi_setup(const kfbi_grid* grid, const kfbi_boundary* bnd, const kf
  * (readings R30/R31) and the irregular nodes with their incident intersections (P:551,
  * App. A.3) run as kernels on `stream` in the caller's scratch d_scratch (device, ≥ the bytes
  * kfbi_setup_scratch_size returns — ≈ 5 GB at 512³ — borrowed for the call only, contents undefined
- * after); the lists come back to the host (the only host↔device traffic) and the rest of Procedure 1
- * (frames, control points, LSQ neighbourhoods, stencils, per-mode tables) runs there as in kfbi_setup.
+ * after), and so do the interpolation stencils (the stencil nodes, the local Vandermonde
+ * systems solved by LU with partial pivoting for the V⁺ and ∂_n V⁺ weight rows, and in 2D the sorted
+ * unique stencil-node list); the lists come back to the host, and the rest of Procedure 1 (frames, arc
+ * length, control points, LSQ neighbourhoods, spline filters, per-mode tables) runs there as in
+ * kfbi_setup (host↔device traffic: the lists, and the control points up for the stencils).
  * The lists are identical to kfbi_setup's (same arithmetic, IEEE round-to-nearest, no contraction; the
  * star level uses the device sin/atan2, so a node within an ulp of Γ could in principle classify
  * differently).  Synchronous.  Errors as kfbi_setup plus KFBI_ENOMEM (scratch too small), KFBI_ECUDA. */

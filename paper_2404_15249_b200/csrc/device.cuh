@@ -230,16 +230,18 @@ __device__ __forceinline__ double w32c(int m) {
 __device__ __forceinline__ double w32s(int m) { return w32c(m - 8); }
 
 // the lanes of one row synchronise: within a warp (N ≤ 1024) or across the CTA (row = CTA)
-template <int NTL>
+// BAR > 0: a thread team of NTL threads (a multiple of 32) synchronises on named barrier BAR
+template <int NTL, int BAR = 0>
 __device__ __forceinline__ void rsync() {
-  if constexpr (NTL > 32) __syncthreads();
+  if constexpr (BAR > 0) asm volatile("bar.sync %0, %1;" ::"r"(BAR), "r"(NTL) : "memory");
+  else if constexpr (NTL > 32) __syncthreads();
   else __syncwarp();
 }
 
 // Compile-time Stockham radix-R pass over one row z[0..M) held by M/16 lanes of one warp (rows never
 // straddle warps, so __syncwarp orders the in-place smem exchange).  Twiddles e^{+2πi r k/(Ns R)} =
 // tw[r k 2NT/(Ns R) mod 2NT] from the (cos, sin)(π m/NT) table of the grid size NT (L1-resident).
-template <int R, int M, int Ns, int NT>
+template <int R, int M, int Ns, int NT, int BAR = 0>
 __device__ __forceinline__ void st_pass(double2* z, const double2* __restrict__ tw, int tid) {
   constexpr int NTH = M / 16, NI = M / R, IT = NI / NTH;
   double2 v[IT * R];
@@ -262,7 +264,7 @@ __device__ __forceinline__ void st_pass(double2* z, const double2* __restrict__ 
     }
     dft_reg<R>(v + it * R);
   }
-  rsync<NTH>();
+  rsync<NTH, BAR>();
 #pragma unroll
   for (int it = 0; it < IT; ++it) {
     const int j = tid + it * NTH;
@@ -270,20 +272,20 @@ __device__ __forceinline__ void st_pass(double2* z, const double2* __restrict__ 
 #pragma unroll
     for (int q = 0; q < R; ++q) z[zpad(base + q * Ns)] = v[it * R + q];
   }
-  rsync<NTH>();
+  rsync<NTH, BAR>();
 }
 
-template <int M, int Ns, int NT>
+template <int M, int Ns, int NT, int BAR = 0>
 __device__ __forceinline__ void st_fft(double2* z, const double2* __restrict__ tw, int tid) {
   if constexpr (Ns * 16 <= M) {
-    st_pass<16, M, Ns, NT>(z, tw, tid);
-    st_fft<M, Ns * 16, NT>(z, tw, tid);
+    st_pass<16, M, Ns, NT, BAR>(z, tw, tid);
+    st_fft<M, Ns * 16, NT, BAR>(z, tw, tid);
   } else if constexpr (M / Ns == 8) {
-    st_pass<8, M, Ns, NT>(z, tw, tid);
+    st_pass<8, M, Ns, NT, BAR>(z, tw, tid);
   } else if constexpr (M / Ns == 4) {
-    st_pass<4, M, Ns, NT>(z, tw, tid);
+    st_pass<4, M, Ns, NT, BAR>(z, tw, tid);
   } else if constexpr (M / Ns == 2) {
-    st_pass<2, M, Ns, NT>(z, tw, tid);
+    st_pass<2, M, Ns, NT, BAR>(z, tw, tid);
   }
 }
 
@@ -415,6 +417,114 @@ __device__ __forceinline__ void dst1_core(double2* z, const double2* __restrict_
     if (k != N - k) z[zpad(N - k)].x = Fk2[s];
   }
   rsync<NTH>();
+}
+
+
+// Split-radix DST-I for one row of N ≥ 2048 on N/16 threads (the CTA), half the FFT points of
+// dst1_core at the same O(ε log N) accuracy (no prefix sums): with f_j, j ∈ [0, N), f_0 = 0, M = N/2,
+//   F_k = E'_k + G_k,  F_{N−k} = G_k − E'_k  (k ∈ [1, M)),  F_M = G_M,
+//   E' = DST-I_M(e), e_m = f_2m  — dst1_core's odd-extension method on an M-point complex FFT;
+//   G_k = Σ_m f_{2m+1} sin(π(2m+1)k/N) = C_{M−k},  C = DCT-II_M(u), u_m = (−1)^m f_{2m+1}  (sin(π(2m+1)k/N)
+//     = (−1)^m cos(π(2m+1)(M−k)/N)); DCT-II by Makhoul: v_n = u_2n, v_{M−1−n} = u_{2n+1},
+//     C_l = Re(e^{iπl/N} V_l), V = FFT⁺_M(v) from one M/2-point complex FFT of w_q = v_2q + i v_2q+1.
+// Team E (threads [0, N/32)) runs the M-point FFT on named barrier 1 while team G (the next N/64) runs
+// the M/2-point FFT on barrier 2; F_k ends in z[zpad(k)].x as with dst1_core.  Input as dst1_core:
+// fp[s] = (f_2m, f_2m+1), m = tid + s·N/16.
+template <int N>
+__device__ __forceinline__ void dst1s_core(double2* z, const double2* __restrict__ tw, int tid, const double2* fp) {
+  constexpr int NTH = N / 16, M = N / 2, TE = N / 32, TG = N / 64, H = M / 2;
+  static_assert(TG % 32 == 0, "dst1s_core needs N >= 2048 (warp-aligned teams)");
+  double2* zE = z;                                  // M complex slots (padded): the odd extension of e
+  double2* zG = z + (M + M / 16 + 2);               // H complex slots (padded): w
+  double* zGd = reinterpret_cast<double*>(zG);      // C_l after the G team's post-processing
+  // scatter the row into the two teams' buffers
+#pragma unroll
+  for (int s = 0; s < 8; ++s) {
+    const int m = tid + s * NTH;
+    // f_{2m}: e index 2m' (m even) or 2m'+1 (m odd), m' = m/2
+    const int mp = m >> 1;
+    if ((m & 1) == 0) {
+      const double v = m ? fp[s].x : 0.0;
+      zE[zpad(mp)].x = v;
+      if (mp > 0) zE[zpad(M - mp)].x = -v;
+      else zE[zpad(M / 2)].x = 0.0;
+    } else {
+      zE[zpad(mp)].y = fp[s].x;
+      zE[zpad(M - mp - 1)].y = -fp[s].x;
+    }
+    // f_{2m+1} = o_m: u_m = (−1)^m o_m at v index m/2 (m even) or M − 1 − (m − 1)/2 (m odd, u = −o_m)
+    const int nv = (m & 1) ? M - 1 - (m >> 1) : (m >> 1);
+    const double u = (m & 1) ? -fp[s].y : fp[s].y;
+    if (nv & 1) zG[zpad(nv >> 1)].y = u;
+    else zG[zpad(nv >> 1)].x = u;
+  }
+  __syncthreads();
+  if (tid < TE) {   // team E: E'_k, k ∈ [1, M), into zE[zpad(k)].x (dst1_core's post-processing at size M)
+    const int te = tid;
+    st_fft<M, 1, N, 1>(zE, tw, te);
+    const double2 wb = __ldg(tw + 2 * (1 + te));   // e^{iπ(1+te)/M}; k = 1 + te + s·M/16 adds s·π/16
+    double Fk[8], Fk2[8];
+#pragma unroll
+    for (int s = 0; s < 8; ++s) {
+      const int k = 1 + te + s * TE;
+      const double2 A = zE[zpad(k)], B = zE[zpad(M - k)];
+      const double2 w = make_double2(fma(wb.x, w32c(s), -wb.y * w32s(s)), fma(wb.y, w32c(s), wb.x * w32s(s)));
+      Fk[s] = 0.5 * (0.5 * (A.y - B.y) - w.x * (0.5 * (A.x - B.x)) + w.y * (0.5 * (A.y + B.y)));
+      Fk2[s] = 0.5 * (0.5 * (B.y - A.y) + w.x * (0.5 * (B.x - A.x)) + w.y * (0.5 * (B.y + A.y)));
+    }
+    rsync<TE, 1>();
+#pragma unroll
+    for (int s = 0; s < 8; ++s) {
+      const int k = 1 + te + s * TE;
+      zE[zpad(k)].x = Fk[s];
+      if (k != M - k) zE[zpad(M - k)].x = Fk2[s];
+    }
+  } else if (tid < TE + TG) {   // team G: C_l, l ∈ [0, M), into zGd[l]
+    const int tg = tid - TE;
+    st_fft<H, 1, N, 2>(zG, tw, tg);
+    // V_l = A_l + e^{2πil/M} B_l, A = (W_l + conj W_{−l})/2, B = (W_l − conj W_{−l})/(2i); l and
+    // l + H share A_l, B_l (W has period H, the twiddle changes sign): C_l = Re(e^{iπl/N} V_l)
+    constexpr int PER = H / TG;   // l ∈ [0, H) per thread: l = tg + r·TG
+    double c0[PER], c1[PER];
+#pragma unroll
+    for (int r = 0; r < PER; ++r) {
+      const int l = tg + r * TG;
+      const double2 Wl = zG[zpad(l)], Wm = zG[zpad((H - l) & (H - 1))];
+      const double Ax = 0.5 * (Wl.x + Wm.x), Ay = 0.5 * (Wl.y - Wm.y);   // A_l
+      const double Bx = 0.5 * (Wl.y + Wm.y), By = -0.5 * (Wl.x - Wm.x);  // B_l = (W_l − conj W_{−l})/(2i)
+      const double2 t = __ldg(tw + ((4 * l) & (2 * N - 1)));            // e^{2πil/M} = e^{iπ·4l/N}
+      const double tBx = t.x * Bx - t.y * By, tBy = t.x * By + t.y * Bx;
+      const double2 e1 = __ldg(tw + l), e2 = __ldg(tw + l + H);           // e^{iπl/N}, e^{iπ(l+H)/N}
+      // V_l = A + tB, V_{l+H} = A − tB
+      c0[r] = e1.x * (Ax + tBx) - e1.y * (Ay + tBy);
+      c1[r] = e2.x * (Ax - tBx) - e2.y * (Ay - tBy);
+    }
+    rsync<TG, 2>();
+#pragma unroll
+    for (int r = 0; r < PER; ++r) {
+      const int l = tg + r * TG;
+      zGd[l] = c0[r];
+      zGd[l + H] = c1[r];
+    }
+  }
+  __syncthreads();
+  // combine: k = 1 + tid + s·NTH covers [1, M]
+  double Fa[8], Fb[8];
+#pragma unroll
+  for (int s = 0; s < 8; ++s) {
+    const int k = 1 + tid + s * NTH;
+    const double e = k < M ? zE[zpad(k)].x : 0.0, g = zGd[M - k];
+    Fa[s] = e + g;
+    Fb[s] = g - e;
+  }
+  __syncthreads();
+#pragma unroll
+  for (int s = 0; s < 8; ++s) {
+    const int k = 1 + tid + s * NTH;
+    z[zpad(k)].x = Fa[s];
+    if (k < M) z[zpad(N - k)].x = Fb[s];
+  }
+  __syncthreads();
 }
 
 

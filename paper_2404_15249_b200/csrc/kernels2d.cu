@@ -978,6 +978,9 @@ __device__ __forceinline__ double dense_src(const DevTables& T, const double* __
   return v;
 }
 
+#ifndef KFBI_DST_SPLIT
+#define KFBI_DST_SPLIT 1
+#endif
 template <int N>
 struct DenseCfg {
   static constexpr int NTH = N / 16, RPC = NTH > 32 ? 1 : 256 / NTH, NTHR = NTH * RPC, ZS = N + N / 16 + 1;
@@ -1216,7 +1219,10 @@ __global__ void __launch_bounds__(DenseCfg<N>::NTHR, 1) k_dst_dense2(DevTables T
   // no transform (CTA-uniform when a CTA holds one row, N ≥ 2048)
   const bool empty = (MODE == 0 && RPC == 1 && mask_omega && bp.nh == 0 && live && !T.row_omega[i]) ||
                      (RPC == 1 && skip1);
-  if (!empty) dst1_core<N>(z, tw, tid, fp);
+  if (!empty) {
+    if constexpr (N >= 2048 && KFBI_DST_SPLIT) dst1s_core<N>(z, tw, tid, fp);   // split radix: half the FFT points
+    else dst1_core<N>(z, tw, tid, fp);
+  }
   if (!live) continue;
   if (MODE == 0) {
     for (int p = tid; p < N; p += NTH) {   // modes → spectral positions

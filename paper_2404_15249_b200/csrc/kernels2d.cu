@@ -962,7 +962,11 @@ __device__ __forceinline__ double dense_src(const DevTables& T, const double* __
   if (src && mask_omega == 2) {   // Ω-compact input: the node's rank among the Ω nodes (row-major)
     const uint32_t* info = T.om_info + (size_t)i * 2 * T.om_nsegp;
     const uint32_t bits = info[j >> 5];
-    if ((bits >> (j & 31)) & 1u) v = src[T.om_row[i] + (int)info[T.om_nsegp + (j >> 5)] + __popc(bits & ((1u << (j & 31)) - 1u))];
+    if ((bits >> (j & 31)) & 1u) {
+      const int r = T.om_row[i] + (int)info[T.om_nsegp + (j >> 5)] + __popc(bits & ((1u << (j & 31)) - 1u));
+      KFBI_CHECK(r < T.om_row[i + 1], r, i);
+      v = src[r];
+    }
   } else if (src && (!mask_omega || T.side[idx])) {
     v = src[idx];
   }
@@ -1124,6 +1128,7 @@ __global__ void __launch_bounds__(DenseCfg<N>::NTHR, 1) k_dst_dense2(DevTables T
         const uint32_t b = bits[j >> 5];
         if (!((b >> (j & 31)) & 1u)) return 0.0;
         const int r = (int)cnt[j >> 5] + __popc(b & ((1u << (j & 31)) - 1u));
+        KFBI_CHECK(r < nv, r, nv);
         return r < nst ? stage[off + r] : src[r0 + r];
       };
 #pragma unroll
@@ -1236,8 +1241,11 @@ __global__ void __launch_bounds__(DenseCfg<N>::NTHR, 1) k_dst_dense2(DevTables T
       const int r0 = T.om_row[i];
       for (int j = tid; j <= N; j += NTH) {
         const uint32_t b = info[j >> 5];
-        if ((b >> (j & 31)) & 1u)
-          __stcs(dst + r0 + (int)info[T.om_nsegp + (j >> 5)] + __popc(b & ((1u << (j & 31)) - 1u)), sc * z[zpad(j)].x);
+        if ((b >> (j & 31)) & 1u) {
+          const int r = r0 + (int)info[T.om_nsegp + (j >> 5)] + __popc(b & ((1u << (j & 31)) - 1u));
+          KFBI_CHECK(r < T.om_row[i + 1], r, i);
+          __stcs(dst + r, sc * z[zpad(j)].x);
+        }
       }
     } else {
       for (int j = tid; j <= N; j += NTH)

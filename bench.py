@@ -281,7 +281,7 @@ def main():
     # u_h is valid on Ω); slab-sharded runs move each rank's node slab of f and u.
     pin = lambda a: torch.tensor(a, dtype=torch.float64).pin_memory()
     compact = not sharded
-    omega_io = compact and prob.dim == 2   # kfbi_solve_opts.omega_io (2D single-context grids)
+    omega_io = compact   # kfbi_solve_opts.omega_io (single-context grids)
     if compact:
         omask = k.node_mask().reshape(-1).astype(bool)
         n_out = int(omask.sum())
@@ -299,7 +299,7 @@ def main():
         of u gathered after; returns the device array the host copy reads.  async_final: the solve
         returns with its final field still running on the stream (the serving loop's next host work
         overlaps it; every later use is stream-ordered)."""
-        if compact and omega_io:   # 2D: the solve reads f and writes u as Ω-node values itself
+        if compact and omega_io:   # the solve reads f and writes u as Ω-node values itself
             u, _, st_ = k.solve(gd, fgd, fqd, fzd, u=u_c if b is None else u_cs[b], method=args.method,
                                 async_final=async_final, omega_io=True)
             return u

@@ -114,13 +114,13 @@ typedef struct {
                             the iteration has converged and the final field (u) is enqueued on
                             `stream` — d_u / d_phi_out are complete when the stream reaches that
                             point (serving loops overlap their next host work with it)          */
-  int32_t omega_io;      /* 0 (default): d_f_grid and d_u are full (N+1)^d node grids; 1 (2D,
-                            world = 1): both hold only the Ω-node values in row-major node order
+  int32_t omega_io;      /* 0 (default): d_f_grid and d_u are full (N+1)^d node grids; 1 (one
+                            context per grid): both hold only the Ω-node values in row-major node order
                             (kfbi_omega_count entries, the layout of kfbi_scatter_omega /
                             kfbi_gather_omega): the dense forward transform reads f and the final
                             field writes u in that layout directly (no full-grid f or u is formed;
-                            16-byte aligned device buffers).  KFBI_EUNSUPPORTED in 3D or with
-                            one rank per process.                                              */
+                            16-byte aligned device buffers).  KFBI_EUNSUPPORTED with one rank
+                            per process.                                                       */
 } kfbi_solve_opts;
 enum { KFBI_GMRES = 0, KFBI_RICHARDSON = 1, KFBI_BICGSTAB = 2 };
 

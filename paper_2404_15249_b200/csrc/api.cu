@@ -165,6 +165,24 @@ void omega_rows(kfbi_ctx* c, const std::vector<int8_t>& side, int64_t rows, int6
   if (c->om_ptr.back() > INT32_MAX) throw ArgError("too many Ω nodes for the compact transfers");
 }
 
+// Ω-compact row tables of the grid rows omega_rows() set up (width = N + 1 nodes per row): om_row32 =
+// Ω nodes before each row, om_info = per row the nsegp 32-node segment bitmasks then the Ω counts
+// before each segment within the row; returns nsegp
+int omega_info(kfbi_ctx* c, const std::vector<int8_t>& side) {
+  const int64_t rows = c->om_rows, W = c->om_width, nseg = (W + 31) / 32, nsegp = (nseg + 3) / 4 * 4;
+  if (c->om_info.size() == (size_t)rows * 2 * nsegp && c->om_row32.size() == (size_t)rows + 1) return (int)nsegp;
+  c->om_row32.assign(c->om_ptr.begin(), c->om_ptr.end());
+  c->om_info.assign((size_t)rows * 2 * nsegp, 0u);
+#pragma omp parallel for schedule(static)
+  for (int64_t r = 0; r < rows; ++r) {
+    uint32_t* info = c->om_info.data() + (size_t)r * 2 * nsegp;
+    for (int64_t j = 0; j < W; ++j)
+      if (side[(size_t)(r * W + j)]) info[j >> 5] |= 1u << (j & 31);
+    for (int64_t g = 0; g < nseg; ++g) info[nsegp + g] = (uint32_t)(c->om_seg[r * nseg + g] - c->om_ptr[r]);
+  }
+  return (int)nsegp;
+}
+
 void layout(kfbi_ctx* c, Arena& A) {
   Setup& S = c->S;
   DevTables& T = c->T;
@@ -224,21 +242,9 @@ void layout(kfbi_ctx* c, Arena& A) {
   c->d_om_ptr = A.table(c->om_ptr);
   c->d_om_seg = A.table(c->om_seg);
   c->d_side = T.side;
-  {   // Ω-compact rows for the dense forward / final field (kfbi_solve_opts.omega_io)
-    const int64_t W = (int64_t)S.N + 1, nseg = (W + 31) / 32, nsegp = (nseg + 3) / 4 * 4;
-    c->om_row32.assign(c->om_ptr.begin(), c->om_ptr.end());
-    c->om_info.assign((size_t)W * 2 * nsegp, 0u);
-    for (int64_t r = 0; r < W; ++r) {
-      uint32_t* info = c->om_info.data() + (size_t)r * 2 * nsegp;
-      for (int64_t j = 0; j < W; ++j)
-        if (S.side[(size_t)(r * W + j)]) info[j >> 5] |= 1u << (j & 31);
-      for (int64_t g = 0; g < nseg; ++g)
-        info[nsegp + g] = (uint32_t)(c->om_seg[r * nseg + g] - c->om_ptr[r]);
-    }
-    T.om_row = A.table(c->om_row32);
-    T.om_info = A.table(c->om_info);
-    T.om_nsegp = (int)nsegp;
-  }
+  T.om_nsegp = omega_info(c, S.side);   // Ω-compact rows for the dense forward / final field (omega_io)
+  T.om_row = A.table(c->om_row32);
+  T.om_info = A.table(c->om_info);
   c->row_omega.assign(S.N + 1, 0);
   for (int i = 0; i <= S.N; ++i) c->row_omega[i] = c->om_ptr[i + 1] > c->om_ptr[i] ? 1 : 0;
   T.row_omega = A.table(c->row_omega);
@@ -325,6 +331,9 @@ void layout3(kfbi_ctx* c, Arena& A) {
   omega_rows(c, S.side, ((int64_t)S.N + 1) * ((int64_t)S.N + 1), (int64_t)S.N + 1);
   c->d_om_ptr = A.table(c->om_ptr);
   c->d_om_seg = A.table(c->om_seg);
+  T.om_nsegp = omega_info(c, S.side);   // Ω-compact rows for the dense forward / final field (omega_io)
+  T.om_row = A.table(c->om_row32);
+  T.om_info = A.table(c->om_info);
   c->d_side = T.side;
   T.tw = A.table(S.tw);
   T.irr_row_perm = A.table(S.irr_row_perm); T.irr_row_nheavy = A.table(S.irr_row_nheavy);
@@ -639,7 +648,7 @@ void forward3(kfbi_ctx* c, const double* fgrid, cudaStream_t s, bool from_work =
   for (int r : my_ranks(c)) {
     const DevTables3 Ts = slab3(c, r);
     if (from_work) launch_dst_rows3(Ts, 0, c->work, nullptr, 1.0, nullptr, s);
-    else launch_dst_rows3(Ts, 3, c->work, nullptr, 1.0, nullptr, s, fgrid, c->corr);
+    else launch_dst_rows3(Ts, 3, c->work, nullptr, 1.0, nullptr, s, fgrid, c->corr, c->io_compact && fgrid);
     launch_transpose3(Ts, c->work, s);
     launch_dst_rows3(Ts, 0, c->work, nullptr, 1.0, nullptr, s);
     launch_sweep3(Ts, c->work, c->zfirst, c->fsep, s);
@@ -653,9 +662,9 @@ void inverse3(kfbi_ctx* c, double* u, cudaStream_t s) {   // u == NULL: result s
     launch_dst_rows3(Ts, 1, c->work, c->hsep, sc, nullptr, s);
     launch_transpose3(Ts, c->work, s);
     if (!u) launch_dst_rows3(Ts, 0, c->work, nullptr, sc, nullptr, s);
-    else launch_dst_rows3(Ts, 2, c->work, nullptr, sc, u, s);   // the slab's planes of u
+    else launch_dst_rows3(Ts, 2, c->work, nullptr, sc, u, s, nullptr, nullptr, c->io_compact);   // the slab's planes of u
   }
-  if (!u) return;
+  if (!u || c->io_compact) return;   // Ω-compact u: the box faces hold no Ω node
   const size_t W = (size_t)c->T3.N + 1;
   if (c->local_io) {   // the slab's planes: only their a = N faces (the box planes 0, N belong to no slab)
     const DevTables3 Ts = slab3(c, c->rank);
@@ -1224,8 +1233,8 @@ kfbi_status kfbi_solve(kfbi_ctx* c, const double* d_g, const double* d_f_grid, c
     return fail(c, KFBI_EINVAL, "f_grid, f_isect, f_ctrl must all be given or all NULL");
   kfbi_solve_opts o{1e-8, 30, 50, KFBI_GMRES, 1.0, 0, 0};
   if (opts) o = *opts;
-  if (o.omega_io && (c->dim != 2 || c->local_io || c->world != 1))
-    return fail(c, KFBI_EUNSUPPORTED, "omega_io: 2D single-context grids only");
+  if (o.omega_io && (c->local_io || c->world != 1))
+    return fail(c, KFBI_EUNSUPPORTED, "omega_io: single-context grids only");
   if (o.restart < 1 || o.restart > kMaxRestart || o.max_restarts < 1 || !(o.tol > 0) || o.method < 0 ||
       o.method > KFBI_BICGSTAB || (o.method == KFBI_RICHARDSON && !(o.gamma > 0 && o.gamma <= 1)))
     return fail(c, KFBI_EINVAL, "bad solve options");

@@ -120,8 +120,9 @@ void launch_sparse3(const DevTables3& T, int which, const double* src, const dou
 // mode 1 inverse with the arrowhead fix-up on load (rows = (i, ll), modes m = ll·N + kk);
 // mode 2 final store into a full (N+1)^3 grid (× scale)
 // mode 3: forward from h²·f·1_Ω (src = full (N+1)³ grid, or NULL) + the compact corrections `corr`
+// compact (modes 2, 3): u / f hold the Ω-node values only (row-major node ranks, omega_io)
 void launch_dst_rows3(const DevTables3& T, int mode, double* work, const double* hsep, double scale, double* out,
-                      cudaStream_t s, const double* src = nullptr, const double* corr = nullptr);
+                      cudaStream_t s, const double* src = nullptr, const double* corr = nullptr, bool compact = false);
 void launch_transpose3(const DevTables3& T, double* work, cudaStream_t s);
 // sparse: the source came from k_fwd3s (planes without irregular nodes are zero and not written; the
 // planes the y-inverse does not read are not stored)

@@ -228,7 +228,7 @@ template <int MODE, int N>
 __global__ void __launch_bounds__(256, 2) k_dst_rows3t(DevTables3 T, double* work, const double* __restrict__ hsep,
                                                        double scale, double* __restrict__ out,
                                                        const double* __restrict__ src,
-                                                       const double* __restrict__ corr) {
+                                                       const double* __restrict__ corr, int compact) {
   constexpr int NTL = N / 32, RPC = 256 / NTL, ZS = N / 2 + N / 32 + 1;
   extern __shared__ double2 smz[];
   const int rl = threadIdx.x / NTL, tid = threadIdx.x % NTL;
@@ -244,13 +244,28 @@ __global__ void __launch_bounds__(256, 2) k_dst_rows3t(DevTables3 T, double* wor
     const int W = N + 1;
     const double h2 = T.h * T.h;
     const size_t gbase = ((size_t)i * W + a) * W;
+    const size_t gr = (size_t)i * W + a;   // grid row (i, a)
+    const uint32_t* info = compact ? T.om_info + gr * 2 * T.om_nsegp : nullptr;
+    // Ω-compact f: the value at node j of the row has rank om_row + (count before j's segment) + popc
+    auto cval = [&](int j) {
+      const uint32_t b = info[j >> 5];
+      if (!((b >> (j & 31)) & 1u)) return 0.0;
+      const int r = T.om_row[gr] + (int)info[T.om_nsegp + (j >> 5)] + __popc(b & ((1u << (j & 31)) - 1u));
+      KFBI_CHECK(r < T.om_row[gr + 1], r, (int)gr);
+      return h2 * src[r];
+    };
 #pragma unroll
     for (int s = 0; s < 16; ++s) {
       const int m = tid + s * NTL;
       double v0 = 0.0, v1 = 0.0;
       if (live && a > 0 && src) {
-        if (m > 0 && T.side[gbase + 2 * m]) v0 = h2 * src[gbase + 2 * m];
-        if (T.side[gbase + 2 * m + 1]) v1 = h2 * src[gbase + 2 * m + 1];
+        if (compact) {
+          if (m > 0) v0 = cval(2 * m);
+          v1 = cval(2 * m + 1);
+        } else {
+          if (m > 0 && T.side[gbase + 2 * m]) v0 = h2 * src[gbase + 2 * m];
+          if (T.side[gbase + 2 * m + 1]) v1 = h2 * src[gbase + 2 * m + 1];
+        }
       }
       z[zpad(m)] = make_double2(v0, v1);
     }
@@ -277,7 +292,27 @@ __global__ void __launch_bounds__(256, 2) k_dst_rows3t(DevTables3 T, double* wor
   if (!live) return;
   const double* F = reinterpret_cast<const double*>(z);
   const double sc = a == 0 ? 0.0 : scale;
-  if (MODE == 2) {
+  if (MODE == 2 && compact) {   // u at the row's Ω nodes only (row-major ranks)
+    const size_t gr = (size_t)i * (N + 1) + a;
+    const uint32_t* info = T.om_info + gr * 2 * T.om_nsegp;
+    const int r0 = T.om_row[gr];
+#pragma unroll
+    for (int s = 0; s < 16; ++s) {
+      const int j = 2 * (tid + s * NTL);
+      const double2 f = *reinterpret_cast<const double2*>(F + fpos(j));
+      const uint32_t b = info[j >> 5];   // j, j + 1 share a segment (j even)
+      const int r = r0 + (int)info[T.om_nsegp + (j >> 5)] + __popc(b & ((1u << (j & 31)) - 1u));
+      if ((b >> (j & 31)) & 1u) {
+        KFBI_CHECK(r < T.om_row[gr + 1], r, (int)gr);
+        out[r] = sc * f.x;
+      }
+      if ((b >> ((j + 1) & 31)) & 1u) {
+        const int r1 = r + (int)((b >> (j & 31)) & 1u);
+        KFBI_CHECK(r1 < T.om_row[gr + 1], r1, (int)gr);
+        out[r1] = sc * f.y;
+      }
+    }
+  } else if (MODE == 2) {
     double* op = out + ((size_t)i * (N + 1) + a) * (N + 1);
 #pragma unroll
     for (int s = 0; s < 16; ++s) {
@@ -838,7 +873,7 @@ void launch_correct3(const DevTables3& T, const double* phi, const double* dphi,
 }
 template <int N>
 static void dst_rows3_n(const DevTables3& T, int mode, double* work, const double* hsep, double scale, double* out,
-                        cudaStream_t s, const double* src, const double* corr) {
+                        cudaStream_t s, const double* src, const double* corr, int compact) {
   constexpr int RPC = 256 / (N / 32);
   const size_t sm = (size_t)RPC * (N / 2 + N / 32 + 1) * sizeof(double2);
   const int grid = cdiv3((long)(T.i_hi - T.i_lo + 1) * N, RPC);
@@ -846,20 +881,21 @@ static void dst_rows3_n(const DevTables3& T, int mode, double* work, const doubl
   smem_optin((const void*)k_dst_rows3t<1, N>, sm);
   smem_optin((const void*)k_dst_rows3t<2, N>, sm);
   smem_optin((const void*)k_dst_rows3t<3, N>, sm);
-  if (mode == 0) k_dst_rows3t<0, N><<<grid, 256, sm, s>>>(T, work, hsep, scale, out, src, corr);
-  else if (mode == 1) k_dst_rows3t<1, N><<<grid, 256, sm, s>>>(T, work, hsep, scale, out, src, corr);
-  else if (mode == 2) k_dst_rows3t<2, N><<<grid, 256, sm, s>>>(T, work, hsep, scale, out, src, corr);
-  else k_dst_rows3t<3, N><<<grid, 256, sm, s>>>(T, work, hsep, scale, out, src, corr);
+  if (mode == 0) k_dst_rows3t<0, N><<<grid, 256, sm, s>>>(T, work, hsep, scale, out, src, corr, 0);
+  else if (mode == 1) k_dst_rows3t<1, N><<<grid, 256, sm, s>>>(T, work, hsep, scale, out, src, corr, 0);
+  else if (mode == 2) k_dst_rows3t<2, N><<<grid, 256, sm, s>>>(T, work, hsep, scale, out, src, corr, compact);
+  else k_dst_rows3t<3, N><<<grid, 256, sm, s>>>(T, work, hsep, scale, out, src, corr, compact);
 }
 void launch_dst_rows3(const DevTables3& T, int mode, double* work, const double* hsep, double scale, double* out,
-                      cudaStream_t s, const double* src, const double* corr) {
+                      cudaStream_t s, const double* src, const double* corr, bool compact) {
   ++g_launches;
+  const int cm = compact ? 1 : 0;
   switch (T.N) {
-    case 32: dst_rows3_n<32>(T, mode, work, hsep, scale, out, s, src, corr); break;
-    case 64: dst_rows3_n<64>(T, mode, work, hsep, scale, out, s, src, corr); break;
-    case 128: dst_rows3_n<128>(T, mode, work, hsep, scale, out, s, src, corr); break;
-    case 256: dst_rows3_n<256>(T, mode, work, hsep, scale, out, s, src, corr); break;
-    default: dst_rows3_n<512>(T, mode, work, hsep, scale, out, s, src, corr); break;
+    case 32: dst_rows3_n<32>(T, mode, work, hsep, scale, out, s, src, corr, cm); break;
+    case 64: dst_rows3_n<64>(T, mode, work, hsep, scale, out, s, src, corr, cm); break;
+    case 128: dst_rows3_n<128>(T, mode, work, hsep, scale, out, s, src, corr, cm); break;
+    case 256: dst_rows3_n<256>(T, mode, work, hsep, scale, out, s, src, corr, cm); break;
+    default: dst_rows3_n<512>(T, mode, work, hsep, scale, out, s, src, corr, cm); break;
   }
 }
 template <int N>

@@ -202,6 +202,10 @@ struct DevTables3 {
   double lo, h, kappa;
   const int32_t* q_axis;
   const double *q_pos, *q_n, *q_e1, *q_e2, *q_kab;
+  // Ω-compact rows (grid rows (i, a), N + 1 nodes each): as DevTables::om_row / om_info
+  const int32_t* om_row;
+  const uint32_t* om_info;
+  int om_nsegp;
   const int64_t* irr_lin;
   const int8_t* irr_side;
   const int32_t *irr_ptr, *pair_q;

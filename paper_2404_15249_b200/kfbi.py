@@ -342,7 +342,7 @@ class KFBI:
               max_restarts=50, u=None, stream=None, raise_on_noconv=True, method="gmres", gamma=1.0,
               async_final=False, omega_io=False):
         """omega_io: f_grid and u hold the Ω-node values only (omega_count() entries, row-major node
-        order; 2D single-context grids) and u is returned flat in that layout."""
+        order; single-context grids) and u is returned flat in that layout."""
         t = self.torch
         nf = self.omega_count() if omega_io else self.local_nodes
         g = self._dev(g, self.M)

@@ -87,12 +87,20 @@ def test_omega_io_solve_bit_exact(prob):
     assert np.array_equal(u_c.cpu().numpy(), u_full.cpu().numpy().reshape(-1)[mask])
 
 
-def test_omega_io_refused_in_3d():
-    from paper_2404_15249_b200 import KfbiError
-    k = _k(W.C4(64))
-    pz = k.points("ctrl")
-    g = torch.tensor(W.u_exact(*pz.T), device="cuda")
-    with pytest.raises(KfbiError):
-        k.solve(g, torch.zeros(k.omega_count(), dtype=torch.float64, device="cuda"),
-                torch.zeros(k.nq, dtype=torch.float64, device="cuda"),
-                torch.zeros(k.M, dtype=torch.float64, device="cuda"), omega_io=True)
+@pytest.mark.parametrize("prob", [W.C4(64), W.C5(128)], ids=lambda p: f"{p.name}{p.n}")
+def test_omega_io_solve_bit_exact_3d(prob):
+    """3D omega_io: the dense forward builds h²·f·1_Ω from the Ω-compact f (row bitmasks and counts) and
+    the final field stores u at the Ω ranks — equal to the full-grid solve bit for bit."""
+    k = _k(prob)
+    pz, pq = k.points("ctrl"), k.points("isect")
+    x = prob.lo + np.arange(prob.n + 1) * prob.h
+    X, Y, Z = np.meshgrid(x, x, x, indexing="ij")
+    f = W.f_exact(prob.kappa, X, Y, Z).ravel()
+    dev = lambda a: torch.tensor(np.ascontiguousarray(a), device="cuda")
+    g, fq, fz = dev(W.u_exact(*pz.T)), dev(W.f_exact(prob.kappa, *pq.T)), dev(W.f_exact(prob.kappa, *pz.T))
+    u_full, phi_full, st_full = k.solve(g, dev(f), fq, fz)
+    mask = k.node_mask().reshape(-1).astype(bool)
+    u_c, phi_c, st_c = k.solve(g, dev(f[mask]), fq, fz, omega_io=True)
+    assert u_c.numel() == k.omega_count() and st_c.iters == st_full.iters
+    assert torch.equal(phi_c, phi_full)
+    assert np.array_equal(u_c.cpu().numpy(), u_full.cpu().numpy().reshape(-1)[mask])

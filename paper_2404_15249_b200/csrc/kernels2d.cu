@@ -377,14 +377,18 @@ __global__ void __launch_bounds__(kSweepThreads, 2) k_sweep(DevTables T, const d
     const double2 cl = icp(LB - 1);
     double z1 = y1[LB - 1] * cl.x, z2 = y2[LB - 1] * cl.y;
     const double zl1 = z1, zl2 = z2;
-    if ((keep >> (LB - 1)) & 1)
-      *reinterpret_cast<double2*>(spec + (size_t)(c0 - 1 + LB - 1) * N + p1) = make_double2(z1, z2);
+    // the block's spectral rows by one pointer walked down a row per step (one 64-bit add per store
+    // instead of a row index product)
+    double2* zp = reinterpret_cast<double2*>(spec + (size_t)(c0 - 1 + LB - 1) * N + p1);
+    const size_t rowN = (size_t)N / 2;   // one spectral row in double2 units
+    if ((keep >> (LB - 1)) & 1) *zp = make_double2(z1, z2);
 #pragma unroll
     for (int p = LB - 2; p >= 0; --p) {
       const double2 c = icp(p);
       z1 = (y1[p] - z1) * c.x;
       z2 = (y2[p] - z2) * c.y;
-      if ((keep >> p) & 1) *reinterpret_cast<double2*>(spec + (size_t)(c0 - 1 + p) * N + p1) = make_double2(z1, z2);
+      zp -= rowN;
+      if ((keep >> p) & 1) *zp = make_double2(z1, z2);
     }
     *reinterpret_cast<double2*>(zB + (size_t)g * N + p1) = make_double2(z1, z2);
     if (g < T.P - 1) *reinterpret_cast<double2*>(zA + (size_t)g * N + p1) = make_double2(sep1 - zl1, sep2 - zl2);

@@ -105,8 +105,10 @@ struct kfbi_ctx {
   bool io_compact = false;         // inside kfbi_solve with opts.omega_io: f and u are Ω-compact
   const int8_t* d_side = nullptr;
   int64_t om_rows = 0, om_width = 0;
-  double* hcol_host = nullptr;   // host-mapped (written by k_copy, read after a stream sync)
-  double* hcol_map = nullptr;    // its device alias
+  double* hcol_host = nullptr;   // host-mapped (written by k_copy, read after a stream sync); the
+  double* hcol_map = nullptr;    // first kMaxRestart + 2 doubles for scalars, then one Hessenberg
+                                 // column slot per Arnoldi step (its device alias: hcol_map)
+  cudaEvent_t ev_step[2] = {nullptr, nullptr};   // end of Arnoldi steps j (j even / odd)
   // host staging of small tables (kept alive for the async uploads)
   std::vector<int32_t> coff, cM, hoff, hM;
   std::vector<double> cdel, hdel, oneh;
@@ -969,8 +971,10 @@ kfbi_status kfbi_set_workspace(kfbi_ctx* c, void* d_ws, size_t bytes) {
   cudaStream_t s = c->stream;
   for (auto& u : A.uploads) ck(cudaMemcpyAsync(u.first, u.second.first, u.second.second, cudaMemcpyHostToDevice, s), "upload");
   if (!c->hcol_host) {
-    ck(cudaHostAlloc(&c->hcol_host, (kMaxRestart + 2) * sizeof(double), cudaHostAllocMapped), "cudaHostAlloc");
+    ck(cudaHostAlloc(&c->hcol_host, (size_t)(kMaxRestart + 1) * (kMaxRestart + 2) * sizeof(double),
+                     cudaHostAllocMapped), "cudaHostAlloc");
     ck(cudaHostGetDevicePointer((void**)&c->hcol_map, c->hcol_host, 0), "cudaHostGetDevicePointer");
+    for (auto& e : c->ev_step) ck(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "event");
   }
   if (c->use_nccl && !c->comm) {   // a second kfbi_set_workspace keeps the communicator
     ckn(ncclCommInitRank(&c->comm, c->world, c->nccl_id, c->rank), "ncclCommInitRank");
@@ -1298,12 +1302,17 @@ kfbi_status kfbi_solve(kfbi_ctx* c, const double* d_g, const double* d_f_grid, c
     std::fill(gv.begin(), gv.end(), 0.0);
     gv[0] = beta;
     int jlast = o.restart - 1;
-    for (int j = 0; j < o.restart; ++j) {
+    // Arnoldi step j on the device: K v_j → w, MGS (deterministic reductions; one fused
+    // cluster for small M) → the Hessenberg column into mapped slot j.  The host runs one step behind:
+    // step j + 1 (whose input v_{j+1} is step j's MGS output, already on the stream) is enqueued before
+    // the host waits for step j and does its Givens update, unless the residual history predicts that
+    // step j converges — so the GPU does not idle through the per-step host round trip, nor
+    // through its mapped write when PCIe is busy with the serving loop's copies.  A step enqueued past
+    // convergence (mispredicted) changes nothing the solution reads and is not counted.
+    auto slot = [&](int j) { return (size_t)(kMaxRestart + 2) * (size_t)(j + 1); };
+    auto enqueue_step = [&](int j) {
       double* w = c->V + (size_t)(j + 1) * M;
       apply_KD(c, c->V + (size_t)j * M, w, s);
-      st.iters++;
-      st.n_applies++;
-      // MGS exactly as P:765-768, deterministic reductions (one fused CTA for small M)
       if (!launch_mgs_fused(M, j, c->V, w, c->hcol, s)) {
       for (int i = 0; i <= j; ++i)
         launch_mgs_step(M, w, i ? c->V + (size_t)(i - 1) * M : nullptr, c->V + (size_t)i * M,
@@ -1313,9 +1322,24 @@ kfbi_status kfbi_solve(kfbi_ctx* c, const double* d_g, const double* d_f_grid, c
                       c->partial + (size_t)(j + 1) * kRedBlocks, c->hcol + j, s);
       launch_norm_scale(M, w, c->partial + (size_t)(j + 1) * kRedBlocks, c->hcol + j + 1, s);
       }
-      launch_copy(j + 2, c->hcol, c->hcol_map, s);
-      ck(cudaStreamSynchronize(s), "sync hcol");
-      for (int i = 0; i <= j + 1; ++i) Hc(i, j) = c->hcol_host[i];
+      launch_copy(j + 2, c->hcol, c->hcol_map + slot(j), s);
+      ck(cudaEventRecord(c->ev_step[j & 1], s), "record step");
+    };
+    int enq = 1;           // steps enqueued in this cycle
+    double rho = 0.25;     // fastest residual reduction per step seen in this cycle (prediction)
+    enqueue_step(0);
+    for (int j = 0; j < o.restart; ++j) {
+      // speculate step j + 1 when the predicted residual after step j stays well above the target
+      const bool spec = enq == j + 1 && j + 1 < o.restart && std::fabs(gv[j]) * rho > 16.0 * o.tol * beta0;
+      if (spec) {
+        enqueue_step(j + 1);
+        enq = j + 2;
+      }
+      ck(cudaEventSynchronize(c->ev_step[j & 1]), "sync hcol");
+      st.iters++;
+      st.n_applies++;
+      const double* hc = c->hcol_host + slot(j);
+      for (int i = 0; i <= j + 1; ++i) Hc(i, j) = hc[i];
       for (int i = 0; i < j; ++i) {   // previous Givens rotations
         const double a = Hc(i, j), b = Hc(i + 1, j);
         Hc(i, j) = cs[i] * a + sn[i] * b;
@@ -1327,10 +1351,16 @@ kfbi_status kfbi_solve(kfbi_ctx* c, const double* d_g, const double* d_f_grid, c
       sn[j] = hnext / rr;
       Hc(j, j) = rr;
       Hc(j + 1, j) = 0.0;
+      const double gj = gv[j];
       gv[j + 1] = -sn[j] * gv[j];
       gv[j] = cs[j] * gv[j];
       if (!std::isfinite(gv[j + 1])) throw BreakdownError("non-finite GMRES residual");
       if (std::fabs(gv[j + 1]) <= o.tol * beta0 || hnext <= 1e-14 * beta0) { jlast = j; break; }
+      if (gj != 0.0) rho = std::min(rho, std::fabs(gv[j + 1] / gj));
+      if (enq == j + 1 && j + 1 < o.restart) {   // not speculated: enqueue step j + 1 now
+        enqueue_step(j + 1);
+        enq = j + 2;
+      }
     }
     const int k = jlast + 1;
     for (int i = k - 1; i >= 0; --i) {
@@ -1522,6 +1552,8 @@ kfbi_status kfbi_destroy(kfbi_ctx* c) {
   DeviceGuard g(c->device);
   if (c->comm) ncclCommDestroy(c->comm);
   if (c->hcol_host) cudaFreeHost(c->hcol_host);
+  for (auto& e : c->ev_step)
+    if (e) cudaEventDestroy(e);
   delete c;
   return KFBI_OK;
 }

@@ -184,6 +184,28 @@ def test_solve_matches_oracle(prob):
     assert np.abs(u[m] - W.u_exact(X, Y)[m]).max() < 50 * prob.h ** 2
 
 
+@pytest.mark.parametrize("prob,restart", [(W.C1(64), 4), (W.C2(512), 5)], ids=["C1-r4", "C2-r5"])
+def test_restarted_solve_matches_oracle(prob, restart):
+    """GMRES(m) with restarts shorter than the iteration count (Alg. 5): the host's one-step-
+    ahead enqueue of Arnoldi steps crosses cycle boundaries and convergence inside a cycle; the solve
+    matches the oracle's GMRES(m) to 1e-8 with the iteration and restart counts within ±1."""
+    o, k = oracle(prob), gpu(prob)
+    n = prob.n
+    f = lambda x, y: W.f_exact(prob.kappa, x, y)
+    zx, zy = o.ctrl_points()
+    u_ref, phi_ref, s_ref = o.solve(W.u_exact(zx, zy), f, restart=restart)
+    pz, pq = k.points("ctrl"), k.points("isect")
+    x = prob.lo + np.arange(n + 1) * prob.h
+    X, Y = np.meshgrid(x, x, indexing="ij")
+    u, phi, s = k.solve(W.u_exact(pz[:, 0], pz[:, 1]), f(X, Y), f(pq[:, 0], pq[:, 1]), f(pz[:, 0], pz[:, 1]),
+                        restart=restart)
+    print(f"{prob.name} GMRES({restart}): {s.iters} iterations, {s.restarts} cycles (oracle {s_ref.iters}, "
+          f"{s_ref.restarts})")
+    assert s.converged and s.restarts > 1 and abs(s.iters - s_ref.iters) <= 1
+    assert rel(u.cpu().numpy()[o.st.side], u_ref[o.st.side]) < 1e-8
+    assert rel(phi.cpu().numpy(), phi_ref) < 1e-8
+
+
 @pytest.mark.slow
 def test_solve_full_size_C3():
     """The bench workload itself: C3 8192² (κ = 0, two holes, hole completion R27) solved by

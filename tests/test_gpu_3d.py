@@ -101,6 +101,23 @@ def test_solve3d_matches_oracle(prob):
     assert rel(phi.cpu().numpy(), phi_ref) < 1e-8
 
 
+def test_restarted_solve3d_matches_oracle():
+    """3D GMRES(m) with m shorter than the iteration count (one-step-ahead Arnoldi enqueue across cycle
+    boundaries): C4 64³ with m = 6 against the oracle's GMRES(6)."""
+    prob = W.C4(64)
+    o, k = oracle(prob), gpu(prob)
+    f = lambda a, b, c: W.f_exact(prob.kappa, a, b, c)
+    u_ref, phi_ref, s_ref = o.solve(W.u_exact(*o.points().T), f, restart=6)
+    X, Y, Z = _grid(prob)
+    p = k.points("ctrl")
+    u, phi, s = k.solve(W.u_exact(*p.T), f(X, Y, Z), f(*p.T), f(*p.T), restart=6)
+    m = o.st.side
+    print(f"C4 GMRES(6): {s.iters} iterations, {s.restarts} cycles (oracle {s_ref.iters}, {s_ref.restarts})")
+    assert s.converged and s.restarts > 1 and abs(s.iters - s_ref.iters) <= 1
+    assert rel(u.cpu().numpy()[m], u_ref[m]) < 1e-8
+    assert rel(phi.cpu().numpy(), phi_ref) < 1e-8
+
+
 @pytest.mark.slow
 def test_interface_solve3d_full_size_C5():
     """Full-size C5 (512³): the piecewise-quadratic witness holds at any size."""

@@ -7,6 +7,7 @@
 #include <climits>
 #include <chrono>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -109,6 +110,18 @@ struct kfbi_ctx {
   double* hcol_map = nullptr;    // first kMaxRestart + 2 doubles for scalars, then one Hessenberg
                                  // column slot per Arnoldi step (its device alias: hcol_map)
   cudaEvent_t ev_step[2] = {nullptr, nullptr};   // end of Arnoldi steps j (j even / odd)
+  // Arnoldi step j (K v_j → v_{j+1}, MGS, Hessenberg column → mapped slot j) as one CUDA graph per j,
+  // captured on first use (the step's pointers are fixed per j for a workspace); single-process contexts
+  // only (no NCCL inside a capture).  launches = the library kernels one replay runs (kfbi_launch_count).
+  struct StepGraph {
+    cudaGraphExec_t exec = nullptr;
+    long long launches = 0;
+  };
+  std::vector<StepGraph> step_graphs;
+  bool graphs_off = [] {   // KFBI_GRAPHS=0: eager launches (A/B runs)
+    const char* e = std::getenv("KFBI_GRAPHS");
+    return e != nullptr && e[0] == '0';
+  }();
   // host staging of small tables (kept alive for the async uploads)
   std::vector<int32_t> coff, cM, hoff, hM;
   std::vector<double> cdel, hdel, oneh;
@@ -958,11 +971,18 @@ kfbi_status kfbi_workspace_size(const kfbi_ctx* ctx, size_t* bytes) {
   return KFBI_OK;
 }
 
+void drop_step_graphs(kfbi_ctx* c) {
+  for (auto& g : c->step_graphs)
+    if (g.exec) cudaGraphExecDestroy(g.exec);
+  c->step_graphs.clear();
+}
+
 kfbi_status kfbi_set_workspace(kfbi_ctx* c, void* d_ws, size_t bytes) {
   if (!c || !d_ws) return KFBI_EINVAL;
   if (bytes < c->ws_need) return fail(c, KFBI_ENOMEM, "workspace too small");
   if (((uintptr_t)d_ws) & 255) return fail(c, KFBI_EINVAL, "workspace must be 256-byte aligned");
   KFBI_TRY(c)
+  drop_step_graphs(c);   // captured pointers refer to the previous workspace
   c->ws = (uint8_t*)d_ws;
   c->ws_bytes = bytes;
   Arena A{c->ws, 0, true};
@@ -1310,7 +1330,7 @@ kfbi_status kfbi_solve(kfbi_ctx* c, const double* d_g, const double* d_f_grid, c
     // through its mapped write when PCIe is busy with the serving loop's copies.  A step enqueued past
     // convergence (mispredicted) changes nothing the solution reads and is not counted.
     auto slot = [&](int j) { return (size_t)(kMaxRestart + 2) * (size_t)(j + 1); };
-    auto enqueue_step = [&](int j) {
+    auto step_body = [&](int j) {
       double* w = c->V + (size_t)(j + 1) * M;
       apply_KD(c, c->V + (size_t)j * M, w, s);
       if (!launch_mgs_fused(M, j, c->V, w, c->hcol, s)) {
@@ -1323,6 +1343,42 @@ kfbi_status kfbi_solve(kfbi_ctx* c, const double* d_g, const double* d_f_grid, c
       launch_norm_scale(M, w, c->partial + (size_t)(j + 1) * kRedBlocks, c->hcol + j + 1, s);
       }
       launch_copy(j + 2, c->hcol, c->hcol_map + slot(j), s);
+    };
+    auto enqueue_step = [&](int j) {
+      if (!c->use_nccl && !c->graphs_off) {
+        if ((int)c->step_graphs.size() <= j) c->step_graphs.resize(kMaxRestart);
+        auto& g = c->step_graphs[j];
+        if (!g.exec) {   // capture once; on any capture failure fall back to eager launches for good
+          const long long l0 = g_launches;
+          cudaGraph_t graph = nullptr;
+          bool ok = cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal) == cudaSuccess;
+          if (ok) {
+            try {
+              step_body(j);
+            } catch (...) {
+              ok = false;
+            }
+            ok = cudaStreamEndCapture(s, &graph) == cudaSuccess && ok;
+            ok = ok && graph && cudaGraphInstantiate(&g.exec, graph, 0) == cudaSuccess;
+            if (graph) cudaGraphDestroy(graph);
+          }
+          g.launches = g_launches - l0;
+          g_launches = l0;
+          if (!ok) {
+            cudaGetLastError();
+            if (g.exec) cudaGraphExecDestroy(g.exec);
+            g.exec = nullptr;
+            c->graphs_off = true;
+          }
+        }
+        if (g.exec) {
+          ck(cudaGraphLaunch(g.exec, s), "graph launch");
+          g_launches += g.launches;
+          ck(cudaEventRecord(c->ev_step[j & 1], s), "record step");
+          return;
+        }
+      }
+      step_body(j);
       ck(cudaEventRecord(c->ev_step[j & 1], s), "record step");
     };
     int enq = 1;           // steps enqueued in this cycle
@@ -1551,6 +1607,7 @@ kfbi_status kfbi_destroy(kfbi_ctx* c) {
   if (!c) return KFBI_OK;
   DeviceGuard g(c->device);
   if (c->comm) ncclCommDestroy(c->comm);
+  drop_step_graphs(c);
   if (c->hcol_host) cudaFreeHost(c->hcol_host);
   for (auto& e : c->ev_step)
     if (e) cudaEventDestroy(e);

@@ -24,6 +24,7 @@
 
 #include <cstdio>
 #include <cstdlib>
+#include <utility>
 
 #include "device.cuh"
 #include "kernels.h"
@@ -45,6 +46,11 @@ __device__ __forceinline__ void spline_eval2(const double* __restrict__ phi, con
 struct Jump6 {
   double v, vx, vy, vxx, vxy, vyy;
 };
+
+// programmatic dependent launch: a kernel launched with PDL runs its prologue (shared tables from setup
+// constants) while its predecessor drains, then waits here for the predecessor's results (a no-op when
+// launched normally)
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 
 // Closed form of the appendix 2×2 + 3×3 systems (reading R7 ψ for ψ_s):
 //   [v] = Φ, [∇v] = Φ_s τ + Ψ n, frame components A_ττ, A_τn, A_nn, [D²v] = F A Fᵀ.
@@ -72,6 +78,7 @@ __global__ void k_spline(DevTables T, const double* __restrict__ phi, double* __
                          const double* __restrict__ hdelta, double* __restrict__ ahole) {
   if ((int)blockIdx.x < nh) {   // hole blocks first: they are the longest, the spline blocks fill in
     __shared__ double scratch[32];
+    pdl_wait();   // φ from the previous kernel
     const int hh = blockIdx.x;
     const int cnt = hcnt[hh], o = hoff[hh];
     double v[1] = {0.0};
@@ -91,6 +98,7 @@ __global__ void k_spline(DevTables T, const double* __restrict__ phi, double* __
   const int gt = (blockIdx.x - nh) * blockDim.x + threadIdx.x;
   const int m = gt / kSplineLanes, sub = gt % kSplineLanes;
   double acc = 0.0;
+  if (m >= T.M) pdl_wait();
   if (m < T.M) {
     const int c = T.z_comp[m], ml = T.z_knot[m];
     const int off = T.c_off[c], Mc = T.c_M[c], nt = T.sp_ntaps[c], first = T.sp_first[c];
@@ -100,14 +108,13 @@ __global__ void k_spline(DevTables T, const double* __restrict__ phi, double* __
     constexpr int U = 64 / kSplineLanes;
     double bv[U], pv[U];
 #pragma unroll
+    for (int u = 0; u < U; ++u) bv[u] = sub + kSplineLanes * u < nt ? b[sub + kSplineLanes * u] : 0.0;
+    pdl_wait();   // φ from the previous kernel (the filter taps above are setup constants)
+#pragma unroll
     for (int u = 0; u < U; ++u) {
       const int r = sub + kSplineLanes * u;
-      bv[u] = 0.0;
       pv[u] = 0.0;
-      if (r < nt) {
-        bv[u] = b[r];
-        pv[u] = phi[off + (base + kSplineLanes * u) % Mc];
-      }
+      if (r < nt) pv[u] = phi[off + (base + kSplineLanes * u) % Mc];
     }
 #pragma unroll
     for (int u = 0; u < U; ++u) acc = fma(bv[u], pv[u], acc);
@@ -121,6 +128,7 @@ __global__ void k_spline(DevTables T, const double* __restrict__ phi, double* __
 __global__ void k_correct(DevTables T, const double* __restrict__ phi, const double* __restrict__ mk,
                           const double* __restrict__ fq, const double* __restrict__ jqg, double* __restrict__ cval) {
   int n = T.irr_lo + blockIdx.x * blockDim.x + threadIdx.x;   // the slab's irregular nodes
+  pdl_wait();   // φ and the spline knots M from k_spline
   if (n >= T.irr_hi) return;
   double acc = 0.0;
   for (int e = T.irr_ptr[n]; e < T.irr_ptr[n + 1]; ++e) {
@@ -224,6 +232,7 @@ __global__ void __launch_bounds__(kSweepThreads, 2) k_sweep(DevTables T, const d
   };
   int4 nm = make_int4(-1, 0, 0, 0);
   meta(0, nm);
+  pdl_wait();   // the corrections (k_correct) and the dense source are ready
   for (int rnd = 0; rnd * G < T.P; ++rnd) {
   const int g = nm.x, e0 = nm.y, e1m = nm.z;
   const int keep = D.stencil_only ? nm.w : 0x7fff;   // positions whose spectral rows are stored
@@ -439,17 +448,18 @@ __global__ void __launch_bounds__(kRed2Modes * kMaxSeg) k_reduced2(DevTables T, 
   const int kk = ok ? k : 1;
   const double a = T.red_a[kk];
   const int gbase = sg * BL2;
-  // all of this segment's right-hand sides first (independent loads, one round trip), while the
-  // per-mode pivot and spike rows (shared by the S segments) are staged once per CTA
+  // the per-mode pivot and spike rows (setup tables, shared by the S segments) are staged once per CTA
+  // while the sweep drains (PDL), then all of this segment's right-hand sides in one batch
+  for (int p = sg; p < LB2; p += blockDim.y) {
+    s_rinv[p][lane] = T.rinv2[(size_t)p * N + kk];
+    s_z2r[p][lane] = T.z2r[(size_t)p * N + kk];
+  }
+  pdl_wait();   // zA, zB from k_sweep
   double z[LB2];
 #pragma unroll
   for (int p = 0; p < LB2; ++p) {
     const int g = gbase + p;
     z[p] = zA[(size_t)g * N + kk] - zB[(size_t)(g + 1) * N + kk];
-  }
-  for (int p = sg; p < LB2; p += blockDim.y) {
-    s_rinv[p][lane] = T.rinv2[(size_t)p * N + kk];
-    s_z2r[p][lane] = T.z2r[(size_t)p * N + kk];
   }
   double rsep = 0.0;
   if (sg < S - 1) {
@@ -654,6 +664,7 @@ __global__ void __launch_bounds__(kInvThreads, 2) k_inv_sparse(DevTables T, cons
     return it;
   };
   Item nx = item(0);
+  pdl_wait();   // the spectral rows (k_sweep) and separators (k_reduced2 / the level-2 fix-up) are ready
   for (int rnd = 0; rnd * G < nit; ++rnd) {
   const Item cur = nx;
   nx = item(rnd + 1);
@@ -836,6 +847,7 @@ __global__ void k_interp(DevTables T, const double* __restrict__ phi, const doub
   if (partial) {   // multi-GPU: a control point whose stencil columns c − 1 … c + 1 miss the slab adds 0
     const int col = T.sn_i[T.st_node[m * 6]];
     if (col + 1 < T.col_lo || col - 1 > T.col_hi) {
+      pdl_wait();
       double acc = 0.0;   // rank 0 still adds the hole-completion term (R27) of every control point
       if (T.rank == 0)
         for (int hh = 0; hh < nh; ++hh) acc = fma(ahole[hh], wg[(size_t)hh * T.M + m], acc);
@@ -857,6 +869,7 @@ __global__ void k_interp(DevTables T, const double* __restrict__ phi, const doub
     dy[p] = T.st_dy[idx];
     wt[p] = T.neumann ? T.st_wn[idx] : T.st_w[idx];   // V⁺ or ∂_n V⁺ (Neumann, R38)
   }
+  pdl_wait();   // vsten (k_inv_sparse), the spline knots and hole coefficients (k_spline)
 #pragma unroll
   for (int p = 0; p < 6; ++p) {
     KFBI_CHECK(sn[p] >= 0 && sn[p] < T.nsn, sn[p], T.nsn);
@@ -1448,16 +1461,37 @@ inline int cdiv(long a, long b) { return (int)((a + b - 1) / b); }
 
 // ============================================================================== launchers
 long long g_launches = 0;
+// launch with programmatic stream serialization (PDL): the kernel may start while its predecessor's
+// last CTAs finish; it calls pdl_wait() before touching the predecessor's results
+template <class... KArgs, class... Args>
+void launch_pdl(void (*k)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s, Args&&... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  static const bool on = [] {   // KFBI_PDL=0: plain serialised launches (A/B runs)
+    const char* e = std::getenv("KFBI_PDL");
+    return !(e != nullptr && e[0] == '0');
+  }();
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = on ? 1 : 0;
+  cudaLaunchKernelEx(&cfg, k, std::forward<Args>(args)...);
+}
+
 void launch_spline(const DevTables& T, const double* phi, double* mk, cudaStream_t s, const int* hole_off,
                    const int* hole_M, const double* hole_delta, int nh, double* ahole) {
   const int nsb = cdiv(T.M * kSplineLanes, 256);
-  { ++g_launches; k_spline<<<nsb + nh, 256, 0, s>>>(T, phi, mk, nh, hole_off, hole_M, hole_delta, ahole); }
+  { ++g_launches; launch_pdl(k_spline, dim3(nsb + nh), dim3(256), 0, s, T, phi, mk, nh, hole_off, hole_M, hole_delta, ahole); }
 }
 
 void launch_correct(const DevTables& T, const double* phi, const double* mk, const double* fq,
                     const double* jq_given, double* cval, cudaStream_t s) {
   if (T.irr_hi <= T.irr_lo) return;
-  { ++g_launches; k_correct<<<cdiv(T.irr_hi - T.irr_lo, 128), 128, 0, s>>>(T, phi, mk, fq, jq_given, cval); }
+  { ++g_launches; launch_pdl(k_correct, dim3(cdiv(T.irr_hi - T.irr_lo, 128)), dim3(128), 0, s, T, phi, mk, fq, jq_given, cval); }
 }
 
 
@@ -1478,9 +1512,9 @@ void launch_sweep(const DevTables& T, const double* cval, const DenseSrc& D, dou
   if (G > T.g_hi - T.g_lo) G = T.g_hi - T.g_lo;
   const int grid = nch * G;
   ++g_launches;
-  if (dense == 2) k_sweep<2><<<grid, kSweepThreads, sm, s>>>(T, cval, D, spec, zfirst, fsep);
-  else if (dense == 1) k_sweep<1><<<grid, kSweepThreads, sm, s>>>(T, cval, D, spec, zfirst, fsep);
-  else k_sweep<0><<<grid, kSweepThreads, sm, s>>>(T, cval, D, spec, zfirst, fsep);
+  if (dense == 2) launch_pdl(k_sweep<2>, grid, kSweepThreads, sm, s, T, cval, D, spec, zfirst, fsep);
+  else if (dense == 1) launch_pdl(k_sweep<1>, grid, kSweepThreads, sm, s, T, cval, D, spec, zfirst, fsep);
+  else launch_pdl(k_sweep<0>, grid, kSweepThreads, sm, s, T, cval, D, spec, zfirst, fsep);
 }
 
 void launch_reduced(const DevTables& T, const double* zfirst, const double* zlast, const double* fsep, double* hsep,
@@ -1489,7 +1523,7 @@ void launch_reduced(const DevTables& T, const double* zfirst, const double* zlas
   if (T.P < 2) return;
   if (T.P >= 2 * BL2 && T.P % BL2 == 0 && T.P / BL2 <= kMaxSeg) {
     dim3 blk(kRed2Modes, T.P / BL2);
-    { ++g_launches; k_reduced2<<<cdiv(T.N - 1, kRed2Modes), blk, 0, s>>>(T, zfirst, fsep, hsep); }
+    { ++g_launches; launch_pdl(k_reduced2, dim3(cdiv(T.N - 1, kRed2Modes)), blk, 0, s, T, zfirst, fsep, hsep); }
   } else {
     { ++g_launches; k_reduced_small<<<cdiv(T.N - 1, 64), 64, 0, s>>>(T, zfirst, fsep, hsep); }
   }
@@ -1506,10 +1540,10 @@ void launch_inverse_sparse(const DevTables& T, const double* spec, const double*
   const size_t sm = (size_t)(T.N + T.N / 16 + 1) * sizeof(double) + red_b;
   ++g_launches;
   switch (qpt) {
-    case 1: smem_optin((const void*)k_inv_sparse<1>, sm); k_inv_sparse<1><<<grid, kInvThreads, sm, s>>>(T, spec, hsep, vsten); break;
-    case 2: smem_optin((const void*)k_inv_sparse<2>, sm); k_inv_sparse<2><<<grid, kInvThreads, sm, s>>>(T, spec, hsep, vsten); break;
-    case 4: smem_optin((const void*)k_inv_sparse<4>, sm); k_inv_sparse<4><<<grid, kInvThreads, sm, s>>>(T, spec, hsep, vsten); break;
-    case 8: smem_optin((const void*)k_inv_sparse<8>, sm); k_inv_sparse<8><<<grid, kInvThreads, sm, s>>>(T, spec, hsep, vsten); break;
+    case 1: smem_optin((const void*)k_inv_sparse<1>, sm); launch_pdl(k_inv_sparse<1>, grid, kInvThreads, sm, s, T, spec, hsep, vsten); break;
+    case 2: smem_optin((const void*)k_inv_sparse<2>, sm); launch_pdl(k_inv_sparse<2>, grid, kInvThreads, sm, s, T, spec, hsep, vsten); break;
+    case 4: smem_optin((const void*)k_inv_sparse<4>, sm); launch_pdl(k_inv_sparse<4>, grid, kInvThreads, sm, s, T, spec, hsep, vsten); break;
+    case 8: smem_optin((const void*)k_inv_sparse<8>, sm); launch_pdl(k_inv_sparse<8>, grid, kInvThreads, sm, s, T, spec, hsep, vsten); break;
     default: break;
   }
 }
@@ -1554,7 +1588,7 @@ void launch_hole_coeffs(const DevTables& T, const int* hole_off, const int* hole
 void launch_interp(const DevTables& T, const double* phi, const double* mk, const double* fz, const double* jz_given,
                    const double* vsten, int nh, const double* wg, const double* a, double* out, cudaStream_t s,
                    bool partial) {
-  { ++g_launches; k_interp<<<cdiv(T.M, 128), 128, 0, s>>>(T, phi, mk, fz, jz_given, vsten, wg ? nh : 0, wg, a, out, partial ? 1 : 0); }
+  { ++g_launches; launch_pdl(k_interp, dim3(cdiv(T.M, 128)), dim3(128), 0, s, T, phi, mk, fz, jz_given, vsten, wg ? nh : 0, wg, a, out, partial ? 1 : 0); }
 }
 
 void launch_mgs_step(int n, double* w, const double* Vprev, const double* Vcur, const double* partial_prev,

@@ -5,6 +5,7 @@
 #pragma once
 #include <cuda_runtime.h>
 
+#include <cstdlib>
 #include <map>
 #include <mutex>
 #include <tuple>
@@ -527,6 +528,32 @@ __device__ __forceinline__ void dst1s_core(double2* z, const double2* __restrict
   __syncthreads();
 }
 
+
+// programmatic dependent launch: a kernel launched by launch_pdl() runs its prologue (shared tables from
+// setup constants) while its predecessor drains, then waits here for the predecessor's results (a no-op
+// when launched normally).  Nothing before the wait may write memory the predecessor touches.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+
+// launch with programmatic stream serialization (PDL): the kernel may start while its predecessor's
+// last CTAs finish; it calls pdl_wait() before touching the predecessor's results
+template <class... KArgs, class... Args>
+void launch_pdl(void (*k)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s, Args&&... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  static const bool on = [] {   // KFBI_PDL=0: plain serialised launches (A/B runs)
+    const char* e = std::getenv("KFBI_PDL");
+    return !(e != nullptr && e[0] == '0');
+  }();
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = on ? 1 : 0;
+  cudaLaunchKernelEx(&cfg, k, std::forward<Args>(args)...);
+}
 
 // Host-side launch caches, kept per device: the shared-memory opt-in of a kernel, its occupancy and
 // the SM count belong to one device, and one process may drive contexts on several GPUs.

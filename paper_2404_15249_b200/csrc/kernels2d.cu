@@ -47,10 +47,6 @@ struct Jump6 {
   double v, vx, vy, vxx, vxy, vyy;
 };
 
-// programmatic dependent launch: a kernel launched with PDL runs its prologue (shared tables from setup
-// constants) while its predecessor drains, then waits here for the predecessor's results (a no-op when
-// launched normally)
-__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 
 // Closed form of the appendix 2×2 + 3×3 systems (reading R7 ψ for ψ_s):
 //   [v] = Φ, [∇v] = Φ_s τ + Ψ n, frame components A_ττ, A_τn, A_nn, [D²v] = F A Fᵀ.
@@ -1351,6 +1347,7 @@ __global__ void __cluster_dims__(kMgsCl, 1, 1) __launch_bounds__(kMgsClThreads)
     k_mgs_cluster(int n, int j, const double* __restrict__ V, double* w, double* hcol) {
   namespace cg = cooperative_groups;
   cg::cluster_group cl = cg::this_cluster();
+  pdl_wait();   // w from the apply's k_interp
   __shared__ double warp_part[kMgsClThreads / 32];
   __shared__ double slot[2][kMgsCl];
   const int rank = (int)cl.block_rank(), lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
@@ -1461,26 +1458,6 @@ inline int cdiv(long a, long b) { return (int)((a + b - 1) / b); }
 
 // ============================================================================== launchers
 long long g_launches = 0;
-// launch with programmatic stream serialization (PDL): the kernel may start while its predecessor's
-// last CTAs finish; it calls pdl_wait() before touching the predecessor's results
-template <class... KArgs, class... Args>
-void launch_pdl(void (*k)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s, Args&&... args) {
-  cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = grid;
-  cfg.blockDim = block;
-  cfg.dynamicSmemBytes = smem;
-  cfg.stream = s;
-  static const bool on = [] {   // KFBI_PDL=0: plain serialised launches (A/B runs)
-    const char* e = std::getenv("KFBI_PDL");
-    return !(e != nullptr && e[0] == '0');
-  }();
-  cudaLaunchAttribute at[1];
-  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-  at[0].val.programmaticStreamSerializationAllowed = 1;
-  cfg.attrs = at;
-  cfg.numAttrs = on ? 1 : 0;
-  cudaLaunchKernelEx(&cfg, k, std::forward<Args>(args)...);
-}
 
 void launch_spline(const DevTables& T, const double* phi, double* mk, cudaStream_t s, const int* hole_off,
                    const int* hole_M, const double* hole_delta, int nh, double* ahole) {
@@ -1599,10 +1576,10 @@ void launch_mgs_step(int n, double* w, const double* Vprev, const double* Vcur, 
 bool launch_mgs_fused(int n, int j, const double* V, double* w, double* hcol, cudaStream_t s) {
   const int per = (n + kMgsCl * kMgsClThreads - 1) / (kMgsCl * kMgsClThreads);   // elements per thread
   switch (per <= 1 ? 1 : per <= 2 ? 2 : per <= 4 ? 4 : per <= 8 ? 8 : 0) {
-    case 1: ++g_launches; k_mgs_cluster<1><<<kMgsCl, kMgsClThreads, 0, s>>>(n, j, V, w, hcol); return true;
-    case 2: ++g_launches; k_mgs_cluster<2><<<kMgsCl, kMgsClThreads, 0, s>>>(n, j, V, w, hcol); return true;
-    case 4: ++g_launches; k_mgs_cluster<4><<<kMgsCl, kMgsClThreads, 0, s>>>(n, j, V, w, hcol); return true;
-    case 8: ++g_launches; k_mgs_cluster<8><<<kMgsCl, kMgsClThreads, 0, s>>>(n, j, V, w, hcol); return true;
+    case 1: ++g_launches; launch_pdl(k_mgs_cluster<1>, dim3(kMgsCl), dim3(kMgsClThreads), 0, s, n, j, V, w, hcol); return true;
+    case 2: ++g_launches; launch_pdl(k_mgs_cluster<2>, dim3(kMgsCl), dim3(kMgsClThreads), 0, s, n, j, V, w, hcol); return true;
+    case 4: ++g_launches; launch_pdl(k_mgs_cluster<4>, dim3(kMgsCl), dim3(kMgsClThreads), 0, s, n, j, V, w, hcol); return true;
+    case 8: ++g_launches; launch_pdl(k_mgs_cluster<8>, dim3(kMgsCl), dim3(kMgsClThreads), 0, s, n, j, V, w, hcol); return true;
     default: return false;
   }
 }

@@ -357,6 +357,7 @@ __global__ void __launch_bounds__(256, 2) k_fwd3s(DevTables3 T, const double* __
   int16_t* s_b = reinterpret_cast<int16_t*>(s_val + T.max_plane_irr);
   const int E0 = T.irr_row_ptr[(size_t)(i - 1) * N];
   for (int a = threadIdx.x; a <= N; a += NTHR) s_ptr[a] = T.irr_row_ptr[(size_t)(i - 1) * N + a] - E0;
+  pdl_wait();   // the corrections from k_correct3
   {
     const int ne = T.irr_row_ptr[(size_t)i * N] - E0;
     for (int e = threadIdx.x; e < ne; e += NTHR) {
@@ -484,6 +485,7 @@ __global__ void __launch_bounds__(256, KFBI_INV3Y_MINB) k_inv3y(DevTables3 T, co
   const int w0 = T.zplane_ptr[i - 1], nn = T.zplane_ptr[i] - w0;
   if (nn == 0) return;   // no stencil row in the plane (CTA-uniform, before any barrier)
   for (int w = threadIdx.x; w < nn; w += NTHR) s_row[w] = (int16_t)(T.zrow_id[w0 + w] - (i - 1) * N);
+  pdl_wait();   // the spectrum (k_sweep3) and the separators (k_reduced3 / the level-2 fix-up)
   load_fixed_row<N>(T, spec, hsep, i, m0, z, tid);
   __syncwarp();
   dst2_core<N>(z, tw, tid);
@@ -522,6 +524,7 @@ __global__ void __launch_bounds__(256) k_zeval3(DevTables3 T, const double* __re
     }
   };
   int w = T.w_lo + (int)(((size_t)blockIdx.x * 256 + threadIdx.x) >> 5);
+  pdl_wait();   // the y-inverse rows from k_inv3y
   if (w >= T.w_hi) return;
   double cur[S][U];
   load(w, cur);
@@ -625,6 +628,7 @@ __global__ void __launch_bounds__(kSweep3Threads) k_sweep3(DevTables3 T, double*
       ic[p] = 1.0 / c;
     }
   }
+  pdl_wait();   // the spectrum from k_fwd3s (the pivots above come from the setup table dk)
   // the next block's LB source planes and its separator plane are loaded while this block is solved
   // and stored (software pipelining: twice the loads in flight per thread)
   auto load = [&](int g, double (&x)[BL]) {
@@ -909,10 +913,11 @@ static void sparse3_n(const DevTables3& T, int which, const double* src, const d
     const size_t sm0 = sm + (size_t)T.max_plane_irr * (sizeof(double) + sizeof(int16_t));
     smem_optin((const void*)k_fwd3s<N>, sm0);
     const dim3 gridf((N / RPC + kFwdGroups - 1) / kFwdGroups, T.i_hi - T.i_lo + 1);
-    k_fwd3s<N><<<gridf, NTHR, sm0, s>>>(T, src, dst);
+    launch_pdl(k_fwd3s<N>, gridf, dim3(NTHR), sm0, s, T, src, dst);
   }
-  else if (which == 1) k_inv3y<N><<<grid, NTHR, sm, s>>>(T, src, hsep, scale, dst);
-  else if (T.w_hi > T.w_lo) k_zeval3<N><<<std::min(cdiv3(T.w_hi - T.w_lo, 8), num_sms() * 2), 256, 0, s>>>(T, src, scale, dst);
+  else if (which == 1) launch_pdl(k_inv3y<N>, grid, dim3(NTHR), sm, s, T, src, hsep, scale, dst);
+  else if (T.w_hi > T.w_lo)
+    launch_pdl(k_zeval3<N>, dim3(std::min(cdiv3(T.w_hi - T.w_lo, 8), num_sms() * 2)), dim3(256), 0, s, T, src, scale, dst);
 }
 // which: 0 forward (corr → work), 1 inverse along y (work, hsep → work2), 2 z-evaluation (work2 → work)
 void launch_sparse3(const DevTables3& T, int which, const double* src, const double* hsep, double scale, double* dst,
@@ -934,7 +939,8 @@ void launch_transpose3(const DevTables3& T, double* work, cudaStream_t s) {
 }
 void launch_sweep3(const DevTables3& T, double* work, double* zB, double* zA, cudaStream_t s, bool sparse) {
   ++g_launches;
-  k_sweep3<<<dim3(cdiv3((long)T.N * T.N, kSweep3Threads), std::max(1, std::min(KFBI_SWEEP3_SPLIT, T.b_hi - T.b_lo))), kSweep3Threads, 0, s>>>(T, work, zB, zA, sparse);
+  launch_pdl(k_sweep3, dim3(cdiv3((long)T.N * T.N, kSweep3Threads), std::max(1, std::min(KFBI_SWEEP3_SPLIT, T.b_hi - T.b_lo))),
+             dim3(kSweep3Threads), 0, s, T, work, zB, zA, sparse);
 }
 void launch_reduced3(const DevTables3& T, const double* zB, const double* zA, double* hsep, cudaStream_t s) {
   if (T.P < 2) return;

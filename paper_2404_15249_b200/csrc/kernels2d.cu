@@ -1439,6 +1439,7 @@ __global__ void k_axpy_basis(int n, int k, const double* __restrict__ V, int ldv
 // plain copy on the SMs (device or host-mapped memory): keeps the solve's small transfers off the copy
 // engines, which a concurrent bulk H2D/D2H (pipelined serving) would otherwise queue them behind
 __global__ void k_copy(int n, const double* __restrict__ src, double* __restrict__ dst) {
+  pdl_wait();   // src from the previous kernel
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) dst[i] = src[i];
 }
 
@@ -1604,7 +1605,7 @@ void launch_axpy_basis(int n, int k, const double* V, int ldv, const double* y_h
 void launch_copy(int n, const double* src, double* dst, cudaStream_t s) {
   if (n <= 0) return;
   const int grid = cdiv(n, 256) < 4 * num_sms() ? cdiv(n, 256) : 4 * num_sms();
-  { ++g_launches; k_copy<<<grid, 256, 0, s>>>(n, src, dst); }
+  { ++g_launches; launch_pdl(k_copy, dim3(grid), dim3(256), 0, s, n, src, dst); }
 }
 
 void launch_sub(int n, const double* a, const double* b, double* out, cudaStream_t s) {

@@ -83,6 +83,7 @@ __device__ __forceinline__ void load_jump3(const DevTables3& T, int q, const dou
 // point stride over its ~30 neighbours; the five moments are summed by a fixed xor tree.
 constexpr int kLsqLanes = 8;
 __global__ void k_lsq3(DevTables3 T, const double* __restrict__ phi, double* __restrict__ dphi) {
+  pdl_wait();   // φ from the previous kernel
   // point p → the p-th control point of the slab's three per-axis ranges
   const int gt = blockIdx.x * blockDim.x + threadIdx.x;
   int e = gt / kLsqLanes;
@@ -153,6 +154,7 @@ __global__ void k_base3(DevTables3 T, const double* __restrict__ f, double* __re
 __global__ void k_correct3(DevTables3 T, const double* __restrict__ phi, const double* __restrict__ dphi,
                            const double* __restrict__ fq, const double* __restrict__ jg, double* __restrict__ work,
                            double* __restrict__ corr) {
+  pdl_wait();   // φ and its LSQ derivatives from k_lsq3
   const int n = T.n_lo + blockIdx.x * blockDim.x + threadIdx.x;   // the slab's irregular nodes
   if (n >= T.n_hi) return;
   double acc = 0.0;
@@ -663,6 +665,7 @@ __global__ void __launch_bounds__(kSweep3Threads) k_sweep3(DevTables3 T, double*
 
 __global__ void k_reduced3(DevTables3 T, const double* __restrict__ zB, const double* __restrict__ zA,
                            double* __restrict__ hsep) {
+  pdl_wait();   // zB, zA from k_sweep3
   // thread per mode: the P − 1 ≤ 31 right-hand sides loaded in one batch, the forward values kept in
   // registers (no re-read of hsep), pivots recomputed for the backward pass
   constexpr int PM = 31;
@@ -823,6 +826,7 @@ __global__ void k_red3_fixup(DevTables3 T, const double* __restrict__ hin, doubl
 __global__ void k_interp3(DevTables3 T, const double* __restrict__ phi, const double* __restrict__ dphi,
                           const double* __restrict__ fz, const double* __restrict__ jg, const double* __restrict__ work,
                           double* __restrict__ out, int partial) {
+  pdl_wait();   // the z-evaluated stencil values from k_zeval3
   const int e = blockIdx.x * blockDim.x + threadIdx.x;
   if (e >= T.nq) return;
   const int N = T.N;
@@ -863,7 +867,7 @@ void launch_lsq3(const DevTables3& T, const double* phi, double* dphi, cudaStrea
   const int n = T.q_hi[0] - T.q_lo[0] + T.q_hi[1] - T.q_lo[1] + T.q_hi[2] - T.q_lo[2];
   if (n <= 0) return;
   ++g_launches;
-  k_lsq3<<<cdiv3((long)n * kLsqLanes, 256), 256, 0, s>>>(T, phi, dphi);
+  launch_pdl(k_lsq3, dim3(cdiv3((long)n * kLsqLanes, 256)), dim3(256), 0, s, T, phi, dphi);
 }
 void launch_base3(const DevTables3& T, const double* fgrid, double* work, cudaStream_t s) {
   ++g_launches;
@@ -873,7 +877,7 @@ void launch_correct3(const DevTables3& T, const double* phi, const double* dphi,
                      const double* jq_given, double* work, cudaStream_t s, double* corr) {
   if (T.n_hi <= T.n_lo) return;
   ++g_launches;
-  k_correct3<<<cdiv3(T.n_hi - T.n_lo, 128), 128, 0, s>>>(T, phi, dphi, fq, jq_given, work, corr);
+  launch_pdl(k_correct3, dim3(cdiv3(T.n_hi - T.n_lo, 128)), dim3(128), 0, s, T, phi, dphi, fq, jq_given, work, corr);
 }
 template <int N>
 static void dst_rows3_n(const DevTables3& T, int mode, double* work, const double* hsep, double scale, double* out,
@@ -945,7 +949,7 @@ void launch_sweep3(const DevTables3& T, double* work, double* zB, double* zA, cu
 void launch_reduced3(const DevTables3& T, const double* zB, const double* zA, double* hsep, cudaStream_t s) {
   if (T.P < 2) return;
   ++g_launches;
-  k_reduced3<<<cdiv3((long)T.N * T.N, 128), 128, 0, s>>>(T, zB, zA, hsep);
+  launch_pdl(k_reduced3, dim3(cdiv3((long)T.N * T.N, 128)), dim3(128), 0, s, T, zB, zA, hsep);
 }
 void launch_red3_local(const DevTables3& T, const double* zB, const double* zA, double* hsep, double* seg, int Kq,
                        cudaStream_t s) {
@@ -964,7 +968,7 @@ void launch_red3_fixup(const DevTables3& T, const double* hin, double* hsep, int
 void launch_interp3(const DevTables3& T, const double* phi, const double* dphi, const double* fz,
                     const double* jz_given, const double* work, double* out, cudaStream_t s, bool partial) {
   ++g_launches;
-  k_interp3<<<cdiv3(T.nq, 128), 128, 0, s>>>(T, phi, dphi, fz, jz_given, work, out, partial ? 1 : 0);
+  launch_pdl(k_interp3, dim3(cdiv3(T.nq, 128)), dim3(128), 0, s, T, phi, dphi, fz, jz_given, work, out, partial ? 1 : 0);
 }
 
 }  // namespace kfbi

@@ -518,6 +518,7 @@ __global__ void __launch_bounds__(kRed2Modes * kMaxSeg) k_reduced2(DevTables T, 
 // after the exchange from rows both owners publish (no rank reads another slab's blocks).
 __global__ void k_red2_local(DevTables T, const double* __restrict__ zB, const double* __restrict__ zA,
                              double* __restrict__ hsep, double* __restrict__ segbuf) {
+  pdl_wait();
   const int N = T.N, S = T.nseg;
   const int k = blockIdx.x * blockDim.x + threadIdx.x + 1;
   const int sg = T.seg_lo + blockIdx.y;
@@ -546,6 +547,7 @@ __global__ void k_red2_local(DevTables T, const double* __restrict__ zB, const d
 
 // (2) every rank: the level-2 tridiagonal system of the S − 1 slab separators per mode
 __global__ void k_red2_solve(DevTables T, const double* __restrict__ segbuf, double* __restrict__ h2) {
+  pdl_wait();
   const int N = T.N, S = T.nseg;
   const int k = blockIdx.x * blockDim.x + threadIdx.x + 1;
   if (k >= N || S < 2) return;
@@ -579,6 +581,7 @@ __global__ void k_red2_solve(DevTables T, const double* __restrict__ segbuf, dou
 
 // (3) owned segments: z − a h2_{σ−1} Z2_L − a h2_σ Z2_R, and the slab separators on both sides
 __global__ void k_red2_fixup(DevTables T, const double* __restrict__ h2, double* __restrict__ hsep) {
+  pdl_wait();
   const int N = T.N, S = T.nseg;
   const int k = blockIdx.x * blockDim.x + threadIdx.x + 1;
   const int sg = T.seg_lo + blockIdx.y;
@@ -1293,6 +1296,7 @@ __device__ __forceinline__ double block_ordered_sum(const double* __restrict__ p
 
 __global__ void k_mgs_step(int n, double* w, const double* Vprev, const double* Vcur, const double* pprev,
                            double* pcur, double* hout) {
+  pdl_wait();
   __shared__ double scratch[32];
   const int per = (n + gridDim.x - 1) / gridDim.x;
   const int b0 = blockIdx.x * per, b1 = min(n, b0 + per);
@@ -1328,6 +1332,7 @@ __global__ void k_mgs_step(int n, double* w, const double* Vprev, const double* 
 }
 
 __global__ void k_norm_scale(int n, double* w, const double* __restrict__ partial, double* hout) {
+  pdl_wait();
   const double hn = sqrt(block_ordered_sum(partial));
   if (blockIdx.x == 0 && threadIdx.x == 0) *hout = hn;
   if (hn == 0.0) return;
@@ -1411,6 +1416,7 @@ __global__ void __cluster_dims__(kMgsCl, 1, 1) __launch_bounds__(kMgsClThreads)
 }
 
 __global__ void k_dot(int n, const double* __restrict__ a, const double* __restrict__ b, double* __restrict__ partial) {
+  pdl_wait();
   __shared__ double scratch[32];
   const int per = (n + gridDim.x - 1) / gridDim.x;
   const int b0 = blockIdx.x * per, b1 = min(n, b0 + per);
@@ -1421,6 +1427,7 @@ __global__ void k_dot(int n, const double* __restrict__ a, const double* __restr
 }
 
 __global__ void k_finish_sum(const double* __restrict__ partial, double* out, int take_sqrt) {
+  pdl_wait();
   if (threadIdx.x < 32 && blockIdx.x == 0) {
     const double s = warp_ordered_sum(partial);
     if (threadIdx.x == 0) *out = take_sqrt ? sqrt(s) : s;
@@ -1429,6 +1436,7 @@ __global__ void k_finish_sum(const double* __restrict__ partial, double* out, in
 
 __global__ void k_axpy_basis(int n, int k, const double* __restrict__ V, int ldv, const YCoef y,
                              double* __restrict__ x) {
+  pdl_wait();
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
     double acc = 0.0;
     for (int q = 0; q < k; ++q) acc = fma(y.v[q], V[(size_t)q * ldv + i], acc);
@@ -1444,11 +1452,13 @@ __global__ void k_copy(int n, const double* __restrict__ src, double* __restrict
 }
 
 __global__ void k_sub(int n, const double* __restrict__ a, const double* __restrict__ b, double* __restrict__ o) {
+  pdl_wait();
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) o[i] = a[i] - b[i];
 }
 
 __global__ void k_scale_copy(int n, const double* __restrict__ a, const double* __restrict__ scal,
                              double* __restrict__ o) {
+  pdl_wait();
   const double s = *scal;
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) o[i] = a[i] / s;
 }
@@ -1530,20 +1540,21 @@ void launch_red2_local(const DevTables& T, const double* zB, const double* zA, d
                        cudaStream_t s) {
   dim3 grid(cdiv(T.N - 1, 128), T.seg_hi - T.seg_lo);
   ++g_launches;
-  k_red2_local<<<grid, 128, 0, s>>>(T, zB, zA, hsep, segbuf);
+  launch_pdl(k_red2_local, grid, dim3(128), 0, s, T, zB, zA, hsep, segbuf);
 }
 void launch_red2_solve(const DevTables& T, const double* segbuf, double* h2, cudaStream_t s) {
   ++g_launches;
-  k_red2_solve<<<cdiv(T.N - 1, 128), 128, 0, s>>>(T, segbuf, h2);
+  launch_pdl(k_red2_solve, dim3(cdiv(T.N - 1, 128)), dim3(128), 0, s, T, segbuf, h2);
 }
 void launch_red2_fixup(const DevTables& T, const double* h2, double* hsep, cudaStream_t s) {
   dim3 grid(cdiv(T.N - 1, 128), T.seg_hi - T.seg_lo);
   ++g_launches;
-  k_red2_fixup<<<grid, 128, 0, s>>>(T, h2, hsep);
+  launch_pdl(k_red2_fixup, grid, dim3(128), 0, s, T, h2, hsep);
 }
 
 namespace {
 __global__ void k_sum_parts(int n, int nparts, const double* __restrict__ parts, double* __restrict__ out) {
+  pdl_wait();
   for (int m = blockIdx.x * blockDim.x + threadIdx.x; m < n; m += gridDim.x * blockDim.x) {
     double s = 0.0;
     for (int r = 0; r < nparts; ++r) s += parts[(size_t)r * n + m];
@@ -1553,7 +1564,7 @@ __global__ void k_sum_parts(int n, int nparts, const double* __restrict__ parts,
 }  // namespace
 void launch_sum_parts(int n, int nparts, const double* parts, double* out, cudaStream_t s) {
   ++g_launches;
-  k_sum_parts<<<cdiv(n, 256), 256, 0, s>>>(n, nparts, parts, out);
+  launch_pdl(k_sum_parts, dim3(cdiv(n, 256)), dim3(256), 0, s, n, nparts, parts, out);
 }
 
 void launch_hole_coeffs(const DevTables& T, const int* hole_off, const int* hole_M, const double* hole_delta, int nh,
@@ -1571,7 +1582,7 @@ void launch_interp(const DevTables& T, const double* phi, const double* mk, cons
 
 void launch_mgs_step(int n, double* w, const double* Vprev, const double* Vcur, const double* partial_prev,
                      double* partial_cur, double* hout, cudaStream_t s) {
-  { ++g_launches; k_mgs_step<<<kRedBlocks, 256, 0, s>>>(n, w, Vprev, Vcur, partial_prev, partial_cur, hout); }
+  { ++g_launches; launch_pdl(k_mgs_step, dim3(kRedBlocks), dim3(256), 0, s, n, w, Vprev, Vcur, partial_prev, partial_cur, hout); }
 }
 
 bool launch_mgs_fused(int n, int j, const double* V, double* w, double* hcol, cudaStream_t s) {
@@ -1586,21 +1597,21 @@ bool launch_mgs_fused(int n, int j, const double* V, double* w, double* hcol, cu
 }
 
 void launch_norm_scale(int n, double* w, const double* partial, double* hout, cudaStream_t s) {
-  { ++g_launches; k_norm_scale<<<kRedBlocks, 256, 0, s>>>(n, w, partial, hout); }
+  { ++g_launches; launch_pdl(k_norm_scale, dim3(kRedBlocks), dim3(256), 0, s, n, w, partial, hout); }
 }
 
 void launch_dot(int n, const double* a, const double* b, double* partial, cudaStream_t s) {
-  { ++g_launches; k_dot<<<kRedBlocks, 256, 0, s>>>(n, a, b, partial); }
+  { ++g_launches; launch_pdl(k_dot, dim3(kRedBlocks), dim3(256), 0, s, n, a, b, partial); }
 }
 
 void launch_finish_sum(const double* partial, double* out, bool take_sqrt, cudaStream_t s) {
-  { ++g_launches; k_finish_sum<<<1, 32, 0, s>>>(partial, out, take_sqrt ? 1 : 0); }
+  { ++g_launches; launch_pdl(k_finish_sum, dim3(1), dim3(32), 0, s, partial, out, take_sqrt ? 1 : 0); }
 }
 
 void launch_axpy_basis(int n, int k, const double* V, int ldv, const double* y_host, double* x, cudaStream_t s) {
   YCoef y{};
   for (int q = 0; q < k && q < kYMax; ++q) y.v[q] = y_host[q];   // by value: no copy engine
-  { ++g_launches; k_axpy_basis<<<cdiv(n, 256), 256, 0, s>>>(n, k, V, ldv, y, x); }
+  { ++g_launches; launch_pdl(k_axpy_basis, dim3(cdiv(n, 256)), dim3(256), 0, s, n, k, V, ldv, y, x); }
 }
 void launch_copy(int n, const double* src, double* dst, cudaStream_t s) {
   if (n <= 0) return;
@@ -1609,11 +1620,11 @@ void launch_copy(int n, const double* src, double* dst, cudaStream_t s) {
 }
 
 void launch_sub(int n, const double* a, const double* b, double* out, cudaStream_t s) {
-  { ++g_launches; k_sub<<<cdiv(n, 256), 256, 0, s>>>(n, a, b, out); }
+  { ++g_launches; launch_pdl(k_sub, dim3(cdiv(n, 256)), dim3(256), 0, s, n, a, b, out); }
 }
 
 void launch_scale_copy(int n, const double* a, const double* scal, double* out, cudaStream_t s) {
-  { ++g_launches; k_scale_copy<<<cdiv(n, 256), 256, 0, s>>>(n, a, scal, out); }
+  { ++g_launches; launch_pdl(k_scale_copy, dim3(cdiv(n, 256)), dim3(256), 0, s, n, a, scal, out); }
 }
 
 template <int MODE, int N>

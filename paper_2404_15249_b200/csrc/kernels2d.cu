@@ -912,6 +912,7 @@ __global__ void k_interp(DevTables T, const double* __restrict__ phi, const doub
 __global__ void k_hole_coeffs(const int* __restrict__ off, const int* __restrict__ cnt,
                               const double* __restrict__ delta, const double* __restrict__ phi,
                               double* __restrict__ a) {
+  pdl_wait();
   __shared__ double scratch[32];
   const int hh = blockIdx.x;
   double v[1] = {0.0};
@@ -1054,6 +1055,7 @@ __global__ void __launch_bounds__(DenseCfg<N>::NTHR, 1) k_dst_dense2(DevTables T
                                                                     int mask_omega, BumpParams bp,
                                                                     const double* __restrict__ hsep,
                                                                     double* __restrict__ dst) {
+  pdl_wait();   // the input rows / spectra from the previous kernel
   using C = DenseCfg<N>;
   constexpr int NTH = C::NTH, RPC = C::RPC;
   extern __shared__ double2 smz[];
@@ -1571,7 +1573,7 @@ void launch_hole_coeffs(const DevTables& T, const int* hole_off, const int* hole
                         const double* phi, double* a, cudaStream_t s) {
   (void)T;
   if (nh == 0) return;
-  { ++g_launches; k_hole_coeffs<<<nh, 256, 0, s>>>(hole_off, hole_M, hole_delta, phi, a); }
+  { ++g_launches; launch_pdl(k_hole_coeffs, dim3(nh), dim3(256), 0, s, hole_off, hole_M, hole_delta, phi, a); }
 }
 
 void launch_interp(const DevTables& T, const double* phi, const double* mk, const double* fz, const double* jz_given,
@@ -1637,7 +1639,7 @@ static void dense_n(const DevTables& T, const double* src, int mask, const BumpP
   const int per = occupancy((const void*)k_dst_dense2<MODE, N>, C::NTHR, sm);
   const int groups = (rows + C::RPC - 1) / C::RPC;
   const int grid = groups < per * num_sms() ? groups : per * num_sms();
-  k_dst_dense2<MODE, N><<<grid, C::NTHR, sm, s>>>(T, src, mask, bp, hsep, dst);
+  launch_pdl(k_dst_dense2<MODE, N>, dim3(grid), dim3(C::NTHR), sm, s, T, src, mask, bp, hsep, dst);
 }
 template <int MODE>
 static void dense_dispatch(const DevTables& T, const double* src, int mask, const BumpParams& bp, const double* hsep,
@@ -1720,6 +1722,7 @@ void launch_fill(double* x, long n, double val, cudaStream_t s) {
 
 __global__ void k_axpy_dcoef(long n, const double* __restrict__ coef, const double* __restrict__ x,
                              double* __restrict__ y) {
+  pdl_wait();
   const double a = *coef;
   for (long i = (long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long)gridDim.x * blockDim.x)
     y[i] = fma(a, __ldcs(x + i), y[i]);
@@ -1727,7 +1730,7 @@ __global__ void k_axpy_dcoef(long n, const double* __restrict__ coef, const doub
 void launch_axpy_dcoef(long n, const double* coef, const double* x, double* y, cudaStream_t s) {
   if (n <= 0) return;
   ++g_launches;
-  k_axpy_dcoef<<<(int)std::min<long>((n + 255) / 256, 8L * num_sms()), 256, 0, s>>>(n, coef, x, y);
+  launch_pdl(k_axpy_dcoef, dim3((int)std::min<long>((n + 255) / 256, 8L * num_sms())), dim3(256), 0, s, n, coef, x, y);
 }
 }  // namespace kfbi
 

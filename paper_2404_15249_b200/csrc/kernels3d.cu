@@ -231,6 +231,7 @@ __global__ void __launch_bounds__(256, 2) k_dst_rows3t(DevTables3 T, double* wor
                                                        double scale, double* __restrict__ out,
                                                        const double* __restrict__ src,
                                                        const double* __restrict__ corr, int compact) {
+  pdl_wait();   // the rows from the previous kernel
   constexpr int NTL = N / 32, RPC = 256 / NTL, ZS = N / 2 + N / 32 + 1;
   extern __shared__ double2 smz[];
   const int rl = threadIdx.x / NTL, tid = threadIdx.x % NTL;
@@ -889,10 +890,10 @@ static void dst_rows3_n(const DevTables3& T, int mode, double* work, const doubl
   smem_optin((const void*)k_dst_rows3t<1, N>, sm);
   smem_optin((const void*)k_dst_rows3t<2, N>, sm);
   smem_optin((const void*)k_dst_rows3t<3, N>, sm);
-  if (mode == 0) k_dst_rows3t<0, N><<<grid, 256, sm, s>>>(T, work, hsep, scale, out, src, corr, 0);
-  else if (mode == 1) k_dst_rows3t<1, N><<<grid, 256, sm, s>>>(T, work, hsep, scale, out, src, corr, 0);
-  else if (mode == 2) k_dst_rows3t<2, N><<<grid, 256, sm, s>>>(T, work, hsep, scale, out, src, corr, compact);
-  else k_dst_rows3t<3, N><<<grid, 256, sm, s>>>(T, work, hsep, scale, out, src, corr, compact);
+  if (mode == 0) launch_pdl(k_dst_rows3t<0, N>, dim3(grid), dim3(256), sm, s, T, work, hsep, scale, out, src, corr, 0);
+  else if (mode == 1) launch_pdl(k_dst_rows3t<1, N>, dim3(grid), dim3(256), sm, s, T, work, hsep, scale, out, src, corr, 0);
+  else if (mode == 2) launch_pdl(k_dst_rows3t<2, N>, dim3(grid), dim3(256), sm, s, T, work, hsep, scale, out, src, corr, compact);
+  else launch_pdl(k_dst_rows3t<3, N>, dim3(grid), dim3(256), sm, s, T, work, hsep, scale, out, src, corr, compact);
 }
 void launch_dst_rows3(const DevTables3& T, int mode, double* work, const double* hsep, double scale, double* out,
                       cudaStream_t s, const double* src, const double* corr, bool compact) {

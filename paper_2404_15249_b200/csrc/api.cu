@@ -533,6 +533,7 @@ kfbi_status fail(kfbi_ctx* c, kfbi_status st, const std::string& msg) {
   catch (const GeomError& e) { return fail(ctx, KFBI_EGEOM, e.what()); } \
   catch (const ArgError& e) { return fail(ctx, KFBI_EINVAL, e.what()); } \
   catch (const BreakdownError& e) { return fail(ctx, KFBI_EBREAKDOWN, e.what()); } \
+  catch (const DeviceError& e) { return fail(ctx, KFBI_ECUDA, e.what()); } \
   catch (const std::exception& e) { return fail(ctx, KFBI_EINVAL, e.what()); }
 
 cudaStream_t pick(kfbi_ctx* c, void* s) { return s ? (cudaStream_t)s : c->stream; }

@@ -552,7 +552,8 @@ void launch_pdl(void (*k)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStr
   at[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = at;
   cfg.numAttrs = on ? 1 : 0;
-  cudaLaunchKernelEx(&cfg, k, std::forward<Args>(args)...);
+  const cudaError_t e = cudaLaunchKernelEx(&cfg, k, std::forward<Args>(args)...);
+  if (e != cudaSuccess) throw DeviceError(std::string("kernel launch: ") + cudaGetErrorString(e));
 }
 
 // Host-side launch caches, kept per device: the shared-memory opt-in of a kernel, its occupancy and

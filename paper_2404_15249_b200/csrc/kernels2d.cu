@@ -625,7 +625,10 @@ __device__ __forceinline__ double fixup_staged(const DevTables& T, const double*
 // Modes N/4, N/2, 3N/4 are added by thread 0.  Thread `tid` owns t = tid + s·B; (s, c) along s
 // follow by rotation with the per-row step e^{iπjB/N}.  Rows come grouped by class (odd,
 // j ≡ 0, j ≡ 2 mod 4; setup order) and are processed up to four at a time.
-constexpr int kInvThreads = 256;
+#ifndef KFBI_INV_THREADS
+#define KFBI_INV_THREADS 256
+#endif
+constexpr int kInvThreads = KFBI_INV_THREADS;
 static_assert(kMaxColRows <= kInvThreads, "k_inv_sparse stages a column's rows one per thread");
 
 template <int QPT>
